@@ -1,0 +1,71 @@
+/*
+ * cdp_b200.h — C ABI of libcdp_b200.so, the sm_100a implementation of the
+ * Cyclic Data Parallelism training step (arXiv 2403.08837).
+ *
+ * Plain C types only (pointers, sizes, ints, floats); no torch types.  Every
+ * entry point returns 0 on success and non-zero on failure, with the message
+ * available from cdp_last_error() (thread-local).  The Python side
+ * (paper_2403_08837_b200/_native.py) binds these with ctypes; INTEGRATION.md
+ * shows the binding a maintainer of the reference would add.
+ *
+ * Reference interfaces replaced (all paths under /root/reference/pkg/src/cyclicdp):
+ *   cdp_mlp_value_grad   <- training/_kernels.pyx:25-132 `mlp_value_grad`
+ *                           (backend protocol training/backend.py:13-30,
+ *                            called from training/models.py:84-88)
+ *   cdp_quad_value_grad  <- training/_kernels.pyx:135-172 `quad_value_grad`
+ *                           (called from training/models.py:148)
+ *   cdp_trainer_*        <- training/engine.py:66-116 `_advance` and its
+ *                           drivers step_dp / step_cdp / run_experiment
+ *                           (engine.py:119-215): the whole training step,
+ *                           device resident, one CUDA graph per step.
+ *   cdp_hop_*            <- comm.py:37-67 `schedule_cdp_ring_reduce` hop
+ *                           (+ engine.py:96-109 accumulate/update) as kernels
+ *   cdp_shard_copy       <- comm.py:126-143 ZeRO-CDP STATE_TRANSFER
+ */
+#ifndef CDP_B200_H
+#define CDP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- library ---------------------------------------------------------- */
+const char *cdp_last_error(void);
+int cdp_version(void);
+/* Number of SMs of the current device (0 if no device). */
+int cdp_device_sm_count(void);
+
+/* Compute precision of the layer kernels. */
+enum cdp_dtype {
+    CDP_DTYPE_FP32 = 0, /* fp32 storage, 3xTF32 tcgen05 products (fp32-accurate) */
+    CDP_DTYPE_BF16 = 1  /* bf16 operands, fp32 accumulate, fp32 master params   */
+};
+
+/* ---- operator level: the reference backend protocol ------------------- */
+/* Loss and flat gradient of the stage-stacked tanh MLP on one micro-batch.
+ * Host fp64 buffers in the reference layout (per stage W[din][dout] then
+ * b[dout]); loss_kind 0 = MSE against y[batch][dims[n-1]], 1 = softmax
+ * cross-entropy against labels[batch].  grad_out is fully overwritten. */
+int cdp_mlp_value_grad(int n_dims, const int64_t *dims, const double *theta, int batch, const double *x,
+                       const double *y, const int64_t *labels, int loss_kind, int dtype, double *loss_out,
+                       double *grad_out);
+
+/* 0.5*|A theta - t|^2 averaged over rows and batch; a is [m][p]. */
+int cdp_quad_value_grad(int m, int p, const double *a, const double *theta, int batch, const double *targets,
+                        double *loss_out, double *grad_out);
+
+/* ---- tensor-core GEMM self-test (parity tests of the tcgen05 kernel) --- */
+/* D[m][n] = sum_s A_s . B_s.  kind 0 = bf16, 1 = fp32/tf32.  A K-major:
+ * A[m*lda+k], MN-major: A[k*lda+m]; B K-major: B[n*ldb+k], MN-major:
+ * B[k*ldb+n].  Device pointers; stream may be NULL. */
+int cdp_test_gemm(int kind, int a_mn, int b_mn, int bn, int M, int N, int K, int n_seg, const void *const *a_ptrs,
+                  int lda, const void *const *b_ptrs, int ldb, float *d, int ldd, int splits, float *ws,
+                  int *counters, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CDP_B200_H */

@@ -1,0 +1,72 @@
+"""ctypes binding of libcdp_b200.so (declarations mirror include/cdp_b200.h).
+
+There is no CPU fallback: `lib()` raises `NativeUnavailable` when the library
+is missing or no CUDA device is visible, and every caller propagates it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcdp_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "cdp_b200.h")
+
+c_int, c_float, c_double, c_void_p, c_size_t = ctypes.c_int, ctypes.c_float, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
+c_int64_p = ctypes.POINTER(ctypes.c_int64)
+c_double_p = ctypes.POINTER(ctypes.c_double)
+c_float_p = ctypes.POINTER(ctypes.c_float)
+c_int_p = ctypes.POINTER(ctypes.c_int)
+c_u8_p = ctypes.POINTER(ctypes.c_uint8)
+
+# name -> (restype, argtypes); kept in the header's order.
+SIGNATURES = {
+    "cdp_last_error": (ctypes.c_char_p, []),
+    "cdp_version": (c_int, []),
+    "cdp_device_sm_count": (c_int, []),
+    "cdp_mlp_value_grad": (c_int, [c_int, c_int64_p, c_double_p, c_int, c_double_p, c_double_p, c_int64_p, c_int,
+                                   c_int, c_double_p, c_double_p]),
+    "cdp_quad_value_grad": (c_int, [c_int, c_int, c_double_p, c_double_p, c_int, c_double_p, c_double_p, c_double_p]),
+    "cdp_test_gemm": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p), c_int,
+                              ctypes.POINTER(c_void_p), c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+}
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """dlopen + bind signatures; does not require a GPU (used by CPU tests)."""
+    if not os.path.exists(path):
+        raise NativeUnavailable(
+            f"{path} not built: run `python -m paper_2403_08837_b200.build` (no CPU fallback exists)")
+    L = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = load_library()
+        if L.cdp_device_sm_count() <= 0:
+            raise NativeUnavailable("no CUDA device visible to libcdp_b200 (the sm_100a path has no CPU fallback)")
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise NativeError(lib().cdp_last_error().decode())

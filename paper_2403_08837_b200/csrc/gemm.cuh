@@ -1,0 +1,221 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a with pluggable fused epilogues.
+//
+//   D[M,N] (fp32, in TMEM) = sum_seg A_seg[M,K] . B_seg[K,N]
+//
+// * one 128 x BN output tile per CTA (cta_group::1, UMMA M=128), split-K over
+//   gridDim.z with a deterministic in-order fix-up by the last-arriving CTA;
+// * operands staged by TMA into 128-byte-swizzled shared memory, a STAGES-deep
+//   mbarrier ring between the TMA warp (warp 0) and the single MMA-issuing
+//   thread (warp 1); warp 2 owns the TMEM allocation; warps 4-7 are the
+//   epilogue (thread t <-> accumulator row t, tcgen05.ld 32 columns at a time);
+// * A and B may each be K-major or MN-major (the instruction descriptor's
+//   transpose bits), so row-major activations [samples, features] and the
+//   row-major weights [din, dout] of the reference layout feed all three
+//   GEMMs of a layer (forward, weight-grad, data-grad) without transposes;
+// * KIND 0: bf16 operands (kind::f16). KIND 1: fp32 operands read as tf32
+//   (kind::tf32); three segments (hi.hi + hi.lo + lo.hi) give the 3xTF32
+//   fp32-accurate product used by the fp32 parity mode.
+#pragma once
+#include "ptx.cuh"
+
+namespace cdp {
+
+struct GemmMaps {
+    CUtensorMap a[3];
+    CUtensorMap b[3];
+};
+
+struct GemmArgs {
+    int M, N;
+    int kb_per_seg;   // k-blocks (of 128 bytes of K) per segment
+    int n_seg;        // 1..3
+    int iters_per_split;
+    float *ws;        // split-K partials [tiles][splits][128][BN]
+    int *counters;    // per tile arrival counters (self-resetting)
+};
+
+template <int KIND, int BN_, bool A_MN, bool B_MN>
+struct GemmCfg {
+    static constexpr int BM = 128;
+    static constexpr int BN = BN_;
+    static constexpr int ELEM = KIND == 0 ? 2 : 4;
+    static constexpr int BK = 128 / ELEM;      // K elements per k-block
+    static constexpr int UMMA_K = 32 / ELEM;   // K per tcgen05.mma
+    static constexpr int CH = 128 / ELEM;      // MN elements per 128-byte swizzle row
+    static constexpr int A_BYTES = BM * 128;
+    static constexpr int B_BYTES = BN * 128;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 6 ? 6 : (200 * 1024 / STAGE_BYTES);
+    static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+    static constexpr uint32_t IDESC = ptx::instr_desc(KIND == 0 ? 1u : 2u, A_MN, B_MN, 128, BN);
+    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN must be a multiple of 32 in [32,256]");
+    static_assert(!B_MN || BN % CH == 0, "MN-major B needs BN multiple of the 128-byte row");
+    static_assert(STAGES >= 2, "not enough shared memory for two stages");
+};
+
+// Load one k-block of a 128-row (A) or BN-row (B) operand tile.
+template <class C, bool MN, int ROWS>
+__device__ __forceinline__ void load_operand(uint8_t *dst, const CUtensorMap *m, uint64_t *bar, int mn0, int k0) {
+    if constexpr (!MN) {
+        ptx::tma_load_2d(dst, m, bar, k0, mn0);  // tensor (inner K, outer MN)
+    } else {
+#pragma unroll
+        for (int c = 0; c < ROWS / C::CH; ++c)  // tensor (inner MN, outer K)
+            ptx::tma_load_2d(dst + c * (C::BK * 128), m, bar, mn0 + c * C::CH, k0);
+    }
+}
+
+template <class C, bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
+    if constexpr (!MN)
+        return ptx::smem_desc_sw128(base + k * 32, 16, 1024);
+    else if constexpr (C::ELEM == 2)
+        return ptx::smem_desc_sw128(base + k * C::UMMA_K * 128, C::BK * 128, 1024);
+    else  // tf32 MN-major: 32-byte swizzle atoms, 4-row groups
+        return ptx::smem_desc_sw128(base + k * C::UMMA_K * 128, C::BK * 128, 512, 1);
+}
+
+template <int KIND, int BN, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args, const typename Epi::Params ep) {
+    using C = GemmCfg<KIND, BN, A_MN, B_MN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + C::STAGES * C::A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
+    uint64_t *empty = full + C::STAGES;
+    uint64_t *tmem_full = empty + C::STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+    int *last_flag = reinterpret_cast<int *>(tmem_slot + 1);
+
+    const uint32_t warp = ptx::warp_id();
+    const int m0 = blockIdx.x * C::BM;
+    const int n0 = blockIdx.y * BN;
+    const int split = blockIdx.z;
+    const int total_iters = args.kb_per_seg * args.n_seg;
+    const int it_lo = split * args.iters_per_split;
+    const int it_hi = min(total_iters, it_lo + args.iters_per_split);
+    const int n_iters = it_hi - it_lo;
+
+    if (warp == 0 && ptx::lane_id() == 0) {
+        for (int s = 0; s < args.n_seg; ++s) {
+            ptx::tma_prefetch_desc(&maps.a[s]);
+            ptx::tma_prefetch_desc(&maps.b[s]);
+        }
+    }
+    if (warp == 1 && ptx::lane_id() == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(tmem_full, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (ptx::lane_id() == 0) {
+            for (int it = 0; it < n_iters; ++it) {
+                const int s = it % C::STAGES;
+                if (it >= C::STAGES) ptx::mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+                const int g = it_lo + it;
+                const int seg = g / args.kb_per_seg;
+                const int k0 = (g % args.kb_per_seg) * C::BK;
+                ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+                load_operand<C, A_MN, 128>(sA + s * C::A_BYTES, &maps.a[seg], &full[s], m0, k0);
+                load_operand<C, B_MN, BN>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, k0);
+            }
+        }
+    } else if (warp == 1) {
+        if (ptx::lane_id() == 0) {
+            for (int it = 0; it < n_iters; ++it) {
+                const int s = it % C::STAGES;
+                ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+                ptx::tc_fence_after();
+                const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
+                const uint32_t b_base = ptx::smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+                for (int k = 0; k < C::BK / C::UMMA_K; ++k) {
+                    ptx::umma<KIND>(tmem_base, operand_desc<C, A_MN>(a_base, k), operand_desc<C, B_MN>(b_base, k),
+                                    C::IDESC, (it > 0 || k > 0) ? 1u : 0u);
+                }
+                ptx::umma_commit(&empty[s]);
+            }
+            ptx::umma_commit(tmem_full);
+        }
+    } else if (warp >= 4) {
+        const int q = warp - 4;          // TMEM lane quarter of this warp
+        const int row = q * 32 + ptx::lane_id();
+        const int m = m0 + row;
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
+        ptx::mbar_wait(tmem_full, 0);
+        ptx::tc_fence_after();
+        if (gridDim.z == 1) {
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                float v[32];
+                ptx::tmem_ld32(taddr + c, v);
+                if (n_iters == 0) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                }
+                Epi::apply(ep, m, n0 + c, v, args.M, args.N);
+            }
+            if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x - 128);
+        } else {
+            const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+            float *mine = args.ws + ((size_t(tile) * gridDim.z + split) * 128 + row) * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                float v[32];
+                ptx::tmem_ld32(taddr + c, v);
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<float4 *>(mine + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+            __threadfence();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (threadIdx.x == 128) {
+                const int prev = atomicAdd(&args.counters[tile], 1);
+                const int last = prev == int(gridDim.z) - 1;
+                if (last) args.counters[tile] = 0;
+                *last_flag = last;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (*last_flag) {
+                __threadfence();
+                const float *base = args.ws + (size_t(tile) * gridDim.z * 128 + row) * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    float v[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                    for (int z = 0; z < int(gridDim.z); ++z) {
+                        const float *p = base + size_t(z) * 128 * BN + c;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            float4 t = __ldcg(reinterpret_cast<const float4 *>(p + i));
+                            v[i] += t.x;
+                            v[i + 1] += t.y;
+                            v[i + 2] += t.z;
+                            v[i + 3] += t.w;
+                        }
+                    }
+                    Epi::apply(ep, m, n0 + c, v, args.M, args.N);
+                }
+                if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x - 128);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+}  // namespace cdp

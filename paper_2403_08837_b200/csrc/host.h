@@ -1,0 +1,59 @@
+// Host-side helpers shared by the C-ABI translation units: error state,
+// CUDA checks, TMA tensor-map encoding through the driver entry point.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace cdp {
+
+void set_error(const std::string &msg);
+const char *get_error();
+
+struct CdpError : std::runtime_error {
+    explicit CdpError(const std::string &m) : std::runtime_error(m) {}
+};
+
+#define CDP_CUDA(expr)                                                                                          \
+    do {                                                                                                        \
+        cudaError_t e__ = (expr);                                                                               \
+        if (e__ != cudaSuccess)                                                                                 \
+            throw ::cdp::CdpError(std::string(#expr) + ": " + cudaGetErrorString(e__) + " @" + __FILE__ + ":" + \
+                                  std::to_string(__LINE__));                                                    \
+    } while (0)
+
+#define CDP_REQUIRE(cond, msg)                               \
+    do {                                                     \
+        if (!(cond)) throw ::cdp::CdpError(std::string(msg)); \
+    } while (0)
+
+// C-ABI guard: run body, convert exceptions to an error code + last-error string.
+template <class F>
+int guarded(F &&f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception &e) {
+        set_error(e.what());
+        return 1;
+    } catch (...) {
+        set_error("unknown error");
+        return 1;
+    }
+}
+
+enum class ElemType { BF16 = 0, F32 = 1 };
+
+// 2-D tiled tensor map, 128-byte swizzle.  inner/outer extents in elements,
+// row stride in bytes (multiple of 16), box {box_inner, box_outer}.
+CUtensorMap make_tmap_2d(const void *base, ElemType t, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                         uint32_t box_inner, uint32_t box_outer,
+                         CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B);
+
+int num_sms();
+
+}  // namespace cdp
