@@ -57,6 +57,48 @@ int cdp_mlp_value_grad(int n_dims, const int64_t *dims, const double *theta, int
 int cdp_quad_value_grad(int m, int p, const double *a, const double *theta, int batch, const double *targets,
                         double *loss_out, double *grad_out);
 
+/* ---- step level: the device-resident CDP / DP trainer ---------------- */
+/* Replaces ref training/engine.py:66-116 (_advance) for the stage MLP.  The
+ * step plan comes from the reference-parity Timeline
+ * (paper_2403_08837_b200/executor.py): ops[n_ops][8] =
+ *   {kind 0=F/1=B, worker i (1-based), stage j (1-based), fresh (rule table),
+ *    input-record slot, output-record slot, hop role, 0}
+ * with hop role 0 first / 1 middle / 2 last (fused SGD update) / 3 only /
+ * 4 gradient only; deps[n_deps][2] = cross-worker edges (before, after);
+ * slots_per_stage[n_dims] = activation-record slots (index 0 unused).
+ * Dataset (optional, n_samples rows): x fp32 [n][dims[0]], labels int32 [n]
+ * (loss_kind 1) or targets fp32 [n][dims[n_dims-1]] (loss_kind 0). */
+typedef struct cdp_trainer cdp_trainer;
+int cdp_trainer_create(int n_dims, const int64_t *dims, int micro_batch, int n_workers, int loss_kind, int dtype,
+                       float momentum, float weight_decay, int n_ops, const int32_t *ops, int n_deps,
+                       const int32_t *deps, const int32_t *slots_per_stage, int n_samples, const float *x,
+                       const int32_t *labels, const float *targets, cdp_trainer **out);
+void cdp_trainer_destroy(cdp_trainer *tr);
+/* which: 0 = current version (theta_t), 1 = previous (theta_{t-1}), -1 = both.
+ * Flat fp32 host buffers in the reference layout. */
+int cdp_trainer_set_params(cdp_trainer *tr, int which, const float *theta);
+int cdp_trainer_get_params(cdp_trainer *tr, int which, float *theta);
+int cdp_trainer_set_velocity(cdp_trainer *tr, const float *v);
+int cdp_trainer_get_velocity(cdp_trainer *tr, float *v);
+/* One training step (asynchronous): perm = n_workers*micro_batch dataset rows,
+ * micro-batch i = perm[(i-1)B, iB) (ref training/models.py:173-181). */
+int cdp_trainer_step(cdp_trainer *tr, const int32_t *perm, float lr);
+/* One step whose inputs are host buffers (n_workers*micro_batch rows, copied
+ * H2D inside the step): the end-to-end path. */
+int cdp_trainer_step_host_batch(cdp_trainer *tr, const float *x, const int32_t *labels, const float *targets,
+                                float lr);
+int cdp_trainer_sync(cdp_trainer *tr);
+/* Mean loss and non-finite flags {grad stage bits, loss, update stage bits}
+ * of the retained steps, oldest first; *count = steps run so far. */
+int cdp_trainer_history(cdp_trainer *tr, int max, double *losses, uint32_t *flags, int *count);
+/* out[0..5] = activation-record bytes, parameter-state bytes, kernels per
+ * step, next step index, worker streams, ops per step. */
+int cdp_trainer_stats(cdp_trainer *tr, int64_t *out, int n_out);
+/* The partial-sum buffer (gradient of the last step in gradient-only plans). */
+int cdp_trainer_get_grad(cdp_trainer *tr, float *grad);
+/* The cudaStream_t the step graphs are launched on. */
+int cdp_trainer_stream(cdp_trainer *tr, void **stream);
+
 /* ---- tensor-core GEMM self-test (parity tests of the tcgen05 kernel) --- */
 /* D[m][n] = sum_s A_s . B_s.  kind 0 = bf16, 1 = fp32/tf32.  A K-major:
  * A[m*lda+k], MN-major: A[k*lda+m]; B K-major: B[n*ldb+k], MN-major:

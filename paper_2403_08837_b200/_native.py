@@ -28,6 +28,22 @@ SIGNATURES = {
     "cdp_mlp_value_grad": (c_int, [c_int, c_int64_p, c_double_p, c_int, c_double_p, c_double_p, c_int64_p, c_int,
                                    c_int, c_double_p, c_double_p]),
     "cdp_quad_value_grad": (c_int, [c_int, c_int, c_double_p, c_double_p, c_int, c_double_p, c_double_p, c_double_p]),
+    "cdp_trainer_create": (c_int, [c_int, c_int64_p, c_int, c_int, c_int, c_int, c_float, c_float, c_int,
+                                   ctypes.POINTER(ctypes.c_int32), c_int, ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_int32), c_int, c_float_p, ctypes.POINTER(ctypes.c_int32),
+                                   c_float_p, ctypes.POINTER(c_void_p)]),
+    "cdp_trainer_destroy": (None, [c_void_p]),
+    "cdp_trainer_set_params": (c_int, [c_void_p, c_int, c_float_p]),
+    "cdp_trainer_get_params": (c_int, [c_void_p, c_int, c_float_p]),
+    "cdp_trainer_set_velocity": (c_int, [c_void_p, c_float_p]),
+    "cdp_trainer_get_velocity": (c_int, [c_void_p, c_float_p]),
+    "cdp_trainer_step": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_int32), c_float]),
+    "cdp_trainer_step_host_batch": (c_int, [c_void_p, c_float_p, ctypes.POINTER(ctypes.c_int32), c_float_p, c_float]),
+    "cdp_trainer_sync": (c_int, [c_void_p]),
+    "cdp_trainer_history": (c_int, [c_void_p, c_int, c_double_p, ctypes.POINTER(ctypes.c_uint32), c_int_p]),
+    "cdp_trainer_stats": (c_int, [c_void_p, c_int64_p, c_int]),
+    "cdp_trainer_get_grad": (c_int, [c_void_p, c_float_p]),
+    "cdp_trainer_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_test_gemm": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p), c_int,
                               ctypes.POINTER(c_void_p), c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
 }

@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
         ptx::mbar_wait(tmem_full, 0);
         ptx::tc_fence_after();
+        typename Epi::State st;
         if (gridDim.z == 1) {
+            Epi::begin(ep, m, st);
 #pragma unroll 1
             for (int c = 0; c < BN; c += 32) {
                 float v[32];
@@ -165,8 +167,9 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = 0.f;
                 }
-                Epi::apply(ep, m, n0 + c, v, args.M, args.N);
+                Epi::apply(ep, m, n0 + c, v, args.M, args.N, st);
             }
+            Epi::finish(ep, m, args.M, st);
             if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x - 128);
         } else {
             const int tile = blockIdx.y * gridDim.x + blockIdx.x;
@@ -191,6 +194,7 @@ __global__ void __launch_bounds__(256, 1)
             if (*last_flag) {
                 __threadfence();
                 const float *base = args.ws + (size_t(tile) * gridDim.z * 128 + row) * BN;
+                Epi::begin(ep, m, st);
 #pragma unroll 1
                 for (int c = 0; c < BN; c += 32) {
                     float v[32];
@@ -207,8 +211,9 @@ __global__ void __launch_bounds__(256, 1)
                             v[i + 3] += t.w;
                         }
                     }
-                    Epi::apply(ep, m, n0 + c, v, args.M, args.N);
+                    Epi::apply(ep, m, n0 + c, v, args.M, args.N, st);
                 }
+                Epi::finish(ep, m, args.M, st);
                 if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x - 128);
             }
         }

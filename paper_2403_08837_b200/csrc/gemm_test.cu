@@ -13,7 +13,10 @@ struct EpiStore {
         float *d;
         int ldd;
     };
-    __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N) {
+    struct State {};
+    __device__ static void begin(const Params &, int, State &) {}
+    __device__ static void finish(const Params &, int, int, State &) {}
+    __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &) {
         if (m >= M) return;
 #pragma unroll
         for (int i = 0; i < 32; ++i)

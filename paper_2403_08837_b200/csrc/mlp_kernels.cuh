@@ -1,0 +1,278 @@
+// Layer kernels of the stage-stacked tanh MLP (ref training/_kernels.pyx:25-132)
+// as fused epilogues of the tcgen05 GEMM, plus the loss and gather kernels.
+//
+// Compute formats (template KIND):
+//   0  bf16 operands      : one bf16 array per tensor
+//   1  fp32 as 3xTF32     : hi = x with the 13 low mantissa bits cleared (exact
+//                           tf32), lo = x - hi (exact); products hi.hi+hi.lo+lo.hi
+#pragma once
+#include <cuda_bf16.h>
+
+#include "gemm.cuh"
+
+namespace cdp {
+
+template <int KIND>
+struct Fmt;
+
+template <>
+struct Fmt<0> {
+    __device__ static void store(void *hi, void *, size_t i, float x) {
+        static_cast<__nv_bfloat16 *>(hi)[i] = __float2bfloat16_rn(x);
+    }
+    __device__ static float load(const void *hi, const void *, size_t i) {
+        return __bfloat162float(static_cast<const __nv_bfloat16 *>(hi)[i]);
+    }
+};
+
+template <>
+struct Fmt<1> {
+    __device__ static void store(void *hi, void *lo, size_t i, float x) {
+        const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+        static_cast<float *>(hi)[i] = h;
+        static_cast<float *>(lo)[i] = __fsub_rn(x, h);
+    }
+    __device__ static float load(const void *hi, const void *lo, size_t i) {
+        return __fadd_rn(static_cast<const float *>(hi)[i], static_cast<const float *>(lo)[i]);
+    }
+};
+
+// Compute-format tensor: hi (and lo for KIND 1), row stride ld elements.
+struct CTensor {
+    void *hi;
+    void *lo;
+    int ld;
+};
+
+// ---------------------------------------------------------------------------
+// Forward: accumulator = (W^T . H^T)[o, s].  out[s, o] = tanh(acc + b[o]) in
+// compute format (next stage input), or z[s, o] = acc + b[o] in fp32 for the
+// last stage (ref _kernels.pyx:40-62).
+template <int KIND>
+struct EpiFwd {
+    struct Params {
+        const float *bias;  // master fp32 bias of this stage (version read)
+        CTensor out;        // next-stage input record (tanh applied)
+        float *z;           // last stage: fp32 logits [B][dout]
+        int last;
+    };
+    struct State {};
+    __device__ static void begin(const Params &, int, State &) {}
+    __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &) {
+        if (m >= M) return;
+        const float b = p.bias[m];
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+            const int s = n0 + i;
+            if (s >= N) break;
+            const float a = __fadd_rn(v[i], b);
+            if (p.last)
+                p.z[size_t(s) * M + m] = a;
+            else
+                Fmt<KIND>::store(p.out.hi, p.out.lo, size_t(s) * p.out.ld + m, tanhf(a));
+        }
+    }
+    __device__ static void finish(const Params &, int, int, State &) {}
+    __device__ static void extra(const Params &, int) {}
+};
+
+// ---------------------------------------------------------------------------
+// Data gradient: accumulator = (W . dZ^T)[k, s].  dprev[s, k] = acc * (1 - h^2)
+// with h the stage input record, and the bias gradient of the previous stage
+// db[k] = sum_s dprev[s, k] in ascending s (ref _kernels.pyx:115-130).
+template <int KIND>
+struct EpiDgrad {
+    struct Params {
+        CTensor h;      // stage-j input record (tanh outputs of stage j-1)
+        CTensor dprev;  // dZ_{j-1} out
+        float *db;      // bias grad of stage j-1 [din]
+    };
+    struct State {
+        float acc;
+    };
+    __device__ static void begin(const Params &, int, State &st) { st.acc = 0.f; }
+    __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &st) {
+        if (m >= M) return;
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+            const int s = n0 + i;
+            if (s >= N) break;
+            const size_t hi = size_t(s) * p.h.ld + m;
+            const float h = Fmt<KIND>::load(p.h.hi, p.h.lo, hi);
+            const float d = __fmul_rn(v[i], __fsub_rn(1.f, __fmul_rn(h, h)));
+            Fmt<KIND>::store(p.dprev.hi, p.dprev.lo, size_t(s) * p.dprev.ld + m, d);
+            st.acc = __fadd_rn(st.acc, d);
+        }
+    }
+    __device__ static void finish(const Params &p, int m, int M, State &st) {
+        if (m < M) p.db[m] = st.acc;
+    }
+    __device__ static void extra(const Params &, int) {}
+};
+
+// ---------------------------------------------------------------------------
+// Weight gradient fused with the CDP gradient hop and, on the last hop, the
+// SGD(+momentum, weight decay) update (ref engine.py:96-109, comm.py:37-67).
+// accumulator = (H^T . dZ)[k, o] = dW[k, o] of this micro-batch.
+//   mode 0 first hop : S[idx] = g
+//   mode 1 mid hop   : S[idx] = S_in[idx] + g      (S_in: previous worker's
+//                      partial; a peer-GPU pointer when workers are GPUs)
+//   mode 2 last hop  : G = S_in[idx] + g, update
+//   mode 3 only      : G = g (N = 1), update
+//   mode 4 grad only : out[idx] = g (operator-level value+grad)
+// Update (fp32): momentum: v = m*v + (G/n + wd*th); th' = th - lr*v.
+//                no momentum: th' = th - (lr/n)*G   (wd: th - lr*(G/n + wd*th)).
+// The new parameters are also written as the packed compute-format copy the
+// next GEMMs read.  Non-finite gradient / parameter -> flag bits.
+struct HopParams {
+    int mode;
+    int stage;            // 1-based
+    int64_t base;         // stage offset in the flat parameter vector
+    int din, dout;
+    const float *s_in;
+    float *s_out;
+    const float *theta_cur;
+    float *theta_new;
+    float *vel;
+    const float *lr;      // device scalar (per-step learning rate)
+    float momentum, wd, n_mb;
+    CTensor wc_new;       // packed compute copy of W (new version)
+    const float *db;      // this micro-batch's bias gradient [dout]
+    unsigned *grad_flags; // bit (stage-1): non-finite gradient
+    unsigned *upd_flags;  // bit (stage-1): non-finite updated parameter
+};
+
+template <int KIND>
+__device__ __forceinline__ void hop_elem(const HopParams &p, int64_t idx, float g, size_t widx, bool is_w,
+                                         bool &bad_g, bool &bad_u) {
+    if (!isfinite(g)) bad_g = true;
+    if (p.mode == 0 || p.mode == 4) {
+        p.s_out[idx] = g;
+        return;
+    }
+    if (p.mode == 1) {
+        p.s_out[idx] = __fadd_rn(__ldcg(p.s_in + idx), g);
+        return;
+    }
+    const float G = p.mode == 2 ? __fadd_rn(__ldcg(p.s_in + idx), g) : g;
+    const float th = p.theta_cur[idx];
+    const float lr = *p.lr;
+    float nt;
+    if (p.momentum != 0.f) {
+        float gg = __fdiv_rn(G, p.n_mb);
+        if (p.wd != 0.f) gg = __fadd_rn(gg, __fmul_rn(p.wd, th));
+        const float v = __fadd_rn(__fmul_rn(p.vel[idx], p.momentum), gg);
+        p.vel[idx] = v;
+        nt = __fsub_rn(th, __fmul_rn(lr, v));
+    } else if (p.wd != 0.f) {
+        nt = __fsub_rn(th, __fmul_rn(lr, __fadd_rn(__fdiv_rn(G, p.n_mb), __fmul_rn(p.wd, th))));
+    } else {
+        nt = __fsub_rn(th, __fmul_rn(__fdiv_rn(lr, p.n_mb), G));
+    }
+    if (!isfinite(nt)) bad_u = true;
+    p.theta_new[idx] = nt;
+    if (is_w) Fmt<KIND>::store(p.wc_new.hi, p.wc_new.lo, widx, nt);
+}
+
+template <int KIND>
+struct EpiWgrad {
+    using Params = HopParams;
+    struct State {
+        bool bad_g, bad_u;
+    };
+    __device__ static void begin(const Params &, int, State &st) { st.bad_g = st.bad_u = false; }
+    __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &st) {
+        if (m >= M) return;
+        const int64_t row = p.base + int64_t(m) * p.dout;
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+            const int o = n0 + i;
+            if (o >= N) break;
+            hop_elem<KIND>(p, row + o, v[i], size_t(m) * p.wc_new.ld + o, true, st.bad_g, st.bad_u);
+        }
+    }
+    __device__ static void finish(const Params &p, int, int, State &st) {
+        if (st.bad_g) atomicOr(p.grad_flags, 1u << (p.stage - 1));
+        if (st.bad_u) atomicOr(p.upd_flags, 1u << (p.stage - 1));
+    }
+    // bias part of the stage: CTA (0,0) epilogue threads
+    __device__ static void extra(const Params &p, int tid) {
+        bool bg = false, bu = false;
+        const int64_t b0 = p.base + int64_t(p.din) * p.dout;
+        for (int o = tid; o < p.dout; o += 128) hop_elem<KIND>(p, b0 + o, p.db[o], 0, false, bg, bu);
+        if (bg) atomicOr(p.grad_flags, 1u << (p.stage - 1));
+        if (bu) atomicOr(p.upd_flags, 1u << (p.stage - 1));
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Loss + dz of the last stage (ref _kernels.pyx:64-100) for one micro-batch.
+// One CTA; thread s handles sample s; the loss is reduced in ascending s.
+template <int KIND>
+__global__ void loss_kernel(const float *__restrict__ z, int B, int dout, int loss_kind, const int *perm,
+                            const int *labels, const float *targets, CTensor dz, float *db, double *loss_out,
+                            unsigned *loss_flag) {
+    extern __shared__ double sh_loss[];
+    const int s = threadIdx.x;
+    double l = 0.0;
+    if (s < B) {
+        const int row = perm[s];
+        const float *zr = z + size_t(s) * dout;
+        if (loss_kind == 0) {
+            const float *tr = targets + size_t(row) * dout;
+            for (int o = 0; o < dout; ++o) {
+                const float d = __fsub_rn(zr[o], tr[o]);
+                l += double(d) * double(d);
+                Fmt<KIND>::store(dz.hi, dz.lo, size_t(s) * dz.ld + o, __fdiv_rn(d, float(B)));
+            }
+        } else {
+            const int lab = labels[row];
+            float mx = zr[0];
+            for (int o = 1; o < dout; ++o) mx = fmaxf(mx, zr[o]);
+            float se = 0.f;
+            for (int o = 0; o < dout; ++o) se = __fadd_rn(se, expf(__fsub_rn(zr[o], mx)));
+            for (int o = 0; o < dout; ++o) {
+                const float pz = __fdiv_rn(expf(__fsub_rn(zr[o], mx)), se);
+                if (o == lab) l = -log(double(pz));
+                Fmt<KIND>::store(dz.hi, dz.lo, size_t(s) * dz.ld + o,
+                                 __fdiv_rn(__fsub_rn(pz, o == lab ? 1.f : 0.f), float(B)));
+            }
+        }
+    }
+    sh_loss[s] = l;
+    __syncthreads();
+    if (s == 0) {
+        double acc = 0.0;
+        for (int k = 0; k < B; ++k) acc += sh_loss[k];
+        acc = loss_kind == 0 ? acc / (2.0 * B) : acc / B;
+        *loss_out = acc;
+        if (!isfinite(acc)) atomicOr(loss_flag, 1u);
+    }
+    // bias gradient of the last stage, ascending s
+    for (int o = threadIdx.x; o < dout; o += blockDim.x) {
+        float acc = 0.f;
+        for (int k = 0; k < B; ++k) acc = __fadd_rn(acc, Fmt<KIND>::load(dz.hi, dz.lo, size_t(k) * dz.ld + o));
+        db[o] = acc;
+    }
+}
+
+// Gather micro-batch rows of the device-resident dataset into a stage-1
+// input record (compute format).
+template <int KIND>
+__global__ void gather_kernel(const float *__restrict__ data, int din, const int *perm, CTensor out) {
+    const int s = blockIdx.x;
+    const float *src = data + size_t(perm[s]) * din;
+    for (int k = threadIdx.x; k < din; k += blockDim.x) Fmt<KIND>::store(out.hi, out.lo, size_t(s) * out.ld + k, src[k]);
+}
+
+// Pack master fp32 W (reference layout [din][dout]) into a compute copy [din][ld].
+template <int KIND>
+__global__ void pack_w_kernel(const float *__restrict__ w, int din, int dout, CTensor out) {
+    const size_t n = size_t(din) * dout;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t k = i / dout, o = i % dout;
+        Fmt<KIND>::store(out.hi, out.lo, k * out.ld + o, w[i]);
+    }
+}
+
+}  // namespace cdp

@@ -1,0 +1,713 @@
+// Device-resident CDP / DP training step for the stage-stacked MLP.
+//
+// Replaces the reference's `_advance` (training/engine.py:66-116) end to end:
+// per-(micro-batch, stage) version selection, per-micro-batch value+grad
+// (training/_kernels.pyx:25-132), ascending-i gradient accumulation and the
+// SGD(+momentum) update.  Execution follows a step plan compiled from the
+// reference-parity Timeline (paper_2403_08837_b200/executor.py):
+//   * one CUDA stream per worker; F/B tasks of worker i are launched in its
+//     plan order; cross-worker edges (ring-hop order, activation-slot reuse)
+//     become event edges;
+//   * each B task = [loss kernel] -> dgrad GEMM (fused tanh', bias grad) ->
+//     wgrad GEMM whose epilogue IS the gradient hop S_i = S_{i-1} + g_i and,
+//     on the last worker, the SGD update writing version t+1;
+//   * the whole step is captured once per version parity into a CUDA graph.
+// Parameter versions live in two slots (slot = version mod 2); the update of
+// step t writes slot (t+1) mod 2, which only held version t-1.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "../../include/cdp_b200.h"
+#include "gemm_launch.cuh"
+#include "mlp_kernels.cuh"
+
+namespace cdp {
+
+enum OpField { OP_KIND = 0, OP_WORKER, OP_STAGE, OP_FRESH, OP_REC_IN, OP_REC_OUT, OP_HOP, OP_FIELDS_PAD, OP_FIELDS };
+enum HopMode { HOP_FIRST = 0, HOP_MID = 1, HOP_LAST = 2, HOP_ONLY = 3, HOP_GRAD = 4 };
+
+static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t b) : bytes(b) {
+        if (b) {
+            CDP_CUDA(cudaMalloc(&p, b));
+            CDP_CUDA(cudaMemset(p, 0, b));
+        }
+    }
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DevBuf &operator=(DevBuf &&o) noexcept {
+        std::swap(p, o.p);
+        std::swap(bytes, o.bytes);
+        return *this;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <class T>
+    T *as() const { return static_cast<T *>(p); }
+};
+
+// A compute-format tensor [rows][ld] (two arrays for 3xTF32).
+struct CBuf {
+    DevBuf hi, lo;
+    int ld = 0;
+    CTensor view() const { return CTensor{hi.p, lo.p, ld}; }
+};
+
+static CBuf make_cbuf(int kind, int rows, int cols) {
+    CBuf b;
+    const int esz = kind == 0 ? 2 : 4;
+    b.ld = round_up(std::max(cols, 1), 16);  // 16-element rows keep TMA strides 16B-aligned
+    b.hi = DevBuf(size_t(rows) * b.ld * esz);
+    if (kind == 1) b.lo = DevBuf(size_t(rows) * b.ld * esz);
+    return b;
+}
+
+struct StageGeom {
+    int din, dout;
+    int64_t base;
+};
+
+struct Control {  // device control block, refreshed from pinned host memory every step
+    float lr;
+    int step;
+    int pad[2];
+};
+
+struct Flags {
+    unsigned grad, loss, upd, pad;
+};
+
+// -------------------------------------------------------------------------
+struct MlpTrainer {
+    int kind = 0;  // 0 bf16, 1 fp32 (3xTF32)
+    int S = 0, W = 0, B = 0, loss_kind = 1;
+    float momentum = 0.f, wd = 0.f;
+    std::vector<StageGeom> st;
+    int64_t P = 0;
+    int n_samples = 0;
+    int dmax = 0;
+
+    // plan
+    std::vector<std::array<int, OP_FIELDS>> ops;
+    std::vector<std::pair<int, int>> deps;
+    std::vector<int> slots;  // per stage (1..S) number of input-record slots
+
+    // device state
+    DevBuf theta[2], vel, partial;
+    std::vector<CBuf> wc[2];                  // [slot][stage]
+    std::vector<std::vector<CBuf>> rec;       // [stage][slot]
+    DevBuf loss_all;  // [W] per-worker micro-batch losses (double)
+    struct Worker {
+        DevBuf z, db, ws, counters;
+        double *loss = nullptr;
+        CBuf dz[2];
+        cudaStream_t stream = nullptr;
+    };
+    std::vector<Worker> wk;
+    DevBuf data_x, data_lab, data_tgt;
+    DevBuf ctrl_dev, perm_dev, flags_dev, hist_loss, hist_flags, hist_count;
+    // ring of pinned host staging blocks {Control, perm}: a block is reused only
+    // after the H2D copy that read it has executed (event), so back-to-back
+    // asynchronous steps never see a later step's permutation or lr
+    static constexpr int RING = 16;
+    uint8_t *stage_host = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_ev[RING] = {};
+    int stage_next = 0;
+    int hist_cap = 1 << 14;
+    size_t ws_floats = 0;
+
+    cudaStream_t main = nullptr;
+    std::vector<cudaEvent_t> op_events;
+    cudaEvent_t fork_ev = nullptr;
+    std::vector<cudaEvent_t> join_ev;
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    int t = 1;  // training step of the next launch; current version = t
+    int kernels_per_step = 0;
+
+    ~MlpTrainer() {
+        for (auto &e : exec)
+            if (e) cudaGraphExecDestroy(e);
+        for (auto e : op_events) cudaEventDestroy(e);
+        for (auto e : join_ev) cudaEventDestroy(e);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        for (auto &w : wk)
+            if (w.stream) cudaStreamDestroy(w.stream);
+        if (main) cudaStreamDestroy(main);
+        for (auto e : stage_ev)
+            if (e) cudaEventDestroy(e);
+        if (stage_host) cudaFreeHost(stage_host);
+    }
+
+    // ---------------------------------------------------------------- GEMM sizing
+    int bn_rows(int rows) const { return std::min(256, round_up(rows, 32)); }
+    int bn_mn(int n) const {  // MN-major B tile width
+        const int ch = kind == 0 ? 64 : 32;
+        int target = n >= 1024 ? 256 : n >= 256 ? 64 : n;
+        return std::min(256, round_up(std::max(target, ch), ch));
+    }
+    int splits_for(int M, int N, int BN, int K) const {
+        const int bk = kind == 0 ? 64 : 32;
+        const int nseg = kind == 0 ? 1 : 3;
+        const int kb = (K + bk - 1) / bk;
+        const int total = kb * nseg;
+        const int tiles = ((M + 127) / 128) * ((N + BN - 1) / BN);
+        int s = std::max(1, std::min(total, 48 / std::max(tiles, 1)));
+        if (kind == 1) s = std::max(s, (total + 7) / 8);  // <= 256 of K per TMEM accumulation
+        s = std::min(s, total);
+        const int per = (total + s - 1) / s;
+        return (total + per - 1) / per;
+    }
+    size_t ws_need(int M, int N, int BN, int K) const {
+        const int s = splits_for(M, N, BN, K);
+        if (s <= 1) return 0;
+        return size_t((M + 127) / 128) * ((N + BN - 1) / BN) * s * 128 * BN;
+    }
+
+    // ---------------------------------------------------------------- setup
+    void setup(const int64_t *dims, int n_dims) {
+        S = n_dims - 1;
+        CDP_REQUIRE(S >= 1, "dims needs at least input and output widths");
+        CDP_REQUIRE(S <= 32, "at most 32 stages");
+        CDP_REQUIRE(B >= 1 && B <= 256, "micro-batch size must be in [1, 256]");
+        int64_t off = 0;
+        for (int j = 0; j < S; ++j) {
+            StageGeom g{int(dims[j]), int(dims[j + 1]), off};
+            CDP_REQUIRE(g.din >= 1 && g.dout >= 1, "layer widths must be positive");
+            off += int64_t(g.din) * g.dout + g.dout;
+            st.push_back(g);
+            dmax = std::max({dmax, g.din, g.dout});
+        }
+        P = off;
+        for (int v = 0; v < 2; ++v) {
+            theta[v] = DevBuf(size_t(P) * 4);
+            for (int j = 0; j < S; ++j) wc[v].push_back(make_cbuf(kind, st[j].din, st[j].dout));
+        }
+        if (momentum != 0.f) vel = DevBuf(size_t(P) * 4);
+        partial = DevBuf(size_t(P) * 4);
+        rec.resize(S);
+        for (int j = 0; j < S; ++j)
+            for (int r = 0; r < std::max(1, slots[j + 1]); ++r) rec[j].push_back(make_cbuf(kind, B, st[j].din));
+        // split-K workspace: the largest need of any GEMM a worker runs
+        for (int j = 0; j < S; ++j) {
+            ws_floats = std::max(ws_floats, ws_need(st[j].dout, B, bn_rows(B), st[j].din));
+            ws_floats = std::max(ws_floats, ws_need(st[j].din, B, bn_rows(B), st[j].dout));
+            ws_floats = std::max(ws_floats, ws_need(st[j].din, st[j].dout, bn_mn(st[j].dout), B));
+        }
+        wk.resize(W);
+        loss_all = DevBuf(size_t(W) * 8);
+        for (int i = 0; i < W; ++i) wk[i].loss = loss_all.as<double>() + i;
+        for (auto &w : wk) {
+            w.z = DevBuf(size_t(B) * st[S - 1].dout * 4);
+            w.db = DevBuf(size_t(S) * dmax * 4);
+            w.ws = DevBuf(std::max<size_t>(ws_floats, 1) * 4);
+            w.counters = DevBuf(4096 * 4);
+            for (int b = 0; b < 2; ++b) w.dz[b] = make_cbuf(kind, B, dmax);
+            CDP_CUDA(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+        }
+        CDP_CUDA(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
+        ctrl_dev = DevBuf(sizeof(Control));
+        perm_dev = DevBuf(size_t(W) * B * 4);
+        flags_dev = DevBuf(sizeof(Flags));
+        hist_loss = DevBuf(size_t(hist_cap) * 8);
+        hist_flags = DevBuf(size_t(hist_cap) * sizeof(Flags));
+        hist_count = DevBuf(4);
+        stage_bytes = (sizeof(Control) + size_t(W) * B * 4 + 255) / 256 * 256;
+        CDP_CUDA(cudaMallocHost(&stage_host, stage_bytes * RING));
+        for (auto &e : stage_ev) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+
+    void upload_data(int n, const float *x, const int *labels, const float *targets) {
+        n_samples = std::max(n, W * B);
+        data_x = DevBuf(size_t(n_samples) * st[0].din * 4);
+        if (x) CDP_CUDA(cudaMemcpy(data_x.p, x, size_t(n) * st[0].din * 4, cudaMemcpyHostToDevice));
+        if (loss_kind == 1) {
+            data_lab = DevBuf(size_t(n_samples) * 4);
+            if (labels) CDP_CUDA(cudaMemcpy(data_lab.p, labels, size_t(n) * 4, cudaMemcpyHostToDevice));
+        } else {
+            data_tgt = DevBuf(size_t(n_samples) * st[S - 1].dout * 4);
+            if (targets)
+                CDP_CUDA(cudaMemcpy(data_tgt.p, targets, size_t(n) * st[S - 1].dout * 4, cudaMemcpyHostToDevice));
+        }
+    }
+
+    // ---------------------------------------------------------------- GEMM launches
+    template <int K>
+    static Operand op_of(const CBuf &b, bool lo, bool mn_major, int mn, int k) {
+        return Operand{lo ? b.lo.p : b.hi.p, mn_major, uint64_t(mn), uint64_t(k), uint64_t(b.ld)};
+    }
+
+    // Segments for (A, B): bf16 1; 3xTF32 (hi,hi), (hi,lo), (lo,hi).
+    template <int K>
+    static int segments(const CBuf &a, bool amn, int am, int ak, const CBuf &b, bool bmn, int bn_, int bk,
+                        Operand *A, Operand *Bo) {
+        if (K == 0) {
+            A[0] = op_of<K>(a, false, amn, am, ak);
+            Bo[0] = op_of<K>(b, false, bmn, bn_, bk);
+            return 1;
+        }
+        A[0] = op_of<K>(a, false, amn, am, ak), Bo[0] = op_of<K>(b, false, bmn, bn_, bk);
+        A[1] = op_of<K>(a, false, amn, am, ak), Bo[1] = op_of<K>(b, true, bmn, bn_, bk);
+        A[2] = op_of<K>(a, true, amn, am, ak), Bo[2] = op_of<K>(b, false, bmn, bn_, bk);
+        return 3;
+    }
+
+    template <int K, bool AMN, bool BMN, class Epi>
+    void gemm(int BN, const Operand *A, const Operand *Bo, int nseg, int M, int N, int Kd, Worker &w,
+              const typename Epi::Params &ep, cudaStream_t s) {
+        const int splits = splits_for(M, N, BN, Kd);
+        GemmPlan p;
+#define CDP_GEMM_BN(BN_)                                                                                            \
+    case BN_:                                                                                                       \
+        if constexpr (!BMN || BN_ % (K == 0 ? 64 : 32) == 0) {                                                      \
+            p = plan_gemm<K, BN_, AMN, BMN>(A, Bo, nseg, M, N, Kd, splits, w.ws.as<float>(), w.counters.as<int>()); \
+            CDP_REQUIRE(gemm_ws_floats(p, BN_) <= ws_floats, "split-K workspace too small");                      \
+            launch_gemm<K, BN_, AMN, BMN, Epi>(p, ep, s);                                                          \
+            ++kernels_per_step;                                                                                    \
+            return;                                                                                                \
+        }                                                                                                           \
+        break;
+        switch (BN) {
+            CDP_GEMM_BN(32)
+            CDP_GEMM_BN(64)
+            CDP_GEMM_BN(128)
+            CDP_GEMM_BN(256)
+            default:
+                break;
+        }
+#undef CDP_GEMM_BN
+        throw CdpError("unsupported GEMM tile width " + std::to_string(BN));
+    }
+
+    // ---------------------------------------------------------------- tasks
+    template <int K>
+    void forward(int w, int j, int vslot, int rin, int rout, cudaStream_t s, const int *perm_w) {
+        const StageGeom &g = st[j];
+        Worker &wr = wk[w];
+        if (j == 0) {
+            gather_kernel<K><<<B, 256, 0, s>>>(data_x.as<float>(), g.din, perm_w, rec[0][rin].view());
+            CDP_CUDA(cudaGetLastError());
+            ++kernels_per_step;
+        }
+        Operand A[3], Bo[3];
+        const int nseg = segments<K>(wc[vslot][j], true, g.dout, g.din, rec[j][rin], false, B, g.din, A, Bo);
+        typename EpiFwd<K>::Params ep{};
+        ep.bias = theta[vslot].as<float>() + g.base + int64_t(g.din) * g.dout;
+        ep.last = j == S - 1;
+        if (ep.last)
+            ep.z = wr.z.as<float>();
+        else
+            ep.out = rec[j + 1][rout].view();
+        gemm<K, true, false, EpiFwd<K>>(bn_rows(B), A, Bo, nseg, g.dout, B, g.din, wr, ep, s);
+    }
+
+    template <int K>
+    void backward(int w, int j, int vslot, int rin, int hop, int cur_slot, cudaStream_t s, const int *perm_w) {
+        const StageGeom &g = st[j];
+        Worker &wr = wk[w];
+        Flags *fl = flags_dev.as<Flags>();
+        const int cur = (S - 1 - j) & 1;
+        float *db = wr.db.as<float>();
+        if (j == S - 1) {
+            loss_kernel<K><<<1, std::max(32, round_up(B, 32)), sizeof(double) * std::max(32, round_up(B, 32)), s>>>(
+                wr.z.as<float>(), B, g.dout, loss_kind, perm_w, data_lab.as<int>(), data_tgt.as<float>(),
+                wr.dz[cur].view(), db + size_t(j) * dmax, wr.loss, &fl->loss);
+            CDP_CUDA(cudaGetLastError());
+            ++kernels_per_step;
+        }
+        Operand A[3], Bo[3];
+        if (j > 0) {  // data gradient into dZ_{j-1} (+ bias grad of stage j-1)
+            const int nseg = segments<K>(wc[vslot][j], false, g.din, g.dout, wr.dz[cur], false, B, g.dout, A, Bo);
+            typename EpiDgrad<K>::Params ep{rec[j][rin].view(), wr.dz[cur ^ 1].view(), db + size_t(j - 1) * dmax};
+            gemm<K, false, false, EpiDgrad<K>>(bn_rows(B), A, Bo, nseg, g.din, B, g.dout, wr, ep, s);
+        }
+        // weight gradient fused with the ring hop / update
+        const int nseg = segments<K>(rec[j][rin], true, g.din, B, wr.dz[cur], true, g.dout, B, A, Bo);
+        HopParams hp{};
+        hp.mode = hop;
+        hp.stage = j + 1;
+        hp.base = g.base;
+        hp.din = g.din;
+        hp.dout = g.dout;
+        hp.s_in = partial.as<float>();
+        hp.s_out = partial.as<float>();
+        hp.theta_cur = theta[cur_slot].as<float>();
+        hp.theta_new = theta[cur_slot ^ 1].as<float>();
+        hp.vel = vel.as<float>();
+        hp.lr = &ctrl_dev.as<Control>()->lr;
+        hp.momentum = momentum;
+        hp.wd = wd;
+        hp.n_mb = float(W);
+        hp.wc_new = wc[cur_slot ^ 1][j].view();
+        hp.db = db + size_t(j) * dmax;
+        hp.grad_flags = &fl->grad;
+        hp.upd_flags = &fl->upd;
+        gemm<K, true, true, EpiWgrad<K>>(bn_mn(g.dout), A, Bo, nseg, g.din, g.dout, B, wr, hp, s);
+    }
+
+    // ---------------------------------------------------------------- capture
+    template <int K>
+    void record_step(int p) {
+        kernels_per_step = 0;
+        CDP_CUDA(cudaEventRecord(fork_ev, main));
+        for (auto &w : wk) CDP_CUDA(cudaStreamWaitEvent(w.stream, fork_ev, 0));
+        std::vector<std::vector<int>> into(ops.size());
+        for (auto &d : deps) into[d.second].push_back(d.first);
+        for (size_t o = 0; o < ops.size(); ++o) {
+            const auto &op = ops[o];
+            const int w = op[OP_WORKER] - 1, j = op[OP_STAGE] - 1;
+            cudaStream_t s = wk[w].stream;
+            for (int d : into[o]) CDP_CUDA(cudaStreamWaitEvent(s, op_events[d], 0));
+            const int vslot = op[OP_FRESH] ? p : (p ^ 1);
+            const int *perm_w = perm_dev.as<int>() + size_t(w) * B;
+            if (op[OP_KIND] == 0)
+                forward<K>(w, j, vslot, op[OP_REC_IN], op[OP_REC_OUT], s, perm_w);
+            else
+                backward<K>(w, j, vslot, op[OP_REC_IN], op[OP_HOP], p, s, perm_w);
+            CDP_CUDA(cudaEventRecord(op_events[o], s));
+        }
+        for (int w = 0; w < W; ++w) {
+            CDP_CUDA(cudaEventRecord(join_ev[w], wk[w].stream));
+            CDP_CUDA(cudaStreamWaitEvent(main, join_ev[w], 0));
+        }
+        finish_step();
+    }
+
+    void finish_step();
+
+    void capture() {
+        op_events.resize(ops.size());
+        for (auto &e : op_events) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        join_ev.resize(W);
+        for (auto &e : join_ev) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CDP_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+        for (int p = 0; p < 2; ++p) {
+            cudaGraph_t g;
+            CDP_CUDA(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
+            try {
+                if (kind == 0)
+                    record_step<0>(p);
+                else
+                    record_step<1>(p);
+            } catch (...) {
+                cudaStreamEndCapture(main, &g);
+                throw;
+            }
+            CDP_CUDA(cudaStreamEndCapture(main, &g));
+            CDP_CUDA(cudaGraphInstantiate(&exec[p], g, 0));
+            CDP_CUDA(cudaGraphDestroy(g));
+        }
+    }
+
+    // ---------------------------------------------------------------- params
+    void pack_all(int slot) {
+        for (int j = 0; j < S; ++j) {
+            const float *w = theta[slot].as<float>() + st[j].base;
+            if (kind == 0)
+                pack_w_kernel<0><<<148, 256, 0, main>>>(w, st[j].din, st[j].dout, wc[slot][j].view());
+            else
+                pack_w_kernel<1><<<148, 256, 0, main>>>(w, st[j].din, st[j].dout, wc[slot][j].view());
+            CDP_CUDA(cudaGetLastError());
+        }
+    }
+
+    void set_params(int which, const float *host) {
+        // which: 0 = current (version t), 1 = previous (version t-1), -1 both
+        for (int v = 0; v < 2; ++v) {
+            if (which >= 0 && v != which) continue;
+            const int slot = v == 0 ? (t & 1) : ((t & 1) ^ 1);
+            CDP_CUDA(cudaMemcpyAsync(theta[slot].p, host, size_t(P) * 4, cudaMemcpyHostToDevice, main));
+            pack_all(slot);
+        }
+        CDP_CUDA(cudaStreamSynchronize(main));
+    }
+
+    void get_params(int which, float *host) {
+        CDP_CUDA(cudaStreamSynchronize(main));
+        const int slot = which == 0 ? (t & 1) : ((t & 1) ^ 1);
+        CDP_CUDA(cudaMemcpy(host, theta[slot].p, size_t(P) * 4, cudaMemcpyDeviceToHost));
+    }
+
+    void set_velocity(const float *host) {
+        CDP_REQUIRE(vel.p != nullptr, "trainer has no momentum buffer");
+        CDP_CUDA(cudaMemcpy(vel.p, host, size_t(P) * 4, cudaMemcpyHostToDevice));
+    }
+    void get_velocity(float *host) {
+        CDP_REQUIRE(vel.p != nullptr, "trainer has no momentum buffer");
+        CDP_CUDA(cudaStreamSynchronize(main));
+        CDP_CUDA(cudaMemcpy(host, vel.p, size_t(P) * 4, cudaMemcpyDeviceToHost));
+    }
+
+    // One training step.  perm: W*B dataset row indices (micro-batch i = rows
+    // [(i-1)B, iB)).  Asynchronous; results land in the history ring.
+    void step(const int *perm, float lr) {
+        const int k = stage_next;
+        stage_next = (stage_next + 1) % RING;
+        CDP_CUDA(cudaEventSynchronize(stage_ev[k]));  // the copy that last read this block has run
+        uint8_t *blk = stage_host + size_t(k) * stage_bytes;
+        Control *c = reinterpret_cast<Control *>(blk);
+        c->lr = lr;
+        c->step = t;
+        std::memcpy(blk + sizeof(Control), perm, size_t(W) * B * 4);
+        CDP_CUDA(cudaMemcpyAsync(ctrl_dev.p, blk, sizeof(Control), cudaMemcpyHostToDevice, main));
+        CDP_CUDA(cudaMemcpyAsync(perm_dev.p, blk + sizeof(Control), size_t(W) * B * 4, cudaMemcpyHostToDevice, main));
+        CDP_CUDA(cudaEventRecord(stage_ev[k], main));
+        CDP_CUDA(cudaGraphLaunch(exec[t & 1], main));
+        ++t;
+    }
+
+    // Host-batch step (end-to-end path): the step's inputs come from host memory.
+    void step_host_batch(const float *x, const int *labels, const float *targets, float lr) {
+        const size_t rows = size_t(W) * B;
+        CDP_CUDA(cudaMemcpyAsync(data_x.p, x, rows * st[0].din * 4, cudaMemcpyHostToDevice, main));
+        if (loss_kind == 1)
+            CDP_CUDA(cudaMemcpyAsync(data_lab.p, labels, rows * 4, cudaMemcpyHostToDevice, main));
+        else
+            CDP_CUDA(cudaMemcpyAsync(data_tgt.p, targets, rows * st[S - 1].dout * 4, cudaMemcpyHostToDevice, main));
+        std::vector<int> ident(rows);
+        for (size_t r = 0; r < rows; ++r) ident[r] = int(r);
+        step(ident.data(), lr);
+    }
+};
+
+__global__ void finish_step_kernel(const double *losses, int W, Flags *flags, double *hist_loss, Flags *hist_flags,
+                                   int *hist_count, int cap) {
+    double acc = 0.0;
+    for (int w = 0; w < W; ++w) acc += losses[w];  // ascending micro-batch (ref engine.py:96)
+    const int c = *hist_count;
+    hist_loss[c % cap] = acc / W;  // ring of the last `cap` steps
+    hist_flags[c % cap] = *flags;
+    *hist_count = c + 1;
+    *flags = Flags{0, 0, 0, 0};
+}
+
+void MlpTrainer::finish_step() {
+    finish_step_kernel<<<1, 1, 0, main>>>(loss_all.as<double>(), W, flags_dev.as<Flags>(), hist_loss.as<double>(),
+                                          hist_flags.as<Flags>(), hist_count.as<int>(), hist_cap);
+    CDP_CUDA(cudaGetLastError());
+    ++kernels_per_step;
+}
+
+}  // namespace cdp
+
+using namespace cdp;
+
+struct cdp_trainer {
+    std::unique_ptr<MlpTrainer> impl;
+};
+
+extern "C" int cdp_trainer_create(int n_dims, const int64_t *dims, int micro_batch, int n_workers, int loss_kind,
+                                  int dtype, float momentum, float weight_decay, int n_ops, const int32_t *ops,
+                                  int n_deps, const int32_t *deps, const int32_t *slots_per_stage, int n_samples,
+                                  const float *x, const int32_t *labels, const float *targets, cdp_trainer **out) {
+    return guarded([&] {
+        CDP_REQUIRE(dtype == CDP_DTYPE_FP32 || dtype == CDP_DTYPE_BF16, "dtype must be CDP_DTYPE_FP32 or CDP_DTYPE_BF16");
+        CDP_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (mse) or 1 (xent)");
+        CDP_REQUIRE(n_workers >= 1, "n_workers must be >= 1");
+        auto tr = std::make_unique<MlpTrainer>();
+        tr->kind = dtype == CDP_DTYPE_BF16 ? 0 : 1;
+        tr->W = n_workers;
+        tr->B = micro_batch;
+        tr->loss_kind = loss_kind;
+        tr->momentum = momentum;
+        tr->wd = weight_decay;
+        tr->slots.assign(n_dims, 1);
+        for (int j = 1; j < n_dims; ++j) tr->slots[j] = slots_per_stage[j];
+        for (int o = 0; o < n_ops; ++o) {
+            std::array<int, OP_FIELDS> a;
+            for (int f = 0; f < OP_FIELDS; ++f) a[f] = ops[o * OP_FIELDS + f];
+            CDP_REQUIRE(a[OP_WORKER] >= 1 && a[OP_WORKER] <= n_workers, "op worker out of range");
+            CDP_REQUIRE(a[OP_STAGE] >= 1 && a[OP_STAGE] < n_dims, "op stage out of range");
+            tr->ops.push_back(a);
+        }
+        for (int d = 0; d < n_deps; ++d) {
+            CDP_REQUIRE(deps[2 * d] < deps[2 * d + 1], "plan edges must point forward in op order");
+            tr->deps.emplace_back(deps[2 * d], deps[2 * d + 1]);
+        }
+        tr->setup(dims, n_dims);
+        for (auto &op : tr->ops) {
+            CDP_REQUIRE(op[OP_REC_IN] < tr->slots[op[OP_STAGE]], "record slot out of range");
+            if (op[OP_KIND] == 0 && op[OP_STAGE] < tr->S)
+                CDP_REQUIRE(op[OP_REC_OUT] < tr->slots[op[OP_STAGE] + 1], "record slot out of range");
+        }
+        tr->upload_data(n_samples, x, labels, targets);
+        tr->capture();
+        *out = new cdp_trainer{std::move(tr)};
+    });
+}
+
+extern "C" void cdp_trainer_destroy(cdp_trainer *tr) {
+    if (tr) {
+        cudaDeviceSynchronize();
+        delete tr;
+    }
+}
+
+extern "C" int cdp_trainer_set_params(cdp_trainer *tr, int which, const float *theta) {
+    return guarded([&] { tr->impl->set_params(which, theta); });
+}
+
+extern "C" int cdp_trainer_get_params(cdp_trainer *tr, int which, float *theta) {
+    return guarded([&] { tr->impl->get_params(which, theta); });
+}
+
+extern "C" int cdp_trainer_set_velocity(cdp_trainer *tr, const float *v) {
+    return guarded([&] { tr->impl->set_velocity(v); });
+}
+
+extern "C" int cdp_trainer_get_velocity(cdp_trainer *tr, float *v) {
+    return guarded([&] { tr->impl->get_velocity(v); });
+}
+
+extern "C" int cdp_trainer_step(cdp_trainer *tr, const int32_t *perm, float lr) {
+    return guarded([&] { tr->impl->step(perm, lr); });
+}
+
+extern "C" int cdp_trainer_step_host_batch(cdp_trainer *tr, const float *x, const int32_t *labels,
+                                           const float *targets, float lr) {
+    return guarded([&] { tr->impl->step_host_batch(x, labels, targets, lr); });
+}
+
+extern "C" int cdp_trainer_sync(cdp_trainer *tr) {
+    return guarded([&] { CDP_CUDA(cudaStreamSynchronize(tr->impl->main)); });
+}
+
+extern "C" int cdp_trainer_history(cdp_trainer *tr, int max, double *losses, uint32_t *flags, int *count) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        int c = 0;
+        CDP_CUDA(cudaMemcpy(&c, m.hist_count.p, 4, cudaMemcpyDeviceToHost));
+        *count = c;
+        // oldest retained step first: steps [c - n, c) live at ring index k % cap
+        const int n = std::min({c, max, m.hist_cap});
+        if (n > 0) {
+            std::vector<double> l(m.hist_cap);
+            std::vector<Flags> f(m.hist_cap);
+            CDP_CUDA(cudaMemcpy(l.data(), m.hist_loss.p, size_t(m.hist_cap) * 8, cudaMemcpyDeviceToHost));
+            CDP_CUDA(cudaMemcpy(f.data(), m.hist_flags.p, size_t(m.hist_cap) * sizeof(Flags), cudaMemcpyDeviceToHost));
+            for (int i = 0; i < n; ++i) {
+                const int k = (c - n + i) % m.hist_cap;
+                losses[i] = l[k];
+                flags[3 * i] = f[k].grad;
+                flags[3 * i + 1] = f[k].loss;
+                flags[3 * i + 2] = f[k].upd;
+            }
+        }
+    });
+}
+
+extern "C" int cdp_trainer_stats(cdp_trainer *tr, int64_t *out, int n_out) {
+    // [0] activation-record bytes, [1] parameter-state bytes, [2] kernels per step,
+    // [3] step (next), [4] stream count, [5] ops per step
+    return guarded([&] {
+        auto &m = *tr->impl;
+        int64_t act = 0;
+        for (auto &stage : m.rec)
+            for (auto &r : stage) act += int64_t(r.hi.bytes + r.lo.bytes);
+        int64_t par = int64_t(m.theta[0].bytes) * 2 + int64_t(m.vel.bytes) + int64_t(m.partial.bytes);
+        for (int v = 0; v < 2; ++v)
+            for (auto &c : m.wc[v]) par += int64_t(c.hi.bytes + c.lo.bytes);
+        int64_t vals[6] = {act, par, m.kernels_per_step, m.t, int64_t(m.W), int64_t(m.ops.size())};
+        for (int i = 0; i < n_out && i < 6; ++i) out[i] = vals[i];
+    });
+}
+
+extern "C" int cdp_trainer_get_grad(cdp_trainer *tr, float *grad) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        CDP_CUDA(cudaMemcpy(grad, m.partial.p, size_t(m.P) * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+extern "C" int cdp_trainer_stream(cdp_trainer *tr, void **stream) {
+    return guarded([&] { *stream = tr->impl->main; });
+}
+
+// ---------------------------------------------------------------------------
+// Operator level (ref training/_kernels.pyx:25-132, backend protocol
+// training/backend.py:13-30): value + flat gradient of one micro-batch, host
+// fp64 in / out.  Runs the same fused layer kernels as the trainer through a
+// cached single-worker plan whose B tasks write the raw gradient (hop mode 4).
+namespace {
+std::mutex g_vg_mu;
+std::map<std::vector<int64_t>, std::unique_ptr<MlpTrainer>> g_vg_cache;
+
+MlpTrainer &value_grad_trainer(int n_dims, const int64_t *dims, int batch, int loss_kind, int dtype) {
+    std::vector<int64_t> key(dims, dims + n_dims);
+    key.push_back(batch);
+    key.push_back(loss_kind);
+    key.push_back(dtype);
+    auto it = g_vg_cache.find(key);
+    if (it != g_vg_cache.end()) return *it->second;
+    auto tr = std::make_unique<MlpTrainer>();
+    tr->kind = dtype == CDP_DTYPE_BF16 ? 0 : 1;
+    tr->W = 1;
+    tr->B = batch;
+    tr->loss_kind = loss_kind;
+    const int S = n_dims - 1;
+    tr->slots.assign(n_dims, 1);
+    for (int j = 1; j <= S; ++j) tr->ops.push_back({0, 1, j, 1, 0, 0, 0, 0});
+    for (int j = S; j >= 1; --j) tr->ops.push_back({1, 1, j, 1, 0, 0, HOP_GRAD, 0});
+    tr->setup(dims, n_dims);
+    tr->upload_data(batch, nullptr, nullptr, nullptr);
+    tr->capture();
+    auto &ref = *tr;
+    g_vg_cache.emplace(std::move(key), std::move(tr));
+    return ref;
+}
+}  // namespace
+
+extern "C" int cdp_mlp_value_grad(int n_dims, const int64_t *dims, const double *theta, int batch, const double *x,
+                                  const double *y, const int64_t *labels, int loss_kind, int dtype, double *loss_out,
+                                  double *grad_out) {
+    return guarded([&] {
+        CDP_REQUIRE(n_dims >= 2, "dims needs at least input and output widths");
+        CDP_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (mse) or 1 (xent)");
+        CDP_REQUIRE(dtype == CDP_DTYPE_FP32 || dtype == CDP_DTYPE_BF16, "bad dtype");
+        CDP_REQUIRE(loss_kind == 0 ? y != nullptr : labels != nullptr, "missing targets");
+        std::lock_guard<std::mutex> lk(g_vg_mu);
+        MlpTrainer &tr = value_grad_trainer(n_dims, dims, batch, loss_kind, dtype);
+        std::vector<float> th(tr.P);
+        for (int64_t i = 0; i < tr.P; ++i) th[i] = float(theta[i]);
+        tr.set_params(-1, th.data());
+        const int din = int(dims[0]), dout = int(dims[n_dims - 1]);
+        std::vector<float> xf(size_t(batch) * din), yf;
+        std::vector<int> lab;
+        for (size_t i = 0; i < xf.size(); ++i) xf[i] = float(x[i]);
+        if (loss_kind == 0) {
+            yf.resize(size_t(batch) * dout);
+            for (size_t i = 0; i < yf.size(); ++i) yf[i] = float(y[i]);
+        } else {
+            lab.resize(batch);
+            for (int i = 0; i < batch; ++i) {
+                CDP_REQUIRE(labels[i] >= 0 && labels[i] < dout, "label out of range");
+                lab[i] = int(labels[i]);
+            }
+        }
+        tr.step_host_batch(xf.data(), lab.data(), yf.data(), 0.f);
+        CDP_CUDA(cudaStreamSynchronize(tr.main));
+        int c = 0;
+        CDP_CUDA(cudaMemcpy(&c, tr.hist_count.p, 4, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemcpy(loss_out, tr.hist_loss.as<double>() + (c - 1) % tr.hist_cap, 8, cudaMemcpyDeviceToHost));
+        std::vector<float> g(tr.P);
+        CDP_CUDA(cudaMemcpy(g.data(), tr.partial.p, size_t(tr.P) * 4, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < tr.P; ++i) grad_out[i] = double(g[i]);
+    });
+}

@@ -1,0 +1,145 @@
+"""Device-resident CDP / DP trainer over the C-ABI (`cdp_trainer_*`).
+
+One `DeviceMlpTrainer` owns the parameter versions (two slots), momentum,
+partial-sum buffer, activation-record slots and the two captured step graphs
+of one (model, rule, dtype) configuration.  `step()` launches one training
+step asynchronously; `history()` returns the per-step mean losses and the
+non-finite flags the kernels raised.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from .executor import StepPlan, compile_step_plan
+from .rules import UpdateRule
+
+DTYPES = {"fp32": 0, "bf16": 1}
+
+
+def _i32(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def _f32(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+class DeviceMlpTrainer:
+    def __init__(self, dims, micro_batch: int, n_workers: int, loss_kind: int, rule: UpdateRule | None,
+                 dtype: str = "fp32", momentum: float = 0.0, weight_decay: float = 0.0,
+                 inputs: np.ndarray | None = None, targets: np.ndarray | None = None, grad_only: bool = False):
+        if dtype not in DTYPES:
+            raise ValueError(f"dtype must be one of {sorted(DTYPES)}")
+        self.lib = N.lib()
+        self.dims = tuple(int(d) for d in dims)
+        self.n_stages = len(self.dims) - 1
+        self.micro_batch = int(micro_batch)
+        self.n_workers = int(n_workers)
+        self.loss_kind = int(loss_kind)
+        self.dtype = dtype
+        self.plan: StepPlan = compile_step_plan(self.n_stages, self.n_workers, rule, grad_only=grad_only)
+        self.sizes = [self.dims[j] * self.dims[j + 1] + self.dims[j + 1] for j in range(self.n_stages)]
+        self.P = sum(self.sizes)
+        dims_a = np.asarray(self.dims, dtype=np.int64)
+        n = 0
+        x = lab = tgt = None
+        if inputs is not None:
+            x = np.ascontiguousarray(inputs, dtype=np.float32)
+            n = x.shape[0]
+            if loss_kind == 1:
+                lab = np.ascontiguousarray(targets, dtype=np.int32)
+            else:
+                tgt = np.ascontiguousarray(targets, dtype=np.float32)
+        ops = np.ascontiguousarray(self.plan.ops, dtype=np.int32)
+        deps = np.ascontiguousarray(self.plan.deps, dtype=np.int32)
+        slots = np.ascontiguousarray(self.plan.slots, dtype=np.int32)
+        h = ctypes.c_void_p()
+        N.check(self.lib.cdp_trainer_create(
+            len(dims_a), dims_a.ctypes.data_as(N.c_int64_p), self.micro_batch, self.n_workers, self.loss_kind,
+            DTYPES[dtype], float(momentum), float(weight_decay), ops.shape[0], _i32(ops), deps.shape[0], _i32(deps),
+            _i32(slots), n, _f32(x) if x is not None else None, _i32(lab) if lab is not None else None,
+            _f32(tgt) if tgt is not None else None, ctypes.byref(h)))
+        self.h = h
+        self.has_momentum = momentum != 0.0
+        self._keep = (x, lab, tgt)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cdp_trainer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- params
+    def set_params(self, flat: np.ndarray, which: int = -1):
+        a = np.ascontiguousarray(flat, dtype=np.float32)
+        assert a.size == self.P
+        N.check(self.lib.cdp_trainer_set_params(self.h, which, _f32(a)))
+
+    def get_params(self, which: int = 0) -> np.ndarray:
+        out = np.empty(self.P, dtype=np.float32)
+        N.check(self.lib.cdp_trainer_get_params(self.h, which, _f32(out)))
+        return out
+
+    def set_velocity(self, flat: np.ndarray):
+        a = np.ascontiguousarray(flat, dtype=np.float32)
+        N.check(self.lib.cdp_trainer_set_velocity(self.h, _f32(a)))
+
+    def get_velocity(self) -> np.ndarray:
+        out = np.empty(self.P, dtype=np.float32)
+        N.check(self.lib.cdp_trainer_get_velocity(self.h, _f32(out)))
+        return out
+
+    def get_grad(self) -> np.ndarray:
+        out = np.empty(self.P, dtype=np.float32)
+        N.check(self.lib.cdp_trainer_get_grad(self.h, _f32(out)))
+        return out
+
+    # -------------------------------------------------------------- steps
+    def step(self, perm: np.ndarray, lr: float):
+        p = np.ascontiguousarray(perm, dtype=np.int32)
+        assert p.size == self.n_workers * self.micro_batch
+        N.check(self.lib.cdp_trainer_step(self.h, _i32(p), float(lr)))
+
+    def step_host_batch(self, x: np.ndarray, y: np.ndarray, lr: float):
+        """Step whose inputs come from host memory (copied H2D inside the step)."""
+        xa = np.ascontiguousarray(x, dtype=np.float32)
+        if self.loss_kind == 1:
+            ya = np.ascontiguousarray(y, dtype=np.int32)
+            N.check(self.lib.cdp_trainer_step_host_batch(self.h, _f32(xa), _i32(ya), None, float(lr)))
+        else:
+            ya = np.ascontiguousarray(y, dtype=np.float32)
+            N.check(self.lib.cdp_trainer_step_host_batch(self.h, _f32(xa), None, _f32(ya), float(lr)))
+        self._keep_step = (xa, ya)
+
+    def sync(self):
+        N.check(self.lib.cdp_trainer_sync(self.h))
+
+    def history(self, max_steps: int = 1 << 16):
+        losses = np.empty(max_steps, dtype=np.float64)
+        flags = np.empty((max_steps, 3), dtype=np.uint32)
+        cnt = ctypes.c_int()
+        N.check(self.lib.cdp_trainer_history(self.h, max_steps, losses.ctypes.data_as(N.c_double_p),
+                                             flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                             ctypes.byref(cnt)))
+        n = min(cnt.value, max_steps)
+        return losses[:n].copy(), flags[:n].copy()
+
+    def stats(self) -> dict:
+        out = np.zeros(6, dtype=np.int64)
+        N.check(self.lib.cdp_trainer_stats(self.h, out.ctypes.data_as(N.c_int64_p), 6))
+        return {"activation_bytes": int(out[0]), "param_state_bytes": int(out[1]), "kernels_per_step": int(out[2]),
+                "next_step": int(out[3]), "streams": int(out[4]), "ops_per_step": int(out[5])}
+
+    def stream_handle(self) -> int:
+        s = ctypes.c_void_p()
+        N.check(self.lib.cdp_trainer_stream(self.h, ctypes.byref(s)))
+        return s.value or 0

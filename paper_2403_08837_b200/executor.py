@@ -1,0 +1,151 @@
+"""Compile a reference-parity Timeline into the device step plan.
+
+The cyclic step scheduler has two halves: this planner (host, pure Python,
+unit-tested on CPU) and the native executor in
+`csrc/mlp_trainer.cu` that captures the plan into CUDA graphs.
+
+Input: the Timeline of the configured scheme (`schedule.build_cdp_timeline`
+/ `build_dp_timeline`, bit-exact with ref `schedule.py:178-257`).
+Output (`StepPlan`), for one training step in steady state:
+
+* `ops`   one row per F/B task in timeline order (start, worker):
+          [kind(0=F,1=B), worker i, stage j, fresh, rec_in, rec_out, hop, 0]
+          - fresh: the rule's table (ref `rules.py:45-51`); the executor reads
+            stage j from version slot t mod 2 (fresh) or (t-1) mod 2 (stale);
+          - rec_in / rec_out: activation-record slots (the stage-j input of
+            micro-batch i lives from its producer F(i, j-1) to B(i, j));
+          - hop: role of B(i, j) in the gradient chain w1 -> ... -> wN
+            (ref `comm.py:37-67`, ascending-i order of `engine.py:96-101`):
+            0 first, 1 middle, 2 last (fused update), 3 only (N = 1);
+* `deps`  cross-worker edges (before_op, after_op): the ring hop
+          B(i-1, j) -> B(i, j) and activation-slot reuse B(i, j) -> producer
+          of the next record in that slot;
+* `slots` activation-record slots per stage, so peak activation memory is
+          the interval-colouring of the plan, not N records per stage.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .profiles import CostWeights, ParallelismConfig, Scheme
+from .rules import UpdateRule
+from .schedule import TaskKind, build_cdp_timeline, build_dp_timeline
+
+OP_FIELDS = 8
+HOP_FIRST, HOP_MID, HOP_LAST, HOP_ONLY, HOP_GRAD = 0, 1, 2, 3, 4
+
+
+@dataclass
+class StepPlan:
+    n_stages: int
+    n_workers: int
+    ops: np.ndarray      # int32 [n_ops, OP_FIELDS]
+    deps: np.ndarray     # int32 [n_deps, 2]
+    slots: np.ndarray    # int32 [n_stages + 1], slots[j] for stage j (index 0 unused)
+    fresh: np.ndarray    # uint8 [n_workers, n_stages]
+
+    def trace(self, step: int) -> list:
+        """(t, i, j, version) reads of one step, ascending i then j (ref engine.py:92-94)."""
+        out = []
+        for i in range(1, self.n_workers + 1):
+            for j in range(1, self.n_stages + 1):
+                out.append((step, i, j, step if self.fresh[i - 1, j - 1] else step - 1))
+        return out
+
+
+def _template_tasks(n_stages: int, n_workers: int, rule: UpdateRule | None, weights: CostWeights):
+    """(start, worker, kind, stage) for one steady step of the plan."""
+    if n_stages == n_workers:
+        scheme = Scheme.SINGLE_GPU_DP if rule is None else Scheme.SINGLE_GPU_CDP
+        cfg = ParallelismConfig(scheme, n_workers, 1, 2, weights)
+        tl = build_dp_timeline(cfg) if rule is None else build_cdp_timeline(cfg, rule)
+        return [(t.start, t.micro_batch, 0 if t.kind is TaskKind.FORWARD else 1, t.stage)
+                for t in tl.tasks if t.training_step == 2]
+    if rule is not None:
+        raise ValueError("a cyclic rule ties stages to micro-batches (n x n table)")
+    fc, bc = weights.forward_cost, weights.backward_cost
+    out = []
+    for i in range(1, n_workers + 1):
+        for j in range(1, n_stages + 1):
+            out.append(((j - 1) * fc + 1, i, 0, j))
+            out.append((n_stages * fc + (n_stages - j) * bc + 1, i, 1, j))
+    return out
+
+
+def compile_step_plan(n_stages: int, n_workers: int, rule: UpdateRule | None = None,
+                      weights: CostWeights = CostWeights(), grad_only: bool = False) -> StepPlan:
+    if rule is not None:
+        if rule.n != n_workers:
+            raise ValueError("rule size does not match task")
+        rule.check_feasible()
+    tasks = sorted(_template_tasks(n_stages, n_workers, rule, weights), key=lambda x: (x[0], x[1], x[2]))
+    fresh = np.ones((n_workers, n_stages), dtype=np.uint8)
+    if rule is not None:
+        fresh[:] = np.array(rule.fresh, dtype=np.uint8)
+
+    ops, deps = [], []
+    index = {}
+    free = {j: [] for j in range(1, n_stages + 1)}     # free slot ids per stage
+    count = {j: 0 for j in range(1, n_stages + 1)}     # slots created per stage
+    last_user = {}                                     # (j, slot) -> op that released it
+    holder = {}                                        # (i, j) -> slot of record (i, j)
+
+    def acquire(j: int, producer_op: int) -> int:
+        if free[j]:
+            s = free[j].pop(0)
+            rel = last_user.get((j, s))
+            if rel is not None:
+                deps.append((rel, producer_op))
+        else:
+            s = count[j]
+            count[j] += 1
+        return s
+
+    for start, i, kind, j in tasks:
+        o = len(ops)
+        row = [kind, i, j, int(fresh[i - 1, j - 1]), 0, 0, 0, 0]
+        if kind == 0:
+            if j == 1:
+                holder[(i, 1)] = acquire(1, o)
+            row[4] = holder[(i, j)]
+            if j < n_stages:
+                holder[(i, j + 1)] = acquire(j + 1, o)
+                row[5] = holder[(i, j + 1)]
+        else:
+            row[4] = holder[(i, j)]
+            if grad_only:
+                row[6] = HOP_GRAD
+            elif n_workers == 1:
+                row[6] = HOP_ONLY
+            else:
+                row[6] = HOP_FIRST if i == 1 else (HOP_LAST if i == n_workers else HOP_MID)
+            if i > 1 and not grad_only:
+                deps.append((index[(1, i - 1, j)], o))
+            s = holder.pop((i, j))
+            free[j].append(s)
+            last_user[(j, s)] = o
+        index[(kind, i, j)] = o
+        ops.append(row)
+
+    deps = sorted(set(deps))
+    for a, b in deps:
+        assert a < b, "plan edges must point forward"
+    slots = np.zeros(n_stages + 1, dtype=np.int32)
+    for j in range(1, n_stages + 1):
+        slots[j] = max(count[j], 1)
+    return StepPlan(
+        n_stages, n_workers,
+        np.asarray(ops, dtype=np.int32).reshape(-1, OP_FIELDS),
+        np.asarray(deps, dtype=np.int32).reshape(-1, 2),
+        slots, fresh,
+    )
+
+
+def record_bytes(plan: StepPlan, dims, micro_batch: int, elem_bytes: int) -> int:
+    """Activation bytes the executor allocates for `plan` (record j = stage-j input)."""
+    pad = lambda c: (c + 15) // 16 * 16
+    return int(sum(int(plan.slots[j]) * micro_batch * pad(dims[j - 1]) * elem_bytes
+                   for j in range(1, plan.n_stages + 1)))
