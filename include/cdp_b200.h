@@ -96,6 +96,16 @@ int cdp_trainer_history(cdp_trainer *tr, int max, double *losses, uint32_t *flag
 int cdp_trainer_stats(cdp_trainer *tr, int64_t *out, int n_out);
 /* The partial-sum buffer (gradient of the last step in gradient-only plans). */
 int cdp_trainer_get_grad(cdp_trainer *tr, float *grad);
+/* Mean loss and flags of the most recent step (synchronises the trainer stream). */
+int cdp_trainer_last(cdp_trainer *tr, double *loss, uint32_t *flags);
+/* Measurement helpers (bench.py): launch op `op`'s sub-kernels selected by
+ * mask (1 gather/loss, 2 fwd/dgrad GEMM, 4 wgrad+hop GEMM) `iters` times
+ * outside the graph and return the mean ms per iteration (destructive to the
+ * trainer state); timing events on the trainer stream; L2 flush (256 MiB). */
+int cdp_trainer_time_op(cdp_trainer *tr, int op, int mask, int iters, float *ms);
+int cdp_trainer_mark(cdp_trainer *tr, int k);
+int cdp_trainer_elapsed(cdp_trainer *tr, int a, int b, float *ms);
+int cdp_trainer_flush_l2(cdp_trainer *tr);
 /* The cudaStream_t the step graphs are launched on. */
 int cdp_trainer_stream(cdp_trainer *tr, void **stream);
 

@@ -43,6 +43,11 @@ SIGNATURES = {
     "cdp_trainer_history": (c_int, [c_void_p, c_int, c_double_p, ctypes.POINTER(ctypes.c_uint32), c_int_p]),
     "cdp_trainer_stats": (c_int, [c_void_p, c_int64_p, c_int]),
     "cdp_trainer_get_grad": (c_int, [c_void_p, c_float_p]),
+    "cdp_trainer_last": (c_int, [c_void_p, c_double_p, ctypes.POINTER(ctypes.c_uint32)]),
+    "cdp_trainer_time_op": (c_int, [c_void_p, c_int, c_int, c_int, c_float_p]),
+    "cdp_trainer_mark": (c_int, [c_void_p, c_int]),
+    "cdp_trainer_elapsed": (c_int, [c_void_p, c_int, c_int, c_float_p]),
+    "cdp_trainer_flush_l2": (c_int, [c_void_p]),
     "cdp_trainer_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_test_gemm": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p), c_int,
                               ctypes.POINTER(c_void_p), c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),

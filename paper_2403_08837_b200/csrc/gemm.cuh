@@ -149,8 +149,9 @@ __global__ void __launch_bounds__(256, 1)
             }
             ptx::umma_commit(tmem_full);
         }
-    } else if (warp >= 4) {
-        const int q = warp - 4;          // TMEM lane quarter of this warp
+    } else if (warp >= 4 && !Epi::kTile) {
+        // ---- per-row epilogue: thread t of warps 4-7 owns accumulator row t
+        const int q = warp - 4;  // TMEM lane quarter of this warp
         const int row = q * 32 + ptx::lane_id();
         const int m = m0 + row;
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(256, 1)
                 Epi::apply(ep, m, n0 + c, v, args.M, args.N, st);
             }
             Epi::finish(ep, m, args.M, st);
-            if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x - 128);
+            if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x - 128, 128);
         } else {
             const int tile = blockIdx.y * gridDim.x + blockIdx.x;
             float *mine = args.ws + ((size_t(tile) * gridDim.z + split) * 128 + row) * BN;
@@ -214,9 +215,37 @@ __global__ void __launch_bounds__(256, 1)
                     Epi::apply(ep, m, n0 + c, v, args.M, args.N, st);
                 }
                 Epi::finish(ep, m, args.M, st);
-                if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x - 128);
+                if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x - 128, 128);
             }
         }
+    }
+    if constexpr (Epi::kTile) {
+        // ---- tile epilogue: TMEM -> shared (the drained operand ring), then all
+        // 256 threads apply the epilogue with coalesced 128-bit global accesses
+        constexpr int LDS = BN + 4;
+        float *stile = reinterpret_cast<float *>(smem);
+        if (warp >= 4) {
+            const int q = warp - 4;
+            const int row = q * 32 + ptx::lane_id();
+            const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
+            ptx::mbar_wait(tmem_full, 0);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                float v[32];
+                ptx::tmem_ld32(taddr + c, v);
+                if (n_iters == 0) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                }
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<float4 *>(stile + row * LDS + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+        }
+        __syncthreads();
+        Epi::template tile<BN>(ep, stile, LDS, m0, n0, args.M, args.N, threadIdx.x, blockDim.x);
+        if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x, blockDim.x);
     }
     ptx::tc_fence_before();
     __syncthreads();

@@ -13,7 +13,10 @@ struct EpiStore {
         float *d;
         int ldd;
     };
+    static constexpr bool kTile = false;
     struct State {};
+    template <int BN>
+    __device__ static void tile(const Params &, const float *, int, int, int, int, int, int, int) {}
     __device__ static void begin(const Params &, int, State &) {}
     __device__ static void finish(const Params &, int, int, State &) {}
     __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &) {
@@ -22,7 +25,7 @@ struct EpiStore {
         for (int i = 0; i < 32; ++i)
             if (n0 + i < N) p.d[size_t(m) * p.ldd + n0 + i] = v[i];
     }
-    __device__ static void extra(const Params &, int) {}
+    __device__ static void extra(const Params &, int, int) {}
 };
 
 template <int KIND, int BN, bool A_MN, bool B_MN>

@@ -73,7 +73,10 @@ struct EpiFwd {
         }
     }
     __device__ static void finish(const Params &, int, int, State &) {}
-    __device__ static void extra(const Params &, int) {}
+    __device__ static void extra(const Params &, int, int) {}
+    static constexpr bool kTile = false;
+    template <int BN>
+    __device__ static void tile(const Params &, const float *, int, int, int, int, int, int, int) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -107,7 +110,10 @@ struct EpiDgrad {
     __device__ static void finish(const Params &p, int m, int M, State &st) {
         if (m < M) p.db[m] = st.acc;
     }
-    __device__ static void extra(const Params &, int) {}
+    __device__ static void extra(const Params &, int, int) {}
+    static constexpr bool kTile = false;
+    template <int BN>
+    __device__ static void tile(const Params &, const float *, int, int, int, int, int, int, int) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -143,6 +149,38 @@ struct HopParams {
 };
 
 template <int KIND>
+__device__ __forceinline__ void store_wc4(const CTensor &t, size_t i, float4 v) {
+    if constexpr (KIND == 0) {
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t *>(&a);
+        u.y = *reinterpret_cast<uint32_t *>(&b);
+        *reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(t.hi) + i) = u;
+    } else {
+        float4 h;
+        h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+        h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+        h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+        h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+        *reinterpret_cast<float4 *>(static_cast<float *>(t.hi) + i) = h;
+        *reinterpret_cast<float4 *>(static_cast<float *>(t.lo) + i) =
+            make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y), __fsub_rn(v.z, h.z), __fsub_rn(v.w, h.w));
+    }
+}
+
+// The update arithmetic of one element (mirrors ref engine.py:102-109 in fp32).
+__device__ __forceinline__ float sgd_update(const HopParams &p, float G, float th, float &v, float lr) {
+    if (p.momentum != 0.f) {
+        float gg = __fdiv_rn(G, p.n_mb);
+        if (p.wd != 0.f) gg = __fadd_rn(gg, __fmul_rn(p.wd, th));
+        v = __fadd_rn(__fmul_rn(v, p.momentum), gg);
+        return __fsub_rn(th, __fmul_rn(lr, v));
+    }
+    if (p.wd != 0.f) return __fsub_rn(th, __fmul_rn(lr, __fadd_rn(__fdiv_rn(G, p.n_mb), __fmul_rn(p.wd, th))));
+    return __fsub_rn(th, __fmul_rn(__fdiv_rn(lr, p.n_mb), G));
+}
+
+template <int KIND>
 __device__ __forceinline__ void hop_elem(const HopParams &p, int64_t idx, float g, size_t widx, bool is_w,
                                          bool &bad_g, bool &bad_u) {
     if (!isfinite(g)) bad_g = true;
@@ -155,51 +193,109 @@ __device__ __forceinline__ void hop_elem(const HopParams &p, int64_t idx, float 
         return;
     }
     const float G = p.mode == 2 ? __fadd_rn(__ldcg(p.s_in + idx), g) : g;
-    const float th = p.theta_cur[idx];
-    const float lr = *p.lr;
-    float nt;
-    if (p.momentum != 0.f) {
-        float gg = __fdiv_rn(G, p.n_mb);
-        if (p.wd != 0.f) gg = __fadd_rn(gg, __fmul_rn(p.wd, th));
-        const float v = __fadd_rn(__fmul_rn(p.vel[idx], p.momentum), gg);
-        p.vel[idx] = v;
-        nt = __fsub_rn(th, __fmul_rn(lr, v));
-    } else if (p.wd != 0.f) {
-        nt = __fsub_rn(th, __fmul_rn(lr, __fadd_rn(__fdiv_rn(G, p.n_mb), __fmul_rn(p.wd, th))));
-    } else {
-        nt = __fsub_rn(th, __fmul_rn(__fdiv_rn(lr, p.n_mb), G));
-    }
+    float v = p.momentum != 0.f ? p.vel[idx] : 0.f;
+    const float nt = sgd_update(p, G, p.theta_cur[idx], v, *p.lr);
+    if (p.momentum != 0.f) p.vel[idx] = v;
     if (!isfinite(nt)) bad_u = true;
     p.theta_new[idx] = nt;
     if (is_w) Fmt<KIND>::store(p.wc_new.hi, p.wc_new.lo, widx, nt);
 }
 
+__device__ __forceinline__ bool finite4(float4 a) {
+    return isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w);
+}
+
 template <int KIND>
 struct EpiWgrad {
     using Params = HopParams;
-    struct State {
-        bool bad_g, bad_u;
-    };
-    __device__ static void begin(const Params &, int, State &st) { st.bad_g = st.bad_u = false; }
-    __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &st) {
-        if (m >= M) return;
-        const int64_t row = p.base + int64_t(m) * p.dout;
-#pragma unroll 4
-        for (int i = 0; i < 32; ++i) {
-            const int o = n0 + i;
-            if (o >= N) break;
-            hop_elem<KIND>(p, row + o, v[i], size_t(m) * p.wc_new.ld + o, true, st.bad_g, st.bad_u);
+    static constexpr bool kTile = true;
+    struct State {};
+    __device__ static void begin(const Params &, int, State &) {}
+    __device__ static void apply(const Params &, int, int, const float (&)[32], int, int, State &) {}
+    __device__ static void finish(const Params &, int, int, State &) {}
+
+    // The 128 x BN tile of dW sits in shared memory (row-major, stride lds).
+    // Threads sweep it in float4 slots so consecutive threads touch consecutive
+    // 16-byte chunks of a parameter row; U slots per thread are loaded before
+    // any is consumed (memory-level parallelism for the peer / HBM reads).
+    template <int BN>
+    __device__ static void tile(const Params &p, const float *st, int lds, int m0, int n0, int M, int N, int tid,
+                                int nth) {
+        bool bad_g = false, bad_u = false;
+        const bool vec = (p.dout % 4 == 0) && (p.base % 4 == 0);
+        if (vec) {
+            constexpr int C4 = BN / 4;
+            constexpr int U = 4;
+            const float lr = *p.lr;
+            const int total = 128 * C4;
+            for (int e0 = tid; e0 < total; e0 += nth * U) {
+                float4 g[U], s[U], th[U], vv[U];
+                int64_t idx[U];
+                size_t widx[U];
+                bool ok[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * nth;
+                    const int r = e / C4, c = (e % C4) * 4;
+                    const int m = m0 + r, n = n0 + c;
+                    ok[u] = e < total && m < M && n < N;
+                    if (!ok[u]) continue;
+                    idx[u] = p.base + int64_t(m) * p.dout + n;
+                    widx[u] = size_t(m) * p.wc_new.ld + n;
+                    g[u] = *reinterpret_cast<const float4 *>(st + r * lds + c);
+                    if (p.mode == 1 || p.mode == 2) s[u] = __ldcg(reinterpret_cast<const float4 *>(p.s_in + idx[u]));
+                    if (p.mode == 2 || p.mode == 3) {
+                        th[u] = *reinterpret_cast<const float4 *>(p.theta_cur + idx[u]);
+                        if (p.momentum != 0.f) vv[u] = *reinterpret_cast<const float4 *>(p.vel + idx[u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (!ok[u]) continue;
+                    if (!finite4(g[u])) bad_g = true;
+                    float4 *so = reinterpret_cast<float4 *>(p.s_out + idx[u]);
+                    if (p.mode == 0 || p.mode == 4) {
+                        *so = g[u];
+                        continue;
+                    }
+                    float4 G = g[u];
+                    if (p.mode == 1 || p.mode == 2)
+                        G = make_float4(__fadd_rn(s[u].x, g[u].x), __fadd_rn(s[u].y, g[u].y),
+                                        __fadd_rn(s[u].z, g[u].z), __fadd_rn(s[u].w, g[u].w));
+                    if (p.mode == 1) {
+                        *so = G;
+                        continue;
+                    }
+                    float4 v = p.momentum != 0.f ? vv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    float4 nt;
+                    nt.x = sgd_update(p, G.x, th[u].x, v.x, lr);
+                    nt.y = sgd_update(p, G.y, th[u].y, v.y, lr);
+                    nt.z = sgd_update(p, G.z, th[u].z, v.z, lr);
+                    nt.w = sgd_update(p, G.w, th[u].w, v.w, lr);
+                    if (p.momentum != 0.f) *reinterpret_cast<float4 *>(p.vel + idx[u]) = v;
+                    if (!finite4(nt)) bad_u = true;
+                    *reinterpret_cast<float4 *>(p.theta_new + idx[u]) = nt;
+                    store_wc4<KIND>(p.wc_new, widx[u], nt);
+                }
+            }
+        } else {
+            for (int e = tid; e < 128 * BN; e += nth) {
+                const int r = e / BN, c = e % BN;
+                const int m = m0 + r, n = n0 + c;
+                if (m >= M || n >= N) continue;
+                hop_elem<KIND>(p, p.base + int64_t(m) * p.dout + n, st[r * lds + c], size_t(m) * p.wc_new.ld + n,
+                               true, bad_g, bad_u);
+            }
         }
+        if (bad_g) atomicOr(p.grad_flags, 1u << (p.stage - 1));
+        if (bad_u) atomicOr(p.upd_flags, 1u << (p.stage - 1));
     }
-    __device__ static void finish(const Params &p, int, int, State &st) {
-        if (st.bad_g) atomicOr(p.grad_flags, 1u << (p.stage - 1));
-        if (st.bad_u) atomicOr(p.upd_flags, 1u << (p.stage - 1));
-    }
-    // bias part of the stage: CTA (0,0) epilogue threads
-    __device__ static void extra(const Params &p, int tid) {
+
+    // bias part of the stage, by CTA (0,0)
+    __device__ static void extra(const Params &p, int tid, int nth) {
         bool bg = false, bu = false;
         const int64_t b0 = p.base + int64_t(p.din) * p.dout;
-        for (int o = tid; o < p.dout; o += 128) hop_elem<KIND>(p, b0 + o, p.db[o], 0, false, bg, bu);
+        for (int o = tid; o < p.dout; o += nth) hop_elem<KIND>(p, b0 + o, p.db[o], 0, false, bg, bu);
         if (bg) atomicOr(p.grad_flags, 1u << (p.stage - 1));
         if (bu) atomicOr(p.upd_flags, 1u << (p.stage - 1));
     }

@@ -139,6 +139,9 @@ struct MlpTrainer {
     cudaGraphExec_t exec[2] = {nullptr, nullptr};
     int t = 1;  // training step of the next launch; current version = t
     int kernels_per_step = 0;
+    int launch_mask = 7;  // bit0 gather/loss, bit1 fwd/dgrad GEMM, bit2 wgrad(+hop) GEMM
+    std::vector<cudaEvent_t> marks;
+    DevBuf flush_buf;
 
     ~MlpTrainer() {
         for (auto &e : exec)
@@ -151,6 +154,7 @@ struct MlpTrainer {
         if (main) cudaStreamDestroy(main);
         for (auto e : stage_ev)
             if (e) cudaEventDestroy(e);
+        for (auto e : marks) cudaEventDestroy(e);
         if (stage_host) cudaFreeHost(stage_host);
     }
 
@@ -161,13 +165,14 @@ struct MlpTrainer {
         int target = n >= 1024 ? 256 : n >= 256 ? 64 : n;
         return std::min(256, round_up(std::max(target, ch), ch));
     }
-    int splits_for(int M, int N, int BN, int K) const {
+    int splits_for(int M, int N, int BN, int K, bool allow_split = true) const {
+        if (!allow_split) return 1;
         const int bk = kind == 0 ? 64 : 32;
         const int nseg = kind == 0 ? 1 : 3;
         const int kb = (K + bk - 1) / bk;
         const int total = kb * nseg;
         const int tiles = ((M + 127) / 128) * ((N + BN - 1) / BN);
-        int s = std::max(1, std::min(total, 48 / std::max(tiles, 1)));
+        int s = std::max(1, std::min(total, 16 / std::max(tiles, 1)));
         if (kind == 1) s = std::max(s, (total + 7) / 8);  // <= 256 of K per TMEM accumulation
         s = std::min(s, total);
         const int per = (total + s - 1) / s;
@@ -207,7 +212,6 @@ struct MlpTrainer {
         for (int j = 0; j < S; ++j) {
             ws_floats = std::max(ws_floats, ws_need(st[j].dout, B, bn_rows(B), st[j].din));
             ws_floats = std::max(ws_floats, ws_need(st[j].din, B, bn_rows(B), st[j].dout));
-            ws_floats = std::max(ws_floats, ws_need(st[j].din, st[j].dout, bn_mn(st[j].dout), B));
         }
         wk.resize(W);
         loss_all = DevBuf(size_t(W) * 8);
@@ -270,7 +274,7 @@ struct MlpTrainer {
     template <int K, bool AMN, bool BMN, class Epi>
     void gemm(int BN, const Operand *A, const Operand *Bo, int nseg, int M, int N, int Kd, Worker &w,
               const typename Epi::Params &ep, cudaStream_t s) {
-        const int splits = splits_for(M, N, BN, Kd);
+        const int splits = splits_for(M, N, BN, Kd, !Epi::kTile);
         GemmPlan p;
 #define CDP_GEMM_BN(BN_)                                                                                            \
     case BN_:                                                                                                       \
@@ -299,7 +303,7 @@ struct MlpTrainer {
     void forward(int w, int j, int vslot, int rin, int rout, cudaStream_t s, const int *perm_w) {
         const StageGeom &g = st[j];
         Worker &wr = wk[w];
-        if (j == 0) {
+        if (j == 0 && (launch_mask & 1)) {
             gather_kernel<K><<<B, 256, 0, s>>>(data_x.as<float>(), g.din, perm_w, rec[0][rin].view());
             CDP_CUDA(cudaGetLastError());
             ++kernels_per_step;
@@ -313,7 +317,7 @@ struct MlpTrainer {
             ep.z = wr.z.as<float>();
         else
             ep.out = rec[j + 1][rout].view();
-        gemm<K, true, false, EpiFwd<K>>(bn_rows(B), A, Bo, nseg, g.dout, B, g.din, wr, ep, s);
+        if (launch_mask & 2) gemm<K, true, false, EpiFwd<K>>(bn_rows(B), A, Bo, nseg, g.dout, B, g.din, wr, ep, s);
     }
 
     template <int K>
@@ -323,7 +327,7 @@ struct MlpTrainer {
         Flags *fl = flags_dev.as<Flags>();
         const int cur = (S - 1 - j) & 1;
         float *db = wr.db.as<float>();
-        if (j == S - 1) {
+        if (j == S - 1 && (launch_mask & 1)) {
             loss_kernel<K><<<1, std::max(32, round_up(B, 32)), sizeof(double) * std::max(32, round_up(B, 32)), s>>>(
                 wr.z.as<float>(), B, g.dout, loss_kind, perm_w, data_lab.as<int>(), data_tgt.as<float>(),
                 wr.dz[cur].view(), db + size_t(j) * dmax, wr.loss, &fl->loss);
@@ -331,7 +335,7 @@ struct MlpTrainer {
             ++kernels_per_step;
         }
         Operand A[3], Bo[3];
-        if (j > 0) {  // data gradient into dZ_{j-1} (+ bias grad of stage j-1)
+        if (j > 0 && (launch_mask & 2)) {  // data gradient into dZ_{j-1} (+ bias grad of stage j-1)
             const int nseg = segments<K>(wc[vslot][j], false, g.din, g.dout, wr.dz[cur], false, B, g.dout, A, Bo);
             typename EpiDgrad<K>::Params ep{rec[j][rin].view(), wr.dz[cur ^ 1].view(), db + size_t(j - 1) * dmax};
             gemm<K, false, false, EpiDgrad<K>>(bn_rows(B), A, Bo, nseg, g.din, B, g.dout, wr, ep, s);
@@ -357,7 +361,7 @@ struct MlpTrainer {
         hp.db = db + size_t(j) * dmax;
         hp.grad_flags = &fl->grad;
         hp.upd_flags = &fl->upd;
-        gemm<K, true, true, EpiWgrad<K>>(bn_mn(g.dout), A, Bo, nseg, g.din, g.dout, B, wr, hp, s);
+        if (launch_mask & 4) gemm<K, true, true, EpiWgrad<K>>(bn_mn(g.dout), A, Bo, nseg, g.din, g.dout, B, wr, hp, s);
     }
 
     // ---------------------------------------------------------------- capture
@@ -405,7 +409,13 @@ struct MlpTrainer {
                 else
                     record_step<1>(p);
             } catch (...) {
-                cudaStreamEndCapture(main, &g);
+                // join the forked worker streams so the capture can be closed cleanly
+                for (int w = 0; w < W; ++w) {
+                    cudaEventRecord(join_ev[w], wk[w].stream);
+                    cudaStreamWaitEvent(main, join_ev[w], 0);
+                }
+                if (cudaStreamEndCapture(main, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+                cudaGetLastError();
                 throw;
             }
             CDP_CUDA(cudaStreamEndCapture(main, &g));
@@ -469,6 +479,59 @@ struct MlpTrainer {
         CDP_CUDA(cudaEventRecord(stage_ev[k], main));
         CDP_CUDA(cudaGraphLaunch(exec[t & 1], main));
         ++t;
+    }
+
+    // Launch one plan op's sub-kernels (mask) `iters` times, outside any graph, on
+    // the main stream; returns the mean duration per iteration (CUDA events).
+    // Destructive for the trainer state (re-applies hops / updates): bench only.
+    float time_op(int o, int mask, int iters) {
+        CDP_REQUIRE(o >= 0 && o < int(ops.size()), "op index out of range");
+        const auto &op = ops[o];
+        const int w = op[OP_WORKER] - 1, j = op[OP_STAGE] - 1;
+        const int p = t & 1, vslot = op[OP_FRESH] ? p : (p ^ 1);
+        const int *perm_w = perm_dev.as<int>() + size_t(w) * B;
+        cudaEvent_t e0, e1;
+        CDP_CUDA(cudaEventCreate(&e0));
+        CDP_CUDA(cudaEventCreate(&e1));
+        launch_mask = mask;
+        auto run = [&] {
+            if (op[OP_KIND] == 0) {
+                if (kind == 0) forward<0>(w, j, vslot, op[OP_REC_IN], op[OP_REC_OUT], main, perm_w);
+                else forward<1>(w, j, vslot, op[OP_REC_IN], op[OP_REC_OUT], main, perm_w);
+            } else {
+                if (kind == 0) backward<0>(w, j, vslot, op[OP_REC_IN], op[OP_HOP], p, main, perm_w);
+                else backward<1>(w, j, vslot, op[OP_REC_IN], op[OP_HOP], p, main, perm_w);
+            }
+        };
+        const int saved = kernels_per_step;
+        const bool warm = iters > 0;  // iters < 0: cold (no warm-up launch), |iters| launches
+        iters = iters > 0 ? iters : -iters;
+        if (warm) run();
+        CDP_CUDA(cudaEventRecord(e0, main));
+        for (int i = 0; i < iters; ++i) run();
+        CDP_CUDA(cudaEventRecord(e1, main));
+        CDP_CUDA(cudaEventSynchronize(e1));
+        launch_mask = 7;
+        kernels_per_step = saved;
+        float ms = 0.f;
+        CDP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return ms / iters;
+    }
+
+    void mark(int k) {
+        while (int(marks.size()) <= k) {
+            cudaEvent_t e;
+            CDP_CUDA(cudaEventCreate(&e));
+            marks.push_back(e);
+        }
+        CDP_CUDA(cudaEventRecord(marks[k], main));
+    }
+
+    void flush_l2() {
+        if (!flush_buf.p) flush_buf = DevBuf(size_t(256) << 20);
+        CDP_CUDA(cudaMemsetAsync(flush_buf.p, t & 0xff, flush_buf.bytes, main));
     }
 
     // Host-batch step (end-to-end path): the step's inputs come from host memory.
@@ -710,4 +773,41 @@ extern "C" int cdp_mlp_value_grad(int n_dims, const int64_t *dims, const double 
         CDP_CUDA(cudaMemcpy(g.data(), tr.partial.p, size_t(tr.P) * 4, cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < tr.P; ++i) grad_out[i] = double(g[i]);
     });
+}
+
+extern "C" int cdp_trainer_last(cdp_trainer *tr, double *loss, uint32_t *flags) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        const int c = m.t - 1;  // steps launched (and now finished)
+        CDP_REQUIRE(c >= 1, "no step has run");
+        const int k = (c - 1) % m.hist_cap;
+        Flags f;
+        CDP_CUDA(cudaMemcpy(loss, m.hist_loss.as<double>() + k, 8, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemcpy(&f, m.hist_flags.as<Flags>() + k, sizeof(Flags), cudaMemcpyDeviceToHost));
+        flags[0] = f.grad;
+        flags[1] = f.loss;
+        flags[2] = f.upd;
+    });
+}
+
+extern "C" int cdp_trainer_time_op(cdp_trainer *tr, int op, int mask, int iters, float *ms) {
+    return guarded([&] { *ms = tr->impl->time_op(op, mask, iters); });
+}
+
+extern "C" int cdp_trainer_mark(cdp_trainer *tr, int k) {
+    return guarded([&] { tr->impl->mark(k); });
+}
+
+extern "C" int cdp_trainer_elapsed(cdp_trainer *tr, int a, int b, float *ms) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_REQUIRE(a >= 0 && b >= 0 && a < int(m.marks.size()) && b < int(m.marks.size()), "mark out of range");
+        CDP_CUDA(cudaEventSynchronize(m.marks[b]));
+        CDP_CUDA(cudaEventElapsedTime(ms, m.marks[a], m.marks[b]));
+    });
+}
+
+extern "C" int cdp_trainer_flush_l2(cdp_trainer *tr) {
+    return guarded([&] { tr->impl->flush_l2(); });
 }

@@ -133,6 +133,45 @@ class DeviceMlpTrainer:
         n = min(cnt.value, max_steps)
         return losses[:n].copy(), flags[:n].copy()
 
+    def last(self):
+        """(mean loss, flags[3]) of the most recent step; synchronises."""
+        loss = ctypes.c_double()
+        flags = (ctypes.c_uint32 * 3)()
+        N.check(self.lib.cdp_trainer_last(self.h, ctypes.byref(loss), flags))
+        return loss.value, tuple(flags)
+
+    def step_host_batch_ptr(self, x_ptr: int, y_ptr: int, lr: float):
+        """Host-batch step from raw (pinned) host pointers: x fp32, y int32 labels or fp32 targets."""
+        if self.loss_kind == 1:
+            N.check(self.lib.cdp_trainer_step_host_batch(self.h, ctypes.cast(x_ptr, N.c_float_p),
+                                                         ctypes.cast(y_ptr, ctypes.POINTER(ctypes.c_int32)), None,
+                                                         float(lr)))
+        else:
+            N.check(self.lib.cdp_trainer_step_host_batch(self.h, ctypes.cast(x_ptr, N.c_float_p), None,
+                                                         ctypes.cast(y_ptr, N.c_float_p), float(lr)))
+
+    def time_op(self, op: int, mask: int, iters: int) -> float:
+        ms = ctypes.c_float()
+        N.check(self.lib.cdp_trainer_time_op(self.h, op, mask, iters, ctypes.byref(ms)))
+        return ms.value
+
+    def mark(self, k: int):
+        N.check(self.lib.cdp_trainer_mark(self.h, k))
+
+    def elapsed(self, a: int, b: int) -> float:
+        ms = ctypes.c_float()
+        N.check(self.lib.cdp_trainer_elapsed(self.h, a, b, ctypes.byref(ms)))
+        return ms.value
+
+    def flush_l2(self):
+        N.check(self.lib.cdp_trainer_flush_l2(self.h))
+
+    def op_index(self, kind: int, worker: int, stage: int) -> int:
+        for o, row in enumerate(self.plan.ops):
+            if row[0] == kind and row[1] == worker and row[2] == stage:
+                return o
+        raise KeyError((kind, worker, stage))
+
     def stats(self) -> dict:
         out = np.zeros(6, dtype=np.int64)
         N.check(self.lib.cdp_trainer_stats(self.h, out.ctypes.data_as(N.c_int64_p), 6))
