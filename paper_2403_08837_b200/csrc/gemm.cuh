@@ -118,6 +118,10 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: the prologue above overlapped the previous kernel; global memory is
+    // touched only after the predecessor's results are visible.
+    ptx::griddep_wait();
+    ptx::griddep_launch();
 
     if (warp == 0) {
         if (ptx::lane_id() == 0) {
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(256, 1)
                     float v[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = 0.f;
+#pragma unroll 4
                     for (int z = 0; z < int(gridDim.z); ++z) {
                         const float *p = base + size_t(z) * 128 * BN + c;
 #pragma unroll

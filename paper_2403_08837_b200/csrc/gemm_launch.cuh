@@ -70,8 +70,7 @@ void launch_gemm(const GemmPlan &p, const typename Epi::Params &ep, cudaStream_t
         CDP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_set = true;
     }
-    kern<<<p.grid, 256, C::SMEM, st>>>(p.maps, p.args, ep);
-    CDP_CUDA(cudaGetLastError());
+    launch_pdl(kern, p.grid, dim3(256), C::SMEM, st, p.maps, p.args, ep);
 }
 
 // Workspace bytes needed by a split-K plan.

@@ -45,6 +45,14 @@ CUtensorMap make_tmap_2d(const void *base, ElemType t, uint64_t inner, uint64_t 
     return m;
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("CDP_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int num_sms() {
     int dev = 0, n = 0;
     CDP_CUDA(cudaGetDevice(&dev));

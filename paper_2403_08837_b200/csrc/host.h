@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -55,5 +57,26 @@ CUtensorMap make_tmap_2d(const void *base, ElemType t, uint64_t inner, uint64_t 
                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B);
 
 int num_sms();
+
+// Programmatic dependent launch (PDL) toggle: CDP_PDL=0 disables it.
+bool pdl_enabled();
+
+// Launch `kern` with the programmatic-stream-serialization attribute so its
+// prologue overlaps the tail of the previous kernel on the stream (the kernel
+// must call griddepcontrol.wait before touching dependent global memory).
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CDP_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 }  // namespace cdp

@@ -96,15 +96,18 @@ struct EpiDgrad {
     __device__ static void begin(const Params &, int, State &st) { st.acc = 0.f; }
     __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &st) {
         if (m >= M) return;
-#pragma unroll 4
+        float h[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)  // all 32 loads in flight before any use
+            h[i] = (n0 + i < N) ? Fmt<KIND>::load(p.h.hi, p.h.lo, size_t(n0 + i) * p.h.ld + m) : 0.f;
+#pragma unroll
         for (int i = 0; i < 32; ++i) {
             const int s = n0 + i;
-            if (s >= N) break;
-            const size_t hi = size_t(s) * p.h.ld + m;
-            const float h = Fmt<KIND>::load(p.h.hi, p.h.lo, hi);
-            const float d = __fmul_rn(v[i], __fsub_rn(1.f, __fmul_rn(h, h)));
-            Fmt<KIND>::store(p.dprev.hi, p.dprev.lo, size_t(s) * p.dprev.ld + m, d);
-            st.acc = __fadd_rn(st.acc, d);
+            if (s < N) {
+                const float d = __fmul_rn(v[i], __fsub_rn(1.f, __fmul_rn(h[i], h[i])));
+                Fmt<KIND>::store(p.dprev.hi, p.dprev.lo, size_t(s) * p.dprev.ld + m, d);
+                st.acc = __fadd_rn(st.acc, d);
+            }
         }
     }
     __device__ static void finish(const Params &p, int m, int M, State &st) {
@@ -279,12 +282,52 @@ struct EpiWgrad {
                 }
             }
         } else {
-            for (int e = tid; e < 128 * BN; e += nth) {
-                const int r = e / BN, c = e % BN;
-                const int m = m0 + r, n = n0 + c;
-                if (m >= M || n >= N) continue;
-                hop_elem<KIND>(p, p.base + int64_t(m) * p.dout + n, st[r * lds + c], size_t(m) * p.wc_new.ld + n,
-                               true, bad_g, bad_u);
+            // unaligned rows (e.g. dout = 10): scalar, but only valid elements and
+            // with U independent loads in flight per thread
+            const int rows = min(128, M - m0), cols = min(BN, N - n0);
+            const int total = rows * cols;
+            constexpr int U = 8;
+            const float lr = *p.lr;
+            for (int e0 = tid; e0 < total; e0 += nth * U) {
+                float g[U], sv[U], th[U], vv[U];
+                int64_t idx[U];
+                size_t widx[U];
+                bool ok[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * nth;
+                    ok[u] = e < total;
+                    if (!ok[u]) continue;
+                    const int r = e / cols, c = e % cols;
+                    idx[u] = p.base + int64_t(m0 + r) * p.dout + n0 + c;
+                    widx[u] = size_t(m0 + r) * p.wc_new.ld + n0 + c;
+                    g[u] = st[r * lds + c];
+                    if (p.mode == 1 || p.mode == 2) sv[u] = __ldcg(p.s_in + idx[u]);
+                    if (p.mode == 2 || p.mode == 3) {
+                        th[u] = p.theta_cur[idx[u]];
+                        if (p.momentum != 0.f) vv[u] = p.vel[idx[u]];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (!ok[u]) continue;
+                    if (!isfinite(g[u])) bad_g = true;
+                    if (p.mode == 0 || p.mode == 4) {
+                        p.s_out[idx[u]] = g[u];
+                        continue;
+                    }
+                    const float G = (p.mode == 1 || p.mode == 2) ? __fadd_rn(sv[u], g[u]) : g[u];
+                    if (p.mode == 1) {
+                        p.s_out[idx[u]] = G;
+                        continue;
+                    }
+                    float v = p.momentum != 0.f ? vv[u] : 0.f;
+                    const float nt = sgd_update(p, G, th[u], v, lr);
+                    if (p.momentum != 0.f) p.vel[idx[u]] = v;
+                    if (!isfinite(nt)) bad_u = true;
+                    p.theta_new[idx[u]] = nt;
+                    Fmt<KIND>::store(p.wc_new.hi, p.wc_new.lo, widx[u], nt);
+                }
             }
         }
         if (bad_g) atomicOr(p.grad_flags, 1u << (p.stage - 1));
@@ -308,7 +351,11 @@ template <int KIND>
 __global__ void loss_kernel(const float *__restrict__ z, int B, int dout, int loss_kind, const int *perm,
                             const int *labels, const float *targets, CTensor dz, float *db, double *loss_out,
                             unsigned *loss_flag) {
+    // shared: per-sample loss [blockDim] doubles, then dz [B][dout] floats
     extern __shared__ double sh_loss[];
+    float *sdz = reinterpret_cast<float *>(sh_loss + blockDim.x);
+    ptx::griddep_wait();
+    ptx::griddep_launch();
     const int s = threadIdx.x;
     double l = 0.0;
     if (s < B) {
@@ -319,7 +366,7 @@ __global__ void loss_kernel(const float *__restrict__ z, int B, int dout, int lo
             for (int o = 0; o < dout; ++o) {
                 const float d = __fsub_rn(zr[o], tr[o]);
                 l += double(d) * double(d);
-                Fmt<KIND>::store(dz.hi, dz.lo, size_t(s) * dz.ld + o, __fdiv_rn(d, float(B)));
+                sdz[s * dout + o] = __fdiv_rn(d, float(B));
             }
         } else {
             const int lab = labels[row];
@@ -330,10 +377,10 @@ __global__ void loss_kernel(const float *__restrict__ z, int B, int dout, int lo
             for (int o = 0; o < dout; ++o) {
                 const float pz = __fdiv_rn(expf(__fsub_rn(zr[o], mx)), se);
                 if (o == lab) l = -log(double(pz));
-                Fmt<KIND>::store(dz.hi, dz.lo, size_t(s) * dz.ld + o,
-                                 __fdiv_rn(__fsub_rn(pz, o == lab ? 1.f : 0.f), float(B)));
+                sdz[s * dout + o] = __fdiv_rn(__fsub_rn(pz, o == lab ? 1.f : 0.f), float(B));
             }
         }
+        for (int o = 0; o < dout; ++o) Fmt<KIND>::store(dz.hi, dz.lo, size_t(s) * dz.ld + o, sdz[s * dout + o]);
     }
     sh_loss[s] = l;
     __syncthreads();
@@ -344,10 +391,10 @@ __global__ void loss_kernel(const float *__restrict__ z, int B, int dout, int lo
         *loss_out = acc;
         if (!isfinite(acc)) atomicOr(loss_flag, 1u);
     }
-    // bias gradient of the last stage, ascending s
+    // bias gradient of the last stage, ascending s (ref _kernels.pyx:115-119)
     for (int o = threadIdx.x; o < dout; o += blockDim.x) {
         float acc = 0.f;
-        for (int k = 0; k < B; ++k) acc = __fadd_rn(acc, Fmt<KIND>::load(dz.hi, dz.lo, size_t(k) * dz.ld + o));
+        for (int k = 0; k < B; ++k) acc = __fadd_rn(acc, sdz[k * dout + o]);
         db[o] = acc;
     }
 }
@@ -356,6 +403,8 @@ __global__ void loss_kernel(const float *__restrict__ z, int B, int dout, int lo
 // input record (compute format).
 template <int KIND>
 __global__ void gather_kernel(const float *__restrict__ data, int din, const int *perm, CTensor out) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
     const int s = blockIdx.x;
     const float *src = data + size_t(perm[s]) * din;
     for (int k = threadIdx.x; k < din; k += blockDim.x) Fmt<KIND>::store(out.hi, out.lo, size_t(s) * out.ld + k, src[k]);

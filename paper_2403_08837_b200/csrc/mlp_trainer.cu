@@ -304,8 +304,8 @@ struct MlpTrainer {
         const StageGeom &g = st[j];
         Worker &wr = wk[w];
         if (j == 0 && (launch_mask & 1)) {
-            gather_kernel<K><<<B, 256, 0, s>>>(data_x.as<float>(), g.din, perm_w, rec[0][rin].view());
-            CDP_CUDA(cudaGetLastError());
+            launch_pdl(gather_kernel<K>, dim3(B), dim3(256), 0, s, (const float *)data_x.as<float>(), g.din, perm_w,
+                       rec[0][rin].view());
             ++kernels_per_step;
         }
         Operand A[3], Bo[3];
@@ -328,10 +328,14 @@ struct MlpTrainer {
         const int cur = (S - 1 - j) & 1;
         float *db = wr.db.as<float>();
         if (j == S - 1 && (launch_mask & 1)) {
-            loss_kernel<K><<<1, std::max(32, round_up(B, 32)), sizeof(double) * std::max(32, round_up(B, 32)), s>>>(
-                wr.z.as<float>(), B, g.dout, loss_kind, perm_w, data_lab.as<int>(), data_tgt.as<float>(),
-                wr.dz[cur].view(), db + size_t(j) * dmax, wr.loss, &fl->loss);
-            CDP_CUDA(cudaGetLastError());
+            const int nt = std::max(32, round_up(B, 32));
+            const size_t lsm = sizeof(double) * nt + sizeof(float) * B * g.dout;
+            CDP_REQUIRE(lsm <= 220 * 1024, "loss kernel: batch x classes too large for shared memory");
+            if (lsm > 48 * 1024)
+                CDP_CUDA(cudaFuncSetAttribute(loss_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsm)));
+            launch_pdl(loss_kernel<K>, dim3(1), dim3(nt), lsm, s, (const float *)wr.z.as<float>(), B,
+                       g.dout, loss_kind, perm_w, (const int *)data_lab.as<int>(), (const float *)data_tgt.as<float>(),
+                       wr.dz[cur].view(), db + size_t(j) * dmax, wr.loss, &fl->loss);
             ++kernels_per_step;
         }
         Operand A[3], Bo[3];

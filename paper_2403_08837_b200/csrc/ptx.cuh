@@ -138,6 +138,12 @@ __host__ __device__ constexpr uint32_t instr_desc(uint32_t ab_format, bool a_mn,
            ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// wait: block until the preceding grid in the stream has completed and its
+// memory is visible; launch_dependents: let the next grid start its prologue.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- system-scope flags (P2P)
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
     uint32_t v;
