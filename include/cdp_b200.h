@@ -74,6 +74,29 @@ int cdp_trainer_create(int n_dims, const int64_t *dims, int micro_batch, int n_w
                        const int32_t *deps, const int32_t *slots_per_stage, int n_samples, const float *x,
                        const int32_t *labels, const float *targets, cdp_trainer **out);
 void cdp_trainer_destroy(cdp_trainer *tr);
+
+/* ---- multi-GPU CDP: one process (rank) per GPU, worker i = rank + 1 ------ */
+/* The rank's plan holds only its own worker's ops plus pull ops (kind 2:
+ * fetch the version of stage j this worker is about to read from the
+ * updater rank world-1).  The gradient hop of B(i,j) reads rank i-2's
+ * partial sum from peer HBM (ref comm.py:37-67), the last rank fuses the
+ * update.  Synchronisation is by step-numbered flags in each rank's shared
+ * region (st.release.sys / ld.acquire.sys); spin-waits time out (~2 s) into
+ * cdp_trainer_ring_error instead of hanging.  Sequence: create_rank ->
+ * (ipc_handle, exchange, ipc_open peers) -> connect(regions) -> steps. */
+int cdp_trainer_create_rank(int n_dims, const int64_t *dims, int micro_batch, int world, int rank, int loss_kind,
+                            int dtype, float momentum, float weight_decay, int n_ops, const int32_t *ops,
+                            int n_samples, const float *x, const int32_t *labels, const float *targets,
+                            cdp_trainer **out);
+/* Base / size of the rank's shared region (flags, both parameter slots, partial sum). */
+int cdp_trainer_region(cdp_trainer *tr, void **base, size_t *bytes);
+/* 64-byte cudaIpcMemHandle_t of the shared region. */
+int cdp_trainer_ipc_handle(cdp_trainer *tr, void *handle64);
+int cdp_ipc_open(const void *handle64, void **ptr);
+int cdp_ipc_close(void *ptr);
+/* regions[r] = rank r's region base, valid in this process; captures the step graphs. */
+int cdp_trainer_connect(cdp_trainer *tr, void *const *regions);
+int cdp_trainer_ring_error(cdp_trainer *tr, int *err);
 /* which: 0 = current version (theta_t), 1 = previous (theta_{t-1}), -1 = both.
  * Flat fp32 host buffers in the reference layout. */
 int cdp_trainer_set_params(cdp_trainer *tr, int which, const float *theta);

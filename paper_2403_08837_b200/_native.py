@@ -33,6 +33,15 @@ SIGNATURES = {
                                    ctypes.POINTER(ctypes.c_int32), c_int, c_float_p, ctypes.POINTER(ctypes.c_int32),
                                    c_float_p, ctypes.POINTER(c_void_p)]),
     "cdp_trainer_destroy": (None, [c_void_p]),
+    "cdp_trainer_create_rank": (c_int, [c_int, c_int64_p, c_int, c_int, c_int, c_int, c_int, c_float, c_float, c_int,
+                                        ctypes.POINTER(ctypes.c_int32), c_int, c_float_p,
+                                        ctypes.POINTER(ctypes.c_int32), c_float_p, ctypes.POINTER(c_void_p)]),
+    "cdp_trainer_region": (c_int, [c_void_p, ctypes.POINTER(c_void_p), ctypes.POINTER(c_size_t)]),
+    "cdp_trainer_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "cdp_ipc_open": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "cdp_ipc_close": (c_int, [c_void_p]),
+    "cdp_trainer_connect": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "cdp_trainer_ring_error": (c_int, [c_void_p, c_int_p]),
     "cdp_trainer_set_params": (c_int, [c_void_p, c_int, c_float_p]),
     "cdp_trainer_get_params": (c_int, [c_void_p, c_int, c_float_p]),
     "cdp_trainer_set_velocity": (c_int, [c_void_p, c_float_p]),

@@ -249,8 +249,10 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
         __syncthreads();
+        Epi::pre(ep, threadIdx.x);
         Epi::template tile<BN>(ep, stile, LDS, m0, n0, args.M, args.N, threadIdx.x, blockDim.x);
         if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x, blockDim.x);
+        Epi::post(ep, threadIdx.x, gridDim.x * gridDim.y);
     }
     ptx::tc_fence_before();
     __syncthreads();

@@ -26,6 +26,8 @@ struct EpiStore {
             if (n0 + i < N) p.d[size_t(m) * p.ldd + n0 + i] = v[i];
     }
     __device__ static void extra(const Params &, int, int) {}
+    __device__ static void pre(const Params &, int) {}
+    __device__ static void post(const Params &, int, unsigned) {}
 };
 
 template <int KIND, int BN, bool A_MN, bool B_MN>

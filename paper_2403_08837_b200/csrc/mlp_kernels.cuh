@@ -77,6 +77,8 @@ struct EpiFwd {
     static constexpr bool kTile = false;
     template <int BN>
     __device__ static void tile(const Params &, const float *, int, int, int, int, int, int, int) {}
+    __device__ static void pre(const Params &, int) {}
+    __device__ static void post(const Params &, int, unsigned) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -117,6 +119,8 @@ struct EpiDgrad {
     static constexpr bool kTile = false;
     template <int BN>
     __device__ static void tile(const Params &, const float *, int, int, int, int, int, int, int) {}
+    __device__ static void pre(const Params &, int) {}
+    __device__ static void post(const Params &, int, unsigned) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -133,6 +137,38 @@ struct EpiDgrad {
 //                no momentum: th' = th - (lr/n)*G   (wd: th - lr*(G/n + wd*th)).
 // The new parameters are also written as the packed compute-format copy the
 // next GEMMs read.  Non-finite gradient / parameter -> flag bits.
+// Cross-GPU ring state, one per rank inside its IPC-shared region (flags are
+// step / version numbers, written with st.release.sys, read with ld.acquire.sys).
+constexpr int kMaxStages = 32;
+struct RingFlags {
+    uint32_t ready[kMaxStages];      // this rank's partial S^j is complete for step `ready[j]`
+    uint32_t consumed[kMaxStages];   // the next rank finished reading this rank's S^j of that step
+    uint32_t updated[kMaxStages];    // updater: stage j holds version `updated[j]`
+    uint32_t pulled[kMaxStages][2];  // updater: readers that pulled version v (slot v % 2)
+    uint32_t err;                    // a spin-wait timed out (protocol failure)
+    uint32_t pad[31];
+};
+
+struct DistSync {
+    int enabled;
+    int n_readers;            // ranks that pull parameters (world - 1)
+    const int *step;          // device control block step t
+    RingFlags *own;
+    RingFlags *prev;          // rank - 1 (peer memory), null on rank 0
+    unsigned *cta_counter;    // local, per stage: CTAs of this launch that finished
+};
+
+__device__ __forceinline__ void spin_ge(const uint32_t *f, uint32_t v, uint32_t *err) {
+    const long long t0 = clock64();
+    while (ptx::ld_acquire_sys(f) < v) {
+        if (clock64() - t0 > (1ll << 32)) {  // ~2 s: report instead of hanging the GPU
+            atomicExch(err, 1u);
+            return;
+        }
+        __nanosleep(64);
+    }
+}
+
 struct HopParams {
     int mode;
     int stage;            // 1-based
@@ -149,6 +185,7 @@ struct HopParams {
     const float *db;      // this micro-batch's bias gradient [dout]
     unsigned *grad_flags; // bit (stage-1): non-finite gradient
     unsigned *upd_flags;  // bit (stage-1): non-finite updated parameter
+    DistSync sync;        // multi-GPU ring protocol (sync.enabled = 0 on one GPU)
 };
 
 template <int KIND>
@@ -334,6 +371,42 @@ struct EpiWgrad {
         if (bad_u) atomicOr(p.upd_flags, 1u << (p.stage - 1));
     }
 
+    // Multi-GPU ring protocol around the hop (comm.py:37-67 made real):
+    //   pre : wait until the previous rank's partial of this step is complete,
+    //         until the next rank has consumed our previous partial (we are
+    //         about to overwrite it), and (updater) until every reader pulled
+    //         the version this update overwrites;
+    //   post: the last CTA publishes ready / consumed / updated.
+    __device__ static void pre(const Params &p, int tid) {
+        if (!p.sync.enabled) return;
+        if (tid == 0) {
+            const uint32_t t = uint32_t(*p.sync.step), j = p.stage - 1;
+            uint32_t *err = &p.sync.own->err;
+            if (p.mode == 1 || p.mode == 2) spin_ge(&p.sync.prev->ready[j], t, err);
+            if (p.mode == 0 || p.mode == 1) spin_ge(&p.sync.own->consumed[j], t - 1, err);
+            if (p.mode == 2 && t >= 3) spin_ge(&p.sync.own->pulled[j][(t + 1) & 1], p.sync.n_readers, err);
+        }
+        __syncthreads();
+    }
+    __device__ static void post(const Params &p, int tid, unsigned n_ctas) {
+        if (!p.sync.enabled) return;
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t t = uint32_t(*p.sync.step), j = p.stage - 1;
+            __threadfence_system();
+            if (atomicAdd(&p.sync.cta_counter[j], 1u) == n_ctas - 1) {
+                p.sync.cta_counter[j] = 0;
+                __threadfence_system();
+                if (p.mode == 1 || p.mode == 2) ptx::st_release_sys(&p.sync.prev->consumed[j], t);
+                if (p.mode == 0 || p.mode == 1) ptx::st_release_sys(&p.sync.own->ready[j], t);
+                if (p.mode == 2) {
+                    p.sync.own->pulled[j][(t + 1) & 1] = 0;
+                    ptx::st_release_sys(&p.sync.own->updated[j], t + 1);
+                }
+            }
+        }
+    }
+
     // bias part of the stage, by CTA (0,0)
     __device__ static void extra(const Params &p, int tid, int nth) {
         bool bg = false, bu = false;
@@ -408,6 +481,42 @@ __global__ void gather_kernel(const float *__restrict__ data, int din, const int
     const int s = blockIdx.x;
     const float *src = data + size_t(perm[s]) * din;
     for (int k = threadIdx.x; k < din; k += blockDim.x) Fmt<KIND>::store(out.hi, out.lo, size_t(s) * out.ld + k, src[k]);
+}
+
+// theta delivery (the step the reference plan leaves implicit):
+// reader ranks copy stage j of version v from the updater's HBM over NVLink
+// into their own slot v % 2 (master fp32 + packed compute copy), then count
+// themselves in the updater's pulled[j][v % 2].  v = t (fresh read) or t-1.
+// Versions <= 1 are the initialisation every rank already holds.
+template <int KIND>
+__global__ void pull_stage_kernel(const float *__restrict__ src, float *dst, int din, int dout, CTensor wc,
+                                  RingFlags *updater, RingFlags *own, int stage, int fresh, const int *step,
+                                  unsigned *cta_counter) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int t = *step;
+    const uint32_t v = uint32_t(fresh ? t : t - 1);
+    if (v <= 1) return;
+    __shared__ int go;
+    if (threadIdx.x == 0) {
+        spin_ge(&updater->updated[stage - 1], v, &own->err);
+        go = 1;
+    }
+    __syncthreads();
+    const int64_t nw = int64_t(din) * dout, n = nw + dout;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const float x = __ldcv(src + i);  // peer memory: bypass stale cached copies
+        dst[i] = x;
+        if (i < nw) Fmt<KIND>::store(wc.hi, wc.lo, size_t(i / dout) * wc.ld + i % dout, x);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(&cta_counter[stage - 1], 1u) == gridDim.x - 1) {
+            cta_counter[stage - 1] = 0;
+            atomicAdd_system(&updater->pulled[stage - 1][v & 1], 1u);
+        }
+    }
 }
 
 // Pack master fp32 W (reference layout [din][dout]) into a compute copy [din][ld].

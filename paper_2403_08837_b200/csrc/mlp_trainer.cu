@@ -108,7 +108,20 @@ struct MlpTrainer {
     std::vector<int> slots;  // per stage (1..S) number of input-record slots
 
     // device state
-    DevBuf theta[2], vel, partial;
+    // IPC-shareable region: [RingFlags | theta slot 0 | theta slot 1 | partial S]
+    DevBuf region, vel;
+    float *theta[2] = {nullptr, nullptr};
+    float *partial = nullptr;
+    RingFlags *ring = nullptr;
+    size_t region_theta_off = 0;
+    int64_t Pp = 0;  // padded slot stride (floats)
+    // multi-GPU (one process per GPU): this rank's global worker index and peers
+    int rank = -1, world = 1;
+    RingFlags *prev_ring = nullptr;      // rank - 1
+    float *prev_partial = nullptr;
+    RingFlags *upd_ring = nullptr;       // updater = rank world - 1
+    float *upd_theta[2] = {nullptr, nullptr};
+    DevBuf cta_counters;                 // [2][kMaxStages]: hop / pull launches
     std::vector<CBuf> wc[2];                  // [slot][stage]
     std::vector<std::vector<CBuf>> rec;       // [stage][slot]
     DevBuf loss_all;  // [W] per-worker micro-batch losses (double)
@@ -200,11 +213,17 @@ struct MlpTrainer {
         }
         P = off;
         for (int v = 0; v < 2; ++v) {
-            theta[v] = DevBuf(size_t(P) * 4);
             for (int j = 0; j < S; ++j) wc[v].push_back(make_cbuf(kind, st[j].din, st[j].dout));
         }
         if (momentum != 0.f) vel = DevBuf(size_t(P) * 4);
-        partial = DevBuf(size_t(P) * 4);
+        region_theta_off = (sizeof(RingFlags) + 255) / 256 * 256;
+        Pp = (P + 63) / 64 * 64;  // slot stride keeps every slot 256-byte aligned
+        region = DevBuf(region_theta_off + size_t(Pp) * 4 * 3);
+        ring = region.as<RingFlags>();
+        theta[0] = reinterpret_cast<float *>(region.as<uint8_t>() + region_theta_off);
+        theta[1] = theta[0] + Pp;
+        partial = theta[1] + Pp;
+        cta_counters = DevBuf(2 * kMaxStages * 4);
         rec.resize(S);
         for (int j = 0; j < S; ++j)
             for (int r = 0; r < std::max(1, slots[j + 1]); ++r) rec[j].push_back(make_cbuf(kind, B, st[j].din));
@@ -311,7 +330,7 @@ struct MlpTrainer {
         Operand A[3], Bo[3];
         const int nseg = segments<K>(wc[vslot][j], true, g.dout, g.din, rec[j][rin], false, B, g.din, A, Bo);
         typename EpiFwd<K>::Params ep{};
-        ep.bias = theta[vslot].as<float>() + g.base + int64_t(g.din) * g.dout;
+        ep.bias = theta[vslot] + g.base + int64_t(g.din) * g.dout;
         ep.last = j == S - 1;
         if (ep.last)
             ep.z = wr.z.as<float>();
@@ -352,20 +371,41 @@ struct MlpTrainer {
         hp.base = g.base;
         hp.din = g.din;
         hp.dout = g.dout;
-        hp.s_in = partial.as<float>();
-        hp.s_out = partial.as<float>();
-        hp.theta_cur = theta[cur_slot].as<float>();
-        hp.theta_new = theta[cur_slot ^ 1].as<float>();
+        hp.s_in = rank >= 0 ? prev_partial : partial;
+        hp.s_out = partial;
+        hp.theta_cur = theta[cur_slot];
+        hp.theta_new = theta[cur_slot ^ 1];
+        if (rank >= 0) {
+            hp.sync.enabled = 1;
+            hp.sync.n_readers = world - 1;
+            hp.sync.step = &ctrl_dev.as<Control>()->step;
+            hp.sync.own = ring;
+            hp.sync.prev = prev_ring;
+            hp.sync.cta_counter = cta_counters.as<unsigned>();
+        }
         hp.vel = vel.as<float>();
         hp.lr = &ctrl_dev.as<Control>()->lr;
         hp.momentum = momentum;
         hp.wd = wd;
-        hp.n_mb = float(W);
+        hp.n_mb = float(rank >= 0 ? world : W);
         hp.wc_new = wc[cur_slot ^ 1][j].view();
         hp.db = db + size_t(j) * dmax;
         hp.grad_flags = &fl->grad;
         hp.upd_flags = &fl->upd;
         if (launch_mask & 4) gemm<K, true, true, EpiWgrad<K>>(bn_mn(g.dout), A, Bo, nseg, g.din, g.dout, B, wr, hp, s);
+    }
+
+    // theta delivery on reader ranks (see pull_stage_kernel)
+    template <int K>
+    void pull(int j, int vslot, int fresh, cudaStream_t s) {
+        CDP_REQUIRE(rank >= 0 && upd_ring && upd_theta[vslot], "pull op outside a connected multi-GPU trainer");
+        const StageGeom &g = st[j];
+        const int64_t n = int64_t(g.din) * g.dout + g.dout;
+        const int blocks = int(std::min<int64_t>(148, (n + 1023) / 1024));
+        launch_pdl(pull_stage_kernel<K>, dim3(blocks), dim3(256), 0, s, (const float *)(upd_theta[vslot] + g.base),
+                   theta[vslot] + g.base, g.din, g.dout, wc[vslot][j].view(), upd_ring, ring, j + 1, fresh,
+                   (const int *)&ctrl_dev.as<Control>()->step, cta_counters.as<unsigned>() + kMaxStages);
+        ++kernels_per_step;
     }
 
     // ---------------------------------------------------------------- capture
@@ -378,12 +418,14 @@ struct MlpTrainer {
         for (auto &d : deps) into[d.second].push_back(d.first);
         for (size_t o = 0; o < ops.size(); ++o) {
             const auto &op = ops[o];
-            const int w = op[OP_WORKER] - 1, j = op[OP_STAGE] - 1;
+            const int w = rank >= 0 ? 0 : op[OP_WORKER] - 1, j = op[OP_STAGE] - 1;
             cudaStream_t s = wk[w].stream;
             for (int d : into[o]) CDP_CUDA(cudaStreamWaitEvent(s, op_events[d], 0));
             const int vslot = op[OP_FRESH] ? p : (p ^ 1);
             const int *perm_w = perm_dev.as<int>() + size_t(w) * B;
-            if (op[OP_KIND] == 0)
+            if (op[OP_KIND] == 2)
+                pull<K>(j, vslot, op[OP_FRESH], s);
+            else if (op[OP_KIND] == 0)
                 forward<K>(w, j, vslot, op[OP_REC_IN], op[OP_REC_OUT], s, perm_w);
             else
                 backward<K>(w, j, vslot, op[OP_REC_IN], op[OP_HOP], p, s, perm_w);
@@ -431,7 +473,7 @@ struct MlpTrainer {
     // ---------------------------------------------------------------- params
     void pack_all(int slot) {
         for (int j = 0; j < S; ++j) {
-            const float *w = theta[slot].as<float>() + st[j].base;
+            const float *w = theta[slot] + st[j].base;
             if (kind == 0)
                 pack_w_kernel<0><<<148, 256, 0, main>>>(w, st[j].din, st[j].dout, wc[slot][j].view());
             else
@@ -445,7 +487,7 @@ struct MlpTrainer {
         for (int v = 0; v < 2; ++v) {
             if (which >= 0 && v != which) continue;
             const int slot = v == 0 ? (t & 1) : ((t & 1) ^ 1);
-            CDP_CUDA(cudaMemcpyAsync(theta[slot].p, host, size_t(P) * 4, cudaMemcpyHostToDevice, main));
+            CDP_CUDA(cudaMemcpyAsync(theta[slot], host, size_t(P) * 4, cudaMemcpyHostToDevice, main));
             pack_all(slot);
         }
         CDP_CUDA(cudaStreamSynchronize(main));
@@ -454,7 +496,7 @@ struct MlpTrainer {
     void get_params(int which, float *host) {
         CDP_CUDA(cudaStreamSynchronize(main));
         const int slot = which == 0 ? (t & 1) : ((t & 1) ^ 1);
-        CDP_CUDA(cudaMemcpy(host, theta[slot].p, size_t(P) * 4, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemcpy(host, theta[slot], size_t(P) * 4, cudaMemcpyDeviceToHost));
     }
 
     void set_velocity(const float *host) {
@@ -578,43 +620,130 @@ struct cdp_trainer {
     std::unique_ptr<MlpTrainer> impl;
 };
 
+static std::unique_ptr<MlpTrainer> create_impl(int n_dims, const int64_t *dims, int micro_batch, int n_workers,
+                                               int loss_kind, int dtype, float momentum, float weight_decay, int n_ops,
+                                               const int32_t *ops, int n_deps, const int32_t *deps,
+                                               const int32_t *slots_per_stage, int n_samples, const float *x,
+                                               const int32_t *labels, const float *targets, int rank, int world) {
+    CDP_REQUIRE(dtype == CDP_DTYPE_FP32 || dtype == CDP_DTYPE_BF16, "dtype must be CDP_DTYPE_FP32 or CDP_DTYPE_BF16");
+    CDP_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (mse) or 1 (xent)");
+    CDP_REQUIRE(n_workers >= 1, "n_workers must be >= 1");
+    CDP_REQUIRE(n_dims - 1 <= kMaxStages, "too many stages");
+    auto tr = std::make_unique<MlpTrainer>();
+    tr->kind = dtype == CDP_DTYPE_BF16 ? 0 : 1;
+    tr->rank = rank;
+    tr->world = world;
+    tr->W = rank >= 0 ? 1 : n_workers;
+    tr->B = micro_batch;
+    tr->loss_kind = loss_kind;
+    tr->momentum = momentum;
+    tr->wd = weight_decay;
+    tr->slots.assign(n_dims, 1);
+    for (int j = 1; j < n_dims; ++j) tr->slots[j] = slots_per_stage[j];
+    for (int o = 0; o < n_ops; ++o) {
+        std::array<int, OP_FIELDS> a;
+        for (int f = 0; f < OP_FIELDS; ++f) a[f] = ops[o * OP_FIELDS + f];
+        CDP_REQUIRE(a[OP_KIND] >= 0 && a[OP_KIND] <= 2, "op kind must be 0 (F), 1 (B) or 2 (pull)");
+        CDP_REQUIRE(a[OP_WORKER] >= 1 && a[OP_WORKER] <= n_workers, "op worker out of range");
+        CDP_REQUIRE(rank < 0 || a[OP_WORKER] == rank + 1, "a rank's plan may only hold its own worker's ops");
+        CDP_REQUIRE(a[OP_KIND] != 2 || rank >= 0, "pull ops need a multi-GPU trainer");
+        CDP_REQUIRE(a[OP_STAGE] >= 1 && a[OP_STAGE] < n_dims, "op stage out of range");
+        tr->ops.push_back(a);
+    }
+    for (int d = 0; d < n_deps; ++d) {
+        CDP_REQUIRE(deps[2 * d] < deps[2 * d + 1], "plan edges must point forward in op order");
+        tr->deps.emplace_back(deps[2 * d], deps[2 * d + 1]);
+    }
+    tr->setup(dims, n_dims);
+    for (auto &op : tr->ops) {
+        if (op[OP_KIND] == 2) continue;
+        CDP_REQUIRE(op[OP_REC_IN] < tr->slots[op[OP_STAGE]], "record slot out of range");
+        if (op[OP_KIND] == 0 && op[OP_STAGE] < tr->S)
+            CDP_REQUIRE(op[OP_REC_OUT] < tr->slots[op[OP_STAGE] + 1], "record slot out of range");
+    }
+    tr->upload_data(n_samples, x, labels, targets);
+    return tr;
+}
+
 extern "C" int cdp_trainer_create(int n_dims, const int64_t *dims, int micro_batch, int n_workers, int loss_kind,
                                   int dtype, float momentum, float weight_decay, int n_ops, const int32_t *ops,
                                   int n_deps, const int32_t *deps, const int32_t *slots_per_stage, int n_samples,
                                   const float *x, const int32_t *labels, const float *targets, cdp_trainer **out) {
     return guarded([&] {
-        CDP_REQUIRE(dtype == CDP_DTYPE_FP32 || dtype == CDP_DTYPE_BF16, "dtype must be CDP_DTYPE_FP32 or CDP_DTYPE_BF16");
-        CDP_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (mse) or 1 (xent)");
-        CDP_REQUIRE(n_workers >= 1, "n_workers must be >= 1");
-        auto tr = std::make_unique<MlpTrainer>();
-        tr->kind = dtype == CDP_DTYPE_BF16 ? 0 : 1;
-        tr->W = n_workers;
-        tr->B = micro_batch;
-        tr->loss_kind = loss_kind;
-        tr->momentum = momentum;
-        tr->wd = weight_decay;
-        tr->slots.assign(n_dims, 1);
-        for (int j = 1; j < n_dims; ++j) tr->slots[j] = slots_per_stage[j];
-        for (int o = 0; o < n_ops; ++o) {
-            std::array<int, OP_FIELDS> a;
-            for (int f = 0; f < OP_FIELDS; ++f) a[f] = ops[o * OP_FIELDS + f];
-            CDP_REQUIRE(a[OP_WORKER] >= 1 && a[OP_WORKER] <= n_workers, "op worker out of range");
-            CDP_REQUIRE(a[OP_STAGE] >= 1 && a[OP_STAGE] < n_dims, "op stage out of range");
-            tr->ops.push_back(a);
-        }
-        for (int d = 0; d < n_deps; ++d) {
-            CDP_REQUIRE(deps[2 * d] < deps[2 * d + 1], "plan edges must point forward in op order");
-            tr->deps.emplace_back(deps[2 * d], deps[2 * d + 1]);
-        }
-        tr->setup(dims, n_dims);
-        for (auto &op : tr->ops) {
-            CDP_REQUIRE(op[OP_REC_IN] < tr->slots[op[OP_STAGE]], "record slot out of range");
-            if (op[OP_KIND] == 0 && op[OP_STAGE] < tr->S)
-                CDP_REQUIRE(op[OP_REC_OUT] < tr->slots[op[OP_STAGE] + 1], "record slot out of range");
-        }
-        tr->upload_data(n_samples, x, labels, targets);
+        auto tr = create_impl(n_dims, dims, micro_batch, n_workers, loss_kind, dtype, momentum, weight_decay, n_ops,
+                              ops, n_deps, deps, slots_per_stage, n_samples, x, labels, targets, -1, 1);
         tr->capture();
         *out = new cdp_trainer{std::move(tr)};
+    });
+}
+
+extern "C" int cdp_trainer_create_rank(int n_dims, const int64_t *dims, int micro_batch, int world, int rank,
+                                       int loss_kind, int dtype, float momentum, float weight_decay, int n_ops,
+                                       const int32_t *ops, int n_samples, const float *x, const int32_t *labels,
+                                       const float *targets, cdp_trainer **out) {
+    return guarded([&] {
+        CDP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
+        std::vector<int32_t> slots(n_dims, 1);
+        auto tr = create_impl(n_dims, dims, micro_batch, world, loss_kind, dtype, momentum, weight_decay, n_ops, ops,
+                              0, nullptr, slots.data(), n_samples, x, labels, targets, rank, world);
+        *out = new cdp_trainer{std::move(tr)};
+    });
+}
+
+extern "C" int cdp_trainer_region(cdp_trainer *tr, void **base, size_t *bytes) {
+    return guarded([&] {
+        *base = tr->impl->region.p;
+        *bytes = tr->impl->region.bytes;
+    });
+}
+
+extern "C" int cdp_trainer_ipc_handle(cdp_trainer *tr, void *handle64) {
+    return guarded([&] {
+        cudaIpcMemHandle_t h;
+        CDP_CUDA(cudaIpcGetMemHandle(&h, tr->impl->region.p));
+        std::memcpy(handle64, &h, sizeof(h));
+    });
+}
+
+extern "C" int cdp_ipc_open(const void *handle64, void **ptr) {
+    return guarded([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        CDP_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+extern "C" int cdp_ipc_close(void *ptr) {
+    return guarded([&] { CDP_CUDA(cudaIpcCloseMemHandle(ptr)); });
+}
+
+// regions[r] = base of rank r's shared region, valid in this process (own
+// region for r == rank; IPC-mapped or same-process pointers for peers).
+extern "C" int cdp_trainer_connect(cdp_trainer *tr, void *const *regions) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_REQUIRE(m.rank >= 0, "connect is for multi-GPU (per-rank) trainers");
+        auto at = [&](int r) { return static_cast<uint8_t *>(regions[r]); };
+        const size_t off = m.region_theta_off;
+        if (m.rank > 0) {
+            m.prev_ring = reinterpret_cast<RingFlags *>(at(m.rank - 1));
+            m.prev_partial = reinterpret_cast<float *>(at(m.rank - 1) + off) + 2 * m.Pp;
+        }
+        const int u = m.world - 1;
+        m.upd_ring = reinterpret_cast<RingFlags *>(at(u));
+        m.upd_theta[0] = reinterpret_cast<float *>(at(u) + off);
+        m.upd_theta[1] = m.upd_theta[0] + m.Pp;
+        m.capture();
+    });
+}
+
+// Non-zero when a cross-GPU spin-wait timed out (protocol failure).
+extern "C" int cdp_trainer_ring_error(cdp_trainer *tr, int *err) {
+    return guarded([&] {
+        CDP_CUDA(cudaStreamSynchronize(tr->impl->main));
+        uint32_t e = 0;
+        CDP_CUDA(cudaMemcpy(&e, &tr->impl->ring->err, 4, cudaMemcpyDeviceToHost));
+        *err = int(e);
     });
 }
 
@@ -687,7 +816,7 @@ extern "C" int cdp_trainer_stats(cdp_trainer *tr, int64_t *out, int n_out) {
         int64_t act = 0;
         for (auto &stage : m.rec)
             for (auto &r : stage) act += int64_t(r.hi.bytes + r.lo.bytes);
-        int64_t par = int64_t(m.theta[0].bytes) * 2 + int64_t(m.vel.bytes) + int64_t(m.partial.bytes);
+        int64_t par = int64_t(m.P) * 4 * 3 + int64_t(m.vel.bytes);
         for (int v = 0; v < 2; ++v)
             for (auto &c : m.wc[v]) par += int64_t(c.hi.bytes + c.lo.bytes);
         int64_t vals[6] = {act, par, m.kernels_per_step, m.t, int64_t(m.W), int64_t(m.ops.size())};
@@ -699,7 +828,7 @@ extern "C" int cdp_trainer_get_grad(cdp_trainer *tr, float *grad) {
     return guarded([&] {
         auto &m = *tr->impl;
         CDP_CUDA(cudaStreamSynchronize(m.main));
-        CDP_CUDA(cudaMemcpy(grad, m.partial.p, size_t(m.P) * 4, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemcpy(grad, m.partial, size_t(m.P) * 4, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -774,7 +903,7 @@ extern "C" int cdp_mlp_value_grad(int n_dims, const int64_t *dims, const double 
         CDP_CUDA(cudaMemcpy(&c, tr.hist_count.p, 4, cudaMemcpyDeviceToHost));
         CDP_CUDA(cudaMemcpy(loss_out, tr.hist_loss.as<double>() + (c - 1) % tr.hist_cap, 8, cudaMemcpyDeviceToHost));
         std::vector<float> g(tr.P);
-        CDP_CUDA(cudaMemcpy(g.data(), tr.partial.p, size_t(tr.P) * 4, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemcpy(g.data(), tr.partial, size_t(tr.P) * 4, cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < tr.P; ++i) grad_out[i] = double(g[i]);
     });
 }

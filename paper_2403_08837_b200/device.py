@@ -14,7 +14,7 @@ import ctypes
 import numpy as np
 
 from . import _native as N
-from .executor import StepPlan, compile_step_plan
+from .executor import StepPlan, compile_rank_plan, compile_step_plan
 from .rules import UpdateRule
 
 DTYPES = {"fp32": 0, "bf16": 1}
@@ -67,10 +67,85 @@ class DeviceMlpTrainer:
         self.has_momentum = momentum != 0.0
         self._keep = (x, lab, tgt)
 
+    @classmethod
+    def for_rank(cls, dims, micro_batch: int, world: int, rank: int, loss_kind: int, rule: UpdateRule | None,
+                 dtype: str = "fp32", momentum: float = 0.0, weight_decay: float = 0.0,
+                 inputs: np.ndarray | None = None, targets: np.ndarray | None = None) -> "DeviceMlpTrainer":
+        """One rank of multi-GPU CDP (worker rank+1 on this process's GPU); call connect_* next."""
+        self = cls.__new__(cls)
+        self.lib = N.lib()
+        self.dims = tuple(int(d) for d in dims)
+        self.n_stages = len(self.dims) - 1
+        if self.n_stages != world:
+            raise ValueError("multi-GPU CDP ties stages = micro-batches = ranks")
+        self.micro_batch, self.n_workers, self.loss_kind, self.dtype = int(micro_batch), 1, int(loss_kind), dtype
+        self.rank, self.world = rank, world
+        self.sizes = [self.dims[j] * self.dims[j + 1] + self.dims[j + 1] for j in range(self.n_stages)]
+        self.P = sum(self.sizes)
+        self.rank_ops = compile_rank_plan(world, rank, rule)
+        self.plan = None
+        dims_a = np.asarray(self.dims, dtype=np.int64)
+        x = lab = tgt = None
+        n = 0
+        if inputs is not None:
+            x = np.ascontiguousarray(inputs, dtype=np.float32)
+            n = x.shape[0]
+            if loss_kind == 1:
+                lab = np.ascontiguousarray(targets, dtype=np.int32)
+            else:
+                tgt = np.ascontiguousarray(targets, dtype=np.float32)
+        ops = np.ascontiguousarray(self.rank_ops, dtype=np.int32)
+        h = ctypes.c_void_p()
+        N.check(self.lib.cdp_trainer_create_rank(
+            len(dims_a), dims_a.ctypes.data_as(N.c_int64_p), self.micro_batch, world, rank, self.loss_kind,
+            DTYPES[dtype], float(momentum), float(weight_decay), ops.shape[0], _i32(ops), n,
+            _f32(x) if x is not None else None, _i32(lab) if lab is not None else None,
+            _f32(tgt) if tgt is not None else None, ctypes.byref(h)))
+        self.h = h
+        self.has_momentum = momentum != 0.0
+        self._keep = (x, lab, tgt)
+        self._opened = []
+        return self
+
+    def region(self) -> int:
+        base, size = ctypes.c_void_p(), ctypes.c_size_t()
+        N.check(self.lib.cdp_trainer_region(self.h, ctypes.byref(base), ctypes.byref(size)))
+        return base.value
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        N.check(self.lib.cdp_trainer_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def connect(self, regions):
+        arr = (ctypes.c_void_p * len(regions))(*regions)
+        N.check(self.lib.cdp_trainer_connect(self.h, arr))
+
+    def connect_ipc(self, handles):
+        """handles[r] = rank r's 64-byte IPC handle (own entry ignored)."""
+        regions = []
+        for r, hd in enumerate(handles):
+            if r == self.rank:
+                regions.append(self.region())
+                continue
+            ptr = ctypes.c_void_p()
+            N.check(self.lib.cdp_ipc_open(ctypes.create_string_buffer(hd, 64), ctypes.byref(ptr)))
+            self._opened.append(ptr.value)
+            regions.append(ptr.value)
+        self.connect(regions)
+
+    def ring_error(self) -> int:
+        e = ctypes.c_int()
+        N.check(self.lib.cdp_trainer_ring_error(self.h, ctypes.byref(e)))
+        return e.value
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.cdp_trainer_destroy(self.h)
             self.h = None
+        for p in getattr(self, "_opened", []):
+            self.lib.cdp_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
 
     def __del__(self):
         try:
@@ -167,7 +242,8 @@ class DeviceMlpTrainer:
         N.check(self.lib.cdp_trainer_flush_l2(self.h))
 
     def op_index(self, kind: int, worker: int, stage: int) -> int:
-        for o, row in enumerate(self.plan.ops):
+        rows = self.plan.ops if self.plan is not None else self.rank_ops
+        for o, row in enumerate(rows):
             if row[0] == kind and row[1] == worker and row[2] == stage:
                 return o
         raise KeyError((kind, worker, stage))

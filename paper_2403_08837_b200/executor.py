@@ -35,6 +35,7 @@ from .rules import UpdateRule
 from .schedule import TaskKind, build_cdp_timeline, build_dp_timeline
 
 OP_FIELDS = 8
+OP_F, OP_B, OP_PULL = 0, 1, 2
 HOP_FIRST, HOP_MID, HOP_LAST, HOP_ONLY, HOP_GRAD = 0, 1, 2, 3, 4
 
 
@@ -149,3 +150,34 @@ def record_bytes(plan: StepPlan, dims, micro_batch: int, elem_bytes: int) -> int
     pad = lambda c: (c + 15) // 16 * 16
     return int(sum(int(plan.slots[j]) * micro_batch * pad(dims[j - 1]) * elem_bytes
                    for j in range(1, plan.n_stages + 1)))
+
+
+def compile_rank_plan(n_workers: int, rank: int, rule: UpdateRule | None = None) -> np.ndarray:
+    """Op list of one rank in multi-GPU CDP / DP (worker i = rank + 1 on its own GPU).
+
+    Per step: [pull(j)] F(i, j) for j = 1..N, then B(i, j) for j = N..1.  The
+    pull fetches, from the updater rank N-1, the version of stage j this
+    worker reads (t if fresh else t-1, ref rules.py:48-51) right before the
+    forward that reads it; the updater itself never pulls.  Every version is
+    therefore pulled exactly once per reader (fresh readers at step v, stale
+    readers at step v+1), which is what the updater's overwrite guard counts.
+    Record slots are all 0: one micro-batch per GPU holds one record per stage.
+    """
+    n = n_workers
+    i = rank + 1
+    if not 0 <= rank < n:
+        raise ValueError("rank out of range")
+    if rule is not None:
+        if rule.n != n:
+            raise ValueError("rule size does not match the number of ranks")
+        rule.check_feasible()
+    fresh = (lambda j: 1) if rule is None else (lambda j: int(rule.reads_fresh(i, j)))
+    hop = HOP_ONLY if n == 1 else HOP_FIRST if i == 1 else HOP_LAST if i == n else HOP_MID
+    ops = []
+    for j in range(1, n + 1):
+        if i != n:
+            ops.append([OP_PULL, i, j, fresh(j), 0, 0, 0, 0])
+        ops.append([OP_F, i, j, fresh(j), 0, 0, 0, 0])
+    for j in range(n, 0, -1):
+        ops.append([OP_B, i, j, fresh(j), 0, 0, hop, 0])
+    return np.asarray(ops, dtype=np.int32)

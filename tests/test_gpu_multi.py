@@ -1,0 +1,86 @@
+"""Multi-GPU CDP protocol (P2P gradient hop over peer memory, fused update on
+the last rank, parameter pulls), emulated with N rank trainers sharing one GPU
+in one process: every rank has its own stream, shared region and flags, and
+the kernels synchronise only through the system-scope flags — the exact code
+path of one-process-per-GPU runs, minus NVLink.
+
+The N-rank run performs the same arithmetic in the same order as the
+single-GPU N-worker trainer (S_i = S_{i-1} + g_i, update on worker N), so the
+parameters must agree bit for bit.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_ranks(task, rule_name, steps, dtype, momentum):
+    from paper_2403_08837_b200.device import DeviceMlpTrainer
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    n = task.n
+    rule = None if rule_name == "dp" else rule_by_name(rule_name, n)
+    ranks = [DeviceMlpTrainer.for_rank(task.model.dims, task.micro_batch_size, n, r, task.model.loss_code, rule,
+                                       dtype=dtype, momentum=momentum, inputs=task.inputs, targets=task.targets)
+             for r in range(n)]
+    regions = [t.region() for t in ranks]
+    init = np.concatenate(task.init_params())
+    for t in ranks:
+        t.set_params(init, which=-1)
+        t.connect(regions)
+    b = task.micro_batch_size
+    for step in range(1, steps + 1):
+        perm = task.permutation(step)
+        for r, t in enumerate(ranks):  # launch every rank's step; they synchronise on device flags
+            t.step(perm[r * b:(r + 1) * b], 0.05)
+    for t in ranks:
+        t.sync()
+        assert t.ring_error() == 0
+    losses = np.mean([t.history(steps)[0] for t in ranks], axis=0)
+    final = ranks[-1].get_params(0)
+    for t in ranks:
+        t.close()
+    return losses, final
+
+
+def _run_single(task, rule_name, steps, dtype, momentum):
+    from paper_2403_08837_b200.device import DeviceMlpTrainer
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = None if rule_name == "dp" else rule_by_name(rule_name, task.n)
+    tr = DeviceMlpTrainer(task.model.dims, task.micro_batch_size, task.n, task.model.loss_code, rule, dtype=dtype,
+                          momentum=momentum, inputs=task.inputs, targets=task.targets)
+    tr.set_params(np.concatenate(task.init_params()), which=-1)
+    for step in range(1, steps + 1):
+        tr.step(task.permutation(step), 0.05)
+    losses = tr.history(steps)[0]
+    final = tr.get_params(0)
+    tr.close()
+    return losses, final
+
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("rule", ["cdp-v1", "cdp-v2", "dp"])
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_ranks_match_single_gpu_bit_exact(cuda, n, rule, dtype):
+    from paper_2403_08837_b200.training import make_mlp_task
+
+    task = make_mlp_task(n=n, micro_batch_size=8, seed=4, width=64, in_dim=96, out_dim=10, loss_kind="xent")
+    l_multi, p_multi = _run_ranks(task, rule, 6, dtype, 0.9)
+    l_single, p_single = _run_single(task, rule, 6, dtype, 0.9)
+    assert np.array_equal(p_multi, p_single)
+    assert np.allclose(l_multi, l_single, rtol=1e-12, atol=0)
+
+
+def test_ranks_match_reference(cuda):
+    """4 ranks, CDP-v2, fp32: against the fp64 oracle (tolerance of the fp32 mode)."""
+    from oracle import engine as OE
+    from paper_2403_08837_b200.training import make_mlp_task
+
+    kw = dict(n=4, micro_batch_size=8, seed=6, width=64, in_dim=96, out_dim=10, loss_kind="xent")
+    losses, final = _run_ranks(make_mlp_task(**kw), "cdp-v2", 8, "fp32", 0.9)
+    ref = OE.run_experiment(OE.make_mlp_task(**kw), rules=("cdp-v2",), steps=8, lr=0.05, momentum=0.9)["cdp-v2"]
+    want = np.concatenate(ref.final_params)
+    assert np.linalg.norm(final - want) / np.linalg.norm(want) <= 1e-5
+    assert np.all(np.abs(losses - np.array(ref.losses)) <= 1e-5 * np.abs(np.array(ref.losses)))
