@@ -31,7 +31,8 @@ def _f32(a):
 class DeviceMlpTrainer:
     def __init__(self, dims, micro_batch: int, n_workers: int, loss_kind: int, rule: UpdateRule | None,
                  dtype: str = "fp32", momentum: float = 0.0, weight_decay: float = 0.0,
-                 inputs: np.ndarray | None = None, targets: np.ndarray | None = None, grad_only: bool = False):
+                 inputs: np.ndarray | None = None, targets: np.ndarray | None = None, grad_only: bool = False,
+                 layer_stage=None):
         if dtype not in DTYPES:
             raise ValueError(f"dtype must be one of {sorted(DTYPES)}")
         self.lib = N.lib()
@@ -41,8 +42,12 @@ class DeviceMlpTrainer:
         self.n_workers = int(n_workers)
         self.loss_kind = int(loss_kind)
         self.dtype = dtype
-        self.plan: StepPlan = compile_step_plan(self.n_stages, self.n_workers, rule, grad_only=grad_only)
-        self.sizes = [self.dims[j] * self.dims[j + 1] + self.dims[j + 1] for j in range(self.n_stages)]
+        self.n_layers = len(self.dims) - 1
+        if layer_stage is not None:
+            self.n_stages = max(layer_stage)
+        self.plan: StepPlan = compile_step_plan(self.n_stages, self.n_workers, rule, grad_only=grad_only,
+                                                layer_stage=layer_stage)
+        self.sizes = [self.dims[j] * self.dims[j + 1] + self.dims[j + 1] for j in range(self.n_layers)]
         self.P = sum(self.sizes)
         dims_a = np.asarray(self.dims, dtype=np.int64)
         n = 0
@@ -70,19 +75,21 @@ class DeviceMlpTrainer:
     @classmethod
     def for_rank(cls, dims, micro_batch: int, world: int, rank: int, loss_kind: int, rule: UpdateRule | None,
                  dtype: str = "fp32", momentum: float = 0.0, weight_decay: float = 0.0,
-                 inputs: np.ndarray | None = None, targets: np.ndarray | None = None) -> "DeviceMlpTrainer":
+                 inputs: np.ndarray | None = None, targets: np.ndarray | None = None,
+                 layer_stage=None) -> "DeviceMlpTrainer":
         """One rank of multi-GPU CDP (worker rank+1 on this process's GPU); call connect_* next."""
         self = cls.__new__(cls)
         self.lib = N.lib()
         self.dims = tuple(int(d) for d in dims)
-        self.n_stages = len(self.dims) - 1
-        if self.n_stages != world:
-            raise ValueError("multi-GPU CDP ties stages = micro-batches = ranks")
+        self.n_layers = len(self.dims) - 1
+        self.n_stages = world if layer_stage is not None else self.n_layers
+        if layer_stage is None and self.n_layers != world:
+            raise ValueError("multi-GPU CDP ties stages = micro-batches = ranks (pass layer_stage to group layers)")
         self.micro_batch, self.n_workers, self.loss_kind, self.dtype = int(micro_batch), 1, int(loss_kind), dtype
         self.rank, self.world = rank, world
-        self.sizes = [self.dims[j] * self.dims[j + 1] + self.dims[j + 1] for j in range(self.n_stages)]
+        self.sizes = [self.dims[j] * self.dims[j + 1] + self.dims[j + 1] for j in range(self.n_layers)]
         self.P = sum(self.sizes)
-        self.rank_ops = compile_rank_plan(world, rank, rule)
+        self.rank_ops = compile_rank_plan(world, rank, rule, layer_stage)
         self.plan = None
         dims_a = np.asarray(self.dims, dtype=np.int64)
         x = lab = tgt = None

@@ -76,8 +76,32 @@ def _template_tasks(n_stages: int, n_workers: int, rule: UpdateRule | None, weig
     return out
 
 
+def layer_stages(n_layers: int, n_stages: int) -> list:
+    """Contiguous, balanced assignment of layers to stages (1-based stage per layer)."""
+    if not 1 <= n_stages <= n_layers:
+        raise ValueError("need 1 <= stages <= layers")
+    base, extra = divmod(n_layers, n_stages)
+    out = []
+    for s in range(1, n_stages + 1):
+        out += [s] * (base + (1 if s <= extra else 0))
+    return out
+
+
+def _check_stage_map(layer_stage, n_stages):
+    if list(layer_stage) != sorted(layer_stage) or set(layer_stage) != set(range(1, n_stages + 1)):
+        raise ValueError("layer_stage must map layers onto stages 1..n contiguously")
+
+
 def compile_step_plan(n_stages: int, n_workers: int, rule: UpdateRule | None = None,
-                      weights: CostWeights = CostWeights(), grad_only: bool = False) -> StepPlan:
+                      weights: CostWeights = CostWeights(), grad_only: bool = False,
+                      layer_stage=None) -> StepPlan:
+    """Single-GPU plan; with `layer_stage` a stage task expands into its layers
+    (F ascending, B descending), all reading the stage's version."""
+    if layer_stage is None:
+        layer_stage = list(range(1, n_stages + 1))
+    _check_stage_map(layer_stage, n_stages)
+    n_layers = len(layer_stage)
+    layers_of = {s: [l for l in range(1, n_layers + 1) if layer_stage[l - 1] == s] for s in range(1, n_stages + 1)}
     if rule is not None:
         if rule.n != n_workers:
             raise ValueError("rule size does not match task")
@@ -89,54 +113,57 @@ def compile_step_plan(n_stages: int, n_workers: int, rule: UpdateRule | None = N
 
     ops, deps = [], []
     index = {}
-    free = {j: [] for j in range(1, n_stages + 1)}     # free slot ids per stage
-    count = {j: 0 for j in range(1, n_stages + 1)}     # slots created per stage
-    last_user = {}                                     # (j, slot) -> op that released it
-    holder = {}                                        # (i, j) -> slot of record (i, j)
+    free = {l: [] for l in range(1, n_layers + 1)}     # free record slots per layer input
+    count = {l: 0 for l in range(1, n_layers + 1)}
+    last_user = {}                                     # (l, slot) -> op that released it
+    holder = {}                                        # (i, l) -> slot of record (i, l)
 
-    def acquire(j: int, producer_op: int) -> int:
-        if free[j]:
-            s = free[j].pop(0)
-            rel = last_user.get((j, s))
+    def acquire(l: int, producer_op: int) -> int:
+        if free[l]:
+            s = free[l].pop(0)
+            rel = last_user.get((l, s))
             if rel is not None:
                 deps.append((rel, producer_op))
         else:
-            s = count[j]
-            count[j] += 1
+            s = count[l]
+            count[l] += 1
         return s
 
-    for start, i, kind, j in tasks:
-        o = len(ops)
-        row = [kind, i, j, int(fresh[i - 1, j - 1]), 0, 0, 0, 0]
-        if kind == 0:
-            if j == 1:
-                holder[(i, 1)] = acquire(1, o)
-            row[4] = holder[(i, j)]
-            if j < n_stages:
-                holder[(i, j + 1)] = acquire(j + 1, o)
-                row[5] = holder[(i, j + 1)]
-        else:
-            row[4] = holder[(i, j)]
-            if grad_only:
-                row[6] = HOP_GRAD
-            elif n_workers == 1:
-                row[6] = HOP_ONLY
+    for _start, i, kind, stage in tasks:
+        f = int(fresh[i - 1, stage - 1])
+        seq = layers_of[stage] if kind == 0 else layers_of[stage][::-1]
+        for l in seq:
+            o = len(ops)
+            row = [kind, i, l, f, 0, 0, 0, 0]
+            if kind == 0:
+                if l == 1:
+                    holder[(i, 1)] = acquire(1, o)
+                row[4] = holder[(i, l)]
+                if l < n_layers:
+                    holder[(i, l + 1)] = acquire(l + 1, o)
+                    row[5] = holder[(i, l + 1)]
             else:
-                row[6] = HOP_FIRST if i == 1 else (HOP_LAST if i == n_workers else HOP_MID)
-            if i > 1 and not grad_only:
-                deps.append((index[(1, i - 1, j)], o))
-            s = holder.pop((i, j))
-            free[j].append(s)
-            last_user[(j, s)] = o
-        index[(kind, i, j)] = o
-        ops.append(row)
+                row[4] = holder[(i, l)]
+                if grad_only:
+                    row[6] = HOP_GRAD
+                elif n_workers == 1:
+                    row[6] = HOP_ONLY
+                else:
+                    row[6] = HOP_FIRST if i == 1 else (HOP_LAST if i == n_workers else HOP_MID)
+                if i > 1 and not grad_only:
+                    deps.append((index[(1, i - 1, l)], o))
+                s = holder.pop((i, l))
+                free[l].append(s)
+                last_user[(l, s)] = o
+            index[(kind, i, l)] = o
+            ops.append(row)
 
     deps = sorted(set(deps))
     for a, b in deps:
         assert a < b, "plan edges must point forward"
-    slots = np.zeros(n_stages + 1, dtype=np.int32)
-    for j in range(1, n_stages + 1):
-        slots[j] = max(count[j], 1)
+    slots = np.zeros(n_layers + 1, dtype=np.int32)
+    for l in range(1, n_layers + 1):
+        slots[l] = max(count[l], 1)
     return StepPlan(
         n_stages, n_workers,
         np.asarray(ops, dtype=np.int32).reshape(-1, OP_FIELDS),
@@ -146,13 +173,13 @@ def compile_step_plan(n_stages: int, n_workers: int, rule: UpdateRule | None = N
 
 
 def record_bytes(plan: StepPlan, dims, micro_batch: int, elem_bytes: int) -> int:
-    """Activation bytes the executor allocates for `plan` (record j = stage-j input)."""
+    """Activation bytes the executor allocates for `plan` (record l = input of layer l)."""
     pad = lambda c: (c + 15) // 16 * 16
-    return int(sum(int(plan.slots[j]) * micro_batch * pad(dims[j - 1]) * elem_bytes
-                   for j in range(1, plan.n_stages + 1)))
+    return int(sum(int(plan.slots[l]) * micro_batch * pad(dims[l - 1]) * elem_bytes
+                   for l in range(1, len(plan.slots))))
 
 
-def compile_rank_plan(n_workers: int, rank: int, rule: UpdateRule | None = None) -> np.ndarray:
+def compile_rank_plan(n_workers: int, rank: int, rule: UpdateRule | None = None, layer_stage=None) -> np.ndarray:
     """Op list of one rank in multi-GPU CDP / DP (worker i = rank + 1 on its own GPU).
 
     Per step: [pull(j)] F(i, j) for j = 1..N, then B(i, j) for j = N..1.  The
@@ -161,23 +188,29 @@ def compile_rank_plan(n_workers: int, rank: int, rule: UpdateRule | None = None)
     forward that reads it; the updater itself never pulls.  Every version is
     therefore pulled exactly once per reader (fresh readers at step v, stale
     readers at step v+1), which is what the updater's overwrite guard counts.
-    Record slots are all 0: one micro-batch per GPU holds one record per stage.
+    Record slots are all 0: one micro-batch per GPU holds one record per layer.
+    With `layer_stage`, pulls and hops run per layer (the per-layer delayed
+    gradient path) while versions follow the layer's stage.
     """
     n = n_workers
     i = rank + 1
     if not 0 <= rank < n:
         raise ValueError("rank out of range")
+    if layer_stage is None:
+        layer_stage = list(range(1, n + 1))
+    _check_stage_map(layer_stage, n)
+    n_layers = len(layer_stage)
     if rule is not None:
         if rule.n != n:
             raise ValueError("rule size does not match the number of ranks")
         rule.check_feasible()
-    fresh = (lambda j: 1) if rule is None else (lambda j: int(rule.reads_fresh(i, j)))
+    fresh = (lambda l: 1) if rule is None else (lambda l: int(rule.reads_fresh(i, layer_stage[l - 1])))
     hop = HOP_ONLY if n == 1 else HOP_FIRST if i == 1 else HOP_LAST if i == n else HOP_MID
     ops = []
-    for j in range(1, n + 1):
+    for l in range(1, n_layers + 1):
         if i != n:
-            ops.append([OP_PULL, i, j, fresh(j), 0, 0, 0, 0])
-        ops.append([OP_F, i, j, fresh(j), 0, 0, 0, 0])
-    for j in range(n, 0, -1):
-        ops.append([OP_B, i, j, fresh(j), 0, 0, hop, 0])
+            ops.append([OP_PULL, i, l, fresh(l), 0, 0, 0, 0])
+        ops.append([OP_F, i, l, fresh(l), 0, 0, 0, 0])
+    for l in range(n_layers, 0, -1):
+        ops.append([OP_B, i, l, fresh(l), 0, 0, hop, 0])
     return np.asarray(ops, dtype=np.int32)

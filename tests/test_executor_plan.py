@@ -74,3 +74,35 @@ def test_trace_matches_rule():
     plan = compile_step_plan(4, 4, min_delay_rule(4))
     tr = plan.trace(7)
     assert (7, 2, 3, 7) in tr and (7, 2, 2, 6) in tr and len(tr) == 16
+
+
+def test_layer_stage_grouping():
+    from paper_2403_08837_b200.executor import compile_rank_plan, layer_stages
+
+    assert layer_stages(8, 4) == [1, 1, 2, 2, 3, 3, 4, 4]
+    assert layer_stages(7, 3) == [1, 1, 1, 2, 2, 3, 3]
+    r = min_delay_rule(4)
+    plan = compile_step_plan(4, 4, r, layer_stage=layer_stages(8, 4))
+    assert plan.ops.shape == (2 * 4 * 8, 8)
+    _simulate_slots_layers(plan, 8)
+    for kind, i, l, fresh, *_x in plan.ops:
+        assert fresh == int(r.reads_fresh(i, (l + 1) // 2))
+    ops = compile_rank_plan(4, 1, r, layer_stages(8, 4))
+    kinds = [tuple(o[:3]) for o in ops]
+    assert kinds[:4] == [(2, 2, 1), (0, 2, 1), (2, 2, 2), (0, 2, 2)]
+    assert kinds[-1] == (1, 2, 1)
+    with pytest.raises(ValueError):
+        compile_step_plan(4, 4, r, layer_stage=[1, 3, 2, 4])
+
+
+def _simulate_slots_layers(plan, n_layers):
+    owner = {}
+    for kind, i, l, fresh, rin, rout, hop, _ in plan.ops:
+        if kind == 0:
+            if l == 1:
+                owner[(1, rin)] = i
+            assert owner[(l, rin)] == i
+            if l < n_layers:
+                owner[(l + 1, rout)] = i
+        else:
+            assert owner[(l, rin)] == i

@@ -84,3 +84,62 @@ def test_ranks_match_reference(cuda):
     want = np.concatenate(ref.final_params)
     assert np.linalg.norm(final - want) / np.linalg.norm(want) <= 1e-5
     assert np.all(np.abs(losses - np.array(ref.losses)) <= 1e-5 * np.abs(np.array(ref.losses)))
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_grouped_layers_ranks_vs_oracle(cuda, n):
+    """8 layers grouped into n stages (stage = contiguous layers, versions per stage,
+    hops and pulls per layer): n ranks vs the single-GPU trainer (bit-exact) and vs
+    the fp64 oracle with the rule expanded to layers."""
+    from oracle import engine as OE
+    from paper_2403_08837_b200.device import DeviceMlpTrainer
+    from paper_2403_08837_b200.executor import layer_stages
+    from paper_2403_08837_b200.rules import min_delay_rule
+    from paper_2403_08837_b200.training import make_mlp_task
+
+    kw = dict(n=8, micro_batch_size=16, seed=9, width=48, in_dim=64, out_dim=10, loss_kind="xent")
+    base = make_mlp_task(**kw)
+    ls = layer_stages(8, n)
+    rule = min_delay_rule(n)
+    inputs, targets = base.inputs[: n * 16], base.targets[: n * 16]
+    steps = 5
+    perms = [np.random.default_rng([1, t]).permutation(n * 16) for t in range(1, steps + 1)]
+    init = np.concatenate(base.init_params())
+    # single GPU, n workers
+    tr = DeviceMlpTrainer(base.model.dims, 16, n, 1, rule, dtype="fp32", momentum=0.9, inputs=inputs,
+                          targets=targets, layer_stage=ls)
+    tr.set_params(init, -1)
+    for t in range(steps):
+        tr.step(perms[t], 0.05)
+    single = tr.get_params(0)
+    tr.close()
+    # n ranks
+    ranks = [DeviceMlpTrainer.for_rank(base.model.dims, 16, n, r, 1, rule, dtype="fp32", momentum=0.9,
+                                       inputs=inputs, targets=targets, layer_stage=ls) for r in range(n)]
+    regions = [r_.region() for r_ in ranks]
+    for r_ in ranks:
+        r_.set_params(init, -1)
+        r_.connect(regions)
+    for t in range(steps):
+        for r, r_ in enumerate(ranks):
+            r_.step(perms[t][r * 16:(r + 1) * 16], 0.05)
+    for r_ in ranks:
+        r_.sync()
+        assert r_.ring_error() == 0
+    multi = ranks[-1].get_params(0)
+    for r_ in ranks:
+        r_.close()
+    assert np.array_equal(single, multi)
+    # oracle: layer-expanded rule table
+    otask = OE.make_mlp_task(**kw)
+    fresh = [[rule.reads_fresh(i, ls[l]) for l in range(8)] for i in range(1, n + 1)]
+    cur = otask.init_params()
+    prev = [p.copy() for p in cur]
+    vel = [np.zeros_like(p) for p in cur]
+    for t in range(1, steps + 1):
+        p = perms[t - 1]
+        batches = [(inputs[p[i * 16:(i + 1) * 16]], targets[p[i * 16:(i + 1) * 16]]) for i in range(n)]
+        new, _ = OE.advance(otask, cur, prev, t, batches, 0.05, fresh, 0.9, vel)
+        prev, cur = cur, new
+    want = np.concatenate(cur)
+    assert np.linalg.norm(multi - want) / np.linalg.norm(want) <= 1e-5
