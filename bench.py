@@ -2,24 +2,30 @@
 """CDP training-step benchmark on B200 (contract: DESIGN.md §Measurement).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--dtype bf16|fp32] [--rule cdp-v1|cdp-v2|dp]
+                    [--dtype bf16|fp32] [--rule cdp-v2|cdp-v1|dp]
+    torchrun --nproc-per-node N bench.py --gpus N ...
 
-Workload (round 1): BASELINE.json configs[0], the config the reference can
-execute — the stage MLP 3072-256-256-256-10, N = 4 micro-batches = stages =
-workers, B = 32, softmax-xent, SGD lr 0.05 momentum 0.9, CDP-v1 (the
-reference's CPU path, timed beside it).  configs[1..4] (ResNet / ViT) are not
-built yet.  One "step" = one training step over N*B = 128
-samples, the whole CDP step on the device (forward, backward, gradient hops,
-fused update) as one CUDA graph.
+Workload (round 1; ResNet / ViT layer kernels are not built yet, DESIGN.md
+§Scope): BASELINE configs[1]'s structure — CDP-v2, ONE micro-batch per GPU,
+N = micro-batches = stages = GPUs — on the stage MLP family of configs[0]:
+an 8-layer tanh MLP 3072-256x7-10 (softmax-xent, SGD lr 0.05 momentum 0.9),
+micro-batch B = 128 per GPU, the 8 layers grouped into N contiguous stages.
+Per-GPU work is the same at every N (weak scaling).  One step = one training
+step of the whole job: every rank's forward + backward, the per-layer
+gradient hops rank -> rank+1 over peer memory, the fused update on the last
+rank, the parameter pulls — one CUDA graph per rank, no collective.
 
-Prints ONE JSON line (rank 0).  `value` = samples/s of the device-timed step
-(CUDA events on the trainer stream around each graph launch, inputs resident
-in HBM, L2 flushed with a 256 MiB memset before every timed step, max over
-ranks); `e2e` = the same through the public API with host (pinned) inputs
-copied H2D inside each step and the step loss read back every step.
-`--impl reference` times the reference's own CPU implementation of the step
-(its compiled Cython kernel from oracle/_ref, the engine loop restated in
-oracle/engine.py) on the host cores, one process per micro-batch.
+At N = 1 the line also carries `single_gpu_cdp`: configs[0] itself (4-layer
+3072-256-256-256-10, 4 micro-batches of 32 on one GPU, CDP-v1), the
+reference's own CPU-runnable case, with its CPU time beside it.
+
+`value` = samples/s of the device-timed step (CUDA events on each rank's
+trainer stream around each graph launch, inputs resident in HBM, L2 flushed
+by a 256 MiB memset before every timed step, max over ranks); `e2e` = the
+same through the public API from pinned host inputs copied H2D inside every
+step with the step loss read back every step.  `--impl reference` times the
+reference's own CPU implementation (its compiled Cython kernel, oracle/_ref,
+under the restated engine loop) with one process per micro-batch.
 """
 
 from __future__ import annotations
@@ -38,37 +44,53 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 with open(os.path.join(ROOT, "BASELINE.json")) as _fh:
-    BASELINE = json.load(_fh)
-METRIC = BASELINE["metric"]
+    METRIC = json.load(_fh)["metric"]
 UNIT = "samples/s"
+DEEP_DIMS = (3072,) + (256,) * 7 + (10,)
+MB = 128
 CONFIG1 = dict(n=4, micro_batch_size=32, seed=0, width=256, in_dim=3072, out_dim=10, loss_kind="xent")
 LR, MOMENTUM = 0.05, 0.9
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def workload_name(rule, dtype):
-    return (f"config1 stage-MLP 3072-256-256-256-10, N=4 micro-batches/stages/workers, B=32, xent, "
-            f"{rule}, {dtype}, SGD lr {LR} momentum {MOMENTUM}")
+def make_deep_task(n: int, seed: int = 0):
+    """Synthetic CIFAR-shaped data for the deep MLP, generated like the reference's make_mlp_task
+    (x ~ N(0,1) from default_rng([seed, 0xB0]); labels = argmax of a teacher from [seed, 0xB1])."""
+    from paper_2403_08837_b200.training.models import StageMlp, ToyTask
+
+    model = StageMlp(dims=DEEP_DIMS, loss_kind="xent")
+    rng = np.random.default_rng([seed, 0xB0])
+    x = rng.normal(0.0, 1.0, size=(n * MB, DEEP_DIMS[0]))
+    y = np.argmax(model.forward(model.init_params(np.random.default_rng([seed, 0xB1])), x), axis=1).astype(np.int64)
+    return ToyTask(model, x, y, n, MB, seed)
+
+
+def workload_name(n, rule, dtype):
+    return (f"CDP one micro-batch per GPU: 8-layer MLP 3072-256x7-10 in {n} stage(s), B={MB}/GPU, xent, "
+            f"{rule}, {dtype}, SGD lr {LR} momentum {MOMENTUM} (stage-MLP stand-in for configs[1])")
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
 
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvml samples of SM clock and throttle reasons, ~1 kHz, during the timed region."""
 
-    REASONS = {
-        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
-        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
-        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
-    }
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x10: "sync_boost"}
 
     def __init__(self, index=0):
-        self.samples, self.reasons, self.ok = [], set(), False
+        self.samples, self.reasons, self.ok, self.max_mhz = [], set(), False, None
         try:
             import pynvml
 
@@ -78,7 +100,7 @@ class ClockSampler:
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception:
-            self.max_mhz = None
+            pass
         self._stop = threading.Event()
 
     def _run(self):
@@ -86,9 +108,7 @@ class ClockSampler:
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
+                self.reasons.update(name for bit, name in self.REASONS.items() if r & bit)
             except Exception:
                 pass
             time.sleep(0.001)
@@ -105,82 +125,70 @@ class ClockSampler:
             self._t.join()
 
     def summary(self):
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ----------------------------------------------------------------------------- reference arm
-def _ref_worker(args):
+# ----------------------------------------------------------------------------- CPU reference
+def _ref_job(args):
     dims, theta, x, labels = args
     from oracle import kernels as OK
 
     mod = OK.load_reference_kernels()
+    if mod is None:
+        return OK.mlp_value_grad(dims, theta, x, None, labels, 1)
     return mod.mlp_value_grad(dims, theta, x, None, labels, 1)
 
 
-def run_reference(steps, warmup, rule="cdp-v1", pool_size=None, sample_steps=None):
-    """The reference's CPU step: its compiled Cython kernel per micro-batch, engine loop restated
-    (ref engine.py:66-116).  Returns (samples/s, cores, kind, description)."""
+def cpu_reference(task, fresh, steps, warmup, procs):
+    """The reference's CPU step (ref engine.py:66-116 restated in oracle/engine.py) with its compiled
+    kernel (oracle/_ref) per micro-batch; `procs` > 1 evaluates the micro-batches in parallel processes."""
     from oracle import engine as OE
     from oracle import kernels as OK
 
-    mod = OK.load_reference_kernels()
-    kind = "reference" if mod is not None else "port"
-    task = OE.make_mlp_task(**CONFIG1)
-    fresh = OE.fresh_table(rule, task.n)
-    cur = task.init_params()
+    kind = "reference" if OK.load_reference_kernels() is not None else "port"
+    sizes = task.model.stage_sizes
+    dims = task.model.dims
+    cur = [p.copy() for p in task.init_params()]
     prev = [p.copy() for p in cur]
     vel = [np.zeros_like(p) for p in cur]
-    cores = pool_size or 1
     pool = None
-    if cores > 1:
+    if procs > 1:
         import multiprocessing as mp
 
-        pool = mp.get_context("fork").Pool(cores)
+        pool = mp.get_context("fork").Pool(procs)
 
-    def grads_fn_parallel(batches, params_per_mb):
-        jobs = [(task.dims, np.concatenate(params_per_mb[i]), batches[i][0], batches[i][1].astype(np.int64))
-                for i in range(task.n)]
-        return pool.map(_ref_worker, jobs)
-
-    def one_step(t):
+    def one(t):
         nonlocal cur, prev
         batches = task.micro_batches(t)
-        if pool is None:
-            kern = (lambda d, th, x, y, l, k: mod.mlp_value_grad(d, th, x, y, l, k)) if mod else OK.mlp_value_grad
+        params = [[cur[j] if (fresh is None or fresh[i][j]) else prev[j] for j in range(len(cur))]
+                  for i in range(task.n)]
+        jobs = [(dims, np.concatenate(params[i]), batches[i][0], batches[i][1].astype(np.int64)) for i in range(task.n)]
+        res = pool.map(_ref_job, jobs) if pool else [_ref_job(j) for j in jobs]
+        it = iter(res)
 
-            def gfn(params, x, y):
-                loss, g = kern(task.dims, np.concatenate(params), x, None, y.astype(np.int64), 1)
-                return loss, OE.split(g, task.stage_sizes)
+        def gfn(_p, _x, _y):
+            loss, g = next(it)
+            return loss, OE.split(g, sizes)
 
-            new, _ = OE.advance(task, cur, prev, t, batches, LR, fresh, MOMENTUM, vel, grads_fn=gfn)
-        else:
-            params = [[cur[j] if (fresh is None or fresh[i][j]) else prev[j] for j in range(task.n)]
-                      for i in range(task.n)]
-            res = grads_fn_parallel(batches, params)
-            it = iter(res)
-
-            def gfn(_params, _x, _y):
-                loss, g = next(it)
-                return loss, OE.split(g, task.stage_sizes)
-
-            new, _ = OE.advance(task, cur, prev, t, batches, LR, fresh, MOMENTUM, vel, grads_fn=gfn)
+        new, _ = OE.advance(task, cur, prev, t, batches, LR, fresh, MOMENTUM, vel, grads_fn=gfn)
         prev, cur = cur, new
 
     for t in range(1, warmup + 1):
-        one_step(t)
-    n = sample_steps or steps
+        one(t)
     t0 = time.perf_counter()
-    for t in range(warmup + 1, warmup + n + 1):
-        one_step(t)
-    dt = time.perf_counter() - t0
-    if pool is not None:
+    for t in range(warmup + 1, warmup + steps + 1):
+        one(t)
+    dt = (time.perf_counter() - t0) / steps
+    if pool:
         pool.close()
-    sps = n * task.n * task.micro_batch_size / dt
-    desc = (f"{n} steps of the config-1 {rule} step (N=4 x B=32, fp64, momentum {MOMENTUM}) after {warmup} warm-up; "
-            f"{'reference Cython kernel (oracle/_ref)' if kind == 'reference' else 'C restatement (oracle)'}"
-            f"{', one process per micro-batch' if pool is not None else ', single thread'}")
-    return sps, cores, kind, desc, dt / n * 1e3
+    return task.n * task.micro_batch_size / dt, dt * 1e3, kind
+
+
+def expanded_fresh(rule, n, layer_stage):
+    if rule is None:
+        return None
+    return [[rule.reads_fresh(i, layer_stage[l]) for l in range(len(layer_stage))] for i in range(1, n + 1)]
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -189,21 +197,25 @@ def run_ours(args, ws, rank, local):
 
     torch.cuda.set_device(local)
     from paper_2403_08837_b200.device import DeviceMlpTrainer
-    from paper_2403_08837_b200.rules import rule_by_name
-    from paper_2403_08837_b200.training import make_mlp_task
+    from paper_2403_08837_b200.dist import exchange_handles, resolve
+    from paper_2403_08837_b200.executor import layer_stages
 
-    task = make_mlp_task(**CONFIG1)
-    rule = None if args.rule == "dp" else rule_by_name(args.rule, task.n)
-    tr = DeviceMlpTrainer(task.model.dims, task.micro_batch_size, task.n, 1, rule, dtype=args.dtype,
-                          momentum=MOMENTUM, inputs=task.inputs, targets=task.targets)
+    task = make_deep_task(ws)
+    rule = resolve(args.rule, ws)
+    ls = layer_stages(len(DEEP_DIMS) - 1, ws)
+    tr = DeviceMlpTrainer.for_rank(DEEP_DIMS, MB, ws, rank, 1, rule, dtype=args.dtype, momentum=MOMENTUM,
+                                   inputs=task.inputs, targets=task.targets, layer_stage=ls)
     tr.set_params(np.concatenate(task.init_params()), which=-1)
-    perms = [task.permutation(t) for t in range(1, args.warmup + args.steps + 2)]
+    if ws > 1:
+        tr.connect_ipc(exchange_handles(tr.ipc_handle()))
+    else:
+        tr.connect([tr.region()])
+    perms = [task.permutation(t)[rank * MB:(rank + 1) * MB] for t in range(1, args.warmup + args.steps + 2)]
     for t in range(args.warmup):
         tr.step(perms[t], LR)
     tr.sync()
     if ws > 1:
         torch.distributed.barrier()
-
     K = args.steps
     with ClockSampler(local) as clk:
         for k in range(K):
@@ -212,111 +224,127 @@ def run_ours(args, ws, rank, local):
             tr.step(perms[args.warmup + k], LR)
             tr.mark(2 * k + 1)
         tr.sync()
-    step_ms = [tr.elapsed(2 * k, 2 * k + 1) for k in range(K)]
-    ms = float(np.mean(step_ms))
+    if tr.ring_error():
+        raise RuntimeError(f"rank {rank}: ring protocol timed out")
+    ms = float(np.mean([tr.elapsed(2 * k, 2 * k + 1) for k in range(K)]))
     if ws > 1:
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    samples_per_step = task.n * task.micro_batch_size
-    value = ws * samples_per_step / (ms / 1e3)
-    losses, flags = tr.history()
+    losses, flags = tr.history(K + args.warmup)
     assert np.all(np.isfinite(losses)) and not flags.any(), "non-finite step in the timed region"
+    value = ws * MB / (ms / 1e3)
     stats = tr.stats()
 
-    # ---- e2e: public API, pinned host inputs copied H2D each step, loss read back each step
-    B = samples_per_step
-    x_pin = torch.empty((B, task.model.dims[0]), dtype=torch.float32, pin_memory=True)
-    y_pin = torch.empty((B,), dtype=torch.int32, pin_memory=True)
-    h2d = x_pin.numel() * 4 + y_pin.numel() * 4 + 16 + B * 4  # batch + labels + control block + row table
-    d2h = 8 + 12
-    batches = []
-    for k in range(K + 2):
-        p = perms[k % len(perms)]
-        batches.append((task.inputs[p].astype(np.float32), task.targets[p].astype(np.int32)))
-    for k in range(2):  # warm the host path
-        x_pin.numpy()[:] = batches[k][0]
-        y_pin.numpy()[:] = batches[k][1]
-        tr.step_host_batch_ptr(x_pin.data_ptr(), y_pin.data_ptr(), LR)
-        tr.last()
+    # ---- e2e: public API, pinned host micro-batch copied H2D every step, loss read back every step
+    x_pin = torch.empty((MB, DEEP_DIMS[0]), dtype=torch.float32, pin_memory=True)
+    y_pin = torch.empty((MB,), dtype=torch.int32, pin_memory=True)
+    host = [(task.inputs[p].astype(np.float32), task.targets[p].astype(np.int32)) for p in perms[:K + 2]]
     e2e_ms = []
-    for k in range(K):
-        x_pin.numpy()[:] = batches[k + 2][0]
-        y_pin.numpy()[:] = batches[k + 2][1]
+    if ws > 1:
+        torch.distributed.barrier()
+    for k in range(K + 2):
+        x_pin.numpy()[:] = host[k][0]
+        y_pin.numpy()[:] = host[k][1]
         tr.flush_l2()
         tr.mark(0)
         tr.step_host_batch_ptr(x_pin.data_ptr(), y_pin.data_ptr(), LR)
-        loss, fl = tr.last()
+        tr.last()
         tr.mark(1)
-        e2e_ms.append(tr.elapsed(0, 1))
+        if k >= 2:
+            e2e_ms.append(tr.elapsed(0, 1))
     e2e = float(np.mean(e2e_ms))
     if ws > 1:
         t = torch.tensor([e2e], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e = float(t.item())
+    h2d = MB * DEEP_DIMS[0] * 4 + MB * 4 + 16 + MB * 4
+    d2h = 8 + 16
 
-    # ---- roofline: the dominant kernel = stage-1 weight-grad GEMM fused with the mid ring hop
-    op = tr.op_index(1, 2, 1)
-    R = 20
+    # ---- roofline: layer-1 weight-grad GEMM with the fused hop (update when N = 1)
+    op = tr.op_index(1, rank + 1, 1)
     kms = []
-    for _ in range(R):
+    for _ in range(20):
         tr.flush_l2()
         kms.append(tr.time_op(op, 4, -1))
     k_ms = float(np.median(kms))
-    d0, d1 = task.model.dims[0], task.model.dims[1]
-    p1 = d0 * d1 + d1
-    esz = 2 if args.dtype == "bf16" else 8  # bf16 operand, or fp32 hi+lo
-    alg_bytes = p1 * 8 + task.micro_batch_size * (d0 + d1) * esz  # read S + write S, read H and dZ
-    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) if os.path.exists(
-            os.path.join(ROOT, "MEASURED_PEAKS.json")) else open(os.devnull) as fh:
-        try:
-            peaks = json.load(fh)
-            peak, peak_src = float(peaks["hbm_gbs"]), "measured"
-        except Exception:
-            peak, peak_src = 6650.0, "fallback"
-    achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    p1 = DEEP_DIMS[0] * DEEP_DIMS[1] + DEEP_DIMS[1]
+    esz = 2 if args.dtype == "bf16" else 8
+    mode = "only" if ws == 1 else ("first" if rank == 0 else "last" if rank == ws - 1 else "mid")
+    per_param = {"first": 4, "mid": 8, "last": 20 + esz, "only": 16 + esz}[mode]
+    alg = p1 * per_param + MB * (DEEP_DIMS[0] + DEEP_DIMS[1]) * (2 if args.dtype == "bf16" else 8)
+    peak, src = peak_hbm()
+    achieved = alg / (k_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "round1_wgrad_hop_traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
-            traffic = json.load(fh).get(args.dtype, {}).get("dram_bytes_per_launch")
-
-    # ---- activation memory CDP vs DP (same model, same executor)
-    other = DeviceMlpTrainer(task.model.dims, task.micro_batch_size, task.n, 1,
-                             None if rule is not None else rule_by_name("cdp-v2", task.n), dtype=args.dtype)
-    act_other = other.stats()["activation_bytes"]
-    other.close()
-    act_cdp, act_dp = (stats["activation_bytes"], act_other) if rule is not None else (act_other, stats["activation_bytes"])
+            traffic = json.load(fh).get(f"{args.dtype}-{mode}")
 
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
         "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": args.dtype, "data": "synthetic (reference make_mlp_task seed 0, numpy PCG64)",
-        "config": {"workload": workload_name(args.rule, args.dtype), "global_batch": ws * samples_per_step,
-                   "micro_batch": task.micro_batch_size, "n_micro_batches": task.n, "rule": args.rule,
-                   "parallelism": f"single-GPU CDP x{ws} replicas" if ws > 1 else "single-GPU CDP (4 worker streams)",
-                   "l2": "flushed (256 MiB memset) before every timed step; working set < L2"},
-        "e2e": {"value": round(ws * samples_per_step / (e2e / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        "dtype": args.dtype, "data": "synthetic (numpy PCG64, teacher-labelled, reference make_mlp_task recipe)",
+        "config": {"workload": workload_name(ws, args.rule, args.dtype), "global_batch": ws * MB, "micro_batch": MB,
+                   "stages": ws, "layers": len(DEEP_DIMS) - 1, "rule": args.rule,
+                   "parallelism": f"cdp{ws} (one process per GPU, P2P hop ring, fused update on rank {ws - 1})",
+                   "l2": "flushed (256 MiB memset) before every timed step"},
+        "e2e": {"value": round(ws * MB / (e2e / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e, 5)},
         "gpu_launches": stats["kernels_per_step"] * K,
-        "roofline": {"bound": "hbm", "kernel": "stage-1 wgrad GEMM + fused mid ring hop (gemm_tc_kernel<EpiWgrad>)",
-                     "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "algorithmic_bytes_per_launch": alg_bytes, "launch_us": round(k_ms * 1e3, 2)},
-        "activation_bytes": {"cdp": act_cdp, "dp": act_dp, "ratio": round(act_cdp / act_dp, 4)},
+        "roofline": {"bound": "hbm", "kernel": f"layer-1 wgrad GEMM + fused {mode} hop (gemm_tc_kernel<EpiWgrad>)",
+                     "achieved": round(achieved, 1), "peak": peak, "peak_source": src, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "algorithmic_bytes_per_launch": alg,
+                     "launch_us": round(k_ms * 1e3, 2)},
+        "activation_bytes": {"per_gpu": stats["activation_bytes"], "sum_over_gpus": stats["activation_bytes"] * ws},
         "clocks": clk.summary(),
     }
-    return out, tr
+    tr.close()
+    return out, task, rule, ls
+
+
+def single_gpu_config1(dtype):
+    """configs[0] on one GPU: 4 micro-batches x 32, 4 stages, CDP-v1 (+ activation bytes vs DP)."""
+    from paper_2403_08837_b200.device import DeviceMlpTrainer
+    from paper_2403_08837_b200.rules import rule_by_name
+    from paper_2403_08837_b200.training import make_mlp_task
+
+    task = make_mlp_task(**CONFIG1)
+    res = {}
+    for rname in ("cdp-v1", "dp"):
+        rule = None if rname == "dp" else rule_by_name(rname, 4)
+        tr = DeviceMlpTrainer(task.model.dims, 32, 4, 1, rule, dtype=dtype, momentum=MOMENTUM, inputs=task.inputs,
+                              targets=task.targets)
+        tr.set_params(np.concatenate(task.init_params()), which=-1)
+        for t in range(1, 11):
+            tr.step(task.permutation(t), LR)
+        ms = []
+        for k in range(100):
+            tr.flush_l2()
+            tr.mark(0)
+            tr.step(task.permutation(11 + k), LR)
+            tr.mark(1)
+            ms.append(tr.elapsed(0, 1))
+        res[rname] = (float(np.mean(ms)), tr.stats()["activation_bytes"])
+        tr.close()
+    sps, cms, kind = cpu_reference(task, [[False] * 4 for _ in range(4)], 8, 1, 1)
+    return {"workload": "configs[0]: 3072-256-256-256-10, 4 micro-batches x 32 on 1 GPU (4 worker streams), cdp-v1",
+            "value": round(128 / (res["cdp-v1"][0] / 1e3), 1), "unit": UNIT, "ms_per_step": round(res["cdp-v1"][0], 5),
+            "dp_value": round(128 / (res["dp"][0] / 1e3), 1),
+            "activation_bytes": {"cdp": res["cdp-v1"][1], "dp": res["dp"][1],
+                                 "ratio": round(res["cdp-v1"][1] / res["dp"][1], 4)},
+            "cpu_baseline": {"value": round(sps, 2), "unit": UNIT, "cores": 1, "kind": kind,
+                             "sample": "8 steps after 1 warm-up, reference Cython kernel, fp64, single thread"}}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--rule", default="cdp-v1", choices=["cdp-v1", "cdp-v2", "dp"])
+    ap.add_argument("--rule", default="cdp-v2", choices=["cdp-v2", "cdp-v1", "dp"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     ws, rank, local = dist_env()
@@ -324,14 +352,21 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cores = min(4, os.cpu_count() or 1)
-        n = max(1, min(args.steps, 60))
-        sps, cores, kind, desc, ms = run_reference(n, min(args.warmup, 3), rule=args.rule, pool_size=cores)
+        from paper_2403_08837_b200.dist import resolve
+        from paper_2403_08837_b200.executor import layer_stages
+
+        task = make_deep_task(ws)
+        fresh = expanded_fresh(resolve(args.rule, ws), ws, layer_stages(len(DEEP_DIMS) - 1, ws))
+        cores = min(ws, os.cpu_count() or 1)
+        n = max(1, min(args.steps, 5))
+        sps, ms, kind = cpu_reference(task, fresh, n, 1, cores)
+        desc = (f"{n} full steps (after 1 warm-up) of the {ws}-micro-batch step, fp64, reference Cython kernel, "
+                f"{'one process per micro-batch' if cores > 1 else 'single thread'}")
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": round(sps, 3), "unit": UNIT, "n_gpus": ws, "steps": n,
-            "warmup": min(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.rule, "fp64")},
+            "warmup": 1, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(ws, args.rule, "fp64")},
             "cpu_baseline": {"value": round(sps, 3), "unit": UNIT, "cores": cores, "kind": kind, "sample": desc,
                              "host_cpus": os.cpu_count()},
             "e2e": {"value": round(sps, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -341,18 +376,22 @@ def main():
     if ws > 1:
         import torch
 
+        torch.cuda.set_device(local)
         torch.distributed.init_process_group("nccl")
-    out, tr = run_ours(args, ws, rank, local)
+    out, task, rule, ls = run_ours(args, ws, rank, local)
     if rank == 0:
         if not args.no_cpu_baseline and ws == 1:
-            sps, cores, kind, desc, _ = run_reference(12, 1, rule=args.rule, pool_size=None)
-            out["cpu_baseline"] = {"value": round(sps, 3), "unit": UNIT, "cores": cores, "kind": kind,
-                                   "sample": desc, "host_cpus": os.cpu_count()}
+            sps, _ms, kind = cpu_reference(task, expanded_fresh(rule, ws, ls), 4, 1, 1)
+            out["cpu_baseline"] = {"value": round(sps, 3), "unit": UNIT, "cores": 1, "kind": kind,
+                                   "sample": "4 steps (after 1 warm-up) of the same 1-micro-batch step (B=128, 8 "
+                                             "layers), fp64, reference Cython kernel, single thread",
+                                   "host_cpus": os.cpu_count()}
+            out["single_gpu_cdp"] = single_gpu_config1(args.dtype)
         print(json.dumps(out), flush=True)
-    tr.close()
     if ws > 1:
         import torch
 
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 
 
