@@ -34,7 +34,7 @@ struct GemmArgs {
     int *counters;    // per tile arrival counters (self-resetting)
 };
 
-template <int KIND, int BN_, bool A_MN, bool B_MN>
+template <int KIND, int BN_, bool A_MN, bool B_MN, int ST = 0, int PF = 0>
 struct GemmCfg {
     static constexpr int BM = 128;
     static constexpr int BN = BN_;
@@ -45,9 +45,10 @@ struct GemmCfg {
     static constexpr int A_BYTES = BM * 128;
     static constexpr int B_BYTES = BN * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 6 ? 6 : (200 * 1024 / STAGE_BYTES);
+    static constexpr int STAGES = ST ? ST : ((200 * 1024 / STAGE_BYTES) > 6 ? 6 : (200 * 1024 / STAGE_BYTES));
+    static constexpr int PF_BYTES = PF;  // epilogue prefetch area (after the operand ring)
     static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + PF_BYTES + 256;
     static constexpr uint32_t IDESC = ptx::instr_desc(KIND == 0 ? 1u : 2u, A_MN, B_MN, 128, BN);
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN must be a multiple of 32 in [32,256]");
     static_assert(!B_MN || BN % CH == 0, "MN-major B needs BN multiple of the 128-byte row");
@@ -79,12 +80,13 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
 template <int KIND, int BN, bool A_MN, bool B_MN, class Epi>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args, const typename Epi::Params ep) {
-    using C = GemmCfg<KIND, BN, A_MN, B_MN>;
+    using C = GemmCfg<KIND, BN, A_MN, B_MN, Epi::kStages, Epi::template pf_bytes<BN>()>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
     uint8_t *sB = smem + C::STAGES * C::A_BYTES;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
+    float *pf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + C::PF_BYTES);
     uint64_t *empty = full + C::STAGES;
     uint64_t *tmem_full = empty + C::STAGES;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
@@ -233,6 +235,11 @@ __global__ void __launch_bounds__(256, 1)
             const int q = warp - 4;
             const int row = q * 32 + ptx::lane_id();
             const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
+            // while TMA + MMA run: protocol waits, then prefetch of the epilogue's
+            // other operands (parameters, momentum, previous partial) into shared
+            Epi::pre(ep, threadIdx.x - 128);
+            Epi::template prefetch<BN>(ep, pf, m0, n0, args.M, args.N, threadIdx.x - 128, 128);
+            ptx::cp_async_commit();
             ptx::mbar_wait(tmem_full, 0);
             ptx::tc_fence_after();
 #pragma unroll 1
@@ -247,10 +254,10 @@ __global__ void __launch_bounds__(256, 1)
                 for (int i = 0; i < 32; i += 4)
                     *reinterpret_cast<float4 *>(stile + row * LDS + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
             }
+            ptx::cp_async_wait_all();
         }
         __syncthreads();
-        Epi::pre(ep, threadIdx.x);
-        Epi::template tile<BN>(ep, stile, LDS, m0, n0, args.M, args.N, threadIdx.x, blockDim.x);
+        Epi::template tile<BN>(ep, stile, LDS, pf, m0, n0, args.M, args.N, threadIdx.x, blockDim.x);
         if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x, blockDim.x);
         Epi::post(ep, threadIdx.x, gridDim.x * gridDim.y);
     }

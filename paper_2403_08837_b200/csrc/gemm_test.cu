@@ -14,9 +14,14 @@ struct EpiStore {
         int ldd;
     };
     static constexpr bool kTile = false;
+    static constexpr int kStages = 0;
+    template <int BN>
+    static constexpr int pf_bytes() { return 0; }
+    template <int BN>
+    __device__ static void prefetch(const Params &, float *, int, int, int, int, int, int) {}
     struct State {};
     template <int BN>
-    __device__ static void tile(const Params &, const float *, int, int, int, int, int, int, int) {}
+    __device__ static void tile(const Params &, const float *, int, const float *, int, int, int, int, int, int) {}
     __device__ static void begin(const Params &, int, State &) {}
     __device__ static void finish(const Params &, int, int, State &) {}
     __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &) {

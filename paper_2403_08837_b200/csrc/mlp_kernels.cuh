@@ -50,33 +50,40 @@ struct CTensor {
 // last stage (ref _kernels.pyx:40-62).
 template <int KIND>
 struct EpiFwd {
+    // The stage input record carries a ones column at index din and the packed
+    // weights a bias row at index din (the reference's flat stage layout
+    // [din][dout] + [dout] IS the [din+1][dout] matrix), so acc already holds
+    // h.W + b.
     struct Params {
-        const float *bias;  // master fp32 bias of this stage (version read)
-        CTensor out;        // next-stage input record (tanh applied)
-        float *z;           // last stage: fp32 logits [B][dout]
+        CTensor out;  // next-stage input record (tanh applied)
+        float *z;     // last stage: fp32 logits [B][dout]
         int last;
     };
     struct State {};
     __device__ static void begin(const Params &, int, State &) {}
     __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &) {
         if (m >= M) return;
-        const float b = p.bias[m];
-#pragma unroll 4
+#pragma unroll 8
         for (int i = 0; i < 32; ++i) {
             const int s = n0 + i;
-            if (s >= N) break;
-            const float a = __fadd_rn(v[i], b);
-            if (p.last)
-                p.z[size_t(s) * M + m] = a;
-            else
-                Fmt<KIND>::store(p.out.hi, p.out.lo, size_t(s) * p.out.ld + m, tanhf(a));
+            if (s < N) {
+                if (p.last)
+                    p.z[size_t(s) * M + m] = v[i];
+                else
+                    Fmt<KIND>::store(p.out.hi, p.out.lo, size_t(s) * p.out.ld + m, tanhf(v[i]));
+            }
         }
     }
     __device__ static void finish(const Params &, int, int, State &) {}
     __device__ static void extra(const Params &, int, int) {}
     static constexpr bool kTile = false;
+    static constexpr int kStages = 0;
     template <int BN>
-    __device__ static void tile(const Params &, const float *, int, int, int, int, int, int, int) {}
+    static constexpr int pf_bytes() { return 0; }
+    template <int BN>
+    __device__ static void prefetch(const Params &, float *, int, int, int, int, int, int) {}
+    template <int BN>
+    __device__ static void tile(const Params &, const float *, int, const float *, int, int, int, int, int, int) {}
     __device__ static void pre(const Params &, int) {}
     __device__ static void post(const Params &, int, unsigned) {}
 };
@@ -87,16 +94,14 @@ struct EpiFwd {
 // db[k] = sum_s dprev[s, k] in ascending s (ref _kernels.pyx:115-130).
 template <int KIND>
 struct EpiDgrad {
+    // accumulator = (W . dZ^T)[k, s];  dprev[s, k] = acc * (1 - h^2)  (ref _kernels.pyx:120-130)
     struct Params {
         CTensor h;      // stage-j input record (tanh outputs of stage j-1)
         CTensor dprev;  // dZ_{j-1} out
-        float *db;      // bias grad of stage j-1 [din]
     };
-    struct State {
-        float acc;
-    };
-    __device__ static void begin(const Params &, int, State &st) { st.acc = 0.f; }
-    __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &st) {
+    struct State {};
+    __device__ static void begin(const Params &, int, State &) {}
+    __device__ static void apply(const Params &p, int m, int n0, const float (&v)[32], int M, int N, State &) {
         if (m >= M) return;
         float h[32];
 #pragma unroll
@@ -105,20 +110,21 @@ struct EpiDgrad {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             const int s = n0 + i;
-            if (s < N) {
-                const float d = __fmul_rn(v[i], __fsub_rn(1.f, __fmul_rn(h[i], h[i])));
-                Fmt<KIND>::store(p.dprev.hi, p.dprev.lo, size_t(s) * p.dprev.ld + m, d);
-                st.acc = __fadd_rn(st.acc, d);
-            }
+            if (s < N)
+                Fmt<KIND>::store(p.dprev.hi, p.dprev.lo, size_t(s) * p.dprev.ld + m,
+                                 __fmul_rn(v[i], __fsub_rn(1.f, __fmul_rn(h[i], h[i]))));
         }
     }
-    __device__ static void finish(const Params &p, int m, int M, State &st) {
-        if (m < M) p.db[m] = st.acc;
-    }
+    __device__ static void finish(const Params &, int, int, State &) {}
     __device__ static void extra(const Params &, int, int) {}
     static constexpr bool kTile = false;
+    static constexpr int kStages = 0;
     template <int BN>
-    __device__ static void tile(const Params &, const float *, int, int, int, int, int, int, int) {}
+    static constexpr int pf_bytes() { return 0; }
+    template <int BN>
+    __device__ static void prefetch(const Params &, float *, int, int, int, int, int, int) {}
+    template <int BN>
+    __device__ static void tile(const Params &, const float *, int, const float *, int, int, int, int, int, int) {}
     __device__ static void pre(const Params &, int) {}
     __device__ static void post(const Params &, int, unsigned) {}
 };
@@ -126,7 +132,9 @@ struct EpiDgrad {
 // ---------------------------------------------------------------------------
 // Weight gradient fused with the CDP gradient hop and, on the last hop, the
 // SGD(+momentum, weight decay) update (ref engine.py:96-109, comm.py:37-67).
-// accumulator = (H^T . dZ)[k, o] = dW[k, o] of this micro-batch.
+// accumulator = (H1^T . dZ)[k, o] with H1 = [H, 1]: rows k < din are dW[k, o],
+// row din is the bias gradient sum_s dZ[s, o] — the whole stage's flat gradient
+// in the reference layout, computed by the tensor core in one GEMM.
 //   mode 0 first hop : S[idx] = g
 //   mode 1 mid hop   : S[idx] = S_in[idx] + g      (S_in: previous worker's
 //                      partial; a peer-GPU pointer when workers are GPUs)
@@ -181,8 +189,7 @@ struct HopParams {
     float *vel;
     const float *lr;      // device scalar (per-step learning rate)
     float momentum, wd, n_mb;
-    CTensor wc_new;       // packed compute copy of W (new version)
-    const float *db;      // this micro-batch's bias gradient [dout]
+    CTensor wc_new;       // packed compute copy of [W; b] (new version)
     unsigned *grad_flags; // bit (stage-1): non-finite gradient
     unsigned *upd_flags;  // bit (stage-1): non-finite updated parameter
     DistSync sync;        // multi-GPU ring protocol (sync.enabled = 0 on one GPU)
@@ -249,6 +256,32 @@ template <int KIND>
 struct EpiWgrad {
     using Params = HopParams;
     static constexpr bool kTile = true;
+    static constexpr int kStages = 2;  // K = micro-batch: at most a few k-blocks
+    // prefetch area: theta_cur, velocity, incoming partial; [3][128][BN] fp32
+    template <int BN>
+    static constexpr int pf_bytes() { return 3 * 128 * BN * 4; }
+    __device__ static bool vec_ok(const Params &p) { return (p.dout % 4 == 0) && (p.base % 4 == 0); }
+
+    // Issued by the 128 epilogue threads while TMA + MMA still run (cp.async,
+    // no registers held): every 16-byte slot of the tile this CTA will update.
+    template <int BN>
+    __device__ static void prefetch(const Params &p, float *pf, int m0, int n0, int M, int N, int tid, int nth) {
+        if (!vec_ok(p)) return;
+        const bool need_th = p.mode == 2 || p.mode == 3;
+        const bool need_v = need_th && p.momentum != 0.f;
+        const bool need_s = p.mode == 1 || p.mode == 2;
+        constexpr int C4 = BN / 4;
+        for (int e = tid; e < 128 * C4; e += nth) {
+            const int r = e / C4, c = (e % C4) * 4;
+            const int m = m0 + r, n = n0 + c;
+            if (m >= M || n >= N) continue;
+            const int64_t idx = p.base + int64_t(m) * p.dout + n;
+            const int so = r * BN + c;
+            if (need_th) ptx::cp_async16(pf + so, p.theta_cur + idx);
+            if (need_v) ptx::cp_async16(pf + 128 * BN + so, p.vel + idx);
+            if (need_s) ptx::cp_async16(pf + 2 * 128 * BN + so, p.s_in + idx);
+        }
+    }
     struct State {};
     __device__ static void begin(const Params &, int, State &) {}
     __device__ static void apply(const Params &, int, int, const float (&)[32], int, int, State &) {}
@@ -259,11 +292,10 @@ struct EpiWgrad {
     // 16-byte chunks of a parameter row; U slots per thread are loaded before
     // any is consumed (memory-level parallelism for the peer / HBM reads).
     template <int BN>
-    __device__ static void tile(const Params &p, const float *st, int lds, int m0, int n0, int M, int N, int tid,
-                                int nth) {
+    __device__ static void tile(const Params &p, const float *st, int lds, const float *pf, int m0, int n0, int M,
+                                int N, int tid, int nth) {
         bool bad_g = false, bad_u = false;
-        const bool vec = (p.dout % 4 == 0) && (p.base % 4 == 0);
-        if (vec) {
+        if (vec_ok(p)) {
             constexpr int C4 = BN / 4;
             constexpr int U = 4;
             const float lr = *p.lr;
@@ -283,10 +315,11 @@ struct EpiWgrad {
                     idx[u] = p.base + int64_t(m) * p.dout + n;
                     widx[u] = size_t(m) * p.wc_new.ld + n;
                     g[u] = *reinterpret_cast<const float4 *>(st + r * lds + c);
-                    if (p.mode == 1 || p.mode == 2) s[u] = __ldcg(reinterpret_cast<const float4 *>(p.s_in + idx[u]));
+                    const int so = r * BN + c;  // prefetched operands (shared)
+                    if (p.mode == 1 || p.mode == 2) s[u] = *reinterpret_cast<const float4 *>(pf + 2 * 128 * BN + so);
                     if (p.mode == 2 || p.mode == 3) {
-                        th[u] = *reinterpret_cast<const float4 *>(p.theta_cur + idx[u]);
-                        if (p.momentum != 0.f) vv[u] = *reinterpret_cast<const float4 *>(p.vel + idx[u]);
+                        th[u] = *reinterpret_cast<const float4 *>(pf + so);
+                        if (p.momentum != 0.f) vv[u] = *reinterpret_cast<const float4 *>(pf + 128 * BN + so);
                     }
                 }
 #pragma unroll
@@ -377,8 +410,9 @@ struct EpiWgrad {
     //         about to overwrite it), and (updater) until every reader pulled
     //         the version this update overwrites;
     //   post: the last CTA publishes ready / consumed / updated.
+    // called by the 128 epilogue threads (named barrier 1)
     __device__ static void pre(const Params &p, int tid) {
-        if (!p.sync.enabled) return;
+        if (!p.sync.enabled || p.mode == 3) return;
         if (tid == 0) {
             const uint32_t t = uint32_t(*p.sync.step), j = p.stage - 1;
             uint32_t *err = &p.sync.own->err;
@@ -386,14 +420,16 @@ struct EpiWgrad {
             if (p.mode == 0 || p.mode == 1) spin_ge(&p.sync.own->consumed[j], t - 1, err);
             if (p.mode == 2 && t >= 3) spin_ge(&p.sync.own->pulled[j][(t + 1) & 1], p.sync.n_readers, err);
         }
-        __syncthreads();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
     }
     __device__ static void post(const Params &p, int tid, unsigned n_ctas) {
-        if (!p.sync.enabled) return;
+        if (!p.sync.enabled || p.mode == 3) return;  // a single worker publishes nothing
         __syncthreads();
         if (tid == 0) {
             const uint32_t t = uint32_t(*p.sync.step), j = p.stage - 1;
-            __threadfence_system();
+            // gpu-scope fence orders this CTA's stores before its arrival; the last
+            // CTA's system-scope release is cumulative over everything it observed
+            __threadfence();
             if (atomicAdd(&p.sync.cta_counter[j], 1u) == n_ctas - 1) {
                 p.sync.cta_counter[j] = 0;
                 __threadfence_system();
@@ -407,14 +443,7 @@ struct EpiWgrad {
         }
     }
 
-    // bias part of the stage, by CTA (0,0)
-    __device__ static void extra(const Params &p, int tid, int nth) {
-        bool bg = false, bu = false;
-        const int64_t b0 = p.base + int64_t(p.din) * p.dout;
-        for (int o = tid; o < p.dout; o += nth) hop_elem<KIND>(p, b0 + o, p.db[o], 0, false, bg, bu);
-        if (bg) atomicOr(p.grad_flags, 1u << (p.stage - 1));
-        if (bu) atomicOr(p.upd_flags, 1u << (p.stage - 1));
-    }
+    __device__ static void extra(const Params &, int, int) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -422,7 +451,7 @@ struct EpiWgrad {
 // One CTA; thread s handles sample s; the loss is reduced in ascending s.
 template <int KIND>
 __global__ void loss_kernel(const float *__restrict__ z, int B, int dout, int loss_kind, const int *perm,
-                            const int *labels, const float *targets, CTensor dz, float *db, double *loss_out,
+                            const int *labels, const float *targets, CTensor dz, double *loss_out,
                             unsigned *loss_flag) {
     // shared: per-sample loss [blockDim] doubles, then dz [B][dout] floats
     extern __shared__ double sh_loss[];
@@ -464,16 +493,11 @@ __global__ void loss_kernel(const float *__restrict__ z, int B, int dout, int lo
         *loss_out = acc;
         if (!isfinite(acc)) atomicOr(loss_flag, 1u);
     }
-    // bias gradient of the last stage, ascending s (ref _kernels.pyx:115-119)
-    for (int o = threadIdx.x; o < dout; o += blockDim.x) {
-        float acc = 0.f;
-        for (int k = 0; k < B; ++k) acc = __fadd_rn(acc, sdz[k * dout + o]);
-        db[o] = acc;
-    }
 }
 
 // Gather micro-batch rows of the device-resident dataset into a stage-1
-// input record (compute format).
+// input record (compute format); column din keeps the constant 1 of the
+// bias-folding ones column (written once at allocation).
 template <int KIND>
 __global__ void gather_kernel(const float *__restrict__ data, int din, const int *perm, CTensor out) {
     ptx::griddep_wait();
@@ -503,11 +527,11 @@ __global__ void pull_stage_kernel(const float *__restrict__ src, float *dst, int
         go = 1;
     }
     __syncthreads();
-    const int64_t nw = int64_t(din) * dout, n = nw + dout;
+    const int64_t n = int64_t(din + 1) * dout;  // [W; b]
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const float x = __ldcv(src + i);  // peer memory: bypass stale cached copies
         dst[i] = x;
-        if (i < nw) Fmt<KIND>::store(wc.hi, wc.lo, size_t(i / dout) * wc.ld + i % dout, x);
+        Fmt<KIND>::store(wc.hi, wc.lo, size_t(i / dout) * wc.ld + i % dout, x);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -519,14 +543,23 @@ __global__ void pull_stage_kernel(const float *__restrict__ src, float *dst, int
     }
 }
 
-// Pack master fp32 W (reference layout [din][dout]) into a compute copy [din][ld].
+// Pack a master fp32 stage ([W; b] = [din+1][dout]) into its compute copy [din+1][ld].
 template <int KIND>
 __global__ void pack_w_kernel(const float *__restrict__ w, int din, int dout, CTensor out) {
-    const size_t n = size_t(din) * dout;
+    const size_t n = size_t(din + 1) * dout;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
         const size_t k = i / dout, o = i % dout;
         Fmt<KIND>::store(out.hi, out.lo, k * out.ld + o, w[i]);
     }
 }
 
+}  // namespace cdp
+
+namespace cdp {
+// Set column `col` of a [rows][ld] compute-format record to 1 (the ones column).
+template <int KIND>
+__global__ void ones_column_kernel(CTensor t, int rows, int col) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+        Fmt<KIND>::store(t.hi, t.lo, size_t(r) * t.ld + col, 1.f);
+}
 }  // namespace cdp

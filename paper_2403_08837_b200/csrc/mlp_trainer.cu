@@ -126,10 +126,11 @@ struct MlpTrainer {
     std::vector<std::vector<CBuf>> rec;       // [stage][slot]
     DevBuf loss_all;  // [W] per-worker micro-batch losses (double)
     struct Worker {
-        DevBuf z, db, ws, counters;
+        DevBuf z, ws, counters;
         double *loss = nullptr;
-        CBuf dz[2];
-        cudaStream_t stream = nullptr;
+        std::vector<CBuf> dz;  // per layer: dZ_l [B][dout_l] (written once per step)
+        cudaStream_t stream = nullptr;   // compute chain: pulls, forward, loss, data gradients
+        cudaStream_t hstream = nullptr;  // gradient hops: weight-grad GEMMs + fused hop / update
     };
     std::vector<Worker> wk;
     DevBuf data_x, data_lab, data_tgt;
@@ -146,7 +147,7 @@ struct MlpTrainer {
     size_t ws_floats = 0;
 
     cudaStream_t main = nullptr;
-    std::vector<cudaEvent_t> op_events;
+    std::vector<cudaEvent_t> op_events, hop_events, loss_events;
     cudaEvent_t fork_ev = nullptr;
     std::vector<cudaEvent_t> join_ev;
     cudaGraphExec_t exec[2] = {nullptr, nullptr};
@@ -160,10 +161,14 @@ struct MlpTrainer {
         for (auto &e : exec)
             if (e) cudaGraphExecDestroy(e);
         for (auto e : op_events) cudaEventDestroy(e);
+        for (auto e : hop_events) cudaEventDestroy(e);
+        for (auto e : loss_events) cudaEventDestroy(e);
         for (auto e : join_ev) cudaEventDestroy(e);
         if (fork_ev) cudaEventDestroy(fork_ev);
-        for (auto &w : wk)
+        for (auto &w : wk) {
             if (w.stream) cudaStreamDestroy(w.stream);
+            if (w.hstream) cudaStreamDestroy(w.hstream);
+        }
         if (main) cudaStreamDestroy(main);
         for (auto e : stage_ev)
             if (e) cudaEventDestroy(e);
@@ -172,11 +177,10 @@ struct MlpTrainer {
     }
 
     // ---------------------------------------------------------------- GEMM sizing
-    int bn_rows(int rows) const { return std::min(256, round_up(rows, 32)); }
+    int bn_rows(int) const { return 32; }  // narrow N tiles: more CTAs for the latency-bound small GEMMs
     int bn_mn(int n) const {  // MN-major B tile width
         const int ch = kind == 0 ? 64 : 32;
-        int target = n >= 1024 ? 256 : n >= 256 ? 64 : n;
-        return std::min(256, round_up(std::max(target, ch), ch));
+        return std::min(256, round_up(std::max(std::min(n, 64), ch), ch));
     }
     int splits_for(int M, int N, int BN, int K, bool allow_split = true) const {
         if (!allow_split) return 1;
@@ -213,7 +217,7 @@ struct MlpTrainer {
         }
         P = off;
         for (int v = 0; v < 2; ++v) {
-            for (int j = 0; j < S; ++j) wc[v].push_back(make_cbuf(kind, st[j].din, st[j].dout));
+            for (int j = 0; j < S; ++j) wc[v].push_back(make_cbuf(kind, st[j].din + 1, st[j].dout));
         }
         if (momentum != 0.f) vel = DevBuf(size_t(P) * 4);
         region_theta_off = (sizeof(RingFlags) + 255) / 256 * 256;
@@ -226,10 +230,17 @@ struct MlpTrainer {
         cta_counters = DevBuf(2 * kMaxStages * 4);
         rec.resize(S);
         for (int j = 0; j < S; ++j)
-            for (int r = 0; r < std::max(1, slots[j + 1]); ++r) rec[j].push_back(make_cbuf(kind, B, st[j].din));
+            for (int r = 0; r < std::max(1, slots[j + 1]); ++r) {
+                rec[j].push_back(make_cbuf(kind, B, st[j].din + 1));
+                if (kind == 0)
+                    ones_column_kernel<0><<<1, 256>>>(rec[j].back().view(), B, st[j].din);
+                else
+                    ones_column_kernel<1><<<1, 256>>>(rec[j].back().view(), B, st[j].din);
+                CDP_CUDA(cudaGetLastError());
+            }
         // split-K workspace: the largest need of any GEMM a worker runs
         for (int j = 0; j < S; ++j) {
-            ws_floats = std::max(ws_floats, ws_need(st[j].dout, B, bn_rows(B), st[j].din));
+            ws_floats = std::max(ws_floats, ws_need(st[j].dout, B, bn_rows(B), st[j].din + 1));
             ws_floats = std::max(ws_floats, ws_need(st[j].din, B, bn_rows(B), st[j].dout));
         }
         wk.resize(W);
@@ -237,11 +248,11 @@ struct MlpTrainer {
         for (int i = 0; i < W; ++i) wk[i].loss = loss_all.as<double>() + i;
         for (auto &w : wk) {
             w.z = DevBuf(size_t(B) * st[S - 1].dout * 4);
-            w.db = DevBuf(size_t(S) * dmax * 4);
             w.ws = DevBuf(std::max<size_t>(ws_floats, 1) * 4);
             w.counters = DevBuf(4096 * 4);
-            for (int b = 0; b < 2; ++b) w.dz[b] = make_cbuf(kind, B, dmax);
+            for (int j = 0; j < S; ++j) w.dz.push_back(make_cbuf(kind, B, st[j].dout));
             CDP_CUDA(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+            CDP_CUDA(cudaStreamCreateWithFlags(&w.hstream, cudaStreamNonBlocking));
         }
         CDP_CUDA(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
         ctrl_dev = DevBuf(sizeof(Control));
@@ -297,7 +308,7 @@ struct MlpTrainer {
         GemmPlan p;
 #define CDP_GEMM_BN(BN_)                                                                                            \
     case BN_:                                                                                                       \
-        if constexpr (!BMN || BN_ % (K == 0 ? 64 : 32) == 0) {                                                      \
+        if constexpr ((!BMN || BN_ % (K == 0 ? 64 : 32) == 0) && (!Epi::kTile || BN_ <= 64)) {                    \
             p = plan_gemm<K, BN_, AMN, BMN>(A, Bo, nseg, M, N, Kd, splits, w.ws.as<float>(), w.counters.as<int>()); \
             CDP_REQUIRE(gemm_ws_floats(p, BN_) <= ws_floats, "split-K workspace too small");                      \
             launch_gemm<K, BN_, AMN, BMN, Epi>(p, ep, s);                                                          \
@@ -328,24 +339,24 @@ struct MlpTrainer {
             ++kernels_per_step;
         }
         Operand A[3], Bo[3];
-        const int nseg = segments<K>(wc[vslot][j], true, g.dout, g.din, rec[j][rin], false, B, g.din, A, Bo);
+        // z = [h, 1] . [W; b]: K = din + 1 folds the bias into the product
+        const int nseg =
+            segments<K>(wc[vslot][j], true, g.dout, g.din + 1, rec[j][rin], false, B, g.din + 1, A, Bo);
         typename EpiFwd<K>::Params ep{};
-        ep.bias = theta[vslot] + g.base + int64_t(g.din) * g.dout;
         ep.last = j == S - 1;
         if (ep.last)
             ep.z = wr.z.as<float>();
         else
             ep.out = rec[j + 1][rout].view();
-        if (launch_mask & 2) gemm<K, true, false, EpiFwd<K>>(bn_rows(B), A, Bo, nseg, g.dout, B, g.din, wr, ep, s);
+        if (launch_mask & 2) gemm<K, true, false, EpiFwd<K>>(bn_rows(B), A, Bo, nseg, g.dout, B, g.din + 1, wr, ep, s);
     }
 
+    // B task, compute half: [loss] then the data gradient dZ_{j-1} (W rows only).
     template <int K>
-    void backward(int w, int j, int vslot, int rin, int hop, int cur_slot, cudaStream_t s, const int *perm_w) {
+    void bwd_compute(int w, int j, int vslot, int rin, cudaStream_t s, const int *perm_w, cudaEvent_t loss_ev) {
         const StageGeom &g = st[j];
         Worker &wr = wk[w];
         Flags *fl = flags_dev.as<Flags>();
-        const int cur = (S - 1 - j) & 1;
-        float *db = wr.db.as<float>();
         if (j == S - 1 && (launch_mask & 1)) {
             const int nt = std::max(32, round_up(B, 32));
             const size_t lsm = sizeof(double) * nt + sizeof(float) * B * g.dout;
@@ -354,17 +365,27 @@ struct MlpTrainer {
                 CDP_CUDA(cudaFuncSetAttribute(loss_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsm)));
             launch_pdl(loss_kernel<K>, dim3(1), dim3(nt), lsm, s, (const float *)wr.z.as<float>(), B,
                        g.dout, loss_kind, perm_w, (const int *)data_lab.as<int>(), (const float *)data_tgt.as<float>(),
-                       wr.dz[cur].view(), db + size_t(j) * dmax, wr.loss, &fl->loss);
+                       wr.dz[j].view(), wr.loss, &fl->loss);
             ++kernels_per_step;
         }
-        Operand A[3], Bo[3];
-        if (j > 0 && (launch_mask & 2)) {  // data gradient into dZ_{j-1} (+ bias grad of stage j-1)
-            const int nseg = segments<K>(wc[vslot][j], false, g.din, g.dout, wr.dz[cur], false, B, g.dout, A, Bo);
-            typename EpiDgrad<K>::Params ep{rec[j][rin].view(), wr.dz[cur ^ 1].view(), db + size_t(j - 1) * dmax};
+        if (loss_ev) CDP_CUDA(cudaEventRecord(loss_ev, s));
+        if (j > 0 && (launch_mask & 2)) {
+            Operand A[3], Bo[3];
+            const int nseg = segments<K>(wc[vslot][j], false, g.din, g.dout, wr.dz[j], false, B, g.dout, A, Bo);
+            typename EpiDgrad<K>::Params ep{rec[j][rin].view(), wr.dz[j - 1].view()};
             gemm<K, false, false, EpiDgrad<K>>(bn_rows(B), A, Bo, nseg, g.din, B, g.dout, wr, ep, s);
         }
-        // weight gradient fused with the ring hop / update
-        const int nseg = segments<K>(rec[j][rin], true, g.din, B, wr.dz[cur], true, g.dout, B, A, Bo);
+    }
+
+    // B task, hop half: [W; b] gradient ([h, 1]^T . dZ, M = din + 1) fused with
+    // the ring hop / update.
+    template <int K>
+    void bwd_hop(int w, int j, int rin, int hop, int cur_slot, cudaStream_t s) {
+        const StageGeom &g = st[j];
+        Worker &wr = wk[w];
+        Flags *fl = flags_dev.as<Flags>();
+        Operand A[3], Bo[3];
+        const int nseg = segments<K>(rec[j][rin], true, g.din + 1, B, wr.dz[j], true, g.dout, B, A, Bo);
         HopParams hp{};
         hp.mode = hop;
         hp.stage = j + 1;
@@ -389,10 +410,17 @@ struct MlpTrainer {
         hp.wd = wd;
         hp.n_mb = float(rank >= 0 ? world : W);
         hp.wc_new = wc[cur_slot ^ 1][j].view();
-        hp.db = db + size_t(j) * dmax;
         hp.grad_flags = &fl->grad;
         hp.upd_flags = &fl->upd;
-        if (launch_mask & 4) gemm<K, true, true, EpiWgrad<K>>(bn_mn(g.dout), A, Bo, nseg, g.din, g.dout, B, wr, hp, s);
+        if (launch_mask & 4)
+            gemm<K, true, true, EpiWgrad<K>>(bn_mn(g.dout), A, Bo, nseg, g.din + 1, g.dout, B, wr, hp, s);
+    }
+
+    // Both halves on one stream (operator-level timing helper).
+    template <int K>
+    void backward(int w, int j, int vslot, int rin, int hop, int cur_slot, cudaStream_t s, const int *perm_w) {
+        bwd_compute<K>(w, j, vslot, rin, s, perm_w, nullptr);
+        bwd_hop<K>(w, j, rin, hop, cur_slot, s);
     }
 
     // theta delivery on reader ranks (see pull_stage_kernel)
@@ -409,31 +437,57 @@ struct MlpTrainer {
     }
 
     // ---------------------------------------------------------------- capture
+    // Capture one training step.  Per worker two streams: the compute chain
+    // (pull, F, loss, dgrad) and the hop stream (wgrad + fused hop / update),
+    // so each layer's gradient hop overlaps the data-gradient chain below it.
+    // Edges: hop(l) <- dZ_l ready; hop(l) <- dgrad(l) when the read was stale
+    // (the update overwrites exactly that slot); ring B(i-1,l) -> B(i,l) on the
+    // hop streams; slot reuse B -> producer F waits for both halves.
     template <int K>
     void record_step(int p) {
         kernels_per_step = 0;
         CDP_CUDA(cudaEventRecord(fork_ev, main));
-        for (auto &w : wk) CDP_CUDA(cudaStreamWaitEvent(w.stream, fork_ev, 0));
+        for (auto &w : wk) {
+            CDP_CUDA(cudaStreamWaitEvent(w.stream, fork_ev, 0));
+            CDP_CUDA(cudaStreamWaitEvent(w.hstream, fork_ev, 0));
+        }
         std::vector<std::vector<int>> into(ops.size());
         for (auto &d : deps) into[d.second].push_back(d.first);
+        std::vector<std::vector<cudaEvent_t>> dz_ready(W, std::vector<cudaEvent_t>(S, nullptr));
         for (size_t o = 0; o < ops.size(); ++o) {
             const auto &op = ops[o];
             const int w = rank >= 0 ? 0 : op[OP_WORKER] - 1, j = op[OP_STAGE] - 1;
-            cudaStream_t s = wk[w].stream;
-            for (int d : into[o]) CDP_CUDA(cudaStreamWaitEvent(s, op_events[d], 0));
+            cudaStream_t s = wk[w].stream, hs = wk[w].hstream;
             const int vslot = op[OP_FRESH] ? p : (p ^ 1);
             const int *perm_w = perm_dev.as<int>() + size_t(w) * B;
-            if (op[OP_KIND] == 2)
-                pull<K>(j, vslot, op[OP_FRESH], s);
-            else if (op[OP_KIND] == 0)
-                forward<K>(w, j, vslot, op[OP_REC_IN], op[OP_REC_OUT], s, perm_w);
-            else
-                backward<K>(w, j, vslot, op[OP_REC_IN], op[OP_HOP], p, s, perm_w);
+            if (op[OP_KIND] != 1) {
+                for (int d : into[o]) {  // producer of a reused record slot: both halves of the releasing B
+                    CDP_CUDA(cudaStreamWaitEvent(s, op_events[d], 0));
+                    if (ops[d][OP_KIND] == 1) CDP_CUDA(cudaStreamWaitEvent(s, hop_events[d], 0));
+                }
+                if (op[OP_KIND] == 2)
+                    pull<K>(j, vslot, op[OP_FRESH], s);
+                else
+                    forward<K>(w, j, vslot, op[OP_REC_IN], op[OP_REC_OUT], s, perm_w);
+                CDP_CUDA(cudaEventRecord(op_events[o], s));
+                continue;
+            }
+            bwd_compute<K>(w, j, vslot, op[OP_REC_IN], s, perm_w, j == S - 1 ? loss_events[o] : nullptr);
             CDP_CUDA(cudaEventRecord(op_events[o], s));
+            if (j == S - 1) dz_ready[w][j] = loss_events[o];
+            if (j > 0) dz_ready[w][j - 1] = op_events[o];
+            CDP_REQUIRE(dz_ready[w][j] != nullptr, "plan runs a backward before the one producing its dZ");
+            CDP_CUDA(cudaStreamWaitEvent(hs, dz_ready[w][j], 0));
+            if (!op[OP_FRESH]) CDP_CUDA(cudaStreamWaitEvent(hs, op_events[o], 0));
+            for (int d : into[o]) CDP_CUDA(cudaStreamWaitEvent(hs, ops[d][OP_KIND] == 1 ? hop_events[d] : op_events[d], 0));
+            bwd_hop<K>(w, j, op[OP_REC_IN], op[OP_HOP], p, hs);
+            CDP_CUDA(cudaEventRecord(hop_events[o], hs));
         }
         for (int w = 0; w < W; ++w) {
-            CDP_CUDA(cudaEventRecord(join_ev[w], wk[w].stream));
-            CDP_CUDA(cudaStreamWaitEvent(main, join_ev[w], 0));
+            CDP_CUDA(cudaEventRecord(join_ev[2 * w], wk[w].stream));
+            CDP_CUDA(cudaStreamWaitEvent(main, join_ev[2 * w], 0));
+            CDP_CUDA(cudaEventRecord(join_ev[2 * w + 1], wk[w].hstream));
+            CDP_CUDA(cudaStreamWaitEvent(main, join_ev[2 * w + 1], 0));
         }
         finish_step();
     }
@@ -441,9 +495,11 @@ struct MlpTrainer {
     void finish_step();
 
     void capture() {
-        op_events.resize(ops.size());
-        for (auto &e : op_events) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        join_ev.resize(W);
+        for (auto *v : {&op_events, &hop_events, &loss_events}) {
+            v->resize(ops.size());
+            for (auto &e : *v) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        join_ev.resize(2 * W);
         for (auto &e : join_ev) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CDP_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
         for (int p = 0; p < 2; ++p) {
@@ -457,8 +513,10 @@ struct MlpTrainer {
             } catch (...) {
                 // join the forked worker streams so the capture can be closed cleanly
                 for (int w = 0; w < W; ++w) {
-                    cudaEventRecord(join_ev[w], wk[w].stream);
-                    cudaStreamWaitEvent(main, join_ev[w], 0);
+                    cudaEventRecord(join_ev[2 * w], wk[w].stream);
+                    cudaStreamWaitEvent(main, join_ev[2 * w], 0);
+                    cudaEventRecord(join_ev[2 * w + 1], wk[w].hstream);
+                    cudaStreamWaitEvent(main, join_ev[2 * w + 1], 0);
                 }
                 if (cudaStreamEndCapture(main, &g) == cudaSuccess && g) cudaGraphDestroy(g);
                 cudaGetLastError();

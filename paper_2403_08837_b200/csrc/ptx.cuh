@@ -138,6 +138,13 @@ __host__ __device__ constexpr uint32_t instr_desc(uint32_t ab_format, bool a_mn,
            ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// ---------------------------------------------------------------- cp.async (LDGSTS) prefetch
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---------------------------------------------------------------- programmatic dependent launch
 // wait: block until the preceding grid in the stream has completed and its
 // memory is visible; launch_dependents: let the next grid start its prologue.
