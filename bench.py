@@ -279,7 +279,7 @@ def run_ours(args, ws, rank, local):
     tp = os.path.join(ROOT, "profiles", "round1_wgrad_hop_traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
-            traffic = json.load(fh).get(f"{args.dtype}-{mode}")
+            traffic = (json.load(fh).get(f"{args.dtype}-{mode}") or {}).get("dram_bytes_per_launch")
 
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
