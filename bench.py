@@ -201,16 +201,33 @@ def run_ours(args, ws, rank, local):
     from paper_2403_08837_b200.executor import layer_stages
 
     task = make_deep_task(ws)
-    rule = resolve(args.rule, ws)
+    allreduce = args.rule == "dp-allreduce"
+    rule = None if allreduce else resolve(args.rule, ws)
     ls = layer_stages(len(DEEP_DIMS) - 1, ws)
     tr = DeviceMlpTrainer.for_rank(DEEP_DIMS, MB, ws, rank, 1, rule, dtype=args.dtype, momentum=MOMENTUM,
-                                   inputs=task.inputs, targets=task.targets, layer_stage=ls)
+                                   inputs=task.inputs, targets=task.targets, layer_stage=ls, allreduce=allreduce)
     tr.set_params(np.concatenate(task.init_params()), which=-1)
     if ws > 1:
         tr.connect_ipc(exchange_handles(tr.ipc_handle()))
     else:
         tr.connect([tr.region()])
     perms = [task.permutation(t)[rank * MB:(rank + 1) * MB] for t in range(1, args.warmup + args.steps + 2)]
+    if allreduce:  # DP baseline: NCCL all-reduce of the gradient on the trainer stream, then the update
+        ext = torch.cuda.ExternalStream(tr.stream_handle())
+        grad = tr.partial_tensor()
+        plain_step = tr.step
+
+        def dp_reduce_update():
+            if ws > 1:
+                with torch.cuda.stream(ext):
+                    torch.distributed.all_reduce(grad)
+            tr.apply_update()
+
+        def dp_step(perm, lr):
+            plain_step(perm, lr)
+            dp_reduce_update()
+
+        tr.step = dp_step
     for t in range(args.warmup):
         tr.step(perms[t], LR)
     tr.sync()
@@ -249,6 +266,8 @@ def run_ours(args, ws, rank, local):
         tr.flush_l2()
         tr.mark(0)
         tr.step_host_batch_ptr(x_pin.data_ptr(), y_pin.data_ptr(), LR)
+        if allreduce:
+            dp_reduce_update()
         tr.last()
         tr.mark(1)
         if k >= 2:
@@ -263,6 +282,8 @@ def run_ours(args, ws, rank, local):
 
     # ---- roofline: layer-1 weight-grad GEMM with the fused hop (update when N = 1)
     op = tr.op_index(1, rank + 1, 1)
+    if allreduce:
+        mode = "grad"
     kms = []
     for _ in range(20):
         tr.flush_l2()
@@ -270,8 +291,9 @@ def run_ours(args, ws, rank, local):
     k_ms = float(np.median(kms))
     p1 = DEEP_DIMS[0] * DEEP_DIMS[1] + DEEP_DIMS[1]
     esz = 2 if args.dtype == "bf16" else 8
-    mode = "only" if ws == 1 else ("first" if rank == 0 else "last" if rank == ws - 1 else "mid")
-    per_param = {"first": 4, "mid": 8, "last": 20 + esz, "only": 16 + esz}[mode]
+    if not allreduce:
+        mode = "only" if ws == 1 else ("first" if rank == 0 else "last" if rank == ws - 1 else "mid")
+    per_param = {"first": 4, "mid": 8, "last": 20 + esz, "only": 16 + esz, "grad": 4}[mode]
     alg = p1 * per_param + MB * (DEEP_DIMS[0] + DEEP_DIMS[1]) * (2 if args.dtype == "bf16" else 8)
     peak, src = peak_hbm()
     achieved = alg / (k_ms / 1e3) / 1e9
@@ -291,7 +313,7 @@ def run_ours(args, ws, rank, local):
                    "l2": "flushed (256 MiB memset) before every timed step"},
         "e2e": {"value": round(ws * MB / (e2e / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e, 5)},
-        "gpu_launches": stats["kernels_per_step"] * K,
+        "gpu_launches": (stats["kernels_per_step"] + (len(DEEP_DIMS) - 1 if allreduce else 0)) * K,
         "roofline": {"bound": "hbm", "kernel": f"layer-1 wgrad GEMM + fused {mode} hop (gemm_tc_kernel<EpiWgrad>)",
                      "achieved": round(achieved, 1), "peak": peak, "peak_source": src, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "algorithmic_bytes_per_launch": alg,
@@ -344,7 +366,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--rule", default="cdp-v2", choices=["cdp-v2", "cdp-v1", "dp"])
+    ap.add_argument("--rule", default="cdp-v2", choices=["cdp-v2", "cdp-v1", "dp", "dp-allreduce"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     ws, rank, local = dist_env()
@@ -356,7 +378,8 @@ def main():
         from paper_2403_08837_b200.executor import layer_stages
 
         task = make_deep_task(ws)
-        fresh = expanded_fresh(resolve(args.rule, ws), ws, layer_stages(len(DEEP_DIMS) - 1, ws))
+        fresh = expanded_fresh(None if args.rule == "dp-allreduce" else resolve(args.rule, ws), ws,
+                               layer_stages(len(DEEP_DIMS) - 1, ws))
         cores = min(ws, os.cpu_count() or 1)
         n = max(1, min(args.steps, 5))
         sps, ms, kind = cpu_reference(task, fresh, n, 1, cores)

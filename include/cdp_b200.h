@@ -97,6 +97,12 @@ int cdp_ipc_close(void *ptr);
 /* regions[r] = rank r's region base, valid in this process; captures the step graphs. */
 int cdp_trainer_connect(cdp_trainer *tr, void *const *regions);
 int cdp_trainer_ring_error(cdp_trainer *tr, int *err);
+/* DP all-reduce baseline (ref comm.py:70-90): plans whose B ops use hop role 4
+ * leave each rank's own micro-batch gradient in the partial buffer; the host
+ * all-reduces it (NCCL) on the trainer stream, then apply_update runs the SGD
+ * update of the step just run on every replica. */
+int cdp_trainer_partial(cdp_trainer *tr, void **ptr, size_t *n_floats);
+int cdp_trainer_apply_update(cdp_trainer *tr);
 /* which: 0 = current version (theta_t), 1 = previous (theta_{t-1}), -1 = both.
  * Flat fp32 host buffers in the reference layout. */
 int cdp_trainer_set_params(cdp_trainer *tr, int which, const float *theta);

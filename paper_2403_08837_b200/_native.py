@@ -42,6 +42,8 @@ SIGNATURES = {
     "cdp_ipc_close": (c_int, [c_void_p]),
     "cdp_trainer_connect": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_trainer_ring_error": (c_int, [c_void_p, c_int_p]),
+    "cdp_trainer_partial": (c_int, [c_void_p, ctypes.POINTER(c_void_p), ctypes.POINTER(c_size_t)]),
+    "cdp_trainer_apply_update": (c_int, [c_void_p]),
     "cdp_trainer_set_params": (c_int, [c_void_p, c_int, c_float_p]),
     "cdp_trainer_get_params": (c_int, [c_void_p, c_int, c_float_p]),
     "cdp_trainer_set_velocity": (c_int, [c_void_p, c_float_p]),

@@ -412,7 +412,7 @@ struct EpiWgrad {
     //   post: the last CTA publishes ready / consumed / updated.
     // called by the 128 epilogue threads (named barrier 1)
     __device__ static void pre(const Params &p, int tid) {
-        if (!p.sync.enabled || p.mode == 3) return;
+        if (!p.sync.enabled || p.mode >= 3) return;
         if (tid == 0) {
             const uint32_t t = uint32_t(*p.sync.step), j = p.stage - 1;
             uint32_t *err = &p.sync.own->err;
@@ -423,7 +423,7 @@ struct EpiWgrad {
         asm volatile("bar.sync 1, 128;" ::: "memory");
     }
     __device__ static void post(const Params &p, int tid, unsigned n_ctas) {
-        if (!p.sync.enabled || p.mode == 3) return;  // a single worker publishes nothing
+        if (!p.sync.enabled || p.mode >= 3) return;  // single worker / gradient-only publish nothing
         __syncthreads();
         if (tid == 0) {
             const uint32_t t = uint32_t(*p.sync.step), j = p.stage - 1;
@@ -561,5 +561,27 @@ template <int KIND>
 __global__ void ones_column_kernel(CTensor t, int rows, int col) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
         Fmt<KIND>::store(t.hi, t.lo, size_t(r) * t.ld + col, 1.f);
+}
+}  // namespace cdp
+
+namespace cdp {
+// DP all-reduce baseline (ref comm.py:70-90): after the collective has summed
+// every rank's gradient into S, each replica applies the same update.
+template <int KIND>
+__global__ void update_from_sum_kernel(HopParams p) {
+    ptx::griddep_wait();
+    const int64_t n = int64_t(p.din + 1) * p.dout;
+    const float lr = *p.lr;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t idx = p.base + i;
+        float v = p.momentum != 0.f ? p.vel[idx] : 0.f;
+        const float nt = sgd_update(p, p.s_in[idx], p.theta_cur[idx], v, lr);
+        if (p.momentum != 0.f) p.vel[idx] = v;
+        if (!isfinite(nt)) bad = true;
+        p.theta_new[idx] = nt;
+        Fmt<KIND>::store(p.wc_new.hi, p.wc_new.lo, size_t(i / p.dout) * p.wc_new.ld + i % p.dout, nt);
+    }
+    if (bad) atomicOr(p.upd_flags, 1u << (p.stage - 1));
 }
 }  // namespace cdp

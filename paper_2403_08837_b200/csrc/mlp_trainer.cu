@@ -528,6 +528,39 @@ struct MlpTrainer {
         }
     }
 
+    // DP all-reduce baseline: apply the update of the step just run from the
+    // (collective-summed) partial buffer, every layer, on the trainer stream.
+    void apply_update() {
+        CDP_REQUIRE(t >= 2, "no step has run");
+        const int p = (t - 1) & 1;
+        Flags *fl = flags_dev.as<Flags>();
+        for (int j = 0; j < S; ++j) {
+            const StageGeom &g = st[j];
+            HopParams hp{};
+            hp.mode = 3;
+            hp.stage = j + 1;
+            hp.base = g.base;
+            hp.din = g.din;
+            hp.dout = g.dout;
+            hp.s_in = partial;
+            hp.theta_cur = theta[p];
+            hp.theta_new = theta[p ^ 1];
+            hp.vel = vel.as<float>();
+            hp.lr = &ctrl_dev.as<Control>()->lr;
+            hp.momentum = momentum;
+            hp.wd = wd;
+            hp.n_mb = float(rank >= 0 ? world : W);
+            hp.wc_new = wc[p ^ 1][j].view();
+            hp.upd_flags = &fl->upd;
+            const int64_t n = int64_t(g.din + 1) * g.dout;
+            const int blocks = int(std::min<int64_t>(4 * 148, (n + 255) / 256));
+            if (kind == 0)
+                launch_pdl(update_from_sum_kernel<0>, dim3(blocks), dim3(256), 0, main, hp);
+            else
+                launch_pdl(update_from_sum_kernel<1>, dim3(blocks), dim3(256), 0, main, hp);
+        }
+    }
+
     // ---------------------------------------------------------------- params
     void pack_all(int slot) {
         for (int j = 0; j < S; ++j) {
@@ -1001,4 +1034,15 @@ extern "C" int cdp_trainer_elapsed(cdp_trainer *tr, int a, int b, float *ms) {
 
 extern "C" int cdp_trainer_flush_l2(cdp_trainer *tr) {
     return guarded([&] { tr->impl->flush_l2(); });
+}
+
+extern "C" int cdp_trainer_partial(cdp_trainer *tr, void **ptr, size_t *n_floats) {
+    return guarded([&] {
+        *ptr = tr->impl->partial;
+        *n_floats = size_t(tr->impl->P);
+    });
+}
+
+extern "C" int cdp_trainer_apply_update(cdp_trainer *tr) {
+    return guarded([&] { tr->impl->apply_update(); });
 }

@@ -76,7 +76,7 @@ class DeviceMlpTrainer:
     def for_rank(cls, dims, micro_batch: int, world: int, rank: int, loss_kind: int, rule: UpdateRule | None,
                  dtype: str = "fp32", momentum: float = 0.0, weight_decay: float = 0.0,
                  inputs: np.ndarray | None = None, targets: np.ndarray | None = None,
-                 layer_stage=None) -> "DeviceMlpTrainer":
+                 layer_stage=None, allreduce: bool = False) -> "DeviceMlpTrainer":
         """One rank of multi-GPU CDP (worker rank+1 on this process's GPU); call connect_* next."""
         self = cls.__new__(cls)
         self.lib = N.lib()
@@ -89,7 +89,7 @@ class DeviceMlpTrainer:
         self.rank, self.world = rank, world
         self.sizes = [self.dims[j] * self.dims[j + 1] + self.dims[j + 1] for j in range(self.n_layers)]
         self.P = sum(self.sizes)
-        self.rank_ops = compile_rank_plan(world, rank, rule, layer_stage)
+        self.rank_ops = compile_rank_plan(world, rank, rule, layer_stage, allreduce=allreduce)
         self.plan = None
         dims_a = np.asarray(self.dims, dtype=np.int64)
         x = lab = tgt = None
@@ -140,6 +140,22 @@ class DeviceMlpTrainer:
             self._opened.append(ptr.value)
             regions.append(ptr.value)
         self.connect(regions)
+
+    def partial_tensor(self):
+        """torch view (no copy) of the partial-sum buffer, for the NCCL all-reduce baseline."""
+        import torch
+
+        ptr, n = ctypes.c_void_p(), ctypes.c_size_t()
+        N.check(self.lib.cdp_trainer_partial(self.h, ctypes.byref(ptr), ctypes.byref(n)))
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n.value,), "typestr": "<f4", "data": (ptr.value, False),
+                                        "version": 3}
+
+        return torch.as_tensor(_View(), device="cuda")
+
+    def apply_update(self):
+        N.check(self.lib.cdp_trainer_apply_update(self.h))
 
     def ring_error(self) -> int:
         e = ctypes.c_int()

@@ -179,7 +179,8 @@ def record_bytes(plan: StepPlan, dims, micro_batch: int, elem_bytes: int) -> int
                    for l in range(1, len(plan.slots))))
 
 
-def compile_rank_plan(n_workers: int, rank: int, rule: UpdateRule | None = None, layer_stage=None) -> np.ndarray:
+def compile_rank_plan(n_workers: int, rank: int, rule: UpdateRule | None = None, layer_stage=None,
+                      allreduce: bool = False) -> np.ndarray:
     """Op list of one rank in multi-GPU CDP / DP (worker i = rank + 1 on its own GPU).
 
     Per step: [pull(j)] F(i, j) for j = 1..N, then B(i, j) for j = N..1.  The
@@ -206,9 +207,13 @@ def compile_rank_plan(n_workers: int, rank: int, rule: UpdateRule | None = None,
         rule.check_feasible()
     fresh = (lambda l: 1) if rule is None else (lambda l: int(rule.reads_fresh(i, layer_stage[l - 1])))
     hop = HOP_ONLY if n == 1 else HOP_FIRST if i == 1 else HOP_LAST if i == n else HOP_MID
+    if allreduce:  # DP baseline: own gradient only; the collective + update run after the step
+        if rule is not None:
+            raise ValueError("the all-reduce baseline is synchronous DP (rule None)")
+        hop = HOP_GRAD
     ops = []
     for l in range(1, n_layers + 1):
-        if i != n:
+        if i != n and not allreduce:
             ops.append([OP_PULL, i, l, fresh(l), 0, 0, 0, 0])
         ops.append([OP_F, i, l, fresh(l), 0, 0, 0, 0])
     for l in range(n_layers, 0, -1):

@@ -143,3 +143,44 @@ def test_grouped_layers_ranks_vs_oracle(cuda, n):
         prev, cur = cur, new
     want = np.concatenate(cur)
     assert np.linalg.norm(multi - want) / np.linalg.norm(want) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_dp_allreduce_baseline_matches_single_gpu_dp(cuda, n):
+    """DP all-reduce baseline (ref comm.py:70-90): every rank computes its micro-batch
+    gradient (hop role 4), the sum is reduced (here in rank order on one device, as the
+    ring does), every replica applies the update -> bit-identical to single-GPU DP."""
+    import torch
+    from paper_2403_08837_b200.device import DeviceMlpTrainer
+    from paper_2403_08837_b200.training import make_mlp_task
+
+    task = make_mlp_task(n=n, micro_batch_size=8, seed=4, width=64, in_dim=96, out_dim=10, loss_kind="xent")
+    ranks = [DeviceMlpTrainer.for_rank(task.model.dims, 8, n, r, 1, None, dtype="bf16", momentum=0.9,
+                                       inputs=task.inputs, targets=task.targets, allreduce=True) for r in range(n)]
+    regions = [t.region() for t in ranks]
+    init = np.concatenate(task.init_params())
+    for t in ranks:
+        t.set_params(init, -1)
+        t.connect(regions)
+    views = [t.partial_tensor() for t in ranks]
+    for step in range(1, 6):
+        perm = task.permutation(step)
+        for r, t in enumerate(ranks):
+            t.step(perm[r * 8:(r + 1) * 8], 0.05)
+        for t in ranks:
+            t.sync()
+        total = views[0].clone()
+        for v in views[1:]:
+            total += v
+        torch.cuda.synchronize()
+        for t, v in zip(ranks, views):
+            v.copy_(total)
+            torch.cuda.synchronize()
+            t.apply_update()
+    finals = [t.get_params(0) for t in ranks]
+    for t in ranks:
+        t.close()
+    single = _run_single(task, "dp", 5, "bf16", 0.9)[1]
+    for f in finals:
+        assert np.array_equal(f, finals[0])
+    assert np.array_equal(finals[0], single)
