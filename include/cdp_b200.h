@@ -135,6 +135,11 @@ int cdp_trainer_time_op(cdp_trainer *tr, int op, int mask, int iters, float *ms)
 int cdp_trainer_mark(cdp_trainer *tr, int k);
 int cdp_trainer_elapsed(cdp_trainer *tr, int a, int b, float *ms);
 int cdp_trainer_flush_l2(cdp_trainer *tr);
+/* Trace mode (re-captures the step graphs): %globaltimer stamps around every
+ * op; cdp_trainer_trace returns [n_ops][4] u64 = compute start, compute end,
+ * hop start, hop end (0 for ops without a hop half) of the last step. */
+int cdp_trainer_set_trace(cdp_trainer *tr, int on);
+int cdp_trainer_trace(cdp_trainer *tr, uint64_t *out, int n_ops);
 /* The cudaStream_t the step graphs are launched on. */
 int cdp_trainer_stream(cdp_trainer *tr, void **stream);
 

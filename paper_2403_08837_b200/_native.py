@@ -59,6 +59,8 @@ SIGNATURES = {
     "cdp_trainer_mark": (c_int, [c_void_p, c_int]),
     "cdp_trainer_elapsed": (c_int, [c_void_p, c_int, c_int, c_float_p]),
     "cdp_trainer_flush_l2": (c_int, [c_void_p]),
+    "cdp_trainer_set_trace": (c_int, [c_void_p, c_int]),
+    "cdp_trainer_trace": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_uint64), c_int]),
     "cdp_trainer_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_test_gemm": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p), c_int,
                               ctypes.POINTER(c_void_p), c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),

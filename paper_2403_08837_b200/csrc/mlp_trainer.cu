@@ -92,6 +92,12 @@ struct Flags {
     unsigned grad, loss, upd, pad;
 };
 
+__global__ void stamp_kernel(uint64_t *out) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *out = t;
+}
+
 // -------------------------------------------------------------------------
 struct MlpTrainer {
     int kind = 0;  // 0 bf16, 1 fp32 (3xTF32)
@@ -154,6 +160,8 @@ struct MlpTrainer {
     int t = 1;  // training step of the next launch; current version = t
     int kernels_per_step = 0;
     int launch_mask = 7;  // bit0 gather/loss, bit1 fwd/dgrad GEMM, bit2 wgrad(+hop) GEMM
+    bool trace = false;   // stamp %globaltimer around every op (executed-schedule export)
+    DevBuf trace_buf;     // [n_ops][4] u64: compute start, compute end, hop start, hop end
     std::vector<cudaEvent_t> marks;
     DevBuf flush_buf;
 
@@ -454,6 +462,13 @@ struct MlpTrainer {
         std::vector<std::vector<int>> into(ops.size());
         for (auto &d : deps) into[d.second].push_back(d.first);
         std::vector<std::vector<cudaEvent_t>> dz_ready(W, std::vector<cudaEvent_t>(S, nullptr));
+        uint64_t *tb = trace_buf.as<uint64_t>();
+        auto stamp = [&](cudaStream_t st, int o, int k) {
+            if (trace) {
+                stamp_kernel<<<1, 1, 0, st>>>(tb + 4 * o + k);
+                CDP_CUDA(cudaGetLastError());
+            }
+        };
         for (size_t o = 0; o < ops.size(); ++o) {
             const auto &op = ops[o];
             const int w = rank >= 0 ? 0 : op[OP_WORKER] - 1, j = op[OP_STAGE] - 1;
@@ -465,14 +480,18 @@ struct MlpTrainer {
                     CDP_CUDA(cudaStreamWaitEvent(s, op_events[d], 0));
                     if (ops[d][OP_KIND] == 1) CDP_CUDA(cudaStreamWaitEvent(s, hop_events[d], 0));
                 }
+                stamp(s, int(o), 0);
                 if (op[OP_KIND] == 2)
                     pull<K>(j, vslot, op[OP_FRESH], s);
                 else
                     forward<K>(w, j, vslot, op[OP_REC_IN], op[OP_REC_OUT], s, perm_w);
+                stamp(s, int(o), 1);
                 CDP_CUDA(cudaEventRecord(op_events[o], s));
                 continue;
             }
+            stamp(s, int(o), 0);
             bwd_compute<K>(w, j, vslot, op[OP_REC_IN], s, perm_w, j == S - 1 ? loss_events[o] : nullptr);
+            stamp(s, int(o), 1);
             CDP_CUDA(cudaEventRecord(op_events[o], s));
             if (j == S - 1) dz_ready[w][j] = loss_events[o];
             if (j > 0) dz_ready[w][j - 1] = op_events[o];
@@ -480,7 +499,9 @@ struct MlpTrainer {
             CDP_CUDA(cudaStreamWaitEvent(hs, dz_ready[w][j], 0));
             if (!op[OP_FRESH]) CDP_CUDA(cudaStreamWaitEvent(hs, op_events[o], 0));
             for (int d : into[o]) CDP_CUDA(cudaStreamWaitEvent(hs, ops[d][OP_KIND] == 1 ? hop_events[d] : op_events[d], 0));
+            stamp(hs, int(o), 2);
             bwd_hop<K>(w, j, op[OP_REC_IN], op[OP_HOP], p, hs);
+            stamp(hs, int(o), 3);
             CDP_CUDA(cudaEventRecord(hop_events[o], hs));
         }
         for (int w = 0; w < W; ++w) {
@@ -495,6 +516,20 @@ struct MlpTrainer {
     void finish_step();
 
     void capture() {
+        for (auto &e : exec)
+            if (e) {
+                CDP_CUDA(cudaGraphExecDestroy(e));
+                e = nullptr;
+            }
+        for (auto *v : {&op_events, &hop_events, &loss_events, &join_ev}) {
+            for (auto e : *v) cudaEventDestroy(e);
+            v->clear();
+        }
+        if (fork_ev) {
+            cudaEventDestroy(fork_ev);
+            fork_ev = nullptr;
+        }
+        if (trace && !trace_buf.p) trace_buf = DevBuf(ops.size() * 4 * 8);
         for (auto *v : {&op_events, &hop_events, &loss_events}) {
             v->resize(ops.size());
             for (auto &e : *v) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1045,4 +1080,23 @@ extern "C" int cdp_trainer_partial(cdp_trainer *tr, void **ptr, size_t *n_floats
 
 extern "C" int cdp_trainer_apply_update(cdp_trainer *tr) {
     return guarded([&] { tr->impl->apply_update(); });
+}
+
+extern "C" int cdp_trainer_set_trace(cdp_trainer *tr, int on) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        m.trace = on != 0;
+        m.capture();
+    });
+}
+
+extern "C" int cdp_trainer_trace(cdp_trainer *tr, uint64_t *out, int n_ops) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_REQUIRE(m.trace_buf.p, "trace mode was never enabled");
+        CDP_REQUIRE(n_ops == int(m.ops.size()), "n_ops must equal the plan's op count");
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        CDP_CUDA(cudaMemcpy(out, m.trace_buf.p, m.ops.size() * 4 * 8, cudaMemcpyDeviceToHost));
+    });
 }

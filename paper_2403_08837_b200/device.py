@@ -271,6 +271,28 @@ class DeviceMlpTrainer:
                 return o
         raise KeyError((kind, worker, stage))
 
+    def trace_step(self, perm: np.ndarray, lr: float, step: int) -> dict:
+        """Run one step with %globaltimer stamps around every op; returns
+        {(TaskKind, micro_batch, layer, step): (start_ns, end_ns)} (task end = max of both halves)."""
+        from .schedule import TaskKind
+
+        if not getattr(self, "_tracing", False):
+            N.check(self.lib.cdp_trainer_set_trace(self.h, 1))
+            self._tracing = True
+        self.step(perm, lr)
+        rows = self.plan.ops if self.plan is not None else self.rank_ops
+        buf = np.zeros((len(rows), 4), dtype=np.uint64)
+        N.check(self.lib.cdp_trainer_trace(self.h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(rows)))
+        out = {}
+        for o, row in enumerate(rows):
+            kind = int(row[0])
+            if kind == 2:
+                continue
+            s0, e0, s1, e1 = (int(v) for v in buf[o])
+            out[(TaskKind.FORWARD if kind == 0 else TaskKind.BACKWARD, int(row[1]), int(row[2]), step)] = (
+                s0, max(e0, e1))
+        return out
+
     def stats(self) -> dict:
         out = np.zeros(6, dtype=np.int64)
         N.check(self.lib.cdp_trainer_stats(self.h, out.ctypes.data_as(N.c_int64_p), 6))
