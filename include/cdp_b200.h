@@ -143,6 +143,38 @@ int cdp_trainer_trace(cdp_trainer *tr, uint64_t *out, int n_ops);
 /* The cudaStream_t the step graphs are launched on. */
 int cdp_trainer_stream(cdp_trainer *tr, void **stream);
 
+/* ---- BasicBlock ResNet (BASELINE configs[1]: ResNet-18 CIFAR shape) ------- */
+/* One worker per process (rank of world; world = 1 = single GPU).  Layers:
+ * 3x3 stem conv(in_channels -> widths[0]) + BN + ReLU, then per stage l
+ * depths[l] BasicBlocks of width widths[l] (first block of stage l > 0 has
+ * stride 2 and a 1x1 projection shortcut), global average pool, classifier.
+ * Parameter tensors (hop units) in torchvision order: conv [R*S*Cin][Cout],
+ * BN [gamma(C) | beta(C)], fc [[W^T]; b] = [C+1][classes]; tensor_stage[i]
+ * (1-based) groups them into world stages, stage_fresh[s] = this rank's rule
+ * row.  Dataset: x fp32 NHWC [n][height][width][in_channels], labels int32. */
+typedef struct cdp_resnet cdp_resnet;
+int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const int32_t *depths, int in_channels, int height,
+                           int width, int classes, int micro_batch, int world, int rank, const int32_t *tensor_stage,
+                           const uint8_t *stage_fresh, int dtype, float momentum, float weight_decay, int n_samples,
+                           const float *x, const int32_t *labels, cdp_resnet **out);
+/* Parameter count, tensor count and (optional) per-tensor base offsets / kinds (0 conv, 1 bn, 2 fc). */
+int cdp_resnet_info(cdp_resnet *tr, int64_t *n_params, int *n_tensors, int64_t *tensor_base, int32_t *tensor_kind);
+int cdp_resnet_region(cdp_resnet *tr, void **base);
+int cdp_resnet_ipc_handle(cdp_resnet *tr, void *handle64);
+int cdp_resnet_connect(cdp_resnet *tr, void *const *regions);
+void cdp_resnet_destroy(cdp_resnet *tr);
+int cdp_resnet_set_params(cdp_resnet *tr, int which, const float *theta);
+int cdp_resnet_get_params(cdp_resnet *tr, int which, float *theta);
+int cdp_resnet_step(cdp_resnet *tr, const int32_t *perm, float lr);
+int cdp_resnet_history(cdp_resnet *tr, int max, double *losses, uint32_t *flags, int *count);
+int cdp_resnet_sync(cdp_resnet *tr);
+int cdp_resnet_ring_error(cdp_resnet *tr, int *err);
+/* out[0..2] = activation bytes, parameter-state bytes, kernels per step. */
+int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out);
+int cdp_resnet_mark(cdp_resnet *tr, int k);
+int cdp_resnet_elapsed(cdp_resnet *tr, int a, int b, float *ms);
+int cdp_resnet_flush_l2(cdp_resnet *tr);
+
 /* ---- tensor-core GEMM self-test (parity tests of the tcgen05 kernel) --- */
 /* D[m][n] = sum_s A_s . B_s.  kind 0 = bf16, 1 = fp32/tf32.  A K-major:
  * A[m*lda+k], MN-major: A[k*lda+m]; B K-major: B[n*ldb+k], MN-major:

@@ -1,0 +1,137 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.  torch-CPU restatement of the CDP step on
+BasicBlock ResNets (BASELINE configs[1]); the reference has no ResNet, so this
+restatement is "parity unpinned" by the reference: the reference's
+`_advance` semantics (oracle/engine.advance: per-(micro-batch, stage) version
+choice, ascending accumulation, SGD-momentum update) applied to per-micro-batch
+gradients computed here with torch autograd in float64.
+
+Model conventions are those of paper_2403_08837_b200/resnet.py (CIFAR stem,
+training-mode batch norm with per-micro-batch statistics, eps 1e-5).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+
+class Block(nn.Module):
+    def __init__(self, cin, cout, stride):
+        super().__init__()
+        self.conv1 = nn.Conv2d(cin, cout, 3, stride, 1, bias=False)
+        self.bn1 = nn.BatchNorm2d(cout, eps=1e-5, track_running_stats=False)
+        self.conv2 = nn.Conv2d(cout, cout, 3, 1, 1, bias=False)
+        self.bn2 = nn.BatchNorm2d(cout, eps=1e-5, track_running_stats=False)
+        self.ds_conv = self.ds_bn = None
+        if stride != 1 or cin != cout:
+            self.ds_conv = nn.Conv2d(cin, cout, 1, stride, 0, bias=False)
+            self.ds_bn = nn.BatchNorm2d(cout, eps=1e-5, track_running_stats=False)
+
+    def forward(self, x):
+        y = F.relu(self.bn1(self.conv1(x)))
+        y = self.bn2(self.conv2(y))
+        s = self.ds_bn(self.ds_conv(x)) if self.ds_conv is not None else x
+        return F.relu(y + s)
+
+
+class CifarResNet(nn.Module):
+    def __init__(self, widths=(64, 128, 256, 512), depths=(2, 2, 2, 2), classes=10):
+        super().__init__()
+        self.stem_conv = nn.Conv2d(3, widths[0], 3, 1, 1, bias=False)
+        self.stem_bn = nn.BatchNorm2d(widths[0], eps=1e-5, track_running_stats=False)
+        blocks = []
+        cin = widths[0]
+        for l, (w, d) in enumerate(zip(widths, depths)):
+            for k in range(d):
+                blocks.append(Block(cin, w, 2 if (l > 0 and k == 0) else 1))
+                cin = w
+        self.blocks = nn.ModuleList(blocks)
+        self.fc = nn.Linear(cin, classes)
+
+    def forward(self, x):
+        y = F.relu(self.stem_bn(self.stem_conv(x)))
+        for b in self.blocks:
+            y = b(y)
+        return self.fc(y.mean(dim=(2, 3)))
+
+
+def init_flat(widths, depths, seed=0):
+    """torch default initialisation under a fixed seed, exported to the trainer layout."""
+    from paper_2403_08837_b200.resnet import torch_to_flat
+
+    torch.manual_seed(seed)
+    return torch_to_flat(CifarResNet(widths, depths))
+
+
+def load_flat(model: CifarResNet, flat: np.ndarray, specs) -> None:
+    from paper_2403_08837_b200.resnet import _ordered, flat_to_tensors
+
+    parts = flat_to_tensors(flat, specs)
+    with torch.no_grad():
+        for (name, p), a, (kind, shape, _) in zip(_ordered(model), parts, specs):
+            if kind == "conv":
+                r, s, cin, cout = shape
+                p.copy_(torch.from_numpy(np.ascontiguousarray(a.reshape(r, s, cin, cout).transpose(3, 2, 0, 1))))
+            elif kind == "bn":
+                c = shape[0] // 2
+                p.pair[0].copy_(torch.from_numpy(a[:c]))
+                p.pair[1].copy_(torch.from_numpy(a[c:]))
+            else:
+                rows, classes = shape
+                m = a.reshape(rows, classes)
+                p.pair[0].copy_(torch.from_numpy(np.ascontiguousarray(m[:-1].T)))
+                p.pair[1].copy_(torch.from_numpy(m[-1]))
+
+
+def grads_flat(model: CifarResNet, specs) -> list:
+    """Gradients of the loaded parameters, per tensor, in the trainer layout."""
+    from paper_2403_08837_b200.resnet import _ordered
+
+    out = []
+    for (name, p), (kind, shape, _) in zip(_ordered(model), specs):
+        if kind == "conv":
+            out.append(p.grad.detach().double().numpy().transpose(2, 3, 1, 0).ravel())
+        elif kind == "bn":
+            out.append(np.concatenate([p.pair[0].grad.double().numpy(), p.pair[1].grad.double().numpy()]))
+        else:
+            out.append(np.concatenate([p.pair[0].grad.double().numpy().T, p.pair[1].grad.double().numpy()[None, :]]).ravel())
+    return out
+
+
+class ResNetOracle:
+    """value + per-tensor gradients of one micro-batch, float64 on the CPU."""
+
+    def __init__(self, widths, depths, specs):
+        self.model = CifarResNet(widths, depths).double()
+        self.specs = specs
+
+    def loss_and_grads(self, params, x, y):
+        load_flat(self.model, np.concatenate(params), self.specs)
+        self.model.zero_grad(set_to_none=True)
+        xt = torch.from_numpy(np.ascontiguousarray(np.asarray(x, np.float64).transpose(0, 3, 1, 2)))
+        loss = F.cross_entropy(self.model(xt), torch.from_numpy(np.asarray(y, np.int64)))
+        loss.backward()
+        return float(loss.item()), grads_flat(self.model, self.specs)
+
+
+def run_cdp(widths, depths, init, inputs, labels, n_workers, micro_batch, perms, lr, momentum, fresh_tensor):
+    """`steps = len(perms)` CDP steps from `init` (flat); fresh_tensor = N x n_tensors table (None = DP)."""
+    from oracle import engine as OE
+    from paper_2403_08837_b200.resnet import flat_to_tensors, layer_specs
+
+    specs = layer_specs(widths, depths)
+    orc = ResNetOracle(widths, depths, specs)
+    cur = [a.copy() for a in flat_to_tensors(np.asarray(init, np.float64), specs)]
+    prev = [a.copy() for a in cur]
+    vel = [np.zeros_like(a) for a in cur] if momentum else None
+    losses = []
+    for t, perm in enumerate(perms, start=1):
+        batches = [(inputs[perm[i * micro_batch:(i + 1) * micro_batch]], labels[perm[i * micro_batch:(i + 1) * micro_batch]])
+                   for i in range(n_workers)]
+        new, loss = OE.advance(None, cur, prev, t, batches, lr, fresh_tensor, momentum, vel,
+                               grads_fn=orc.loss_and_grads)
+        prev, cur = cur, new
+        losses.append(loss)
+    return np.concatenate(cur), losses

@@ -62,6 +62,24 @@ SIGNATURES = {
     "cdp_trainer_set_trace": (c_int, [c_void_p, c_int]),
     "cdp_trainer_trace": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_uint64), c_int]),
     "cdp_trainer_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "cdp_resnet_create_rank": (c_int, [c_int, c_int_p, c_int_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                       c_int_p, c_u8_p, c_int, c_float, c_float, c_int, c_float_p, c_int_p,
+                                       ctypes.POINTER(c_void_p)]),
+    "cdp_resnet_info": (c_int, [c_void_p, c_int64_p, c_int_p, c_int64_p, c_int_p]),
+    "cdp_resnet_region": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "cdp_resnet_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "cdp_resnet_connect": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "cdp_resnet_destroy": (None, [c_void_p]),
+    "cdp_resnet_set_params": (c_int, [c_void_p, c_int, c_float_p]),
+    "cdp_resnet_get_params": (c_int, [c_void_p, c_int, c_float_p]),
+    "cdp_resnet_step": (c_int, [c_void_p, c_int_p, c_float]),
+    "cdp_resnet_history": (c_int, [c_void_p, c_int, c_double_p, ctypes.POINTER(ctypes.c_uint32), c_int_p]),
+    "cdp_resnet_sync": (c_int, [c_void_p]),
+    "cdp_resnet_ring_error": (c_int, [c_void_p, c_int_p]),
+    "cdp_resnet_stats": (c_int, [c_void_p, c_int64_p, c_int]),
+    "cdp_resnet_mark": (c_int, [c_void_p, c_int]),
+    "cdp_resnet_elapsed": (c_int, [c_void_p, c_int, c_int, c_float_p]),
+    "cdp_resnet_flush_l2": (c_int, [c_void_p]),
     "cdp_test_gemm": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p), c_int,
                               ctypes.POINTER(c_void_p), c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
 }

@@ -228,9 +228,12 @@ __global__ void __launch_bounds__(256, 1)
     }
     if constexpr (Epi::kTile) {
         // ---- tile epilogue: TMEM -> shared (the drained operand ring), then all
-        // 256 threads apply the epilogue with coalesced 128-bit global accesses
+        // 256 threads apply the epilogue with coalesced 128-bit global accesses.
+        // Split-K: every CTA parks its partial tile in the workspace; the last
+        // arriving CTA of the tile sums them in split order and runs the epilogue.
         constexpr int LDS = BN + 4;
         float *stile = reinterpret_cast<float *>(smem);
+        const bool split = gridDim.z > 1;
         if (warp >= 4) {
             const int q = warp - 4;
             const int row = q * 32 + ptx::lane_id();
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(256, 1)
             // while TMA + MMA run: protocol waits, then prefetch of the epilogue's
             // other operands (parameters, momentum, previous partial) into shared
             Epi::pre(ep, threadIdx.x - 128);
-            Epi::template prefetch<BN>(ep, pf, m0, n0, args.M, args.N, threadIdx.x - 128, 128);
+            if (!split) Epi::template prefetch<BN>(ep, pf, m0, n0, args.M, args.N, threadIdx.x - 128, 128);
             ptx::cp_async_commit();
             ptx::mbar_wait(tmem_full, 0);
             ptx::tc_fence_after();
@@ -257,9 +260,49 @@ __global__ void __launch_bounds__(256, 1)
             ptx::cp_async_wait_all();
         }
         __syncthreads();
-        Epi::template tile<BN>(ep, stile, LDS, pf, m0, n0, args.M, args.N, threadIdx.x, blockDim.x);
-        if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x, blockDim.x);
-        Epi::post(ep, threadIdx.x, gridDim.x * gridDim.y);
+        bool run = true;
+        if (split) {
+            const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+            float *mine = args.ws + (size_t(tile) * gridDim.z + blockIdx.z) * 128 * BN;
+            constexpr int C4 = BN / 4;
+            for (int e = threadIdx.x; e < 128 * C4; e += blockDim.x) {
+                const int r = e / C4, c = (e % C4) * 4;
+                *reinterpret_cast<float4 *>(mine + r * BN + c) = *reinterpret_cast<const float4 *>(stile + r * LDS + c);
+            }
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const int prev = atomicAdd(&args.counters[tile], 1);
+                const int last = prev == int(gridDim.z) - 1;
+                if (last) args.counters[tile] = 0;
+                *last_flag = last;
+            }
+            __syncthreads();
+            run = *last_flag != 0;
+            if (run) {
+                __threadfence();
+                const float *base = args.ws + size_t(tile) * gridDim.z * 128 * BN;
+                for (int e = threadIdx.x; e < 128 * C4; e += blockDim.x) {
+                    const int r = e / C4, c = (e % C4) * 4;
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int z = 0; z < int(gridDim.z); ++z) {
+                        const float4 t = __ldcg(reinterpret_cast<const float4 *>(base + size_t(z) * 128 * BN + r * BN + c));
+                        acc.x += t.x;
+                        acc.y += t.y;
+                        acc.z += t.z;
+                        acc.w += t.w;
+                    }
+                    *reinterpret_cast<float4 *>(stile + r * LDS + c) = acc;
+                }
+                __syncthreads();
+            }
+        }
+        if (run) {
+            Epi::template tile<BN>(ep, stile, LDS, split ? nullptr : pf, m0, n0, args.M, args.N, threadIdx.x,
+                                   blockDim.x);
+            if (blockIdx.x == 0 && blockIdx.y == 0) Epi::extra(ep, threadIdx.x, blockDim.x);
+            Epi::post(ep, threadIdx.x, gridDim.x * gridDim.y);
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();

@@ -64,7 +64,6 @@ void launch_gemm(const GemmPlan &p, const typename Epi::Params &ep, cudaStream_t
     using C = GemmCfg<KIND, BN, A_MN, B_MN, Epi::kStages, Epi::template pf_bytes<BN>()>;
     static_assert(!Epi::kTile || 128 * (BN + 4) * 4 <= C::STAGES * C::STAGE_BYTES, "tile epilogue staging too big");
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget exceeded");
-    CDP_REQUIRE(!Epi::kTile || p.grid.z == 1, "tile epilogues do not support split-K");
     auto kern = gemm_tc_kernel<KIND, BN, A_MN, B_MN, Epi>;
     static bool attr_set = false;
     if (!attr_set) {

@@ -147,7 +147,7 @@ struct EpiDgrad {
 // next GEMMs read.  Non-finite gradient / parameter -> flag bits.
 // Cross-GPU ring state, one per rank inside its IPC-shared region (flags are
 // step / version numbers, written with st.release.sys, read with ld.acquire.sys).
-constexpr int kMaxStages = 32;
+constexpr int kMaxStages = 64;  // ring flag slots: one per hop unit (layer / parameter tensor)
 struct RingFlags {
     uint32_t ready[kMaxStages];      // this rank's partial S^j is complete for step `ready[j]`
     uint32_t consumed[kMaxStages];   // the next rank finished reading this rank's S^j of that step
@@ -315,11 +315,19 @@ struct EpiWgrad {
                     idx[u] = p.base + int64_t(m) * p.dout + n;
                     widx[u] = size_t(m) * p.wc_new.ld + n;
                     g[u] = *reinterpret_cast<const float4 *>(st + r * lds + c);
-                    const int so = r * BN + c;  // prefetched operands (shared)
-                    if (p.mode == 1 || p.mode == 2) s[u] = *reinterpret_cast<const float4 *>(pf + 2 * 128 * BN + so);
-                    if (p.mode == 2 || p.mode == 3) {
-                        th[u] = *reinterpret_cast<const float4 *>(pf + so);
-                        if (p.momentum != 0.f) vv[u] = *reinterpret_cast<const float4 *>(pf + 128 * BN + so);
+                    if (pf) {
+                        const int so = r * BN + c;  // prefetched operands (shared)
+                        if (p.mode == 1 || p.mode == 2) s[u] = *reinterpret_cast<const float4 *>(pf + 2 * 128 * BN + so);
+                        if (p.mode == 2 || p.mode == 3) {
+                            th[u] = *reinterpret_cast<const float4 *>(pf + so);
+                            if (p.momentum != 0.f) vv[u] = *reinterpret_cast<const float4 *>(pf + 128 * BN + so);
+                        }
+                    } else {  // split-K tail CTA: operands straight from global memory
+                        if (p.mode == 1 || p.mode == 2) s[u] = __ldcg(reinterpret_cast<const float4 *>(p.s_in + idx[u]));
+                        if (p.mode == 2 || p.mode == 3) {
+                            th[u] = *reinterpret_cast<const float4 *>(p.theta_cur + idx[u]);
+                            if (p.momentum != 0.f) vv[u] = *reinterpret_cast<const float4 *>(p.vel + idx[u]);
+                        }
                     }
                 }
 #pragma unroll
@@ -400,8 +408,8 @@ struct EpiWgrad {
                 }
             }
         }
-        if (bad_g) atomicOr(p.grad_flags, 1u << (p.stage - 1));
-        if (bad_u) atomicOr(p.upd_flags, 1u << (p.stage - 1));
+        if (bad_g) atomicOr(p.grad_flags, 1u << ((p.stage - 1) & 31));
+        if (bad_u) atomicOr(p.upd_flags, 1u << ((p.stage - 1) & 31));
     }
 
     // Multi-GPU ring protocol around the hop (comm.py:37-67 made real):
@@ -582,6 +590,6 @@ __global__ void update_from_sum_kernel(HopParams p) {
         p.theta_new[idx] = nt;
         Fmt<KIND>::store(p.wc_new.hi, p.wc_new.lo, size_t(i / p.dout) * p.wc_new.ld + i % p.dout, nt);
     }
-    if (bad) atomicOr(p.upd_flags, 1u << (p.stage - 1));
+    if (bad) atomicOr(p.upd_flags, 1u << ((p.stage - 1) & 31));
 }
 }  // namespace cdp

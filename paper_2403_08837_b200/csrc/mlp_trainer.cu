@@ -28,75 +28,17 @@
 #include "../../include/cdp_b200.h"
 #include "gemm_launch.cuh"
 #include "mlp_kernels.cuh"
+#include "trainer_common.cuh"
 
 namespace cdp {
 
 enum OpField { OP_KIND = 0, OP_WORKER, OP_STAGE, OP_FRESH, OP_REC_IN, OP_REC_OUT, OP_HOP, OP_FIELDS_PAD, OP_FIELDS };
 enum HopMode { HOP_FIRST = 0, HOP_MID = 1, HOP_LAST = 2, HOP_ONLY = 3, HOP_GRAD = 4 };
 
-static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
-
-struct DevBuf {
-    void *p = nullptr;
-    size_t bytes = 0;
-    DevBuf() = default;
-    explicit DevBuf(size_t b) : bytes(b) {
-        if (b) {
-            CDP_CUDA(cudaMalloc(&p, b));
-            CDP_CUDA(cudaMemset(p, 0, b));
-        }
-    }
-    DevBuf(const DevBuf &) = delete;
-    DevBuf &operator=(const DevBuf &) = delete;
-    DevBuf(DevBuf &&o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
-    DevBuf &operator=(DevBuf &&o) noexcept {
-        std::swap(p, o.p);
-        std::swap(bytes, o.bytes);
-        return *this;
-    }
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    template <class T>
-    T *as() const { return static_cast<T *>(p); }
-};
-
-// A compute-format tensor [rows][ld] (two arrays for 3xTF32).
-struct CBuf {
-    DevBuf hi, lo;
-    int ld = 0;
-    CTensor view() const { return CTensor{hi.p, lo.p, ld}; }
-};
-
-static CBuf make_cbuf(int kind, int rows, int cols) {
-    CBuf b;
-    const int esz = kind == 0 ? 2 : 4;
-    b.ld = round_up(std::max(cols, 1), 16);  // 16-element rows keep TMA strides 16B-aligned
-    b.hi = DevBuf(size_t(rows) * b.ld * esz);
-    if (kind == 1) b.lo = DevBuf(size_t(rows) * b.ld * esz);
-    return b;
-}
-
 struct StageGeom {
     int din, dout;
     int64_t base;
 };
-
-struct Control {  // device control block, refreshed from pinned host memory every step
-    float lr;
-    int step;
-    int pad[2];
-};
-
-struct Flags {
-    unsigned grad, loss, upd, pad;
-};
-
-__global__ void stamp_kernel(uint64_t *out) {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    *out = t;
-}
 
 // -------------------------------------------------------------------------
 struct MlpTrainer {
@@ -213,7 +155,7 @@ struct MlpTrainer {
     void setup(const int64_t *dims, int n_dims) {
         S = n_dims - 1;
         CDP_REQUIRE(S >= 1, "dims needs at least input and output widths");
-        CDP_REQUIRE(S <= 32, "at most 32 stages");
+        CDP_REQUIRE(S <= kMaxStages, "too many layers");
         CDP_REQUIRE(B >= 1 && B <= 256, "micro-batch size must be in [1, 256]");
         int64_t off = 0;
         for (int j = 0; j < S; ++j) {

@@ -1,0 +1,274 @@
+"""BasicBlock ResNets on the device trainer (BASELINE configs[1]: ResNet-18, CIFAR-10 shape).
+
+The reference has no ResNet; this is the north star's "layer
+compute of the named models" for the CDP step, parity-checked against a
+torch-CPU restatement of the same step (oracle/resnet_torch.py, "parity
+unpinned" by the reference).  Conventions:
+
+* ResNet-18 CIFAR variant (`PAPER.md:312`): 3x3 stride-1 stem, no max-pool,
+  stages of BasicBlocks (widths 64/128/256/512, depths 2/2/2/2), 1x1
+  projection shortcuts, global average pool, linear classifier.
+* Batch norm in training mode with per-micro-batch statistics; running
+  statistics are not tracked (SURVEY §7 hard part 4 — one convention fixed).
+* Parameter tensors in torchvision `named_parameters` order; flat layout per
+  tensor: conv `[R][S][Cin][Cout]`, BN `[gamma | beta]`, fc `[[W^T]; b]`.
+* Stages: contiguous tensor groups, FLOP-balanced (`stage_partition`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from .device import DTYPES
+
+RESNET18 = dict(widths=(64, 128, 256, 512), depths=(2, 2, 2, 2))
+
+
+def layer_specs(widths, depths, in_ch=3, hw=32):
+    """[(kind, shape, flops_per_sample)] per tensor, in the trainer's order."""
+    out = []
+    H = hw
+
+    def conv(cin, cout, r, stride, H):
+        Ho = (H + 2 * (r // 2) - r) // stride + 1
+        out.append(("conv", (r, r, cin, cout), 2 * 3 * r * r * cin * cout * Ho * Ho))
+        out.append(("bn", (2 * cout,), 0))
+        return Ho
+
+    H = conv(in_ch, widths[0], 3, 1, H)
+    cin = widths[0]
+    for l, (w, d) in enumerate(zip(widths, depths)):
+        for k in range(d):
+            stride = 2 if (l > 0 and k == 0) else 1
+            Ho = conv(cin, w, 3, stride, H)
+            conv(w, w, 3, 1, Ho)
+            if stride != 1 or cin != w:
+                conv(cin, w, 1, stride, H)
+            cin, H = w, Ho
+    out.append(("fc", (cin + 1, 10), 0))
+    return out
+
+
+def stage_partition(specs, n_stages):
+    """Contiguous groups of tensors with balanced FLOPs (BN/fc ride with their neighbour)."""
+    flops = np.array([max(f, 1) for _, _, f in specs], dtype=np.float64)
+    cum = np.cumsum(flops)
+    total = cum[-1]
+    stage = np.empty(len(specs), dtype=np.int32)
+    s = 1
+    for i in range(len(specs)):
+        while s < n_stages and cum[i] - flops[i] / 2 > total * s / n_stages:
+            s += 1
+        stage[i] = s
+    # every stage non-empty and contiguous
+    for k in range(1, n_stages + 1):
+        if not (stage == k).any():
+            stage = np.repeat(np.arange(1, n_stages + 1), int(np.ceil(len(specs) / n_stages)))[: len(specs)]
+            break
+    return stage.astype(np.int32)
+
+
+# ----------------------------------------------------------------------------- layout conversion
+def torch_to_flat(model) -> np.ndarray:
+    """torch ResNet (oracle/resnet_torch.CifarResNet) -> flat float64 theta in the trainer layout."""
+    parts = []
+    for name, p in _ordered(model):
+        a = p.detach().double().cpu().numpy()
+        if name.endswith("conv"):
+            parts.append(np.transpose(a, (2, 3, 1, 0)).ravel())  # [Cout][Cin][R][S] -> [R][S][Cin][Cout]
+        elif name.endswith("bn"):
+            parts.append(np.concatenate([a[0], a[1]]))
+        else:  # fc: (weight [classes][C], bias [classes]) -> [[W^T]; b]
+            parts.append(np.concatenate([a[0].T, a[1][None, :]]).ravel())
+    return np.concatenate(parts)
+
+
+def flat_to_tensors(flat: np.ndarray, specs) -> list:
+    out, pos = [], 0
+    for kind, shape, _ in specs:
+        n = int(np.prod(shape))
+        out.append(flat[pos:pos + n])
+        pos += n
+    return out
+
+
+def _ordered(model):
+    """(name, tensor-or-pair) in trainer order, from the oracle torch model."""
+    items = [("stem.conv", model.stem_conv.weight), ("stem.bn", (model.stem_bn.weight, model.stem_bn.bias))]
+    for bi, b in enumerate(model.blocks):
+        items.append((f"b{bi}.c1.conv", b.conv1.weight))
+        items.append((f"b{bi}.c1.bn", (b.bn1.weight, b.bn1.bias)))
+        items.append((f"b{bi}.c2.conv", b.conv2.weight))
+        items.append((f"b{bi}.c2.bn", (b.bn2.weight, b.bn2.bias)))
+        if b.ds_conv is not None:
+            items.append((f"b{bi}.ds.conv", b.ds_conv.weight))
+            items.append((f"b{bi}.ds.bn", (b.ds_bn.weight, b.ds_bn.bias)))
+    items.append(("fc", (model.fc.weight, model.fc.bias)))
+    out = []
+    for name, p in items:
+        if isinstance(p, tuple):
+            out.append((name, _Pair(p)))
+        else:
+            out.append((name, p))
+    return out
+
+
+class _Pair:
+    def __init__(self, pair):
+        self.pair = pair
+
+    def detach(self):
+        return self
+
+    def double(self):
+        return self
+
+    def cpu(self):
+        return self
+
+    def numpy(self):
+        return [t.detach().double().cpu().numpy() for t in self.pair]
+
+
+# ----------------------------------------------------------------------------- device trainer
+def _i32p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+
+
+class DeviceResNet:
+    """One rank (worker) of CDP training of a BasicBlock ResNet on this process's GPU."""
+
+    def __init__(self, widths=RESNET18["widths"], depths=RESNET18["depths"], micro_batch=128, world=1, rank=0,
+                 rule=None, dtype="bf16", momentum=0.0, weight_decay=0.0, inputs=None, labels=None, classes=10,
+                 image_hw=32, stage_of_tensor=None):
+        self.lib = N.lib()
+        self.widths, self.depths = tuple(widths), tuple(depths)
+        self.micro_batch, self.world, self.rank = int(micro_batch), int(world), int(rank)
+        self.specs = layer_specs(self.widths, self.depths, 3, image_hw)
+        n_t = len(self.specs)
+        self.stage = np.ascontiguousarray(stage_of_tensor if stage_of_tensor is not None
+                                          else stage_partition(self.specs, world), dtype=np.int32)
+        fresh = np.ones(world, dtype=np.uint8)
+        if rule is not None:
+            if rule.n != world:
+                raise ValueError("rule size must equal the number of ranks")
+            rule.check_feasible()
+            fresh = np.array([rule.reads_fresh(rank + 1, s) for s in range(1, world + 1)], dtype=np.uint8)
+        self.fresh = fresh
+        w = np.asarray(self.widths, dtype=np.int32)
+        d = np.asarray(self.depths, dtype=np.int32)
+        x = lab = None
+        n = 0
+        if inputs is not None:
+            x = np.ascontiguousarray(inputs, dtype=np.float32)
+            lab = np.ascontiguousarray(labels, dtype=np.int32)
+            n = x.shape[0]
+        h = ctypes.c_void_p()
+        N.check(self.lib.cdp_resnet_create_rank(
+            len(w), _i32p(w), _i32p(d), 3, image_hw, image_hw, classes, self.micro_batch, world, rank,
+            _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), DTYPES[dtype], float(momentum), float(weight_decay),
+            n, x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
+            ctypes.byref(h)))
+        self.h = h
+        self._keep = (x, lab)
+        np_, nt = ctypes.c_int64(), ctypes.c_int()
+        N.check(self.lib.cdp_resnet_info(self.h, ctypes.byref(np_), ctypes.byref(nt), None, None))
+        assert nt.value == n_t, (nt.value, n_t)
+        self.P = np_.value
+        self._opened = []
+
+    def region(self) -> int:
+        b = ctypes.c_void_p()
+        N.check(self.lib.cdp_resnet_region(self.h, ctypes.byref(b)))
+        return b.value
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        N.check(self.lib.cdp_resnet_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def connect(self, regions):
+        N.check(self.lib.cdp_resnet_connect(self.h, (ctypes.c_void_p * len(regions))(*regions)))
+
+    def connect_ipc(self, handles):
+        regions = []
+        for r, hd in enumerate(handles):
+            if r == self.rank:
+                regions.append(self.region())
+                continue
+            ptr = ctypes.c_void_p()
+            N.check(self.lib.cdp_ipc_open(ctypes.create_string_buffer(hd, 64), ctypes.byref(ptr)))
+            self._opened.append(ptr.value)
+            regions.append(ptr.value)
+        self.connect(regions)
+
+    def set_params(self, flat, which=-1):
+        a = np.ascontiguousarray(flat, dtype=np.float32)
+        assert a.size == self.P
+        N.check(self.lib.cdp_resnet_set_params(self.h, which, a.ctypes.data_as(N.c_float_p)))
+
+    def get_params(self, which=0) -> np.ndarray:
+        out = np.empty(self.P, dtype=np.float32)
+        N.check(self.lib.cdp_resnet_get_params(self.h, which, out.ctypes.data_as(N.c_float_p)))
+        return out
+
+    def step(self, perm, lr):
+        p = np.ascontiguousarray(perm, dtype=np.int32)
+        assert p.size == self.micro_batch
+        N.check(self.lib.cdp_resnet_step(self.h, _i32p(p), float(lr)))
+
+    def history(self, max_steps=1 << 14):
+        losses = np.empty(max_steps)
+        flags = np.empty((max_steps, 3), dtype=np.uint32)
+        c = ctypes.c_int()
+        N.check(self.lib.cdp_resnet_history(self.h, max_steps, losses.ctypes.data_as(N.c_double_p),
+                                            flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), ctypes.byref(c)))
+        n = min(c.value, max_steps)
+        return losses[:n].copy(), flags[:n].copy()
+
+    def sync(self):
+        N.check(self.lib.cdp_resnet_sync(self.h))
+
+    def ring_error(self) -> int:
+        e = ctypes.c_int()
+        N.check(self.lib.cdp_resnet_ring_error(self.h, ctypes.byref(e)))
+        return e.value
+
+    def stats(self) -> dict:
+        out = np.zeros(3, dtype=np.int64)
+        N.check(self.lib.cdp_resnet_stats(self.h, out.ctypes.data_as(N.c_int64_p), 3))
+        return {"activation_bytes": int(out[0]), "param_state_bytes": int(out[1]), "kernels_per_step": int(out[2])}
+
+    def mark(self, k):
+        N.check(self.lib.cdp_resnet_mark(self.h, k))
+
+    def elapsed(self, a, b) -> float:
+        ms = ctypes.c_float()
+        N.check(self.lib.cdp_resnet_elapsed(self.h, a, b, ctypes.byref(ms)))
+        return ms.value
+
+    def flush_l2(self):
+        N.check(self.lib.cdp_resnet_flush_l2(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cdp_resnet_destroy(self.h)
+            self.h = None
+        for p in getattr(self, "_opened", []):
+            self.lib.cdp_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def synthetic_cifar(n, seed=0, hw=32, classes=10):
+    """x ~ N(0,1) NHWC [n][hw][hw][3], labels uniform in [0, classes) from default_rng([seed, 0xD0])."""
+    rng = np.random.default_rng([seed, 0xD0])
+    return rng.normal(0.0, 1.0, size=(n, hw, hw, 3)).astype(np.float32), rng.integers(0, classes, size=n).astype(np.int32)

@@ -1,0 +1,79 @@
+"""ResNet CDP step on the B200 vs the torch-CPU float64 restatement (oracle/resnet_torch.py).
+
+Tolerances: fp32 mode (3xTF32 products, split-K over up to 2K pixels per TMEM
+accumulation, batch-norm reductions in fp64): parameters rel-L2 <= 2e-4 and
+losses rel <= 2e-4 after the steps run here; bf16 mode: rel-L2 <= 3e-2.
+Parity is against the restatement only — the reference has no ResNet.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+W, D, HW, MB = (64, 128), (1, 1), 16, 8
+
+
+def _data(n, seed=0):
+    from paper_2403_08837_b200.resnet import synthetic_cifar
+
+    return synthetic_cifar(n, seed, hw=HW)
+
+
+def _ranks(world, rule, dtype, steps, momentum=0.9):
+    from oracle.resnet_torch import init_flat
+    from paper_2403_08837_b200.resnet import DeviceResNet
+
+    x, y = _data(world * MB * 2)
+    init = init_flat(W, D, seed=0)
+    perms = [np.random.default_rng([5, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
+    tr = [DeviceResNet(W, D, MB, world, r, rule, dtype, momentum, inputs=x, labels=y, image_hw=HW)
+          for r in range(world)]
+    regions = [t.region() for t in tr]
+    for t in tr:
+        t.set_params(init, -1)
+        t.connect(regions)
+    for step in range(steps):
+        for r, t in enumerate(tr):
+            t.step(perms[step][r * MB:(r + 1) * MB], 0.05)
+    for t in tr:
+        t.sync()
+        assert t.ring_error() == 0
+    losses = np.mean([t.history(steps)[0] for t in tr], axis=0)
+    final = tr[-1].get_params(0)
+    stage = tr[0].stage
+    for t in tr:
+        t.close()
+    return init, x, y, perms, losses, final, stage
+
+
+def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9):
+    from oracle.resnet_torch import run_cdp
+
+    fresh = None
+    if rule is not None:
+        fresh = [[rule.reads_fresh(i, int(s)) for s in stage] for i in range(1, world + 1)]
+    return run_cdp(W, D, init, x.astype(np.float64), y, world, MB, perms, 0.05, momentum, fresh)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp32", 2e-4), ("bf16", 3e-2)])
+def test_single_gpu_steps_vs_torch_restatement(cuda, dtype, tol):
+    init, x, y, perms, losses, final, stage = _ranks(1, None, dtype, 3)
+    want, wl = _oracle(init, x, y, perms, 1, None, stage)
+    assert _rel(final, want) <= tol, _rel(final, want)
+    assert np.all(np.abs(losses - np.array(wl)) <= tol * np.abs(np.array(wl)) + 1e-6), (losses, wl)
+
+
+@pytest.mark.parametrize("rule_name", ["cdp-v1", "cdp-v2"])
+def test_two_ranks_cdp_vs_torch_restatement(cuda, rule_name):
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = rule_by_name(rule_name, 2)
+    init, x, y, perms, losses, final, stage = _ranks(2, rule, "fp32", 4)
+    want, wl = _oracle(init, x, y, perms, 2, rule, stage)
+    assert _rel(final, want) <= 2e-4, _rel(final, want)
+    assert np.all(np.abs(losses - np.array(wl)) <= 2e-4 * np.abs(np.array(wl))), (losses, wl)
