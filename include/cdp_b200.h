@@ -143,20 +143,26 @@ int cdp_trainer_trace(cdp_trainer *tr, uint64_t *out, int n_ops);
 /* The cudaStream_t the step graphs are launched on. */
 int cdp_trainer_stream(cdp_trainer *tr, void **stream);
 
-/* ---- BasicBlock ResNet (BASELINE configs[1]: ResNet-18 CIFAR shape) ------- */
-/* One worker per process (rank of world; world = 1 = single GPU).  Layers:
- * 3x3 stem conv(in_channels -> widths[0]) + BN + ReLU, then per stage l
- * depths[l] BasicBlocks of width widths[l] (first block of stage l > 0 has
- * stride 2 and a 1x1 projection shortcut), global average pool, classifier.
- * Parameter tensors (hop units) in torchvision order: conv [R*S*Cin][Cout],
- * BN [gamma(C) | beta(C)], fc [[W^T]; b] = [C+1][classes]; tensor_stage[i]
- * (1-based) groups them into world stages, stage_fresh[s] = this rank's rule
- * row.  Dataset: x fp32 NHWC [n][height][width][in_channels], labels int32. */
+/* ---- ResNets (BASELINE configs[1..2,4]: ResNet-18 CIFAR, ResNet-50 ImageNet) */
+/* One worker per process (rank of world; world = 1 = single GPU).  Replaces the
+ * per-micro-batch value+grad + _advance accumulate/update of the reference
+ * (training/engine.py:66-116) for a convolutional model.  Layers: stem
+ * (stem_kind 0: 3x3/s1 conv, CIFAR; 1: 7x7/s2 conv + 3x3/s2 max pool,
+ * ImageNet) + BN + ReLU, then per stage l depths[l] blocks (block_kind 0:
+ * BasicBlock of width widths[l]; 1: Bottleneck of width widths[l], expansion
+ * 4); the first block of stage l > 0 has stride 2 (on the 3x3 conv) and a 1x1
+ * projection shortcut whenever the shape changes; global average pool,
+ * classifier.  Parameter tensors (hop units) in torchvision order: conv
+ * [R*S*Cin][Cout], BN [gamma(C) | beta(C)], fc [[W^T]; b] = [C+1][classes];
+ * tensor_stage[i] (1-based) groups them into world stages, stage_fresh[s] =
+ * this rank's rule row.  Dataset: x fp32 NHWC [n][height][width][in_channels],
+ * labels int32. */
 typedef struct cdp_resnet cdp_resnet;
-int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const int32_t *depths, int in_channels, int height,
-                           int width, int classes, int micro_batch, int world, int rank, const int32_t *tensor_stage,
-                           const uint8_t *stage_fresh, int dtype, float momentum, float weight_decay, int n_samples,
-                           const float *x, const int32_t *labels, cdp_resnet **out);
+int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const int32_t *depths, int block_kind, int stem_kind,
+                           int in_channels, int height, int width, int classes, int micro_batch, int world, int rank,
+                           const int32_t *tensor_stage, const uint8_t *stage_fresh, int dtype, float momentum,
+                           float weight_decay, int n_samples, const float *x, const int32_t *labels,
+                           cdp_resnet **out);
 /* Parameter count, tensor count and (optional) per-tensor base offsets / kinds (0 conv, 1 bn, 2 fc). */
 int cdp_resnet_info(cdp_resnet *tr, int64_t *n_params, int *n_tensors, int64_t *tensor_base, int32_t *tensor_kind);
 int cdp_resnet_region(cdp_resnet *tr, void **base);
@@ -166,10 +172,19 @@ void cdp_resnet_destroy(cdp_resnet *tr);
 int cdp_resnet_set_params(cdp_resnet *tr, int which, const float *theta);
 int cdp_resnet_get_params(cdp_resnet *tr, int which, float *theta);
 int cdp_resnet_step(cdp_resnet *tr, const int32_t *perm, float lr);
+/* End-to-end step: micro_batch images x (host, fp32 NHWC) and labels copied H2D inside the step. */
+int cdp_resnet_step_host_batch(cdp_resnet *tr, const float *x, const int32_t *labels, float lr);
+/* Loss of the most recent step (synchronises). */
+int cdp_resnet_last_loss(cdp_resnet *tr, double *loss);
+/* One real training step launched eagerly with timing events around every kernel:
+ * per launch its name (name_len bytes each), algorithmic flops / bytes and duration. */
+int cdp_resnet_profile_step(cdp_resnet *tr, const int32_t *perm, float lr, int max_ops, char *names, int name_len,
+                            double *flops, double *bytes, float *ms, int *n_ops);
 int cdp_resnet_history(cdp_resnet *tr, int max, double *losses, uint32_t *flags, int *count);
 int cdp_resnet_sync(cdp_resnet *tr);
 int cdp_resnet_ring_error(cdp_resnet *tr, int *err);
-/* out[0..2] = activation bytes, parameter-state bytes, kernels per step. */
+/* out[0..4] = activation bytes, parameter-state bytes, kernels per step, tensor-core flops per step,
+ * fp32 gradient scratch bytes. */
 int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out);
 int cdp_resnet_mark(cdp_resnet *tr, int k);
 int cdp_resnet_elapsed(cdp_resnet *tr, int a, int b, float *ms);

@@ -1,5 +1,5 @@
 """ORACLE — TEST INFRASTRUCTURE ONLY.  torch-CPU restatement of the CDP step on
-BasicBlock ResNets (BASELINE configs[1]); the reference has no ResNet, so this
+ResNets (BasicBlock / Bottleneck, CIFAR / ImageNet stem; BASELINE configs[1..2,4]); the reference has no ResNet, so this
 restatement is "parity unpinned" by the reference: the reference's
 `_advance` semantics (oracle/engine.advance: per-(micro-batch, stage) version
 choice, ascending accumulation, SGD-momentum update) applied to per-micro-batch
@@ -18,54 +18,75 @@ import torch.nn.functional as F
 
 
 class Block(nn.Module):
-    def __init__(self, cin, cout, stride):
+    """BasicBlock (two 3x3) or Bottleneck (1x1, 3x3 with the stride, 1x1 x4; torchvision v1.5)."""
+
+    def __init__(self, cin, width, stride, bottleneck=False):
         super().__init__()
-        self.conv1 = nn.Conv2d(cin, cout, 3, stride, 1, bias=False)
-        self.bn1 = nn.BatchNorm2d(cout, eps=1e-5, track_running_stats=False)
-        self.conv2 = nn.Conv2d(cout, cout, 3, 1, 1, bias=False)
-        self.bn2 = nn.BatchNorm2d(cout, eps=1e-5, track_running_stats=False)
+        exp = 4 if bottleneck else 1
+        cout = width * exp
+        if bottleneck:
+            shapes = [(cin, width, 1, 1), (width, width, 3, stride), (width, cout, 1, 1)]
+        else:
+            shapes = [(cin, width, 3, stride), (width, width, 3, 1)]
+        self.convs = nn.ModuleList([nn.Conv2d(a, b, k, st, k // 2, bias=False) for a, b, k, st in shapes])
+        self.bns = nn.ModuleList([nn.BatchNorm2d(b, eps=1e-5, track_running_stats=False) for _, b, _, _ in shapes])
         self.ds_conv = self.ds_bn = None
         if stride != 1 or cin != cout:
             self.ds_conv = nn.Conv2d(cin, cout, 1, stride, 0, bias=False)
             self.ds_bn = nn.BatchNorm2d(cout, eps=1e-5, track_running_stats=False)
 
     def forward(self, x):
-        y = F.relu(self.bn1(self.conv1(x)))
-        y = self.bn2(self.conv2(y))
+        y = x
+        n = len(self.convs)
+        for i, (cv, bn) in enumerate(zip(self.convs, self.bns)):
+            y = bn(cv(y))
+            if i < n - 1:
+                y = F.relu(y)
         s = self.ds_bn(self.ds_conv(x)) if self.ds_conv is not None else x
         return F.relu(y + s)
 
 
-class CifarResNet(nn.Module):
-    def __init__(self, widths=(64, 128, 256, 512), depths=(2, 2, 2, 2), classes=10):
+class TorchResNet(nn.Module):
+    def __init__(self, widths=(64, 128, 256, 512), depths=(2, 2, 2, 2), classes=10, block="basic", stem="cifar"):
         super().__init__()
-        self.stem_conv = nn.Conv2d(3, widths[0], 3, 1, 1, bias=False)
+        self.imagenet = stem == "imagenet"
+        if self.imagenet:
+            self.stem_conv = nn.Conv2d(3, widths[0], 7, 2, 3, bias=False)
+        else:
+            self.stem_conv = nn.Conv2d(3, widths[0], 3, 1, 1, bias=False)
         self.stem_bn = nn.BatchNorm2d(widths[0], eps=1e-5, track_running_stats=False)
+        bott = block == "bottleneck"
+        exp = 4 if bott else 1
         blocks = []
         cin = widths[0]
         for l, (w, d) in enumerate(zip(widths, depths)):
             for k in range(d):
-                blocks.append(Block(cin, w, 2 if (l > 0 and k == 0) else 1))
-                cin = w
+                blocks.append(Block(cin, w, 2 if (l > 0 and k == 0) else 1, bott))
+                cin = w * exp
         self.blocks = nn.ModuleList(blocks)
         self.fc = nn.Linear(cin, classes)
 
     def forward(self, x):
         y = F.relu(self.stem_bn(self.stem_conv(x)))
+        if self.imagenet:
+            y = F.max_pool2d(y, 3, 2, 1)
         for b in self.blocks:
             y = b(y)
         return self.fc(y.mean(dim=(2, 3)))
 
 
-def init_flat(widths, depths, seed=0):
+CifarResNet = TorchResNet
+
+
+def init_flat(widths, depths, seed=0, block="basic", stem="cifar", classes=10):
     """torch default initialisation under a fixed seed, exported to the trainer layout."""
     from paper_2403_08837_b200.resnet import torch_to_flat
 
     torch.manual_seed(seed)
-    return torch_to_flat(CifarResNet(widths, depths))
+    return torch_to_flat(TorchResNet(widths, depths, classes, block, stem))
 
 
-def load_flat(model: CifarResNet, flat: np.ndarray, specs) -> None:
+def load_flat(model: TorchResNet, flat: np.ndarray, specs) -> None:
     from paper_2403_08837_b200.resnet import _ordered, flat_to_tensors
 
     parts = flat_to_tensors(flat, specs)
@@ -85,7 +106,7 @@ def load_flat(model: CifarResNet, flat: np.ndarray, specs) -> None:
                 p.pair[1].copy_(torch.from_numpy(m[-1]))
 
 
-def grads_flat(model: CifarResNet, specs) -> list:
+def grads_flat(model: TorchResNet, specs) -> list:
     """Gradients of the loaded parameters, per tensor, in the trainer layout."""
     from paper_2403_08837_b200.resnet import _ordered
 
@@ -103,8 +124,8 @@ def grads_flat(model: CifarResNet, specs) -> list:
 class ResNetOracle:
     """value + per-tensor gradients of one micro-batch, float64 on the CPU."""
 
-    def __init__(self, widths, depths, specs):
-        self.model = CifarResNet(widths, depths).double()
+    def __init__(self, widths, depths, specs, block="basic", stem="cifar", classes=10):
+        self.model = TorchResNet(widths, depths, classes, block, stem).double()
         self.specs = specs
 
     def loss_and_grads(self, params, x, y):
@@ -116,13 +137,15 @@ class ResNetOracle:
         return float(loss.item()), grads_flat(self.model, self.specs)
 
 
-def run_cdp(widths, depths, init, inputs, labels, n_workers, micro_batch, perms, lr, momentum, fresh_tensor):
+def run_cdp(widths, depths, init, inputs, labels, n_workers, micro_batch, perms, lr, momentum, fresh_tensor,
+            block="basic", stem="cifar", classes=10, weight_decay=0.0):
     """`steps = len(perms)` CDP steps from `init` (flat); fresh_tensor = N x n_tensors table (None = DP)."""
     from oracle import engine as OE
     from paper_2403_08837_b200.resnet import flat_to_tensors, layer_specs
 
-    specs = layer_specs(widths, depths)
-    orc = ResNetOracle(widths, depths, specs)
+    hw = int(np.asarray(inputs).shape[1])
+    specs = layer_specs(widths, depths, 3, hw, block, stem, classes)
+    orc = ResNetOracle(widths, depths, specs, block, stem, classes)
     cur = [a.copy() for a in flat_to_tensors(np.asarray(init, np.float64), specs)]
     prev = [a.copy() for a in cur]
     vel = [np.zeros_like(a) for a in cur] if momentum else None
@@ -131,7 +154,7 @@ def run_cdp(widths, depths, init, inputs, labels, n_workers, micro_batch, perms,
         batches = [(inputs[perm[i * micro_batch:(i + 1) * micro_batch]], labels[perm[i * micro_batch:(i + 1) * micro_batch]])
                    for i in range(n_workers)]
         new, loss = OE.advance(None, cur, prev, t, batches, lr, fresh_tensor, momentum, vel,
-                               grads_fn=orc.loss_and_grads)
+                               weight_decay=weight_decay, grads_fn=orc.loss_and_grads)
         prev, cur = cur, new
         losses.append(loss)
     return np.concatenate(cur), losses

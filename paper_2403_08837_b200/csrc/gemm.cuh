@@ -25,6 +25,38 @@ struct GemmMaps {
     CUtensorMap b[3];
 };
 
+// Implicit-GEMM convolution geometry (MODE 1-3 of gemm_tc_kernel).  Pixels
+// are tiled in boxes (bw x bh x bn) of a [Bn][Ho][Wo] grid; one box is one
+// 4-D TMA load (channels innermost) of an NHWC tensor, with element strides
+// for strided convolutions and out-of-bounds zero fill as the padding.
+struct ConvGeom {
+    int C;              // channels of the gathered NHWC tensor
+    int R, S, stride, pad;
+    int cpt;            // CH-channel chunks per filter tap (C / CH)
+    int bw, bh, bn;     // pixel box (output space; dgrad: input space)
+    int nbw, nbh;       // boxes along W and H
+    int Wo, Ho, Bn;     // extents of the boxed pixel grid
+    int Cw;             // dgrad: Cin (rows per tap of W viewed [R*S*Cin][Cout])
+};
+
+__host__ __device__ inline void conv_box_origin(const ConvGeom &g, int idx, int &w0, int &h0, int &b0) {
+    const int iw = idx % g.nbw;
+    const int t = idx / g.nbw;
+    const int ih = t % g.nbh;
+    w0 = iw * g.bw;
+    h0 = ih * g.bh;
+    b0 = (t / g.nbh) * g.bn;
+}
+
+// Row `row` of box `idx` -> flat pixel index (b*Ho + h)*Wo + w, or -1 outside the grid.
+__host__ __device__ inline int conv_box_row(const ConvGeom &g, int idx, int row) {
+    int w0, h0, b0;
+    conv_box_origin(g, idx, w0, h0, b0);
+    const int w = w0 + row % g.bw, h = h0 + (row / g.bw) % g.bh, b = b0 + row / (g.bw * g.bh);
+    if (w >= g.Wo || h >= g.Ho || b >= g.Bn) return -1;
+    return (b * g.Ho + h) * g.Wo + w;
+}
+
 struct GemmArgs {
     int M, N;
     int kb_per_seg;   // k-blocks (of 128 bytes of K) per segment
@@ -32,7 +64,10 @@ struct GemmArgs {
     int iters_per_split;
     float *ws;        // split-K partials [tiles][splits][128][BN]
     int *counters;    // per tile arrival counters (self-resetting)
+    ConvGeom cv;      // MODE 1-3 only
 };
+
+enum GemmMode { GM_PLAIN = 0, GM_FPROP = 1, GM_DGRAD = 2, GM_WGRAD = 3 };
 
 template <int KIND, int BN_, bool A_MN, bool B_MN, int ST = 0, int PF = 0>
 struct GemmCfg {
@@ -67,6 +102,50 @@ __device__ __forceinline__ void load_operand(uint8_t *dst, const CUtensorMap *m,
     }
 }
 
+// Implicit-GEMM convolution producer: the k-block `kb` of segment `seg` for the
+// CTA's M tile (box `m_tile` for FPROP / DGRAD, rows m0.. for WGRAD).
+//   FPROP: A = input gathered at tap (r,s) (box shifted by r-pad, s-pad, strided),
+//          B = weights [R*S*C][Cout] (MN-major), k-block = one CH-channel chunk of a tap;
+//   DGRAD: (stride 1) A = dy gathered at (pad-r, pad-s), B = W^T: rows tap*Cin + n of
+//          W viewed [R*S*Cin][Cout] (K-major);
+//   WGRAD: M = (tap, c), K = pixels: A = input gathered per 64-row chunk at its tap
+//          (MN-major), B = dy (MN-major), k-block = one pixel box.
+template <class C, int MODE, bool B_MN, int BN>
+__device__ __forceinline__ void conv_load(uint8_t *sa, uint8_t *sb, const GemmMaps &maps, const GemmArgs &args,
+                                          uint64_t *bar, int seg, int kb, int m_tile, int m0, int n0) {
+    const ConvGeom &g = args.cv;
+    if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD) {
+        const int tap = kb / g.cpt, cc = kb - tap * g.cpt;
+        const int r = tap / g.S, s = tap - r * g.S;
+        int w0, h0, b0;
+        conv_box_origin(g, m_tile, w0, h0, b0);
+        if constexpr (MODE == GM_FPROP) {
+            ptx::tma_load_4d(sa, &maps.a[seg], bar, cc * C::CH, w0 * g.stride - g.pad + s, h0 * g.stride - g.pad + r,
+                             b0);
+            load_operand<C, B_MN, BN>(sb, &maps.b[seg], bar, n0, kb * C::BK);
+        } else {
+            ptx::tma_load_4d(sa, &maps.a[seg], bar, cc * C::CH, w0 + g.pad - s, h0 + g.pad - r, b0);
+            ptx::tma_load_2d(sb, &maps.b[seg], bar, cc * C::CH, tap * g.Cw + n0);
+        }
+    } else {
+        int w0, h0, b0;
+        conv_box_origin(g, kb, w0, h0, b0);
+        const int taps = g.R * g.S;
+#pragma unroll
+        for (int q = 0; q < 128 / C::CH; ++q) {
+            const int mrow = m0 + q * C::CH;
+            const int tap = min(mrow / g.C, taps - 1);
+            const int c0 = mrow - (mrow / g.C) * g.C;
+            const int r = tap / g.S, s = tap - r * g.S;
+            ptx::tma_load_4d(sa + q * (C::BK * 128), &maps.a[seg], bar, c0, w0 * g.stride - g.pad + s,
+                             h0 * g.stride - g.pad + r, b0);
+        }
+#pragma unroll
+        for (int q = 0; q < BN / C::CH; ++q)
+            ptx::tma_load_4d(sb + q * (C::BK * 128), &maps.b[seg], bar, n0 + q * C::CH, w0, h0, b0);
+    }
+}
+
 template <class C, bool MN>
 __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
     if constexpr (!MN)
@@ -77,7 +156,7 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
         return ptx::smem_desc_sw128(base + k * C::UMMA_K * 128, C::BK * 128, 512, 1);
 }
 
-template <int KIND, int BN, bool A_MN, bool B_MN, class Epi>
+template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE = GM_PLAIN>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args, const typename Epi::Params ep) {
     using C = GemmCfg<KIND, BN, A_MN, B_MN, Epi::kStages, Epi::template pf_bytes<BN>()>;
@@ -134,8 +213,13 @@ __global__ void __launch_bounds__(256, 1)
                 const int seg = g / args.kb_per_seg;
                 const int k0 = (g % args.kb_per_seg) * C::BK;
                 ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-                load_operand<C, A_MN, 128>(sA + s * C::A_BYTES, &maps.a[seg], &full[s], m0, k0);
-                load_operand<C, B_MN, BN>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, k0);
+                if constexpr (MODE == GM_PLAIN) {
+                    load_operand<C, A_MN, 128>(sA + s * C::A_BYTES, &maps.a[seg], &full[s], m0, k0);
+                    load_operand<C, B_MN, BN>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, k0);
+                } else {
+                    conv_load<C, MODE, B_MN, BN>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args, &full[s], seg,
+                                                 g % args.kb_per_seg, blockIdx.x, m0, n0);
+                }
             }
         }
     } else if (warp == 1) {
@@ -159,7 +243,11 @@ __global__ void __launch_bounds__(256, 1)
         // ---- per-row epilogue: thread t of warps 4-7 owns accumulator row t
         const int q = warp - 4;  // TMEM lane quarter of this warp
         const int row = q * 32 + ptx::lane_id();
-        const int m = m0 + row;
+        int m = m0 + row;
+        if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD) {
+            m = conv_box_row(args.cv, blockIdx.x, row);
+            if (m < 0) m = args.M;  // outside the pixel grid: the epilogue skips rows >= M
+        }
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
         ptx::mbar_wait(tmem_full, 0);
         ptx::tc_fence_after();

@@ -52,25 +52,152 @@ GemmPlan plan_gemm(const Operand *A, const Operand *B, int n_seg, int M, int N, 
     splits = std::max(1, std::min(splits, total));
     const int per = (total + splits - 1) / splits;
     splits = (total + per - 1) / per;
-    p.args = GemmArgs{M, N, kb, n_seg, per, ws, counters};
+    p.args = GemmArgs{M, N, kb, n_seg, per, ws, counters, ConvGeom{}};
     p.grid = dim3((M + 127) / 128, (N + BN - 1) / BN, splits);
     p.smem = C::SMEM;
     CDP_REQUIRE(splits == 1 || (ws && counters), "split-K needs a workspace");
     return p;
 }
 
-template <int KIND, int BN, bool A_MN, bool B_MN, class Epi>
+template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE = GM_PLAIN>
 void launch_gemm(const GemmPlan &p, const typename Epi::Params &ep, cudaStream_t st) {
     using C = GemmCfg<KIND, BN, A_MN, B_MN, Epi::kStages, Epi::template pf_bytes<BN>()>;
     static_assert(!Epi::kTile || 128 * (BN + 4) * 4 <= C::STAGES * C::STAGE_BYTES, "tile epilogue staging too big");
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget exceeded");
-    auto kern = gemm_tc_kernel<KIND, BN, A_MN, B_MN, Epi>;
+    auto kern = gemm_tc_kernel<KIND, BN, A_MN, B_MN, Epi, MODE>;
     static bool attr_set = false;
     if (!attr_set) {
         CDP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_set = true;
     }
     launch_pdl(kern, p.grid, dim3(256), C::SMEM, st, p.maps, p.args, ep);
+}
+
+// ---------------------------------------------------------------------------
+// Implicit-GEMM convolution plans (gemm_tc_kernel MODE 1-3).
+
+// An NHWC tensor in compute format: element (n, h, w, c) at hi[((n*H + h)*W + w)*ld + c].
+struct Nhwc {
+    const void *hi = nullptr, *lo = nullptr;
+    int ld = 0, C = 0, W = 0, H = 0, N = 0;
+};
+
+inline int pow2_ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Pixel boxes of `box_pixels` over a [Bn][Ho][Wo] grid (W fastest).
+inline ConvGeom conv_geom(int C, int R, int S, int stride, int pad, int Wo, int Ho, int Bn, int box_pixels, int CH) {
+    ConvGeom g{};
+    g.C = C;
+    g.R = R;
+    g.S = S;
+    g.stride = stride;
+    g.pad = pad;
+    g.cpt = C / CH;
+    g.bw = std::min(box_pixels, pow2_ceil(Wo));
+    g.bh = std::min(box_pixels / g.bw, pow2_ceil(Ho));
+    g.bn = box_pixels / (g.bw * g.bh);
+    g.nbw = (Wo + g.bw - 1) / g.bw;
+    g.nbh = (Ho + g.bh - 1) / g.bh;
+    g.Wo = Wo;
+    g.Ho = Ho;
+    g.Bn = Bn;
+    return g;
+}
+inline int conv_boxes(const ConvGeom &g) { return g.nbw * g.nbh * ((g.Bn + g.bn - 1) / g.bn); }
+
+// 4-D map over an NHWC tensor; box = CH channels x (bw, bh, bn) pixels at element stride es.
+template <int KIND>
+CUtensorMap nhwc_map(const void *ptr, const Nhwc &t, int bw, int bh, int bn, int es, bool mn_major) {
+    constexpr int ELEM = KIND == 0 ? 2 : 4;
+    constexpr uint32_t CH = 128 / ELEM;
+    const uint64_t dims[4] = {uint64_t(t.C), uint64_t(t.W), uint64_t(t.H), uint64_t(t.N)};
+    const uint64_t rs = uint64_t(t.ld) * ELEM;
+    const uint64_t strides[3] = {rs, rs * t.W, rs * t.W * t.H};
+    const uint32_t box[4] = {CH, uint32_t(bw * es), uint32_t(bh * es), uint32_t(bn)};
+    const uint32_t estr[4] = {1, uint32_t(es), uint32_t(es), 1};
+    const CUtensorMapSwizzle swz =
+        (mn_major && KIND == 1) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+    return make_tmap_4d(ptr, KIND == 0 ? ElemType::BF16 : ElemType::F32, dims, strides, box, estr, swz);
+}
+
+// Segments of the 3xTF32 product (hi.hi + hi.lo + lo.hi); bf16: one segment.
+template <int KIND>
+inline int seg_pick(int s, bool a) {
+    // s: 0 -> (hi, hi), 1 -> (hi, lo), 2 -> (lo, hi); returns 1 for "lo"
+    return a ? (s == 2) : (s == 1);
+}
+
+// FPROP: out[P_out][Cout] = conv(x, W);  x NHWC (C % CH == 0), W compute copy [R*S*C][Cout].
+// DGRAD: dx[P_in][Cin] = conv^T(dy, W) for stride 1;  dy NHWC [.][Cout], W as above.
+// WGRAD: dW[R*S*C][Cout] = sum_pixels x_tap^T dy;  x NHWC, dy NHWC.
+template <int KIND, int BN, int MODE>
+GemmPlan plan_conv(const Nhwc &a, const void *b_hi, const void *b_lo, int b_ld, const Nhwc &dy, int R, int S,
+                   int stride, int pad, int Cin, int Cout, int splits, float *ws, int *counters) {
+    constexpr int ELEM = KIND == 0 ? 2 : 4;
+    constexpr int CH = 128 / ELEM;
+    constexpr bool A_MN = MODE == GM_WGRAD;
+    constexpr bool B_MN = MODE != GM_DGRAD;
+    using Cfg = GemmCfg<KIND, BN, A_MN, B_MN>;
+    const int n_seg = KIND == 0 ? 1 : 3;
+    GemmPlan p{};
+    std::memset(&p.maps, 0, sizeof(p.maps));
+    ConvGeom g{};
+    int M = 0, N = 0, kb = 0, tiles_m = 0;
+    if (MODE == GM_FPROP) {
+        CDP_REQUIRE(a.C % CH == 0 && a.C == Cin, "implicit conv: input channels must be a multiple of the chunk");
+        const int Ho = (a.H + 2 * pad - R) / stride + 1, Wo = (a.W + 2 * pad - S) / stride + 1;
+        g = conv_geom(Cin, R, S, stride, pad, Wo, Ho, a.N, 128, CH);
+        M = a.N * Ho * Wo;
+        N = Cout;
+        kb = R * S * g.cpt;
+        tiles_m = conv_boxes(g);
+        for (int s = 0; s < n_seg; ++s) {
+            p.maps.a[s] = nhwc_map<KIND>(seg_pick<KIND>(s, true) ? a.lo : a.hi, a, g.bw, g.bh, g.bn, stride, false);
+            Operand bo{seg_pick<KIND>(s, false) ? b_lo : b_hi, true, uint64_t(Cout), uint64_t(R * S * Cin),
+                       uint64_t(b_ld)};
+            p.maps.b[s] = operand_map<KIND>(bo, BN);
+        }
+    } else if (MODE == GM_DGRAD) {
+        CDP_REQUIRE(stride == 1, "implicit dgrad: stride 1 only");
+        CDP_REQUIRE(dy.C % CH == 0 && dy.C == Cout, "implicit dgrad: output channels must be a multiple of the chunk");
+        const int H = dy.H + R - 1 - 2 * pad, W = dy.W + S - 1 - 2 * pad;  // forward input extents
+        g = conv_geom(Cout, R, S, 1, pad, W, H, dy.N, 128, CH);
+        g.Cw = Cin;
+        M = dy.N * H * W;
+        N = Cin;
+        kb = R * S * g.cpt;
+        tiles_m = conv_boxes(g);
+        for (int s = 0; s < n_seg; ++s) {
+            p.maps.a[s] = nhwc_map<KIND>(seg_pick<KIND>(s, true) ? dy.lo : dy.hi, dy, g.bw, g.bh, g.bn, 1, false);
+            Operand bo{seg_pick<KIND>(s, false) ? b_lo : b_hi, false, uint64_t(R * S * Cin), uint64_t(Cout),
+                       uint64_t(b_ld)};
+            p.maps.b[s] = operand_map<KIND>(bo, BN);
+        }
+    } else {
+        CDP_REQUIRE(a.C % CH == 0 && a.C == Cin && dy.C == Cout, "implicit wgrad: channel mismatch");
+        g = conv_geom(Cin, R, S, stride, pad, dy.W, dy.H, dy.N, Cfg::BK, CH);
+        M = R * S * Cin;
+        N = Cout;
+        kb = conv_boxes(g);
+        tiles_m = (M + 127) / 128;
+        for (int s = 0; s < n_seg; ++s) {
+            p.maps.a[s] = nhwc_map<KIND>(seg_pick<KIND>(s, true) ? a.lo : a.hi, a, g.bw, g.bh, g.bn, stride, true);
+            p.maps.b[s] = nhwc_map<KIND>(seg_pick<KIND>(s, false) ? dy.lo : dy.hi, dy, g.bw, g.bh, g.bn, 1, true);
+        }
+    }
+    const int total = kb * n_seg;
+    splits = std::max(1, std::min(splits, total));
+    const int per = (total + splits - 1) / splits;
+    splits = (total + per - 1) / per;
+    p.args = GemmArgs{M, N, kb, n_seg, per, ws, counters, g};
+    p.grid = dim3(tiles_m, (N + BN - 1) / BN, splits);
+    p.smem = Cfg::SMEM;
+    CDP_REQUIRE(splits == 1 || (ws && counters), "split-K needs a workspace");
+    return p;
 }
 
 // Workspace bytes needed by a split-K plan.

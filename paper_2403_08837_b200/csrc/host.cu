@@ -45,6 +45,30 @@ CUtensorMap make_tmap_2d(const void *base, ElemType t, uint64_t inner, uint64_t 
     return m;
 }
 
+CUtensorMap make_tmap_4d(const void *base, ElemType t, const uint64_t dims_in[4], const uint64_t strides_bytes[3],
+                         const uint32_t box_in[4], const uint32_t estr_in[4], CUtensorMapSwizzle swz) {
+    CUtensorMap m;
+    cuuint64_t dims[4], strides[3];
+    cuuint32_t box[4], estr[4];
+    for (int i = 0; i < 4; ++i) {
+        dims[i] = dims_in[i];
+        box[i] = box_in[i];
+        estr[i] = estr_in[i];
+        CDP_REQUIRE(box[i] >= 1 && box[i] <= 256, "TMA box dimension out of range");
+        CDP_REQUIRE(estr[i] >= 1 && estr[i] <= 8, "TMA element stride out of range");
+    }
+    for (int i = 0; i < 3; ++i) {
+        strides[i] = strides_bytes[i];
+        CDP_REQUIRE(strides[i] % 16 == 0, "TMA strides must be multiples of 16 bytes");
+    }
+    CDP_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, "TMA base must be 16-byte aligned");
+    CUresult r = encode_fn()(&m, t == ElemType::BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                             4, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CDP_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (4-D) failed (code " + std::to_string(int(r)) + ")");
+    return m;
+}
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char *e = std::getenv("CDP_PDL");

@@ -56,6 +56,11 @@ CUtensorMap make_tmap_2d(const void *base, ElemType t, uint64_t inner, uint64_t 
                          uint32_t box_inner, uint32_t box_outer,
                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B);
 
+// 4-D tiled tensor map (NHWC activations: dims {C, W, H, N} innermost first),
+// strides in bytes for dims 1..3, element strides for dims 1..3 (dim 0 must be 1).
+CUtensorMap make_tmap_4d(const void *base, ElemType t, const uint64_t dims[4], const uint64_t strides_bytes[3],
+                         const uint32_t box[4], const uint32_t estr[4], CUtensorMapSwizzle swz);
+
 int num_sms();
 
 // Programmatic dependent launch (PDL) toggle: CDP_PDL=0 disables it.

@@ -147,7 +147,7 @@ struct EpiDgrad {
 // next GEMMs read.  Non-finite gradient / parameter -> flag bits.
 // Cross-GPU ring state, one per rank inside its IPC-shared region (flags are
 // step / version numbers, written with st.release.sys, read with ld.acquire.sys).
-constexpr int kMaxStages = 64;  // ring flag slots: one per hop unit (layer / parameter tensor)
+constexpr int kMaxStages = 256;  // ring flag slots: one per hop unit (layer / parameter tensor)
 struct RingFlags {
     uint32_t ready[kMaxStages];      // this rank's partial S^j is complete for step `ready[j]`
     uint32_t consumed[kMaxStages];   // the next rank finished reading this rank's S^j of that step
@@ -164,6 +164,7 @@ struct DistSync {
     RingFlags *own;
     RingFlags *prev;          // rank - 1 (peer memory), null on rank 0
     unsigned *cta_counter;    // local, per stage: CTAs of this launch that finished
+    int pre_external;         // the pre-hop waits ran in a preceding one-CTA kernel (hop_wait_kernel)
 };
 
 __device__ __forceinline__ void spin_ge(const uint32_t *f, uint32_t v, uint32_t *err) {
@@ -419,8 +420,8 @@ struct EpiWgrad {
     //         the version this update overwrites;
     //   post: the last CTA publishes ready / consumed / updated.
     // called by the 128 epilogue threads (named barrier 1)
-    __device__ static void pre(const Params &p, int tid) {
-        if (!p.sync.enabled || p.mode >= 3) return;
+    __device__ static void pre(const Params &p, int tid, bool external = false) {
+        if (!p.sync.enabled || p.mode >= 3 || (p.sync.pre_external && !external)) return;
         if (tid == 0) {
             const uint32_t t = uint32_t(*p.sync.step), j = p.stage - 1;
             uint32_t *err = &p.sync.own->err;

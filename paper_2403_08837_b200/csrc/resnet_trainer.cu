@@ -1,26 +1,29 @@
-// Device-resident CDP training step for BasicBlock ResNets (BASELINE configs[1]:
-// ResNet-18, CIFAR-10 shape 32x32, one micro-batch per GPU).
+// Device-resident CDP training step for ResNets (BASELINE configs[1..2,4]):
+// BasicBlock or Bottleneck residual stages, CIFAR stem (3x3/s1) or ImageNet
+// stem (7x7/s2 + 3x3/s2 max pool), one micro-batch per GPU.
 //
 // Same step semantics as the MLP trainer (ref training/engine.py:66-116 with
 // the per-stage version rule, gradient hops w_i -> w_{i+1}, fused update on
 // the last worker, parameter pulls) with convolutional layer compute:
-//   conv  = im2col + tcgen05 GEMM (rows = output pixels, NHWC), fp32 output;
-//   BN    = training-mode batch statistics (fp64 fixed-order reductions),
-//           affine + residual + ReLU fused into one pass;
-//   dgrad = tcgen05 GEMM into im2col space + deterministic col2im gather;
-//   wgrad = tcgen05 GEMM (split-K over pixels) whose epilogue is the hop /
-//           SGD update of the weight tensor (EpiWgrad, as for the MLP);
+//   conv fprop = tcgen05 implicit GEMM: TMA gathers NHWC pixel boxes of the
+//                input per filter tap (element strides, OOB zero fill = padding);
+//                epilogue writes y and the per-tile BN statistics;
+//   BN         = training-mode batch statistics (fp64 fixed-order finalise),
+//                affine + residual + ReLU in one vectorised pass;
+//   dgrad      = implicit GEMM over dy (stride 1), or GEMM into im2col space +
+//                deterministic col2im gather (stride 2);
+//   wgrad      = implicit GEMM (K = pixel boxes, split-K) whose epilogue is the
+//                hop / SGD update of the weight tensor (EpiWgrad);
 //   BN gamma|beta hop / update by a vector kernel.
-// One worker per process (rank mode; world = 1 is plain single-GPU training).
 // Hop units are parameter tensors in torchvision order: conv weights
 // [R*S*Cin][Cout], BN [gamma(C) | beta(C)], classifier [[W^T]; b] = [C+1][classes].
 #include <cuda_bf16.h>
 
-#include <array>
 #include <cstring>
 #include <functional>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/cdp_b200.h"
@@ -33,6 +36,7 @@ namespace cdp {
 namespace {
 
 enum TensorKind { T_CONV = 0, T_BN = 1, T_FC = 2 };
+enum ConvImpl { CI_IMPLICIT = 0, CI_PLAIN = 1, CI_STEM = 2 };
 
 struct TensorSpec {
     int kind;
@@ -44,32 +48,35 @@ struct TensorSpec {
 
 struct ConvL {
     int cin, cout, R, S, stride, pad, H, W, Ho, Wo, K;
-    int tw, tb;  // tensor indices of the conv weight and its BN
-    int64_t P;   // output rows B*Ho*Wo
+    int impl;
+    int tw, tb;        // tensor indices of the weight and its BN
+    int in_act;        // activation index of the input (-1: the stem's im2col record)
+    int64_t P, Pin;    // output / input pixels
+    int tiles_fwd;     // M tiles of the forward GEMM (rows of the BN statistics)
     DevBuf y, mean, rstd, dbeta, dgamma;
-    CBuf dy;     // gradient w.r.t. the conv output (GEMM operand)
+    CBuf dy;           // gradient w.r.t. the conv output (GEMM operand)
 };
 
 struct BlockL {
-    int c1, c2, ds;         // conv indices (ds = -1: identity shortcut)
-    int a_in, a1, a_out;    // activation indices
+    std::vector<int> convs;  // main path
+    std::vector<int> mid;    // activation after convs[i] (i < n-1)
+    int ds = -1;             // projection shortcut conv (-1: identity)
+    int a_in = 0, a_out = 0;
 };
 
-template <int KIND>
-__global__ void gather_image_kernel_k(const float *__restrict__ data, int HWC, int C, const int *perm, CTensor out) {
-    ptx::griddep_wait();
-    ptx::griddep_launch();
-    const int s = blockIdx.x;
-    const float *src = data + size_t(perm[s]) * HWC;
-    const int HW = HWC / C;
-    for (int i = threadIdx.x; i < HWC; i += blockDim.x) {
-        const int pix = i / C, c = i % C;
-        Fmt<KIND>::store(out.hi, out.lo, (size_t(s) * HW + pix) * out.ld + c, src[i]);
-    }
+struct OpRec {
+    std::string name;
+    double flops, bytes;
+    cudaEvent_t a, b;
+};
+
+// Wait (one thread) until the updater holds the version this rank reads of `unit`.
+__global__ void pull_wait_kernel(RingFlags *updater, RingFlags *own, int unit, int fresh, const int *step) {
+    const int t = *step;
+    const uint32_t v = uint32_t(fresh ? t : t - 1);
+    if (v > 1 && threadIdx.x == 0) spin_ge(&updater->updated[unit - 1], v, &own->err);
 }
 
-// Copy one parameter tensor of version v from the updater (peer HBM) into the
-// local slot, packing the GEMM compute copy when it has one; count the pull.
 template <int KIND>
 __global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, int64_t n, int cols, CTensor wc,
                                    RingFlags *updater, RingFlags *own, int unit, int fresh, const int *step,
@@ -79,8 +86,6 @@ __global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, in
     const int t = *step;
     const uint32_t v = uint32_t(fresh ? t : t - 1);
     if (v <= 1) return;
-    if (threadIdx.x == 0) spin_ge(&updater->updated[unit - 1], v, &own->err);
-    __syncthreads();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const float x = __ldcv(src + i);
         dst[i] = x;
@@ -110,17 +115,33 @@ __global__ void pack_tensor_kernel(const float *__restrict__ w, int64_t n, int c
         Fmt<KIND>::store(out.hi, out.lo, size_t(i / cols) * out.ld + i % cols, w[i]);
 }
 
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+template <class F>
+void bn_switch(int BN, F &&f) {
+    switch (BN) {
+        case 32: f(IC<32>{}); return;
+        case 64: f(IC<64>{}); return;
+        case 128: f(IC<128>{}); return;
+        case 256: f(IC<256>{}); return;
+        default: throw CdpError("unsupported GEMM tile width " + std::to_string(BN));
+    }
+}
+
 }  // namespace
 
 struct ResNetTrainer {
     // ---------------------------------------------------------------- config
     int kind = 0, B = 0, Hin = 32, Win = 32, Cin0 = 3, classes = 10, loss_kind = 1;
+    int block_kind = 0, stem_kind = 0;
     float momentum = 0.f, wd = 0.f, eps = 1e-5f;
     int rank = 0, world = 1;
     std::vector<TensorSpec> tens;
     std::vector<ConvL> convs;
     std::vector<BlockL> blocks;
     int stem = 0, fc_t = -1, fc_in = 0;
+    int stem_act = 0, pool_act = -1;  // ImageNet stem: conv output act, max-pool output act
     int64_t P = 0, Pp = 0;
 
     // ---------------------------------------------------------------- state
@@ -133,11 +154,12 @@ struct ResNetTrainer {
     float *prev_partial = nullptr, *upd_theta[2] = {nullptr, nullptr};
     std::vector<CBuf> wc[2];   // per tensor (empty CBuf for BN)
     std::vector<CBuf> acts;    // activations (compute format)
-    std::vector<DevBuf> gacts; // fp32 gradients w.r.t. activations
-    std::vector<int> act_C;
+    std::vector<int> act_C, act_H, act_W;
     std::vector<int64_t> act_P;
-    CBuf x_in, cols_c, cols_h, pooled, dz;
-    DevBuf dcols, dpooled, z, gtmp, bn_partial, loss_dev;
+    DevBuf gbuf[4];            // fp32 gradients w.r.t. activations (block in / chain / chain / shortcut)
+    CBuf cols, pooled, dz;     // stem im2col record, pooled features (+ ones column), dZ
+    DevBuf dcols, dpooled, z, loss_dev, loss_rows, stats_fwd, bnpart[2], pool_arg;
+    int64_t max_act = 0;
     DevBuf ws_c, cnt_c, ws_h, cnt_h;
     size_t ws_c_floats = 0, ws_h_floats = 0;
     DevBuf data_x, data_lab, ctrl_dev, perm_dev, flags_dev, hist_loss, hist_flags;
@@ -153,14 +175,19 @@ struct ResNetTrainer {
     cudaGraphExec_t exec[2] = {nullptr, nullptr};
     int t = 1;
     int kernels_per_step = 0;
+    double flops_per_step = 0.0;
     std::vector<cudaEvent_t> marks;
     DevBuf flush_buf;
+    bool sizing = false;       // dry run: size the split-K workspaces, launch nothing
+    bool instr = false;        // eager instrumented step: events around every launch
+    std::vector<OpRec> oprecs;
 
     ~ResNetTrainer() {
         for (auto &e : exec)
             if (e) cudaGraphExecDestroy(e);
         for (auto e : events) cudaEventDestroy(e);
         for (auto e : marks) cudaEventDestroy(e);
+        clear_oprecs();
         for (auto e : stage_ev)
             if (e) cudaEventDestroy(e);
         if (stage_host) cudaFreeHost(stage_host);
@@ -168,22 +195,55 @@ struct ResNetTrainer {
             if (s) cudaStreamDestroy(s);
     }
 
+    void clear_oprecs() {
+        for (auto &o : oprecs) {
+            cudaEventDestroy(o.a);
+            cudaEventDestroy(o.b);
+        }
+        oprecs.clear();
+    }
+
+    // Every launch of the step goes through here: counts kernels / flops and,
+    // in an instrumented step, brackets the launch with timing events.
+    template <class F>
+    void L(const char *name, double flops, double bytes, cudaStream_t s, F &&f) {
+        if (sizing) return;
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (instr) {
+            CDP_CUDA(cudaEventCreate(&a));
+            CDP_CUDA(cudaEventCreate(&b));
+            CDP_CUDA(cudaEventRecord(a, s));
+        }
+        f();
+        ++kernels_per_step;
+        flops_per_step += flops;
+        if (instr) {
+            CDP_CUDA(cudaEventRecord(b, s));
+            oprecs.push_back(OpRec{name, flops, bytes, a, b});
+        }
+    }
+
     // ---------------------------------------------------------------- model
-    int add_tensor(int k, int64_t n, int rows, int cols) {
+    int chunk() const { return kind == 0 ? 64 : 32; }
+
+    int add_tensor(int k, int64_t n, int rows, int cols_) {
         int64_t base = tens.empty() ? 0 : tens.back().base + tens.back().n;
-        tens.push_back(TensorSpec{k, base, n, rows, cols, 1, 1});
+        tens.push_back(TensorSpec{k, base, n, rows, cols_, 1, 1});
         return int(tens.size()) - 1;
     }
 
-    int add_act(int64_t rows, int C) {
+    int add_act(int H, int W, int C) {
+        const int64_t rows = int64_t(B) * H * W;
         acts.push_back(make_cbuf(kind, int(rows), C));
-        gacts.emplace_back(size_t(rows) * C * 4);
         act_C.push_back(C);
+        act_H.push_back(H);
+        act_W.push_back(W);
         act_P.push_back(rows);
+        max_act = std::max(max_act, rows * C);
         return int(acts.size()) - 1;
     }
 
-    int add_conv(int cin, int cout, int R, int stride, int H, int W) {
+    int add_conv(int cin, int cout, int R, int stride, int H, int W, int in_act) {
         ConvL c{};
         c.cin = cin;
         c.cout = cout;
@@ -196,64 +256,105 @@ struct ResNetTrainer {
         c.Wo = (W + 2 * c.pad - R) / stride + 1;
         c.K = R * R * cin;
         c.P = int64_t(B) * c.Ho * c.Wo;
+        c.Pin = int64_t(B) * H * W;
+        c.in_act = in_act;
+        c.impl = in_act < 0 ? CI_STEM : (R == 1 && stride == 1) ? CI_PLAIN : CI_IMPLICIT;
+        if (c.impl == CI_IMPLICIT) CDP_REQUIRE(cin % chunk() == 0, "conv input channels must fill a TMA chunk");
         c.tw = add_tensor(T_CONV, int64_t(c.K) * cout, c.K, cout);
         c.tb = add_tensor(T_BN, 2 * int64_t(cout), 0, 0);
+        if (c.impl == CI_IMPLICIT) {
+            const ConvGeom g = conv_geom(cin, R, R, stride, c.pad, c.Wo, c.Ho, B, 128, chunk());
+            c.tiles_fwd = conv_boxes(g);
+        } else {
+            c.tiles_fwd = int((c.P + 127) / 128);
+        }
         convs.push_back(std::move(c));
         return int(convs.size()) - 1;
     }
 
     void build(const int *widths, const int *depths, int n_layers) {
         int H = Hin, W = Win;
-        x_in = make_cbuf(kind, B * H * W, Cin0);
-        stem = add_conv(Cin0, widths[0], 3, 1, H, W);
-        int a = add_act(int64_t(B) * H * W, widths[0]);
+        // stem
+        if (stem_kind == 0) {
+            stem = add_conv(Cin0, widths[0], 3, 1, H, W, -1);
+            stem_act = add_act(H, W, widths[0]);
+        } else {
+            stem = add_conv(Cin0, widths[0], 7, 2, H, W, -1);
+            convs[stem].pad = 3;
+            H = convs[stem].Ho;
+            W = convs[stem].Wo;
+            stem_act = add_act(H, W, widths[0]);
+            H = (H + 2 - 3) / 2 + 1;
+            W = (W + 2 - 3) / 2 + 1;
+            pool_act = add_act(H, W, widths[0]);
+        }
+        int a = pool_act >= 0 ? pool_act : stem_act;
         int cin = widths[0];
+        const int expansion = block_kind == 1 ? 4 : 1;
         for (int l = 0; l < n_layers; ++l) {
             for (int d = 0; d < depths[l]; ++d) {
                 const int stride = (l > 0 && d == 0) ? 2 : 1;
-                const int cout = widths[l];
-                BlockL b{};
+                const int w = widths[l], cout = w * expansion;
+                BlockL b;
                 b.a_in = a;
-                b.c1 = add_conv(cin, cout, 3, stride, H, W);
-                const int Ho = convs[b.c1].Ho, Wo = convs[b.c1].Wo;
-                b.a1 = add_act(int64_t(B) * Ho * Wo, cout);
-                b.c2 = add_conv(cout, cout, 3, 1, Ho, Wo);
-                b.ds = (stride != 1 || cin != cout) ? add_conv(cin, cout, 1, stride, H, W) : -1;
-                b.a_out = add_act(int64_t(B) * Ho * Wo, cout);
+                if (block_kind == 0) {
+                    const int c1 = add_conv(cin, w, 3, stride, H, W, a);
+                    const int Ho = convs[c1].Ho, Wo = convs[c1].Wo;
+                    const int m = add_act(Ho, Wo, w);
+                    const int c2 = add_conv(w, w, 3, 1, Ho, Wo, m);
+                    b.convs = {c1, c2};
+                    b.mid = {m};
+                } else {
+                    const int c1 = add_conv(cin, w, 1, 1, H, W, a);
+                    const int m1 = add_act(H, W, w);
+                    const int c2 = add_conv(w, w, 3, stride, H, W, m1);
+                    const int Ho = convs[c2].Ho, Wo = convs[c2].Wo;
+                    const int m2 = add_act(Ho, Wo, w);
+                    const int c3 = add_conv(w, cout, 1, 1, Ho, Wo, m2);
+                    b.convs = {c1, c2, c3};
+                    b.mid = {m1, m2};
+                }
+                if (stride != 1 || cin != cout) b.ds = add_conv(cin, cout, 1, stride, H, W, a);
+                const ConvL &last = convs[b.convs.back()];
+                H = last.Ho;
+                W = last.Wo;
+                b.a_out = add_act(H, W, cout);
                 blocks.push_back(b);
                 a = b.a_out;
                 cin = cout;
-                H = Ho;
-                W = Wo;
             }
         }
         fc_in = cin;
         fc_t = add_tensor(T_FC, int64_t(cin + 1) * classes, cin + 1, classes);
         P = tens.back().base + tens.back().n;
         // ---- buffers
-        int64_t max_cols = 0, max_dc = 0;
+        int64_t max_dcols = 1, max_stats = 1, max_part = 1;
         for (auto &c : convs) {
-            c.y = DevBuf(size_t(c.P) * c.cout * 4);
+            c.y = DevBuf(size_t(c.P) * c.cout * (kind == 0 ? 2 : 4));
             c.mean = DevBuf(c.cout * 4);
             c.rstd = DevBuf(c.cout * 4);
             c.dbeta = DevBuf(c.cout * 4);
             c.dgamma = DevBuf(c.cout * 4);
             c.dy = make_cbuf(kind, int(c.P), c.cout);
-            max_cols = std::max<int64_t>(max_cols, c.P * round_up(c.K, 16));
-            max_dc = std::max<int64_t>(max_dc, c.P * round_up(c.K, 16));
+            if (c.impl == CI_IMPLICIT && c.stride != 1)
+                max_dcols = std::max<int64_t>(max_dcols, c.P * round_up(c.K, 16));
+            max_stats = std::max<int64_t>(max_stats, int64_t(c.tiles_fwd) * c.cout * 2);
+            max_part = std::max<int64_t>(max_part, ((c.P + kBnRows - 1) / kBnRows) * c.cout * 2);
         }
-        int64_t maxP = 0;
-        for (auto &c : convs) maxP = std::max(maxP, c.P);
-        cols_c = make_cbuf(kind, 1, int(max_cols));  // viewed with per-conv ld
-        cols_h = make_cbuf(kind, 1, int(max_cols));
-        dcols = DevBuf(size_t(max_dc) * 4);
-        gtmp = DevBuf(size_t(maxP) * 512 * 4 + size_t(maxP) * 64 * 4);
-        bn_partial = DevBuf(size_t((maxP + kBnRowsPerBlock - 1) / kBnRowsPerBlock) * 512 * 2 * 8);
+        const ConvL &c0 = convs[stem];
+        cols = make_cbuf(kind, int(c0.P), c0.K);
+        for (auto &g : gbuf) g = DevBuf(size_t(max_act) * 4);
+        dcols = DevBuf(size_t(max_dcols) * 4);
+        stats_fwd = DevBuf(size_t(max_stats) * 4);
+        bnpart[0] = DevBuf(size_t(max_part) * 8);
+        bnpart[1] = DevBuf(size_t(max_part) * 8);
+        if (pool_act >= 0) pool_arg = DevBuf(size_t(act_P[pool_act]) * act_C[pool_act]);
         pooled = make_cbuf(kind, B, fc_in + 1);
         dz = make_cbuf(kind, B, classes);
         dpooled = DevBuf(size_t(B) * fc_in * 4);
         z = DevBuf(size_t(B) * classes * 4);
         loss_dev = DevBuf(8);
+        loss_rows = DevBuf(size_t(B) * 8);
         // shared region: RingFlags | theta0 | theta1 | partial
         region_off = (sizeof(RingFlags) + 255) / 256 * 256;
         Pp = (P + 63) / 64 * 64;
@@ -267,17 +368,6 @@ struct ResNetTrainer {
         for (int v = 0; v < 2; ++v)
             for (auto &ts : tens) wc[v].push_back(ts.kind == T_BN ? CBuf{} : make_cbuf(kind, ts.rows, ts.cols));
         CDP_REQUIRE(int(tens.size()) <= kMaxStages, "too many parameter tensors for the ring flags");
-        // split-K workspaces (sized by a dry run of the split heuristic)
-        for (auto &c : convs) {
-            ws_c_floats = std::max(ws_c_floats, ws_need(c.P, c.cout, bn_cout(c.cout), c.K));
-            ws_c_floats = std::max(ws_c_floats, ws_need(c.P, c.K, 128, c.cout));
-            ws_h_floats = std::max(ws_h_floats, ws_need(c.K, c.cout, 64, c.P));
-        }
-        ws_h_floats = std::max(ws_h_floats, ws_need(fc_in + 1, classes, 64, B));
-        ws_c = DevBuf(std::max<size_t>(ws_c_floats, 1) * 4);
-        ws_h = DevBuf(std::max<size_t>(ws_h_floats, 1) * 4);
-        cnt_c = DevBuf(1 << 16);
-        cnt_h = DevBuf(1 << 16);
         CDP_CUDA(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
         CDP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         CDP_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
@@ -289,134 +379,212 @@ struct ResNetTrainer {
         stage_bytes = (sizeof(Control) + size_t(B) * 4 + 255) / 256 * 256;
         CDP_CUDA(cudaMallocHost(&stage_host, stage_bytes * RING_N));
         for (auto &e : stage_ev) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cnt_c = DevBuf(1 << 18);
+        cnt_h = DevBuf(1 << 18);
+        // split-K workspaces: a dry run of the step records the largest need per stream
+        sizing = true;
+        if (kind == 0)
+            record_step<0>(0);
+        else
+            record_step<1>(0);
+        sizing = false;
+        for (auto e : events) cudaEventDestroy(e);
+        events.clear();
+        ws_c = DevBuf(std::max<size_t>(ws_c_floats, 1) * 4);
+        ws_h = DevBuf(std::max<size_t>(ws_h_floats, 1) * 4);
     }
 
     // ---------------------------------------------------------------- GEMM plumbing
-    static int bn_cout(int cout) { return std::min(256, cout); }
-    int splits_for(int64_t M, int64_t N, int BN, int64_t K) const {
-        const int bk = kind == 0 ? 64 : 32, nseg = kind == 0 ? 1 : 3;
-        const int64_t total = ((K + bk - 1) / bk) * nseg;
-        const int64_t tiles = ((M + 127) / 128) * ((N + BN - 1) / BN);
+    int splits_for(int64_t tiles, int64_t kblocks) const {
+        const int nseg = kind == 0 ? 1 : 3;
+        const int64_t total = kblocks * nseg;
         int64_t s = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
         s = std::min(s, total);
         const int64_t per = (total + s - 1) / s;
         return int((total + per - 1) / per);
     }
-    size_t ws_need(int64_t M, int64_t N, int BN, int64_t K) const {
-        const int s = splits_for(M, N, BN, K);
-        return s <= 1 ? 0 : size_t((M + 127) / 128) * ((N + BN - 1) / BN) * s * 128 * BN;
+    float *ws_for(bool hop) {
+        if (sizing) return reinterpret_cast<float *>(uintptr_t(256));  // placeholder: plans only, no launch
+        return hop ? ws_h.as<float>() : ws_c.as<float>();
+    }
+    int *cnt_for(bool hop) { return hop ? cnt_h.as<int>() : cnt_c.as<int>(); }
+
+    // Account for / check the split-K workspace of a plan, then launch it.
+    template <int K, int BN, bool AMN, bool BMN, class Epi, int MODE>
+    void run_plan(const char *name, double flops, const GemmPlan &p, const typename Epi::Params &ep, cudaStream_t s,
+                  bool hop) {
+        const size_t need = gemm_ws_floats(p, BN);
+        size_t &cap = hop ? ws_h_floats : ws_c_floats;
+        if (sizing) {
+            cap = std::max(cap, need);
+            return;
+        }
+        CDP_REQUIRE(need <= cap, "split-K workspace too small");
+        CDP_REQUIRE(size_t(p.grid.x) * p.grid.y * 4 <= (1u << 18), "split-K counters too small");
+        L(name, flops, 0.0, s, [&] { launch_gemm<K, BN, AMN, BMN, Epi, MODE>(p, ep, s); });
     }
 
-    template <int K>
-    static int segs(const Operand &a_hi, const Operand &a_lo, const Operand &b_hi, const Operand &b_lo, Operand *A,
-                    Operand *Bo) {
-        if (K == 0) {
-            A[0] = a_hi, Bo[0] = b_hi;
-            return 1;
-        }
-        A[0] = a_hi, Bo[0] = b_hi;
-        A[1] = a_hi, Bo[1] = b_lo;
-        A[2] = a_lo, Bo[2] = b_hi;
-        return 3;
-    }
     static Operand opnd(const CTensor &t, bool lo, bool mn, int64_t mn_ext, int64_t k_ext) {
         return Operand{lo ? t.lo : t.hi, mn, uint64_t(mn_ext), uint64_t(k_ext), uint64_t(t.ld)};
     }
 
+    // Plain GEMM D[M,N] = A.B (3 segments in the 3xTF32 mode).
     template <int K, bool AMN, bool BMN, class Epi>
-    void gemm(int BN, const CTensor &a, int64_t am, int64_t ak, const CTensor &b, int64_t bn_, int64_t bk, int64_t M,
-              int64_t N, int64_t Kd, const typename Epi::Params &ep, cudaStream_t s, bool hop_stream) {
+    void gemm(const char *name, int BN, const CTensor &a, const CTensor &b, int64_t M, int64_t N, int64_t Kd,
+              const typename Epi::Params &ep, cudaStream_t s, bool hop) {
         Operand A[3], Bo[3];
-        const int nseg = segs<K>(opnd(a, false, AMN, am, ak), opnd(a, true, AMN, am, ak), opnd(b, false, BMN, bn_, bk),
-                                 opnd(b, true, BMN, bn_, bk), A, Bo);
-        const int splits = splits_for(M, N, BN, Kd);
-        float *ws = hop_stream ? ws_h.as<float>() : ws_c.as<float>();
-        int *cnt = hop_stream ? cnt_h.as<int>() : cnt_c.as<int>();
-        const size_t cap = hop_stream ? ws_h_floats : ws_c_floats;
-#define CDP_RG(BN_)                                                                                             \
-    case BN_:                                                                                                   \
-        if constexpr ((!BMN || BN_ % (K == 0 ? 64 : 32) == 0) && (!Epi::kTile || BN_ <= 64)) {                  \
-            GemmPlan p = plan_gemm<K, BN_, AMN, BMN>(A, Bo, nseg, int(M), int(N), int(Kd), splits, ws, cnt);     \
-            CDP_REQUIRE(gemm_ws_floats(p, BN_) <= cap, "split-K workspace too small");                        \
-            launch_gemm<K, BN_, AMN, BMN, Epi>(p, ep, s);                                                      \
-            ++kernels_per_step;                                                                                \
-            return;                                                                                            \
-        }                                                                                                       \
-        break;
-        switch (BN) {
-            CDP_RG(32)
-            CDP_RG(64)
-            CDP_RG(128)
-            CDP_RG(256)
-            default:
-                break;
+        int nseg = 1;
+        A[0] = opnd(a, false, AMN, M, Kd);
+        Bo[0] = opnd(b, false, BMN, N, Kd);
+        if (K == 1) {
+            nseg = 3;
+            A[1] = A[0];
+            Bo[1] = opnd(b, true, BMN, N, Kd);
+            A[2] = opnd(a, true, AMN, M, Kd);
+            Bo[2] = Bo[0];
         }
-#undef CDP_RG
-        throw CdpError("unsupported GEMM tile width " + std::to_string(BN));
+        const int bk = K == 0 ? 64 : 32;
+        const int64_t tiles = ((M + 127) / 128) * ((N + BN - 1) / BN);
+        const int splits = splits_for(tiles, (Kd + bk - 1) / bk);
+        bn_switch(BN, [&](auto bnc) {
+            constexpr int BNc = decltype(bnc)::value;
+            if constexpr ((!BMN || BNc % (K == 0 ? 64 : 32) == 0) && (!Epi::kTile || BNc <= 64 ||
+                                                                      std::is_same<Epi, EpiConvOut<K>>::value)) {
+                GemmPlan p = plan_gemm<K, BNc, AMN, BMN>(A, Bo, nseg, int(M), int(N), int(Kd), splits, ws_for(hop),
+                                                          cnt_for(hop));
+                run_plan<K, BNc, AMN, BMN, Epi, GM_PLAIN>(name, 2.0 * M * N * Kd, p, ep, s, hop);
+            } else {
+                throw CdpError("unsupported GEMM configuration");
+            }
+        });
     }
 
-    CTensor cols_view(const CBuf &c, int K) const { return CTensor{c.hi.p, c.lo.p, round_up(K, 16)}; }
-    static int blocks_for(int64_t n, int per = 256) { return int(std::min<int64_t>(4 * 148, (n + per - 1) / per)); }
+    Nhwc nhwc_act(int a) const {
+        const CBuf &t = acts[a];
+        return Nhwc{t.hi.p, t.lo.p, t.ld, act_C[a], act_W[a], act_H[a], B};
+    }
+    Nhwc nhwc_dy(const ConvL &c) const { return Nhwc{c.dy.hi.p, c.dy.lo.p, c.dy.ld, c.cout, c.Wo, c.Ho, B}; }
+
+    // Implicit conv GEMM (MODE = GM_FPROP / GM_DGRAD / GM_WGRAD).
+    template <int K, int MODE, class Epi>
+    void conv_gemm(const char *name, int BN, const ConvL &c, const CBuf &w, const typename Epi::Params &ep,
+                   cudaStream_t s, bool hop) {
+        const Nhwc a = c.in_act >= 0 ? nhwc_act(c.in_act) : Nhwc{};
+        const Nhwc dy = nhwc_dy(c);
+        const int ch = chunk();
+        int64_t tiles = 0, kb = 0;
+        if (MODE == GM_FPROP) {
+            const ConvGeom g = conv_geom(c.cin, c.R, c.S, c.stride, c.pad, c.Wo, c.Ho, B, 128, ch);
+            tiles = int64_t(conv_boxes(g)) * ((c.cout + BN - 1) / BN);
+            kb = int64_t(c.R) * c.S * (c.cin / ch);
+        } else if (MODE == GM_DGRAD) {
+            const ConvGeom g = conv_geom(c.cout, c.R, c.S, 1, c.pad, c.W, c.H, B, 128, ch);
+            tiles = int64_t(conv_boxes(g)) * ((c.cin + BN - 1) / BN);
+            kb = int64_t(c.R) * c.S * (c.cout / ch);
+        } else {
+            const ConvGeom g = conv_geom(c.cin, c.R, c.S, c.stride, c.pad, c.Wo, c.Ho, B, ch, ch);
+            tiles = ((int64_t(c.K) + 127) / 128) * ((c.cout + BN - 1) / BN);
+            kb = conv_boxes(g);
+        }
+        const int splits = splits_for(tiles, kb);
+        const double flops = 2.0 * double(c.P) * c.K * c.cout;
+        bn_switch(BN, [&](auto bnc) {
+            constexpr int BNc = decltype(bnc)::value;
+            constexpr bool AMN = MODE == GM_WGRAD, BMN = MODE != GM_DGRAD;
+            if constexpr ((!BMN || BNc % (K == 0 ? 64 : 32) == 0) &&
+                          (std::is_same<Epi, EpiConvOut<K>>::value || BNc <= 64)) {
+                GemmPlan p = plan_conv<K, BNc, MODE>(a, w.hi.p, w.lo.p, w.ld, dy, c.R, c.S, c.stride, c.pad, c.cin,
+                                                     c.cout, splits, ws_for(hop), cnt_for(hop));
+                run_plan<K, BNc, AMN, BMN, Epi, MODE>(name, flops, p, ep, s, hop);
+            } else {
+                throw CdpError("unsupported conv GEMM configuration");
+            }
+        });
+    }
+
+    static int blocks_for(int64_t n, int per = 256) { return int(std::min<int64_t>(8 * 148, (n + per - 1) / per)); }
+    static int tile_n(int n) { return std::min(256, std::max(64, n)); }
 
     // ---------------------------------------------------------------- forward pieces
     template <int K>
-    void conv_forward(int ci, const CTensor &in, int vslot, cudaStream_t s) {
+    void conv_forward(int ci, int vslot, cudaStream_t s) {
         ConvL &c = convs[ci];
-        const CTensor cv = cols_view(cols_c, c.K);
-        launch_pdl(im2col_kernel<K>, dim3(blocks_for(c.P, 1)), dim3(128), 0, s, in, B, c.H, c.W, c.cin, c.R, c.S,
-                   c.stride, c.pad, c.Ho, c.Wo, cv);
-        ++kernels_per_step;
-        EpiRowF32::Params ep{c.y.as<float>(), c.cout};
-        gemm<K, false, true, EpiRowF32>(bn_cout(c.cout), cv, c.P, c.K, wc[vslot][c.tw].view(), c.cout, c.K, c.P,
-                                         c.cout, c.K, ep, s, false);
-        bn_stats(c, s);
-    }
-
-    void bn_stats(ConvL &c, cudaStream_t s) {
-        const int nblk = int((c.P + kBnRowsPerBlock - 1) / kBnRowsPerBlock);
-        launch_pdl(bn_partial_kernel<0>, dim3(nblk), dim3(std::min(256, c.cout)), 0, s, (const float *)c.y.as<float>(),
-                   c.cout, c.P, c.cout, 0, (const float *)nullptr, 0, CTensor{}, (const float *)nullptr,
-                   (const float *)nullptr, bn_partial.as<double>());
-        launch_pdl(bn_finalize_kernel, dim3((c.cout + 127) / 128), dim3(128), 0, s,
-                   (const double *)bn_partial.as<double>(), nblk, c.cout, c.P, 0, eps, c.mean.as<float>(),
-                   c.rstd.as<float>());
-        kernels_per_step += 2;
+        typename EpiConvOut<K>::Params ep{};
+        ep.out = c.y.p;
+        ep.ld = c.cout;
+        ep.out_f32 = 0;
+        ep.stats = stats_fwd.as<float>();
+        const CBuf &w = wc[vslot][c.tw];
+        if (c.impl == CI_IMPLICIT) {
+            ep.boxed = 1;
+            ep.g = conv_geom(c.cin, c.R, c.S, c.stride, c.pad, c.Wo, c.Ho, B, 128, chunk());
+            conv_gemm<K, GM_FPROP, EpiConvOut<K>>("conv_fprop", tile_n(c.cout), c, w, ep, s, false);
+        } else {
+            ep.boxed = 0;
+            const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
+            const int64_t Kd = c.impl == CI_STEM ? c.K : c.cin;
+            gemm<K, false, true, EpiConvOut<K>>(c.impl == CI_STEM ? "stem_fprop" : "conv_fprop_1x1",
+                                                tile_n(c.cout), in, w.view(), c.P, c.cout, Kd, ep, s, false);
+        }
+        L("bn_finalize_fwd", 0, double(c.tiles_fwd) * c.cout * 8, s, [&] {
+            launch_pdl(bn_finalize_fwd_kernel, dim3((c.cout * 32 + 255) / 256), dim3(256), 0, s,
+                       (const float *)stats_fwd.as<float>(), c.tiles_fwd, c.cout, c.P, eps, c.mean.as<float>(),
+                       c.rstd.as<float>());
+        });
     }
 
     const float *gamma(int ci, int vslot) const { return theta[vslot] + tens[convs[ci].tb].base; }
     const float *beta(int ci, int vslot) const { return theta[vslot] + tens[convs[ci].tb].base + convs[ci].cout; }
     int vs(int tensor, int p) const { return tens[tensor].fresh ? p : (p ^ 1); }
+    int esz() const { return kind == 0 ? 2 : 8; }
+
+    template <int K>
+    void bn_apply(int ci, int vslot, const BnResidual &res, const CTensor &out, cudaStream_t s) {
+        ConvL &c = convs[ci];
+        const double bytes = double(c.P) * c.cout * (esz() * 2 + ((res.act.hi || res.y) ? esz() : 0));
+        L("bn_apply", 0, bytes, s, [&] {
+            launch_pdl(bn_apply_kernel<K>, dim3(blocks_for(c.P * c.cout / 4)), dim3(256), 0, s, (const void *)c.y.p,
+                       c.P, c.cout, (const float *)c.mean.as<float>(), (const float *)c.rstd.as<float>(),
+                       gamma(ci, vslot), beta(ci, vslot), res, 1, out);
+        });
+    }
 
     template <int K>
     void forward(int p, cudaStream_t s, const std::function<void(int)> &pull) {
-        // input
-        launch_pdl(gather_image_kernel_k<K>, dim3(B), dim3(256), 0, s, (const float *)data_x.as<float>(),
-                   Hin * Win * Cin0, Cin0, (const int *)perm_dev.as<int>(), x_in.view());
-        ++kernels_per_step;
-        // stem
         ConvL &c0 = convs[stem];
+        L("stem_im2col", 0, double(c0.P) * cols.ld * esz(), s, [&] {
+            launch_pdl(stem_im2col_kernel<K>, dim3(blocks_for(c0.P * cols.ld)), dim3(256), 0, s,
+                       (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), Hin, Win, Cin0, c0.R, c0.S,
+                       c0.stride, c0.pad, c0.Ho, c0.Wo, c0.P, cols.view());
+        });
         pull(c0.tw);
         pull(c0.tb);
-        conv_forward<K>(stem, x_in.view(), vs(c0.tw, p), s);
-        bn_apply<K>(stem, vs(c0.tb, p), BnResidual{}, 1, acts[0].view(), s);
+        conv_forward<K>(stem, vs(c0.tw, p), s);
+        bn_apply<K>(stem, vs(c0.tb, p), BnResidual{}, acts[stem_act].view(), s);
+        if (pool_act >= 0) {
+            const int a = stem_act, o = pool_act;
+            L("maxpool_fwd", 0, double(act_P[a] + act_P[o]) * act_C[a] * esz(), s, [&] {
+                launch_pdl(maxpool_fwd_kernel<K>, dim3(blocks_for(act_P[o] * act_C[o])), dim3(256), 0, s,
+                           acts[a].view(), B, act_H[a], act_W[a], act_C[a], act_H[o], act_W[o], acts[o].view(),
+                           pool_arg.as<uint8_t>());
+            });
+        }
         for (auto &b : blocks) {
-            ConvL &c1 = convs[b.c1];
-            pull(c1.tw);
-            pull(c1.tb);
-            conv_forward<K>(b.c1, acts[b.a_in].view(), vs(c1.tw, p), s);
-            bn_apply<K>(b.c1, vs(c1.tb, p), BnResidual{}, 1, acts[b.a1].view(), s);
-            ConvL &c2 = convs[b.c2];
-            pull(c2.tw);
-            pull(c2.tb);
-            conv_forward<K>(b.c2, acts[b.a1].view(), vs(c2.tw, p), s);
+            const int n = int(b.convs.size());
+            for (int i = 0; i < n; ++i) {
+                ConvL &c = convs[b.convs[i]];
+                pull(c.tw);
+                pull(c.tb);
+                conv_forward<K>(b.convs[i], vs(c.tw, p), s);
+                if (i < n - 1) bn_apply<K>(b.convs[i], vs(c.tb, p), BnResidual{}, acts[b.mid[i]].view(), s);
+            }
             BnResidual res{};
             if (b.ds >= 0) {
                 ConvL &cd = convs[b.ds];
                 pull(cd.tw);
                 pull(cd.tb);
-                conv_forward<K>(b.ds, acts[b.a_in].view(), vs(cd.tw, p), s);
-                res.x = cd.y.as<float>();
-                res.ldx = cd.cout;
+                conv_forward<K>(b.ds, vs(cd.tw, p), s);
+                res.y = cd.y.p;
                 res.mean = cd.mean.as<float>();
                 res.rstd = cd.rstd.as<float>();
                 res.gamma = gamma(b.ds, vs(cd.tb, p));
@@ -424,61 +592,94 @@ struct ResNetTrainer {
             } else {
                 res.act = acts[b.a_in].view();
             }
-            bn_apply<K>(b.c2, vs(c2.tb, p), res, 1, acts[b.a_out].view(), s);
+            const int last = b.convs.back();
+            bn_apply<K>(last, vs(convs[last].tb, p), res, acts[b.a_out].view(), s);
         }
         // pool + classifier
-        const int last = blocks.empty() ? 0 : blocks.back().a_out;
-        const int HW = int(act_P[last] / B);
-        launch_pdl(avgpool_kernel<K>, dim3(B), dim3(256), 0, s, acts[last].view(), B, HW, fc_in, pooled.view());
-        ++kernels_per_step;
+        const int la = blocks.empty() ? stem_act : blocks.back().a_out;
+        const int HW = int(act_P[la] / B);
+        L("avgpool", 0, double(act_P[la]) * fc_in * esz(), s, [&] {
+            launch_pdl(avgpool_kernel<K>, dim3(B), dim3(256), 0, s, acts[la].view(), B, HW, fc_in, pooled.view());
+        });
         pull(fc_t);
         typename EpiFwd<K>::Params ep{};
         ep.last = 1;
         ep.z = z.as<float>();
-        gemm<K, true, false, EpiFwd<K>>(32, wc[vs(fc_t, p)][fc_t].view(), classes, fc_in + 1, pooled.view(), B,
-                                         fc_in + 1, classes, B, fc_in + 1, ep, s, false);
-    }
-
-    template <int K>
-    void bn_apply(int ci, int vslot, const BnResidual &res, int relu, const CTensor &out, cudaStream_t s) {
-        ConvL &c = convs[ci];
-        launch_pdl(bn_apply_kernel<K>, dim3(blocks_for(c.P * c.cout)), dim3(256), 0, s, (const float *)c.y.as<float>(),
-                   c.cout, c.P, c.cout, (const float *)c.mean.as<float>(), (const float *)c.rstd.as<float>(),
-                   gamma(ci, vslot), beta(ci, vslot), res, relu, out);
-        ++kernels_per_step;
+        gemm<K, true, false, EpiFwd<K>>("fc_fwd", 32, wc[vs(fc_t, p)][fc_t].view(), pooled.view(), classes, B,
+                                        fc_in + 1, ep, s, false);
     }
 
     // ---------------------------------------------------------------- backward pieces
-    // BN backward for conv ci: g (fp32, w.r.t. the BN+ReLU output), mask = that output.
+    // BN backward of conv ci (and of the projection conv `ds` sharing g' and the mask):
+    // statistics, finalise, dy = BN'(g') in compute format.
     template <int K>
-    void bn_backward(int ci, int vslot, const float *g, const CTensor &mask, cudaStream_t s) {
+    void bn_backward(int ci, int ds, int p, const float *g, const CTensor &mask, cudaStream_t s) {
         ConvL &c = convs[ci];
-        const int nblk = int((c.P + kBnRowsPerBlock - 1) / kBnRowsPerBlock);
-        launch_pdl(bn_partial_kernel<K>, dim3(nblk), dim3(std::min(256, c.cout)), 0, s,
-                   (const float *)c.y.as<float>(), c.cout, c.P, c.cout, 1, g, c.cout, mask,
-                   (const float *)c.mean.as<float>(), (const float *)c.rstd.as<float>(), bn_partial.as<double>());
-        launch_pdl(bn_finalize_kernel, dim3((c.cout + 127) / 128), dim3(128), 0, s,
-                   (const double *)bn_partial.as<double>(), nblk, c.cout, c.P, 1, eps, c.dbeta.as<float>(),
-                   c.dgamma.as<float>());
-        launch_pdl(bn_backward_kernel<K>, dim3(blocks_for(c.P * c.cout)), dim3(256), 0, s,
-                   (const float *)c.y.as<float>(), c.cout, c.P, c.cout, (const float *)c.mean.as<float>(),
-                   (const float *)c.rstd.as<float>(), gamma(ci, vslot), (const float *)c.dbeta.as<float>(),
-                   (const float *)c.dgamma.as<float>(), g, c.cout, mask, c.dy.view());
-        kernels_per_step += 3;
+        const int nblk = int((c.P + kBnRows - 1) / kBnRows);
+        const int C4 = c.cout / 4, TPR = C4 < 32 ? C4 : 32;
+        const ConvL *cd = ds >= 0 ? &convs[ds] : nullptr;
+        const double bytes = double(c.P) * c.cout * (4 + esz() + esz() + (cd ? esz() : 0));
+        L("bn_bwd_stats", 0, bytes, s, [&] {
+            launch_pdl(bn_bwd_stats_kernel<K>, dim3(nblk, (C4 + TPR - 1) / TPR), dim3(256), 0, s, g, mask, c.P,
+                       c.cout, (const void *)c.y.p, (const float *)c.mean.as<float>(),
+                       (const float *)c.rstd.as<float>(), bnpart[0].as<double>(),
+                       cd ? (const void *)cd->y.p : (const void *)nullptr,
+                       cd ? (const float *)cd->mean.as<float>() : (const float *)nullptr,
+                       cd ? (const float *)cd->rstd.as<float>() : (const float *)nullptr,
+                       cd ? bnpart[1].as<double>() : (double *)nullptr);
+        });
+        for (int k = 0; k < (cd ? 2 : 1); ++k) {
+            ConvL &cc = k == 0 ? c : convs[ds];
+            L("bn_finalize_bwd", 0, double(nblk) * cc.cout * 16, s, [&] {
+                launch_pdl(bn_finalize_bwd_kernel, dim3((cc.cout * 32 + 255) / 256), dim3(256), 0, s,
+                           (const double *)bnpart[k].as<double>(), nblk, cc.cout, cc.dbeta.as<float>(),
+                           cc.dgamma.as<float>());
+            });
+            const int cidx = k == 0 ? ci : ds;
+            const int vslot = vs(cc.tb, p);
+            L("bn_bwd_apply", 0, double(cc.P) * cc.cout * (4 + esz() * 3), s, [&] {
+                launch_pdl(bn_bwd_apply_kernel<K>, dim3(blocks_for(cc.P * cc.cout / 4)), dim3(256), 0, s, g, mask,
+                           (const void *)cc.y.p, cc.P, cc.cout, (const float *)cc.mean.as<float>(),
+                           (const float *)cc.rstd.as<float>(), gamma(cidx, vslot),
+                           (const float *)cc.dbeta.as<float>(), (const float *)cc.dgamma.as<float>(), cc.dy.view());
+            });
+        }
     }
 
-    // conv data gradient: dcols = dy . W^T, then col2im into g_in (fp32 [P_in][cin]).
+    // conv data gradient into g_in (fp32 [Pin][cin]).
     template <int K>
     void conv_dgrad(int ci, int vslot, float *g_in, cudaStream_t s) {
         ConvL &c = convs[ci];
-        const int Kp = round_up(c.K, 16);
-        EpiRowF32::Params ep{dcols.as<float>(), Kp};
-        gemm<K, false, false, EpiRowF32>(128, c.dy.view(), c.P, c.cout, wc[vslot][c.tw].view(), c.K, c.cout, c.P, c.K,
-                                          c.cout, ep, s, false);
-        const int64_t nin = int64_t(B) * c.H * c.W * c.cin;
-        launch_pdl(col2im_kernel, dim3(blocks_for(nin)), dim3(256), 0, s, (const float *)dcols.as<float>(), Kp, B, c.H,
-                   c.W, c.cin, c.R, c.S, c.stride, c.pad, c.Ho, c.Wo, g_in, c.cin);
-        ++kernels_per_step;
+        const CBuf &w = wc[vslot][c.tw];
+        typename EpiConvOut<K>::Params ep{};
+        ep.out_f32 = 1;
+        ep.stats = nullptr;
+        if (c.impl == CI_PLAIN) {
+            ep.out = g_in;
+            ep.ld = c.cin;
+            ep.boxed = 0;
+            gemm<K, false, false, EpiConvOut<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(), c.P, c.cin,
+                                                 c.cout, ep, s, false);
+        } else if (c.stride == 1) {
+            ep.out = g_in;
+            ep.ld = c.cin;
+            ep.boxed = 1;
+            ep.g = conv_geom(c.cout, c.R, c.S, 1, c.pad, c.W, c.H, B, 128, chunk());
+            conv_gemm<K, GM_DGRAD, EpiConvOut<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
+        } else {
+            const int Kp = round_up(c.K, 16);
+            ep.out = dcols.p;
+            ep.ld = Kp;
+            ep.boxed = 0;
+            // dcols[P][K] = dy[P][Cout] . W^T, W viewed [K][Cout] (K-major B)
+            gemm<K, false, false, EpiConvOut<K>>("conv_dgrad_s2", tile_n(c.K), c.dy.view(), w.view(), c.P, c.K,
+                                                 c.cout, ep, s, false);
+            const int64_t nin = c.Pin * c.cin / 4;
+            L("col2im", 0, double(c.P) * Kp * 4 + double(c.Pin) * c.cin * 4, s, [&] {
+                launch_pdl(col2im_kernel, dim3(blocks_for(nin)), dim3(256), 0, s, (const float *)dcols.as<float>(),
+                           Kp, B, c.H, c.W, c.cin, c.R, c.S, c.stride, c.pad, c.Ho, c.Wo, g_in);
+            });
+        }
     }
 
     HopParams hop_params(int tensor, int p) {
@@ -508,27 +709,39 @@ struct ResNetTrainer {
         hp.sync.own = ring;
         hp.sync.prev = prev_ring;
         hp.sync.cta_counter = cta_counters.as<unsigned>();
+        hp.sync.pre_external = 1;
         return hp;
+    }
+
+    // Ring waits of a hop (multi-GPU) ahead of its kernel on the hop stream.
+    void hop_wait(const HopParams &hp, cudaStream_t s) {
+        if (world == 1 || hp.mode >= 3) return;
+        L("hop_wait", 0, 0, s, [&] { hop_wait_kernel<<<1, 128, 0, s>>>(hp); CDP_CUDA(cudaGetLastError()); });
     }
 
     // weight gradient of conv ci fused with its hop / update (hop stream).
     template <int K>
-    void conv_wgrad_hop(int ci, const CTensor &in, int p, cudaStream_t s) {
+    void conv_wgrad_hop(int ci, int p, cudaStream_t s) {
         ConvL &c = convs[ci];
-        const CTensor cv = cols_view(cols_h, c.K);
-        launch_pdl(im2col_kernel<K>, dim3(blocks_for(c.P, 1)), dim3(128), 0, s, in, B, c.H, c.W, c.cin, c.R, c.S,
-                   c.stride, c.pad, c.Ho, c.Wo, cv);
-        ++kernels_per_step;
         HopParams hp = hop_params(c.tw, p);
-        gemm<K, true, true, EpiWgrad<K>>(64, cv, c.K, c.P, c.dy.view(), c.cout, c.P, c.K, c.cout, c.P, hp, s, true);
+        hop_wait(hp, s);
+        if (c.impl == CI_IMPLICIT) {
+            conv_gemm<K, GM_WGRAD, EpiWgradConv<K>>("conv_wgrad_hop", 64, c, wc[0][c.tw], hp, s, true);
+        } else {
+            const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
+            gemm<K, true, true, EpiWgradConv<K>>(c.impl == CI_STEM ? "stem_wgrad_hop" : "conv_wgrad_hop_1x1", 64, in,
+                                                 c.dy.view(), c.K, c.cout, c.P, hp, s, true);
+        }
     }
 
     void bn_hop(int ci, int p, cudaStream_t s) {
         ConvL &c = convs[ci];
         HopParams hp = hop_params(c.tb, p);
-        launch_pdl(vector_hop_kernel, dim3(1), dim3(128), 0, s, hp, (const float *)c.dgamma.as<float>(),
-                   (const float *)c.dbeta.as<float>(), c.cout);
-        ++kernels_per_step;
+        hop_wait(hp, s);
+        L("bn_hop", 0, double(c.cout) * 2 * 24, s, [&] {
+            launch_pdl(vector_hop_kernel, dim3(1), dim3(128), 0, s, hp, (const float *)c.dgamma.as<float>(),
+                       (const float *)c.dbeta.as<float>(), c.cout);
+        });
     }
 
     // ---------------------------------------------------------------- step capture
@@ -536,10 +749,12 @@ struct ResNetTrainer {
         cudaEvent_t e;
         CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         events.push_back(e);
-        CDP_CUDA(cudaEventRecord(e, s));
+        if (!sizing) CDP_CUDA(cudaEventRecord(e, s));
         return e;
     }
-    void wait(cudaStream_t s, cudaEvent_t e) { CDP_CUDA(cudaStreamWaitEvent(s, e, 0)); }
+    void wait(cudaStream_t s, cudaEvent_t e) {
+        if (!sizing) CDP_CUDA(cudaStreamWaitEvent(s, e, 0));
+    }
     bool last_updater() const { return rank == world - 1; }
 
     template <int K>
@@ -547,18 +762,37 @@ struct ResNetTrainer {
         if (rank == world - 1 || world == 1) return;
         const TensorSpec &ts = tens[tensor];
         const int vslot = vs(tensor, p);
+        if (sizing) return;
         CDP_REQUIRE(upd_ring && upd_theta[vslot], "pull outside a connected multi-GPU trainer");
         CTensor w = ts.kind == T_BN ? CTensor{} : wc[vslot][tensor].view();
-        launch_pdl(pull_tensor_kernel<K>, dim3(blocks_for(ts.n, 1024)), dim3(256), 0, s,
-                   (const float *)(upd_theta[vslot] + ts.base), theta[vslot] + ts.base, ts.n, std::max(ts.cols, 1), w,
-                   upd_ring, ring, tensor + 1, ts.fresh, (const int *)&ctrl_dev.as<Control>()->step,
-                   cta_counters.as<unsigned>() + kMaxStages);
-        ++kernels_per_step;
+        L("pull_wait", 0, 0, s, [&] {
+            pull_wait_kernel<<<1, 32, 0, s>>>(upd_ring, ring, tensor + 1, ts.fresh,
+                                              (const int *)&ctrl_dev.as<Control>()->step);
+            CDP_CUDA(cudaGetLastError());
+        });
+        L("pull", 0, double(ts.n) * (4 + 4 + esz()), s, [&] {
+            launch_pdl(pull_tensor_kernel<K>, dim3(blocks_for(ts.n, 1024)), dim3(256), 0, s,
+                       (const float *)(upd_theta[vslot] + ts.base), theta[vslot] + ts.base, ts.n,
+                       std::max(ts.cols, 1), w, upd_ring, ring, tensor + 1, ts.fresh,
+                       (const int *)&ctrl_dev.as<Control>()->step, cta_counters.as<unsigned>() + kMaxStages);
+        });
+    }
+
+    // Weight hop of conv ci on the hop stream once its dy is ready (and, for a
+    // stale read on the updater, once its data gradient has read the old copy).
+    template <int K>
+    void hop_conv(int ci, int p, cudaEvent_t dy_ready, cudaEvent_t dgrad_done) {
+        ConvL &c = convs[ci];
+        wait(hs, dy_ready);
+        bn_hop(ci, p, hs);
+        if (dgrad_done && !tens[c.tw].fresh && last_updater()) wait(hs, dgrad_done);
+        conv_wgrad_hop<K>(ci, p, hs);
     }
 
     template <int K>
     void record_step(int p) {
         kernels_per_step = 0;
+        flops_per_step = 0.0;
         cudaEvent_t fork = ev(main);
         wait(cs, fork);
         wait(hs, fork);
@@ -567,101 +801,111 @@ struct ResNetTrainer {
         Flags *fl = flags_dev.as<Flags>();
         const int nt = std::max(32, round_up(B, 32));
         const size_t lsm = sizeof(double) * nt + sizeof(float) * B * classes;
-        launch_pdl(loss_kernel<K>, dim3(1), dim3(nt), lsm, cs, (const float *)z.as<float>(), B, classes, loss_kind,
-                   (const int *)perm_dev.as<int>(), (const int *)data_lab.as<int>(), (const float *)nullptr, dz.view(),
-                   loss_dev.as<double>(), &fl->loss);
-        ++kernels_per_step;
+        if (classes <= 64 && lsm <= 48 * 1024) {
+            L("loss", 0, 0, cs, [&] {
+                launch_pdl(loss_kernel<K>, dim3(1), dim3(nt), lsm, cs, (const float *)z.as<float>(), B, classes,
+                           loss_kind, (const int *)perm_dev.as<int>(), (const int *)data_lab.as<int>(),
+                           (const float *)nullptr, dz.view(), loss_dev.as<double>(), &fl->loss);
+            });
+        } else {
+            L("loss", 0, 0, cs, [&] {
+                launch_pdl(xent_rows_kernel<K>, dim3(B), dim3(256), 0, cs, (const float *)z.as<float>(), B, classes,
+                           (const int *)perm_dev.as<int>(), (const int *)data_lab.as<int>(), dz.view(),
+                           loss_rows.as<double>());
+            });
+            L("loss_sum", 0, 0, cs, [&] {
+                launch_pdl(loss_sum_kernel, dim3(1), dim3(1), 0, cs, (const double *)loss_rows.as<double>(), B,
+                           loss_dev.as<double>(), &fl->loss);
+            });
+        }
         cudaEvent_t dz_ready = ev(cs);
         typename EpiDgradLinear::Params dep{dpooled.as<float>(), fc_in};
         const int vfc = vs(fc_t, p);
-        gemm<K, false, false, EpiDgradLinear>(32, wc[vfc][fc_t].view(), fc_in, classes, dz.view(), B, classes, fc_in,
-                                               B, classes, dep, cs, false);
+        gemm<K, false, false, EpiDgradLinear>("fc_dgrad", 32, wc[vfc][fc_t].view(), dz.view(), fc_in, B, classes, dep,
+                                              cs, false);
         cudaEvent_t fc_dgrad_done = ev(cs);
-        // classifier hop
         wait(hs, dz_ready);
         if (!tens[fc_t].fresh && last_updater()) wait(hs, fc_dgrad_done);
         {
             HopParams hp = hop_params(fc_t, p);
-            gemm<K, true, true, EpiWgrad<K>>(64, pooled.view(), fc_in + 1, B, dz.view(), classes, B, fc_in + 1,
-                                              classes, B, hp, hs, true);
+            hop_wait(hp, hs);
+            gemm<K, true, true, EpiWgrad<K>>("fc_wgrad_hop", 64, pooled.view(), dz.view(), fc_in + 1, classes, B, hp,
+                                             hs, true);
         }
-        // pool backward -> gradient w.r.t. the last activation
-        const int last = blocks.back().a_out;
-        const int HW = int(act_P[last] / B);
-        launch_pdl(avgpool_backward_kernel, dim3(blocks_for(act_P[last] * fc_in)), dim3(256), 0, cs,
-                   (const float *)dpooled.as<float>(), fc_in, B, HW, fc_in, gacts[last].as<float>(), fc_in);
-        ++kernels_per_step;
-        // blocks in reverse
+        float *G0 = gbuf[0].as<float>(), *G1 = gbuf[1].as<float>(), *G2 = gbuf[2].as<float>(),
+              *G3 = gbuf[3].as<float>();
+        // pool backward -> gradient w.r.t. the last activation (G0 holds the block-output gradient)
+        const int la = blocks.empty() ? stem_act : blocks.back().a_out;
+        const int HW = int(act_P[la] / B);
+        L("avgpool_bwd", 0, double(act_P[la]) * fc_in * 4, cs, [&] {
+            launch_pdl(avgpool_backward_kernel, dim3(blocks_for(act_P[la] * fc_in / 4)), dim3(256), 0, cs,
+                       (const float *)dpooled.as<float>(), fc_in, B, HW, fc_in, G0);
+        });
         for (int bi = int(blocks.size()) - 1; bi >= 0; --bi) {
             BlockL &b = blocks[bi];
-            ConvL &c1 = convs[b.c1], &c2 = convs[b.c2];
-            const float *g_out = gacts[b.a_out].as<float>();
+            const int n = int(b.convs.size());
             const CTensor m_out = acts[b.a_out].view();
-            // second BN (+ shortcut BN)
-            bn_backward<K>(b.c2, vs(c2.tb, p), g_out, m_out, cs);
-            cudaEvent_t dy2 = ev(cs);
-            cudaEvent_t dyd = nullptr;
-            if (b.ds >= 0) {
-                bn_backward<K>(b.ds, vs(convs[b.ds].tb, p), g_out, m_out, cs);
-                dyd = ev(cs);
+            // last BN (+ projection BN): g' = G0 masked by the block output
+            bn_backward<K>(b.convs[n - 1], b.ds, p, G0, m_out, cs);
+            cudaEvent_t dy_last = ev(cs);
+            float *chain[2] = {G1, G2};
+            float *g_main = nullptr;
+            cudaEvent_t dy_next = dy_last;
+            for (int i = n - 1; i >= 0; --i) {
+                const int ci = b.convs[i];
+                float *out = chain[(n - 1 - i) & 1];
+                conv_dgrad<K>(ci, vs(convs[ci].tw, p), out, cs);
+                cudaEvent_t dg = ev(cs);
+                hop_conv<K>(ci, p, dy_next, dg);
+                if (i > 0) {
+                    bn_backward<K>(b.convs[i - 1], -1, p, out, acts[b.mid[i - 1]].view(), cs);
+                    dy_next = ev(cs);
+                } else {
+                    g_main = out;
+                }
             }
-            // conv2: data gradient into a1's gradient
-            conv_dgrad<K>(b.c2, vs(c2.tw, p), gacts[b.a1].as<float>(), cs);
-            cudaEvent_t c2_dg = ev(cs);
-            // hops of conv2 / bn2 (and the shortcut) overlap the rest of the block
-            wait(hs, dy2);
-            bn_hop(b.c2, p, hs);
-            if (!tens[c2.tw].fresh && last_updater()) wait(hs, c2_dg);
-            conv_wgrad_hop<K>(b.c2, acts[b.a1].view(), p, hs);
-            // first BN
-            bn_backward<K>(b.c1, vs(c1.tb, p), gacts[b.a1].as<float>(), acts[b.a1].view(), cs);
-            cudaEvent_t dy1 = ev(cs);
-            // conv1 data gradient -> input gradient (main path) in gtmp
-            float *g_in = gacts[b.a_in].as<float>();
-            float *g_main = gtmp.as<float>();
-            conv_dgrad<K>(b.c1, vs(c1.tw, p), g_main, cs);
-            cudaEvent_t c1_dg = ev(cs);
+            const int64_t Pin = act_P[b.a_in];
+            const int Cin = act_C[b.a_in];
             if (b.ds >= 0) {
-                ConvL &cd = convs[b.ds];
-                float *g_ds = gtmp.as<float>() + size_t(act_P[b.a_in]) * act_C[b.a_in];
-                conv_dgrad<K>(b.ds, vs(cd.tw, p), g_ds, cs);
-                cudaEvent_t cd_dg = ev(cs);
-                launch_pdl(add_kernel<K>, dim3(blocks_for(act_P[b.a_in] * act_C[b.a_in])), dim3(256), 0, cs,
-                           (const float *)g_main, (const float *)g_ds, act_C[b.a_in], act_P[b.a_in], act_C[b.a_in],
-                           CTensor{}, g_in);
-                ++kernels_per_step;
-                wait(hs, dyd);
-                bn_hop(b.ds, p, hs);
-                if (!tens[cd.tw].fresh && last_updater()) wait(hs, cd_dg);
-                conv_wgrad_hop<K>(b.ds, acts[b.a_in].view(), p, hs);
+                conv_dgrad<K>(b.ds, vs(convs[b.ds].tw, p), G3, cs);
+                cudaEvent_t dg = ev(cs);
+                hop_conv<K>(b.ds, p, dy_last, dg);
+                L("residual_add", 0, double(Pin) * Cin * 12, cs, [&] {
+                    launch_pdl(add_kernel<K>, dim3(blocks_for(Pin * Cin / 4)), dim3(256), 0, cs, (const float *)g_main,
+                               (const float *)G3, Pin, Cin, CTensor{}, G0);
+                });
             } else {
-                // identity shortcut: g_in = g_main + g_out masked by the block output
-                launch_pdl(add_kernel<K>, dim3(blocks_for(act_P[b.a_in] * act_C[b.a_in])), dim3(256), 0, cs,
-                           (const float *)g_main, g_out, act_C[b.a_in], act_P[b.a_in], act_C[b.a_in], m_out, g_in);
-                ++kernels_per_step;
+                L("residual_add", 0, double(Pin) * Cin * (12 + esz()), cs, [&] {
+                    launch_pdl(add_kernel<K>, dim3(blocks_for(Pin * Cin / 4)), dim3(256), 0, cs, (const float *)g_main,
+                               (const float *)G0, Pin, Cin, m_out, G0);
+                });
             }
-            cudaEvent_t gin_done = ev(cs);
-            (void)gin_done;
-            wait(hs, dy1);
-            bn_hop(b.c1, p, hs);
-            if (!tens[c1.tw].fresh && last_updater()) wait(hs, c1_dg);
-            conv_wgrad_hop<K>(b.c1, acts[b.a_in].view(), p, hs);
-            // the next (earlier) block's compute reuses gtmp: its dgrad must not race the add above
         }
-        // stem
+        // stem (gradient w.r.t. the stem output / max-pool output in G0)
         ConvL &c0 = convs[stem];
-        bn_backward<K>(stem, vs(c0.tb, p), gacts[0].as<float>(), acts[0].view(), cs);
+        const float *gs = G0;
+        if (pool_act >= 0) {
+            const int a = stem_act, o = pool_act;
+            L("maxpool_bwd", 0, double(act_P[o]) * act_C[o] * 5 + double(act_P[a]) * act_C[a] * 4, cs, [&] {
+                launch_pdl(maxpool_bwd_kernel, dim3(blocks_for(act_P[a] * act_C[a])), dim3(256), 0, cs,
+                           (const float *)G0, (const uint8_t *)pool_arg.as<uint8_t>(), B, act_H[a], act_W[a],
+                           act_C[a], act_H[o], act_W[o], G1);
+            });
+            gs = G1;
+        }
+        bn_backward<K>(stem, -1, p, gs, acts[stem_act].view(), cs);
         cudaEvent_t dy0 = ev(cs);
-        wait(hs, dy0);
-        bn_hop(stem, p, hs);
-        conv_wgrad_hop<K>(stem, x_in.view(), p, hs);
+        hop_conv<K>(stem, p, dy0, nullptr);
         // join + bookkeeping
         wait(main, ev(cs));
         wait(main, ev(hs));
-        finish_step_kernel_rn<<<1, 1, 0, main>>>(loss_dev.as<double>(), flags_dev.as<Flags>(), hist_loss.as<double>(),
-                                                 hist_flags.as<Flags>(), hist_cap, &ctrl_dev.as<Control>()->step);
-        CDP_CUDA(cudaGetLastError());
-        ++kernels_per_step;
+        L("finish_step", 0, 0, main, [&] {
+            finish_step_kernel_rn<<<1, 1, 0, main>>>(loss_dev.as<double>(), flags_dev.as<Flags>(),
+                                                     hist_loss.as<double>(), hist_flags.as<Flags>(), hist_cap,
+                                                     &ctrl_dev.as<Control>()->step);
+            CDP_CUDA(cudaGetLastError());
+        });
+        (void)c0;
     }
 
     void capture() {
@@ -731,7 +975,7 @@ struct ResNetTrainer {
         CDP_CUDA(cudaMemcpy(host, theta[slot], size_t(P) * 4, cudaMemcpyDeviceToHost));
     }
 
-    void step(const int *perm, float lr) {
+    void stage_control(const int *perm, float lr) {
         const int k = stage_next;
         stage_next = (stage_next + 1) % RING_N;
         CDP_CUDA(cudaEventSynchronize(stage_ev[k]));
@@ -743,8 +987,44 @@ struct ResNetTrainer {
         CDP_CUDA(cudaMemcpyAsync(ctrl_dev.p, blk, sizeof(Control), cudaMemcpyHostToDevice, main));
         CDP_CUDA(cudaMemcpyAsync(perm_dev.p, blk + sizeof(Control), size_t(B) * 4, cudaMemcpyHostToDevice, main));
         CDP_CUDA(cudaEventRecord(stage_ev[k], main));
+    }
+
+    void step(const int *perm, float lr) {
+        stage_control(perm, lr);
         CDP_CUDA(cudaGraphLaunch(exec[t & 1], main));
         ++t;
+    }
+
+    // End-to-end step: this step's images / labels come from host memory (copied
+    // H2D inside the step, into dataset rows 0..B-1), then the step runs on them.
+    void step_host_batch(const float *x, const int32_t *labels, float lr) {
+        const size_t img = size_t(Hin) * Win * Cin0;
+        CDP_CUDA(cudaMemcpyAsync(data_x.p, x, size_t(B) * img * 4, cudaMemcpyHostToDevice, main));
+        CDP_CUDA(cudaMemcpyAsync(data_lab.p, labels, size_t(B) * 4, cudaMemcpyHostToDevice, main));
+        std::vector<int> ident(B);
+        for (int i = 0; i < B; ++i) ident[i] = i;
+        step(ident.data(), lr);
+    }
+
+    // One real training step run eagerly (not from the graph) with timing events
+    // around every launch; returns the per-launch records.
+    void profile_step(const int *perm, float lr) {
+        stage_control(perm, lr);
+        clear_oprecs();
+        instr = true;
+        try {
+            if (kind == 0)
+                record_step<0>(t & 1);
+            else
+                record_step<1>(t & 1);
+        } catch (...) {
+            instr = false;
+            throw;
+        }
+        instr = false;
+        ++t;
+        CDP_CUDA(cudaStreamSynchronize(main));
+        CDP_CUDA(cudaDeviceSynchronize());
     }
 };
 
@@ -756,20 +1036,26 @@ struct cdp_resnet {
     std::unique_ptr<ResNetTrainer> impl;
 };
 
-extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const int32_t *depths, int in_channels,
-                                      int height, int width, int classes, int micro_batch, int world, int rank,
-                                      const int32_t *tensor_stage, const uint8_t *stage_fresh, int dtype,
-                                      float momentum, float weight_decay, int n_samples, const float *x,
-                                      const int32_t *labels, cdp_resnet **out) {
+extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const int32_t *depths, int block_kind,
+                                      int stem_kind, int in_channels, int height, int width, int classes,
+                                      int micro_batch, int world, int rank, const int32_t *tensor_stage,
+                                      const uint8_t *stage_fresh, int dtype, float momentum, float weight_decay,
+                                      int n_samples, const float *x, const int32_t *labels, cdp_resnet **out) {
     return guarded([&] {
         CDP_REQUIRE(dtype == CDP_DTYPE_FP32 || dtype == CDP_DTYPE_BF16, "bad dtype");
         CDP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
         CDP_REQUIRE(micro_batch >= 1 && micro_batch <= 256, "micro-batch must be in [1, 256]");
         CDP_REQUIRE(n_layers >= 1 && n_layers <= 8, "1..8 residual stages");
-        for (int l = 0; l < n_layers; ++l) CDP_REQUIRE(widths[l] % 64 == 0 && widths[l] <= 512, "widths: multiples of 64 up to 512");
+        CDP_REQUIRE(block_kind == 0 || block_kind == 1, "block_kind: 0 basic, 1 bottleneck");
+        CDP_REQUIRE(stem_kind == 0 || stem_kind == 1, "stem_kind: 0 CIFAR 3x3, 1 ImageNet 7x7 + max pool");
+        CDP_REQUIRE(in_channels >= 1 && in_channels <= 4, "stem input channels: 1..4");
+        for (int l = 0; l < n_layers; ++l)
+            CDP_REQUIRE(widths[l] % 64 == 0 && widths[l] <= 512, "widths: multiples of 64 up to 512");
         auto tr = std::make_unique<ResNetTrainer>();
         tr->kind = dtype == CDP_DTYPE_BF16 ? 0 : 1;
         tr->B = micro_batch;
+        tr->block_kind = block_kind;
+        tr->stem_kind = stem_kind;
         tr->Cin0 = in_channels;
         tr->Hin = height;
         tr->Win = width;
@@ -778,6 +1064,12 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
         tr->wd = weight_decay;
         tr->rank = rank;
         tr->world = world;
+        tr->n_samples = std::max(n_samples, micro_batch);
+        const int HWC = height * width * in_channels;
+        tr->data_x = DevBuf(size_t(tr->n_samples) * HWC * 4);
+        tr->data_lab = DevBuf(size_t(tr->n_samples) * 4);
+        if (x) CDP_CUDA(cudaMemcpy(tr->data_x.p, x, size_t(n_samples) * HWC * 4, cudaMemcpyHostToDevice));
+        if (labels) CDP_CUDA(cudaMemcpy(tr->data_lab.p, labels, size_t(n_samples) * 4, cudaMemcpyHostToDevice));
         tr->build(widths, depths, n_layers);
         for (size_t i = 0; i < tr->tens.size(); ++i) {
             const int st = tensor_stage[i];
@@ -785,12 +1077,6 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
             tr->tens[i].stage = st;
             tr->tens[i].fresh = stage_fresh[st - 1] != 0;
         }
-        tr->n_samples = std::max(n_samples, micro_batch);
-        const int HWC = height * width * in_channels;
-        tr->data_x = DevBuf(size_t(tr->n_samples) * HWC * 4);
-        tr->data_lab = DevBuf(size_t(tr->n_samples) * 4);
-        if (x) CDP_CUDA(cudaMemcpy(tr->data_x.p, x, size_t(n_samples) * HWC * 4, cudaMemcpyHostToDevice));
-        if (labels) CDP_CUDA(cudaMemcpy(tr->data_lab.p, labels, size_t(n_samples) * 4, cudaMemcpyHostToDevice));
         *out = new cdp_resnet{std::move(tr)};
     });
 }
@@ -855,6 +1141,36 @@ extern "C" int cdp_resnet_step(cdp_resnet *tr, const int32_t *perm, float lr) {
     return guarded([&] { tr->impl->step(perm, lr); });
 }
 
+extern "C" int cdp_resnet_step_host_batch(cdp_resnet *tr, const float *x, const int32_t *labels, float lr) {
+    return guarded([&] { tr->impl->step_host_batch(x, labels, lr); });
+}
+
+extern "C" int cdp_resnet_last_loss(cdp_resnet *tr, double *loss) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        CDP_CUDA(cudaMemcpy(loss, m.loss_dev.p, 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+extern "C" int cdp_resnet_profile_step(cdp_resnet *tr, const int32_t *perm, float lr, int max_ops, char *names,
+                                       int name_len, double *flops, double *bytes, float *ms, int *n_ops) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        m.profile_step(perm, lr);
+        const int n = std::min<int>(max_ops, int(m.oprecs.size()));
+        *n_ops = int(m.oprecs.size());
+        for (int i = 0; i < n; ++i) {
+            const OpRec &o = m.oprecs[i];
+            std::strncpy(names + size_t(i) * name_len, o.name.c_str(), name_len - 1);
+            names[size_t(i) * name_len + name_len - 1] = 0;
+            flops[i] = o.flops;
+            bytes[i] = o.bytes;
+            CDP_CUDA(cudaEventElapsedTime(&ms[i], o.a, o.b));
+        }
+    });
+}
+
 extern "C" int cdp_resnet_history(cdp_resnet *tr, int max, double *losses, uint32_t *flags, int *count) {
     return guarded([&] {
         auto &m = *tr->impl;
@@ -890,17 +1206,20 @@ extern "C" int cdp_resnet_ring_error(cdp_resnet *tr, int *err) {
 }
 
 extern "C" int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out) {
-    // [0] activation bytes (activations, conv outputs, dy), [1] parameter-state bytes, [2] kernels / step
+    // [0] activation bytes (activations, conv outputs, dy, stem record), [1] parameter-state bytes,
+    // [2] kernels / step, [3] tensor-core flops / step, [4] fp32 gradient scratch bytes
     return guarded([&] {
         auto &m = *tr->impl;
-        int64_t act = 0;
+        int64_t act = int64_t(m.cols.hi.bytes + m.cols.lo.bytes);
         for (auto &a : m.acts) act += int64_t(a.hi.bytes + a.lo.bytes);
         for (auto &c : m.convs) act += int64_t(c.y.bytes + c.dy.hi.bytes + c.dy.lo.bytes);
         int64_t par = int64_t(m.Pp) * 12 + int64_t(m.vel.bytes);
         for (int v = 0; v < 2; ++v)
             for (auto &w : m.wc[v]) par += int64_t(w.hi.bytes + w.lo.bytes);
-        int64_t vals[3] = {act, par, m.kernels_per_step};
-        for (int i = 0; i < n_out && i < 3; ++i) out[i] = vals[i];
+        int64_t scratch = int64_t(m.dcols.bytes);
+        for (auto &g : m.gbuf) scratch += int64_t(g.bytes);
+        int64_t vals[5] = {act, par, m.kernels_per_step, int64_t(m.flops_per_step), scratch};
+        for (int i = 0; i < n_out && i < 5; ++i) out[i] = vals[i];
     });
 }
 

@@ -1,4 +1,5 @@
-"""BasicBlock ResNets on the device trainer (BASELINE configs[1]: ResNet-18, CIFAR-10 shape).
+"""ResNets on the device trainer (BASELINE configs[1]: ResNet-18, CIFAR-10 shape; configs[2,4]: ResNet-50,
+ImageNet shape).
 
 The reference has no ResNet; this is the north star's "layer
 compute of the named models" for the CDP step, parity-checked against a
@@ -8,6 +9,8 @@ unpinned" by the reference).  Conventions:
 * ResNet-18 CIFAR variant (`PAPER.md:312`): 3x3 stride-1 stem, no max-pool,
   stages of BasicBlocks (widths 64/128/256/512, depths 2/2/2/2), 1x1
   projection shortcuts, global average pool, linear classifier.
+* ResNet-50 (torchvision v1.5 layout): 7x7/s2 stem + 3x3/s2 max pool,
+  Bottleneck blocks (1x1, 3x3 with the stride, 1x1 x4), depths 3/4/6/3.
 * Batch norm in training mode with per-micro-batch statistics; running
   statistics are not tracked (SURVEY §7 hard part 4 — one convention fixed).
 * Parameter tensors in torchvision `named_parameters` order; flat layout per
@@ -24,31 +27,47 @@ import numpy as np
 from . import _native as N
 from .device import DTYPES
 
-RESNET18 = dict(widths=(64, 128, 256, 512), depths=(2, 2, 2, 2))
+RESNET18 = dict(widths=(64, 128, 256, 512), depths=(2, 2, 2, 2), block="basic", stem="cifar")
+RESNET50 = dict(widths=(64, 128, 256, 512), depths=(3, 4, 6, 3), block="bottleneck", stem="imagenet")
+BLOCKS = {"basic": 0, "bottleneck": 1}
+STEMS = {"cifar": 0, "imagenet": 1}
 
 
-def layer_specs(widths, depths, in_ch=3, hw=32):
-    """[(kind, shape, flops_per_sample)] per tensor, in the trainer's order."""
+def layer_specs(widths, depths, in_ch=3, hw=32, block="basic", stem="cifar", classes=10):
+    """[(kind, shape, flops_per_sample)] per parameter tensor, in the trainer's (torchvision) order.
+
+    flops = forward + backward (data and weight gradients) tensor-core flops of the conv."""
     out = []
-    H = hw
 
-    def conv(cin, cout, r, stride, H):
-        Ho = (H + 2 * (r // 2) - r) // stride + 1
+    def conv(cin, cout, r, stride, H, pad=None):
+        pad = r // 2 if pad is None else pad
+        Ho = (H + 2 * pad - r) // stride + 1
         out.append(("conv", (r, r, cin, cout), 2 * 3 * r * r * cin * cout * Ho * Ho))
         out.append(("bn", (2 * cout,), 0))
         return Ho
 
-    H = conv(in_ch, widths[0], 3, 1, H)
+    H = hw
+    if stem == "cifar":
+        H = conv(in_ch, widths[0], 3, 1, H)
+    else:
+        H = conv(in_ch, widths[0], 7, 2, H, pad=3)
+        H = (H + 2 - 3) // 2 + 1
     cin = widths[0]
+    exp = 4 if block == "bottleneck" else 1
     for l, (w, d) in enumerate(zip(widths, depths)):
         for k in range(d):
             stride = 2 if (l > 0 and k == 0) else 1
-            Ho = conv(cin, w, 3, stride, H)
-            conv(w, w, 3, 1, Ho)
-            if stride != 1 or cin != w:
-                conv(cin, w, 1, stride, H)
-            cin, H = w, Ho
-    out.append(("fc", (cin + 1, 10), 0))
+            if block == "basic":
+                Ho = conv(cin, w, 3, stride, H)
+                conv(w, w, 3, 1, Ho)
+            else:
+                conv(cin, w, 1, 1, H)
+                Ho = conv(w, w, 3, stride, H)
+                conv(w, w * exp, 1, 1, Ho)
+            if stride != 1 or cin != w * exp:
+                conv(cin, w * exp, 1, stride, H)
+            cin, H = w * exp, Ho
+    out.append(("fc", (cin + 1, classes), 2 * 3 * cin * classes))
     return out
 
 
@@ -73,7 +92,7 @@ def stage_partition(specs, n_stages):
 
 # ----------------------------------------------------------------------------- layout conversion
 def torch_to_flat(model) -> np.ndarray:
-    """torch ResNet (oracle/resnet_torch.CifarResNet) -> flat float64 theta in the trainer layout."""
+    """torch ResNet (oracle/resnet_torch.TorchResNet) -> flat float64 theta in the trainer layout."""
     parts = []
     for name, p in _ordered(model):
         a = p.detach().double().cpu().numpy()
@@ -96,13 +115,12 @@ def flat_to_tensors(flat: np.ndarray, specs) -> list:
 
 
 def _ordered(model):
-    """(name, tensor-or-pair) in trainer order, from the oracle torch model."""
+    """(name, tensor-or-pair) in trainer order, from an oracle torch model (oracle/resnet_torch.TorchResNet)."""
     items = [("stem.conv", model.stem_conv.weight), ("stem.bn", (model.stem_bn.weight, model.stem_bn.bias))]
     for bi, b in enumerate(model.blocks):
-        items.append((f"b{bi}.c1.conv", b.conv1.weight))
-        items.append((f"b{bi}.c1.bn", (b.bn1.weight, b.bn1.bias)))
-        items.append((f"b{bi}.c2.conv", b.conv2.weight))
-        items.append((f"b{bi}.c2.bn", (b.bn2.weight, b.bn2.bias)))
+        for ci, (cv, bn) in enumerate(zip(b.convs, b.bns)):
+            items.append((f"b{bi}.c{ci}.conv", cv.weight))
+            items.append((f"b{bi}.c{ci}.bn", (bn.weight, bn.bias)))
         if b.ds_conv is not None:
             items.append((f"b{bi}.ds.conv", b.ds_conv.weight))
             items.append((f"b{bi}.ds.bn", (b.ds_bn.weight, b.ds_bn.bias)))
@@ -139,15 +157,17 @@ def _i32p(a):
 
 
 class DeviceResNet:
-    """One rank (worker) of CDP training of a BasicBlock ResNet on this process's GPU."""
+    """One rank (worker) of CDP training of a ResNet (BasicBlock / Bottleneck, CIFAR / ImageNet stem)
+    on this process's GPU."""
 
     def __init__(self, widths=RESNET18["widths"], depths=RESNET18["depths"], micro_batch=128, world=1, rank=0,
                  rule=None, dtype="bf16", momentum=0.0, weight_decay=0.0, inputs=None, labels=None, classes=10,
-                 image_hw=32, stage_of_tensor=None):
+                 image_hw=32, stage_of_tensor=None, block="basic", stem="cifar"):
         self.lib = N.lib()
         self.widths, self.depths = tuple(widths), tuple(depths)
+        self.block, self.stem, self.classes, self.image_hw = block, stem, int(classes), int(image_hw)
         self.micro_batch, self.world, self.rank = int(micro_batch), int(world), int(rank)
-        self.specs = layer_specs(self.widths, self.depths, 3, image_hw)
+        self.specs = layer_specs(self.widths, self.depths, 3, image_hw, block, stem, classes)
         n_t = len(self.specs)
         self.stage = np.ascontiguousarray(stage_of_tensor if stage_of_tensor is not None
                                           else stage_partition(self.specs, world), dtype=np.int32)
@@ -168,7 +188,7 @@ class DeviceResNet:
             n = x.shape[0]
         h = ctypes.c_void_p()
         N.check(self.lib.cdp_resnet_create_rank(
-            len(w), _i32p(w), _i32p(d), 3, image_hw, image_hw, classes, self.micro_batch, world, rank,
+            len(w), _i32p(w), _i32p(d), BLOCKS[block], STEMS[stem], 3, image_hw, image_hw, classes, self.micro_batch, world, rank,
             _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), DTYPES[dtype], float(momentum), float(weight_decay),
             n, x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
             ctypes.byref(h)))
@@ -220,6 +240,41 @@ class DeviceResNet:
         assert p.size == self.micro_batch
         N.check(self.lib.cdp_resnet_step(self.h, _i32p(p), float(lr)))
 
+    def step_host_batch_ptr(self, x_ptr: int, y_ptr: int, lr: float):
+        """End-to-end step from raw (pinned) host pointers: x fp32 NHWC [B][H][W][3], y int32 labels."""
+        N.check(self.lib.cdp_resnet_step_host_batch(self.h, ctypes.cast(x_ptr, N.c_float_p),
+                                                    ctypes.cast(y_ptr, ctypes.POINTER(ctypes.c_int)), float(lr)))
+
+    def step_host_batch(self, x, y, lr):
+        xa = np.ascontiguousarray(x, dtype=np.float32)
+        ya = np.ascontiguousarray(y, dtype=np.int32)
+        assert xa.shape[0] == self.micro_batch and ya.shape[0] == self.micro_batch
+        self.step_host_batch_ptr(xa.ctypes.data, ya.ctypes.data, lr)
+        self._keep_step = (xa, ya)
+
+    def last_loss(self) -> float:
+        out = ctypes.c_double()
+        N.check(self.lib.cdp_resnet_last_loss(self.h, ctypes.byref(out)))
+        return out.value
+
+    def profile_step(self, perm, lr, max_ops=4096):
+        """One real training step, launched eagerly with CUDA events around every kernel (on the stream it is
+        launched on).  Returns [(name, flops, bytes, ms)] in launch order."""
+        p = np.ascontiguousarray(perm, dtype=np.int32)
+        NL = 48
+        names = ctypes.create_string_buffer(max_ops * NL)
+        fl = np.zeros(max_ops)
+        by = np.zeros(max_ops)
+        ms = np.zeros(max_ops, dtype=np.float32)
+        n = ctypes.c_int()
+        N.check(self.lib.cdp_resnet_profile_step(self.h, _i32p(p), float(lr), max_ops, names, NL,
+                                                 fl.ctypes.data_as(N.c_double_p), by.ctypes.data_as(N.c_double_p),
+                                                 ms.ctypes.data_as(N.c_float_p), ctypes.byref(n)))
+        k = min(n.value, max_ops)
+        raw = names.raw
+        return [(raw[i * NL:(i + 1) * NL].split(b"\0", 1)[0].decode(), float(fl[i]), float(by[i]), float(ms[i]))
+                for i in range(k)]
+
     def history(self, max_steps=1 << 14):
         losses = np.empty(max_steps)
         flags = np.empty((max_steps, 3), dtype=np.uint32)
@@ -238,9 +293,10 @@ class DeviceResNet:
         return e.value
 
     def stats(self) -> dict:
-        out = np.zeros(3, dtype=np.int64)
-        N.check(self.lib.cdp_resnet_stats(self.h, out.ctypes.data_as(N.c_int64_p), 3))
-        return {"activation_bytes": int(out[0]), "param_state_bytes": int(out[1]), "kernels_per_step": int(out[2])}
+        out = np.zeros(5, dtype=np.int64)
+        N.check(self.lib.cdp_resnet_stats(self.h, out.ctypes.data_as(N.c_int64_p), 5))
+        return {"activation_bytes": int(out[0]), "param_state_bytes": int(out[1]), "kernels_per_step": int(out[2]),
+                "tensor_flops_per_step": int(out[3]), "gradient_scratch_bytes": int(out[4])}
 
     def mark(self, k):
         N.check(self.lib.cdp_resnet_mark(self.h, k))
@@ -266,6 +322,11 @@ class DeviceResNet:
             self.close()
         except Exception:
             pass
+
+
+def synthetic_images(n, seed=0, hw=32, classes=10):
+    """x ~ N(0,1) NHWC [n][hw][hw][3] float32, labels uniform in [0, classes) from default_rng([seed, 0xD0])."""
+    return synthetic_cifar(n, seed, hw, classes)
 
 
 def synthetic_cifar(n, seed=0, hw=32, classes=10):

@@ -12,22 +12,26 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 W, D, HW, MB = (64, 128), (1, 1), 16, 8
+ARCH = {"basic": dict(block="basic", stem="cifar", hw=16, classes=10),
+        "bottleneck": dict(block="bottleneck", stem="imagenet", hw=32, classes=100)}
 
 
-def _data(n, seed=0):
+def _data(n, seed=0, hw=HW, classes=10):
     from paper_2403_08837_b200.resnet import synthetic_cifar
 
-    return synthetic_cifar(n, seed, hw=HW)
+    return synthetic_cifar(n, seed, hw=hw, classes=classes)
 
 
-def _ranks(world, rule, dtype, steps, momentum=0.9):
+def _ranks(world, rule, dtype, steps, momentum=0.9, arch="basic"):
     from oracle.resnet_torch import init_flat
     from paper_2403_08837_b200.resnet import DeviceResNet
 
-    x, y = _data(world * MB * 2)
-    init = init_flat(W, D, seed=0)
+    a = ARCH[arch]
+    x, y = _data(world * MB * 2, hw=a["hw"], classes=a["classes"])
+    init = init_flat(W, D, seed=0, block=a["block"], stem=a["stem"], classes=a["classes"])
     perms = [np.random.default_rng([5, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
-    tr = [DeviceResNet(W, D, MB, world, r, rule, dtype, momentum, inputs=x, labels=y, image_hw=HW)
+    tr = [DeviceResNet(W, D, MB, world, r, rule, dtype, momentum, inputs=x, labels=y, image_hw=a["hw"],
+                       block=a["block"], stem=a["stem"], classes=a["classes"])
           for r in range(world)]
     regions = [t.region() for t in tr]
     for t in tr:
@@ -47,23 +51,26 @@ def _ranks(world, rule, dtype, steps, momentum=0.9):
     return init, x, y, perms, losses, final, stage
 
 
-def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9):
+def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9, arch="basic"):
     from oracle.resnet_torch import run_cdp
 
     fresh = None
     if rule is not None:
         fresh = [[rule.reads_fresh(i, int(s)) for s in stage] for i in range(1, world + 1)]
-    return run_cdp(W, D, init, x.astype(np.float64), y, world, MB, perms, 0.05, momentum, fresh)
+    a = ARCH[arch]
+    return run_cdp(W, D, init, x.astype(np.float64), y, world, MB, perms, 0.05, momentum, fresh, block=a["block"],
+                   stem=a["stem"], classes=a["classes"])
 
 
 def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
 
 
+@pytest.mark.parametrize("arch", ["basic", "bottleneck"])
 @pytest.mark.parametrize("dtype,tol", [("fp32", 2e-4), ("bf16", 3e-2)])
-def test_single_gpu_steps_vs_torch_restatement(cuda, dtype, tol):
-    init, x, y, perms, losses, final, stage = _ranks(1, None, dtype, 3)
-    want, wl = _oracle(init, x, y, perms, 1, None, stage)
+def test_single_gpu_steps_vs_torch_restatement(cuda, dtype, tol, arch):
+    init, x, y, perms, losses, final, stage = _ranks(1, None, dtype, 3, arch=arch)
+    want, wl = _oracle(init, x, y, perms, 1, None, stage, arch=arch)
     assert _rel(final, want) <= tol, _rel(final, want)
     assert np.all(np.abs(losses - np.array(wl)) <= tol * np.abs(np.array(wl)) + 1e-6), (losses, wl)
 
@@ -77,3 +84,44 @@ def test_two_ranks_cdp_vs_torch_restatement(cuda, rule_name):
     want, wl = _oracle(init, x, y, perms, 2, rule, stage)
     assert _rel(final, want) <= 2e-4, _rel(final, want)
     assert np.all(np.abs(losses - np.array(wl)) <= 2e-4 * np.abs(np.array(wl))), (losses, wl)
+
+
+@pytest.mark.parametrize("arch", ["basic", "bottleneck"])
+def test_two_ranks_cdp_v2_bottleneck_vs_torch_restatement(cuda, arch):
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = rule_by_name("cdp-v2", 2)
+    init, x, y, perms, losses, final, stage = _ranks(2, rule, "fp32", 3, arch=arch)
+    want, wl = _oracle(init, x, y, perms, 2, rule, stage, arch=arch)
+    assert _rel(final, want) <= 2e-4, _rel(final, want)
+
+
+def test_profile_and_host_batch_steps(cuda):
+    """The instrumented eager step and the host-batch step are real training steps of the same math."""
+    from oracle.resnet_torch import init_flat
+    from paper_2403_08837_b200.resnet import DeviceResNet
+
+    x, y = _data(MB * 2)
+    init = init_flat(W, D, seed=0)
+    res = []
+    for how in ("graph", "profile", "host"):
+        tr = DeviceResNet(W, D, MB, 1, 0, None, "fp32", 0.9, inputs=x, labels=y, image_hw=HW)
+        tr.set_params(init, -1)
+        tr.connect([tr.region()])
+        perm = np.arange(MB)
+        if how == "graph":
+            tr.step(perm, 0.05)
+        elif how == "profile":
+            ops = tr.profile_step(perm, 0.05)
+            names = {o[0] for o in ops}
+            assert {"conv_fprop", "conv_dgrad", "conv_wgrad_hop", "bn_apply", "stem_fprop"} <= names, names
+            assert all(o[3] > 0 for o in ops)
+            assert len(ops) == tr.stats()["kernels_per_step"]
+        else:
+            tr.step_host_batch(x[:MB], y[:MB], 0.05)
+        tr.sync()
+        res.append((tr.history(1)[0][0], tr.get_params(0)))
+        tr.close()
+    for loss, params in res[1:]:
+        assert loss == res[0][0]
+        assert np.array_equal(params, res[0][1])

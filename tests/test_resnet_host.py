@@ -49,3 +49,48 @@ def test_oracle_gradients_match_autograd_layout():
         f2[base + k] += eps
         l2, _ = orc.loss_and_grads(flat_to_tensors(f2, specs), x, y)
         assert abs((l2 - loss) / eps - grads[t_idx][k]) < 1e-4 * max(1.0, abs(grads[t_idx][k]))
+
+
+def test_resnet50_parameter_count_matches_torchvision():
+    from paper_2403_08837_b200.resnet import RESNET50
+
+    specs = layer_specs(**RESNET50, classes=1000, hw=224)
+    assert sum(int(np.prod(s)) for _, s, _ in specs) == 25_557_032
+    assert len(specs) == 107
+
+
+def test_resnet50_layout_matches_torchvision_order():
+    """Our tensor order / shapes == torchvision.models.resnet50 named_parameters (conv/bn/fc)."""
+    import torchvision
+
+    from paper_2403_08837_b200.resnet import RESNET50
+
+    tv = torchvision.models.resnet50(num_classes=1000)
+    shapes = []
+    for name, p in tv.named_parameters():
+        if name.endswith("bn1.bias") or ".bn" in name and name.endswith("bias") or name.endswith("downsample.1.bias"):
+            continue
+        shapes.append(tuple(p.shape))
+    ours = []
+    for kind, shape, _ in layer_specs(**RESNET50, classes=1000, hw=224):
+        if kind == "conv":
+            r, s, cin, cout = shape
+            ours.append((cout, cin, r, s))
+        elif kind == "bn":
+            ours.append((shape[0] // 2,))
+        else:
+            ours.append((shape[1], shape[0] - 1))
+            ours.append((shape[1],))
+    assert ours == shapes
+
+
+def test_bottleneck_imagenet_layout_roundtrip():
+    from oracle.resnet_torch import TorchResNet
+
+    w, d = (64, 128), (1, 1)
+    specs = layer_specs(w, d, hw=32, block="bottleneck", stem="imagenet")
+    flat = init_flat(w, d, seed=3, block="bottleneck", stem="imagenet")
+    assert flat.size == sum(int(np.prod(s)) for _, s, _ in specs)
+    m = TorchResNet(w, d, 10, "bottleneck", "imagenet").double()
+    load_flat(m, flat, specs)
+    assert np.array_equal(torch_to_flat(m), flat)
