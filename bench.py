@@ -1,31 +1,35 @@
 #!/usr/bin/env python
-"""CDP training-step benchmark on B200 (contract: DESIGN.md §Measurement).
+"""CDP training-step benchmark on B200 (contract: DESIGN.md §8 Measurement).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--dtype bf16|fp32] [--rule cdp-v2|cdp-v1|dp]
+                    [--model resnet18|resnet50|mlp] [--dtype bf16|fp32] [--rule cdp-v2|cdp-v1|dp]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Workload (round 1; ResNet / ViT layer kernels are not built yet, DESIGN.md
-§Scope): BASELINE configs[1]'s structure — CDP-v2, ONE micro-batch per GPU,
-N = micro-batches = stages = GPUs — on the stage MLP family of configs[0]:
-an 8-layer tanh MLP 3072-256x7-10 (softmax-xent, SGD lr 0.05 momentum 0.9),
-micro-batch B = 128 per GPU, the 8 layers grouped into N contiguous stages.
-Per-GPU work is the same at every N (weak scaling).  One step = one training
-step of the whole job: every rank's forward + backward, the per-layer
-gradient hops rank -> rank+1 over peer memory, the fused update on the last
-rank, the parameter pulls — one CUDA graph per rank, no collective.
-
-At N = 1 the line also carries `single_gpu_cdp`: configs[0] itself (4-layer
-3072-256-256-256-10, 4 micro-batches of 32 on one GPU, CDP-v1), the
-reference's own CPU-runnable case, with its CPU time beside it.
+Headline workload (default, --model resnet18) = BASELINE configs[1]:
+ResNet-18 (CIFAR variant: 3x3 stem, no max pool) on CIFAR-10-shaped synthetic
+data (32x32x3, 10 classes), CDP-v2, ONE micro-batch of B = 128 per GPU,
+N = micro-batches = stages = GPUs (FLOP-balanced contiguous tensor groups),
+SGD lr 0.05 momentum 0.9, bf16 operands / fp32 master state.  One step = the
+whole job's training step: every rank's forward + backward, the per-tensor
+gradient hops rank -> rank+1 over peer memory fused into the weight-gradient
+GEMM epilogues, the fused update on the last rank, the parameter pulls; one
+CUDA graph per rank, no collective.  Per-GPU work is fixed as N grows (weak
+scaling).
 
 `value` = samples/s of the device-timed step (CUDA events on each rank's
-trainer stream around each graph launch, inputs resident in HBM, L2 flushed
-by a 256 MiB memset before every timed step, max over ranks); `e2e` = the
-same through the public API from pinned host inputs copied H2D inside every
-step with the step loss read back every step.  `--impl reference` times the
-reference's own CPU implementation (its compiled Cython kernel, oracle/_ref,
-under the restated engine loop) with one process per micro-batch.
+launch stream around each graph launch, inputs resident in HBM, L2 flushed by
+a 256 MiB memset before every timed step, max over ranks); `e2e` = the same
+through the public API with the step's images / labels copied H2D from pinned
+host memory inside every step and the loss read back every step.  `roofline`
+= the dominant tensor-core kernel class of a serialised instrumented step
+(algorithmic conv flops / event-timed duration) against MEASURED_PEAKS.json.
+At N = 1 the line also carries `resnet50` (BASELINE configs[2] shape on one
+GPU: ResNet-50 224x224, B = 128, bf16, CDP-v2) and `single_gpu_cdp`
+(configs[0]: the reference's own CPU-runnable MLP case with its CPU time).
+`cpu_baseline` / `--impl reference`: the reference has no ResNet,
+so the CPU arm is the oracle port (oracle/resnet_torch.py: the reference's
+`_advance` semantics over torch-CPU float64 autograd) on all host cores, on a
+bounded sample of the same workload.
 """
 
 from __future__ import annotations
@@ -46,6 +50,8 @@ sys.path.insert(0, ROOT)
 with open(os.path.join(ROOT, "BASELINE.json")) as _fh:
     METRIC = json.load(_fh)["metric"]
 UNIT = "samples/s"
+RN_MB = 128
+RN_LR, RN_MOMENTUM = 0.05, 0.9
 DEEP_DIMS = (3072,) + (256,) * 7 + (10,)
 MB = 128
 CONFIG1 = dict(n=4, micro_batch_size=32, seed=0, width=256, in_dim=3072, out_dim=10, loss_kind="xent")
@@ -325,6 +331,203 @@ def run_ours(args, ws, rank, local):
     return out, task, rule, ls
 
 
+# ----------------------------------------------------------------------------- ResNet arm
+def resnet_cfg(model):
+    from paper_2403_08837_b200.resnet import RESNET18, RESNET50
+
+    if model == "resnet18":
+        return dict(RESNET18), 32, 10
+    return dict(RESNET50), 224, 1000
+
+
+def peak_tensor():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["bf16_tflops"]), "measured (burst)"
+    except Exception:
+        return 2250.0, "fallback (spec dense bf16)"
+
+
+def kernel_table(ops):
+    """Group an instrumented step's launches by kernel class: {name: [launches, ms, flops, bytes]}."""
+    agg = {}
+    for name, fl, by, ms in ops:
+        a = agg.setdefault(name, [0, 0.0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += ms
+        a[2] += fl
+        a[3] += by
+    return agg
+
+
+def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
+    import torch
+
+    from paper_2403_08837_b200.dist import exchange_handles, resolve
+    from paper_2403_08837_b200.resnet import DeviceResNet, init_params, layer_specs, synthetic_images
+
+    torch.cuda.set_device(local)
+    cfg, hw, classes = resnet_cfg(model)
+    B = RN_MB
+    rule = resolve(args.rule, ws)
+    n_data = 2 * B * ws
+    x, y = synthetic_images(n_data, seed=0, hw=hw, classes=classes)
+    specs = layer_specs(cfg["widths"], cfg["depths"], 3, hw, cfg["block"], cfg["stem"], classes)
+    tr = DeviceResNet(cfg["widths"], cfg["depths"], B, ws, rank, rule, args.dtype, RN_MOMENTUM, inputs=x, labels=y,
+                      classes=classes, image_hw=hw, block=cfg["block"], stem=cfg["stem"])
+    tr.set_params(init_params(specs, seed=0), -1)
+    if ws > 1:
+        tr.connect_ipc(exchange_handles(tr.ipc_handle()))
+    else:
+        tr.connect([tr.region()])
+    perms = [np.random.default_rng([0, t]).permutation(n_data)[rank * B:(rank + 1) * B]
+             for t in range(1, warmup + steps + 8)]
+    for t in range(warmup):
+        tr.step(perms[t], RN_LR)
+    tr.sync()
+    if ws > 1:
+        torch.distributed.barrier()
+    with ClockSampler(local) as clk:
+        for k in range(steps):
+            tr.flush_l2()
+            tr.mark(2 * k)
+            tr.step(perms[warmup + k], RN_LR)
+            tr.mark(2 * k + 1)
+        tr.sync()
+    if tr.ring_error():
+        raise RuntimeError(f"rank {rank}: ring protocol timed out")
+    ms = float(np.mean([tr.elapsed(2 * k, 2 * k + 1) for k in range(steps)]))
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    losses, flags = tr.history(steps + warmup)
+    assert np.all(np.isfinite(losses)) and not flags.any(), "non-finite step in the timed region"
+    st = tr.stats()
+    out = {"value": round(ws * B / (ms / 1e3), 1), "ms_per_step": round(ms, 4), "clocks": clk.summary(),
+           "losses_first_last": [round(float(losses[0]), 5), round(float(losses[-1]), 5)],
+           "activation_bytes": {"per_gpu": st["activation_bytes"], "sum_over_gpus": st["activation_bytes"] * ws},
+           "param_state_bytes": st["param_state_bytes"], "gpu_launches": st["kernels_per_step"] * steps,
+           "tensor_flops_per_step": st["tensor_flops_per_step"],
+           "tensor_tflops_per_s": round(st["tensor_flops_per_step"] / (ms / 1e3) / 1e12, 1)}
+    # ---- e2e: public API, pinned host images copied H2D every step, loss read back every step
+    if e2e:
+        x_pin = torch.empty((B, hw, hw, 3), dtype=torch.float32, pin_memory=True)
+        y_pin = torch.empty((B,), dtype=torch.int32, pin_memory=True)
+        host = [(x[p], y[p]) for p in perms[:steps + 2]]
+        e_ms = []
+        if ws > 1:
+            torch.distributed.barrier()
+        for k in range(min(steps, 20) + 2):
+            x_pin.numpy()[:] = host[k][0]
+            y_pin.numpy()[:] = host[k][1]
+            tr.flush_l2()
+            tr.mark(0)
+            tr.step_host_batch_ptr(x_pin.data_ptr(), y_pin.data_ptr(), RN_LR)
+            loss = tr.last_loss()
+            tr.mark(1)
+            assert np.isfinite(loss)
+            if k >= 2:
+                e_ms.append(tr.elapsed(0, 1))
+        e = float(np.mean(e_ms))
+        if ws > 1:
+            t = torch.tensor([e], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e = float(t.item())
+        out["e2e"] = {"value": round(ws * B / (e / 1e3), 1), "unit": UNIT,
+                      "h2d_bytes_per_step": B * hw * hw * 3 * 4 + B * 4 + 16 + B * 4, "d2h_bytes_per_step": 8,
+                      "ms_per_step": round(e, 4)}
+    # ---- per-kernel breakdown: one serialised instrumented (real) step
+    ops = tr.profile_step(perms[warmup + steps], RN_LR, serial=True)
+    agg = kernel_table(ops)
+    tot = sum(a[1] for a in agg.values())
+    gemm = {k: a for k, a in agg.items() if a[2] > 0}
+    dom = max(gemm, key=lambda k: gemm[k][1])
+    d = gemm[dom]
+    peak, src = peak_tensor()
+    achieved = d[2] / (d[1] / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r1_resnet_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = (json.load(fh).get(f"{model}-{args.dtype}-{dom}") or {}).get("dram_bytes_per_launch")
+    out["roofline"] = {"bound": "tensor", "kernel": f"{dom} (gemm_tc_kernel, tcgen05 + TMA; {d[0]} launches)",
+                       "achieved": round(achieved, 1), "peak": peak, "peak_source": src, "unit": "TFLOP/s",
+                       "frac": round(achieved / peak, 4), "traffic": traffic,
+                       "algorithmic_flops_per_launch": round(d[2] / d[0]), "launch_us": round(d[1] / d[0] * 1e3, 2),
+                       "share_of_serial_step": round(d[1] / tot, 3)}
+    out["kernel_breakdown"] = {
+        k: {"launches": a[0], "ms": round(a[1], 4), "share": round(a[1] / tot, 3),
+            **({"tflops": round(a[2] / (a[1] / 1e3) / 1e12, 1)} if a[2] else
+               {"gbs": round(a[3] / (a[1] / 1e3) / 1e9, 1)})}
+        for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])}
+    out["serial_step_ms"] = round(tot, 4)
+    tr.close()
+    return out
+
+
+def cpu_resnet_reference(model, ws, rule, sample_images, steps, threads):
+    """The oracle port (oracle/resnet_torch.py, float64 torch-CPU autograd under the reference's `_advance`
+    semantics) on `sample_images` images per micro-batch, one micro-batch per worker, `steps` steps."""
+    import torch
+
+    from oracle.resnet_torch import run_cdp
+    from paper_2403_08837_b200.resnet import init_params, layer_specs, stage_partition, synthetic_images
+
+    torch.set_num_threads(threads)
+    cfg, hw, classes = resnet_cfg(model)
+    specs = layer_specs(cfg["widths"], cfg["depths"], 3, hw, cfg["block"], cfg["stem"], classes)
+    x, y = synthetic_images(sample_images * ws, seed=0, hw=hw, classes=classes)
+    fresh = None
+    if rule is not None:
+        stage = stage_partition(specs, ws)
+        fresh = [[rule.reads_fresh(i, int(s)) for s in stage] for i in range(1, ws + 1)]
+    init = init_params(specs, 0)
+    perms = [np.random.default_rng([0, t]).permutation(len(x)) for t in range(1, steps + 2)]
+    run_cdp(cfg["widths"], cfg["depths"], init, x.astype(np.float64), y, ws, sample_images, perms[:1], RN_LR,
+            RN_MOMENTUM, fresh, block=cfg["block"], stem=cfg["stem"], classes=classes)  # warm-up
+    t0 = time.perf_counter()
+    run_cdp(cfg["widths"], cfg["depths"], init, x.astype(np.float64), y, ws, sample_images, perms[1:steps + 1],
+            RN_LR, RN_MOMENTUM, fresh, block=cfg["block"], stem=cfg["stem"], classes=classes)
+    dt = (time.perf_counter() - t0) / steps
+    return ws * sample_images / dt, dt * 1e3
+
+
+def resnet_workload(model, ws, rule_name, dtype):
+    if model == "resnet18":
+        what = "ResNet-18 CIFAR variant (3x3 stem, no max pool), 32x32x3, 10 classes"
+    else:
+        what = "ResNet-50 (torchvision v1.5 layout), 224x224x3, 1000 classes"
+    return (f"{what}; {rule_name}; one micro-batch of {RN_MB} per GPU; {ws} stage(s) = {ws} GPU(s); {dtype} "
+            f"operands, fp32 master/momentum; SGD lr {RN_LR} momentum {RN_MOMENTUM}")
+
+
+def main_resnet(args, ws, rank, local):
+    from paper_2403_08837_b200.dist import resolve
+
+    model = args.model
+    res = run_resnet(args, ws, rank, local, model, args.steps, args.warmup)
+    if rank != 0:
+        return None
+    peak_note = "configs[1]" if model == "resnet18" else "configs[2] shape"
+    out = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (x ~ N(0,1) NHWC, uniform labels; numpy PCG64), deterministic He-normal init",
+        "config": {"workload": resnet_workload(model, ws, args.rule, args.dtype), "baseline_config": peak_note,
+                   "global_batch": ws * RN_MB, "micro_batch": RN_MB, "stages": ws, "rule": args.rule,
+                   "parallelism": f"cdp{ws} (one process per GPU, P2P gradient hop ring, fused update on rank {ws - 1})",
+                   "l2": "flushed (256 MiB memset) before every timed step"},
+        "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "roofline": res["roofline"],
+        "activation_bytes": res["activation_bytes"], "tensor_tflops_per_s": res["tensor_tflops_per_s"],
+        "clocks": res["clocks"], "kernel_breakdown": res["kernel_breakdown"],
+        "serial_step_ms": res["serial_step_ms"], "losses_first_last": res["losses_first_last"],
+    }
+    return out
+
+
 def single_gpu_config1(dtype):
     """configs[0] on one GPU: 4 micro-batches x 32, 4 stages, CDP-v1 (+ activation bytes vs DP)."""
     from paper_2403_08837_b200.device import DeviceMlpTrainer
@@ -367,9 +570,69 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--rule", default="cdp-v2", choices=["cdp-v2", "cdp-v1", "dp", "dp-allreduce"])
+    ap.add_argument("--model", default="resnet18", choices=["resnet18", "resnet50", "mlp"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the resnet50 / config-1 sub-lines at N=1")
     args = ap.parse_args()
     ws, rank, local = dist_env()
+
+    if args.model != "mlp":
+        if args.rule == "dp-allreduce":
+            raise SystemExit("--rule dp-allreduce is built for --model mlp only")
+        if args.impl == "reference":
+            if rank != 0:
+                return
+            from paper_2403_08837_b200.dist import resolve
+
+            threads = os.cpu_count() or 1
+            n = max(1, min(args.steps, 2))
+            sample = 16 if args.model == "resnet18" else 2
+            sps, ms = cpu_resnet_reference(args.model, ws, resolve(args.rule, ws), sample, n, threads)
+            desc = (f"{n} steps (after 1 warm-up) of the {ws}-micro-batch CDP step on {sample} images per "
+                    f"micro-batch (of {RN_MB}), float64 torch-CPU oracle port, {threads} threads")
+            print(json.dumps({
+                "impl": "reference", "metric": METRIC, "value": round(sps, 3), "unit": UNIT, "n_gpus": ws,
+                "steps": n, "warmup": 1, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": resnet_workload(args.model, ws, args.rule, "fp64")},
+                "cpu_baseline": {"value": round(sps, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                                 "sample": desc, "host_cpus": os.cpu_count()},
+                "e2e": {"value": round(sps, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            }), flush=True)
+            return
+        if ws > 1:
+            import torch
+
+            torch.cuda.set_device(local)
+            torch.distributed.init_process_group("nccl")
+        out = main_resnet(args, ws, rank, local)
+        if rank == 0:
+            if ws == 1 and not args.no_extras:
+                if args.model == "resnet18":
+                    r50 = run_resnet(args, 1, 0, local, "resnet50", 10, 3, e2e=False)
+                    out["resnet50"] = {"workload": resnet_workload("resnet50", 1, args.rule, args.dtype),
+                                       "value": r50["value"], "unit": UNIT, "ms_per_step": r50["ms_per_step"],
+                                       "tensor_tflops_per_s": r50["tensor_tflops_per_s"],
+                                       "roofline": r50["roofline"], "activation_bytes": r50["activation_bytes"],
+                                       "clocks": r50["clocks"], "kernel_breakdown": r50["kernel_breakdown"]}
+                out["single_gpu_cdp"] = single_gpu_config1(args.dtype)
+            if ws == 1 and not args.no_cpu_baseline:
+                threads = os.cpu_count() or 1
+                from paper_2403_08837_b200.dist import resolve
+
+                sample = 16 if args.model == "resnet18" else 2
+                sps, _ms = cpu_resnet_reference(args.model, 1, resolve(args.rule, 1), sample, 2, threads)
+                out["cpu_baseline"] = {"value": round(sps, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                                       "sample": f"2 steps (after 1 warm-up) of the same CDP step on {sample} "
+                                                 f"images (of {RN_MB}), float64 torch-CPU oracle port, "
+                                                 f"{threads} threads", "host_cpus": os.cpu_count()}
+            print(json.dumps(out), flush=True)
+        if ws > 1:
+            import torch
+
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
 
     if args.impl == "reference":
         if rank != 0:

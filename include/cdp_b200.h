@@ -177,9 +177,10 @@ int cdp_resnet_step_host_batch(cdp_resnet *tr, const float *x, const int32_t *la
 /* Loss of the most recent step (synchronises). */
 int cdp_resnet_last_loss(cdp_resnet *tr, double *loss);
 /* One real training step launched eagerly with timing events around every kernel:
- * per launch its name (name_len bytes each), algorithmic flops / bytes and duration. */
-int cdp_resnet_profile_step(cdp_resnet *tr, const int32_t *perm, float lr, int max_ops, char *names, int name_len,
-                            double *flops, double *bytes, float *ms, int *n_ops);
+ * per launch its name (name_len bytes each), algorithmic flops / bytes and duration.
+ * serial != 0: all launches on one stream (clean per-kernel durations). */
+int cdp_resnet_profile_step(cdp_resnet *tr, const int32_t *perm, float lr, int serial, int max_ops, char *names,
+                            int name_len, double *flops, double *bytes, float *ms, int *n_ops);
 int cdp_resnet_history(cdp_resnet *tr, int max, double *losses, uint32_t *flags, int *count);
 int cdp_resnet_sync(cdp_resnet *tr);
 int cdp_resnet_ring_error(cdp_resnet *tr, int *err);

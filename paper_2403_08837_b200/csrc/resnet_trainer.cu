@@ -1008,10 +1008,13 @@ struct ResNetTrainer {
 
     // One real training step run eagerly (not from the graph) with timing events
     // around every launch; returns the per-launch records.
-    void profile_step(const int *perm, float lr) {
+    // serial: every launch on one stream (clean per-kernel durations, no overlap).
+    void profile_step(const int *perm, float lr, bool serial) {
         stage_control(perm, lr);
         clear_oprecs();
         instr = true;
+        cudaStream_t saved_cs = cs, saved_hs = hs;
+        if (serial) cs = hs = main;
         try {
             if (kind == 0)
                 record_step<0>(t & 1);
@@ -1019,8 +1022,12 @@ struct ResNetTrainer {
                 record_step<1>(t & 1);
         } catch (...) {
             instr = false;
+            cs = saved_cs;
+            hs = saved_hs;
             throw;
         }
+        cs = saved_cs;
+        hs = saved_hs;
         instr = false;
         ++t;
         CDP_CUDA(cudaStreamSynchronize(main));
@@ -1153,11 +1160,12 @@ extern "C" int cdp_resnet_last_loss(cdp_resnet *tr, double *loss) {
     });
 }
 
-extern "C" int cdp_resnet_profile_step(cdp_resnet *tr, const int32_t *perm, float lr, int max_ops, char *names,
-                                       int name_len, double *flops, double *bytes, float *ms, int *n_ops) {
+extern "C" int cdp_resnet_profile_step(cdp_resnet *tr, const int32_t *perm, float lr, int serial, int max_ops,
+                                       char *names, int name_len, double *flops, double *bytes, float *ms,
+                                       int *n_ops) {
     return guarded([&] {
         auto &m = *tr->impl;
-        m.profile_step(perm, lr);
+        m.profile_step(perm, lr, serial != 0);
         const int n = std::min<int>(max_ops, int(m.oprecs.size()));
         *n_ops = int(m.oprecs.size());
         for (int i = 0; i < n; ++i) {

@@ -257,9 +257,10 @@ class DeviceResNet:
         N.check(self.lib.cdp_resnet_last_loss(self.h, ctypes.byref(out)))
         return out.value
 
-    def profile_step(self, perm, lr, max_ops=4096):
+    def profile_step(self, perm, lr, serial=False, max_ops=4096):
         """One real training step, launched eagerly with CUDA events around every kernel (on the stream it is
-        launched on).  Returns [(name, flops, bytes, ms)] in launch order."""
+        launched on; serial=True puts every launch on one stream so durations are not inflated by the
+        concurrent stream).  Returns [(name, flops, bytes, ms)] in launch order."""
         p = np.ascontiguousarray(perm, dtype=np.int32)
         NL = 48
         names = ctypes.create_string_buffer(max_ops * NL)
@@ -267,7 +268,7 @@ class DeviceResNet:
         by = np.zeros(max_ops)
         ms = np.zeros(max_ops, dtype=np.float32)
         n = ctypes.c_int()
-        N.check(self.lib.cdp_resnet_profile_step(self.h, _i32p(p), float(lr), max_ops, names, NL,
+        N.check(self.lib.cdp_resnet_profile_step(self.h, _i32p(p), float(lr), int(serial), max_ops, names, NL,
                                                  fl.ctypes.data_as(N.c_double_p), by.ctypes.data_as(N.c_double_p),
                                                  ms.ctypes.data_as(N.c_float_p), ctypes.byref(n)))
         k = min(n.value, max_ops)
@@ -322,6 +323,25 @@ class DeviceResNet:
             self.close()
         except Exception:
             pass
+
+
+def init_params(specs, seed=0) -> np.ndarray:
+    """Deterministic initialisation in the trainer layout (numpy PCG64): conv He-normal (fan_in = R*S*Cin),
+    BN gamma = 1 / beta = 0, classifier U(-1/sqrt(C), 1/sqrt(C)) for W and b (torch's Linear bounds)."""
+    rng = np.random.default_rng([seed, 0xE0])
+    parts = []
+    for kind, shape, _ in specs:
+        if kind == "conv":
+            r, s, cin, cout = shape
+            parts.append(rng.normal(0.0, np.sqrt(2.0 / (r * s * cin)), size=r * s * cin * cout))
+        elif kind == "bn":
+            c = shape[0] // 2
+            parts.append(np.concatenate([np.ones(c), np.zeros(c)]))
+        else:
+            rows, classes = shape
+            b = 1.0 / np.sqrt(rows - 1)
+            parts.append(rng.uniform(-b, b, size=rows * classes))
+    return np.concatenate(parts)
 
 
 def synthetic_images(n, seed=0, hw=32, classes=10):

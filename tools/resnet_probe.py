@@ -35,7 +35,7 @@ print(f"{arch} B={B} {dtype}: step ms median {med:.3f} samples/s {B / med * 1e3:
 print("losses", tr.history(steps + 3)[0][-5:])
 if os.environ.get("PROFILE"):
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
-    ops = tr.profile_step(rng.permutation(len(x))[:B], 0.05)
+    ops = tr.profile_step(rng.permutation(len(x))[:B], 0.05, serial=True)
     for name, fl, by, t in ops:
         a = agg[name]; a[0] += 1; a[1] += t; a[2] += fl; a[3] += by
     tot = sum(a[1] for a in agg.values())
