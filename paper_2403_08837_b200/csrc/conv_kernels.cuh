@@ -8,9 +8,12 @@
 // row-blocked partial kernel; both are finalised in fp64 in a fixed order.
 //
 // Storage: activations in the GEMM compute format (bf16, or fp32 hi/lo for the
-// 3xTF32 mode); conv outputs y in "Y format" (bf16 / fp32); gradients flowing
-// between layers fp32.  All elementwise kernels move 4 channels per thread.
+// 3xTF32 mode); conv outputs y and the gradients flowing between layers in
+// "Y format" (bf16 in the bf16 mode, fp32 in the fp32 mode); every reduction
+// and every elementwise computation in fp32 registers.  All elementwise
+// kernels move 4 channels per thread.
 #pragma once
+#include "gemm_pk.cuh"
 #include "mlp_kernels.cuh"
 
 namespace cdp {
@@ -55,36 +58,114 @@ __device__ __forceinline__ float4 relu_mask4(float4 g, float4 a) {
 __device__ __forceinline__ float4 ld_f4(const float *p, size_t i) { return *reinterpret_cast<const float4 *>(p + i); }
 __device__ __forceinline__ void st_f4(float *p, size_t i, float4 v) { *reinterpret_cast<float4 *>(p + i) = v; }
 
-// ---------------------------------------------------------------------------
-// Stem: gather the micro-batch's images (fp32 NHWC dataset rows, C = 3) and
-// im2col them in one pass: cols[p][k], k = (r*S + s)*C + c, zero padding and
-// zero columns K..ld-1.  The cols matrix is the stem's activation record.
+// 8-wide (16-byte bf16) vectors
+struct F8 {
+    float v[8];
+};
+__device__ __forceinline__ void bf16x8_to_f8(const uint4 u, F8 &o) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w[k]));
+        o.v[2 * k] = f.x;
+        o.v[2 * k + 1] = f.y;
+    }
+}
+__device__ __forceinline__ uint4 f8_to_bf16x8(const F8 &a) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 b = __floats2bfloat162_rn(a.v[2 * k], a.v[2 * k + 1]);
+        w[k] = *reinterpret_cast<uint32_t *>(&b);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ F8 ld_f8(const float *p, size_t i) {
+    F8 o;
+    const float4 a = *reinterpret_cast<const float4 *>(p + i), b = *reinterpret_cast<const float4 *>(p + i + 4);
+    o.v[0] = a.x, o.v[1] = a.y, o.v[2] = a.z, o.v[3] = a.w, o.v[4] = b.x, o.v[5] = b.y, o.v[6] = b.z, o.v[7] = b.w;
+    return o;
+}
 template <int KIND>
-__global__ void stem_im2col_kernel(const float *__restrict__ data, const int *perm, int H, int W, int C, int R, int S,
-                                   int stride, int pad, int Ho, int Wo, int64_t P, CTensor cols) {
+__device__ __forceinline__ F8 ld_y8(const void *y, size_t i) {
+    if constexpr (KIND == 0) {
+        F8 o;
+        bf16x8_to_f8(*reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(y) + i), o);
+        return o;
+    } else {
+        return ld_f8(static_cast<const float *>(y), i);
+    }
+}
+template <int KIND>
+__device__ __forceinline__ void st_y8(void *y, size_t i, const F8 &a) {
+    if constexpr (KIND == 0) {
+        *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(y) + i) = f8_to_bf16x8(a);
+    } else {
+        float *p = static_cast<float *>(y) + i;
+        *reinterpret_cast<float4 *>(p) = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
+        *reinterpret_cast<float4 *>(p + 4) = make_float4(a.v[4], a.v[5], a.v[6], a.v[7]);
+    }
+}
+template <int KIND>
+__device__ __forceinline__ F8 ld_c8(const CTensor &t, size_t i) {
+    if constexpr (KIND == 0) {
+        return ld_y8<0>(t.hi, i);
+    } else {
+        F8 h = ld_f8(static_cast<const float *>(t.hi), i), l = ld_f8(static_cast<const float *>(t.lo), i);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) h.v[k] = __fadd_rn(h.v[k], l.v[k]);
+        return h;
+    }
+}
+template <int KIND>
+__device__ __forceinline__ void st_c8(const CTensor &t, size_t i, const F8 &a) {
+    store_wc4<KIND>(t, i, make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
+    store_wc4<KIND>(t, i + 4, make_float4(a.v[4], a.v[5], a.v[6], a.v[7]));
+}
+
+// ---------------------------------------------------------------------------
+// Stem: gather the micro-batch's images (fp32 NHWC dataset rows, C channels)
+// and im2col them in one pass: cols[p][k], k = (r*S + s)*C + c, zero padding
+// and zero columns K..ld-1.  The cols matrix is the stem's activation record.
+// One thread per (pixel, 8 consecutive k): 16-byte (bf16) stores.
+template <int KIND, int R, int C>
+__global__ void stem_im2col_kernel(const float *__restrict__ data, const int *perm, int H, int W, int stride, int pad,
+                                   int Ho, int Wo, int P, CTensor cols) {
     ptx::griddep_wait();
     ptx::griddep_launch();
-    const int K = R * S * C;
-    const int64_t n = P * cols.ld;
+    constexpr int S = R, K = R * S * C;
+    const int G = cols.ld / 8;
+    const int64_t n = int64_t(P) * G;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int k = int(i % cols.ld);
-        const int64_t p = i / cols.ld;
-        float v = 0.f;
-        if (k < K) {
-            const int c = k % C, rs = k / C, s = rs % S, r = rs / S;
-            const int wo = int(p % Wo), ho = int((p / Wo) % Ho), b = int(p / (int64_t(Wo) * Ho));
-            const int h = ho * stride - pad + r, w = wo * stride - pad + s;
-            if (h >= 0 && h < H && w >= 0 && w < W) v = data[((size_t(perm[b]) * H + h) * W + w) * C + c];
+        const int p = int(i / G), k0 = int(i - int64_t(p) * G) * 8;
+        const int wo = p % Wo, t = p / Wo, ho = t % Ho, b = t / Ho;
+        const float *img = data + size_t(perm[b]) * H * W * C;
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = k0 + j;
+            float x = 0.f;
+            if (k < K) {
+                const int r = k / (S * C), rem = k - r * (S * C), s = rem / C, c = rem - s * C;
+                const int h = ho * stride - pad + r, w = wo * stride - pad + s;
+                if (h >= 0 && h < H && w >= 0 && w < W) x = __ldg(img + (size_t(h) * W + w) * C + c);
+            }
+            v[j] = x;
         }
-        Fmt<KIND>::store(cols.hi, cols.lo, size_t(i), v);
+        const size_t o = size_t(p) * cols.ld + k0;
+        store_wc4<KIND>(cols, o, make_float4(v[0], v[1], v[2], v[3]));
+        store_wc4<KIND>(cols, o + 4, make_float4(v[4], v[5], v[6], v[7]));
     }
 }
 
 // col2im (deterministic gather) for the convs whose data gradient is an explicit
 // GEMM into im2col space (stride 2): dx[b,h,w,c] = sum over (r, s) ascending of
 // dcols[(b, ho, wo), (r, s, c)] with h = ho*stride - pad + r.  4 channels per thread.
-__global__ void col2im_kernel(const float *__restrict__ dcols, int ldc, int B, int H, int W, int C, int R, int S,
-                              int stride, int pad, int Ho, int Wo, float *dx) {
+// add != null: dx = col2im + (add masked by (add_mask > 0) when add_mask.hi) - the
+// residual branch of a block folded into the gradient of its first conv.
+template <int KIND>
+__global__ void col2im_kernel(const void *__restrict__ dcols, int ldc, int B, int H, int W, int C, int R, int S,
+                              int stride, int pad, int Ho, int Wo, void *dx, const void *add, CTensor add_mask) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int C4 = C / 4;
@@ -104,96 +185,268 @@ __global__ void col2im_kernel(const float *__restrict__ dcols, int ldc, int B, i
                 if (ww < 0 || ww % stride) continue;
                 const int wo = ww / stride;
                 if (wo >= Wo) continue;
-                const float4 v = ld_f4(dcols, (size_t(b) * Ho * Wo + size_t(ho) * Wo + wo) * ldc + (r * S + s) * C + c);
+                const float4 v =
+                    ld_y4<KIND>(dcols, (size_t(b) * Ho * Wo + size_t(ho) * Wo + wo) * ldc + (r * S + s) * C + c);
                 acc.x += v.x;
                 acc.y += v.y;
                 acc.z += v.z;
                 acc.w += v.w;
             }
         }
-        st_f4(dx, size_t(pix) * C + c, acc);
+        const size_t o = size_t(pix) * C + c;
+        if (add) {
+            float4 a = ld_y4<KIND>(add, o);
+            if (add_mask.hi) a = relu_mask4(a, ld_c4<KIND>(add_mask, o));
+            acc.x += a.x;
+            acc.y += a.y;
+            acc.z += a.z;
+            acc.w += a.w;
+        }
+        st_y4<KIND>(dx, o, acc);
     }
 }
 
 // ---------------------------------------------------------------------------
-// Conv GEMM epilogue (tile form): the 128 x BN fp32 tile is in shared memory.
-// Stores the rows that map to pixels (boxed tiles: conv_box_row; plain tiles:
-// m0 + r) either in Y format (forward conv output) or fp32 (data gradient),
-// and, when stats != null, the tile's per-channel (sum, sum of squares) over its
-// valid rows in ascending row order -> stats[tile][N][2] (BN forward statistics).
-template <int KIND>
-struct EpiConvOut {
-    struct Params {
-        void *out;
-        int ld;
-        int out_f32;   // 1: fp32 rows (gradients); 0: Y format
-        float *stats;  // null: no statistics
-        int boxed;
-        ConvGeom g;
-    };
-    static constexpr bool kTile = true;
-    static constexpr int kStages = 4;
-    template <int BN>
-    static constexpr int pf_bytes() { return 0; }
-    struct State {};
-    __device__ static void begin(const Params &, int, State &) {}
-    __device__ static void apply(const Params &, int, int, const float (&)[32], int, int, State &) {}
-    __device__ static void finish(const Params &, int, int, State &) {}
-    __device__ static void extra(const Params &, int, int) {}
-    template <int BN>
-    __device__ static void prefetch(const Params &, float *, int, int, int, int, int, int) {}
-    __device__ static void pre(const Params &, int) {}
-    __device__ static void post(const Params &, int, unsigned) {}
+// Epilogues of the persistent GEMM (gemm_pk_kernel / pk_reduce_kernel): run()
+// gets a shared sub-tile st[nrows][ncols] (row stride lds), the row map
+// rowm[r] (output row or -1) and the absolute column col0 of st's column 0.
 
-    template <int BN>
-    __device__ static void tile(const Params &p, const float *st, int lds, const float *, int m0, int n0, int M, int N,
-                                int tid, int nth) {
-        int *rowm = const_cast<int *>(reinterpret_cast<const int *>(st + 128 * lds));
-        for (int r = tid; r < 128; r += nth) {
-            int m = p.boxed ? conv_box_row(p.g, blockIdx.x, r) : m0 + r;
-            rowm[r] = (m >= 0 && m < M) ? m : -1;
+// Conv output (Y format) or data gradient (fp32) rows, plus (stats != null) the
+// tile's per-channel (sum, sum sq) over its valid rows in ascending row order
+// -> stats[tile_m][N][2] (requires the whole 128-row tile in one call).
+template <int KIND>
+struct EpiConvOut2 {
+    struct Params {
+        void *out;           // Y format (bf16 / fp32): conv outputs and activation gradients
+        int ld;
+        float *stats;        // [N][tiles][2] (channel-major: the finalise reads it coalesced)
+        int tiles;
+        const void *add;     // Y-format [rows][ld] added to the output (residual gradient), or null
+        CTensor add_mask;    // add masked by (add_mask > 0) when add_mask.hi
+    };
+    static constexpr int kStages = 0;
+    static constexpr bool kColStats = true;  // the persistent kernel reduces columns during the drain
+    // Stores (8 columns per element: 16-byte bf16 / 2 x 16-byte fp32 stores).
+    template <int NTH>
+    __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
+                               int ncols, int tm, int N, int tid) {
+        const int C8 = ncols / 8;
+        const int total = nrows * C8;
+        constexpr int U = 2;
+        for (int e0 = tid; e0 < total; e0 += NTH * U) {
+            float4 v[U][2], a[U][2], mk[U][2];
+            size_t o[U];
+            bool ok[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * NTH;
+                const int r = e / C8, c = (e - r * C8) * 8;
+                ok[u] = e < total && rowm[r] >= 0;
+                if (!ok[u]) continue;
+                v[u][0] = *reinterpret_cast<const float4 *>(st + r * lds + c);
+                v[u][1] = *reinterpret_cast<const float4 *>(st + r * lds + c + 4);
+                o[u] = size_t(rowm[r]) * p.ld + col0 + c;
+                if (p.add) {
+                    a[u][0] = ld_y4<KIND>(p.add, o[u]);
+                    a[u][1] = ld_y4<KIND>(p.add, o[u] + 4);
+                    if (p.add_mask.hi) {
+                        mk[u][0] = ld_c4<KIND>(p.add_mask, o[u]);
+                        mk[u][1] = ld_c4<KIND>(p.add_mask, o[u] + 4);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!ok[u]) continue;
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (p.add) {
+                        const float4 b = p.add_mask.hi ? relu_mask4(a[u][k], mk[u][k]) : a[u][k];
+                        v[u][k].x += b.x;
+                        v[u][k].y += b.y;
+                        v[u][k].z += b.z;
+                        v[u][k].w += b.w;
+                    }
+                }
+                if (KIND == 0) {
+                    __nv_bfloat162 b0 = __floats2bfloat162_rn(v[u][0].x, v[u][0].y);
+                    __nv_bfloat162 b1 = __floats2bfloat162_rn(v[u][0].z, v[u][0].w);
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(v[u][1].x, v[u][1].y);
+                    __nv_bfloat162 b3 = __floats2bfloat162_rn(v[u][1].z, v[u][1].w);
+                    uint4 w;
+                    w.x = *reinterpret_cast<uint32_t *>(&b0);
+                    w.y = *reinterpret_cast<uint32_t *>(&b1);
+                    w.z = *reinterpret_cast<uint32_t *>(&b2);
+                    w.w = *reinterpret_cast<uint32_t *>(&b3);
+                    *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + o[u]) = w;
+                } else {
+                    st_y4<KIND>(p.out, o[u], v[u][0]);
+                    st_y4<KIND>(p.out, o[u] + 4, v[u][1]);
+                }
+            }
         }
-        __syncthreads();
-        constexpr int C4 = BN / 4;
-        for (int e = tid; e < 128 * C4; e += nth) {
-            const int r = e / C4, c = (e % C4) * 4;
-            const int m = rowm[r];
-            if (m < 0 || n0 + c >= N) continue;
-            const float4 v = *reinterpret_cast<const float4 *>(st + r * lds + c);
-            const size_t o = size_t(m) * p.ld + n0 + c;
-            if (p.out_f32)
-                st_f4(static_cast<float *>(p.out), o, v);
-            else
-                st_y4<KIND>(p.out, o, v);
+    }
+    // Persistent kernel: the CTA's running per-column (sum, sum sq) over its units (in
+    // its fixed unit order) lives in stats[c][blockIdx.x][2]; col_stats_init zeroes the
+    // CTA's slice, col_stats adds the 4 TMEM-quarter partials of a unit (fixed order).
+    // Column a is always handled by epilogue thread a % pcols (program order, no race).
+    template <int NTH>
+    __device__ static void col_stats_init(const Params &p, int N, int pcols, int tid) {
+        if (!p.stats || tid >= pcols) return;
+        for (int a = tid; a < N; a += pcols)
+            *reinterpret_cast<float2 *>(p.stats + (size_t(a) * gridDim.x + blockIdx.x) * 2) = make_float2(0.f, 0.f);
+    }
+    template <int NTH>
+    __device__ static void col_stats(const Params &p, const float *part, int pcols, int col0, int ncols, int tm,
+                                     int tid) {
+        if (!p.stats) return;
+        for (int c = tid; c < ncols; c += NTH) {
+            float s = 0.f, q = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                s += part[(k * pcols + c) * 2];
+                q += part[(k * pcols + c) * 2 + 1];
+            }
+            float2 *o = reinterpret_cast<float2 *>(p.stats + (size_t(col0 + c) * gridDim.x + blockIdx.x) * 2);
+            const float2 cur = *o;
+            *o = make_float2(cur.x + s, cur.y + q);
         }
+    }
+    // Split-K reduce kernel: the whole 128-row tile is in `st` (rows in order).
+    template <int NTH>
+    __device__ static void run_with_stats(const Params &p, const float *st, int lds, const int *rowm, int nrows,
+                                          int col0, int ncols, int tm, int N, int tid) {
+        run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid);
         if (p.stats) {
-            for (int c = tid; c < BN; c += nth) {
-                if (n0 + c >= N) continue;
+            for (int c = tid; c < ncols; c += NTH) {
                 float s = 0.f, q = 0.f;
-                for (int r = 0; r < 128; ++r) {
+                for (int r = 0; r < nrows; ++r) {
                     if (rowm[r] < 0) continue;
                     const float v = st[r * lds + c];
                     s += v;
                     q = fmaf(v, v, q);
                 }
-                float *o = p.stats + (size_t(blockIdx.x) * N + n0 + c) * 2;
+                float *o = p.stats + (size_t(col0 + c) * p.tiles + tm) * 2;
                 o[0] = s;
                 o[1] = q;
             }
         }
     }
+    template <int NTH>
+    __device__ static void done(const Params &, int, unsigned) {}
 };
 
-// Weight gradient of a conv fused with its hop / update: EpiWgrad with a deeper
-// operand ring (K = pixels is long).
+// Weight gradient fused with the CDP hop / SGD update (same modes, arithmetic
+// and ring protocol as EpiWgrad; the pre-hop waits run in hop_wait_kernel).
 template <int KIND>
-struct EpiWgradConv : EpiWgrad<KIND> {
-    static constexpr int kStages = 4;
+struct EpiHop2 {
+    using Params = HopParams;
+    static constexpr int kStages = 0;
+    static constexpr bool kColStats = false;
+    template <int NTH>
+    __device__ static void col_stats(const Params &, const float *, int, int, int, int, int) {}
+    template <int NTH>
+    __device__ static void col_stats_init(const Params &, int, int, int) {}
+    template <int NTH>
+    __device__ static void run_with_stats(const Params &p, const float *st, int lds, const int *rowm, int nrows,
+                                          int col0, int ncols, int tm, int N, int tid) {
+        run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid);
+    }
+    template <int NTH>
+    __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
+                               int ncols, int, int, int tid) {
+        bool bad_g = false, bad_u = false;
+        const float lr = *p.lr;
+        if ((p.dout % 4) == 0 && (p.base % 4) == 0 && (ncols % 4) == 0) {
+            const int C4 = ncols / 4;
+            const int total = nrows * C4;
+            constexpr int U = 4;
+            for (int e0 = tid; e0 < total; e0 += NTH * U) {
+                float4 g[U], s[U], th[U], vv[U];
+                int64_t idx[U];
+                size_t widx[U];
+                bool ok[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * NTH;
+                    const int r = e / C4, c = (e - r * C4) * 4;
+                    ok[u] = e < total && rowm[r] >= 0;
+                    if (!ok[u]) continue;
+                    const int m = rowm[r], n = col0 + c;
+                    idx[u] = p.base + int64_t(m) * p.dout + n;
+                    widx[u] = size_t(m) * p.wc_new.ld + n;
+                    g[u] = *reinterpret_cast<const float4 *>(st + r * lds + c);
+                    if (p.mode == 1 || p.mode == 2) s[u] = __ldcg(reinterpret_cast<const float4 *>(p.s_in + idx[u]));
+                    if (p.mode == 2 || p.mode == 3) {
+                        th[u] = *reinterpret_cast<const float4 *>(p.theta_cur + idx[u]);
+                        if (p.momentum != 0.f) vv[u] = *reinterpret_cast<const float4 *>(p.vel + idx[u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (!ok[u]) continue;
+                    if (!finite4(g[u])) bad_g = true;
+                    float4 *so = reinterpret_cast<float4 *>(p.s_out + idx[u]);
+                    if (p.mode == 0 || p.mode == 4) {
+                        *so = g[u];
+                        continue;
+                    }
+                    float4 G = g[u];
+                    if (p.mode == 1 || p.mode == 2)
+                        G = make_float4(__fadd_rn(s[u].x, g[u].x), __fadd_rn(s[u].y, g[u].y),
+                                        __fadd_rn(s[u].z, g[u].z), __fadd_rn(s[u].w, g[u].w));
+                    if (p.mode == 1) {
+                        *so = G;
+                        continue;
+                    }
+                    float4 v = p.momentum != 0.f ? vv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    float4 nt;
+                    nt.x = sgd_update(p, G.x, th[u].x, v.x, lr);
+                    nt.y = sgd_update(p, G.y, th[u].y, v.y, lr);
+                    nt.z = sgd_update(p, G.z, th[u].z, v.z, lr);
+                    nt.w = sgd_update(p, G.w, th[u].w, v.w, lr);
+                    if (p.momentum != 0.f) *reinterpret_cast<float4 *>(p.vel + idx[u]) = v;
+                    if (!finite4(nt)) bad_u = true;
+                    *reinterpret_cast<float4 *>(p.theta_new + idx[u]) = nt;
+                    store_wc4<KIND>(p.wc_new, widx[u], nt);
+                }
+            }
+        } else {
+            for (int e = tid; e < nrows * ncols; e += NTH) {
+                const int r = e / ncols, c = e - r * ncols;
+                if (rowm[r] < 0) continue;
+                hop_elem<KIND>(p, p.base + int64_t(rowm[r]) * p.dout + col0 + c, st[r * lds + c],
+                               size_t(rowm[r]) * p.wc_new.ld + col0 + c, true, bad_g, bad_u);
+            }
+        }
+        if (bad_g) atomicOr(p.grad_flags, 1u << ((p.stage - 1) & 31));
+        if (bad_u) atomicOr(p.upd_flags, 1u << ((p.stage - 1) & 31));
+    }
+    // ring protocol: the last of `arrivals` epilogue invocations of this tensor publishes
+    template <int NTH>
+    __device__ static void done(const Params &p, int tid, unsigned arrivals) {
+        if (!p.sync.enabled || p.mode >= 3) return;
+        pk_bar(2, NTH);
+        if (tid == 0) {
+            const uint32_t t = uint32_t(*p.sync.step), j = p.stage - 1;
+            __threadfence();
+            if (atomicAdd(&p.sync.cta_counter[j], 1u) == arrivals - 1) {
+                p.sync.cta_counter[j] = 0;
+                __threadfence_system();
+                if (p.mode == 1 || p.mode == 2) ptx::st_release_sys(&p.sync.prev->consumed[j], t);
+                if (p.mode == 0 || p.mode == 1) ptx::st_release_sys(&p.sync.own->ready[j], t);
+                if (p.mode == 2) {
+                    p.sync.own->pulled[j][(t + 1) & 1] = 0;
+                    ptx::st_release_sys(&p.sync.own->updated[j], t + 1);
+                }
+            }
+        }
+    }
 };
 
 // ---------------------------------------------------------------------------
 // Batch norm (training mode).
-// Forward finalise: per channel, the per-tile (sum, sum sq) in tile order (fp64)
+// Forward finalise: per channel, the per-tile (sum, sum sq) [C][tiles][2] (fp64)
 // -> mean, rstd (biased variance, eps).  One warp per channel, lanes take tiles
 // lane, lane+32, ... then a fixed xor-tree: deterministic.
 __global__ void bn_finalize_fwd_kernel(const float *__restrict__ stats, int tiles, int C, int64_t P, float eps,
@@ -204,9 +457,11 @@ __global__ void bn_finalize_fwd_kernel(const float *__restrict__ stats, int tile
     const int lane = threadIdx.x & 31;
     if (c >= C) return;
     double s0 = 0.0, s1 = 0.0;
+    const float2 *sc = reinterpret_cast<const float2 *>(stats) + size_t(c) * tiles;  // [C][tiles] (sum, sum sq)
     for (int t = lane; t < tiles; t += 32) {
-        s0 += double(stats[(size_t(t) * C + c) * 2]);
-        s1 += double(stats[(size_t(t) * C + c) * 2 + 1]);
+        const float2 v = sc[t];
+        s0 += double(v.x);
+        s1 += double(v.y);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -235,51 +490,51 @@ __global__ void bn_apply_kernel(const void *__restrict__ y, int64_t P, int C, co
                                 const float *gamma, const float *beta, BnResidual res, int relu, CTensor out) {
     ptx::griddep_wait();
     ptx::griddep_launch();
-    const int C4 = C / 4;
-    const int64_t n = P * C4;
+    const int C8 = C / 8;
+    const int64_t n = P * C8;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % C4) * 4;
-        const size_t o = size_t(i) * 4;
-        const float4 x = ld_y4<KIND>(y, o);
-        const float4 mu = ld_f4(mean, c), rs = ld_f4(rstd, c), ga = ld_f4(gamma, c), be = ld_f4(beta, c);
-        float4 v = make_float4(ga.x * ((x.x - mu.x) * rs.x) + be.x, ga.y * ((x.y - mu.y) * rs.y) + be.y,
-                               ga.z * ((x.z - mu.z) * rs.z) + be.z, ga.w * ((x.w - mu.w) * rs.w) + be.w);
+        const int c = int(i % C8) * 8;
+        const size_t o = size_t(i) * 8;
+        const F8 x = ld_y8<KIND>(y, o);
+        F8 ra, rx;
+        if (res.act.hi) ra = ld_c8<KIND>(res.act, o);
+        if (res.y) rx = ld_y8<KIND>(res.y, o);
+        const F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), be = ld_f8(beta, c);
+        F8 v;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v.v[k] = ga.v[k] * ((x.v[k] - mu.v[k]) * rs.v[k]) + be.v[k];
         if (res.act.hi) {
-            const float4 a = ld_c4<KIND>(res.act, o);
-            v.x += a.x;
-            v.y += a.y;
-            v.z += a.z;
-            v.w += a.w;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v.v[k] += ra.v[k];
         }
         if (res.y) {
-            const float4 x2 = ld_y4<KIND>(res.y, o);
-            const float4 m2 = ld_f4(res.mean, c), r2 = ld_f4(res.rstd, c), g2 = ld_f4(res.gamma, c),
-                         b2 = ld_f4(res.beta, c);
-            v.x += g2.x * ((x2.x - m2.x) * r2.x) + b2.x;
-            v.y += g2.y * ((x2.y - m2.y) * r2.y) + b2.y;
-            v.z += g2.z * ((x2.z - m2.z) * r2.z) + b2.z;
-            v.w += g2.w * ((x2.w - m2.w) * r2.w) + b2.w;
+            const F8 m2 = ld_f8(res.mean, c), r2 = ld_f8(res.rstd, c), g2 = ld_f8(res.gamma, c), b2 = ld_f8(res.beta, c);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v.v[k] += g2.v[k] * ((rx.v[k] - m2.v[k]) * r2.v[k]) + b2.v[k];
         }
-        if (relu) v = make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
-        store_wc4<KIND>(out, o, v);
+        if (relu) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v.v[k] = fmaxf(v.v[k], 0.f);
+        }
+        st_c8<KIND>(out, o, v);
     }
 }
 
 // Backward statistics: per row block (kBnRows rows), per channel,
 // (sum g', sum g' * xhat) with g' = g masked by (act > 0) when mask != null.
 // TPR threads per row (4 channels each), 256/TPR row phases; the phases are
-// combined in fixed order in fp64 -> partial[blk][C][2].  A second conv output
-// (projection shortcut: same g', own y / stats) gives partial2.
+// combined in fixed order in fp64 -> partial[C][blocks][2].  A second conv
+// output (projection shortcut: same g', own y / stats) gives partial2.
 constexpr int kBnRows = 256;
 
 template <int KIND>
-__global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const float *__restrict__ g, CTensor mask, int64_t P, int C,
+__global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__restrict__ g, CTensor mask, int64_t P, int C,
                                                            const void *y, const float *mean, const float *rstd,
                                                            double *partial, const void *y2, const float *mean2,
                                                            const float *rstd2, double *partial2) {
     ptx::griddep_wait();
     ptx::griddep_launch();
-    __shared__ float red[4][256 * 4];
+    __shared__ float red[3][256 * 4];
     const int C4 = C / 4;
     const int TPR = C4 < 32 ? C4 : 32;
     const int phases = 256 / TPR;
@@ -297,7 +552,7 @@ __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const float *__restri
         }
         for (int64_t r = r0 + ty; r < r1; r += phases) {
             const size_t o = size_t(r) * C + c;
-            float4 gv = ld_f4(g, o);
+            float4 gv = ld_y4<KIND>(g, o);
             if (mask.hi) gv = relu_mask4(gv, ld_c4<KIND>(mask, o));
             const float4 x = ld_y4<KIND>(y, o);
             a0.x += gv.x;
@@ -335,11 +590,11 @@ __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const float *__restri
                 s1 += double(red[1][idx]);
                 s2 += double(red[2][idx]);
             }
-            double *o = partial + (size_t(blockIdx.x) * C + cc) * 2;
+            double *o = partial + (size_t(cc) * gridDim.x + blockIdx.x) * 2;  // [C][blocks][2]
             o[0] = s0;
             o[1] = s1;
             if (partial2) {
-                double *o2 = partial2 + (size_t(blockIdx.x) * C + cc) * 2;
+                double *o2 = partial2 + (size_t(cc) * gridDim.x + blockIdx.x) * 2;
                 o2[0] = s0;
                 o2[1] = s2;
             }
@@ -356,9 +611,11 @@ __global__ void bn_finalize_bwd_kernel(const double *__restrict__ partial, int n
     const int lane = threadIdx.x & 31;
     if (c >= C) return;
     double s0 = 0.0, s1 = 0.0;
+    const double2 *pc = reinterpret_cast<const double2 *>(partial) + size_t(c) * nblk;  // [C][blocks]
     for (int t = lane; t < nblk; t += 32) {
-        s0 += partial[(size_t(t) * C + c) * 2];
-        s1 += partial[(size_t(t) * C + c) * 2 + 1];
+        const double2 v = pc[t];
+        s0 += v.x;
+        s1 += v.y;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -374,43 +631,30 @@ __global__ void bn_finalize_bwd_kernel(const double *__restrict__ partial, int n
 // Backward through BN (+ReLU mask): dx = gamma * rstd * (g' - dbeta/P - xhat * dgamma/P)
 // in compute format (the conv's output gradient, a GEMM operand).
 template <int KIND>
-__global__ void bn_bwd_apply_kernel(const float *__restrict__ g, CTensor mask, const void *__restrict__ y, int64_t P,
+__global__ void bn_bwd_apply_kernel(const void *__restrict__ g, CTensor mask, const void *__restrict__ y, int64_t P,
                                     int C, const float *mean, const float *rstd, const float *gamma,
                                     const float *dbeta, const float *dgamma, CTensor dx) {
     ptx::griddep_wait();
     ptx::griddep_launch();
-    const int C4 = C / 4;
-    const int64_t n = P * C4;
+    const int C8 = C / 8;
+    const int64_t n = P * C8;
     const float inv = 1.f / float(P);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % C4) * 4;
-        const size_t o = size_t(i) * 4;
-        float4 gv = ld_f4(g, o);
-        if (mask.hi) gv = relu_mask4(gv, ld_c4<KIND>(mask, o));
-        const float4 x = ld_y4<KIND>(y, o);
-        const float4 mu = ld_f4(mean, c), rs = ld_f4(rstd, c), ga = ld_f4(gamma, c), db = ld_f4(dbeta, c),
-                     dg = ld_f4(dgamma, c);
-        float4 d;
-        d.x = ga.x * rs.x * (gv.x - db.x * inv - ((x.x - mu.x) * rs.x) * dg.x * inv);
-        d.y = ga.y * rs.y * (gv.y - db.y * inv - ((x.y - mu.y) * rs.y) * dg.y * inv);
-        d.z = ga.z * rs.z * (gv.z - db.z * inv - ((x.z - mu.z) * rs.z) * dg.z * inv);
-        d.w = ga.w * rs.w * (gv.w - db.w * inv - ((x.w - mu.w) * rs.w) * dg.w * inv);
-        store_wc4<KIND>(dx, o, d);
-    }
-}
-
-// out = a + b (fp32 [P][C]), b masked by (mask > 0) when mask != null.
-template <int KIND>
-__global__ void add_kernel(const float *a, const float *b, int64_t P, int C, CTensor mask_b, float *out) {
-    ptx::griddep_wait();
-    ptx::griddep_launch();
-    const int64_t n = P * C / 4;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const size_t o = size_t(i) * 4;
-        float4 vb = ld_f4(b, o);
-        if (mask_b.hi) vb = relu_mask4(vb, ld_c4<KIND>(mask_b, o));
-        const float4 va = ld_f4(a, o);
-        st_f4(out, o, make_float4(va.x + vb.x, va.y + vb.y, va.z + vb.z, va.w + vb.w));
+        const int c = int(i % C8) * 8;
+        const size_t o = size_t(i) * 8;
+        F8 gv = ld_y8<KIND>(g, o);
+        const F8 x = ld_y8<KIND>(y, o);
+        F8 mk;
+        if (mask.hi) mk = ld_c8<KIND>(mask, o);
+        const F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), db = ld_f8(dbeta, c),
+                 dg = ld_f8(dgamma, c);
+        F8 d;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float gk = (mask.hi && !(mk.v[k] > 0.f)) ? 0.f : gv.v[k];
+            d.v[k] = ga.v[k] * rs.v[k] * (gk - db.v[k] * inv - ((x.v[k] - mu.v[k]) * rs.v[k]) * dg.v[k] * inv);
+        }
+        st_c8<KIND>(dx, o, d);
     }
 }
 
@@ -423,41 +667,47 @@ __global__ void maxpool_fwd_kernel(CTensor in, int B, int H, int W, int C, int H
                                    uint8_t *arg) {
     ptx::griddep_wait();
     ptx::griddep_launch();
-    const int64_t n = int64_t(B) * Ho * Wo * C;
+    const int C4 = C / 4;
+    const int64_t n = int64_t(B) * Ho * Wo * C4;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % C);
-        const int64_t p = i / C;
-        const int wo = int(p % Wo), ho = int((p / Wo) % Ho), b = int(p / (int64_t(Wo) * Ho));
-        float best = -INFINITY;
-        int bt = 0;
+        const int c = int(i % C4) * 4;
+        const int p = int(i / C4);
+        const int wo = p % Wo, t = p / Wo, ho = t % Ho, b = t / Ho;
+        float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int bt[4] = {0, 0, 0, 0};
         for (int r = 0; r < 3; ++r) {
             const int h = ho * 2 - 1 + r;
             if (h < 0 || h >= H) continue;
             for (int s = 0; s < 3; ++s) {
                 const int w = wo * 2 - 1 + s;
                 if (w < 0 || w >= W) continue;
-                const float v = Fmt<KIND>::load(in.hi, in.lo, ((size_t(b) * H + h) * W + w) * in.ld + c);
-                if (v > best) {
-                    best = v;
-                    bt = r * 3 + s;
-                }
+                const float4 v = ld_c4<KIND>(in, ((size_t(b) * H + h) * W + w) * in.ld + c);
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (vv[j] > best[j]) {
+                        best[j] = vv[j];
+                        bt[j] = r * 3 + s;
+                    }
             }
         }
-        Fmt<KIND>::store(out.hi, out.lo, size_t(p) * out.ld + c, best);
-        arg[i] = uint8_t(bt);
+        store_wc4<KIND>(out, size_t(p) * out.ld + c, make_float4(best[0], best[1], best[2], best[3]));
+        *reinterpret_cast<uchar4 *>(arg + size_t(p) * C + c) = make_uchar4(bt[0], bt[1], bt[2], bt[3]);
     }
 }
 
-__global__ void maxpool_bwd_kernel(const float *__restrict__ gout, const uint8_t *__restrict__ arg, int B, int H, int W,
-                                   int C, int Ho, int Wo, float *gin) {
+template <int KIND>
+__global__ void maxpool_bwd_kernel(const void *__restrict__ gout, const uint8_t *__restrict__ arg, int B, int H, int W,
+                                   int C, int Ho, int Wo, void *gin) {
     ptx::griddep_wait();
     ptx::griddep_launch();
-    const int64_t n = int64_t(B) * H * W * C;
+    const int C4 = C / 4;
+    const int64_t n = int64_t(B) * H * W * C4;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % C);
-        const int64_t p = i / C;
-        const int w = int(p % W), h = int((p / W) % H), b = int(p / (int64_t(W) * H));
-        float acc = 0.f;
+        const int c = int(i % C4) * 4;
+        const int p = int(i / C4);
+        const int w = p % W, t = p / W, h = t % H, b = t / H;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int r = 0; r < 3; ++r) {
             const int hh = h + 1 - r;
             if (hh < 0 || (hh & 1)) continue;
@@ -469,10 +719,16 @@ __global__ void maxpool_bwd_kernel(const float *__restrict__ gout, const uint8_t
                 const int wo = ww >> 1;
                 if (wo >= Wo) continue;
                 const size_t o = ((size_t(b) * Ho + ho) * Wo + wo) * C + c;
-                if (arg[o] == r * 3 + s) acc += gout[o];
+                const uchar4 a = *reinterpret_cast<const uchar4 *>(arg + o);
+                const float4 g = ld_y4<KIND>(gout, o);
+                const int tap = r * 3 + s;
+                if (a.x == tap) acc.x += g.x;
+                if (a.y == tap) acc.y += g.y;
+                if (a.z == tap) acc.z += g.z;
+                if (a.w == tap) acc.w += g.w;
             }
         }
-        gin[i] = acc;
+        st_y4<KIND>(gin, size_t(p) * C + c, acc);
     }
 }
 
@@ -494,8 +750,9 @@ __global__ void avgpool_kernel(CTensor act, int B, int HW, int C, CTensor pooled
     }
 }
 
-// d act[b, k, c] = dpooled[b][c] / HW, fp32, 4 channels per thread.
-__global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, int HW, int C, float *g) {
+// d act[b, k, c] = dpooled[b][c] / HW (Y format), 4 channels per thread.
+template <int KIND>
+__global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, int HW, int C, void *g) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int C4 = C / 4;
@@ -505,7 +762,7 @@ __global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, int HW,
         const int c = int(i % C4) * 4;
         const int64_t r = i / C4;
         const float *s = dp + (r / HW) * ldp + c;
-        st_f4(g, size_t(r) * C + c, make_float4(s[0] * inv, s[1] * inv, s[2] * inv, s[3] * inv));
+        st_y4<KIND>(g, size_t(r) * C + c, make_float4(s[0] * inv, s[1] * inv, s[2] * inv, s[3] * inv));
     }
 }
 

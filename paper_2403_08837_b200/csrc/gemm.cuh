@@ -111,9 +111,8 @@ __device__ __forceinline__ void load_operand(uint8_t *dst, const CUtensorMap *m,
 //   WGRAD: M = (tap, c), K = pixels: A = input gathered per 64-row chunk at its tap
 //          (MN-major), B = dy (MN-major), k-block = one pixel box.
 template <class C, int MODE, bool B_MN, int BN>
-__device__ __forceinline__ void conv_load(uint8_t *sa, uint8_t *sb, const GemmMaps &maps, const GemmArgs &args,
+__device__ __forceinline__ void conv_load(uint8_t *sa, uint8_t *sb, const GemmMaps &maps, const ConvGeom &g,
                                           uint64_t *bar, int seg, int kb, int m_tile, int m0, int n0) {
-    const ConvGeom &g = args.cv;
     if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD) {
         const int tap = kb / g.cpt, cc = kb - tap * g.cpt;
         const int r = tap / g.S, s = tap - r * g.S;
@@ -160,8 +159,8 @@ template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE = GM_PLAIN
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args, const typename Epi::Params ep) {
     using C = GemmCfg<KIND, BN, A_MN, B_MN, Epi::kStages, Epi::template pf_bytes<BN>()>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = smem;
     uint8_t *sB = smem + C::STAGES * C::A_BYTES;
     float *pf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
@@ -217,8 +216,8 @@ __global__ void __launch_bounds__(256, 1)
                     load_operand<C, A_MN, 128>(sA + s * C::A_BYTES, &maps.a[seg], &full[s], m0, k0);
                     load_operand<C, B_MN, BN>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, k0);
                 } else {
-                    conv_load<C, MODE, B_MN, BN>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args, &full[s], seg,
-                                                 g % args.kb_per_seg, blockIdx.x, m0, n0);
+                    conv_load<C, MODE, B_MN, BN>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args.cv, &full[s],
+                                                 seg, g % args.kb_per_seg, blockIdx.x, m0, n0);
                 }
             }
         }

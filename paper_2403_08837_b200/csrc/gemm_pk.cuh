@@ -1,0 +1,304 @@
+// Persistent tcgen05 GEMM for sm_100a (the conv / ResNet hot path).
+//
+//   D[M,N] (fp32, TMEM) = sum_seg A_seg[M,K] . B_seg[K,N], plain or implicit-conv
+//   operands (GemmMode, conv_load in gemm.cuh), fused epilogue per output tile.
+//
+// One CTA per SM loops over work units (tile_m, tile_n, split) with three
+// pipelines:
+//   * smem ring  : warp 0 (one thread) issues TMA into a STAGES-deep
+//                  full/empty mbarrier ring;
+//   * TMEM ring  : warp 1 (one thread) issues tcgen05.mma into one of TWO
+//                  accumulators (2 x BN columns), so the epilogue of unit j
+//                  overlaps the mainloop of unit j+1;
+//   * epilogue   : warps 4-11 drain the accumulator (tcgen05.ld; warp w reads
+//                  TMEM lane quarter w % 4, column half (w - 4) / 4) into a
+//                  padded shared tile, release the accumulator, then run the
+//                  fused epilogue on the shared tile with all 256 threads
+//                  (coalesced 16-byte global accesses, several in flight each).
+// Split-K units write their partial tile to a workspace; a separate kernel
+// (pk_reduce_kernel) sums the partials in split order - deterministic and
+// parallel over (tile, row chunk) - and runs the same epilogue.
+#pragma once
+#include "gemm.cuh"
+
+namespace cdp {
+
+struct PkArgs {
+    int M, N;
+    int tiles_m, tiles_n, splits;
+    int kb_per_seg, n_seg, iters_per_split, total_iters;
+    int units;
+    int boxed;     // rows of an M tile are a pixel box of cv (FPROP / DGRAD)
+    float *ws;     // split partials [tile][split][128][BN]
+    ConvGeom cv;
+};
+
+template <int KIND, int BN, bool A_MN, bool B_MN, int ST>
+struct PkCfg {
+    static constexpr int BM = 128;
+    static constexpr int ELEM = KIND == 0 ? 2 : 4;
+    static constexpr int BK = 128 / ELEM;
+    static constexpr int UMMA_K = 32 / ELEM;
+    static constexpr int CH = 128 / ELEM;
+    static constexpr int A_BYTES = BM * 128;
+    static constexpr int B_BYTES = BN * 128;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int EPI_COLS = BN < 128 ? BN : 128;  // columns staged per epilogue pass
+    static constexpr int LDS = EPI_COLS + 4;
+    static constexpr int STILE_BYTES = 128 * LDS * 4;
+    static constexpr int PART_BYTES = 4 * EPI_COLS * 2 * 4;  // per TMEM quarter column (sum, sum sq)
+    static constexpr int BUDGET = 220 * 1024 - STILE_BYTES - PART_BYTES - 2048;
+    static constexpr int STAGES = ST ? ST : (BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES);
+    static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + STILE_BYTES + PART_BYTES + 512 + 256;
+    static constexpr uint32_t IDESC = ptx::instr_desc(KIND == 0 ? 1u : 2u, A_MN, B_MN, 128, BN);
+    static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN must be 64, 128 or 256");
+    static_assert(!B_MN || BN % CH == 0, "MN-major B needs BN multiple of the 128-byte row");
+    static_assert(STAGES >= 2, "not enough shared memory for two stages");
+    static_assert(SMEM <= 227 * 1024, "shared memory budget exceeded");
+};
+
+__device__ __forceinline__ void pk_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Column sums of a warp's 32 x 32 block (lane = row, v[i] = column i):
+// recursive-halving reduce-scatter, 31 shuffles; lane l returns column l's sum
+// over the 32 rows in a fixed order.
+__device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
+    const int lane = ptx::lane_id();
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            const float send = upper ? v[i] : v[i + off];
+            const float keep = upper ? v[i + off] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0];
+}
+
+__device__ __forceinline__ void pk_unit(const PkArgs &a, int u, int &tm, int &tn, int &split) {
+    split = u % a.splits;
+    const int t = u / a.splits;
+    tn = t % a.tiles_n;
+    tm = t / a.tiles_n;
+}
+
+// tile row -> output row m (or -1): pixel box rows (FPROP / DGRAD) or m0 + r.
+__device__ __forceinline__ int pk_row_m(const PkArgs &a, int tm, int r) {
+    if (a.boxed) return conv_box_row(a.cv, tm, r);
+    const int m = tm * 128 + r;
+    return m < a.M ? m : -1;
+}
+
+constexpr int kPkThreads = 384;  // 4 control warps + 8 epilogue warps
+constexpr int kPkEpi = 256;
+
+template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE>
+__global__ void __launch_bounds__(kPkThreads, 1)
+    gemm_pk_kernel(const __grid_constant__ GemmMaps maps, const PkArgs args, const typename Epi::Params ep) {
+    using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages>;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    // 1024-byte alignment by pointer arithmetic on the shared array (keeps the
+    // shared address space visible to the compiler: LDS/STS, not generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + C::STAGES * C::A_BYTES;
+    float *stile = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
+    float *spart = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + C::STILE_BYTES);
+    int *rowm = reinterpret_cast<int *>(smem + C::STAGES * C::STAGE_BYTES + C::STILE_BYTES + C::PART_BYTES);
+    uint64_t *full = reinterpret_cast<uint64_t *>(rowm + 128);
+    uint64_t *empty = full + C::STAGES;
+    uint64_t *tfull = empty + C::STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const uint32_t warp = ptx::warp_id();
+    if (warp == 0 && ptx::lane_id() == 0) {
+        for (int s = 0; s < args.n_seg; ++s) {
+            ptx::tma_prefetch_desc(&maps.a[s]);
+            ptx::tma_prefetch_desc(&maps.b[s]);
+        }
+    }
+    if (warp == 1 && ptx::lane_id() == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 1);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+
+    if (warp == 0) {
+        if (ptx::lane_id() == 0) {
+            int it = 0;
+            for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+                int tm, tn, sp;
+                pk_unit(args, u, tm, tn, sp);
+                const int lo = sp * args.iters_per_split, hi = min(args.total_iters, lo + args.iters_per_split);
+                const int m0 = tm * 128, n0 = tn * BN;
+                for (int g = lo; g < hi; ++g, ++it) {
+                    const int s = it % C::STAGES;
+                    if (it >= C::STAGES) ptx::mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+                    const int seg = g / args.kb_per_seg, kb = g - seg * args.kb_per_seg;
+                    ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+                    if constexpr (MODE == GM_PLAIN) {
+                        load_operand<C, A_MN, 128>(sA + s * C::A_BYTES, &maps.a[seg], &full[s], m0, kb * C::BK);
+                        load_operand<C, B_MN, BN>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, kb * C::BK);
+                    } else {
+                        conv_load<C, MODE, B_MN, BN>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args.cv, &full[s],
+                                                     seg, kb, tm, m0, n0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (ptx::lane_id() == 0) {
+            int it = 0, j = 0;
+            for (int u = blockIdx.x; u < args.units; u += gridDim.x, ++j) {
+                int tm, tn, sp;
+                pk_unit(args, u, tm, tn, sp);
+                const int lo = sp * args.iters_per_split, hi = min(args.total_iters, lo + args.iters_per_split);
+                const int acc = j & 1;
+                if (j >= 2) ptx::mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + uint32_t(acc * BN);
+                for (int g = lo; g < hi; ++g, ++it) {
+                    const int s = it % C::STAGES;
+                    ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
+                    const uint32_t b_base = ptx::smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < C::BK / C::UMMA_K; ++k)
+                        ptx::umma<KIND>(d, operand_desc<C, A_MN>(a_base, k), operand_desc<C, B_MN>(b_base, k), C::IDESC,
+                                        (g > lo || k > 0) ? 1u : 0u);
+                    ptx::umma_commit(&empty[s]);
+                }
+                ptx::umma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int tid = threadIdx.x - 128;  // 0..255
+        const int q = warp & 3;             // TMEM lane quarter this warp may access
+        const int half = (warp - 4) >> 2;   // column half of each staging pass
+        const int row = q * 32 + ptx::lane_id();
+        constexpr int HC = C::EPI_COLS / 2;
+        if (Epi::kColStats && args.splits == 1) {
+            Epi::template col_stats_init<kPkEpi>(ep, args.N, C::EPI_COLS, tid);
+            pk_bar(1, kPkEpi);
+        }
+        int j = 0;
+        for (int u = blockIdx.x; u < args.units; u += gridDim.x, ++j) {
+            int tm, tn, sp;
+            pk_unit(args, u, tm, tn, sp);
+            const int acc = j & 1;
+            const bool split = args.splits > 1;
+            if (tid < 128) rowm[tid] = pk_row_m(args, tm, tid);  // the previous unit's last barrier protects rowm / stile
+            ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
+            ptx::tc_fence_after();
+            const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+#pragma unroll 1
+            for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+                const bool row_ok = pk_row_m(args, tm, row) >= 0;  // own computation: rowm is not yet synced
+#pragma unroll 1
+                for (int c = half * HC; c < (half + 1) * HC; c += 32) {
+                    float v[32];
+                    ptx::tmem_ld32(taddr + h * C::EPI_COLS + c, v);
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4)
+                        *reinterpret_cast<float4 *>(stile + row * C::LDS + c + i) =
+                            make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    if (Epi::kColStats && !split) {
+                        // per-quarter column (sum, sum sq) over the valid rows -> spart[q][c][2]
+                        float sq[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            v[i] = row_ok ? v[i] : 0.f;
+                            sq[i] = v[i] * v[i];
+                        }
+                        const float cs = warp_colsum32(v);
+                        const float cq = warp_colsum32(sq);
+                        float *pp = spart + (q * C::EPI_COLS + c + ptx::lane_id()) * 2;
+                        pp[0] = cs;
+                        pp[1] = cq;
+                    }
+                }
+                if (h == BN / C::EPI_COLS - 1) ptx::tc_fence_before();
+                pk_bar(1, kPkEpi);
+                if (h == BN / C::EPI_COLS - 1 && tid == 0) ptx::mbar_arrive(&tempty[acc]);  // accumulator free
+                const int col0 = tn * BN + h * C::EPI_COLS;
+                if (split) {
+                    float *dst = args.ws + ((size_t(tm) * args.tiles_n + tn) * args.splits + sp) * 128 * BN +
+                                 h * C::EPI_COLS;
+                    constexpr int C4 = C::EPI_COLS / 4;
+                    for (int e = tid; e < 128 * C4; e += kPkEpi) {
+                        const int r = e / C4, cc = (e % C4) * 4;
+                        *reinterpret_cast<float4 *>(dst + size_t(r) * BN + cc) =
+                            *reinterpret_cast<const float4 *>(stile + r * C::LDS + cc);
+                    }
+                } else {
+                    Epi::template run<kPkEpi>(ep, stile, C::LDS, rowm, 128, col0, min(C::EPI_COLS, args.N - col0), tm,
+                                              args.N, tid);
+                    if (Epi::kColStats)
+                        Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0),
+                                                        tm, tid);
+                }
+                pk_bar(1, kPkEpi);  // shared tile reused by the next pass / unit
+            }
+            if (!split) Epi::template done<kPkEpi>(ep, tid, unsigned(args.tiles_m * args.tiles_n));
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+// Split-K tail: per (tile, row chunk of RC rows, column chunk of CC columns),
+// sum the split partials in split order into shared memory and run the
+// epilogue on that sub-tile.  256 threads.
+template <int BN, class Epi, int RC, int CC>
+__global__ void __launch_bounds__(256) pk_reduce_kernel(const PkArgs args, const typename Epi::Params ep) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    __shared__ __align__(16) float st[RC * (CC + 4)];
+    __shared__ int rowm[RC];
+    const int tile = blockIdx.x;
+    const int tm = tile / args.tiles_n, tn = tile % args.tiles_n;
+    const int row0 = blockIdx.y * RC, c0 = blockIdx.z * CC;
+    for (int r = threadIdx.x; r < RC; r += 256) rowm[r] = pk_row_m(args, tm, row0 + r);
+    const float *base = args.ws + size_t(tile) * args.splits * 128 * BN;
+    constexpr int C4 = CC / 4;
+    for (int e = threadIdx.x; e < RC * C4; e += 256) {
+        const int r = e / C4, c = (e % C4) * 4;
+        const float *p = base + size_t(row0 + r) * BN + c0 + c;
+        float4 acc = __ldcg(reinterpret_cast<const float4 *>(p));
+#pragma unroll 8
+        for (int z = 1; z < args.splits; ++z) {
+            const float4 t = __ldcg(reinterpret_cast<const float4 *>(p + size_t(z) * 128 * BN));
+            acc.x += t.x;
+            acc.y += t.y;
+            acc.z += t.z;
+            acc.w += t.w;
+        }
+        *reinterpret_cast<float4 *>(st + r * (CC + 4) + c) = acc;
+    }
+    __syncthreads();
+    const int col0 = tn * BN + c0;
+    Epi::template run_with_stats<256>(ep, st, CC + 4, rowm, RC, col0, min(CC, args.N - col0), tm, args.N,
+                                      threadIdx.x);
+    Epi::template done<256>(ep, threadIdx.x, gridDim.x * gridDim.y * gridDim.z);
+}
+
+}  // namespace cdp

@@ -338,13 +338,13 @@ struct ResNetTrainer {
             c.dy = make_cbuf(kind, int(c.P), c.cout);
             if (c.impl == CI_IMPLICIT && c.stride != 1)
                 max_dcols = std::max<int64_t>(max_dcols, c.P * round_up(c.K, 16));
-            max_stats = std::max<int64_t>(max_stats, int64_t(c.tiles_fwd) * c.cout * 2);
+            max_stats = std::max<int64_t>(max_stats, int64_t(std::max(c.tiles_fwd, 160)) * c.cout * 2);
             max_part = std::max<int64_t>(max_part, ((c.P + kBnRows - 1) / kBnRows) * c.cout * 2);
         }
         const ConvL &c0 = convs[stem];
         cols = make_cbuf(kind, int(c0.P), c0.K);
-        for (auto &g : gbuf) g = DevBuf(size_t(max_act) * 4);
-        dcols = DevBuf(size_t(max_dcols) * 4);
+        for (auto &g : gbuf) g = DevBuf(size_t(max_act) * ysz());
+        dcols = DevBuf(size_t(max_dcols) * ysz());
         stats_fwd = DevBuf(size_t(max_stats) * 4);
         bnpart[0] = DevBuf(size_t(max_part) * 8);
         bnpart[1] = DevBuf(size_t(max_part) * 8);
@@ -448,8 +448,7 @@ struct ResNetTrainer {
         const int splits = splits_for(tiles, (Kd + bk - 1) / bk);
         bn_switch(BN, [&](auto bnc) {
             constexpr int BNc = decltype(bnc)::value;
-            if constexpr ((!BMN || BNc % (K == 0 ? 64 : 32) == 0) && (!Epi::kTile || BNc <= 64 ||
-                                                                      std::is_same<Epi, EpiConvOut<K>>::value)) {
+            if constexpr ((!BMN || BNc % (K == 0 ? 64 : 32) == 0) && (!Epi::kTile || BNc <= 64)) {
                 GemmPlan p = plan_gemm<K, BNc, AMN, BMN>(A, Bo, nseg, int(M), int(N), int(Kd), splits, ws_for(hop),
                                                           cnt_for(hop));
                 run_plan<K, BNc, AMN, BMN, Epi, GM_PLAIN>(name, 2.0 * M * N * Kd, p, ep, s, hop);
@@ -465,37 +464,100 @@ struct ResNetTrainer {
     }
     Nhwc nhwc_dy(const ConvL &c) const { return Nhwc{c.dy.hi.p, c.dy.lo.p, c.dy.ld, c.cout, c.Wo, c.Ho, B}; }
 
-    // Implicit conv GEMM (MODE = GM_FPROP / GM_DGRAD / GM_WGRAD).
+    // ---------------------------------------------------------------- persistent GEMM path
+    int sms_ = 0;
+    int last_stat_slots = 0;
+    int sms() {
+        if (!sms_) sms_ = num_sms();
+        return sms_;
+    }
+
+    template <int K, int BNc, bool AMN, bool BMN, class Epi, int MODE>
+    void run_pk(const char *name, double flops, const GemmPlan &gp, const typename Epi::Params &ep, cudaStream_t s,
+                bool hop) {
+        using Cfg = PkCfg<K, BNc, AMN, BMN, Epi::kStages>;
+        PkArgs a{};
+        a.M = gp.args.M;
+        a.N = gp.args.N;
+        a.tiles_m = int(gp.grid.x);
+        a.tiles_n = int(gp.grid.y);
+        a.kb_per_seg = gp.args.kb_per_seg;
+        a.n_seg = gp.args.n_seg;
+        a.total_iters = a.kb_per_seg * a.n_seg;
+        const int tiles = a.tiles_m * a.tiles_n;
+        int splits = 1;
+        if (tiles < sms()) splits = std::max(1, std::min(sms() / tiles, a.total_iters / 4));  // units <= one wave
+        a.iters_per_split = (a.total_iters + splits - 1) / splits;
+        a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
+        a.units = tiles * a.splits;
+        a.boxed = (MODE == GM_FPROP || MODE == GM_DGRAD) ? 1 : 0;
+        a.cv = gp.args.cv;
+        const size_t need = a.splits > 1 ? size_t(tiles) * a.splits * 128 * BNc : 0;
+        size_t &cap = hop ? ws_h_floats : ws_c_floats;
+        if (sizing) {
+            cap = std::max(cap, need);
+            return;
+        }
+        CDP_REQUIRE(need <= cap, "split-K workspace too small");
+        a.ws = ws_for(hop);
+        auto kern = gemm_pk_kernel<K, BNc, AMN, BMN, Epi, MODE>;
+        static bool attr = false;
+        if (!attr) {
+            CDP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+            attr = true;
+        }
+        const int grid = std::min(a.units, sms());
+        last_stat_slots = a.splits > 1 ? a.tiles_m : grid;  // EpiConvOut2 statistics rows
+        L(name, flops, 0.0, s, [&] { launch_pdl(kern, dim3(grid), dim3(kPkThreads), Cfg::SMEM, s, gp.maps, a, ep); });
+        if (a.splits > 1) {
+            constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
+            constexpr int RC = kStats ? 128 : 4;
+            constexpr int CC = kStats ? 32 : (BNc < 64 ? BNc : 64);
+            L("splitk_reduce", 0, double(need) * 4, s, [&] {
+                launch_pdl(pk_reduce_kernel<BNc, Epi, RC, CC>, dim3(tiles, 128 / RC, BNc / CC), dim3(256), 0, s, a,
+                           ep);
+            });
+        }
+    }
+
+    template <int K, bool AMN, bool BMN, class Epi>
+    void pk_plain(const char *name, int BN, const CTensor &a, const CTensor &b, int64_t M, int64_t N, int64_t Kd,
+                  const typename Epi::Params &ep, cudaStream_t s, bool hop) {
+        Operand A[3], Bo[3];
+        int nseg = 1;
+        A[0] = opnd(a, false, AMN, M, Kd);
+        Bo[0] = opnd(b, false, BMN, N, Kd);
+        if (K == 1) {
+            nseg = 3;
+            A[1] = A[0];
+            Bo[1] = opnd(b, true, BMN, N, Kd);
+            A[2] = opnd(a, true, AMN, M, Kd);
+            Bo[2] = Bo[0];
+        }
+        bn_switch(BN, [&](auto bnc) {
+            constexpr int BNc = decltype(bnc)::value;
+            if constexpr (BNc >= 64 && (!BMN || BNc % (K == 0 ? 64 : 32) == 0)) {
+                GemmPlan p = plan_gemm<K, BNc, AMN, BMN>(A, Bo, nseg, int(M), int(N), int(Kd), 1, nullptr, nullptr);
+                run_pk<K, BNc, AMN, BMN, Epi, GM_PLAIN>(name, 2.0 * M * N * Kd, p, ep, s, hop);
+            } else {
+                throw CdpError("unsupported GEMM configuration");
+            }
+        });
+    }
+
     template <int K, int MODE, class Epi>
-    void conv_gemm(const char *name, int BN, const ConvL &c, const CBuf &w, const typename Epi::Params &ep,
-                   cudaStream_t s, bool hop) {
+    void pk_conv(const char *name, int BN, const ConvL &c, const CBuf &w, const typename Epi::Params &ep,
+                 cudaStream_t s, bool hop) {
         const Nhwc a = c.in_act >= 0 ? nhwc_act(c.in_act) : Nhwc{};
         const Nhwc dy = nhwc_dy(c);
-        const int ch = chunk();
-        int64_t tiles = 0, kb = 0;
-        if (MODE == GM_FPROP) {
-            const ConvGeom g = conv_geom(c.cin, c.R, c.S, c.stride, c.pad, c.Wo, c.Ho, B, 128, ch);
-            tiles = int64_t(conv_boxes(g)) * ((c.cout + BN - 1) / BN);
-            kb = int64_t(c.R) * c.S * (c.cin / ch);
-        } else if (MODE == GM_DGRAD) {
-            const ConvGeom g = conv_geom(c.cout, c.R, c.S, 1, c.pad, c.W, c.H, B, 128, ch);
-            tiles = int64_t(conv_boxes(g)) * ((c.cin + BN - 1) / BN);
-            kb = int64_t(c.R) * c.S * (c.cout / ch);
-        } else {
-            const ConvGeom g = conv_geom(c.cin, c.R, c.S, c.stride, c.pad, c.Wo, c.Ho, B, ch, ch);
-            tiles = ((int64_t(c.K) + 127) / 128) * ((c.cout + BN - 1) / BN);
-            kb = conv_boxes(g);
-        }
-        const int splits = splits_for(tiles, kb);
         const double flops = 2.0 * double(c.P) * c.K * c.cout;
         bn_switch(BN, [&](auto bnc) {
             constexpr int BNc = decltype(bnc)::value;
             constexpr bool AMN = MODE == GM_WGRAD, BMN = MODE != GM_DGRAD;
-            if constexpr ((!BMN || BNc % (K == 0 ? 64 : 32) == 0) &&
-                          (std::is_same<Epi, EpiConvOut<K>>::value || BNc <= 64)) {
+            if constexpr (BNc >= 64 && (!BMN || BNc % (K == 0 ? 64 : 32) == 0)) {
                 GemmPlan p = plan_conv<K, BNc, MODE>(a, w.hi.p, w.lo.p, w.ld, dy, c.R, c.S, c.stride, c.pad, c.cin,
-                                                     c.cout, splits, ws_for(hop), cnt_for(hop));
-                run_plan<K, BNc, AMN, BMN, Epi, MODE>(name, flops, p, ep, s, hop);
+                                                     c.cout, 1, nullptr, nullptr);
+                run_pk<K, BNc, AMN, BMN, Epi, MODE>(name, flops, p, ep, s, hop);
             } else {
                 throw CdpError("unsupported conv GEMM configuration");
             }
@@ -509,26 +571,24 @@ struct ResNetTrainer {
     template <int K>
     void conv_forward(int ci, int vslot, cudaStream_t s) {
         ConvL &c = convs[ci];
-        typename EpiConvOut<K>::Params ep{};
+        typename EpiConvOut2<K>::Params ep{};
         ep.out = c.y.p;
         ep.ld = c.cout;
-        ep.out_f32 = 0;
         ep.stats = stats_fwd.as<float>();
+        ep.tiles = c.tiles_fwd;
         const CBuf &w = wc[vslot][c.tw];
         if (c.impl == CI_IMPLICIT) {
-            ep.boxed = 1;
-            ep.g = conv_geom(c.cin, c.R, c.S, c.stride, c.pad, c.Wo, c.Ho, B, 128, chunk());
-            conv_gemm<K, GM_FPROP, EpiConvOut<K>>("conv_fprop", tile_n(c.cout), c, w, ep, s, false);
+            pk_conv<K, GM_FPROP, EpiConvOut2<K>>("conv_fprop", tile_n(c.cout), c, w, ep, s, false);
         } else {
-            ep.boxed = 0;
             const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
             const int64_t Kd = c.impl == CI_STEM ? c.K : c.cin;
-            gemm<K, false, true, EpiConvOut<K>>(c.impl == CI_STEM ? "stem_fprop" : "conv_fprop_1x1",
-                                                tile_n(c.cout), in, w.view(), c.P, c.cout, Kd, ep, s, false);
+            pk_plain<K, false, true, EpiConvOut2<K>>(c.impl == CI_STEM ? "stem_fprop" : "conv_fprop_1x1",
+                                                     tile_n(c.cout), in, w.view(), c.P, c.cout, Kd, ep, s, false);
         }
-        L("bn_finalize_fwd", 0, double(c.tiles_fwd) * c.cout * 8, s, [&] {
+        const int slots = sizing ? c.tiles_fwd : last_stat_slots;
+        L("bn_finalize_fwd", 0, double(slots) * c.cout * 8, s, [&] {
             launch_pdl(bn_finalize_fwd_kernel, dim3((c.cout * 32 + 255) / 256), dim3(256), 0, s,
-                       (const float *)stats_fwd.as<float>(), c.tiles_fwd, c.cout, c.P, eps, c.mean.as<float>(),
+                       (const float *)stats_fwd.as<float>(), slots, c.cout, c.P, eps, c.mean.as<float>(),
                        c.rstd.as<float>());
         });
     }
@@ -536,14 +596,15 @@ struct ResNetTrainer {
     const float *gamma(int ci, int vslot) const { return theta[vslot] + tens[convs[ci].tb].base; }
     const float *beta(int ci, int vslot) const { return theta[vslot] + tens[convs[ci].tb].base + convs[ci].cout; }
     int vs(int tensor, int p) const { return tens[tensor].fresh ? p : (p ^ 1); }
-    int esz() const { return kind == 0 ? 2 : 8; }
+    int esz() const { return kind == 0 ? 2 : 8; }   // compute-format bytes per element
+    int ysz() const { return kind == 0 ? 2 : 4; }   // Y-format (conv outputs, gradients) bytes per element
 
     template <int K>
     void bn_apply(int ci, int vslot, const BnResidual &res, const CTensor &out, cudaStream_t s) {
         ConvL &c = convs[ci];
-        const double bytes = double(c.P) * c.cout * (esz() * 2 + ((res.act.hi || res.y) ? esz() : 0));
+        const double bytes = double(c.P) * c.cout * (ysz() + esz() + (res.act.hi ? esz() : res.y ? ysz() : 0));
         L("bn_apply", 0, bytes, s, [&] {
-            launch_pdl(bn_apply_kernel<K>, dim3(blocks_for(c.P * c.cout / 4)), dim3(256), 0, s, (const void *)c.y.p,
+            launch_pdl(bn_apply_kernel<K>, dim3(blocks_for(c.P * c.cout / 8)), dim3(256), 0, s, (const void *)c.y.p,
                        c.P, c.cout, (const float *)c.mean.as<float>(), (const float *)c.rstd.as<float>(),
                        gamma(ci, vslot), beta(ci, vslot), res, 1, out);
         });
@@ -553,9 +614,15 @@ struct ResNetTrainer {
     void forward(int p, cudaStream_t s, const std::function<void(int)> &pull) {
         ConvL &c0 = convs[stem];
         L("stem_im2col", 0, double(c0.P) * cols.ld * esz(), s, [&] {
-            launch_pdl(stem_im2col_kernel<K>, dim3(blocks_for(c0.P * cols.ld)), dim3(256), 0, s,
-                       (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), Hin, Win, Cin0, c0.R, c0.S,
-                       c0.stride, c0.pad, c0.Ho, c0.Wo, c0.P, cols.view());
+            const int64_t n = c0.P * (cols.ld / 8);
+            if (c0.R == 3)
+                launch_pdl(stem_im2col_kernel<K, 3, 3>, dim3(blocks_for(n)), dim3(256), 0, s,
+                           (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), Hin, Win, c0.stride,
+                           c0.pad, c0.Ho, c0.Wo, int(c0.P), cols.view());
+            else
+                launch_pdl(stem_im2col_kernel<K, 7, 3>, dim3(blocks_for(n)), dim3(256), 0, s,
+                           (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), Hin, Win, c0.stride,
+                           c0.pad, c0.Ho, c0.Wo, int(c0.P), cols.view());
         });
         pull(c0.tw);
         pull(c0.tb);
@@ -564,7 +631,7 @@ struct ResNetTrainer {
         if (pool_act >= 0) {
             const int a = stem_act, o = pool_act;
             L("maxpool_fwd", 0, double(act_P[a] + act_P[o]) * act_C[a] * esz(), s, [&] {
-                launch_pdl(maxpool_fwd_kernel<K>, dim3(blocks_for(act_P[o] * act_C[o])), dim3(256), 0, s,
+                launch_pdl(maxpool_fwd_kernel<K>, dim3(blocks_for(act_P[o] * act_C[o] / 4)), dim3(256), 0, s,
                            acts[a].view(), B, act_H[a], act_W[a], act_C[a], act_H[o], act_W[o], acts[o].view(),
                            pool_arg.as<uint8_t>());
             });
@@ -613,12 +680,12 @@ struct ResNetTrainer {
     // BN backward of conv ci (and of the projection conv `ds` sharing g' and the mask):
     // statistics, finalise, dy = BN'(g') in compute format.
     template <int K>
-    void bn_backward(int ci, int ds, int p, const float *g, const CTensor &mask, cudaStream_t s) {
+    void bn_backward(int ci, int ds, int p, const void *g, const CTensor &mask, cudaStream_t s) {
         ConvL &c = convs[ci];
         const int nblk = int((c.P + kBnRows - 1) / kBnRows);
         const int C4 = c.cout / 4, TPR = C4 < 32 ? C4 : 32;
         const ConvL *cd = ds >= 0 ? &convs[ds] : nullptr;
-        const double bytes = double(c.P) * c.cout * (4 + esz() + esz() + (cd ? esz() : 0));
+        const double bytes = double(c.P) * c.cout * (ysz() + esz() + ysz() + (cd ? ysz() : 0));
         L("bn_bwd_stats", 0, bytes, s, [&] {
             launch_pdl(bn_bwd_stats_kernel<K>, dim3(nblk, (C4 + TPR - 1) / TPR), dim3(256), 0, s, g, mask, c.P,
                        c.cout, (const void *)c.y.p, (const float *)c.mean.as<float>(),
@@ -637,8 +704,8 @@ struct ResNetTrainer {
             });
             const int cidx = k == 0 ? ci : ds;
             const int vslot = vs(cc.tb, p);
-            L("bn_bwd_apply", 0, double(cc.P) * cc.cout * (4 + esz() * 3), s, [&] {
-                launch_pdl(bn_bwd_apply_kernel<K>, dim3(blocks_for(cc.P * cc.cout / 4)), dim3(256), 0, s, g, mask,
+            L("bn_bwd_apply", 0, double(cc.P) * cc.cout * (2 * ysz() + 2 * esz()), s, [&] {
+                launch_pdl(bn_bwd_apply_kernel<K>, dim3(blocks_for(cc.P * cc.cout / 8)), dim3(256), 0, s, g, mask,
                            (const void *)cc.y.p, cc.P, cc.cout, (const float *)cc.mean.as<float>(),
                            (const float *)cc.rstd.as<float>(), gamma(cidx, vslot),
                            (const float *)cc.dbeta.as<float>(), (const float *)cc.dgamma.as<float>(), cc.dy.view());
@@ -647,37 +714,37 @@ struct ResNetTrainer {
     }
 
     // conv data gradient into g_in (fp32 [Pin][cin]).
+    // add != null: g_in = dgrad + (add masked by add_mask) (the block's residual branch).
     template <int K>
-    void conv_dgrad(int ci, int vslot, float *g_in, cudaStream_t s) {
+    void conv_dgrad(int ci, int vslot, void *g_in, cudaStream_t s, const void *add = nullptr,
+                    CTensor add_mask = CTensor{}) {
         ConvL &c = convs[ci];
         const CBuf &w = wc[vslot][c.tw];
-        typename EpiConvOut<K>::Params ep{};
-        ep.out_f32 = 1;
+        typename EpiConvOut2<K>::Params ep{};
         ep.stats = nullptr;
+        ep.add = add;
+        ep.add_mask = add_mask;
         if (c.impl == CI_PLAIN) {
             ep.out = g_in;
             ep.ld = c.cin;
-            ep.boxed = 0;
-            gemm<K, false, false, EpiConvOut<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(), c.P, c.cin,
-                                                 c.cout, ep, s, false);
+            pk_plain<K, false, false, EpiConvOut2<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(), c.P,
+                                                      c.cin, c.cout, ep, s, false);
         } else if (c.stride == 1) {
             ep.out = g_in;
             ep.ld = c.cin;
-            ep.boxed = 1;
-            ep.g = conv_geom(c.cout, c.R, c.S, 1, c.pad, c.W, c.H, B, 128, chunk());
-            conv_gemm<K, GM_DGRAD, EpiConvOut<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
+            pk_conv<K, GM_DGRAD, EpiConvOut2<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
         } else {
             const int Kp = round_up(c.K, 16);
             ep.out = dcols.p;
             ep.ld = Kp;
-            ep.boxed = 0;
+            ep.add = nullptr;
+            ep.add_mask = CTensor{};
             // dcols[P][K] = dy[P][Cout] . W^T, W viewed [K][Cout] (K-major B)
-            gemm<K, false, false, EpiConvOut<K>>("conv_dgrad_s2", tile_n(c.K), c.dy.view(), w.view(), c.P, c.K,
-                                                 c.cout, ep, s, false);
+            pk_plain<K, false, false, EpiConvOut2<K>>("conv_dgrad_s2", tile_n(c.K), c.dy.view(), w.view(), c.P, c.K,
+                                                      c.cout, ep, s, false);
             const int64_t nin = c.Pin * c.cin / 4;
-            L("col2im", 0, double(c.P) * Kp * 4 + double(c.Pin) * c.cin * 4, s, [&] {
-                launch_pdl(col2im_kernel, dim3(blocks_for(nin)), dim3(256), 0, s, (const float *)dcols.as<float>(),
-                           Kp, B, c.H, c.W, c.cin, c.R, c.S, c.stride, c.pad, c.Ho, c.Wo, g_in);
+            L("col2im", 0, (double(c.P) * Kp + double(c.Pin) * c.cin * (add ? 2 : 1)) * ysz(), s, [&] {
+                launch_pdl(col2im_kernel<K>, dim3(blocks_for(nin)), dim3(256), 0, s, (const void *)dcols.p, Kp, B, c.H, c.W, c.cin, c.R, c.S, c.stride, c.pad, c.Ho, c.Wo, g_in, add, add_mask);
             });
         }
     }
@@ -726,11 +793,11 @@ struct ResNetTrainer {
         HopParams hp = hop_params(c.tw, p);
         hop_wait(hp, s);
         if (c.impl == CI_IMPLICIT) {
-            conv_gemm<K, GM_WGRAD, EpiWgradConv<K>>("conv_wgrad_hop", 64, c, wc[0][c.tw], hp, s, true);
+            pk_conv<K, GM_WGRAD, EpiHop2<K>>("conv_wgrad_hop", tile_n(c.cout), c, wc[0][c.tw], hp, s, true);
         } else {
             const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
-            gemm<K, true, true, EpiWgradConv<K>>(c.impl == CI_STEM ? "stem_wgrad_hop" : "conv_wgrad_hop_1x1", 64, in,
-                                                 c.dy.view(), c.K, c.cout, c.P, hp, s, true);
+            pk_plain<K, true, true, EpiHop2<K>>(c.impl == CI_STEM ? "stem_wgrad_hop" : "conv_wgrad_hop_1x1",
+                                                tile_n(c.cout), in, c.dy.view(), c.K, c.cout, c.P, hp, s, true);
         }
     }
 
@@ -832,13 +899,12 @@ struct ResNetTrainer {
             gemm<K, true, true, EpiWgrad<K>>("fc_wgrad_hop", 64, pooled.view(), dz.view(), fc_in + 1, classes, B, hp,
                                              hs, true);
         }
-        float *G0 = gbuf[0].as<float>(), *G1 = gbuf[1].as<float>(), *G2 = gbuf[2].as<float>(),
-              *G3 = gbuf[3].as<float>();
+        void *G0 = gbuf[0].p, *G1 = gbuf[1].p, *G2 = gbuf[2].p, *G3 = gbuf[3].p;
         // pool backward -> gradient w.r.t. the last activation (G0 holds the block-output gradient)
         const int la = blocks.empty() ? stem_act : blocks.back().a_out;
         const int HW = int(act_P[la] / B);
-        L("avgpool_bwd", 0, double(act_P[la]) * fc_in * 4, cs, [&] {
-            launch_pdl(avgpool_backward_kernel, dim3(blocks_for(act_P[la] * fc_in / 4)), dim3(256), 0, cs,
+        L("avgpool_bwd", 0, double(act_P[la]) * fc_in * ysz(), cs, [&] {
+            launch_pdl(avgpool_backward_kernel<K>, dim3(blocks_for(act_P[la] * fc_in / 4)), dim3(256), 0, cs,
                        (const float *)dpooled.as<float>(), fc_in, B, HW, fc_in, G0);
         });
         for (int bi = int(blocks.size()) - 1; bi >= 0; --bi) {
@@ -848,47 +914,43 @@ struct ResNetTrainer {
             // last BN (+ projection BN): g' = G0 masked by the block output
             bn_backward<K>(b.convs[n - 1], b.ds, p, G0, m_out, cs);
             cudaEvent_t dy_last = ev(cs);
-            float *chain[2] = {G1, G2};
-            float *g_main = nullptr;
-            cudaEvent_t dy_next = dy_last;
-            for (int i = n - 1; i >= 0; --i) {
-                const int ci = b.convs[i];
-                float *out = chain[(n - 1 - i) & 1];
-                conv_dgrad<K>(ci, vs(convs[ci].tw, p), out, cs);
-                cudaEvent_t dg = ev(cs);
-                hop_conv<K>(ci, p, dy_next, dg);
-                if (i > 0) {
-                    bn_backward<K>(b.convs[i - 1], -1, p, out, acts[b.mid[i - 1]].view(), cs);
-                    dy_next = ev(cs);
-                } else {
-                    g_main = out;
-                }
-            }
-            const int64_t Pin = act_P[b.a_in];
-            const int Cin = act_C[b.a_in];
+            // projection shortcut first: its data gradient is folded into the first conv's
             if (b.ds >= 0) {
                 conv_dgrad<K>(b.ds, vs(convs[b.ds].tw, p), G3, cs);
                 cudaEvent_t dg = ev(cs);
                 hop_conv<K>(b.ds, p, dy_last, dg);
-                L("residual_add", 0, double(Pin) * Cin * 12, cs, [&] {
-                    launch_pdl(add_kernel<K>, dim3(blocks_for(Pin * Cin / 4)), dim3(256), 0, cs, (const float *)g_main,
-                               (const float *)G3, Pin, Cin, CTensor{}, G0);
-                });
-            } else {
-                L("residual_add", 0, double(Pin) * Cin * (12 + esz()), cs, [&] {
-                    launch_pdl(add_kernel<K>, dim3(blocks_for(Pin * Cin / 4)), dim3(256), 0, cs, (const float *)g_main,
-                               (const float *)G0, Pin, Cin, m_out, G0);
-                });
+            }
+            void *chain[2] = {G1, G2};
+            cudaEvent_t dy_next = dy_last;
+            for (int i = n - 1; i >= 0; --i) {
+                const int ci = b.convs[i];
+                if (i > 0) {
+                    void *out = chain[(n - 1 - i) & 1];
+                    conv_dgrad<K>(ci, vs(convs[ci].tw, p), out, cs);
+                    cudaEvent_t dg = ev(cs);
+                    hop_conv<K>(ci, p, dy_next, dg);
+                    bn_backward<K>(b.convs[i - 1], -1, p, out, acts[b.mid[i - 1]].view(), cs);
+                    dy_next = ev(cs);
+                } else {
+                    // block input gradient = main branch + shortcut branch, written over G0
+                    if (b.ds >= 0)
+                        conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, G3, CTensor{});
+                    else
+                        conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, G0, m_out);
+                    cudaEvent_t dg = ev(cs);
+                    hop_conv<K>(ci, p, dy_next, dg);
+                }
             }
         }
         // stem (gradient w.r.t. the stem output / max-pool output in G0)
         ConvL &c0 = convs[stem];
-        const float *gs = G0;
+        const void *gs = G0;
         if (pool_act >= 0) {
             const int a = stem_act, o = pool_act;
-            L("maxpool_bwd", 0, double(act_P[o]) * act_C[o] * 5 + double(act_P[a]) * act_C[a] * 4, cs, [&] {
-                launch_pdl(maxpool_bwd_kernel, dim3(blocks_for(act_P[a] * act_C[a])), dim3(256), 0, cs,
-                           (const float *)G0, (const uint8_t *)pool_arg.as<uint8_t>(), B, act_H[a], act_W[a],
+            L("maxpool_bwd", 0, double(act_P[o]) * act_C[o] * (1 + ysz()) + double(act_P[a]) * act_C[a] * ysz(), cs,
+              [&] {
+                launch_pdl(maxpool_bwd_kernel<K>, dim3(blocks_for(act_P[a] * act_C[a] / 4)), dim3(256), 0, cs,
+                           (const void *)G0, (const uint8_t *)pool_arg.as<uint8_t>(), B, act_H[a], act_W[a],
                            act_C[a], act_H[o], act_W[o], G1);
             });
             gs = G1;
@@ -1055,7 +1117,7 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
         CDP_REQUIRE(n_layers >= 1 && n_layers <= 8, "1..8 residual stages");
         CDP_REQUIRE(block_kind == 0 || block_kind == 1, "block_kind: 0 basic, 1 bottleneck");
         CDP_REQUIRE(stem_kind == 0 || stem_kind == 1, "stem_kind: 0 CIFAR 3x3, 1 ImageNet 7x7 + max pool");
-        CDP_REQUIRE(in_channels >= 1 && in_channels <= 4, "stem input channels: 1..4");
+        CDP_REQUIRE(in_channels == 3, "stem input channels: 3 (RGB)");
         for (int l = 0; l < n_layers; ++l)
             CDP_REQUIRE(widths[l] % 64 == 0 && widths[l] <= 512, "widths: multiples of 64 up to 512");
         auto tr = std::make_unique<ResNetTrainer>();

@@ -21,6 +21,16 @@ theta = np.concatenate([rng.normal(0, (2.0 / (np.prod(s[:3]) if k == "conv" else
                         for k, s, _ in specs])
 tr.set_params(theta, -1)
 tr.connect([tr.region()])
+GEMM_NAMES = {"conv_fprop", "conv_fprop_1x1", "conv_dgrad", "conv_dgrad_1x1", "conv_dgrad_s2", "conv_wgrad_hop",
+              "conv_wgrad_hop_1x1", "stem_fprop", "stem_wgrad_hop"}
+if os.environ.get("ONLY"):  # one eager instrumented step only (for ncu --launch-skip over gemm_pk launches)
+    ops = tr.profile_step(rng.permutation(len(x))[:B], 0.05, serial=True)
+    gi = 0
+    for i, (name, fl, by, t) in enumerate(ops):
+        if name in GEMM_NAMES:
+            print(f"gemm_pk #{gi:3d} op {i:4d} {name:22s} {t * 1e3:8.1f} us")
+            gi += 1
+    sys.exit(0)
 for k in range(3):
     tr.step(rng.permutation(len(x))[:B], 0.05)
 tr.sync()
@@ -43,3 +53,8 @@ if os.environ.get("PROFILE"):
     for name, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         rate = f"{a[2] / a[1] / 1e9:8.1f} TFLOP/s" if a[2] else f"{a[3] / a[1] / 1e6:8.1f} GB/s"
         print(f"  {name:24s} n={a[0]:4d} {a[1]:8.3f} ms {100 * a[1] / tot:5.1f}%  {rate}")
+    if os.environ.get("TOP"):
+        print("top launches:")
+        for i, (name, fl, by, t) in sorted(enumerate(ops), key=lambda kv: -kv[1][3])[:int(os.environ["TOP"])]:
+            rate = f"{fl / t / 1e9:8.1f} TFLOP/s" if fl else f"{by / t / 1e6:8.1f} GB/s"
+            print(f"  #{i:4d} {name:24s} {t * 1e3:8.1f} us  {rate}  flops {fl:.3g} bytes {by:.3g}")
