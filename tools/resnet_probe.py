@@ -28,7 +28,7 @@ if os.environ.get("ONLY"):  # one eager instrumented step only (for ncu --launch
     gi = 0
     for i, (name, fl, by, t) in enumerate(ops):
         if name in GEMM_NAMES:
-            print(f"gemm_pk #{gi:3d} op {i:4d} {name:22s} {t * 1e3:8.1f} us")
+            print(f"gemm_pk {gi} op {i} {name} {t * 1e3:.1f} us")
             gi += 1
     sys.exit(0)
 for k in range(3):
