@@ -162,7 +162,13 @@ int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const int32_t *d
                            int in_channels, int height, int width, int classes, int micro_batch, int world, int rank,
                            const int32_t *tensor_stage, const uint8_t *stage_fresh, int dtype, float momentum,
                            float weight_decay, int n_samples, const float *x, const int32_t *labels,
-                           cdp_resnet **out);
+                           const int32_t *zero_table, cdp_resnet **out);
+/* zero_table != NULL (world > 1): ZeRO-CDP state passing (ref comm.py:93-144), [world stages][2 (F, B)]
+ * [world ranks][3] = (use-index base, predecessor rank, predecessor step offset) from zero.py; every
+ * use of a parameter tensor copies the tensor's state (both theta slots + momentum) from its
+ * predecessor's HBM.  cdp_resnet_zero_drain publishes the forward uses of the next (unlaunched) step
+ * at the end of a run (call on every rank before synchronising). */
+int cdp_resnet_zero_drain(cdp_resnet *tr);
 /* Parameter count, tensor count and (optional) per-tensor base offsets / kinds (0 conv, 1 bn, 2 fc). */
 int cdp_resnet_info(cdp_resnet *tr, int64_t *n_params, int *n_tensors, int64_t *tensor_base, int32_t *tensor_kind);
 int cdp_resnet_region(cdp_resnet *tr, void **base);
@@ -184,8 +190,8 @@ int cdp_resnet_profile_step(cdp_resnet *tr, const int32_t *perm, float lr, int s
 int cdp_resnet_history(cdp_resnet *tr, int max, double *losses, uint32_t *flags, int *count);
 int cdp_resnet_sync(cdp_resnet *tr);
 int cdp_resnet_ring_error(cdp_resnet *tr, int *err);
-/* out[0..4] = activation bytes, parameter-state bytes, kernels per step, tensor-core flops per step,
- * fp32 gradient scratch bytes. */
+/* out[0..5] = activation bytes, parameter-state bytes, kernels per step, tensor-core flops per step,
+ * gradient scratch bytes, ZeRO-CDP state bytes received per step. */
 int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out);
 int cdp_resnet_mark(cdp_resnet *tr, int k);
 int cdp_resnet_elapsed(cdp_resnet *tr, int a, int b, float *ms);

@@ -153,6 +153,7 @@ struct RingFlags {
     uint32_t consumed[kMaxStages];   // the next rank finished reading this rank's S^j of that step
     uint32_t updated[kMaxStages];    // updater: stage j holds version `updated[j]`
     uint32_t pulled[kMaxStages][2];  // updater: readers that pulled version v (slot v % 2)
+    uint32_t zdone[kMaxStages];      // ZeRO-CDP: global use index of this rank's last finished use of a unit
     uint32_t err;                    // a spin-wait timed out (protocol failure)
     uint32_t pad[31];
 };

@@ -101,6 +101,57 @@ __global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, in
     }
 }
 
+// ---------------------------------------------------------------- ZeRO-CDP state passing
+// (zero.py: use index u = base + (t-1)*2N + kZeroOff; predecessor on rank `src` in step t + dstep)
+constexpr uint32_t kZeroOff = 1024;
+
+struct ZeroUse {
+    int base, src, dstep, uses_per_step;
+};
+
+__device__ __forceinline__ uint32_t zero_u(const ZeroUse &z, int t) {
+    return uint32_t(z.base + (t - 1) * z.uses_per_step) + kZeroOff;
+}
+
+// Wait (one thread) until the predecessor's rank finished its use of `unit`.
+__global__ void zero_wait_kernel(ZeroUse z, int self, const RingFlags *src_flags, RingFlags *own, int unit,
+                                 const int *step, int step_delta) {
+    const int t = *step + step_delta;
+    if (threadIdx.x != 0 || z.src == self || t + z.dstep < 1) return;
+    const uint32_t pu = zero_u(z, t) - 1;
+    spin_ge(&src_flags->zdone[unit - 1], pu, &own->err);
+}
+
+// Copy the unit's state (both theta version slots, momentum) from the predecessor's HBM
+// (peer memory) and repack the compute copies of both slots.
+template <int KIND>
+__global__ void zero_copy_kernel(ZeroUse z, int self, const float *src_t0, const float *src_t1, const float *src_v,
+                                 float *t0, float *t1, float *v, int64_t n, int cols, CTensor wc0, CTensor wc1,
+                                 const int *step) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int t = *step;
+    if (z.src == self || t + z.dstep < 1) return;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const float a = __ldcv(src_t0 + i), b = __ldcv(src_t1 + i);
+        t0[i] = a;
+        t1[i] = b;
+        if (v) v[i] = __ldcv(src_v + i);
+        if (wc0.hi) {
+            const size_t w = size_t(i / cols) * wc0.ld + i % cols;
+            Fmt<KIND>::store(wc0.hi, wc0.lo, w, a);
+            Fmt<KIND>::store(wc1.hi, wc1.lo, w, b);
+        }
+    }
+}
+
+// Publish the end of this rank's use of `unit` (after all its kernels on the stream).
+__global__ void zero_done_kernel(ZeroUse z, RingFlags *own, int unit, const int *step, int step_delta) {
+    const int t = *step + step_delta;
+    __threadfence_system();
+    ptx::st_release_sys(&own->zdone[unit - 1], zero_u(z, t));
+}
+
 __global__ void finish_step_kernel_rn(const double *loss, Flags *flags, double *hist_loss, Flags *hist_flags, int cap,
                                       const int *step) {
     const int c = *step - 1;
@@ -145,7 +196,8 @@ struct ResNetTrainer {
     int64_t P = 0, Pp = 0;
 
     // ---------------------------------------------------------------- state
-    DevBuf region, vel, cta_counters;
+    DevBuf region, cta_counters;
+    float *vel = nullptr;  // momentum, inside the shared region (ZeRO-CDP peers copy it)
     float *theta[2] = {nullptr, nullptr};
     float *partial = nullptr;
     RingFlags *ring = nullptr;
@@ -164,6 +216,11 @@ struct ResNetTrainer {
     size_t ws_c_floats = 0, ws_h_floats = 0;
     DevBuf data_x, data_lab, ctrl_dev, perm_dev, flags_dev, hist_loss, hist_flags;
     int n_samples = 0;
+    // ZeRO-CDP: per (stage, kind F/B, rank) use table from zero.py; peers' shared regions
+    bool zero = false;
+    std::vector<int> ztab;  // [stages][2][world][3] = (base, src rank, dstep)
+    std::vector<uint8_t *> peers;
+    int64_t zero_bytes_per_step = 0;
     static constexpr int RING_N = 16;
     uint8_t *stage_host = nullptr;
     size_t stage_bytes = 0;
@@ -358,12 +415,13 @@ struct ResNetTrainer {
         // shared region: RingFlags | theta0 | theta1 | partial
         region_off = (sizeof(RingFlags) + 255) / 256 * 256;
         Pp = (P + 63) / 64 * 64;
-        region = DevBuf(region_off + size_t(Pp) * 4 * 3);
+        // shared region: RingFlags | theta0 | theta1 | partial | momentum
+        region = DevBuf(region_off + size_t(Pp) * 4 * (momentum != 0.f ? 4 : 3));
         ring = region.as<RingFlags>();
         theta[0] = reinterpret_cast<float *>(region.as<uint8_t>() + region_off);
         theta[1] = theta[0] + Pp;
         partial = theta[1] + Pp;
-        if (momentum != 0.f) vel = DevBuf(size_t(P) * 4);
+        if (momentum != 0.f) vel = partial + Pp;
         cta_counters = DevBuf(2 * kMaxStages * 4);
         for (int v = 0; v < 2; ++v)
             for (auto &ts : tens) wc[v].push_back(ts.kind == T_BN ? CBuf{} : make_cbuf(kind, ts.rows, ts.cols));
@@ -627,7 +685,9 @@ struct ResNetTrainer {
         pull(c0.tw);
         pull(c0.tb);
         conv_forward<K>(stem, vs(c0.tw, p), s);
+        zdone(c0.tw, 0, s);
         bn_apply<K>(stem, vs(c0.tb, p), BnResidual{}, acts[stem_act].view(), s);
+        zdone(c0.tb, 0, s);
         if (pool_act >= 0) {
             const int a = stem_act, o = pool_act;
             L("maxpool_fwd", 0, double(act_P[a] + act_P[o]) * act_C[a] * esz(), s, [&] {
@@ -643,7 +703,11 @@ struct ResNetTrainer {
                 pull(c.tw);
                 pull(c.tb);
                 conv_forward<K>(b.convs[i], vs(c.tw, p), s);
-                if (i < n - 1) bn_apply<K>(b.convs[i], vs(c.tb, p), BnResidual{}, acts[b.mid[i]].view(), s);
+                zdone(c.tw, 0, s);
+                if (i < n - 1) {
+                    bn_apply<K>(b.convs[i], vs(c.tb, p), BnResidual{}, acts[b.mid[i]].view(), s);
+                    zdone(c.tb, 0, s);
+                }
             }
             BnResidual res{};
             if (b.ds >= 0) {
@@ -651,6 +715,7 @@ struct ResNetTrainer {
                 pull(cd.tw);
                 pull(cd.tb);
                 conv_forward<K>(b.ds, vs(cd.tw, p), s);
+                zdone(cd.tw, 0, s);
                 res.y = cd.y.p;
                 res.mean = cd.mean.as<float>();
                 res.rstd = cd.rstd.as<float>();
@@ -661,6 +726,8 @@ struct ResNetTrainer {
             }
             const int last = b.convs.back();
             bn_apply<K>(last, vs(convs[last].tb, p), res, acts[b.a_out].view(), s);
+            zdone(convs[last].tb, 0, s);
+            if (b.ds >= 0) zdone(convs[b.ds].tb, 0, s);
         }
         // pool + classifier
         const int la = blocks.empty() ? stem_act : blocks.back().a_out;
@@ -674,6 +741,7 @@ struct ResNetTrainer {
         ep.z = z.as<float>();
         gemm<K, true, false, EpiFwd<K>>("fc_fwd", 32, wc[vs(fc_t, p)][fc_t].view(), pooled.view(), classes, B,
                                         fc_in + 1, ep, s, false);
+        zdone(fc_t, 0, s);
     }
 
     // ---------------------------------------------------------------- backward pieces
@@ -682,6 +750,8 @@ struct ResNetTrainer {
     template <int K>
     void bn_backward(int ci, int ds, int p, const void *g, const CTensor &mask, cudaStream_t s) {
         ConvL &c = convs[ci];
+        zrecv<K>(c.tb, 1, s);
+        if (ds >= 0) zrecv<K>(convs[ds].tb, 1, s);
         const int nblk = int((c.P + kBnRows - 1) / kBnRows);
         const int C4 = c.cout / 4, TPR = C4 < 32 ? C4 : 32;
         const ConvL *cd = ds >= 0 ? &convs[ds] : nullptr;
@@ -719,6 +789,7 @@ struct ResNetTrainer {
     void conv_dgrad(int ci, int vslot, void *g_in, cudaStream_t s, const void *add = nullptr,
                     CTensor add_mask = CTensor{}) {
         ConvL &c = convs[ci];
+        zrecv<K>(c.tw, 1, s);
         const CBuf &w = wc[vslot][c.tw];
         typename EpiConvOut2<K>::Params ep{};
         ep.stats = nullptr;
@@ -761,7 +832,7 @@ struct ResNetTrainer {
         hp.s_out = partial;
         hp.theta_cur = theta[p];
         hp.theta_new = theta[p ^ 1];
-        hp.vel = vel.as<float>();
+        hp.vel = vel;
         hp.lr = &ctrl_dev.as<Control>()->lr;
         hp.momentum = momentum;
         hp.wd = wd;
@@ -771,7 +842,7 @@ struct ResNetTrainer {
         hp.grad_flags = &fl->grad;
         hp.upd_flags = &fl->upd;
         hp.sync.enabled = 1;
-        hp.sync.n_readers = world - 1;
+        hp.sync.n_readers = zero ? 0 : world - 1;  // ZeRO-CDP: no parameter pulls from the updater
         hp.sync.step = &ctrl_dev.as<Control>()->step;
         hp.sync.own = ring;
         hp.sync.prev = prev_ring;
@@ -824,8 +895,59 @@ struct ResNetTrainer {
     }
     bool last_updater() const { return rank == world - 1; }
 
+    // ---------------------------------------------------------------- ZeRO-CDP windows
+    ZeroUse zuse(int tensor, int kindFB) const {
+        const int st = tens[tensor].stage - 1;
+        const int *e = &ztab[((size_t(st) * 2 + kindFB) * world + rank) * 3];
+        return ZeroUse{e[0], e[1], e[2], 2 * world};
+    }
+    const float *peer_theta(int r, int slot) const {
+        return reinterpret_cast<const float *>(peers[r] + region_off) + size_t(slot) * Pp;
+    }
+    // Before this rank's first access to `tensor` in its F (0) / B (1) use: wait for the
+    // predecessor, copy the state from its HBM.
+    template <int K>
+    void zrecv(int tensor, int kindFB, cudaStream_t s, int step_delta = 0, bool copy = true) {
+        if (!zero || sizing) return;
+        CDP_REQUIRE(int(peers.size()) == world, "ZeRO-CDP needs connected peers");
+        const ZeroUse z = zuse(tensor, kindFB);
+        if (z.src == rank) return;
+        const TensorSpec &ts = tens[tensor];
+        const RingFlags *src_flags = reinterpret_cast<const RingFlags *>(peers[z.src]);
+        L("zero_wait", 0, 0, s, [&] {
+            zero_wait_kernel<<<1, 32, 0, s>>>(z, rank, src_flags, ring, tensor + 1,
+                                              (const int *)&ctrl_dev.as<Control>()->step, step_delta);
+            CDP_CUDA(cudaGetLastError());
+        });
+        if (!copy) return;
+        const float *sv = vel ? reinterpret_cast<const float *>(peers[z.src] + region_off) + 3 * size_t(Pp) : nullptr;
+        CTensor w0 = ts.kind == T_BN ? CTensor{} : wc[0][tensor].view();
+        CTensor w1 = ts.kind == T_BN ? CTensor{} : wc[1][tensor].view();
+        zero_bytes_per_step += ts.n * 4 * (vel ? 3 : 2);
+        L("zero_copy", 0, double(ts.n) * (vel ? 3 : 2) * 8, s, [&] {
+            launch_pdl(zero_copy_kernel<K>, dim3(blocks_for(ts.n, 1024)), dim3(256), 0, s, z, rank,
+                       peer_theta(z.src, 0) + ts.base, peer_theta(z.src, 1) + ts.base,
+                       sv ? sv + ts.base : (const float *)nullptr, theta[0] + ts.base, theta[1] + ts.base,
+                       vel ? vel + ts.base : (float *)nullptr, ts.n, std::max(ts.cols, 1), w0, w1,
+                       (const int *)&ctrl_dev.as<Control>()->step);
+        });
+    }
+    void zdone(int tensor, int kindFB, cudaStream_t s, int step_delta = 0) {
+        if (!zero || sizing) return;
+        const ZeroUse z = zuse(tensor, kindFB);
+        L("zero_done", 0, 0, s, [&] {
+            zero_done_kernel<<<1, 1, 0, s>>>(z, ring, tensor + 1, (const int *)&ctrl_dev.as<Control>()->step,
+                                             step_delta);
+            CDP_CUDA(cudaGetLastError());
+        });
+    }
+
     template <int K>
     void pull_tensor(int tensor, int p, cudaStream_t s) {
+        if (zero) {
+            zrecv<K>(tensor, 0, s);
+            return;
+        }
         if (rank == world - 1 || world == 1) return;
         const TensorSpec &ts = tens[tensor];
         const int vslot = vs(tensor, p);
@@ -852,14 +974,18 @@ struct ResNetTrainer {
         ConvL &c = convs[ci];
         wait(hs, dy_ready);
         bn_hop(ci, p, hs);
-        if (dgrad_done && !tens[c.tw].fresh && last_updater()) wait(hs, dgrad_done);
+        zdone(c.tb, 1, hs);
+        if (dgrad_done && (zero || (!tens[c.tw].fresh && last_updater()))) wait(hs, dgrad_done);
+        if (!dgrad_done) zrecv<K>(c.tw, 1, hs);  // the stem: its weight's only backward access is the hop
         conv_wgrad_hop<K>(ci, p, hs);
+        zdone(c.tw, 1, hs);
     }
 
     template <int K>
     void record_step(int p) {
         kernels_per_step = 0;
         flops_per_step = 0.0;
+        zero_bytes_per_step = 0;
         cudaEvent_t fork = ev(main);
         wait(cs, fork);
         wait(hs, fork);
@@ -888,16 +1014,18 @@ struct ResNetTrainer {
         cudaEvent_t dz_ready = ev(cs);
         typename EpiDgradLinear::Params dep{dpooled.as<float>(), fc_in};
         const int vfc = vs(fc_t, p);
+        zrecv<K>(fc_t, 1, cs);
         gemm<K, false, false, EpiDgradLinear>("fc_dgrad", 32, wc[vfc][fc_t].view(), dz.view(), fc_in, B, classes, dep,
                                               cs, false);
         cudaEvent_t fc_dgrad_done = ev(cs);
         wait(hs, dz_ready);
-        if (!tens[fc_t].fresh && last_updater()) wait(hs, fc_dgrad_done);
+        if (zero || (!tens[fc_t].fresh && last_updater())) wait(hs, fc_dgrad_done);
         {
             HopParams hp = hop_params(fc_t, p);
             hop_wait(hp, hs);
             gemm<K, true, true, EpiWgrad<K>>("fc_wgrad_hop", 64, pooled.view(), dz.view(), fc_in + 1, classes, B, hp,
                                              hs, true);
+            zdone(fc_t, 1, hs);
         }
         void *G0 = gbuf[0].p, *G1 = gbuf[1].p, *G2 = gbuf[2].p, *G3 = gbuf[3].p;
         // pool backward -> gradient w.r.t. the last activation (G0 holds the block-output gradient)
@@ -968,6 +1096,33 @@ struct ResNetTrainer {
             CDP_CUDA(cudaGetLastError());
         });
         (void)c0;
+    }
+
+    // ZeRO-CDP end of a run: a backward of the last step may follow (in the plan's use
+    // order) a forward of the NEXT step on another rank; publish those forward uses of
+    // step t (= the next, unlaunched step) after their own predecessors, without compute.
+    void zero_drain() {
+        if (!zero) return;
+        // stage the control block of step t (the next, unlaunched step) asynchronously: no host
+        // synchronisation here (other ranks' drains may be what this rank's last step waits for)
+        std::vector<int> ident(B, 0);
+        stage_control(ident.data(), 0.f);
+        for (size_t k = 0; k < tens.size(); ++k) {
+            const int tensor = int(k);
+            // only forwards some other rank's backward of the last step waits for (zero.py drain_units)
+            const int st = tens[k].stage - 1;
+            bool needed = false;
+            for (int j = 0; j < world; ++j) {
+                const int *e = &ztab[((size_t(st) * 2 + 1) * world + j) * 3];
+                needed |= (e[1] == rank && e[2] == 1);
+            }
+            if (!needed) continue;
+            if (kind == 0)
+                zrecv<0>(tensor, 0, main, 0, false);
+            else
+                zrecv<1>(tensor, 0, main, 0, false);
+            zdone(tensor, 0, main);
+        }
     }
 
     void capture() {
@@ -1109,7 +1264,8 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
                                       int stem_kind, int in_channels, int height, int width, int classes,
                                       int micro_batch, int world, int rank, const int32_t *tensor_stage,
                                       const uint8_t *stage_fresh, int dtype, float momentum, float weight_decay,
-                                      int n_samples, const float *x, const int32_t *labels, cdp_resnet **out) {
+                                      int n_samples, const float *x, const int32_t *labels,
+                                      const int32_t *zero_table, cdp_resnet **out) {
     return guarded([&] {
         CDP_REQUIRE(dtype == CDP_DTYPE_FP32 || dtype == CDP_DTYPE_BF16, "bad dtype");
         CDP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
@@ -1134,6 +1290,14 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
         tr->rank = rank;
         tr->world = world;
         tr->n_samples = std::max(n_samples, micro_batch);
+        if (zero_table && world > 1) {
+            tr->zero = true;
+            tr->ztab.assign(zero_table, zero_table + size_t(world) * 2 * world * 3);
+            for (int k = 0; k < world * 2 * world; ++k) {
+                CDP_REQUIRE(tr->ztab[k * 3 + 1] >= 0 && tr->ztab[k * 3 + 1] < world, "ZeRO table: bad source rank");
+                CDP_REQUIRE(tr->ztab[k * 3 + 2] >= -1 && tr->ztab[k * 3 + 2] <= 1, "ZeRO table: bad step offset");
+            }
+        }
         const int HWC = height * width * in_channels;
         tr->data_x = DevBuf(size_t(tr->n_samples) * HWC * 4);
         tr->data_lab = DevBuf(size_t(tr->n_samples) * 4);
@@ -1183,6 +1347,8 @@ extern "C" int cdp_resnet_connect(cdp_resnet *tr, void *const *regions) {
             m.prev_ring = reinterpret_cast<RingFlags *>(at(m.rank - 1));
             m.prev_partial = reinterpret_cast<float *>(at(m.rank - 1) + m.region_off) + 2 * m.Pp;
         }
+        m.peers.assign(size_t(m.world), nullptr);
+        for (int r = 0; r < m.world; ++r) m.peers[r] = at(r);
         const int u = m.world - 1;
         m.upd_ring = reinterpret_cast<RingFlags *>(at(u));
         m.upd_theta[0] = reinterpret_cast<float *>(at(u) + m.region_off);
@@ -1212,6 +1378,10 @@ extern "C" int cdp_resnet_step(cdp_resnet *tr, const int32_t *perm, float lr) {
 
 extern "C" int cdp_resnet_step_host_batch(cdp_resnet *tr, const float *x, const int32_t *labels, float lr) {
     return guarded([&] { tr->impl->step_host_batch(x, labels, lr); });
+}
+
+extern "C" int cdp_resnet_zero_drain(cdp_resnet *tr) {
+    return guarded([&] { tr->impl->zero_drain(); });
 }
 
 extern "C" int cdp_resnet_last_loss(cdp_resnet *tr, double *loss) {
@@ -1277,19 +1447,20 @@ extern "C" int cdp_resnet_ring_error(cdp_resnet *tr, int *err) {
 
 extern "C" int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out) {
     // [0] activation bytes (activations, conv outputs, dy, stem record), [1] parameter-state bytes,
-    // [2] kernels / step, [3] tensor-core flops / step, [4] fp32 gradient scratch bytes
+    // [2] kernels / step, [3] tensor-core flops / step, [4] gradient scratch bytes,
+    // [5] ZeRO-CDP state bytes received per step
     return guarded([&] {
         auto &m = *tr->impl;
         int64_t act = int64_t(m.cols.hi.bytes + m.cols.lo.bytes);
         for (auto &a : m.acts) act += int64_t(a.hi.bytes + a.lo.bytes);
         for (auto &c : m.convs) act += int64_t(c.y.bytes + c.dy.hi.bytes + c.dy.lo.bytes);
-        int64_t par = int64_t(m.Pp) * 12 + int64_t(m.vel.bytes);
+        int64_t par = int64_t(m.Pp) * (m.vel ? 16 : 12);
         for (int v = 0; v < 2; ++v)
             for (auto &w : m.wc[v]) par += int64_t(w.hi.bytes + w.lo.bytes);
         int64_t scratch = int64_t(m.dcols.bytes);
         for (auto &g : m.gbuf) scratch += int64_t(g.bytes);
-        int64_t vals[5] = {act, par, m.kernels_per_step, int64_t(m.flops_per_step), scratch};
-        for (int i = 0; i < n_out && i < 5; ++i) out[i] = vals[i];
+        int64_t vals[6] = {act, par, m.kernels_per_step, int64_t(m.flops_per_step), scratch, m.zero_bytes_per_step};
+        for (int i = 0; i < n_out && i < 6; ++i) out[i] = vals[i];
     });
 }
 

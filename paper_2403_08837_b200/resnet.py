@@ -162,7 +162,7 @@ class DeviceResNet:
 
     def __init__(self, widths=RESNET18["widths"], depths=RESNET18["depths"], micro_batch=128, world=1, rank=0,
                  rule=None, dtype="bf16", momentum=0.0, weight_decay=0.0, inputs=None, labels=None, classes=10,
-                 image_hw=32, stage_of_tensor=None, block="basic", stem="cifar"):
+                 image_hw=32, stage_of_tensor=None, block="basic", stem="cifar", zero=False):
         self.lib = N.lib()
         self.widths, self.depths = tuple(widths), tuple(depths)
         self.block, self.stem, self.classes, self.image_hw = block, stem, int(classes), int(image_hw)
@@ -186,12 +186,22 @@ class DeviceResNet:
             x = np.ascontiguousarray(inputs, dtype=np.float32)
             lab = np.ascontiguousarray(labels, dtype=np.int32)
             n = x.shape[0]
+        self.zero = bool(zero) and world > 1
+        ztab = None
+        if self.zero:
+            from .zero import zero_plan
+
+            if rule is None or any(rule.reads_fresh(i, j) != (j >= world - i + 1)
+                                   for i in range(1, world + 1) for j in range(1, world + 1)):
+                raise ValueError("ZeRO-CDP uses the CDP-v2 placement (ref schedule.py:471): rule must be cdp-v2")
+            ztab = zero_plan(world).table()
+        self._ztab = ztab
         h = ctypes.c_void_p()
         N.check(self.lib.cdp_resnet_create_rank(
             len(w), _i32p(w), _i32p(d), BLOCKS[block], STEMS[stem], 3, image_hw, image_hw, classes, self.micro_batch, world, rank,
             _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), DTYPES[dtype], float(momentum), float(weight_decay),
             n, x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
-            ctypes.byref(h)))
+            _i32p(ztab) if ztab is not None else None, ctypes.byref(h)))
         self.h = h
         self._keep = (x, lab)
         np_, nt = ctypes.c_int64(), ctypes.c_int()
@@ -285,6 +295,12 @@ class DeviceResNet:
         n = min(c.value, max_steps)
         return losses[:n].copy(), flags[:n].copy()
 
+    def zero_drain(self):
+        """ZeRO-CDP: publish the next step's forward uses (call on every rank before synchronising at the
+        end of a run; see include/cdp_b200.h)."""
+        if self.zero:
+            N.check(self.lib.cdp_resnet_zero_drain(self.h))
+
     def sync(self):
         N.check(self.lib.cdp_resnet_sync(self.h))
 
@@ -294,10 +310,11 @@ class DeviceResNet:
         return e.value
 
     def stats(self) -> dict:
-        out = np.zeros(5, dtype=np.int64)
-        N.check(self.lib.cdp_resnet_stats(self.h, out.ctypes.data_as(N.c_int64_p), 5))
+        out = np.zeros(6, dtype=np.int64)
+        N.check(self.lib.cdp_resnet_stats(self.h, out.ctypes.data_as(N.c_int64_p), 6))
         return {"activation_bytes": int(out[0]), "param_state_bytes": int(out[1]), "kernels_per_step": int(out[2]),
-                "tensor_flops_per_step": int(out[3]), "gradient_scratch_bytes": int(out[4])}
+                "tensor_flops_per_step": int(out[3]), "gradient_scratch_bytes": int(out[4]),
+                "zero_state_bytes_per_step": int(out[5])}
 
     def mark(self, k):
         N.check(self.lib.cdp_resnet_mark(self.h, k))

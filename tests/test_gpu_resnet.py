@@ -125,3 +125,48 @@ def test_profile_and_host_batch_steps(cuda):
     for loss, params in res[1:]:
         assert loss == res[0][0]
         assert np.array_equal(params, res[0][1])
+
+
+@pytest.mark.parametrize("world,arch", [(2, "basic"), (4, "basic"), (3, "bottleneck")])
+def test_zero_cdp_state_passing_bit_identical_to_cdp_v2(cuda, world, arch):
+    """ZeRO-CDP (parameter state handed holder -> next user by P2P copy, ref comm.py:93-144) computes exactly
+    what CDP-v2 with a full replica per rank computes; a mid-run drain + sync (end of a run, then
+    continuing) does not change the result."""
+    from oracle.resnet_torch import init_flat
+    from paper_2403_08837_b200.resnet import DeviceResNet
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    a = ARCH[arch]
+    rule = rule_by_name("cdp-v2", world)
+    x, y = _data(world * MB * 2, hw=a["hw"], classes=a["classes"])
+    init = init_flat(W, D, seed=0, block=a["block"], stem=a["stem"], classes=a["classes"])
+    steps = 5
+    perms = [np.random.default_rng([7, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
+    out = {}
+    for zero in (False, True):
+        tr = [DeviceResNet(W, D, MB, world, r, rule, "fp32", 0.9, inputs=x, labels=y, image_hw=a["hw"],
+                           block=a["block"], stem=a["stem"], classes=a["classes"], zero=zero) for r in range(world)]
+        regions = [t.region() for t in tr]
+        for t in tr:
+            t.set_params(init, -1)
+            t.connect(regions)
+        for k in range(steps):
+            for r, t in enumerate(tr):
+                t.step(perms[k][r * MB:(r + 1) * MB], 0.05)
+            if zero and k == 2:  # end-of-run drain in the middle, then continue
+                for t in tr:
+                    t.zero_drain()
+                for t in tr:
+                    t.sync()
+        for t in tr:
+            t.zero_drain()
+        for t in tr:
+            t.sync()
+            assert t.ring_error() == 0
+        out[zero] = (np.mean([t.history(steps)[0] for t in tr], axis=0), tr[-1].get_params(0),
+                     tr[0].stats()["zero_state_bytes_per_step"])
+        for t in tr:
+            t.close()
+    assert np.array_equal(out[True][0], out[False][0])
+    assert np.array_equal(out[True][1], out[False][1])
+    assert out[True][2] > 0 and out[False][2] == 0
