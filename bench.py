@@ -367,15 +367,18 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     from paper_2403_08837_b200.dist import exchange_handles, resolve
     from paper_2403_08837_b200.resnet import DeviceResNet, init_params, layer_specs, synthetic_images
 
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())  # (ranks may share a GPU in tests)
     cfg, hw, classes = resnet_cfg(model)
     B = RN_MB
-    rule = resolve(args.rule, ws)
+    allreduce = args.rule == "dp-allreduce"
+    rule = None if allreduce else resolve(args.rule, ws)
+    zero = bool(getattr(args, "zero", False)) and ws > 1
     n_data = 2 * B * ws
     x, y = synthetic_images(n_data, seed=0, hw=hw, classes=classes)
     specs = layer_specs(cfg["widths"], cfg["depths"], 3, hw, cfg["block"], cfg["stem"], classes)
     tr = DeviceResNet(cfg["widths"], cfg["depths"], B, ws, rank, rule, args.dtype, RN_MOMENTUM, inputs=x, labels=y,
-                      classes=classes, image_hw=hw, block=cfg["block"], stem=cfg["stem"])
+                      classes=classes, image_hw=hw, block=cfg["block"], stem=cfg["stem"], zero=zero,
+                      dp_allreduce=allreduce)
     tr.set_params(init_params(specs, seed=0), -1)
     if ws > 1:
         tr.connect_ipc(exchange_handles(tr.ipc_handle()))
@@ -383,18 +386,39 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
         tr.connect([tr.region()])
     perms = [np.random.default_rng([0, t]).permutation(n_data)[rank * B:(rank + 1) * B]
              for t in range(1, warmup + steps + 8)]
+    if allreduce:  # DP baseline: NCCL all-reduce of the flat gradient on the trainer stream, then the update
+        ext = torch.cuda.ExternalStream(tr.stream_handle())
+        grad = tr.partial_tensor()
+
+        def reduce_update():
+            if ws > 1:
+                with torch.cuda.stream(ext):
+                    torch.distributed.all_reduce(grad)
+            tr.apply_update()
+    else:
+        def reduce_update():
+            pass
+
+    def do_step(perm):
+        tr.step(perm, RN_LR)
+        reduce_update()
+
+    def settle():  # ZeRO-CDP: publish the next step's forwards other ranks' last step waits for
+        tr.zero_drain()
+        tr.sync()
+
     for t in range(warmup):
-        tr.step(perms[t], RN_LR)
-    tr.sync()
+        do_step(perms[t])
+    settle()
     if ws > 1:
         torch.distributed.barrier()
     with ClockSampler(local) as clk:
         for k in range(steps):
             tr.flush_l2()
             tr.mark(2 * k)
-            tr.step(perms[warmup + k], RN_LR)
+            do_step(perms[warmup + k])
             tr.mark(2 * k + 1)
-        tr.sync()
+        settle()
     if tr.ring_error():
         raise RuntimeError(f"rank {rank}: ring protocol timed out")
     ms = float(np.mean([tr.elapsed(2 * k, 2 * k + 1) for k in range(steps)]))
@@ -410,6 +434,7 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
            "activation_bytes": {"per_gpu": st["activation_bytes"], "sum_over_gpus": st["activation_bytes"] * ws},
            "param_state_bytes": st["param_state_bytes"], "gpu_launches": st["kernels_per_step"] * steps,
            "tensor_flops_per_step": st["tensor_flops_per_step"],
+           "zero_state_bytes_per_step": st["zero_state_bytes_per_step"],
            "tensor_tflops_per_s": round(st["tensor_flops_per_step"] / (ms / 1e3) / 1e12, 1)}
     # ---- e2e: public API, pinned host images copied H2D every step, loss read back every step
     if e2e:
@@ -425,6 +450,8 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
             tr.flush_l2()
             tr.mark(0)
             tr.step_host_batch_ptr(x_pin.data_ptr(), y_pin.data_ptr(), RN_LR)
+            reduce_update()
+            tr.zero_drain()
             loss = tr.last_loss()
             tr.mark(1)
             assert np.isfinite(loss)
@@ -439,7 +466,11 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
                       "h2d_bytes_per_step": B * hw * hw * 3 * 4 + B * 4 + 16 + B * 4, "d2h_bytes_per_step": 8,
                       "ms_per_step": round(e, 4)}
     # ---- per-kernel breakdown: one serialised instrumented (real) step
-    ops = tr.profile_step(perms[warmup + steps], RN_LR, serial=True)
+    if ws > 1:
+        torch.distributed.barrier()
+    ops = tr.profile_step(perms[warmup + steps], RN_LR, serial=ws == 1)
+    reduce_update()
+    settle()
     agg = kernel_table(ops)
     tot = sum(a[1] for a in agg.values())
     gemm = {k: a for k, a in agg.items() if a[2] > 0}
@@ -518,13 +549,21 @@ def main_resnet(args, ws, rank, local):
         "data": "synthetic (x ~ N(0,1) NHWC, uniform labels; numpy PCG64), deterministic He-normal init",
         "config": {"workload": resnet_workload(model, ws, args.rule, args.dtype), "baseline_config": peak_note,
                    "global_batch": ws * RN_MB, "micro_batch": RN_MB, "stages": ws, "rule": args.rule,
-                   "parallelism": f"cdp{ws} (one process per GPU, P2P gradient hop ring, fused update on rank {ws - 1})",
+                   "parallelism": (f"dp{ws} (NCCL all-reduce of the flat gradient + update kernel)"
+                                   if args.rule == "dp-allreduce" else
+                                   f"{'zero-' if args.zero and ws > 1 else ''}cdp{ws} (one process per GPU, P2P "
+                                   f"gradient hop ring, fused update on rank {ws - 1}"
+                                   f"{', ZeRO-CDP P2P state passing' if args.zero and ws > 1 else ''})"),
                    "l2": "flushed (256 MiB memset) before every timed step"},
         "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "roofline": res["roofline"],
         "activation_bytes": res["activation_bytes"], "tensor_tflops_per_s": res["tensor_tflops_per_s"],
         "clocks": res["clocks"], "kernel_breakdown": res["kernel_breakdown"],
         "serial_step_ms": res["serial_step_ms"], "losses_first_last": res["losses_first_last"],
     }
+    if args.zero and ws > 1:
+        out["zero_cdp"] = {"state_bytes_received_per_step_rank0": res["zero_state_bytes_per_step"],
+                           "what": "both theta version slots + momentum of every received tensor use (P2P copy "
+                                   "kernels, ref comm.py:93-144 holder chain)"}
     return out
 
 
@@ -573,12 +612,13 @@ def main():
     ap.add_argument("--model", default="resnet18", choices=["resnet18", "resnet50", "mlp"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the resnet50 / config-1 sub-lines at N=1")
+    ap.add_argument("--zero", action="store_true", help="ZeRO-CDP state passing (ResNets, N > 1)")
     args = ap.parse_args()
     ws, rank, local = dist_env()
 
     if args.model != "mlp":
-        if args.rule == "dp-allreduce":
-            raise SystemExit("--rule dp-allreduce is built for --model mlp only")
+        if args.zero and args.rule != "cdp-v2":
+            raise SystemExit("--zero uses the CDP-v2 placement (ref schedule.py:471)")
         if args.impl == "reference":
             if rank != 0:
                 return
@@ -587,7 +627,8 @@ def main():
             threads = os.cpu_count() or 1
             n = max(1, min(args.steps, 2))
             sample = 16 if args.model == "resnet18" else 2
-            sps, ms = cpu_resnet_reference(args.model, ws, resolve(args.rule, ws), sample, n, threads)
+            sps, ms = cpu_resnet_reference(args.model, ws, None if args.rule == "dp-allreduce" else resolve(args.rule, ws),
+                                           sample, n, threads)
             desc = (f"{n} steps (after 1 warm-up) of the {ws}-micro-batch CDP step on {sample} images per "
                     f"micro-batch (of {RN_MB}), float64 torch-CPU oracle port, {threads} threads")
             print(json.dumps({
@@ -603,8 +644,8 @@ def main():
         if ws > 1:
             import torch
 
-            torch.cuda.set_device(local)
-            torch.distributed.init_process_group("nccl")
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            torch.distributed.init_process_group("nccl" if torch.cuda.device_count() >= ws else "gloo")
         out = main_resnet(args, ws, rank, local)
         if rank == 0:
             if ws == 1 and not args.no_extras:

@@ -162,7 +162,13 @@ int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const int32_t *d
                            int in_channels, int height, int width, int classes, int micro_batch, int world, int rank,
                            const int32_t *tensor_stage, const uint8_t *stage_fresh, int dtype, float momentum,
                            float weight_decay, int n_samples, const float *x, const int32_t *labels,
-                           const int32_t *zero_table, cdp_resnet **out);
+                           const int32_t *zero_table, int options, cdp_resnet **out);
+/* options bit 0: DP all-reduce baseline (ref comm.py:70-90): the weight-gradient epilogues write this
+ * rank's gradient into the flat buffer (cdp_resnet_partial); the caller sums it across ranks on the
+ * trainer stream (cdp_resnet_stream, e.g. ncclAllReduce) and calls cdp_resnet_apply_update. */
+int cdp_resnet_apply_update(cdp_resnet *tr);
+int cdp_resnet_partial(cdp_resnet *tr, void **ptr, size_t *n);
+int cdp_resnet_stream(cdp_resnet *tr, void **stream);
 /* zero_table != NULL (world > 1): ZeRO-CDP state passing (ref comm.py:93-144), [world stages][2 (F, B)]
  * [world ranks][3] = (use-index base, predecessor rank, predecessor step offset) from zero.py; every
  * use of a parameter tensor copies the tensor's state (both theta slots + momentum) from its

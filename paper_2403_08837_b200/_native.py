@@ -64,8 +64,11 @@ SIGNATURES = {
     "cdp_trainer_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_resnet_create_rank": (c_int, [c_int, c_int_p, c_int_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                        c_int, c_int, c_int_p, c_u8_p, c_int, c_float, c_float, c_int, c_float_p,
-                                       c_int_p, c_int_p, ctypes.POINTER(c_void_p)]),
+                                       c_int_p, c_int_p, c_int, ctypes.POINTER(c_void_p)]),
     "cdp_resnet_zero_drain": (c_int, [c_void_p]),
+    "cdp_resnet_apply_update": (c_int, [c_void_p]),
+    "cdp_resnet_partial": (c_int, [c_void_p, ctypes.POINTER(c_void_p), ctypes.POINTER(ctypes.c_size_t)]),
+    "cdp_resnet_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_resnet_step_host_batch": (c_int, [c_void_p, c_float_p, c_int_p, c_float]),
     "cdp_resnet_last_loss": (c_int, [c_void_p, c_double_p]),
     "cdp_resnet_profile_step": (c_int, [c_void_p, c_int_p, c_float, c_int, c_int, ctypes.c_char_p, c_int, c_double_p,

@@ -842,6 +842,27 @@ struct EpiDgradLinear {
     __device__ static void post(const Params &, int, unsigned) {}
 };
 
+// DP all-reduce baseline: update of one parameter tensor from the collective-summed
+// gradient (p.s_in), the reference's update arithmetic (engine.py:102-109) in fp32,
+// repacking the GEMM compute copy ([rows][ld], `cols` per row) when the tensor has one.
+template <int KIND>
+__global__ void update_flat_kernel(HopParams p, int64_t n, int cols) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const float lr = *p.lr;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t idx = p.base + i;
+        float v = p.momentum != 0.f ? p.vel[idx] : 0.f;
+        const float nt = sgd_update(p, p.s_in[idx], p.theta_cur[idx], v, lr);
+        if (p.momentum != 0.f) p.vel[idx] = v;
+        if (!isfinite(nt)) bad = true;
+        p.theta_new[idx] = nt;
+        if (p.wc_new.hi) Fmt<KIND>::store(p.wc_new.hi, p.wc_new.lo, size_t(i / cols) * p.wc_new.ld + i % cols, nt);
+    }
+    if (bad) atomicOr(p.upd_flags, 1u << ((p.stage - 1) & 31));
+}
+
 // The pre-hop waits of a weight hop (EpiWgrad::pre) in a one-CTA kernel ahead
 // of the GEMM, so that a GEMM grid never occupies SMs while it waits for a peer
 // (no dependent launch is triggered before the waits are over).

@@ -216,6 +216,7 @@ struct ResNetTrainer {
     size_t ws_c_floats = 0, ws_h_floats = 0;
     DevBuf data_x, data_lab, ctrl_dev, perm_dev, flags_dev, hist_loss, hist_flags;
     int n_samples = 0;
+    bool allreduce = false;  // DP all-reduce baseline: gradients only, NCCL sum + apply_update on the host side
     // ZeRO-CDP: per (stage, kind F/B, rank) use table from zero.py; peers' shared regions
     bool zero = false;
     std::vector<int> ztab;  // [stages][2][world][3] = (base, src rank, dstep)
@@ -848,7 +849,43 @@ struct ResNetTrainer {
         hp.sync.prev = prev_ring;
         hp.sync.cta_counter = cta_counters.as<unsigned>();
         hp.sync.pre_external = 1;
+        if (allreduce) {  // gradient of this rank's micro-batch only, into the flat buffer
+            hp.mode = 4;
+            hp.s_out = partial;
+            hp.sync.enabled = 0;
+        }
         return hp;
+    }
+
+    // DP all-reduce baseline: the update of the step just run from the summed flat gradient.
+    void apply_update() {
+        CDP_REQUIRE(allreduce, "apply_update is the DP all-reduce baseline's update");
+        CDP_REQUIRE(t >= 2, "no step has run");
+        const int p = (t - 1) & 1;
+        Flags *fl = flags_dev.as<Flags>();
+        for (size_t k = 0; k < tens.size(); ++k) {
+            const TensorSpec &ts = tens[k];
+            HopParams hp{};
+            hp.mode = 3;
+            hp.stage = int(k) + 1;
+            hp.base = ts.base;
+            hp.s_in = partial;
+            hp.theta_cur = theta[p];
+            hp.theta_new = theta[p ^ 1];
+            hp.vel = vel;
+            hp.lr = &ctrl_dev.as<Control>()->lr;
+            hp.momentum = momentum;
+            hp.wd = wd;
+            hp.n_mb = float(world);
+            hp.wc_new = ts.kind == T_BN ? CTensor{} : wc[p ^ 1][k].view();
+            hp.upd_flags = &fl->upd;
+            if (kind == 0)
+                launch_pdl(update_flat_kernel<0>, dim3(blocks_for(ts.n)), dim3(256), 0, main, hp, ts.n,
+                           std::max(ts.cols, 1));
+            else
+                launch_pdl(update_flat_kernel<1>, dim3(blocks_for(ts.n)), dim3(256), 0, main, hp, ts.n,
+                           std::max(ts.cols, 1));
+        }
     }
 
     // Ring waits of a hop (multi-GPU) ahead of its kernel on the hop stream.
@@ -948,7 +985,7 @@ struct ResNetTrainer {
             zrecv<K>(tensor, 0, s);
             return;
         }
-        if (rank == world - 1 || world == 1) return;
+        if (rank == world - 1 || world == 1 || allreduce) return;
         const TensorSpec &ts = tens[tensor];
         const int vslot = vs(tensor, p);
         if (sizing) return;
@@ -1265,7 +1302,7 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
                                       int micro_batch, int world, int rank, const int32_t *tensor_stage,
                                       const uint8_t *stage_fresh, int dtype, float momentum, float weight_decay,
                                       int n_samples, const float *x, const int32_t *labels,
-                                      const int32_t *zero_table, cdp_resnet **out) {
+                                      const int32_t *zero_table, int options, cdp_resnet **out) {
     return guarded([&] {
         CDP_REQUIRE(dtype == CDP_DTYPE_FP32 || dtype == CDP_DTYPE_BF16, "bad dtype");
         CDP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
@@ -1290,6 +1327,8 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
         tr->rank = rank;
         tr->world = world;
         tr->n_samples = std::max(n_samples, micro_batch);
+        tr->allreduce = (options & 1) != 0;
+        CDP_REQUIRE(!(tr->allreduce && zero_table), "the DP all-reduce baseline and ZeRO-CDP are exclusive");
         if (zero_table && world > 1) {
             tr->zero = true;
             tr->ztab.assign(zero_table, zero_table + size_t(world) * 2 * world * 3);
@@ -1378,6 +1417,21 @@ extern "C" int cdp_resnet_step(cdp_resnet *tr, const int32_t *perm, float lr) {
 
 extern "C" int cdp_resnet_step_host_batch(cdp_resnet *tr, const float *x, const int32_t *labels, float lr) {
     return guarded([&] { tr->impl->step_host_batch(x, labels, lr); });
+}
+
+extern "C" int cdp_resnet_apply_update(cdp_resnet *tr) {
+    return guarded([&] { tr->impl->apply_update(); });
+}
+
+extern "C" int cdp_resnet_partial(cdp_resnet *tr, void **ptr, size_t *n) {
+    return guarded([&] {
+        *ptr = tr->impl->partial;
+        *n = size_t(tr->impl->P);
+    });
+}
+
+extern "C" int cdp_resnet_stream(cdp_resnet *tr, void **stream) {
+    return guarded([&] { *stream = tr->impl->main; });
 }
 
 extern "C" int cdp_resnet_zero_drain(cdp_resnet *tr) {

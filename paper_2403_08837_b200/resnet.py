@@ -162,7 +162,7 @@ class DeviceResNet:
 
     def __init__(self, widths=RESNET18["widths"], depths=RESNET18["depths"], micro_batch=128, world=1, rank=0,
                  rule=None, dtype="bf16", momentum=0.0, weight_decay=0.0, inputs=None, labels=None, classes=10,
-                 image_hw=32, stage_of_tensor=None, block="basic", stem="cifar", zero=False):
+                 image_hw=32, stage_of_tensor=None, block="basic", stem="cifar", zero=False, dp_allreduce=False):
         self.lib = N.lib()
         self.widths, self.depths = tuple(widths), tuple(depths)
         self.block, self.stem, self.classes, self.image_hw = block, stem, int(classes), int(image_hw)
@@ -201,7 +201,8 @@ class DeviceResNet:
             len(w), _i32p(w), _i32p(d), BLOCKS[block], STEMS[stem], 3, image_hw, image_hw, classes, self.micro_batch, world, rank,
             _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), DTYPES[dtype], float(momentum), float(weight_decay),
             n, x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
-            _i32p(ztab) if ztab is not None else None, ctypes.byref(h)))
+            _i32p(ztab) if ztab is not None else None, 1 if dp_allreduce else 0, ctypes.byref(h)))
+        self.dp_allreduce = bool(dp_allreduce)
         self.h = h
         self._keep = (x, lab)
         np_, nt = ctypes.c_int64(), ctypes.c_int()
@@ -294,6 +295,28 @@ class DeviceResNet:
                                             flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), ctypes.byref(c)))
         n = min(c.value, max_steps)
         return losses[:n].copy(), flags[:n].copy()
+
+    # ---- DP all-reduce baseline (ref comm.py:70-90)
+    def partial_tensor(self):
+        """torch view (no copy) of the flat gradient buffer, summed across ranks by the caller."""
+        import torch
+
+        ptr, n = ctypes.c_void_p(), ctypes.c_size_t()
+        N.check(self.lib.cdp_resnet_partial(self.h, ctypes.byref(ptr), ctypes.byref(n)))
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n.value,), "typestr": "<f4", "data": (ptr.value, False),
+                                        "version": 3}
+
+        return torch.as_tensor(_View(), device="cuda")
+
+    def stream_handle(self) -> int:
+        s = ctypes.c_void_p()
+        N.check(self.lib.cdp_resnet_stream(self.h, ctypes.byref(s)))
+        return s.value or 0
+
+    def apply_update(self):
+        N.check(self.lib.cdp_resnet_apply_update(self.h))
 
     def zero_drain(self):
         """ZeRO-CDP: publish the next step's forward uses (call on every rank before synchronising at the

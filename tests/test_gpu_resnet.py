@@ -170,3 +170,45 @@ def test_zero_cdp_state_passing_bit_identical_to_cdp_v2(cuda, world, arch):
     assert np.array_equal(out[True][0], out[False][0])
     assert np.array_equal(out[True][1], out[False][1])
     assert out[True][2] > 0 and out[False][2] == 0
+
+
+def test_dp_allreduce_baseline_bit_identical_to_dp_ring(cuda):
+    """DP all-reduce baseline (gradient epilogues + a summed flat buffer + apply_update) == the DP step with
+    the ring hop and fused update (same fp32 summation order g0 + g1)."""
+    import torch
+
+    from oracle.resnet_torch import init_flat
+    from paper_2403_08837_b200.resnet import DeviceResNet
+
+    world, steps = 2, 3
+    x, y = _data(world * MB * 2)
+    init = init_flat(W, D, seed=0)
+    perms = [np.random.default_rng([9, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
+    out = {}
+    for ar in (False, True):
+        tr = [DeviceResNet(W, D, MB, world, r, None, "fp32", 0.9, inputs=x, labels=y, image_hw=HW, dp_allreduce=ar)
+              for r in range(world)]
+        regions = [t.region() for t in tr]
+        for t in tr:
+            t.set_params(init, -1)
+            t.connect(regions)
+        for k in range(steps):
+            for r, t in enumerate(tr):
+                t.step(perms[k][r * MB:(r + 1) * MB], 0.05)
+            if ar:
+                for t in tr:
+                    t.sync()
+                g = [t.partial_tensor() for t in tr]
+                total = g[0] + g[1]
+                for gi in g:
+                    gi.copy_(total)
+                torch.cuda.synchronize()
+                for t in tr:
+                    t.apply_update()
+        for t in tr:
+            t.sync()
+        out[ar] = [t.get_params(0) for t in tr]
+        for t in tr:
+            t.close()
+    assert np.array_equal(out[True][0], out[True][1])
+    assert np.array_equal(out[True][1], out[False][1])
