@@ -223,9 +223,92 @@ struct EpiConvOut2 {
         int tiles;
         const void *add;     // Y-format [rows][ld] added to the output (residual gradient), or null
         CTensor add_mask;    // add masked by (add_mask > 0) when add_mask.hi
+        // fused BN-backward statistics of the BN this gradient feeds (persistent, non-split only):
+        // g' = out * (bn_mask > 0); bstats[C][CTA][3] += (sum g', sum g' xhat, sum g' xhat2)
+        float *bstats;
+        CTensor bn_mask;
+        const void *bn_y, *bn_y2;            // conv outputs (Y format) of the BN (and projection BN)
+        const float *bn_mean, *bn_rstd, *bn_mean2, *bn_rstd2;
     };
     static constexpr int kStages = 0;
-    static constexpr bool kColStats = true;  // the persistent kernel reduces columns during the drain
+    // Split-K units cannot fuse the backward statistics (partials): the caller falls back.
+    static Params for_split(const Params &p) {
+        Params q = p;
+        q.bstats = nullptr;
+        return q;
+    }
+
+    // Drain hook (per warp, lane = tile row, v = 32 consecutive columns from TMEM).
+    __device__ static void drain(const Params &p, bool split, int m, int col, float (&v)[32], float *srow,
+                                 float *pp) {
+        const bool fwd = p.stats && !split;
+        const bool bwd = p.bstats && !split;
+        if (bwd && p.add && m >= 0) {  // the residual branch is folded here (run() skips it)
+            const size_t o = size_t(m) * p.ld + col;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                F8 a = ld_y8<KIND>(p.add, o + 8 * k);
+                if (p.add_mask.hi) {
+                    const F8 mk = ld_c8<KIND>(p.add_mask, o + 8 * k);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) a.v[i] = mk.v[i] > 0.f ? a.v[i] : 0.f;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[8 * k + i] += a.v[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4 *>(srow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        if (fwd) {
+            float sq[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                v[i] = m >= 0 ? v[i] : 0.f;
+                sq[i] = v[i] * v[i];
+            }
+            pp[1] = warp_colsum32(sq);
+            pp[0] = warp_colsum32(v);
+        } else if (bwd) {
+            float t[32];
+            if (m >= 0) {
+                const size_t o = size_t(m) * p.ld + col;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const F8 mk = ld_c8<KIND>(p.bn_mask, o + 8 * k);
+                    const F8 y = ld_y8<KIND>(p.bn_y, o + 8 * k);
+                    const F8 mu = ld_f8(p.bn_mean, col + 8 * k), rs = ld_f8(p.bn_rstd, col + 8 * k);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float g = mk.v[i] > 0.f ? v[8 * k + i] : 0.f;
+                        v[8 * k + i] = g;
+                        t[8 * k + i] = g * ((y.v[i] - mu.v[i]) * rs.v[i]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = t[i] = 0.f;
+            }
+            pp[1] = warp_colsum32(t);
+            if (p.bn_y2) {
+                if (m >= 0) {
+                    const size_t o = size_t(m) * p.ld + col;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const F8 y = ld_y8<KIND>(p.bn_y2, o + 8 * k);
+                        const F8 mu = ld_f8(p.bn_mean2, col + 8 * k), rs = ld_f8(p.bn_rstd2, col + 8 * k);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) t[8 * k + i] = v[8 * k + i] * ((y.v[i] - mu.v[i]) * rs.v[i]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) t[i] = 0.f;
+                }
+                pp[2] = warp_colsum32(t);
+            }
+            pp[0] = warp_colsum32(v);
+        }
+    }
     // Stores (8 columns per element: 16-byte bf16 / 2 x 16-byte fp32 stores).
     template <int NTH>
     __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
@@ -246,7 +329,7 @@ struct EpiConvOut2 {
                 v[u][0] = *reinterpret_cast<const float4 *>(st + r * lds + c);
                 v[u][1] = *reinterpret_cast<const float4 *>(st + r * lds + c + 4);
                 o[u] = size_t(rowm[r]) * p.ld + col0 + c;
-                if (p.add) {
+                if (p.add && !p.bstats) {
                     a[u][0] = ld_y4<KIND>(p.add, o[u]);
                     a[u][1] = ld_y4<KIND>(p.add, o[u] + 4);
                     if (p.add_mask.hi) {
@@ -260,7 +343,7 @@ struct EpiConvOut2 {
                 if (!ok[u]) continue;
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
-                    if (p.add) {
+                    if (p.add && !p.bstats) {
                         const float4 b = p.add_mask.hi ? relu_mask4(a[u][k], mk[u][k]) : a[u][k];
                         v[u][k].x += b.x;
                         v[u][k].y += b.y;
@@ -292,24 +375,46 @@ struct EpiConvOut2 {
     // Column a is always handled by epilogue thread a % pcols (program order, no race).
     template <int NTH>
     __device__ static void col_stats_init(const Params &p, int N, int pcols, int tid) {
-        if (!p.stats || tid >= pcols) return;
-        for (int a = tid; a < N; a += pcols)
-            *reinterpret_cast<float2 *>(p.stats + (size_t(a) * gridDim.x + blockIdx.x) * 2) = make_float2(0.f, 0.f);
+        if (tid >= pcols) return;
+        if (p.stats)
+            for (int a = tid; a < N; a += pcols)
+                *reinterpret_cast<float2 *>(p.stats + (size_t(a) * gridDim.x + blockIdx.x) * 2) = make_float2(0.f, 0.f);
+        if (p.bstats)
+            for (int a = tid; a < N; a += pcols) {
+                float *o = p.bstats + (size_t(a) * gridDim.x + blockIdx.x) * 3;
+                o[0] = o[1] = o[2] = 0.f;
+            }
     }
     template <int NTH>
     __device__ static void col_stats(const Params &p, const float *part, int pcols, int col0, int ncols, int tm,
                                      int tid) {
-        if (!p.stats) return;
-        for (int c = tid; c < ncols; c += NTH) {
-            float s = 0.f, q = 0.f;
+        if (p.stats) {
+            for (int c = tid; c < ncols; c += NTH) {
+                float s = 0.f, q = 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                s += part[(k * pcols + c) * 2];
-                q += part[(k * pcols + c) * 2 + 1];
+                for (int k = 0; k < 4; ++k) {
+                    s += part[(k * pcols + c) * 3];
+                    q += part[(k * pcols + c) * 3 + 1];
+                }
+                float2 *o = reinterpret_cast<float2 *>(p.stats + (size_t(col0 + c) * gridDim.x + blockIdx.x) * 2);
+                const float2 cur = *o;
+                *o = make_float2(cur.x + s, cur.y + q);
             }
-            float2 *o = reinterpret_cast<float2 *>(p.stats + (size_t(col0 + c) * gridDim.x + blockIdx.x) * 2);
-            const float2 cur = *o;
-            *o = make_float2(cur.x + s, cur.y + q);
+        }
+        if (p.bstats) {
+            for (int c = tid; c < ncols; c += NTH) {
+                float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    s0 += part[(k * pcols + c) * 3];
+                    s1 += part[(k * pcols + c) * 3 + 1];
+                    if (p.bn_y2) s2 += part[(k * pcols + c) * 3 + 2];
+                }
+                float *o = p.bstats + (size_t(col0 + c) * gridDim.x + blockIdx.x) * 3;
+                o[0] += s0;
+                o[1] += s1;
+                o[2] += s2;
+            }
         }
     }
     // Split-K reduce kernel: the whole 128-row tile is in `st` (rows in order).
@@ -342,7 +447,12 @@ template <int KIND>
 struct EpiHop2 {
     using Params = HopParams;
     static constexpr int kStages = 0;
-    static constexpr bool kColStats = false;
+    static Params for_split(const Params &p) { return p; }
+    __device__ static void drain(const Params &, bool, int, int, float (&v)[32], float *srow, float *) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4 *>(srow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    }
     template <int NTH>
     __device__ static void col_stats(const Params &, const float *, int, int, int, int, int) {}
     template <int NTH>
@@ -598,6 +708,39 @@ __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__restric
                 o2[0] = s0;
                 o2[1] = s2;
             }
+        }
+    }
+}
+
+// Backward finalise of the statistics fused into the data-gradient GEMM epilogue:
+// per channel the per-CTA (sum g', sum g' xhat, sum g' xhat2) [C][CTAs][3] in CTA order
+// (fp64) -> dbeta, dgamma (and dgamma2 of the projection BN, which shares dbeta).
+__global__ void bn_finalize_bwd_cta_kernel(const float *__restrict__ part, int nct, int C, float *dbeta,
+                                           float *dgamma, float *dbeta2, float *dgamma2) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= C) return;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const float *pc = part + size_t(c) * nct * 3;
+    for (int t = lane; t < nct; t += 32) {
+        s0 += double(pc[t * 3]);
+        s1 += double(pc[t * 3 + 1]);
+        s2 += double(pc[t * 3 + 2]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+        dbeta[c] = float(s0);
+        dgamma[c] = float(s1);
+        if (dbeta2) {
+            dbeta2[c] = float(s0);
+            dgamma2[c] = float(s2);
         }
     }
 }

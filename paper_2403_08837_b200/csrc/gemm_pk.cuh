@@ -46,7 +46,7 @@ struct PkCfg {
     static constexpr int EPI_COLS = BN < 128 ? BN : 128;  // columns staged per epilogue pass
     static constexpr int LDS = EPI_COLS + 4;
     static constexpr int STILE_BYTES = 128 * LDS * 4;
-    static constexpr int PART_BYTES = 4 * EPI_COLS * 2 * 4;  // per TMEM quarter column (sum, sum sq)
+    static constexpr int PART_BYTES = 4 * EPI_COLS * 3 * 4;  // per TMEM quarter column: up to 3 statistics
     static constexpr int BUDGET = 220 * 1024 - STILE_BYTES - PART_BYTES - 2048;
     static constexpr int STAGES = ST ? ST : (BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES);
     static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         const int half = (warp - 4) >> 2;   // column half of each staging pass
         const int row = q * 32 + ptx::lane_id();
         constexpr int HC = C::EPI_COLS / 2;
-        if (Epi::kColStats && args.splits == 1) {
+        if (args.splits == 1) {
             Epi::template col_stats_init<kPkEpi>(ep, args.N, C::EPI_COLS, tid);
             pk_bar(1, kPkEpi);
         }
@@ -211,29 +211,15 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
             for (int h = 0; h < BN / C::EPI_COLS; ++h) {
-                const bool row_ok = pk_row_m(args, tm, row) >= 0;  // own computation: rowm is not yet synced
+                const int row_m = pk_row_m(args, tm, row);  // own computation: rowm is not yet synced
 #pragma unroll 1
                 for (int c = half * HC; c < (half + 1) * HC; c += 32) {
                     float v[32];
                     ptx::tmem_ld32(taddr + h * C::EPI_COLS + c, v);
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4)
-                        *reinterpret_cast<float4 *>(stile + row * C::LDS + c + i) =
-                            make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                    if (Epi::kColStats && !split) {
-                        // per-quarter column (sum, sum sq) over the valid rows -> spart[q][c][2]
-                        float sq[32];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            v[i] = row_ok ? v[i] : 0.f;
-                            sq[i] = v[i] * v[i];
-                        }
-                        const float cs = warp_colsum32(v);
-                        const float cq = warp_colsum32(sq);
-                        float *pp = spart + (q * C::EPI_COLS + c + ptx::lane_id()) * 2;
-                        pp[0] = cs;
-                        pp[1] = cq;
-                    }
+                    // epilogue drain hook (whole warp, lockstep): may fold extra operands into the
+                    // row and reduce per-column statistics into spart[q][c + lane][0..2]
+                    Epi::drain(ep, split, row_m, tn * BN + h * C::EPI_COLS + c, v, stile + row * C::LDS + c,
+                               spart + (q * C::EPI_COLS + c + ptx::lane_id()) * 3);
                 }
                 if (h == BN / C::EPI_COLS - 1) ptx::tc_fence_before();
                 pk_bar(1, kPkEpi);
@@ -251,9 +237,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 } else {
                     Epi::template run<kPkEpi>(ep, stile, C::LDS, rowm, 128, col0, min(C::EPI_COLS, args.N - col0), tm,
                                               args.N, tid);
-                    if (Epi::kColStats)
-                        Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0),
-                                                        tm, tid);
+                    Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), tm,
+                                                    tid);
                 }
                 pk_bar(1, kPkEpi);  // shared tile reused by the next pass / unit
             }
