@@ -203,6 +203,38 @@ int cdp_resnet_mark(cdp_resnet *tr, int k);
 int cdp_resnet_elapsed(cdp_resnet *tr, int a, int b, float *ms);
 int cdp_resnet_flush_l2(cdp_resnet *tr);
 
+/* ---- Vision Transformers (BASELINE configs[3]: ViT-B/16, 224x224), bf16 operands ------------ */
+/* One worker per process, same ring / hop / pull protocol as the ResNet trainer.  Model:
+ * conv patch embedding (kernel = stride = patch), class token, position embedding, `depth`
+ * pre-LN blocks (LN eps 1e-6, fused qkv attention with head dim 64, GELU MLP), final LN, head
+ * on the class token.  Hop units in order: patch [[W^T]; b] ([patch*patch*3 + 1][dim]), cls [dim],
+ * pos [tokens][dim], per block ln1 [g | b], qkv [[W^T]; b] ([dim+1][3 dim]), proj, ln2, fc1
+ * ([dim+1][mlp]), fc2 ([mlp+1][dim]), final ln, head ([dim+1][classes]); unit_stage[i] groups them
+ * into world stages.  Dataset: x fp32 NHWC [n][image][image][3], labels int32. */
+typedef struct cdp_vit cdp_vit;
+int cdp_vit_create_rank(int image, int patch, int dim, int depth, int heads, int mlp, int classes, int micro_batch,
+                        int world, int rank, const int32_t *unit_stage, const uint8_t *stage_fresh, float momentum,
+                        float weight_decay, int n_samples, const float *x, const int32_t *labels, cdp_vit **out);
+int cdp_vit_info(cdp_vit *tr, int64_t *n_params, int *n_units);
+int cdp_vit_region(cdp_vit *tr, void **base);
+int cdp_vit_ipc_handle(cdp_vit *tr, void *handle64);
+int cdp_vit_connect(cdp_vit *tr, void *const *regions);
+void cdp_vit_destroy(cdp_vit *tr);
+int cdp_vit_set_params(cdp_vit *tr, int which, const float *theta);
+int cdp_vit_get_params(cdp_vit *tr, int which, float *theta);
+int cdp_vit_step(cdp_vit *tr, const int32_t *perm, float lr);
+int cdp_vit_step_host_batch(cdp_vit *tr, const float *x, const int32_t *labels, float lr);
+int cdp_vit_profile_step(cdp_vit *tr, const int32_t *perm, float lr, int serial, int max_ops, char *names,
+                         int name_len, double *flops, double *bytes, float *ms, int *n_ops);
+int cdp_vit_history(cdp_vit *tr, int max, double *losses, uint32_t *flags, int *count);
+int cdp_vit_sync(cdp_vit *tr);
+int cdp_vit_ring_error(cdp_vit *tr, int *err);
+/* out[0..3] = activation bytes kept for the backward, parameter-state bytes, kernels per step, tensor flops. */
+int cdp_vit_stats(cdp_vit *tr, int64_t *out, int n_out);
+int cdp_vit_mark(cdp_vit *tr, int k);
+int cdp_vit_elapsed(cdp_vit *tr, int a, int b, float *ms);
+int cdp_vit_flush_l2(cdp_vit *tr);
+
 /* ---- tensor-core GEMM self-test (parity tests of the tcgen05 kernel) --- */
 /* D[m][n] = sum_s A_s . B_s.  kind 0 = bf16, 1 = fp32/tf32.  A K-major:
  * A[m*lda+k], MN-major: A[k*lda+m]; B K-major: B[n*ldb+k], MN-major:

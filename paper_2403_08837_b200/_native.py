@@ -88,6 +88,26 @@ SIGNATURES = {
     "cdp_resnet_mark": (c_int, [c_void_p, c_int]),
     "cdp_resnet_elapsed": (c_int, [c_void_p, c_int, c_int, c_float_p]),
     "cdp_resnet_flush_l2": (c_int, [c_void_p]),
+    "cdp_vit_create_rank": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int_p,
+                                    c_u8_p, c_float, c_float, c_int, c_float_p, c_int_p, ctypes.POINTER(c_void_p)]),
+    "cdp_vit_info": (c_int, [c_void_p, c_int64_p, c_int_p]),
+    "cdp_vit_region": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "cdp_vit_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "cdp_vit_connect": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    "cdp_vit_destroy": (None, [c_void_p]),
+    "cdp_vit_set_params": (c_int, [c_void_p, c_int, c_float_p]),
+    "cdp_vit_get_params": (c_int, [c_void_p, c_int, c_float_p]),
+    "cdp_vit_step": (c_int, [c_void_p, c_int_p, c_float]),
+    "cdp_vit_step_host_batch": (c_int, [c_void_p, c_float_p, c_int_p, c_float]),
+    "cdp_vit_profile_step": (c_int, [c_void_p, c_int_p, c_float, c_int, c_int, ctypes.c_char_p, c_int, c_double_p,
+                                     c_double_p, c_float_p, c_int_p]),
+    "cdp_vit_history": (c_int, [c_void_p, c_int, c_double_p, ctypes.POINTER(ctypes.c_uint32), c_int_p]),
+    "cdp_vit_sync": (c_int, [c_void_p]),
+    "cdp_vit_ring_error": (c_int, [c_void_p, c_int_p]),
+    "cdp_vit_stats": (c_int, [c_void_p, c_int64_p, c_int]),
+    "cdp_vit_mark": (c_int, [c_void_p, c_int]),
+    "cdp_vit_elapsed": (c_int, [c_void_p, c_int, c_int, c_float_p]),
+    "cdp_vit_flush_l2": (c_int, [c_void_p]),
     "cdp_test_gemm": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p), c_int,
                               ctypes.POINTER(c_void_p), c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
 }

@@ -129,7 +129,7 @@ __device__ __forceinline__ void st_c8(const CTensor &t, size_t i, const F8 &a) {
 // and zero columns K..ld-1.  The cols matrix is the stem's activation record.
 // One thread per (pixel, 8 consecutive k): 16-byte (bf16) stores.
 template <int KIND, int R, int C>
-__global__ void stem_im2col_kernel(const float *__restrict__ data, const int *perm, int H, int W, int stride, int pad,
+static __global__ void stem_im2col_kernel(const float *__restrict__ data, const int *perm, int H, int W, int stride, int pad,
                                    int Ho, int Wo, int P, CTensor cols) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -164,7 +164,7 @@ __global__ void stem_im2col_kernel(const float *__restrict__ data, const int *pe
 // add != null: dx = col2im + (add masked by (add_mask > 0) when add_mask.hi) - the
 // residual branch of a block folded into the gradient of its first conv.
 template <int KIND>
-__global__ void col2im_kernel(const void *__restrict__ dcols, int ldc, int B, int H, int W, int C, int R, int S,
+static __global__ void col2im_kernel(const void *__restrict__ dcols, int ldc, int B, int H, int W, int C, int R, int S,
                               int stride, int pad, int Ho, int Wo, void *dx, const void *add, CTensor add_mask) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -206,6 +206,12 @@ __global__ void col2im_kernel(const void *__restrict__ dcols, int ldc, int B, in
     }
 }
 
+// exact-erf GELU and its derivative (torch.nn.functional.gelu default)
+__device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_grad(float x) {
+    return 0.5f * (1.f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * __expf(-0.5f * x * x);
+}
+
 // ---------------------------------------------------------------------------
 // Epilogues of the persistent GEMM (gemm_pk_kernel / pk_reduce_kernel): run()
 // gets a shared sub-tile st[nrows][ncols] (row stride lds), the row map
@@ -223,6 +229,9 @@ struct EpiConvOut2 {
         int tiles;
         const void *add;     // Y-format [rows][ld] added to the output (residual gradient), or null
         CTensor add_mask;    // add masked by (add_mask > 0) when add_mask.hi
+        int out_f32;         // 1: fp32 output rows (and `add` is fp32): the ViT residual stream
+        CTensor gelu_out;    // also write gelu(out) here (compute format, own ld), or null
+        const void *gelu_z;  // out *= gelu'(z), z Y-format with the output's layout, or null
         // fused BN-backward statistics of the BN this gradient feeds (persistent, non-split only):
         // g' = out * (bn_mask > 0); bstats[C][CTA][3] += (sum g', sum g' xhat, sum g' xhat2)
         float *bstats;
@@ -312,13 +321,38 @@ struct EpiConvOut2 {
     // Stores (8 columns per element: 16-byte bf16 / 2 x 16-byte fp32 stores).
     template <int NTH>
     __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
-                               int ncols, int tm, int N, int tid) {
+                               int ncols, int tm, int N, int tid, int64_t off) {
+        if (((p.ld | col0 | ncols) & 7) || (off & 7)) {  // unaligned rows (e.g. a 10-class head): scalar
+            for (int e = tid; e < nrows * ncols; e += NTH) {
+                const int r = e / ncols, c = e - r * ncols;
+                const int m = rowm[r];
+                if (m < 0) continue;
+                float x = st[r * lds + c];
+                const size_t o = size_t(off) + size_t(m) * p.ld + col0 + c;
+                if (p.add && !p.bstats) {
+                    float a = p.out_f32 ? static_cast<const float *>(p.add)[o] : Fmt<0>::load(p.add, nullptr, o);
+                    if (KIND == 1 && !p.out_f32) a = static_cast<const float *>(p.add)[o];
+                    if (p.add_mask.hi && !(Fmt<KIND>::load(p.add_mask.hi, p.add_mask.lo, o) > 0.f)) a = 0.f;
+                    x += a;
+                }
+                if (p.gelu_z) x *= gelu_grad(KIND == 0 ? Fmt<0>::load(p.gelu_z, nullptr, o)
+                                                       : static_cast<const float *>(p.gelu_z)[o]);
+                if (p.gelu_out.hi)
+                    Fmt<KIND>::store(p.gelu_out.hi, p.gelu_out.lo, size_t(m) * p.gelu_out.ld + col0 + c, gelu(x));
+                if (p.out_f32 || KIND == 1)
+                    static_cast<float *>(p.out)[o] = x;
+                else
+                    Fmt<0>::store(p.out, nullptr, o, x);
+            }
+            return;
+        }
         const int C8 = ncols / 8;
         const int total = nrows * C8;
         constexpr int U = 2;
         for (int e0 = tid; e0 < total; e0 += NTH * U) {
             float4 v[U][2], a[U][2], mk[U][2];
             size_t o[U];
+            int gm[U], gc[U];
             bool ok[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -328,10 +362,17 @@ struct EpiConvOut2 {
                 if (!ok[u]) continue;
                 v[u][0] = *reinterpret_cast<const float4 *>(st + r * lds + c);
                 v[u][1] = *reinterpret_cast<const float4 *>(st + r * lds + c + 4);
-                o[u] = size_t(rowm[r]) * p.ld + col0 + c;
+                o[u] = size_t(off) + size_t(rowm[r]) * p.ld + col0 + c;
+                gm[u] = rowm[r];
+                gc[u] = col0 + c;
                 if (p.add && !p.bstats) {
-                    a[u][0] = ld_y4<KIND>(p.add, o[u]);
-                    a[u][1] = ld_y4<KIND>(p.add, o[u] + 4);
+                    if (p.out_f32) {
+                        a[u][0] = ld_f4(static_cast<const float *>(p.add), o[u]);
+                        a[u][1] = ld_f4(static_cast<const float *>(p.add), o[u] + 4);
+                    } else {
+                        a[u][0] = ld_y4<KIND>(p.add, o[u]);
+                        a[u][1] = ld_y4<KIND>(p.add, o[u] + 4);
+                    }
                     if (p.add_mask.hi) {
                         mk[u][0] = ld_c4<KIND>(p.add_mask, o[u]);
                         mk[u][1] = ld_c4<KIND>(p.add_mask, o[u] + 4);
@@ -351,7 +392,26 @@ struct EpiConvOut2 {
                         v[u][k].w += b.w;
                     }
                 }
-                if (KIND == 0) {
+                if (p.gelu_z) {
+                    const F8 zz = ld_y8<KIND>(p.gelu_z, o[u]);
+                    float w8[8] = {v[u][0].x, v[u][0].y, v[u][0].z, v[u][0].w,
+                                   v[u][1].x, v[u][1].y, v[u][1].z, v[u][1].w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) w8[i] *= gelu_grad(zz.v[i]);
+                    v[u][0] = make_float4(w8[0], w8[1], w8[2], w8[3]);
+                    v[u][1] = make_float4(w8[4], w8[5], w8[6], w8[7]);
+                }
+                if (p.gelu_out.hi) {
+                    const size_t og = size_t(gm[u]) * p.gelu_out.ld + gc[u];
+                    store_wc4<KIND>(p.gelu_out, og, make_float4(gelu(v[u][0].x), gelu(v[u][0].y), gelu(v[u][0].z),
+                                                                gelu(v[u][0].w)));
+                    store_wc4<KIND>(p.gelu_out, og + 4, make_float4(gelu(v[u][1].x), gelu(v[u][1].y),
+                                                                    gelu(v[u][1].z), gelu(v[u][1].w)));
+                }
+                if (p.out_f32) {
+                    st_f4(static_cast<float *>(p.out), o[u], v[u][0]);
+                    st_f4(static_cast<float *>(p.out), o[u] + 4, v[u][1]);
+                } else if (KIND == 0) {
                     __nv_bfloat162 b0 = __floats2bfloat162_rn(v[u][0].x, v[u][0].y);
                     __nv_bfloat162 b1 = __floats2bfloat162_rn(v[u][0].z, v[u][0].w);
                     __nv_bfloat162 b2 = __floats2bfloat162_rn(v[u][1].x, v[u][1].y);
@@ -420,8 +480,8 @@ struct EpiConvOut2 {
     // Split-K reduce kernel: the whole 128-row tile is in `st` (rows in order).
     template <int NTH>
     __device__ static void run_with_stats(const Params &p, const float *st, int lds, const int *rowm, int nrows,
-                                          int col0, int ncols, int tm, int N, int tid) {
-        run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid);
+                                          int col0, int ncols, int tm, int N, int tid, int64_t off) {
+        run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid, off);
         if (p.stats) {
             for (int c = tid; c < ncols; c += NTH) {
                 float s = 0.f, q = 0.f;
@@ -459,12 +519,12 @@ struct EpiHop2 {
     __device__ static void col_stats_init(const Params &, int, int, int) {}
     template <int NTH>
     __device__ static void run_with_stats(const Params &p, const float *st, int lds, const int *rowm, int nrows,
-                                          int col0, int ncols, int tm, int N, int tid) {
-        run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid);
+                                          int col0, int ncols, int tm, int N, int tid, int64_t off) {
+        run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid, off);
     }
     template <int NTH>
     __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
-                               int ncols, int, int, int tid) {
+                               int ncols, int, int, int tid, int64_t) {
         bool bad_g = false, bad_u = false;
         const float lr = *p.lr;
         if ((p.dout % 4) == 0 && (p.base % 4) == 0 && (ncols % 4) == 0) {
@@ -559,7 +619,7 @@ struct EpiHop2 {
 // Forward finalise: per channel, the per-tile (sum, sum sq) [C][tiles][2] (fp64)
 // -> mean, rstd (biased variance, eps).  One warp per channel, lanes take tiles
 // lane, lane+32, ... then a fixed xor-tree: deterministic.
-__global__ void bn_finalize_fwd_kernel(const float *__restrict__ stats, int tiles, int C, int64_t P, float eps,
+static __global__ void bn_finalize_fwd_kernel(const float *__restrict__ stats, int tiles, int C, int64_t P, float eps,
                                        float *mean, float *rstd) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -596,7 +656,7 @@ struct BnResidual {
 };
 
 template <int KIND>
-__global__ void bn_apply_kernel(const void *__restrict__ y, int64_t P, int C, const float *mean, const float *rstd,
+static __global__ void bn_apply_kernel(const void *__restrict__ y, int64_t P, int C, const float *mean, const float *rstd,
                                 const float *gamma, const float *beta, BnResidual res, int relu, CTensor out) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -638,7 +698,7 @@ __global__ void bn_apply_kernel(const void *__restrict__ y, int64_t P, int C, co
 constexpr int kBnRows = 256;
 
 template <int KIND>
-__global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__restrict__ g, CTensor mask, int64_t P, int C,
+static __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__restrict__ g, CTensor mask, int64_t P, int C,
                                                            const void *y, const float *mean, const float *rstd,
                                                            double *partial, const void *y2, const float *mean2,
                                                            const float *rstd2, double *partial2) {
@@ -715,7 +775,7 @@ __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__restric
 // Backward finalise of the statistics fused into the data-gradient GEMM epilogue:
 // per channel the per-CTA (sum g', sum g' xhat, sum g' xhat2) [C][CTAs][3] in CTA order
 // (fp64) -> dbeta, dgamma (and dgamma2 of the projection BN, which shares dbeta).
-__global__ void bn_finalize_bwd_cta_kernel(const float *__restrict__ part, int nct, int C, float *dbeta,
+static __global__ void bn_finalize_bwd_cta_kernel(const float *__restrict__ part, int nct, int C, float *dbeta,
                                            float *dgamma, float *dbeta2, float *dgamma2) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -746,7 +806,7 @@ __global__ void bn_finalize_bwd_cta_kernel(const float *__restrict__ part, int n
 }
 
 // Backward finalise: dbeta = sum g', dgamma = sum g' xhat over the row blocks in order.
-__global__ void bn_finalize_bwd_kernel(const double *__restrict__ partial, int nblk, int C, float *dbeta,
+static __global__ void bn_finalize_bwd_kernel(const double *__restrict__ partial, int nblk, int C, float *dbeta,
                                        float *dgamma) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -774,7 +834,7 @@ __global__ void bn_finalize_bwd_kernel(const double *__restrict__ partial, int n
 // Backward through BN (+ReLU mask): dx = gamma * rstd * (g' - dbeta/P - xhat * dgamma/P)
 // in compute format (the conv's output gradient, a GEMM operand).
 template <int KIND>
-__global__ void bn_bwd_apply_kernel(const void *__restrict__ g, CTensor mask, const void *__restrict__ y, int64_t P,
+static __global__ void bn_bwd_apply_kernel(const void *__restrict__ g, CTensor mask, const void *__restrict__ y, int64_t P,
                                     int C, const float *mean, const float *rstd, const float *gamma,
                                     const float *dbeta, const float *dgamma, CTensor dx) {
     ptx::griddep_wait();
@@ -806,7 +866,7 @@ __global__ void bn_bwd_apply_kernel(const void *__restrict__ g, CTensor mask, co
 // tap (first maximum in (r, s) order) per output element; backward is a
 // deterministic gather over the (at most 4) windows containing an input pixel.
 template <int KIND>
-__global__ void maxpool_fwd_kernel(CTensor in, int B, int H, int W, int C, int Ho, int Wo, CTensor out,
+static __global__ void maxpool_fwd_kernel(CTensor in, int B, int H, int W, int C, int Ho, int Wo, CTensor out,
                                    uint8_t *arg) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -840,7 +900,7 @@ __global__ void maxpool_fwd_kernel(CTensor in, int B, int H, int W, int C, int H
 }
 
 template <int KIND>
-__global__ void maxpool_bwd_kernel(const void *__restrict__ gout, const uint8_t *__restrict__ arg, int B, int H, int W,
+static __global__ void maxpool_bwd_kernel(const void *__restrict__ gout, const uint8_t *__restrict__ arg, int B, int H, int W,
                                    int C, int Ho, int Wo, void *gin) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -877,7 +937,7 @@ __global__ void maxpool_bwd_kernel(const void *__restrict__ gout, const uint8_t 
 
 // Global average pool: act [B*HW][ld] -> pooled [B][C+1] (ones column at C for the fc bias).
 template <int KIND>
-__global__ void avgpool_kernel(CTensor act, int B, int HW, int C, CTensor pooled) {
+static __global__ void avgpool_kernel(CTensor act, int B, int HW, int C, CTensor pooled) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int b = blockIdx.x;
@@ -895,7 +955,7 @@ __global__ void avgpool_kernel(CTensor act, int B, int HW, int C, CTensor pooled
 
 // d act[b, k, c] = dpooled[b][c] / HW (Y format), 4 channels per thread.
 template <int KIND>
-__global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, int HW, int C, void *g) {
+static __global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, int HW, int C, void *g) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int C4 = C / 4;
@@ -913,7 +973,7 @@ __global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, int HW,
 // fixed-tree block reductions; per-sample losses summed in ascending sample
 // order by loss_sum_kernel (ref _kernels.pyx:80-100 semantics).
 template <int KIND>
-__global__ void __launch_bounds__(256) xent_rows_kernel(const float *__restrict__ z, int B, int C, const int *perm,
+static __global__ void __launch_bounds__(256) xent_rows_kernel(const float *__restrict__ z, int B, int C, const int *perm,
                                                         const int *labels, CTensor dz, double *loss_rows) {
     ptx::griddep_wait();
     ptx::griddep_launch();
@@ -947,7 +1007,7 @@ __global__ void __launch_bounds__(256) xent_rows_kernel(const float *__restrict_
     }
 }
 
-__global__ void loss_sum_kernel(const double *rows, int B, double *loss_out, unsigned *loss_flag) {
+static __global__ void loss_sum_kernel(const double *rows, int B, double *loss_out, unsigned *loss_flag) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     double acc = 0.0;
@@ -989,7 +1049,7 @@ struct EpiDgradLinear {
 // gradient (p.s_in), the reference's update arithmetic (engine.py:102-109) in fp32,
 // repacking the GEMM compute copy ([rows][ld], `cols` per row) when the tensor has one.
 template <int KIND>
-__global__ void update_flat_kernel(HopParams p, int64_t n, int cols) {
+static __global__ void update_flat_kernel(HopParams p, int64_t n, int cols) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const float lr = *p.lr;
@@ -1009,12 +1069,12 @@ __global__ void update_flat_kernel(HopParams p, int64_t n, int cols) {
 // The pre-hop waits of a weight hop (EpiWgrad::pre) in a one-CTA kernel ahead
 // of the GEMM, so that a GEMM grid never occupies SMs while it waits for a peer
 // (no dependent launch is triggered before the waits are over).
-__global__ void hop_wait_kernel(HopParams p) { EpiWgrad<0>::pre(p, threadIdx.x, true); }
+static __global__ void hop_wait_kernel(HopParams p) { EpiWgrad<0>::pre(p, threadIdx.x, true); }
 
 // Hop / update of a small parameter vector (batch-norm gamma|beta, gradient
 // g[0..n) = [dgamma | dbeta] in the parameter order) with the same modes and
 // ring protocol as the weight-gradient epilogue.  One CTA of 128 threads.
-__global__ void vector_hop_kernel(HopParams p, const float *dgamma, const float *dbeta, int C) {
+static __global__ void vector_hop_kernel(HopParams p, const float *dgamma, const float *dbeta, int C) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     EpiWgrad<0>::pre(p, threadIdx.x);

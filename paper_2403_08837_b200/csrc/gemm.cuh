@@ -67,7 +67,9 @@ struct GemmArgs {
     ConvGeom cv;      // MODE 1-3 only
 };
 
-enum GemmMode { GM_PLAIN = 0, GM_FPROP = 1, GM_DGRAD = 2, GM_WGRAD = 3 };
+// GM_BATCH: independent GEMMs over a (head, sample) grid, every operand a 4-D TMA view
+// {inner, rows, heads, samples} of a token-major buffer (attention score / value products).
+enum GemmMode { GM_PLAIN = 0, GM_FPROP = 1, GM_DGRAD = 2, GM_WGRAD = 3, GM_BATCH = 4 };
 
 template <int KIND, int BN_, bool A_MN, bool B_MN, int ST = 0, int PF = 0>
 struct GemmCfg {

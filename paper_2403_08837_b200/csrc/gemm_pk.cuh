@@ -31,6 +31,10 @@ struct PkArgs {
     int boxed;     // rows of an M tile are a pixel box of cv (FPROP / DGRAD)
     float *ws;     // split partials [tile][split][128][BN]
     ConvGeom cv;
+    // GM_BATCH: nbatch = heads * samples independent GEMMs; batch g = (head g % nh, sample g / nh);
+    // the epilogue's output offset of batch g = (g / nh) * out_bs + (g % nh) * out_hs elements
+    int nbatch, nh;
+    int64_t out_bs, out_hs;
 };
 
 template <int KIND, int BN, bool A_MN, bool B_MN, int ST>
@@ -78,11 +82,17 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
     return v[0];
 }
 
-__device__ __forceinline__ void pk_unit(const PkArgs &a, int u, int &tm, int &tn, int &split) {
+__device__ __forceinline__ void pk_unit(const PkArgs &a, int u, int &tm, int &tn, int &split, int &g) {
     split = u % a.splits;
     const int t = u / a.splits;
     tn = t % a.tiles_n;
-    tm = t / a.tiles_n;
+    const int r = t / a.tiles_n;
+    tm = r % a.tiles_m;
+    g = r / a.tiles_m;
+}
+__device__ __forceinline__ void pk_unit(const PkArgs &a, int u, int &tm, int &tn, int &split) {
+    int g;
+    pk_unit(a, u, tm, tn, split, g);
 }
 
 // tile row -> output row m (or -1): pixel box rows (FPROP / DGRAD) or m0 + r.
@@ -156,6 +166,26 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     if constexpr (MODE == GM_PLAIN) {
                         load_operand<C, A_MN, 128>(sA + s * C::A_BYTES, &maps.a[seg], &full[s], m0, kb * C::BK);
                         load_operand<C, B_MN, BN>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, kb * C::BK);
+                    } else if constexpr (MODE == GM_BATCH) {
+                        int tm2, tn2, sp2, g;
+                        pk_unit(args, u, tm2, tn2, sp2, g);
+                        const int hh = g % args.nh, bb = g / args.nh, k0 = kb * C::BK;
+                        if constexpr (!A_MN) {
+                            ptx::tma_load_4d(sA + s * C::A_BYTES, &maps.a[seg], &full[s], k0, m0, hh, bb);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 128 / C::CH; ++c)
+                                ptx::tma_load_4d(sA + s * C::A_BYTES + c * (C::BK * 128), &maps.a[seg], &full[s],
+                                                 m0 + c * C::CH, k0, hh, bb);
+                        }
+                        if constexpr (!B_MN) {
+                            ptx::tma_load_4d(sB + s * C::B_BYTES, &maps.b[seg], &full[s], k0, n0, hh, bb);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < BN / C::CH; ++c)
+                                ptx::tma_load_4d(sB + s * C::B_BYTES + c * (C::BK * 128), &maps.b[seg], &full[s],
+                                                 n0 + c * C::CH, k0, hh, bb);
+                        }
                     } else {
                         conv_load<C, MODE, B_MN, BN>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args.cv, &full[s],
                                                      seg, kb, tm, m0, n0);
@@ -201,8 +231,9 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         }
         int j = 0;
         for (int u = blockIdx.x; u < args.units; u += gridDim.x, ++j) {
-            int tm, tn, sp;
-            pk_unit(args, u, tm, tn, sp);
+            int tm, tn, sp, g;
+            pk_unit(args, u, tm, tn, sp, g);
+            const int64_t out_off = MODE == GM_BATCH ? (g / args.nh) * args.out_bs + (g % args.nh) * args.out_hs : 0;
             const int acc = j & 1;
             const bool split = args.splits > 1;
             if (tid < 128) rowm[tid] = pk_row_m(args, tm, tid);  // the previous unit's last barrier protects rowm / stile
@@ -236,7 +267,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     }
                 } else {
                     Epi::template run<kPkEpi>(ep, stile, C::LDS, rowm, 128, col0, min(C::EPI_COLS, args.N - col0), tm,
-                                              args.N, tid);
+                                              args.N, tid, out_off);
                     Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), tm,
                                                     tid);
                 }
@@ -282,7 +313,7 @@ __global__ void __launch_bounds__(256) pk_reduce_kernel(const PkArgs args, const
     __syncthreads();
     const int col0 = tn * BN + c0;
     Epi::template run_with_stats<256>(ep, st, CC + 4, rowm, RC, col0, min(CC, args.N - col0), tm, args.N,
-                                      threadIdx.x);
+                                      threadIdx.x, 0);
     Epi::template done<256>(ep, threadIdx.x, gridDim.x * gridDim.y * gridDim.z);
 }
 

@@ -1,0 +1,74 @@
+// Kernels and helpers shared by the one-worker-per-process trainers (ResNet, ViT):
+// parameter pulls from the updater (the theta delivery of SURVEY §5), the step
+// bookkeeping kernel, compute-copy packing, and the GEMM tile-width dispatch.
+#pragma once
+#include <string>
+#include <type_traits>
+
+#include "conv_kernels.cuh"
+#include "trainer_common.cuh"
+
+namespace cdp {
+namespace {
+
+// Wait (one thread) until the updater holds the version this rank reads of `unit`.
+__global__ void pull_wait_kernel(RingFlags *updater, RingFlags *own, int unit, int fresh, const int *step) {
+    const int t = *step;
+    const uint32_t v = uint32_t(fresh ? t : t - 1);
+    if (v > 1 && threadIdx.x == 0) spin_ge(&updater->updated[unit - 1], v, &own->err);
+}
+
+template <int KIND>
+__global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, int64_t n, int cols, CTensor wc,
+                                   RingFlags *updater, RingFlags *own, int unit, int fresh, const int *step,
+                                   unsigned *cta_counter) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int t = *step;
+    const uint32_t v = uint32_t(fresh ? t : t - 1);
+    if (v <= 1) return;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const float x = __ldcv(src + i);
+        dst[i] = x;
+        if (wc.hi) Fmt<KIND>::store(wc.hi, wc.lo, size_t(i / cols) * wc.ld + i % cols, x);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(&cta_counter[unit - 1], 1u) == gridDim.x - 1) {
+            cta_counter[unit - 1] = 0;
+            atomicAdd_system(&updater->pulled[unit - 1][v & 1], 1u);
+        }
+    }
+}
+
+__global__ void finish_step_kernel_rn(const double *loss, Flags *flags, double *hist_loss, Flags *hist_flags, int cap,
+                                      const int *step) {
+    const int c = *step - 1;
+    hist_loss[c % cap] = *loss;
+    hist_flags[c % cap] = *flags;
+    *flags = Flags{0, 0, 0, 0};
+}
+
+template <int KIND>
+__global__ void pack_tensor_kernel(const float *__restrict__ w, int64_t n, int cols, CTensor out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        Fmt<KIND>::store(out.hi, out.lo, size_t(i / cols) * out.ld + i % cols, w[i]);
+}
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+template <class F>
+void bn_switch(int BN, F &&f) {
+    switch (BN) {
+        case 32: f(IC<32>{}); return;
+        case 64: f(IC<64>{}); return;
+        case 128: f(IC<128>{}); return;
+        case 256: f(IC<256>{}); return;
+        default: throw CdpError("unsupported GEMM tile width " + std::to_string(BN));
+    }
+}
+
+}  // namespace
+}  // namespace cdp

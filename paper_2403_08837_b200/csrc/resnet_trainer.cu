@@ -31,6 +31,7 @@
 #include "conv_kernels.cuh"
 #include "gemm_launch.cuh"
 #include "trainer_common.cuh"
+#include "rank_common.cuh"
 
 namespace cdp {
 
@@ -70,37 +71,6 @@ struct OpRec {
     double flops, bytes;
     cudaEvent_t a, b;
 };
-
-// Wait (one thread) until the updater holds the version this rank reads of `unit`.
-__global__ void pull_wait_kernel(RingFlags *updater, RingFlags *own, int unit, int fresh, const int *step) {
-    const int t = *step;
-    const uint32_t v = uint32_t(fresh ? t : t - 1);
-    if (v > 1 && threadIdx.x == 0) spin_ge(&updater->updated[unit - 1], v, &own->err);
-}
-
-template <int KIND>
-__global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, int64_t n, int cols, CTensor wc,
-                                   RingFlags *updater, RingFlags *own, int unit, int fresh, const int *step,
-                                   unsigned *cta_counter) {
-    ptx::griddep_wait();
-    ptx::griddep_launch();
-    const int t = *step;
-    const uint32_t v = uint32_t(fresh ? t : t - 1);
-    if (v <= 1) return;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const float x = __ldcv(src + i);
-        dst[i] = x;
-        if (wc.hi) Fmt<KIND>::store(wc.hi, wc.lo, size_t(i / cols) * wc.ld + i % cols, x);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        if (atomicAdd(&cta_counter[unit - 1], 1u) == gridDim.x - 1) {
-            cta_counter[unit - 1] = 0;
-            atomicAdd_system(&updater->pulled[unit - 1][v & 1], 1u);
-        }
-    }
-}
 
 // ---------------------------------------------------------------- ZeRO-CDP state passing
 // (zero.py: use index u = base + (t-1)*2N + kZeroOff; predecessor on rank `src` in step t + dstep)
@@ -151,34 +121,6 @@ __global__ void zero_done_kernel(ZeroUse z, RingFlags *own, int unit, const int 
     const int t = *step + step_delta;
     __threadfence_system();
     ptx::st_release_sys(&own->zdone[unit - 1], zero_u(z, t));
-}
-
-__global__ void finish_step_kernel_rn(const double *loss, Flags *flags, double *hist_loss, Flags *hist_flags, int cap,
-                                      const int *step) {
-    const int c = *step - 1;
-    hist_loss[c % cap] = *loss;
-    hist_flags[c % cap] = *flags;
-    *flags = Flags{0, 0, 0, 0};
-}
-
-template <int KIND>
-__global__ void pack_tensor_kernel(const float *__restrict__ w, int64_t n, int cols, CTensor out) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-        Fmt<KIND>::store(out.hi, out.lo, size_t(i / cols) * out.ld + i % cols, w[i]);
-}
-
-template <int V>
-using IC = std::integral_constant<int, V>;
-
-template <class F>
-void bn_switch(int BN, F &&f) {
-    switch (BN) {
-        case 32: f(IC<32>{}); return;
-        case 64: f(IC<64>{}); return;
-        case 128: f(IC<128>{}); return;
-        case 256: f(IC<256>{}); return;
-        default: throw CdpError("unsupported GEMM tile width " + std::to_string(BN));
-    }
 }
 
 }  // namespace
@@ -632,7 +574,7 @@ struct ResNetTrainer {
     }
 
     static int blocks_for(int64_t n, int per = 256) { return int(std::min<int64_t>(8 * 148, (n + per - 1) / per)); }
-    static int tile_n(int n) { return std::min(256, std::max(64, n)); }
+    static int tile_n(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }  // a supported BN covering n
 
     // ---------------------------------------------------------------- forward pieces
     template <int K>

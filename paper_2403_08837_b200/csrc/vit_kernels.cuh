@@ -1,0 +1,217 @@
+// Vision-Transformer layer kernels (BASELINE configs[3]: ViT-B/16) around the
+// persistent tcgen05 GEMM: patch im2col, token assembly, LayerNorm forward /
+// backward / parameter gradients, attention softmax forward / backward, token
+// gradients of the embeddings, and a multi-CTA flat hop for vector parameters.
+// The residual stream is fp32; GEMM operands are bf16 (KIND 0), with a constant
+// ones column after the features of every linear layer's input (bias folding:
+// [x, 1] . [W; b], the reference's flat [W][b] layout).  Reductions run in a
+// fixed order (warp xor trees over fixed lane assignments, row blocks in order).
+#pragma once
+#include "conv_kernels.cuh"
+
+namespace cdp {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// patches[b*np + gy*G + gx][(r*P + s)*3 + c] = image[perm[b]][gy*P + r][gx*P + s][c];
+// column K = P*P*3 is the constant 1 (bias), columns above it 0.
+template <int KIND>
+static __global__ void patch_im2col_kernel(const float *__restrict__ data, const int *perm, int img, int P, int G, int rows,
+                                    CTensor out) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int K = P * P * 3;
+    const int64_t n = int64_t(rows) * out.ld;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int k = int(i % out.ld);
+        const int row = int(i / out.ld);
+        float v = k == K ? 1.f : 0.f;
+        if (k < K) {
+            const int np = G * G;
+            const int b = row / np, pi = row % np, gy = pi / G, gx = pi % G;
+            const int r = k / (P * 3), rem = k % (P * 3), s = rem / 3, c = rem % 3;
+            v = data[((size_t(perm[b]) * img + gy * P + r) * img + gx * P + s) * 3 + c];
+        }
+        Fmt<KIND>::store(out.hi, out.lo, size_t(i), v);
+    }
+}
+
+// h0[b*T + 0] = cls + pos[0];  h0[b*T + 1 + p] = E[b*np + p] + pos[1 + p]   (fp32, D features)
+static __global__ void embed_assemble_kernel(const float *__restrict__ E, const float *cls, const float *pos, int B, int T,
+                                      int D, float *h0) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int64_t n = int64_t(B) * T * D;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int d = int(i % D);
+        const int64_t row = i / D;
+        const int t = int(row % T), b = int(row / T);
+        const float e = t == 0 ? cls[d] : E[(size_t(b) * (T - 1) + t - 1) * D + d];
+        h0[i] = e + pos[size_t(t) * D + d];
+    }
+}
+
+// LayerNorm forward, one warp per row (row r reads x row r * in_stride):
+// out = gamma * (x - mean) * rstd + beta  (compute format, ones column at D), mean / rstd saved.
+template <int KIND>
+static __global__ void ln_fwd_kernel(const float *__restrict__ x, int rows, int in_stride, int D, const float *gb, float eps,
+                              CTensor out, float *mean, float *rstd) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float *xr = x + size_t(w) * in_stride * D;
+    float s = 0.f;
+    for (int d = lane; d < D; d += 32) s += xr[d];
+    const float mu = warp_sum(s) / float(D);
+    float q = 0.f;
+    for (int d = lane; d < D; d += 32) {
+        const float c = xr[d] - mu;
+        q += c * c;
+    }
+    const float rs = rsqrtf(warp_sum(q) / float(D) + eps);
+    for (int d = lane; d < D; d += 32)
+        Fmt<KIND>::store(out.hi, out.lo, size_t(w) * out.ld + d, gb[d] * ((xr[d] - mu) * rs) + gb[D + d]);
+    if (lane == 0) {
+        Fmt<KIND>::store(out.hi, out.lo, size_t(w) * out.ld + D, 1.f);
+        mean[w] = mu;
+        rstd[w] = rs;
+    }
+}
+
+// LayerNorm backward of the input, one warp per row:
+//   dx = rstd * (g*gamma - mean(g*gamma) - xhat * mean(g*gamma*xhat));  dh_out = dh_in + dx
+// (row r of g / dh_* is row r * in_stride of the residual stream; dh_in may be null).
+static __global__ void ln_bwd_kernel(const float *__restrict__ g, const float *__restrict__ x, int rows, int in_stride, int D,
+                              const float *gb, const float *mean, const float *rstd, const float *dh_in,
+                              float *dh_out) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const size_t xo = size_t(w) * in_stride * D, go = size_t(w) * D;
+    const float mu = mean[w], rs = rstd[w];
+    float a = 0.f, b = 0.f;
+    for (int d = lane; d < D; d += 32) {
+        const float gg = g[go + d] * gb[d];
+        a += gg;
+        b += gg * ((x[xo + d] - mu) * rs);
+    }
+    a = warp_sum(a) / float(D);
+    b = warp_sum(b) / float(D);
+    for (int d = lane; d < D; d += 32) {
+        const float xh = (x[xo + d] - mu) * rs;
+        const float dx = rs * (g[go + d] * gb[d] - a - xh * b);
+        dh_out[xo + d] = (dh_in ? dh_in[xo + d] : 0.f) + dx;
+    }
+}
+
+// LayerNorm parameter gradients, row-block partials: partial[d][blk][2] = (sum g xhat, sum g)
+// over the block's rows in order (fp64) -> bn_finalize_bwd_kernel (dbeta = [1], dgamma = [0]).
+constexpr int kLnRows = 128;
+static __global__ void ln_param_partial_kernel(const float *__restrict__ g, const float *__restrict__ x, int rows,
+                                        int in_stride, int D, const float *mean, const float *rstd,
+                                        double *partial) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int r0 = blockIdx.x * kLnRows, r1 = min(rows, r0 + kLnRows);
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        double sx = 0.0, sg = 0.0;
+        for (int r = r0; r < r1; ++r) {
+            const float gv = g[size_t(r) * D + d];
+            const float xh = (x[size_t(r) * in_stride * D + d] - mean[r]) * rstd[r];
+            sg += double(gv);
+            sx += double(gv) * double(xh);
+        }
+        double *o = partial + (size_t(d) * gridDim.x + blockIdx.x) * 2;
+        o[0] = sg;  // -> dbeta
+        o[1] = sx;  // -> dgamma
+    }
+}
+
+// Row softmax of scale * S (fp32 [rows][lds], n valid columns) -> P (bf16 [rows][ldp]); one warp per row.
+static __global__ void softmax_fwd_kernel(const float *__restrict__ S, int rows, int n, int lds, float scale,
+                                   __nv_bfloat16 *P, int ldp) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float *sr = S + size_t(w) * lds;
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, sr[j] * scale);
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int j = lane; j < n; j += 32) sum += __expf(sr[j] * scale - mx);
+    const float inv = 1.f / warp_sum(sum);
+    for (int j = lane; j < n; j += 32) P[size_t(w) * ldp + j] = __float2bfloat16_rn(__expf(sr[j] * scale - mx) * inv);
+}
+
+// dS = scale * P (dP - sum_j dP_j P_j)   (gradient w.r.t. the unscaled scores), bf16.
+static __global__ void softmax_bwd_kernel(const float *__restrict__ dP, const __nv_bfloat16 *__restrict__ P, int rows, int n,
+                                   int lds, int ldp, float scale, __nv_bfloat16 *dS) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    float dot = 0.f;
+    for (int j = lane; j < n; j += 32) dot += dP[size_t(w) * lds + j] * __bfloat162float(P[size_t(w) * ldp + j]);
+    dot = warp_sum(dot);
+    for (int j = lane; j < n; j += 32) {
+        const float p = __bfloat162float(P[size_t(w) * ldp + j]);
+        dS[size_t(w) * ldp + j] = __float2bfloat16_rn(scale * p * (dP[size_t(w) * lds + j] - dot));
+    }
+}
+
+// fp32 [rows][D] -> compute format [rows][ld] (GEMM operand), optional row gather
+// (out row r <- in row (r / per) * in_per + skip + r % per).
+template <int KIND>
+static __global__ void cast_rows_kernel(const float *__restrict__ in, int rows, int D, int per, int in_per, int skip,
+                                 CTensor out) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int64_t n = int64_t(rows) * D;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int d = int(i % D);
+        const int r = int(i / D);
+        const int64_t src = int64_t(r / per) * in_per + skip + r % per;
+        Fmt<KIND>::store(out.hi, out.lo, size_t(r) * out.ld + d, in[size_t(src) * D + d]);
+    }
+}
+
+// Embedding gradients: pos[t][d] = sum_b dh[b*T + t][d], cls[d] = sum_b dh[b*T][d] (ascending b).
+static __global__ void token_grad_kernel(const float *__restrict__ dh, int B, int T, int D, float *gpos, float *gcls) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int64_t n = int64_t(T) * D;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        float s = 0.f;
+        for (int b = 0; b < B; ++b) s += dh[size_t(b) * T * D + i];
+        gpos[i] = s;
+        if (i < D) gcls[i] = s;
+    }
+}
+
+// Hop / update of a flat vector parameter (class token, position embedding) from a gradient g[0..n)
+// with the ring protocol of the weight hops (multi-CTA: the last CTA publishes).
+static __global__ void flat_hop_kernel(HopParams p, const float *g, int64_t n) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    EpiWgrad<0>::pre(p, threadIdx.x);
+    bool bg = false, bu = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        hop_elem<0>(p, p.base + i, g[i], 0, false, bg, bu);
+    if (bg) atomicOr(p.grad_flags, 1u << ((p.stage - 1) & 31));
+    if (bu) atomicOr(p.upd_flags, 1u << ((p.stage - 1) & 31));
+    EpiWgrad<0>::post(p, threadIdx.x, gridDim.x);
+}
+
+}  // namespace cdp

@@ -1,0 +1,1065 @@
+// Device-resident CDP training step for Vision Transformers (BASELINE configs[3]:
+// ViT-B/16, 224x224), bf16 operands, fp32 residual stream / master state.
+//
+// Same step semantics as the other trainers (ref training/engine.py:66-116: the
+// per-stage version rule, gradient hops w_i -> w_{i+1} fused into the weight-gradient
+// GEMM epilogues, the SGD-momentum update on the last worker, parameter pulls), one
+// worker (micro-batch) per process.  Layer compute:
+//   linear layers  = persistent tcgen05 GEMMs (gemm_pk_kernel, GM_PLAIN) with the bias
+//                    folded in by a ones column ([x, 1] . [W; b] = the reference's
+//                    flat [W][b] layout); GELU and the residual add fused in epilogues;
+//   attention      = batched tcgen05 GEMMs (GM_BATCH) over 4-D TMA views of the fused
+//                    qkv buffer {64 dims, tokens, heads, samples} + row softmax kernels;
+//   LayerNorm      = warp-per-row kernels, parameter gradients by fixed-order row blocks.
+// Hop units (parameter tensors, torchvision order): patch [[W^T]; b], cls, pos, per
+// block ln1 [g | b], qkv, proj, ln2, fc1, fc2 (linear [[W^T]; b]), final ln, head.
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/cdp_b200.h"
+#include "gemm_launch.cuh"
+#include "rank_common.cuh"
+#include "trainer_common.cuh"
+#include "vit_kernels.cuh"
+
+namespace cdp {
+
+namespace {
+
+enum VitUnitKind { V_LIN = 0, V_LN = 1, V_VEC = 2 };
+
+struct VUnit {
+    int kind;
+    int64_t base, n;
+    int rows, cols;  // GEMM view of a linear unit ([in + 1][out])
+    int stage, fresh;
+};
+
+struct VLayer {
+    int ln1, qkv, proj, ln2, fc1, fc2;  // unit indices
+    DevBuf h, hmid;                     // fp32 residual stream: block input, after attention
+    DevBuf m1, r1, m2, r2;              // LayerNorm row statistics
+    CBuf u1, u2, attn, g1, qkvb, z1;    // LN outputs, attention output, GELU output, qkv, FC1 pre-activation
+    DevBuf P;                           // softmax probabilities bf16 [B*H][T][ldp]
+    CBuf dhc, dz1, dhmc, dqkv;          // backward GEMM operands read by the hop stream (per layer)
+    DevBuf dg1, db1, dg2, db2;          // LayerNorm parameter gradients
+};
+
+struct BView {  // a 4-D TMA view {inner, rows, heads, samples} of a token-major bf16 buffer
+    const void *ptr;
+    int inner, rows;
+    int64_t ld, hs, bs;  // elements
+};
+
+}  // namespace
+
+struct VitTrainer {
+    // ---------------------------------------------------------------- config
+    int B = 0, img = 224, P = 16, G = 14, NP = 196, T = 197, D = 768, H = 12, HD = 64, F = 3072, L = 12;
+    int classes = 1000, loss_kind = 1;
+    float momentum = 0.f, wd = 0.f, eps = 1e-6f;
+    int rank = 0, world = 1;
+    std::vector<VUnit> units;
+    std::vector<VLayer> layers;
+    int u_patch = 0, u_cls = 0, u_pos = 0, u_ln = 0, u_head = 0;
+    int64_t Pn = 0, Pp = 0;
+    int R = 0, lds = 0, ldp = 0;
+
+    // ---------------------------------------------------------------- state
+    DevBuf region, cta_counters;
+    float *vel = nullptr, *theta[2] = {nullptr, nullptr}, *partial = nullptr;
+    RingFlags *ring = nullptr;
+    size_t region_off = 0;
+    RingFlags *prev_ring = nullptr, *upd_ring = nullptr;
+    float *prev_partial = nullptr, *upd_theta[2] = {nullptr, nullptr};
+    std::vector<CBuf> wc[2];
+    CBuf patches, uf, dz, dE;
+    DevBuf E, hL, mf, rf, z, loss_dev, loss_rows, S, dP, du, duf, dh, dhm, gpos, gcls, lnpart, dgf, dbf;
+    CBuf dattn, dS;
+    DevBuf ws_c, ws_h, cnt_c, cnt_h;
+    size_t ws_c_floats = 0, ws_h_floats = 0;
+    DevBuf data_x, data_lab, ctrl_dev, perm_dev, flags_dev, hist_loss, hist_flags;
+    int n_samples = 0;
+    static constexpr int RING_N = 16;
+    uint8_t *stage_host = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_ev[RING_N] = {};
+    int stage_next = 0;
+    int hist_cap = 1 << 14;
+    cudaStream_t main = nullptr, cs = nullptr, hs = nullptr;
+    std::vector<cudaEvent_t> events;
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    int t = 1;
+    int kernels_per_step = 0;
+    double flops_per_step = 0.0;
+    std::vector<cudaEvent_t> marks;
+    DevBuf flush_buf;
+    bool sizing = false, instr = false;
+    struct OpRec {
+        std::string name;
+        double flops, bytes;
+        cudaEvent_t a, b;
+    };
+    std::vector<OpRec> oprecs;
+    int sms_ = 0;
+
+    ~VitTrainer() {
+        for (auto &e : exec)
+            if (e) cudaGraphExecDestroy(e);
+        for (auto e : events) cudaEventDestroy(e);
+        for (auto e : marks) cudaEventDestroy(e);
+        clear_oprecs();
+        for (auto e : stage_ev)
+            if (e) cudaEventDestroy(e);
+        if (stage_host) cudaFreeHost(stage_host);
+        for (auto s : {main, cs, hs})
+            if (s) cudaStreamDestroy(s);
+    }
+    void clear_oprecs() {
+        for (auto &o : oprecs) {
+            cudaEventDestroy(o.a);
+            cudaEventDestroy(o.b);
+        }
+        oprecs.clear();
+    }
+    template <class Fn>
+    void L_(const char *name, double flops, double bytes, cudaStream_t s, Fn &&f) {
+        if (sizing) return;
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (instr) {
+            CDP_CUDA(cudaEventCreate(&a));
+            CDP_CUDA(cudaEventCreate(&b));
+            CDP_CUDA(cudaEventRecord(a, s));
+        }
+        f();
+        ++kernels_per_step;
+        flops_per_step += flops;
+        if (instr) {
+            CDP_CUDA(cudaEventRecord(b, s));
+            oprecs.push_back(OpRec{name, flops, bytes, a, b});
+        }
+    }
+    int sms() {
+        if (!sms_) sms_ = num_sms();
+        return sms_;
+    }
+    static int blocks_for(int64_t n, int per = 256) { return int(std::min<int64_t>(8 * 148, (n + per - 1) / per)); }
+    static int tile_n(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }  // a supported BN covering n
+
+    // ---------------------------------------------------------------- model
+    int add_unit(int kind, int64_t n, int rows, int cols) {
+        const int64_t base = units.empty() ? 0 : units.back().base + units.back().n;
+        units.push_back(VUnit{kind, base, n, rows, cols, 1, 1});
+        return int(units.size()) - 1;
+    }
+
+    void build() {
+        G = img / P;
+        NP = G * G;
+        T = NP + 1;
+        HD = D / H;
+        CDP_REQUIRE(HD == 64, "head dim must be 64 (one 128-byte TMA chunk)");
+        CDP_REQUIRE(D % 64 == 0 && F % 64 == 0 && img % P == 0, "dims: multiples of 64; image a multiple of the patch");
+        R = B * T;
+        lds = round_up(T, 4);
+        ldp = round_up(T, 16);
+        const int K0 = P * P * 3;
+        u_patch = add_unit(V_LIN, int64_t(K0 + 1) * D, K0 + 1, D);
+        u_cls = add_unit(V_VEC, D, 0, 0);
+        u_pos = add_unit(V_VEC, int64_t(T) * D, 0, 0);
+        layers.resize(L);
+        for (auto &ly : layers) {
+            ly.ln1 = add_unit(V_LN, 2 * D, 0, 0);
+            ly.qkv = add_unit(V_LIN, int64_t(D + 1) * 3 * D, D + 1, 3 * D);
+            ly.proj = add_unit(V_LIN, int64_t(D + 1) * D, D + 1, D);
+            ly.ln2 = add_unit(V_LN, 2 * D, 0, 0);
+            ly.fc1 = add_unit(V_LIN, int64_t(D + 1) * F, D + 1, F);
+            ly.fc2 = add_unit(V_LIN, int64_t(F + 1) * D, F + 1, D);
+        }
+        u_ln = add_unit(V_LN, 2 * D, 0, 0);
+        u_head = add_unit(V_LIN, int64_t(D + 1) * classes, D + 1, classes);
+        Pn = units.back().base + units.back().n;
+        CDP_REQUIRE(int(units.size()) <= kMaxStages, "too many parameter tensors for the ring flags");
+        // ---- activations / gradients
+        auto ones = [&](CBuf &b, int rows, int col) {  // constant 1 in column `col` (bias folding)
+            std::vector<__nv_bfloat16> one(size_t(rows), __float2bfloat16(1.f));
+            CDP_CUDA(cudaMemcpy2D(static_cast<__nv_bfloat16 *>(b.hi.p) + col, size_t(b.ld) * 2, one.data(), 2, 2,
+                                  size_t(rows), cudaMemcpyHostToDevice));
+        };
+        patches = make_cbuf(0, B * NP, K0 + 1);
+        E = DevBuf(size_t(B) * NP * D * 4);
+        for (auto &ly : layers) {
+            ly.h = DevBuf(size_t(R) * D * 4);
+            ly.hmid = DevBuf(size_t(R) * D * 4);
+            ly.m1 = DevBuf(size_t(R) * 4);
+            ly.r1 = DevBuf(size_t(R) * 4);
+            ly.m2 = DevBuf(size_t(R) * 4);
+            ly.r2 = DevBuf(size_t(R) * 4);
+            ly.u1 = make_cbuf(0, R, D + 1);
+            ly.u2 = make_cbuf(0, R, D + 1);
+            ly.attn = make_cbuf(0, R, D + 1);
+            ones(ly.attn, R, D);
+            ly.g1 = make_cbuf(0, R, F + 1);
+            ones(ly.g1, R, F);
+            ly.qkvb = make_cbuf(0, R, 3 * D);
+            ly.z1 = make_cbuf(0, R, F);
+            ly.P = DevBuf(size_t(B) * H * T * ldp * 2);
+            ly.dhc = make_cbuf(0, R, D);
+            ly.dz1 = make_cbuf(0, R, F);
+            ly.dhmc = make_cbuf(0, R, D);
+            ly.dqkv = make_cbuf(0, R, 3 * D);
+            for (DevBuf *g : {&ly.dg1, &ly.db1, &ly.dg2, &ly.db2}) *g = DevBuf(size_t(D) * 4);
+        }
+        hL = DevBuf(size_t(R) * D * 4);
+        mf = DevBuf(size_t(B) * 4);
+        rf = DevBuf(size_t(B) * 4);
+        uf = make_cbuf(0, B, D + 1);
+        z = DevBuf(size_t(B) * classes * 4);
+        dz = make_cbuf(0, B, classes);
+        loss_dev = DevBuf(8);
+        loss_rows = DevBuf(size_t(B) * 8);
+        S = DevBuf(size_t(B) * H * T * lds * 4);
+        dP = DevBuf(size_t(B) * H * T * lds * 4);
+        dS = make_cbuf(0, B * H * T, T);  // ld = ldp
+        du = DevBuf(size_t(R) * D * 4);
+        duf = DevBuf(size_t(B) * D * 4);
+        dh = DevBuf(size_t(R) * D * 4);
+        dhm = DevBuf(size_t(R) * D * 4);
+        dattn = make_cbuf(0, R, D);
+        gpos = DevBuf(size_t(T) * D * 4);
+        gcls = DevBuf(size_t(D) * 4);
+        dE = make_cbuf(0, B * NP, D);
+        lnpart = DevBuf(size_t(D) * ((R + kLnRows - 1) / kLnRows) * 16);
+        dgf = DevBuf(size_t(D) * 4);
+        dbf = DevBuf(size_t(D) * 4);
+        // ---- shared region: RingFlags | theta0 | theta1 | partial | momentum
+        region_off = (sizeof(RingFlags) + 255) / 256 * 256;
+        Pp = (Pn + 63) / 64 * 64;
+        region = DevBuf(region_off + size_t(Pp) * 4 * (momentum != 0.f ? 4 : 3));
+        ring = region.as<RingFlags>();
+        theta[0] = reinterpret_cast<float *>(region.as<uint8_t>() + region_off);
+        theta[1] = theta[0] + Pp;
+        partial = theta[1] + Pp;
+        if (momentum != 0.f) vel = partial + Pp;
+        cta_counters = DevBuf(2 * kMaxStages * 4);
+        for (int v = 0; v < 2; ++v)
+            for (auto &u : units) wc[v].push_back(u.kind == V_LIN ? make_cbuf(0, u.rows, u.cols) : CBuf{});
+        CDP_CUDA(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
+        CDP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CDP_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+        ctrl_dev = DevBuf(sizeof(Control));
+        perm_dev = DevBuf(size_t(B) * 4);
+        flags_dev = DevBuf(sizeof(Flags));
+        hist_loss = DevBuf(size_t(hist_cap) * 8);
+        hist_flags = DevBuf(size_t(hist_cap) * sizeof(Flags));
+        stage_bytes = (sizeof(Control) + size_t(B) * 4 + 255) / 256 * 256;
+        CDP_CUDA(cudaMallocHost(&stage_host, stage_bytes * RING_N));
+        for (auto &e : stage_ev) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cnt_c = DevBuf(1 << 18);
+        cnt_h = DevBuf(1 << 18);
+        sizing = true;
+        record_step(0);
+        sizing = false;
+        for (auto e : events) cudaEventDestroy(e);
+        events.clear();
+        ws_c = DevBuf(std::max<size_t>(ws_c_floats, 1) * 4);
+        ws_h = DevBuf(std::max<size_t>(ws_h_floats, 1) * 4);
+    }
+
+    // ---------------------------------------------------------------- GEMMs
+    float *ws_for(bool hop) {
+        if (sizing) return reinterpret_cast<float *>(uintptr_t(256));
+        return hop ? ws_h.as<float>() : ws_c.as<float>();
+    }
+
+    template <int BNc, bool AMN, bool BMN, class Epi, int MODE>
+    void run_pk(const char *name, double flops, const GemmPlan &gp, const typename Epi::Params &ep_in, cudaStream_t s,
+                bool hop, int nh = 1, int nb = 1, int64_t out_bs = 0, int64_t out_hs = 0) {
+        using Cfg = PkCfg<0, BNc, AMN, BMN, Epi::kStages>;
+        PkArgs a{};
+        a.M = gp.args.M;
+        a.N = gp.args.N;
+        a.tiles_m = int(gp.grid.x);
+        a.tiles_n = int(gp.grid.y);
+        a.kb_per_seg = gp.args.kb_per_seg;
+        a.n_seg = gp.args.n_seg;
+        a.total_iters = a.kb_per_seg * a.n_seg;
+        a.nbatch = nh * nb;
+        a.nh = nh;
+        a.out_bs = out_bs;
+        a.out_hs = out_hs;
+        const int tiles = a.tiles_m * a.tiles_n * a.nbatch;
+        int splits = 1;
+        if (MODE != GM_BATCH && tiles < sms()) splits = std::max(1, std::min(sms() / tiles, a.total_iters / 4));
+        a.iters_per_split = (a.total_iters + splits - 1) / splits;
+        a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
+        a.units = tiles * a.splits;
+        const typename Epi::Params ep = a.splits > 1 ? Epi::for_split(ep_in) : ep_in;
+        const size_t need = a.splits > 1 ? size_t(tiles) * a.splits * 128 * BNc : 0;
+        size_t &cap = hop ? ws_h_floats : ws_c_floats;
+        if (sizing) {
+            cap = std::max(cap, need);
+            return;
+        }
+        CDP_REQUIRE(need <= cap, "split-K workspace too small");
+        a.ws = ws_for(hop);
+        auto kern = gemm_pk_kernel<0, BNc, AMN, BMN, Epi, MODE>;
+        static bool attr = false;
+        if (!attr) {
+            CDP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+            attr = true;
+        }
+        const int grid = std::min(a.units, sms());
+        L_(name, flops, 0.0, s, [&] { launch_pdl(kern, dim3(grid), dim3(kPkThreads), Cfg::SMEM, s, gp.maps, a, ep); });
+        if (a.splits > 1) {
+            constexpr bool kStats = std::is_same<Epi, EpiConvOut2<0>>::value;
+            constexpr int RC = kStats ? 128 : 4;
+            constexpr int CC = kStats ? 32 : (BNc < 64 ? BNc : 64);
+            L_("splitk_reduce", 0, double(need) * 4, s, [&] {
+                launch_pdl(pk_reduce_kernel<BNc, Epi, RC, CC>, dim3(tiles, 128 / RC, BNc / CC), dim3(256), 0, s, a,
+                           ep);
+            });
+        }
+    }
+
+    static Operand opnd(const void *ptr, bool mn, int64_t mn_ext, int64_t k_ext, int64_t ld) {
+        return Operand{ptr, mn, uint64_t(mn_ext), uint64_t(k_ext), uint64_t(ld)};
+    }
+
+    // D[M,N] = A . B with plain 2-D operands (bf16).
+    template <bool AMN, bool BMN, class Epi>
+    void gemm(const char *name, const Operand &A, const Operand &Bo, int64_t M, int64_t N, int64_t Kd,
+              const typename Epi::Params &ep, cudaStream_t s, bool hop) {
+        bn_switch(tile_n(int(N)), [&](auto bnc) {
+            constexpr int BNc = decltype(bnc)::value;
+            if constexpr (BNc >= 64) {
+                GemmPlan p = plan_gemm<0, BNc, AMN, BMN>(&A, &Bo, 1, int(M), int(N), int(Kd), 1, nullptr, nullptr);
+                run_pk<BNc, AMN, BMN, Epi, GM_PLAIN>(name, 2.0 * M * N * Kd, p, ep, s, hop);
+            } else {
+                throw CdpError("unsupported GEMM tile width");
+            }
+        });
+    }
+
+    // Batched GEMM over (head, sample): operands are 4-D views {inner, rows, heads, samples}.
+    template <bool AMN, bool BMN>
+    void bgemm(const char *name, const BView &A, const BView &Bv, int M, int N, int K, void *out, int ld_out,
+               int64_t out_bs, int64_t out_hs, int out_f32, cudaStream_t s) {
+        bn_switch(tile_n(N), [&](auto bnc) {
+            constexpr int BNc = decltype(bnc)::value;
+            if constexpr (BNc >= 64) {
+                using Cfg = PkCfg<0, BNc, AMN, BMN, 0>;
+                GemmPlan p{};
+                std::memset(&p.maps, 0, sizeof(p.maps));
+                auto mk = [&](const BView &v, bool mn, int box_rows) {
+                    const uint64_t dims[4] = {uint64_t(v.inner), uint64_t(v.rows), uint64_t(H), uint64_t(B)};
+                    const uint64_t st[3] = {uint64_t(v.ld) * 2, uint64_t(v.hs) * 2, uint64_t(v.bs) * 2};
+                    const uint32_t box[4] = {64u, uint32_t(mn ? Cfg::BK : box_rows), 1u, 1u};
+                    const uint32_t es[4] = {1u, 1u, 1u, 1u};
+                    return make_tmap_4d(v.ptr, ElemType::BF16, dims, st, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
+                };
+                p.maps.a[0] = mk(A, AMN, 128);
+                p.maps.b[0] = mk(Bv, BMN, BNc);
+                p.args.M = M;
+                p.args.N = N;
+                p.args.kb_per_seg = (K + Cfg::BK - 1) / Cfg::BK;
+                p.args.n_seg = 1;
+                p.grid = dim3((M + 127) / 128, (N + BNc - 1) / BNc, 1);
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = out;
+                ep.ld = ld_out;
+                ep.out_f32 = out_f32;
+                run_pk<BNc, AMN, BMN, EpiConvOut2<0>, GM_BATCH>(name, 2.0 * M * N * K * H * B, p, ep, s, false, H, B,
+                                                                 out_bs, out_hs);
+            } else {
+                throw CdpError("unsupported batched GEMM tile width");
+            }
+        });
+    }
+
+    // ---------------------------------------------------------------- plumbing
+    cudaEvent_t ev(cudaStream_t s) {
+        cudaEvent_t e;
+        CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        events.push_back(e);
+        if (!sizing) CDP_CUDA(cudaEventRecord(e, s));
+        return e;
+    }
+    void wait(cudaStream_t s, cudaEvent_t e) {
+        if (!sizing) CDP_CUDA(cudaStreamWaitEvent(s, e, 0));
+    }
+    bool last_updater() const { return rank == world - 1; }
+    int vs(int unit, int p) const { return units[unit].fresh ? p : (p ^ 1); }
+    const float *th(int unit, int p) const { return theta[vs(unit, p)] + units[unit].base; }
+    const CBuf &W(int unit, int p) const { return wc[vs(unit, p)][unit]; }
+
+    HopParams hop_params(int unit, int p) {
+        const VUnit &u = units[unit];
+        HopParams hp{};
+        hp.mode = world == 1 ? 3 : (rank == 0 ? 0 : rank == world - 1 ? 2 : 1);
+        hp.stage = unit + 1;
+        hp.base = u.base;
+        hp.din = u.rows;
+        hp.dout = u.cols;
+        hp.s_in = rank > 0 ? prev_partial : partial;
+        hp.s_out = partial;
+        hp.theta_cur = theta[p];
+        hp.theta_new = theta[p ^ 1];
+        hp.vel = vel;
+        hp.lr = &ctrl_dev.as<Control>()->lr;
+        hp.momentum = momentum;
+        hp.wd = wd;
+        hp.n_mb = float(world);
+        hp.wc_new = u.kind == V_LIN ? wc[p ^ 1][unit].view() : CTensor{};
+        Flags *fl = flags_dev.as<Flags>();
+        hp.grad_flags = &fl->grad;
+        hp.upd_flags = &fl->upd;
+        hp.sync.enabled = 1;
+        hp.sync.n_readers = world - 1;
+        hp.sync.step = &ctrl_dev.as<Control>()->step;
+        hp.sync.own = ring;
+        hp.sync.prev = prev_ring;
+        hp.sync.cta_counter = cta_counters.as<unsigned>();
+        hp.sync.pre_external = 1;
+        return hp;
+    }
+    void hop_wait(const HopParams &hp, cudaStream_t s) {
+        if (world == 1 || hp.mode >= 3) return;
+        L_("hop_wait", 0, 0, s, [&] {
+            hop_wait_kernel<<<1, 128, 0, s>>>(hp);
+            CDP_CUDA(cudaGetLastError());
+        });
+    }
+    void pull(int unit, int p, cudaStream_t s) {
+        if (rank == world - 1 || world == 1 || sizing) return;
+        const VUnit &u = units[unit];
+        const int vslot = vs(unit, p);
+        CTensor w = u.kind == V_LIN ? wc[vslot][unit].view() : CTensor{};
+        L_("pull_wait", 0, 0, s, [&] {
+            pull_wait_kernel<<<1, 32, 0, s>>>(upd_ring, ring, unit + 1, u.fresh,
+                                              (const int *)&ctrl_dev.as<Control>()->step);
+            CDP_CUDA(cudaGetLastError());
+        });
+        L_("pull", 0, double(u.n) * 10, s, [&] {
+            launch_pdl(pull_tensor_kernel<0>, dim3(blocks_for(u.n, 1024)), dim3(256), 0, s,
+                       (const float *)(upd_theta[vslot] + u.base), theta[vslot] + u.base, u.n, std::max(u.cols, 1),
+                       w, upd_ring, ring, unit + 1, u.fresh, (const int *)&ctrl_dev.as<Control>()->step,
+                       cta_counters.as<unsigned>() + kMaxStages);
+        });
+    }
+
+    // Weight gradient of a linear unit fused with its hop / update: [A, 1]^T . dY on the hop stream.
+    void lin_hop(int unit, int p, const CTensor &a_in, int64_t krows, const CTensor &dy, cudaEvent_t dy_ready,
+                 cudaEvent_t dgrad_done) {
+        const VUnit &u = units[unit];
+        wait(hs, dy_ready);
+        if (dgrad_done && !u.fresh && last_updater()) wait(hs, dgrad_done);
+        HopParams hp = hop_params(unit, p);
+        hop_wait(hp, hs);
+        gemm<true, true, EpiHop2<0>>("lin_wgrad_hop", opnd(a_in.hi, true, u.rows, krows, a_in.ld),
+                                     opnd(dy.hi, true, u.cols, krows, dy.ld), u.rows, u.cols, krows, hp, hs, true);
+    }
+    void ln_hop(int unit, int p, const float *dg, const float *db, cudaEvent_t ready) {
+        wait(hs, ready);
+        HopParams hp = hop_params(unit, p);
+        hop_wait(hp, hs);
+        L_("ln_hop", 0, double(D) * 2 * 24, hs, [&] {
+            launch_pdl(vector_hop_kernel, dim3(1), dim3(128), 0, hs, hp, dg, db, D);
+        });
+    }
+
+    // ---------------------------------------------------------------- layers
+    void layernorm(const float *x, int rows, int stride, int unit, int p, const CTensor &out, float *mean,
+                   float *rstd, cudaStream_t s) {
+        L_("ln_fwd", 0, double(rows) * D * 6, s, [&] {
+            launch_pdl(ln_fwd_kernel<0>, dim3((rows * 32 + 255) / 256), dim3(256), 0, s, x, rows, stride, D,
+                       th(unit, p), eps, out, mean, rstd);
+        });
+    }
+    // LayerNorm backward of `unit`: dh_out = dh_in + LN'(g); parameter gradients -> dgam / dbet.
+    void layernorm_bwd(const float *g, const float *x, int rows, int stride, int unit, int p, const float *mean,
+                       const float *rstd, const float *dh_in, float *dh_out, float *dgam, float *dbet,
+                       cudaStream_t s) {
+        L_("ln_bwd", 0, double(rows) * D * 16, s, [&] {
+            launch_pdl(ln_bwd_kernel, dim3((rows * 32 + 255) / 256), dim3(256), 0, s, g, x, rows, stride, D,
+                       th(unit, p), mean, rstd, dh_in, dh_out);
+        });
+        const int nblk = (rows + kLnRows - 1) / kLnRows;
+        L_("ln_param_grad", 0, double(rows) * D * 8, s, [&] {
+            launch_pdl(ln_param_partial_kernel, dim3(nblk), dim3(256), 0, s, g, x, rows, stride, D, mean, rstd,
+                       lnpart.as<double>());
+        });
+        L_("ln_param_finalize", 0, double(nblk) * D * 16, s, [&] {
+            launch_pdl(bn_finalize_bwd_kernel, dim3((D * 32 + 255) / 256), dim3(256), 0, s,
+                       (const double *)lnpart.as<double>(), nblk, D, dbet, dgam);
+        });
+    }
+
+    void forward(int p, cudaStream_t s) {
+        // patch embedding + tokens
+        pull(u_patch, p, s);
+        pull(u_cls, p, s);
+        pull(u_pos, p, s);
+        const int K0 = P * P * 3;
+        L_("patch_im2col", 0, double(B) * NP * patches.ld * 2, s, [&] {
+            launch_pdl(patch_im2col_kernel<0>, dim3(blocks_for(int64_t(B) * NP * patches.ld)), dim3(256), 0, s,
+                       (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), img, P, G, B * NP,
+                       patches.view());
+        });
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = E.p;
+            ep.ld = D;
+            ep.out_f32 = 1;
+            const CBuf &w = W(u_patch, p);
+            gemm<false, true, EpiConvOut2<0>>("patch_embed", opnd(patches.hi.p, false, B * NP, K0 + 1, patches.ld),
+                                              opnd(w.hi.p, true, D, K0 + 1, w.ld), B * NP, D, K0 + 1, ep, s, false);
+        }
+        L_("embed_assemble", 0, double(R) * D * 12, s, [&] {
+            launch_pdl(embed_assemble_kernel, dim3(blocks_for(int64_t(R) * D)), dim3(256), 0, s,
+                       (const float *)E.as<float>(), th(u_cls, p), th(u_pos, p), B, T, D, layers[0].h.as<float>());
+        });
+        const float scale = 1.f / std::sqrt(float(HD));
+        for (int l = 0; l < L; ++l) {
+            VLayer &y = layers[l];
+            float *hout = l + 1 < L ? layers[l + 1].h.as<float>() : hL.as<float>();
+            for (int u : {y.ln1, y.qkv, y.proj, y.ln2, y.fc1, y.fc2}) pull(u, p, s);
+            layernorm(y.h.as<float>(), R, 1, y.ln1, p, y.u1.view(), y.m1.as<float>(), y.r1.as<float>(), s);
+            {
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = y.qkvb.hi.p;
+                ep.ld = y.qkvb.ld;
+                const CBuf &w = W(y.qkv, p);
+                gemm<false, true, EpiConvOut2<0>>("qkv", opnd(y.u1.hi.p, false, R, D + 1, y.u1.ld),
+                                                  opnd(w.hi.p, true, 3 * D, D + 1, w.ld), R, 3 * D, D + 1, ep, s,
+                                                  false);
+            }
+            // attention: S = Q K^T (fp32) -> P = softmax(scale S) (bf16) -> O = P V
+            const int64_t qld = y.qkvb.ld;
+            const BView Q{y.qkvb.hi.p, HD, T, qld, HD, int64_t(T) * qld};
+            const BView Kv{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + D, HD, T, qld, HD, int64_t(T) * qld};
+            const BView V{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + 2 * D, HD, T, qld, HD, int64_t(T) * qld};
+            const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+            bgemm<false, false>("attn_scores", Q, Kv, T, T, HD, S.p, lds, int64_t(H) * T * lds, int64_t(T) * lds, 1,
+                                s);
+            L_("softmax", 0, double(B) * H * T * T * 6, s, [&] {
+                launch_pdl(softmax_fwd_kernel, dim3((B * H * T * 32 + 255) / 256), dim3(256), 0, s,
+                           (const float *)S.as<float>(), B * H * T, T, lds, scale, y.P.as<__nv_bfloat16>(), ldp);
+            });
+            bgemm<false, true>("attn_values", Pv, V, T, HD, T, y.attn.hi.p, y.attn.ld, int64_t(T) * y.attn.ld, HD, 0,
+                               s);
+            {
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = y.hmid.p;
+                ep.ld = D;
+                ep.out_f32 = 1;
+                ep.add = y.h.p;
+                const CBuf &w = W(y.proj, p);
+                gemm<false, true, EpiConvOut2<0>>("proj", opnd(y.attn.hi.p, false, R, D + 1, y.attn.ld),
+                                                  opnd(w.hi.p, true, D, D + 1, w.ld), R, D, D + 1, ep, s, false);
+            }
+            layernorm(y.hmid.as<float>(), R, 1, y.ln2, p, y.u2.view(), y.m2.as<float>(), y.r2.as<float>(), s);
+            {
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = y.z1.hi.p;
+                ep.ld = y.z1.ld;
+                ep.gelu_out = y.g1.view();
+                const CBuf &w = W(y.fc1, p);
+                gemm<false, true, EpiConvOut2<0>>("fc1_gelu", opnd(y.u2.hi.p, false, R, D + 1, y.u2.ld),
+                                                  opnd(w.hi.p, true, F, D + 1, w.ld), R, F, D + 1, ep, s, false);
+            }
+            {
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = hout;
+                ep.ld = D;
+                ep.out_f32 = 1;
+                ep.add = y.hmid.p;
+                const CBuf &w = W(y.fc2, p);
+                gemm<false, true, EpiConvOut2<0>>("fc2", opnd(y.g1.hi.p, false, R, F + 1, y.g1.ld),
+                                                  opnd(w.hi.p, true, D, F + 1, w.ld), R, D, F + 1, ep, s, false);
+            }
+        }
+        // head on the class token
+        pull(u_ln, p, s);
+        pull(u_head, p, s);
+        layernorm(hL.as<float>(), B, T, u_ln, p, uf.view(), mf.as<float>(), rf.as<float>(), s);
+        typename EpiConvOut2<0>::Params ep{};
+        ep.out = z.p;
+        ep.ld = classes;
+        ep.out_f32 = 1;
+        const CBuf &w = W(u_head, p);
+        gemm<false, true, EpiConvOut2<0>>("head", opnd(uf.hi.p, false, B, D + 1, uf.ld),
+                                          opnd(w.hi.p, true, classes, D + 1, w.ld), B, classes, D + 1, ep, s, false);
+    }
+
+    void cast(const float *in, int rows, int per, int in_per, int skip, const CTensor &out, cudaStream_t s) {
+        L_("cast", 0, double(rows) * D * 6, s, [&] {
+            launch_pdl(cast_rows_kernel<0>, dim3(blocks_for(int64_t(rows) * D)), dim3(256), 0, s, in, rows, D, per,
+                       in_per, skip, out);
+        });
+    }
+
+    void record_step(int p) {
+        kernels_per_step = 0;
+        flops_per_step = 0.0;
+        cudaEvent_t fork = ev(main);
+        wait(cs, fork);
+        wait(hs, fork);
+        forward(p, cs);
+        // loss
+        Flags *fl = flags_dev.as<Flags>();
+        const int nt = std::max(32, round_up(B, 32));
+        const size_t lsm = sizeof(double) * nt + sizeof(float) * B * classes;
+        if (classes <= 64 && lsm <= 48 * 1024) {
+            L_("loss", 0, 0, cs, [&] {
+                launch_pdl(loss_kernel<0>, dim3(1), dim3(nt), lsm, cs, (const float *)z.as<float>(), B, classes,
+                           loss_kind, (const int *)perm_dev.as<int>(), (const int *)data_lab.as<int>(),
+                           (const float *)nullptr, dz.view(), loss_dev.as<double>(), &fl->loss);
+            });
+        } else {
+            L_("loss", 0, 0, cs, [&] {
+                launch_pdl(xent_rows_kernel<0>, dim3(B), dim3(256), 0, cs, (const float *)z.as<float>(), B, classes,
+                           (const int *)perm_dev.as<int>(), (const int *)data_lab.as<int>(), dz.view(),
+                           loss_rows.as<double>());
+            });
+            L_("loss_sum", 0, 0, cs, [&] {
+                launch_pdl(loss_sum_kernel, dim3(1), dim3(1), 0, cs, (const double *)loss_rows.as<double>(), B,
+                           loss_dev.as<double>(), &fl->loss);
+            });
+        }
+        cudaEvent_t dz_ready = ev(cs);
+        // head: data gradient (fp32) and weight gradient + hop
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = duf.p;
+            ep.ld = D;
+            ep.out_f32 = 1;
+            const CBuf &w = W(u_head, p);
+            gemm<false, false, EpiConvOut2<0>>("head_dgrad", opnd(dz.hi.p, false, B, classes, dz.ld),
+                                               opnd(w.hi.p, false, D, classes, w.ld), B, D, classes, ep, cs, false);
+        }
+        cudaEvent_t head_dg = ev(cs);
+        lin_hop(u_head, p, uf.view(), B, dz.view(), dz_ready, head_dg);
+        // final LayerNorm (class-token rows only): dh = 0 elsewhere
+        if (!sizing) CDP_CUDA(cudaMemsetAsync(dh.p, 0, dh.bytes, cs));
+        layernorm_bwd(duf.as<float>(), hL.as<float>(), B, T, u_ln, p, mf.as<float>(), rf.as<float>(), nullptr,
+                      dh.as<float>(), dgf.as<float>(), dbf.as<float>(), cs);
+        ln_hop(u_ln, p, dgf.as<float>(), dbf.as<float>(), ev(cs));
+        const float scale = 1.f / std::sqrt(float(HD));
+        for (int l = L - 1; l >= 0; --l) {
+            VLayer &y = layers[l];
+            // ---- MLP
+            cast(dh.as<float>(), R, 1, 1, 0, y.dhc.view(), cs);
+            cudaEvent_t dhc_ready = ev(cs);
+            {
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = y.dz1.hi.p;
+                ep.ld = y.dz1.ld;
+                ep.gelu_z = y.z1.hi.p;
+                const CBuf &w = W(y.fc2, p);
+                gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(y.dhc.hi.p, false, R, D, y.dhc.ld),
+                                                   opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
+            }
+            cudaEvent_t dz1_ready = ev(cs);
+            lin_hop(y.fc2, p, y.g1.view(), R, y.dhc.view(), dhc_ready, dz1_ready);
+            {
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = du.p;
+                ep.ld = D;
+                ep.out_f32 = 1;
+                const CBuf &w = W(y.fc1, p);
+                gemm<false, false, EpiConvOut2<0>>("fc1_dgrad", opnd(y.dz1.hi.p, false, R, F, y.dz1.ld),
+                                                   opnd(w.hi.p, false, D, F, w.ld), R, D, F, ep, cs, false);
+            }
+            cudaEvent_t fc1_dg = ev(cs);
+            lin_hop(y.fc1, p, y.u2.view(), R, y.dz1.view(), dz1_ready, fc1_dg);
+            layernorm_bwd(du.as<float>(), y.hmid.as<float>(), R, 1, y.ln2, p, y.m2.as<float>(), y.r2.as<float>(),
+                          dh.as<float>(), dhm.as<float>(), y.dg2.as<float>(), y.db2.as<float>(), cs);
+            ln_hop(y.ln2, p, y.dg2.as<float>(), y.db2.as<float>(), ev(cs));
+            // ---- attention
+            cast(dhm.as<float>(), R, 1, 1, 0, y.dhmc.view(), cs);
+            cudaEvent_t dhmc_ready = ev(cs);
+            {
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = dattn.hi.p;
+                ep.ld = dattn.ld;
+                const CBuf &w = W(y.proj, p);
+                gemm<false, false, EpiConvOut2<0>>("proj_dgrad", opnd(y.dhmc.hi.p, false, R, D, y.dhmc.ld),
+                                                   opnd(w.hi.p, false, D, D, w.ld), R, D, D, ep, cs, false);
+            }
+            cudaEvent_t proj_dg = ev(cs);
+            lin_hop(y.proj, p, y.attn.view(), R, y.dhmc.view(), dhmc_ready, proj_dg);
+            const int64_t qld = y.qkvb.ld;
+            auto qv = [&](int col) {
+                return BView{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + col, HD, T, qld, HD, int64_t(T) * qld};
+            };
+            const BView dO{dattn.hi.p, HD, T, dattn.ld, HD, int64_t(T) * dattn.ld};
+            const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+            const BView dSv{dS.hi.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+            bgemm<false, false>("attn_dprobs", dO, qv(2 * D), T, T, HD, dP.p, lds, int64_t(H) * T * lds,
+                                int64_t(T) * lds, 1, cs);
+            L_("softmax_bwd", 0, double(B) * H * T * T * 8, cs, [&] {
+                launch_pdl(softmax_bwd_kernel, dim3((B * H * T * 32 + 255) / 256), dim3(256), 0, cs,
+                           (const float *)dP.as<float>(), (const __nv_bfloat16 *)y.P.as<__nv_bfloat16>(), B * H * T,
+                           T, lds, ldp, scale, static_cast<__nv_bfloat16 *>(dS.hi.p));
+            });
+            __nv_bfloat16 *dq = static_cast<__nv_bfloat16 *>(y.dqkv.hi.p);
+            const int64_t dld = y.dqkv.ld;
+            bgemm<true, true>("attn_dvalues", Pv, dO, T, HD, T, dq + 2 * D, int(dld), int64_t(T) * dld, HD, 0, cs);
+            bgemm<false, true>("attn_dquery", dSv, qv(D), T, HD, T, dq, int(dld), int64_t(T) * dld, HD, 0, cs);
+            bgemm<true, true>("attn_dkey", dSv, qv(0), T, HD, T, dq + D, int(dld), int64_t(T) * dld, HD, 0, cs);
+            cudaEvent_t dqkv_ready = ev(cs);
+            {
+                typename EpiConvOut2<0>::Params ep{};
+                ep.out = du.p;
+                ep.ld = D;
+                ep.out_f32 = 1;
+                const CBuf &w = W(y.qkv, p);
+                gemm<false, false, EpiConvOut2<0>>("qkv_dgrad", opnd(y.dqkv.hi.p, false, R, 3 * D, dld),
+                                                   opnd(w.hi.p, false, D, 3 * D, w.ld), R, D, 3 * D, ep, cs, false);
+            }
+            cudaEvent_t qkv_dg = ev(cs);
+            lin_hop(y.qkv, p, y.u1.view(), R, y.dqkv.view(), dqkv_ready, qkv_dg);
+            layernorm_bwd(du.as<float>(), y.h.as<float>(), R, 1, y.ln1, p, y.m1.as<float>(), y.r1.as<float>(),
+                          dhm.as<float>(), dh.as<float>(), y.dg1.as<float>(), y.db1.as<float>(), cs);
+            ln_hop(y.ln1, p, y.dg1.as<float>(), y.db1.as<float>(), ev(cs));
+        }
+        // ---- embeddings
+        L_("token_grad", 0, double(R) * D * 4, cs, [&] {
+            launch_pdl(token_grad_kernel, dim3(blocks_for(int64_t(T) * D)), dim3(256), 0, cs,
+                       (const float *)dh.as<float>(), B, T, D, gpos.as<float>(), gcls.as<float>());
+        });
+        cast(dh.as<float>(), B * NP, NP, T, 1, dE.view(), cs);
+        cudaEvent_t emb_ready = ev(cs);
+        wait(hs, emb_ready);
+        for (int u : {u_pos, u_cls}) {
+            HopParams hp = hop_params(u, p);
+            hop_wait(hp, hs);
+            const float *g = u == u_pos ? gpos.as<float>() : gcls.as<float>();
+            L_("vec_hop", 0, double(units[u].n) * 24, hs, [&] {
+                launch_pdl(flat_hop_kernel, dim3(blocks_for(units[u].n, 1024)), dim3(256), 0, hs, hp, g,
+                           units[u].n);
+            });
+        }
+        lin_hop(u_patch, p, patches.view(), B * NP, dE.view(), emb_ready, nullptr);
+        // join + bookkeeping
+        wait(main, ev(cs));
+        wait(main, ev(hs));
+        L_("finish_step", 0, 0, main, [&] {
+            finish_step_kernel_rn<<<1, 1, 0, main>>>(loss_dev.as<double>(), flags_dev.as<Flags>(),
+                                                     hist_loss.as<double>(), hist_flags.as<Flags>(), hist_cap,
+                                                     &ctrl_dev.as<Control>()->step);
+            CDP_CUDA(cudaGetLastError());
+        });
+    }
+
+    void capture() {
+        for (auto &e : exec)
+            if (e) {
+                CDP_CUDA(cudaGraphExecDestroy(e));
+                e = nullptr;
+            }
+        for (auto e : events) cudaEventDestroy(e);
+        events.clear();
+        for (int p = 0; p < 2; ++p) {
+            cudaGraph_t g;
+            CDP_CUDA(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
+            try {
+                record_step(p);
+            } catch (...) {
+                cudaEvent_t a, b;
+                cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+                cudaEventRecord(a, cs);
+                cudaEventRecord(b, hs);
+                cudaStreamWaitEvent(main, a, 0);
+                cudaStreamWaitEvent(main, b, 0);
+                if (cudaStreamEndCapture(main, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+                cudaGetLastError();
+                throw;
+            }
+            CDP_CUDA(cudaStreamEndCapture(main, &g));
+            CDP_CUDA(cudaGraphInstantiate(&exec[p], g, 0));
+            CDP_CUDA(cudaGraphDestroy(g));
+        }
+    }
+
+    // ---------------------------------------------------------------- params / steps
+    void pack_slot(int slot) {
+        for (size_t i = 0; i < units.size(); ++i) {
+            const VUnit &u = units[i];
+            if (u.kind != V_LIN) continue;
+            pack_tensor_kernel<0><<<blocks_for(u.n), 256, 0, main>>>(theta[slot] + u.base, u.n, u.cols,
+                                                                     wc[slot][i].view());
+            CDP_CUDA(cudaGetLastError());
+        }
+    }
+    void set_params(int which, const float *host) {
+        for (int v = 0; v < 2; ++v) {
+            if (which >= 0 && v != which) continue;
+            const int slot = v == 0 ? (t & 1) : ((t & 1) ^ 1);
+            CDP_CUDA(cudaMemcpyAsync(theta[slot], host, size_t(Pn) * 4, cudaMemcpyHostToDevice, main));
+            pack_slot(slot);
+        }
+        CDP_CUDA(cudaStreamSynchronize(main));
+    }
+    void get_params(int which, float *host) {
+        CDP_CUDA(cudaStreamSynchronize(main));
+        const int slot = which == 0 ? (t & 1) : ((t & 1) ^ 1);
+        CDP_CUDA(cudaMemcpy(host, theta[slot], size_t(Pn) * 4, cudaMemcpyDeviceToHost));
+    }
+    void stage_control(const int *perm, float lr) {
+        const int k = stage_next;
+        stage_next = (stage_next + 1) % RING_N;
+        CDP_CUDA(cudaEventSynchronize(stage_ev[k]));
+        uint8_t *blk = stage_host + size_t(k) * stage_bytes;
+        Control *c = reinterpret_cast<Control *>(blk);
+        c->lr = lr;
+        c->step = t;
+        std::memcpy(blk + sizeof(Control), perm, size_t(B) * 4);
+        CDP_CUDA(cudaMemcpyAsync(ctrl_dev.p, blk, sizeof(Control), cudaMemcpyHostToDevice, main));
+        CDP_CUDA(cudaMemcpyAsync(perm_dev.p, blk + sizeof(Control), size_t(B) * 4, cudaMemcpyHostToDevice, main));
+        CDP_CUDA(cudaEventRecord(stage_ev[k], main));
+    }
+    void step(const int *perm, float lr) {
+        stage_control(perm, lr);
+        CDP_CUDA(cudaGraphLaunch(exec[t & 1], main));
+        ++t;
+    }
+    void step_host_batch(const float *x, const int32_t *labels, float lr) {
+        const size_t im = size_t(img) * img * 3;
+        CDP_CUDA(cudaMemcpyAsync(data_x.p, x, size_t(B) * im * 4, cudaMemcpyHostToDevice, main));
+        CDP_CUDA(cudaMemcpyAsync(data_lab.p, labels, size_t(B) * 4, cudaMemcpyHostToDevice, main));
+        std::vector<int> ident(B);
+        for (int i = 0; i < B; ++i) ident[i] = i;
+        step(ident.data(), lr);
+    }
+    void profile_step(const int *perm, float lr, bool serial) {
+        stage_control(perm, lr);
+        clear_oprecs();
+        instr = true;
+        cudaStream_t sc = cs, sh = hs;
+        if (serial) cs = hs = main;
+        try {
+            record_step(t & 1);
+        } catch (...) {
+            instr = false;
+            cs = sc;
+            hs = sh;
+            throw;
+        }
+        cs = sc;
+        hs = sh;
+        instr = false;
+        ++t;
+        CDP_CUDA(cudaDeviceSynchronize());
+    }
+};
+
+}  // namespace cdp
+
+using namespace cdp;
+
+struct cdp_vit {
+    std::unique_ptr<VitTrainer> impl;
+};
+
+extern "C" int cdp_vit_create_rank(int image, int patch, int dim, int depth, int heads, int mlp, int classes,
+                                   int micro_batch, int world, int rank, const int32_t *unit_stage,
+                                   const uint8_t *stage_fresh, float momentum, float weight_decay, int n_samples,
+                                   const float *x, const int32_t *labels, cdp_vit **out) {
+    return guarded([&] {
+        CDP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
+        CDP_REQUIRE(micro_batch >= 1 && micro_batch <= 256, "micro-batch must be in [1, 256]");
+        CDP_REQUIRE(depth >= 1 && depth <= 40, "depth: 1..40");
+        auto tr = std::make_unique<VitTrainer>();
+        tr->B = micro_batch;
+        tr->img = image;
+        tr->P = patch;
+        tr->D = dim;
+        tr->L = depth;
+        tr->H = heads;
+        tr->F = mlp;
+        tr->classes = classes;
+        tr->momentum = momentum;
+        tr->wd = weight_decay;
+        tr->rank = rank;
+        tr->world = world;
+        tr->n_samples = std::max(n_samples, micro_batch);
+        const size_t im = size_t(image) * image * 3;
+        tr->data_x = DevBuf(size_t(tr->n_samples) * im * 4);
+        tr->data_lab = DevBuf(size_t(tr->n_samples) * 4);
+        if (x) CDP_CUDA(cudaMemcpy(tr->data_x.p, x, size_t(n_samples) * im * 4, cudaMemcpyHostToDevice));
+        if (labels) CDP_CUDA(cudaMemcpy(tr->data_lab.p, labels, size_t(n_samples) * 4, cudaMemcpyHostToDevice));
+        tr->build();
+        for (size_t i = 0; i < tr->units.size(); ++i) {
+            const int st = unit_stage[i];
+            CDP_REQUIRE(st >= 1 && st <= world, "unit stage out of range");
+            tr->units[i].stage = st;
+            tr->units[i].fresh = stage_fresh[st - 1] != 0;
+        }
+        *out = new cdp_vit{std::move(tr)};
+    });
+}
+
+extern "C" int cdp_vit_info(cdp_vit *tr, int64_t *n_params, int *n_units) {
+    return guarded([&] {
+        *n_params = tr->impl->Pn;
+        *n_units = int(tr->impl->units.size());
+    });
+}
+
+extern "C" int cdp_vit_region(cdp_vit *tr, void **base) {
+    return guarded([&] { *base = tr->impl->region.p; });
+}
+
+extern "C" int cdp_vit_ipc_handle(cdp_vit *tr, void *handle64) {
+    return guarded([&] {
+        cudaIpcMemHandle_t h;
+        CDP_CUDA(cudaIpcGetMemHandle(&h, tr->impl->region.p));
+        std::memcpy(handle64, &h, sizeof(h));
+    });
+}
+
+extern "C" int cdp_vit_connect(cdp_vit *tr, void *const *regions) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        auto at = [&](int r) { return static_cast<uint8_t *>(regions[r]); };
+        if (m.rank > 0) {
+            m.prev_ring = reinterpret_cast<RingFlags *>(at(m.rank - 1));
+            m.prev_partial = reinterpret_cast<float *>(at(m.rank - 1) + m.region_off) + 2 * m.Pp;
+        }
+        const int u = m.world - 1;
+        m.upd_ring = reinterpret_cast<RingFlags *>(at(u));
+        m.upd_theta[0] = reinterpret_cast<float *>(at(u) + m.region_off);
+        m.upd_theta[1] = m.upd_theta[0] + m.Pp;
+        m.capture();
+    });
+}
+
+extern "C" void cdp_vit_destroy(cdp_vit *tr) {
+    if (tr) {
+        cudaDeviceSynchronize();
+        delete tr;
+    }
+}
+
+extern "C" int cdp_vit_set_params(cdp_vit *tr, int which, const float *theta) {
+    return guarded([&] { tr->impl->set_params(which, theta); });
+}
+
+extern "C" int cdp_vit_get_params(cdp_vit *tr, int which, float *theta) {
+    return guarded([&] { tr->impl->get_params(which, theta); });
+}
+
+extern "C" int cdp_vit_step(cdp_vit *tr, const int32_t *perm, float lr) {
+    return guarded([&] { tr->impl->step(perm, lr); });
+}
+
+extern "C" int cdp_vit_step_host_batch(cdp_vit *tr, const float *x, const int32_t *labels, float lr) {
+    return guarded([&] { tr->impl->step_host_batch(x, labels, lr); });
+}
+
+extern "C" int cdp_vit_profile_step(cdp_vit *tr, const int32_t *perm, float lr, int serial, int max_ops, char *names,
+                                    int name_len, double *flops, double *bytes, float *ms, int *n_ops) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        m.profile_step(perm, lr, serial != 0);
+        const int n = std::min<int>(max_ops, int(m.oprecs.size()));
+        *n_ops = int(m.oprecs.size());
+        for (int i = 0; i < n; ++i) {
+            const auto &o = m.oprecs[i];
+            std::strncpy(names + size_t(i) * name_len, o.name.c_str(), name_len - 1);
+            names[size_t(i) * name_len + name_len - 1] = 0;
+            flops[i] = o.flops;
+            bytes[i] = o.bytes;
+            CDP_CUDA(cudaEventElapsedTime(&ms[i], o.a, o.b));
+        }
+    });
+}
+
+extern "C" int cdp_vit_history(cdp_vit *tr, int max, double *losses, uint32_t *flags, int *count) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        const int c = m.t - 1;
+        *count = c;
+        const int n = std::min({c, max, m.hist_cap});
+        std::vector<double> l(m.hist_cap);
+        std::vector<Flags> f(m.hist_cap);
+        CDP_CUDA(cudaMemcpy(l.data(), m.hist_loss.p, size_t(m.hist_cap) * 8, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemcpy(f.data(), m.hist_flags.p, size_t(m.hist_cap) * sizeof(Flags), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < n; ++i) {
+            const int k = (c - n + i) % m.hist_cap;
+            losses[i] = l[k];
+            flags[3 * i] = f[k].grad;
+            flags[3 * i + 1] = f[k].loss;
+            flags[3 * i + 2] = f[k].upd;
+        }
+    });
+}
+
+extern "C" int cdp_vit_sync(cdp_vit *tr) {
+    return guarded([&] { CDP_CUDA(cudaStreamSynchronize(tr->impl->main)); });
+}
+
+extern "C" int cdp_vit_ring_error(cdp_vit *tr, int *err) {
+    return guarded([&] {
+        CDP_CUDA(cudaStreamSynchronize(tr->impl->main));
+        uint32_t e = 0;
+        CDP_CUDA(cudaMemcpy(&e, &tr->impl->ring->err, 4, cudaMemcpyDeviceToHost));
+        *err = int(e);
+    });
+}
+
+extern "C" int cdp_vit_stats(cdp_vit *tr, int64_t *out, int n_out) {
+    // [0] activation bytes kept for the backward, [1] parameter-state bytes, [2] kernels / step,
+    // [3] tensor-core flops / step
+    return guarded([&] {
+        auto &m = *tr->impl;
+        int64_t act = int64_t(m.patches.hi.bytes + m.E.bytes + m.hL.bytes + m.uf.hi.bytes);
+        for (auto &y : m.layers)
+            act += int64_t(y.h.bytes + y.hmid.bytes + y.u1.hi.bytes + y.u2.hi.bytes + y.attn.hi.bytes + y.g1.hi.bytes +
+                           y.qkvb.hi.bytes + y.z1.hi.bytes + y.P.bytes + 4 * y.m1.bytes);
+        int64_t par = int64_t(m.Pp) * (m.vel ? 16 : 12);
+        for (int v = 0; v < 2; ++v)
+            for (auto &w : m.wc[v]) par += int64_t(w.hi.bytes);
+        int64_t vals[4] = {act, par, m.kernels_per_step, int64_t(m.flops_per_step)};
+        for (int i = 0; i < n_out && i < 4; ++i) out[i] = vals[i];
+    });
+}
+
+extern "C" int cdp_vit_mark(cdp_vit *tr, int k) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        while (int(m.marks.size()) <= k) {
+            cudaEvent_t e;
+            CDP_CUDA(cudaEventCreate(&e));
+            m.marks.push_back(e);
+        }
+        CDP_CUDA(cudaEventRecord(m.marks[k], m.main));
+    });
+}
+
+extern "C" int cdp_vit_elapsed(cdp_vit *tr, int a, int b, float *ms) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_CUDA(cudaEventSynchronize(m.marks[b]));
+        CDP_CUDA(cudaEventElapsedTime(ms, m.marks[a], m.marks[b]));
+    });
+}
+
+extern "C" int cdp_vit_flush_l2(cdp_vit *tr) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        if (!m.flush_buf.p) m.flush_buf = DevBuf(size_t(256) << 20);
+        CDP_CUDA(cudaMemsetAsync(m.flush_buf.p, m.t & 0xff, m.flush_buf.bytes, m.main));
+    });
+}
