@@ -340,6 +340,34 @@ def resnet_cfg(model):
     return dict(RESNET50), 224, 1000
 
 
+VIT_MB = 32  # BASELINE configs[3] / SURVEY §8d: ViT-B/16, B = 32
+
+
+def make_trainer(args, model, ws, rank, rule, allreduce, zero):
+    """(trainer, micro-batch, image side, classes, dataset x, labels) for a bench model."""
+    from paper_2403_08837_b200.resnet import DeviceResNet, init_params, layer_specs, synthetic_images
+
+    if model == "vit_b16":
+        from paper_2403_08837_b200.vit import VIT_B16, DeviceVit, vit_init
+
+        if allreduce or zero:
+            raise SystemExit("vit_b16: --rule dp-allreduce / --zero are built for the ResNets")
+        B = VIT_MB
+        x, y = synthetic_images(2 * B * ws, seed=0, hw=224, classes=1000)
+        tr = DeviceVit(VIT_B16, B, ws, rank, rule, RN_MOMENTUM, inputs=x, labels=y)
+        tr.set_params(vit_init(VIT_B16, seed=0), -1)
+        return tr, B, 224, 1000, x, y
+    cfg, hw, classes = resnet_cfg(model)
+    B = RN_MB
+    x, y = synthetic_images(2 * B * ws, seed=0, hw=hw, classes=classes)
+    specs = layer_specs(cfg["widths"], cfg["depths"], 3, hw, cfg["block"], cfg["stem"], classes)
+    tr = DeviceResNet(cfg["widths"], cfg["depths"], B, ws, rank, rule, args.dtype, RN_MOMENTUM, inputs=x, labels=y,
+                      classes=classes, image_hw=hw, block=cfg["block"], stem=cfg["stem"], zero=zero,
+                      dp_allreduce=allreduce)
+    tr.set_params(init_params(specs, seed=0), -1)
+    return tr, B, hw, classes, x, y
+
+
 def peak_tensor():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -368,18 +396,11 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     from paper_2403_08837_b200.resnet import DeviceResNet, init_params, layer_specs, synthetic_images
 
     torch.cuda.set_device(local % torch.cuda.device_count())  # (ranks may share a GPU in tests)
-    cfg, hw, classes = resnet_cfg(model)
-    B = RN_MB
     allreduce = args.rule == "dp-allreduce"
     rule = None if allreduce else resolve(args.rule, ws)
     zero = bool(getattr(args, "zero", False)) and ws > 1
-    n_data = 2 * B * ws
-    x, y = synthetic_images(n_data, seed=0, hw=hw, classes=classes)
-    specs = layer_specs(cfg["widths"], cfg["depths"], 3, hw, cfg["block"], cfg["stem"], classes)
-    tr = DeviceResNet(cfg["widths"], cfg["depths"], B, ws, rank, rule, args.dtype, RN_MOMENTUM, inputs=x, labels=y,
-                      classes=classes, image_hw=hw, block=cfg["block"], stem=cfg["stem"], zero=zero,
-                      dp_allreduce=allreduce)
-    tr.set_params(init_params(specs, seed=0), -1)
+    tr, B, hw, classes, x, y = make_trainer(args, model, ws, rank, rule, allreduce, zero)
+    n_data = x.shape[0]
     if ws > 1:
         tr.connect_ipc(exchange_handles(tr.ipc_handle()))
     else:
@@ -434,7 +455,7 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
            "activation_bytes": {"per_gpu": st["activation_bytes"], "sum_over_gpus": st["activation_bytes"] * ws},
            "param_state_bytes": st["param_state_bytes"], "gpu_launches": st["kernels_per_step"] * steps,
            "tensor_flops_per_step": st["tensor_flops_per_step"],
-           "zero_state_bytes_per_step": st["zero_state_bytes_per_step"],
+           "zero_state_bytes_per_step": st.get("zero_state_bytes_per_step", 0),
            "tensor_tflops_per_s": round(st["tensor_flops_per_step"] / (ms / 1e3) / 1e12, 1)}
     # ---- e2e: public API, pinned host images copied H2D every step, loss read back every step
     if e2e:
@@ -498,6 +519,16 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     return out
 
 
+def vit_activation_model(res, n=4):
+    """configs[3] reading: single-GPU CDP over N sequential micro-batches keeps (N+1)/2 micro-batches of
+    activations alive vs N for DP (ref costs.py:111-115, cross-checked by tests/test_plan_parity.py); the
+    per-micro-batch bytes are the trainer's measured activation records."""
+    per = res["activation_bytes"]["per_gpu"]
+    return {"micro_batches": n, "activation_bytes_per_micro_batch": per,
+            "cdp_peak_bytes": per * (n + 1) // 2, "dp_peak_bytes": per * n, "cdp_over_dp": (n + 1) / (2 * n),
+            "source": "measured per-micro-batch records x the reference plan's live-activation count"}
+
+
 def cpu_resnet_reference(model, ws, rule, sample_images, steps, threads):
     """The oracle port (oracle/resnet_torch.py, float64 torch-CPU autograd under the reference's `_advance`
     semantics) on `sample_images` images per micro-batch, one micro-batch per worker, `steps` steps."""
@@ -507,6 +538,23 @@ def cpu_resnet_reference(model, ws, rule, sample_images, steps, threads):
     from paper_2403_08837_b200.resnet import init_params, layer_specs, stage_partition, synthetic_images
 
     torch.set_num_threads(threads)
+    if model == "vit_b16":
+        from oracle.vit_torch import run_cdp as vit_cdp
+        from paper_2403_08837_b200.vit import VIT_B16, stage_partition as vit_stages, vit_init, vit_units
+
+        x, y = synthetic_images(sample_images * ws, seed=0, hw=224, classes=1000)
+        fresh = None
+        if rule is not None:
+            stage = vit_stages(vit_units(**VIT_B16), ws)
+            fresh = [[rule.reads_fresh(i, int(s)) for s in stage] for i in range(1, ws + 1)]
+        init = vit_init(VIT_B16, 0)
+        perms = [np.random.default_rng([0, t]).permutation(len(x)) for t in range(1, steps + 2)]
+        vit_cdp(VIT_B16, init, x.astype(np.float64), y, ws, sample_images, perms[:1], RN_LR, RN_MOMENTUM, fresh)
+        t0 = time.perf_counter()
+        vit_cdp(VIT_B16, init, x.astype(np.float64), y, ws, sample_images, perms[1:steps + 1], RN_LR, RN_MOMENTUM,
+                fresh)
+        dt = (time.perf_counter() - t0) / steps
+        return ws * sample_images / dt, dt * 1e3
     cfg, hw, classes = resnet_cfg(model)
     specs = layer_specs(cfg["widths"], cfg["depths"], 3, hw, cfg["block"], cfg["stem"], classes)
     x, y = synthetic_images(sample_images * ws, seed=0, hw=hw, classes=classes)
@@ -526,11 +574,16 @@ def cpu_resnet_reference(model, ws, rule, sample_images, steps, threads):
 
 
 def resnet_workload(model, ws, rule_name, dtype):
+    mb = RN_MB
     if model == "resnet18":
         what = "ResNet-18 CIFAR variant (3x3 stem, no max pool), 32x32x3, 10 classes"
+    elif model == "vit_b16":
+        what = "ViT-B/16 (torchvision layout), 224x224x3, 1000 classes, fp32 residual stream"
+        mb = VIT_MB
+        dtype = "bf16"
     else:
         what = "ResNet-50 (torchvision v1.5 layout), 224x224x3, 1000 classes"
-    return (f"{what}; {rule_name}; one micro-batch of {RN_MB} per GPU; {ws} stage(s) = {ws} GPU(s); {dtype} "
+    return (f"{what}; {rule_name}; one micro-batch of {mb} per GPU; {ws} stage(s) = {ws} GPU(s); {dtype} "
             f"operands, fp32 master/momentum; SGD lr {RN_LR} momentum {RN_MOMENTUM}")
 
 
@@ -609,7 +662,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--rule", default="cdp-v2", choices=["cdp-v2", "cdp-v1", "dp", "dp-allreduce"])
-    ap.add_argument("--model", default="resnet18", choices=["resnet18", "resnet50", "mlp"])
+    ap.add_argument("--model", default="resnet18", choices=["resnet18", "resnet50", "vit_b16", "mlp"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the resnet50 / config-1 sub-lines at N=1")
     ap.add_argument("--zero", action="store_true", help="ZeRO-CDP state passing (ResNets, N > 1)")
@@ -626,11 +679,12 @@ def main():
 
             threads = os.cpu_count() or 1
             n = max(1, min(args.steps, 2))
-            sample = 16 if args.model == "resnet18" else 2
+            sample = 16 if args.model == "resnet18" else 1 if args.model == "vit_b16" else 2
             sps, ms = cpu_resnet_reference(args.model, ws, None if args.rule == "dp-allreduce" else resolve(args.rule, ws),
                                            sample, n, threads)
             desc = (f"{n} steps (after 1 warm-up) of the {ws}-micro-batch CDP step on {sample} images per "
-                    f"micro-batch (of {RN_MB}), float64 torch-CPU oracle port, {threads} threads")
+                    f"micro-batch (of {VIT_MB if args.model == 'vit_b16' else RN_MB}), float64 torch-CPU oracle port, "
+                    f"{threads} threads")
             print(json.dumps({
                 "impl": "reference", "metric": METRIC, "value": round(sps, 3), "unit": UNIT, "n_gpus": ws,
                 "steps": n, "warmup": 1, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
@@ -656,17 +710,25 @@ def main():
                                        "tensor_tflops_per_s": r50["tensor_tflops_per_s"],
                                        "roofline": r50["roofline"], "activation_bytes": r50["activation_bytes"],
                                        "clocks": r50["clocks"], "kernel_breakdown": r50["kernel_breakdown"]}
+                    vit = run_resnet(args, 1, 0, local, "vit_b16", 10, 3, e2e=False)
+                    out["vit_b16"] = {"workload": resnet_workload("vit_b16", 1, args.rule, "bf16"),
+                                      "value": vit["value"], "unit": UNIT, "ms_per_step": vit["ms_per_step"],
+                                      "tensor_tflops_per_s": vit["tensor_tflops_per_s"], "roofline": vit["roofline"],
+                                      "activation_bytes": vit["activation_bytes"],
+                                      "single_gpu_cdp_activation_model": vit_activation_model(vit),
+                                      "clocks": vit["clocks"], "kernel_breakdown": vit["kernel_breakdown"]}
                 out["single_gpu_cdp"] = single_gpu_config1(args.dtype)
             if ws == 1 and not args.no_cpu_baseline:
                 threads = os.cpu_count() or 1
                 from paper_2403_08837_b200.dist import resolve
 
-                sample = 16 if args.model == "resnet18" else 2
+                sample = 16 if args.model == "resnet18" else 1 if args.model == "vit_b16" else 2
                 sps, _ms = cpu_resnet_reference(args.model, 1, resolve(args.rule, 1), sample, 2, threads)
                 out["cpu_baseline"] = {"value": round(sps, 3), "unit": UNIT, "cores": threads, "kind": "port",
                                        "sample": f"2 steps (after 1 warm-up) of the same CDP step on {sample} "
-                                                 f"images (of {RN_MB}), float64 torch-CPU oracle port, "
-                                                 f"{threads} threads", "host_cpus": os.cpu_count()}
+                                                 f"images (of {VIT_MB if args.model == 'vit_b16' else RN_MB}), "
+                                                 f"float64 torch-CPU oracle port, {threads} threads",
+                                       "host_cpus": os.cpu_count()}
             print(json.dumps(out), flush=True)
         if ws > 1:
             import torch

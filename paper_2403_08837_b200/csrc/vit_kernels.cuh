@@ -138,6 +138,71 @@ static __global__ void ln_param_partial_kernel(const float *__restrict__ g, cons
     }
 }
 
+// Fused LayerNorm backward over a block of kLnRows rows (8 warps, a warp per row, lane owns
+// columns lane + 32 k): dh_out = dh_in + dx (fp32) and, when copy.hi, the same row in compute
+// format (the next GEMM's operand); per-column (sum g, sum g xhat) of the block's rows combined
+// over the warps in fixed order -> partial[d][blk][2] (fp64), finalised by bn_finalize_bwd_kernel.
+constexpr int kLnBwdRows = 32;  // rows per CTA of the fused backward (4 per warp)
+template <int KIND, int CPL>
+static __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const float *__restrict__ g,
+                                                                  const float *__restrict__ x, int rows,
+                                                                  int in_stride, int D, const float *gb,
+                                                                  const float *mean, const float *rstd,
+                                                                  const float *dh_in, float *dh_out, CTensor copy,
+                                                                  double *partial) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    extern __shared__ float red[];  // [8][D][2]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float sg[CPL], sx[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) sg[k] = sx[k] = 0.f;
+    const int r0 = blockIdx.x * kLnBwdRows, r1 = min(rows, r0 + kLnBwdRows);
+    for (int w = r0 + warp; w < r1; w += 8) {
+        const size_t xo = size_t(w) * in_stride * D, go = size_t(w) * D;
+        const float mu = mean[w], rs = rstd[w];
+        float gv[CPL], xh[CPL];
+        float a = 0.f, b = 0.f;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int d = lane + 32 * k;
+            gv[k] = g[go + d];
+            xh[k] = (x[xo + d] - mu) * rs;
+            const float gg = gv[k] * gb[d];
+            a += gg;
+            b += gg * xh[k];
+            sg[k] += gv[k];
+            sx[k] = fmaf(gv[k], xh[k], sx[k]);
+        }
+        a = warp_sum(a) / float(D);
+        b = warp_sum(b) / float(D);
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int d = lane + 32 * k;
+            const float v = (dh_in ? dh_in[xo + d] : 0.f) + rs * (gv[k] * gb[d] - a - xh[k] * b);
+            dh_out[xo + d] = v;
+            if (copy.hi) Fmt<KIND>::store(copy.hi, copy.lo, size_t(w) * in_stride * copy.ld + d, v);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+        const int d = lane + 32 * k;
+        red[(warp * D + d) * 2] = sg[k];
+        red[(warp * D + d) * 2 + 1] = sx[k];
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int q = 0; q < 8; ++q) {
+            s0 += double(red[(q * D + d) * 2]);
+            s1 += double(red[(q * D + d) * 2 + 1]);
+        }
+        double *o = partial + (size_t(d) * gridDim.x + blockIdx.x) * 2;
+        o[0] = s0;  // -> dbeta
+        o[1] = s1;  // -> dgamma
+    }
+}
+
 // Row softmax of scale * S (fp32 [rows][lds], n valid columns) -> P (bf16 [rows][ldp]); one warp per row.
 static __global__ void softmax_fwd_kernel(const float *__restrict__ S, int rows, int n, int lds, float scale,
                                    __nv_bfloat16 *P, int ldp) {

@@ -234,7 +234,7 @@ struct VitTrainer {
         gpos = DevBuf(size_t(T) * D * 4);
         gcls = DevBuf(size_t(D) * 4);
         dE = make_cbuf(0, B * NP, D);
-        lnpart = DevBuf(size_t(D) * ((R + kLnRows - 1) / kLnRows) * 16);
+        lnpart = DevBuf(size_t(D) * ((R + kLnBwdRows - 1) / kLnBwdRows) * 16);
         dgf = DevBuf(size_t(D) * 4);
         dbf = DevBuf(size_t(D) * 4);
         // ---- shared region: RingFlags | theta0 | theta1 | partial | momentum
@@ -484,21 +484,34 @@ struct VitTrainer {
     // LayerNorm backward of `unit`: dh_out = dh_in + LN'(g); parameter gradients -> dgam / dbet.
     void layernorm_bwd(const float *g, const float *x, int rows, int stride, int unit, int p, const float *mean,
                        const float *rstd, const float *dh_in, float *dh_out, float *dgam, float *dbet,
-                       cudaStream_t s) {
-        L_("ln_bwd", 0, double(rows) * D * 16, s, [&] {
-            launch_pdl(ln_bwd_kernel, dim3((rows * 32 + 255) / 256), dim3(256), 0, s, g, x, rows, stride, D,
-                       th(unit, p), mean, rstd, dh_in, dh_out);
-        });
-        const int nblk = (rows + kLnRows - 1) / kLnRows;
-        L_("ln_param_grad", 0, double(rows) * D * 8, s, [&] {
-            launch_pdl(ln_param_partial_kernel, dim3(nblk), dim3(256), 0, s, g, x, rows, stride, D, mean, rstd,
-                       lnpart.as<double>());
-        });
+                       cudaStream_t s, CTensor copy = CTensor{}) {
+        const int nblk = (rows + kLnBwdRows - 1) / kLnBwdRows;
+        const size_t smem = size_t(8) * D * 2 * 4;
+        auto go = [&](auto kern) {
+            if (!ln_attr_) {
+                CDP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            }
+            L_("ln_bwd", 0, double(rows) * D * (16 + (copy.hi ? 2 : 0)), s, [&] {
+                launch_pdl(kern, dim3(nblk), dim3(256), smem, s, g, x, rows, stride, D, th(unit, p), mean, rstd,
+                           dh_in, dh_out, copy, lnpart.as<double>());
+            });
+        };
+        switch (D / 32) {
+            case 2: go(ln_bwd_fused_kernel<0, 2>); break;
+            case 4: go(ln_bwd_fused_kernel<0, 4>); break;
+            case 8: go(ln_bwd_fused_kernel<0, 8>); break;
+            case 16: go(ln_bwd_fused_kernel<0, 16>); break;
+            case 24: go(ln_bwd_fused_kernel<0, 24>); break;
+            case 32: go(ln_bwd_fused_kernel<0, 32>); break;
+            default: throw CdpError("LayerNorm width must be 64, 128, 256, 512, 768 or 1024");
+        }
+        ln_attr_ = !sizing;
         L_("ln_param_finalize", 0, double(nblk) * D * 16, s, [&] {
             launch_pdl(bn_finalize_bwd_kernel, dim3((D * 32 + 255) / 256), dim3(256), 0, s,
                        (const double *)lnpart.as<double>(), nblk, D, dbet, dgam);
         });
     }
+    bool ln_attr_ = false;
 
     void forward(int p, cudaStream_t s) {
         // patch embedding + tokens
@@ -645,16 +658,18 @@ struct VitTrainer {
         }
         cudaEvent_t head_dg = ev(cs);
         lin_hop(u_head, p, uf.view(), B, dz.view(), dz_ready, head_dg);
-        // final LayerNorm (class-token rows only): dh = 0 elsewhere
-        if (!sizing) CDP_CUDA(cudaMemsetAsync(dh.p, 0, dh.bytes, cs));
+        // final LayerNorm (class-token rows only): dh = 0 elsewhere (and its bf16 copy, the last block's operand)
+        if (!sizing) {
+            CDP_CUDA(cudaMemsetAsync(dh.p, 0, dh.bytes, cs));
+            CDP_CUDA(cudaMemsetAsync(layers[L - 1].dhc.hi.p, 0, layers[L - 1].dhc.hi.bytes, cs));
+        }
         layernorm_bwd(duf.as<float>(), hL.as<float>(), B, T, u_ln, p, mf.as<float>(), rf.as<float>(), nullptr,
-                      dh.as<float>(), dgf.as<float>(), dbf.as<float>(), cs);
+                      dh.as<float>(), dgf.as<float>(), dbf.as<float>(), cs, layers[L - 1].dhc.view());
         ln_hop(u_ln, p, dgf.as<float>(), dbf.as<float>(), ev(cs));
         const float scale = 1.f / std::sqrt(float(HD));
         for (int l = L - 1; l >= 0; --l) {
             VLayer &y = layers[l];
-            // ---- MLP
-            cast(dh.as<float>(), R, 1, 1, 0, y.dhc.view(), cs);
+            // ---- MLP (y.dhc = bf16(dh), written by the LayerNorm backward that produced dh)
             cudaEvent_t dhc_ready = ev(cs);
             {
                 typename EpiConvOut2<0>::Params ep{};
@@ -679,10 +694,9 @@ struct VitTrainer {
             cudaEvent_t fc1_dg = ev(cs);
             lin_hop(y.fc1, p, y.u2.view(), R, y.dz1.view(), dz1_ready, fc1_dg);
             layernorm_bwd(du.as<float>(), y.hmid.as<float>(), R, 1, y.ln2, p, y.m2.as<float>(), y.r2.as<float>(),
-                          dh.as<float>(), dhm.as<float>(), y.dg2.as<float>(), y.db2.as<float>(), cs);
+                          dh.as<float>(), dhm.as<float>(), y.dg2.as<float>(), y.db2.as<float>(), cs, y.dhmc.view());
             ln_hop(y.ln2, p, y.dg2.as<float>(), y.db2.as<float>(), ev(cs));
             // ---- attention
-            cast(dhm.as<float>(), R, 1, 1, 0, y.dhmc.view(), cs);
             cudaEvent_t dhmc_ready = ev(cs);
             {
                 typename EpiConvOut2<0>::Params ep{};
@@ -726,7 +740,8 @@ struct VitTrainer {
             cudaEvent_t qkv_dg = ev(cs);
             lin_hop(y.qkv, p, y.u1.view(), R, y.dqkv.view(), dqkv_ready, qkv_dg);
             layernorm_bwd(du.as<float>(), y.h.as<float>(), R, 1, y.ln1, p, y.m1.as<float>(), y.r1.as<float>(),
-                          dhm.as<float>(), dh.as<float>(), y.dg1.as<float>(), y.db1.as<float>(), cs);
+                          dhm.as<float>(), dh.as<float>(), y.dg1.as<float>(), y.db1.as<float>(), cs,
+                          l > 0 ? layers[l - 1].dhc.view() : CTensor{});
             ln_hop(y.ln1, p, y.dg1.as<float>(), y.db1.as<float>(), ev(cs));
         }
         // ---- embeddings

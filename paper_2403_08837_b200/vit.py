@@ -59,6 +59,24 @@ def stage_partition(units, n_stages):
     return stage.astype(np.int32)
 
 
+def vit_init(cfg, seed=0) -> np.ndarray:
+    """Deterministic initialisation in the trainer layout (numpy PCG64): linear weights N(0, 0.02),
+    biases 0, LayerNorm (1, 0), class token / position embedding N(0, 0.02)."""
+    rng = np.random.default_rng([seed, 0xF0])
+    parts = []
+    for name, shape, _ in vit_units(**cfg):
+        n = int(np.prod(shape))
+        if name.endswith(("ln1", "ln2")) or name == "ln":
+            c = shape[0] // 2
+            parts.append(np.concatenate([np.ones(c), np.zeros(c)]))
+        elif name in ("cls", "pos"):
+            parts.append(rng.normal(0.0, 0.02, size=n))
+        else:
+            rows, cols = shape
+            parts.append(np.concatenate([rng.normal(0.0, 0.02, size=(rows - 1, cols)), np.zeros((1, cols))]).ravel())
+    return np.concatenate(parts)
+
+
 def _i32p(a):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
 
