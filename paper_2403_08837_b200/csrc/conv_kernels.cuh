@@ -477,23 +477,36 @@ struct EpiConvOut2 {
             }
         }
     }
-    // Split-K reduce kernel: the whole 128-row tile is in `st` (rows in order).
+    // Split-K reduce kernel: the whole 128-row tile is in `st` (rows in order).  Column
+    // statistics: NTH/ncols row groups per column, combined in group order (fixed).
     template <int NTH>
     __device__ static void run_with_stats(const Params &p, const float *st, int lds, const int *rowm, int nrows,
                                           int col0, int ncols, int tm, int N, int tid, int64_t off) {
         run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid, off);
         if (p.stats) {
-            for (int c = tid; c < ncols; c += NTH) {
-                float s = 0.f, q = 0.f;
-                for (int r = 0; r < nrows; ++r) {
+            __shared__ float red[2][NTH];
+            const int groups = NTH / ncols;
+            const int c = tid % ncols, grp = tid / ncols;
+            float s = 0.f, q = 0.f;
+            if (grp < groups)
+                for (int r = grp; r < nrows; r += groups) {
                     if (rowm[r] < 0) continue;
                     const float v = st[r * lds + c];
                     s += v;
                     q = fmaf(v, v, q);
                 }
-                float *o = p.stats + (size_t(col0 + c) * p.tiles + tm) * 2;
-                o[0] = s;
-                o[1] = q;
+            red[0][tid] = s;
+            red[1][tid] = q;
+            __syncthreads();
+            if (tid < ncols) {
+                float a = 0.f, b = 0.f;
+                for (int g = 0; g < groups; ++g) {
+                    a += red[0][g * ncols + tid];
+                    b += red[1][g * ncols + tid];
+                }
+                float *o = p.stats + (size_t(col0 + tid) * p.tiles + tm) * 2;
+                o[0] = a;
+                o[1] = b;
             }
         }
     }
