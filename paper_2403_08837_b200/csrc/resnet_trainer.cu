@@ -520,8 +520,8 @@ struct ResNetTrainer {
         L(name, flops, 0.0, s, [&] { launch_pdl(kern, dim3(grid), dim3(kPkThreads), Cfg::SMEM, s, gp.maps, a, ep); });
         if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
-            constexpr int RC = kStats ? 128 : 4;
-            constexpr int CC = kStats ? 32 : (BNc < 64 ? BNc : 64);
+            constexpr int RC = kStats ? 128 : 16;  // 256 threads x one float4 (hop) / 8 float4 (stats)
+            constexpr int CC = 64;
             L("splitk_reduce", 0, double(need) * 4, s, [&] {
                 launch_pdl(pk_reduce_kernel<BNc, Epi, RC, CC>, dim3(tiles, 128 / RC, BNc / CC), dim3(256), 0, s, a,
                            ep);
