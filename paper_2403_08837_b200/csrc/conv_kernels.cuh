@@ -1,8 +1,8 @@
 // Convolutional-network layer kernels for the ResNet configs (BASELINE
-// configs[1..2,4]).  Convolutions are tcgen05 GEMMs (gemm_tc_kernel): implicit
-// (TMA-gathered NHWC boxes, MODE 1-3) for every conv whose input channels fill a
-// 128-byte chunk, a plain GEMM for 1x1 stride-1 convs, and an explicit im2col
-// only for the 3-channel stem.  Batch norm runs in training mode (per
+// configs[1..2,4]).  Convolutions are tcgen05 GEMMs (gemm_pk_kernel): implicit
+// (TMA-gathered NHWC boxes, MODE 1-3; stride-2 data gradients as four sub-pixel
+// phases) for every conv whose input channels fill a 128-byte chunk, a plain
+// GEMM for 1x1 stride-1 convs, and an explicit im2col only for the 3-channel stem.  Batch norm runs in training mode (per
 // micro-batch statistics) with fixed-order reductions: the forward statistics
 // come out of the conv GEMM's epilogue (per M tile), the backward ones from a
 // row-blocked partial kernel; both are finalised in fp64 in a fixed order.
@@ -155,54 +155,6 @@ static __global__ void stem_im2col_kernel(const float *__restrict__ data, const 
         const size_t o = size_t(p) * cols.ld + k0;
         store_wc4<KIND>(cols, o, make_float4(v[0], v[1], v[2], v[3]));
         store_wc4<KIND>(cols, o + 4, make_float4(v[4], v[5], v[6], v[7]));
-    }
-}
-
-// col2im (deterministic gather) for the convs whose data gradient is an explicit
-// GEMM into im2col space (stride 2): dx[b,h,w,c] = sum over (r, s) ascending of
-// dcols[(b, ho, wo), (r, s, c)] with h = ho*stride - pad + r.  4 channels per thread.
-// add != null: dx = col2im + (add masked by (add_mask > 0) when add_mask.hi) - the
-// residual branch of a block folded into the gradient of its first conv.
-template <int KIND>
-static __global__ void col2im_kernel(const void *__restrict__ dcols, int ldc, int B, int H, int W, int C, int R, int S,
-                              int stride, int pad, int Ho, int Wo, void *dx, const void *add, CTensor add_mask) {
-    ptx::griddep_wait();
-    ptx::griddep_launch();
-    const int C4 = C / 4;
-    const int64_t n = int64_t(B) * H * W * C4;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % C4) * 4;
-        const int64_t pix = i / C4;
-        const int w = int(pix % W), h = int((pix / W) % H), b = int(pix / (int64_t(W) * H));
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int r = 0; r < R; ++r) {
-            const int hh = h + pad - r;
-            if (hh < 0 || hh % stride) continue;
-            const int ho = hh / stride;
-            if (ho >= Ho) continue;
-            for (int s = 0; s < S; ++s) {
-                const int ww = w + pad - s;
-                if (ww < 0 || ww % stride) continue;
-                const int wo = ww / stride;
-                if (wo >= Wo) continue;
-                const float4 v =
-                    ld_y4<KIND>(dcols, (size_t(b) * Ho * Wo + size_t(ho) * Wo + wo) * ldc + (r * S + s) * C + c);
-                acc.x += v.x;
-                acc.y += v.y;
-                acc.z += v.z;
-                acc.w += v.w;
-            }
-        }
-        const size_t o = size_t(pix) * C + c;
-        if (add) {
-            float4 a = ld_y4<KIND>(add, o);
-            if (add_mask.hi) a = relu_mask4(a, ld_c4<KIND>(add_mask, o));
-            acc.x += a.x;
-            acc.y += a.y;
-            acc.z += a.z;
-            acc.w += a.w;
-        }
-        st_y4<KIND>(dx, o, acc);
     }
 }
 

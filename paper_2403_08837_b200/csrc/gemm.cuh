@@ -37,6 +37,12 @@ struct ConvGeom {
     int nbw, nbh;       // boxes along W and H
     int Wo, Ho, Bn;     // extents of the boxed pixel grid
     int Cw;             // dgrad: Cin (rows per tap of W viewed [R*S*Cin][Cout])
+    // dgrad taps: A box offset (toh, tow) on dy and weight tap twt (= r*S + s) of tap k;
+    // a stride-2 data gradient runs as 4 sub-pixel phases, each with its own tap subset
+    int ntap;
+    signed char toh[9], tow[9], twt[9];
+    // output row of grid pixel (b, h, w): (b*oH + h*omul + oph)*oW + w*omul + opw
+    int omul, oph, opw, oH, oW;
 };
 
 __host__ __device__ inline void conv_box_origin(const ConvGeom &g, int idx, int &w0, int &h0, int &b0) {
@@ -54,7 +60,7 @@ __host__ __device__ inline int conv_box_row(const ConvGeom &g, int idx, int row)
     conv_box_origin(g, idx, w0, h0, b0);
     const int w = w0 + row % g.bw, h = h0 + (row / g.bw) % g.bh, b = b0 + row / (g.bw * g.bh);
     if (w >= g.Wo || h >= g.Ho || b >= g.Bn) return -1;
-    return (b * g.Ho + h) * g.Wo + w;
+    return (b * g.oH + h * g.omul + g.oph) * g.oW + w * g.omul + g.opw;
 }
 
 struct GemmArgs {
@@ -125,8 +131,10 @@ __device__ __forceinline__ void conv_load(uint8_t *sa, uint8_t *sb, const GemmMa
                              b0);
             load_operand<C, B_MN, BN>(sb, &maps.b[seg], bar, n0, kb * C::BK);
         } else {
-            ptx::tma_load_4d(sa, &maps.a[seg], bar, cc * C::CH, w0 + g.pad - s, h0 + g.pad - r, b0);
-            ptx::tma_load_2d(sb, &maps.b[seg], bar, cc * C::CH, tap * g.Cw + n0);
+            (void)r;
+            (void)s;
+            ptx::tma_load_4d(sa, &maps.a[seg], bar, cc * C::CH, w0 + g.tow[tap], h0 + g.toh[tap], b0);
+            ptx::tma_load_2d(sb, &maps.b[seg], bar, cc * C::CH, g.twt[tap] * g.Cw + n0);
         }
     } else {
         int w0, h0, b0;

@@ -105,7 +105,35 @@ inline ConvGeom conv_geom(int C, int R, int S, int stride, int pad, int Wo, int 
     g.Wo = Wo;
     g.Ho = Ho;
     g.Bn = Bn;
+    g.omul = 1;
+    g.oph = g.opw = 0;
+    g.oH = Ho;
+    g.oW = Wo;
     return g;
+}
+
+// Data-gradient taps.  phase < 0: a stride-1 conv, all R*S taps, dx(h, w) <- dy(h + pad - r, w + pad - s).
+// phase = ph*2 + pw (stride 2): output pixels (2i + ph, 2j + pw) <- dy(i + (ph + pad - r)/2, ...) over the
+// taps with (ph + pad - r) and (pw + pad - s) even.
+inline void dgrad_taps(ConvGeom &g, int R, int S, int pad, int phase) {
+    g.ntap = 0;
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) {
+            int oh, ow;
+            if (phase < 0) {
+                oh = pad - r;
+                ow = pad - s;
+            } else {
+                const int ph = phase >> 1, pw = phase & 1;
+                if (((ph + pad - r) & 1) || ((pw + pad - s) & 1)) continue;
+                oh = (ph + pad - r) / 2;
+                ow = (pw + pad - s) / 2;
+            }
+            g.toh[g.ntap] = (signed char)oh;
+            g.tow[g.ntap] = (signed char)ow;
+            g.twt[g.ntap] = (signed char)(r * S + s);
+            ++g.ntap;
+        }
 }
 inline int conv_boxes(const ConvGeom &g) { return g.nbw * g.nbh * ((g.Bn + g.bn - 1) / g.bn); }
 
@@ -136,7 +164,7 @@ inline int seg_pick(int s, bool a) {
 // WGRAD: dW[R*S*C][Cout] = sum_pixels x_tap^T dy;  x NHWC, dy NHWC.
 template <int KIND, int BN, int MODE>
 GemmPlan plan_conv(const Nhwc &a, const void *b_hi, const void *b_lo, int b_ld, const Nhwc &dy, int R, int S,
-                   int stride, int pad, int Cin, int Cout, int splits, float *ws, int *counters) {
+                   int stride, int pad, int Cin, int Cout, int splits, float *ws, int *counters, int phase = -1) {
     constexpr int ELEM = KIND == 0 ? 2 : 4;
     constexpr int CH = 128 / ELEM;
     constexpr bool A_MN = MODE == GM_WGRAD;
@@ -162,14 +190,28 @@ GemmPlan plan_conv(const Nhwc &a, const void *b_hi, const void *b_lo, int b_ld, 
             p.maps.b[s] = operand_map<KIND>(bo, BN);
         }
     } else if (MODE == GM_DGRAD) {
-        CDP_REQUIRE(stride == 1, "implicit dgrad: stride 1 only");
         CDP_REQUIRE(dy.C % CH == 0 && dy.C == Cout, "implicit dgrad: output channels must be a multiple of the chunk");
-        const int H = dy.H + R - 1 - 2 * pad, W = dy.W + S - 1 - 2 * pad;  // forward input extents
-        g = conv_geom(Cout, R, S, 1, pad, W, H, dy.N, 128, CH);
+        if (stride == 1) {
+            CDP_REQUIRE(phase < 0, "stride-1 dgrad has no phases");
+            const int H = dy.H + R - 1 - 2 * pad, W = dy.W + S - 1 - 2 * pad;  // forward input extents
+            g = conv_geom(Cout, R, S, 1, pad, W, H, dy.N, 128, CH);
+            M = dy.N * H * W;
+        } else {
+            CDP_REQUIRE(stride == 2 && phase >= 0 && phase < 4, "stride-2 dgrad runs as 4 sub-pixel phases");
+            // phase grid = the dy grid (input extents 2*Ho x 2*Wo)
+            g = conv_geom(Cout, R, S, 2, pad, dy.W, dy.H, dy.N, 128, CH);
+            g.omul = 2;
+            g.oph = phase >> 1;
+            g.opw = phase & 1;
+            g.oH = 2 * dy.H;
+            g.oW = 2 * dy.W;
+            M = dy.N * 4 * dy.H * dy.W;
+        }
+        dgrad_taps(g, R, S, pad, phase);
+        CDP_REQUIRE(g.ntap > 0, "empty dgrad phase");
         g.Cw = Cin;
-        M = dy.N * H * W;
         N = Cin;
-        kb = R * S * g.cpt;
+        kb = g.ntap * g.cpt;
         tiles_m = conv_boxes(g);
         for (int s = 0; s < n_seg; ++s) {
             p.maps.a[s] = nhwc_map<KIND>(seg_pick<KIND>(s, true) ? dy.lo : dy.hi, dy, g.bw, g.bh, g.bn, 1, false);

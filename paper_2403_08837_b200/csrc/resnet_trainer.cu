@@ -10,8 +10,8 @@
 //                epilogue writes y and the per-tile BN statistics;
 //   BN         = training-mode batch statistics (fp64 fixed-order finalise),
 //                affine + residual + ReLU in one vectorised pass;
-//   dgrad      = implicit GEMM over dy (stride 1), or GEMM into im2col space +
-//                deterministic col2im gather (stride 2);
+//   dgrad      = implicit GEMM over dy (stride 1), or four sub-pixel phases of
+//                stride-1 implicit GEMMs with the phase's taps (stride 2);
 //   wgrad      = implicit GEMM (K = pixel boxes, split-K) whose epilogue is the
 //                hop / SGD update of the weight tensor (EpiWgrad);
 //   BN gamma|beta hop / update by a vector kernel.
@@ -153,7 +153,7 @@ struct ResNetTrainer {
     std::vector<int64_t> act_P;
     DevBuf gbuf[4];            // fp32 gradients w.r.t. activations (block in / chain / chain / shortcut)
     CBuf cols, pooled, dz;     // stem im2col record, pooled features (+ ones column), dZ
-    DevBuf dcols, dpooled, z, loss_dev, loss_rows, stats_fwd, stats_bwd, bnpart[2], pool_arg;
+    DevBuf dpooled, z, loss_dev, loss_rows, stats_fwd, stats_bwd, bnpart[2], pool_arg;
     int64_t max_act = 0;
     DevBuf ws_c, cnt_c, ws_h, cnt_h;
     size_t ws_c_floats = 0, ws_h_floats = 0;
@@ -329,7 +329,7 @@ struct ResNetTrainer {
         fc_t = add_tensor(T_FC, int64_t(cin + 1) * classes, cin + 1, classes);
         P = tens.back().base + tens.back().n;
         // ---- buffers
-        int64_t max_dcols = 1, max_stats = 1, max_part = 1;
+        int64_t max_stats = 1, max_part = 1;
         for (auto &c : convs) {
             c.y = DevBuf(size_t(c.P) * c.cout * (kind == 0 ? 2 : 4));
             c.mean = DevBuf(c.cout * 4);
@@ -337,15 +337,12 @@ struct ResNetTrainer {
             c.dbeta = DevBuf(c.cout * 4);
             c.dgamma = DevBuf(c.cout * 4);
             c.dy = make_cbuf(kind, int(c.P), c.cout);
-            if (c.impl == CI_IMPLICIT && c.stride != 1)
-                max_dcols = std::max<int64_t>(max_dcols, c.P * round_up(c.K, 16));
             max_stats = std::max<int64_t>(max_stats, int64_t(std::max(c.tiles_fwd, 160)) * c.cout * 2);
             max_part = std::max<int64_t>(max_part, ((c.P + kBnRows - 1) / kBnRows) * c.cout * 2);
         }
         const ConvL &c0 = convs[stem];
         cols = make_cbuf(kind, int(c0.P), c0.K);
         for (auto &g : gbuf) g = DevBuf(size_t(max_act) * ysz());
-        dcols = DevBuf(size_t(max_dcols) * ysz());
         stats_fwd = DevBuf(size_t(max_stats) * 4);
         stats_bwd = DevBuf(size_t(max_stats) * 2 * 4);  // [C][<=160 CTAs][3]
         bnpart[0] = DevBuf(size_t(max_part) * 8);
@@ -556,16 +553,21 @@ struct ResNetTrainer {
 
     template <int K, int MODE, class Epi>
     void pk_conv(const char *name, int BN, const ConvL &c, const CBuf &w, const typename Epi::Params &ep,
-                 cudaStream_t s, bool hop) {
+                 cudaStream_t s, bool hop, int phase = -1) {
         const Nhwc a = c.in_act >= 0 ? nhwc_act(c.in_act) : Nhwc{};
         const Nhwc dy = nhwc_dy(c);
-        const double flops = 2.0 * double(c.P) * c.K * c.cout;
+        double flops = 2.0 * double(c.P) * c.K * c.cout;
+        if (phase >= 0) {  // one sub-pixel phase: its taps only
+            ConvGeom probe{};
+            dgrad_taps(probe, c.R, c.S, c.pad, phase);
+            flops = 2.0 * double(c.P) * probe.ntap * c.cin * c.cout;
+        }
         bn_switch(BN, [&](auto bnc) {
             constexpr int BNc = decltype(bnc)::value;
             constexpr bool AMN = MODE == GM_WGRAD, BMN = MODE != GM_DGRAD;
             if constexpr (BNc >= 64 && (!BMN || BNc % (K == 0 ? 64 : 32) == 0)) {
                 GemmPlan p = plan_conv<K, BNc, MODE>(a, w.hi.p, w.lo.p, w.ld, dy, c.R, c.S, c.stride, c.pad, c.cin,
-                                                     c.cout, 1, nullptr, nullptr);
+                                                     c.cout, 1, nullptr, nullptr, phase);
                 run_pk<K, BNc, AMN, BMN, Epi, MODE>(name, flops, p, ep, s, hop);
             } else {
                 throw CdpError("unsupported conv GEMM configuration");
@@ -773,7 +775,7 @@ struct ResNetTrainer {
             const char *e = std::getenv("CDP_FUSE_BN_BWD");
             return e && e[0] == '1';
         }();
-        const bool want = fuse_env && bn_ci >= 0 && (c.impl == CI_PLAIN || c.stride == 1);  // not via col2im
+        const bool want = fuse_env && bn_ci >= 0 && (c.impl == CI_PLAIN || c.stride == 1);  // not the phases
         if (want) {
             const ConvL &b1 = convs[bn_ci];
             ep.bstats = stats_bwd.as<float>();
@@ -807,19 +809,21 @@ struct ResNetTrainer {
                 fused_slots = last_grid;
             }
         } else {
+            // stride 2: four sub-pixel phases, each a stride-1 implicit GEMM over dy with its own taps
+            // (pixels (2i + ph, 2j + pw)); phases without taps (1x1 convs) leave zeros
             ep.bstats = nullptr;
-            const int Kp = round_up(c.K, 16);
-            ep.out = dcols.p;
-            ep.ld = Kp;
-            ep.add = nullptr;
-            ep.add_mask = CTensor{};
-            // dcols[P][K] = dy[P][Cout] . W^T, W viewed [K][Cout] (K-major B)
-            pk_plain<K, false, false, EpiConvOut2<K>>("conv_dgrad_s2", tile_n(c.K), c.dy.view(), w.view(), c.P, c.K,
-                                                      c.cout, ep, s, false);
-            const int64_t nin = c.Pin * c.cin / 4;
-            L("col2im", 0, (double(c.P) * Kp + double(c.Pin) * c.cin * (add ? 2 : 1)) * ysz(), s, [&] {
-                launch_pdl(col2im_kernel<K>, dim3(blocks_for(nin)), dim3(256), 0, s, (const void *)dcols.p, Kp, B, c.H, c.W, c.cin, c.R, c.S, c.stride, c.pad, c.Ho, c.Wo, g_in, add, add_mask);
-            });
+            ep.out = g_in;
+            ep.ld = c.cin;
+            if (c.R == 1) {
+                CDP_REQUIRE(add == nullptr, "a 1x1 stride-2 data gradient cannot fold a residual branch");
+                if (!sizing) CDP_CUDA(cudaMemsetAsync(g_in, 0, size_t(c.Pin) * c.cin * ysz(), s));
+            }
+            for (int ph = 0; ph < 4; ++ph) {
+                ConvGeom probe{};
+                dgrad_taps(probe, c.R, c.S, c.pad, ph);
+                if (probe.ntap == 0) continue;
+                pk_conv<K, GM_DGRAD, EpiConvOut2<K>>("conv_dgrad_s2", tile_n(c.cin), c, w, ep, s, false, ph);
+            }
         }
     }
 
@@ -1525,7 +1529,7 @@ extern "C" int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out) {
         int64_t par = int64_t(m.Pp) * (m.vel ? 16 : 12);
         for (int v = 0; v < 2; ++v)
             for (auto &w : m.wc[v]) par += int64_t(w.hi.bytes + w.lo.bytes);
-        int64_t scratch = int64_t(m.dcols.bytes);
+        int64_t scratch = 0;
         for (auto &g : m.gbuf) scratch += int64_t(g.bytes);
         int64_t vals[6] = {act, par, m.kernels_per_step, int64_t(m.flops_per_step), scratch, m.zero_bytes_per_step};
         for (int i = 0; i < n_out && i < 6; ++i) out[i] = vals[i];
