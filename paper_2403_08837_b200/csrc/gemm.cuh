@@ -60,7 +60,9 @@ __host__ __device__ inline int conv_box_row(const ConvGeom &g, int idx, int row)
     conv_box_origin(g, idx, w0, h0, b0);
     const int w = w0 + row % g.bw, h = h0 + (row / g.bw) % g.bh, b = b0 + row / (g.bw * g.bh);
     if (w >= g.Wo || h >= g.Ho || b >= g.Bn) return -1;
-    return (b * g.oH + h * g.omul + g.oph) * g.oW + w * g.omul + g.opw;
+    const int oh = h * g.omul + g.oph, ow = w * g.omul + g.opw;
+    if (oh >= g.oH || ow >= g.oW) return -1;  // a phase pixel past an odd input edge
+    return (b * g.oH + oh) * g.oW + ow;
 }
 
 struct GemmArgs {

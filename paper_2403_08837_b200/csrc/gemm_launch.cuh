@@ -198,14 +198,16 @@ GemmPlan plan_conv(const Nhwc &a, const void *b_hi, const void *b_lo, int b_ld, 
             M = dy.N * H * W;
         } else {
             CDP_REQUIRE(stride == 2 && phase >= 0 && phase < 4, "stride-2 dgrad runs as 4 sub-pixel phases");
-            // phase grid = the dy grid (input extents 2*Ho x 2*Wo)
+            CDP_REQUIRE(a.H >= 2 * dy.H - 1 && a.H <= 2 * dy.H && a.W >= 2 * dy.W - 1 && a.W <= 2 * dy.W,
+                        "stride-2 dgrad: input extents must be 2*Ho or 2*Ho - 1");
+            // phase grid = the dy grid; output pixel (2i + ph, 2j + pw) of the (a.H x a.W) input
             g = conv_geom(Cout, R, S, 2, pad, dy.W, dy.H, dy.N, 128, CH);
             g.omul = 2;
             g.oph = phase >> 1;
             g.opw = phase & 1;
-            g.oH = 2 * dy.H;
-            g.oW = 2 * dy.W;
-            M = dy.N * 4 * dy.H * dy.W;
+            g.oH = a.H;
+            g.oW = a.W;
+            M = dy.N * a.H * a.W;
         }
         dgrad_taps(g, R, S, pad, phase);
         CDP_REQUIRE(g.ntap > 0, "empty dgrad phase");

@@ -13,7 +13,15 @@ pytestmark = pytest.mark.gpu
 
 W, D, HW, MB = (64, 128), (1, 1), 16, 8
 ARCH = {"basic": dict(block="basic", stem="cifar", hw=16, classes=10),
-        "bottleneck": dict(block="bottleneck", stem="imagenet", hw=32, classes=100)}
+        "bottleneck": dict(block="bottleneck", stem="imagenet", hw=32, classes=100),
+        # 112x112 input: stem 56x56 -> pool 28x28 -> 14x14: feature maps that are not powers of two, so
+        # the implicit-GEMM pixel boxes are partial (28 valid of 32 columns, 14 of 16) as at 224x224
+        "bottleneck112": dict(block="bottleneck", stem="imagenet", hw=112, classes=100),
+        # four stages at 112x112: 28, 14, 7 (boxes of 8x8x2 images, 98 valid rows of 128) and 4 (a stride-2
+        # conv over an odd 7x7 input).  Ill-conditioned (BN over 4x4x8 values): torch's own float32 step
+        # differs from float64 by 1.9e-3 here, so its fp32 tolerance is 3e-3 (ours: 1.2e-3)
+        "bottleneck112x4": dict(block="bottleneck", stem="imagenet", hw=112, classes=10, W=(64, 64, 64, 64),
+                                D=(1, 1, 1, 1), fp32_tol=3e-3)}
 
 
 def _data(n, seed=0, hw=HW, classes=10):
@@ -27,6 +35,7 @@ def _ranks(world, rule, dtype, steps, momentum=0.9, arch="basic"):
     from paper_2403_08837_b200.resnet import DeviceResNet
 
     a = ARCH[arch]
+    W, D = a.get("W", globals()["W"]), a.get("D", globals()["D"])
     x, y = _data(world * MB * 2, hw=a["hw"], classes=a["classes"])
     init = init_flat(W, D, seed=0, block=a["block"], stem=a["stem"], classes=a["classes"])
     perms = [np.random.default_rng([5, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
@@ -54,6 +63,7 @@ def _ranks(world, rule, dtype, steps, momentum=0.9, arch="basic"):
 def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9, arch="basic"):
     from oracle.resnet_torch import run_cdp
 
+    W, D = ARCH[arch].get("W", globals()["W"]), ARCH[arch].get("D", globals()["D"])
     fresh = None
     if rule is not None:
         fresh = [[rule.reads_fresh(i, int(s)) for s in stage] for i in range(1, world + 1)]
@@ -66,9 +76,11 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("arch", ["basic", "bottleneck"])
+@pytest.mark.parametrize("arch", ["basic", "bottleneck", "bottleneck112", "bottleneck112x4"])
 @pytest.mark.parametrize("dtype,tol", [("fp32", 2e-4), ("bf16", 3e-2)])
 def test_single_gpu_steps_vs_torch_restatement(cuda, dtype, tol, arch):
+    if dtype == "fp32":
+        tol = ARCH[arch].get("fp32_tol", tol)
     init, x, y, perms, losses, final, stage = _ranks(1, None, dtype, 3, arch=arch)
     want, wl = _oracle(init, x, y, perms, 1, None, stage, arch=arch)
     assert _rel(final, want) <= tol, _rel(final, want)
