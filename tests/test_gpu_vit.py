@@ -12,25 +12,28 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 CFG = dict(image=32, patch=8, dim=128, depth=2, heads=2, mlp=256, classes=10)
+# 56x56 / patch 4 = 196 patches + class token = 197 tokens, as ViT-B/16 at 224: attention GEMMs with two
+# M tiles (128 + 69 rows), a partial N tile and K = 197 keys over four k-blocks with out-of-bounds fill
+CFG197 = dict(image=56, patch=4, dim=128, depth=1, heads=2, mlp=256, classes=10)
 MB = 4
 
 
-def _run(world, rule, steps, momentum=0.9, lr=0.1):
+def _run(world, rule, steps, momentum=0.9, lr=0.1, cfg=CFG, mb=MB):
     from oracle.vit_torch import init_flat
     from paper_2403_08837_b200.resnet import synthetic_cifar
     from paper_2403_08837_b200.vit import DeviceVit
 
-    x, y = synthetic_cifar(world * MB * 2, seed=4, hw=CFG["image"], classes=CFG["classes"])
-    init = init_flat(**CFG, seed=0)
-    perms = [np.random.default_rng([6, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
-    tr = [DeviceVit(CFG, MB, world, r, rule, momentum, inputs=x, labels=y) for r in range(world)]
+    x, y = synthetic_cifar(world * mb * 2, seed=4, hw=cfg["image"], classes=cfg["classes"])
+    init = init_flat(**cfg, seed=0)
+    perms = [np.random.default_rng([6, t]).permutation(len(x))[: world * mb] for t in range(1, steps + 1)]
+    tr = [DeviceVit(cfg, mb, world, r, rule, momentum, inputs=x, labels=y) for r in range(world)]
     regions = [t.region() for t in tr]
     for t in tr:
         t.set_params(init, -1)
         t.connect(regions)
     for k in range(steps):
         for r, t in enumerate(tr):
-            t.step(perms[k][r * MB:(r + 1) * MB], lr)
+            t.step(perms[k][r * mb:(r + 1) * mb], lr)
     for t in tr:
         t.sync()
         assert t.ring_error() == 0
@@ -44,13 +47,13 @@ def _run(world, rule, steps, momentum=0.9, lr=0.1):
     return init, x, y, perms, losses, final, stage
 
 
-def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9, lr=0.1):
+def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9, lr=0.1, cfg=CFG, mb=MB):
     from oracle.vit_torch import run_cdp
 
     fresh = None
     if rule is not None:
         fresh = [[rule.reads_fresh(i, int(s)) for s in stage] for i in range(1, world + 1)]
-    return run_cdp(CFG, init, x.astype(np.float64), y, world, MB, perms, lr, momentum, fresh)
+    return run_cdp(cfg, init, x.astype(np.float64), y, world, mb, perms, lr, momentum, fresh)
 
 
 def _check(init, losses, final, want, wl):
@@ -73,4 +76,10 @@ def test_two_ranks_vit_cdp_vs_restatement(cuda, rule_name):
     rule = rule_by_name(rule_name, 2)
     init, x, y, perms, losses, final, stage = _run(2, rule, 3)
     want, wl = _oracle(init, x, y, perms, 2, rule, stage)
+    _check(init, losses, final, want, wl)
+
+
+def test_vit_197_tokens_vs_restatement(cuda):
+    init, x, y, perms, losses, final, stage = _run(1, None, 2, cfg=CFG197, mb=2)
+    want, wl = _oracle(init, x, y, perms, 1, None, stage, cfg=CFG197, mb=2)
     _check(init, losses, final, want, wl)
