@@ -184,96 +184,37 @@ struct EpiConvOut2 {
         int out_f32;         // 1: fp32 output rows (and `add` is fp32): the ViT residual stream
         CTensor gelu_out;    // also write gelu(out) here (compute format, own ld), or null
         const void *gelu_z;  // out *= gelu'(z), z Y-format with the output's layout, or null
-        // fused BN-backward statistics of the BN this gradient feeds (persistent, non-split only):
-        // g' = out * (bn_mask > 0); bstats[C][CTA][3] += (sum g', sum g' xhat, sum g' xhat2)
-        float *bstats;
-        CTensor bn_mask;
-        const void *bn_y, *bn_y2;            // conv outputs (Y format) of the BN (and projection BN)
-        const float *bn_mean, *bn_rstd, *bn_mean2, *bn_rstd2;
     };
     static constexpr int kStages = 0;
-    // Split-K units cannot fuse the backward statistics (partials): the caller falls back.
-    static Params for_split(const Params &p) {
-        Params q = p;
-        q.bstats = nullptr;
-        return q;
-    }
+    static Params for_split(const Params &p) { return p; }
 
     // Drain hook (per warp, lane = tile row, v = 32 consecutive columns from TMEM).
     __device__ static void drain(const Params &p, bool split, int m, int col, float (&v)[32], float *srow,
                                  float *pp) {
-        const bool fwd = p.stats && !split;
-        const bool bwd = p.bstats && !split;
-        if (bwd && p.add && m >= 0) {  // the residual branch is folded here (run() skips it)
-            const size_t o = size_t(m) * p.ld + col;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                F8 a = ld_y8<KIND>(p.add, o + 8 * k);
-                if (p.add_mask.hi) {
-                    const F8 mk = ld_c8<KIND>(p.add_mask, o + 8 * k);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) a.v[i] = mk.v[i] > 0.f ? a.v[i] : 0.f;
-                }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[8 * k + i] += a.v[i];
-            }
-        }
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
             *reinterpret_cast<float4 *>(srow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        if (fwd) {
-            float sq[32];
+        if (p.stats && !split) {  // squares in place, then the values again from the shared row (32 live)
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                v[i] = m >= 0 ? v[i] : 0.f;
-                sq[i] = v[i] * v[i];
-            }
-            pp[1] = warp_colsum32(sq);
-            pp[0] = warp_colsum32(v);
-        } else if (bwd) {
-            float t[32];
-            if (m >= 0) {
-                const size_t o = size_t(m) * p.ld + col;
+            for (int i = 0; i < 32; ++i) v[i] = m >= 0 ? v[i] * v[i] : 0.f;
+            pp[1] = warp_colsum32(v);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const F8 mk = ld_c8<KIND>(p.bn_mask, o + 8 * k);
-                    const F8 y = ld_y8<KIND>(p.bn_y, o + 8 * k);
-                    const F8 mu = ld_f8(p.bn_mean, col + 8 * k), rs = ld_f8(p.bn_rstd, col + 8 * k);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float g = mk.v[i] > 0.f ? v[8 * k + i] : 0.f;
-                        v[8 * k + i] = g;
-                        t[8 * k + i] = g * ((y.v[i] - mu.v[i]) * rs.v[i]);
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = t[i] = 0.f;
-            }
-            pp[1] = warp_colsum32(t);
-            if (p.bn_y2) {
-                if (m >= 0) {
-                    const size_t o = size_t(m) * p.ld + col;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const F8 y = ld_y8<KIND>(p.bn_y2, o + 8 * k);
-                        const F8 mu = ld_f8(p.bn_mean2, col + 8 * k), rs = ld_f8(p.bn_rstd2, col + 8 * k);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) t[8 * k + i] = v[8 * k + i] * ((y.v[i] - mu.v[i]) * rs.v[i]);
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) t[i] = 0.f;
-                }
-                pp[2] = warp_colsum32(t);
+            for (int i = 0; i < 32; i += 4) {
+                const float4 t = *reinterpret_cast<const float4 *>(srow + i);
+                v[i] = m >= 0 ? t.x : 0.f;
+                v[i + 1] = m >= 0 ? t.y : 0.f;
+                v[i + 2] = m >= 0 ? t.z : 0.f;
+                v[i + 3] = m >= 0 ? t.w : 0.f;
             }
             pp[0] = warp_colsum32(v);
         }
     }
     // Stores (8 columns per element: 16-byte bf16 / 2 x 16-byte fp32 stores).
-    template <int NTH>
+    // FIXC: ncols known at compile time (the persistent kernel's full passes), 0 = runtime.
+    template <int NTH, int FIXC = 0>
     __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
                                int ncols, int tm, int N, int tid, int64_t off) {
+        if (FIXC) ncols = FIXC;
         if (((p.ld | col0 | ncols) & 7) || (off & 7)) {  // unaligned rows (e.g. a 10-class head): scalar
             for (int e = tid; e < nrows * ncols; e += NTH) {
                 const int r = e / ncols, c = e - r * ncols;
@@ -281,7 +222,7 @@ struct EpiConvOut2 {
                 if (m < 0) continue;
                 float x = st[r * lds + c];
                 const size_t o = size_t(off) + size_t(m) * p.ld + col0 + c;
-                if (p.add && !p.bstats) {
+                if (p.add) {
                     float a = p.out_f32 ? static_cast<const float *>(p.add)[o] : Fmt<0>::load(p.add, nullptr, o);
                     if (KIND == 1 && !p.out_f32) a = static_cast<const float *>(p.add)[o];
                     if (p.add_mask.hi && !(Fmt<KIND>::load(p.add_mask.hi, p.add_mask.lo, o) > 0.f)) a = 0.f;
@@ -298,7 +239,7 @@ struct EpiConvOut2 {
             }
             return;
         }
-        const int C8 = ncols / 8;
+        const int C8 = FIXC ? FIXC / 8 : ncols / 8;
         const int total = nrows * C8;
         constexpr int U = 2;
         for (int e0 = tid; e0 < total; e0 += NTH * U) {
@@ -317,7 +258,7 @@ struct EpiConvOut2 {
                 o[u] = size_t(off) + size_t(rowm[r]) * p.ld + col0 + c;
                 gm[u] = rowm[r];
                 gc[u] = col0 + c;
-                if (p.add && !p.bstats) {
+                if (p.add) {
                     if (p.out_f32) {
                         a[u][0] = ld_f4(static_cast<const float *>(p.add), o[u]);
                         a[u][1] = ld_f4(static_cast<const float *>(p.add), o[u] + 4);
@@ -336,7 +277,7 @@ struct EpiConvOut2 {
                 if (!ok[u]) continue;
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
-                    if (p.add && !p.bstats) {
+                    if (p.add) {
                         const float4 b = p.add_mask.hi ? relu_mask4(a[u][k], mk[u][k]) : a[u][k];
                         v[u][k].x += b.x;
                         v[u][k].y += b.y;
@@ -391,42 +332,26 @@ struct EpiConvOut2 {
         if (p.stats)
             for (int a = tid; a < N; a += pcols)
                 *reinterpret_cast<float2 *>(p.stats + (size_t(a) * gridDim.x + blockIdx.x) * 2) = make_float2(0.f, 0.f);
-        if (p.bstats)
-            for (int a = tid; a < N; a += pcols) {
-                float *o = p.bstats + (size_t(a) * gridDim.x + blockIdx.x) * 3;
-                o[0] = o[1] = o[2] = 0.f;
-            }
     }
-    template <int NTH>
+    // The running value of the thread's column, loaded before the unit's accumulator is
+    // ready (hides the load latency; the same thread stored it at its previous unit).
+    using Pre = float2;
+    __device__ static Pre col_stats_pre(const Params &p, int col0, int ncols, int tid) {
+        if (!p.stats || tid >= ncols) return make_float2(0.f, 0.f);
+        return *reinterpret_cast<const float2 *>(p.stats + (size_t(col0 + tid) * gridDim.x + blockIdx.x) * 2);
+    }
+    template <int NTH>  // one column per thread (ncols <= NTH)
     __device__ static void col_stats(const Params &p, const float *part, int pcols, int col0, int ncols, int tm,
-                                     int tid) {
-        if (p.stats) {
-            for (int c = tid; c < ncols; c += NTH) {
-                float s = 0.f, q = 0.f;
+                                     int tid, Pre cur) {
+        if (p.stats && tid < ncols) {
+            float s = 0.f, q = 0.f;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    s += part[(k * pcols + c) * 3];
-                    q += part[(k * pcols + c) * 3 + 1];
-                }
-                float2 *o = reinterpret_cast<float2 *>(p.stats + (size_t(col0 + c) * gridDim.x + blockIdx.x) * 2);
-                const float2 cur = *o;
-                *o = make_float2(cur.x + s, cur.y + q);
+            for (int k = 0; k < 4; ++k) {
+                s += part[(k * pcols + tid) * 3];
+                q += part[(k * pcols + tid) * 3 + 1];
             }
-        }
-        if (p.bstats) {
-            for (int c = tid; c < ncols; c += NTH) {
-                float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    s0 += part[(k * pcols + c) * 3];
-                    s1 += part[(k * pcols + c) * 3 + 1];
-                    if (p.bn_y2) s2 += part[(k * pcols + c) * 3 + 2];
-                }
-                float *o = p.bstats + (size_t(col0 + c) * gridDim.x + blockIdx.x) * 3;
-                o[0] += s0;
-                o[1] += s1;
-                o[2] += s2;
-            }
+            *reinterpret_cast<float2 *>(p.stats + (size_t(col0 + tid) * gridDim.x + blockIdx.x) * 2) =
+                make_float2(cur.x + s, cur.y + q);
         }
     }
     // Split-K reduce kernel: the whole 128-row tile is in `st` (rows in order).  Column
@@ -478,8 +403,10 @@ struct EpiHop2 {
         for (int i = 0; i < 32; i += 4)
             *reinterpret_cast<float4 *>(srow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     }
+    struct Pre {};
+    __device__ static Pre col_stats_pre(const Params &, int, int, int) { return Pre{}; }
     template <int NTH>
-    __device__ static void col_stats(const Params &, const float *, int, int, int, int, int) {}
+    __device__ static void col_stats(const Params &, const float *, int, int, int, int, int, Pre) {}
     template <int NTH>
     __device__ static void col_stats_init(const Params &, int, int, int) {}
     template <int NTH>
@@ -487,15 +414,15 @@ struct EpiHop2 {
                                           int col0, int ncols, int tm, int N, int tid, int64_t off) {
         run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid, off);
     }
-    template <int NTH>
+    template <int NTH, int FIXC = 0>
     __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
-                               int ncols, int, int, int tid, int64_t) {
+                               int ncols, int, int, int tid, int64_t) {  // FIXC unused (register pressure)
         bool bad_g = false, bad_u = false;
         const float lr = *p.lr;
         if ((p.dout % 4) == 0 && (p.base % 4) == 0 && (ncols % 4) == 0) {
             const int C4 = ncols / 4;
             const int total = nrows * C4;
-            constexpr int U = 4;
+            constexpr int U = 2;
             for (int e0 = tid; e0 < total; e0 += NTH * U) {
                 float4 g[U], s[U], th[U], vv[U];
                 int64_t idx[U];
@@ -737,39 +664,6 @@ static __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__
     }
 }
 
-// Backward finalise of the statistics fused into the data-gradient GEMM epilogue:
-// per channel the per-CTA (sum g', sum g' xhat, sum g' xhat2) [C][CTAs][3] in CTA order
-// (fp64) -> dbeta, dgamma (and dgamma2 of the projection BN, which shares dbeta).
-static __global__ void bn_finalize_bwd_cta_kernel(const float *__restrict__ part, int nct, int C, float *dbeta,
-                                           float *dgamma, float *dbeta2, float *dgamma2) {
-    ptx::griddep_wait();
-    ptx::griddep_launch();
-    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (c >= C) return;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    const float *pc = part + size_t(c) * nct * 3;
-    for (int t = lane; t < nct; t += 32) {
-        s0 += double(pc[t * 3]);
-        s1 += double(pc[t * 3 + 1]);
-        s2 += double(pc[t * 3 + 2]);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    }
-    if (lane == 0) {
-        dbeta[c] = float(s0);
-        dgamma[c] = float(s1);
-        if (dbeta2) {
-            dbeta2[c] = float(s0);
-            dgamma2[c] = float(s2);
-        }
-    }
-}
-
 // Backward finalise: dbeta = sum g', dgamma = sum g' xhat over the row blocks in order.
 static __global__ void bn_finalize_bwd_kernel(const double *__restrict__ partial, int nblk, int C, float *dbeta,
                                        float *dgamma) {
@@ -968,7 +862,7 @@ static __global__ void __launch_bounds__(256) xent_rows_kernel(const float *__re
     for (int o = tid; o < C; o += blockDim.x) {
         const float pz = __fdiv_rn(expf(zr[o] - mx), se);
         Fmt<KIND>::store(dz.hi, dz.lo, size_t(s) * dz.ld + o, __fdiv_rn(pz - (o == lab ? 1.f : 0.f), float(B)));
-        if (o == lab) loss_rows[s] = -log(double(pz));
+        if (o == lab) loss_rows[s] = double(mx) - double(zr[o]) + log(double(se));  // finite when pz underflows
     }
 }
 

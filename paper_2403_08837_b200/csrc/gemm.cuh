@@ -120,9 +120,25 @@ __device__ __forceinline__ void load_operand(uint8_t *dst, const CUtensorMap *m,
 //          W viewed [R*S*Cin][Cout] (K-major);
 //   WGRAD: M = (tap, c), K = pixels: A = input gathered per 64-row chunk at its tap
 //          (MN-major), B = dy (MN-major), k-block = one pixel box.
-template <class C, int MODE, bool B_MN, int BN>
+// B operand of a CTA pair (CL = 2, MN-major B only): each CTA loads every other
+// 128-byte column chunk of the B tile and multicasts it to both CTAs.
+template <class C, bool MN, int BN, int CL>
+__device__ __forceinline__ void load_b(uint8_t *dst, const CUtensorMap *m, uint64_t *bar, int n0, int k0, int rank) {
+    if constexpr (CL == 1) {
+        (void)rank;
+        load_operand<C, MN, BN>(dst, m, bar, n0, k0);
+    } else {
+        static_assert(MN && BN / C::CH >= 2, "paired B loads need an MN-major B of at least two chunks");
+#pragma unroll
+        for (int c = 0; c < BN / C::CH; ++c)
+            if ((c & 1) == rank) ptx::tma_load_2d_mc(dst + c * (C::BK * 128), m, bar, n0 + c * C::CH, k0, 3);
+    }
+}
+
+template <class C, int MODE, bool B_MN, int BN, int CL = 1>
 __device__ __forceinline__ void conv_load(uint8_t *sa, uint8_t *sb, const GemmMaps &maps, const ConvGeom &g,
-                                          uint64_t *bar, int seg, int kb, int m_tile, int m0, int n0) {
+                                          uint64_t *bar, int seg, int kb, int m_tile, int m0, int n0, int rank = 0) {
+    static_assert(CL == 1 || (MODE != GM_DGRAD && B_MN && BN / C::CH >= 2), "paired B loads need an MN-major B");
     if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD) {
         const int tap = kb / g.cpt, cc = kb - tap * g.cpt;
         const int r = tap / g.S, s = tap - r * g.S;
@@ -131,7 +147,7 @@ __device__ __forceinline__ void conv_load(uint8_t *sa, uint8_t *sb, const GemmMa
         if constexpr (MODE == GM_FPROP) {
             ptx::tma_load_4d(sa, &maps.a[seg], bar, cc * C::CH, w0 * g.stride - g.pad + s, h0 * g.stride - g.pad + r,
                              b0);
-            load_operand<C, B_MN, BN>(sb, &maps.b[seg], bar, n0, kb * C::BK);
+            load_b<C, B_MN, BN, CL>(sb, &maps.b[seg], bar, n0, kb * C::BK, rank);
         } else {
             (void)r;
             (void)s;
@@ -152,8 +168,12 @@ __device__ __forceinline__ void conv_load(uint8_t *sa, uint8_t *sb, const GemmMa
                              h0 * g.stride - g.pad + r, b0);
         }
 #pragma unroll
-        for (int q = 0; q < BN / C::CH; ++q)
-            ptx::tma_load_4d(sb + q * (C::BK * 128), &maps.b[seg], bar, n0 + q * C::CH, w0, h0, b0);
+        for (int q = 0; q < BN / C::CH; ++q) {
+            if constexpr (CL == 1)
+                ptx::tma_load_4d(sb + q * (C::BK * 128), &maps.b[seg], bar, n0 + q * C::CH, w0, h0, b0);
+            else if ((q & 1) == rank)
+                ptx::tma_load_4d_mc(sb + q * (C::BK * 128), &maps.b[seg], bar, n0 + q * C::CH, w0, h0, b0, 3);
+        }
     }
 }
 

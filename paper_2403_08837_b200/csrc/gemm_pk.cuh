@@ -19,7 +19,10 @@
 // (pk_reduce_kernel) sums the partials in split order - deterministic and
 // parallel over (tile, row chunk) - and runs the same epilogue.
 #pragma once
+#include <cstdlib>
+
 #include "gemm.cuh"
+#include "host.h"
 
 namespace cdp {
 
@@ -35,6 +38,9 @@ struct PkArgs {
     // the epilogue's output offset of batch g = (g / nh) * out_bs + (g % nh) * out_hs elements
     int nbatch, nh;
     int64_t out_bs, out_hs;
+    // CTA pairs (CL = 2): units enumerate (tile-pair, tile_n, split); rank r of the
+    // pair takes M tile 2 * pair + r (>= tiles_m: a phantom that only feeds its partner)
+    int tiles_pm;
 };
 
 template <int KIND, int BN, bool A_MN, bool B_MN, int ST>
@@ -94,6 +100,20 @@ __device__ __forceinline__ void pk_unit(const PkArgs &a, int u, int &tm, int &tn
     int g;
     pk_unit(a, u, tm, tn, split, g);
 }
+template <int CL>
+__device__ __forceinline__ void pk_unit_cl(const PkArgs &a, int u, int rank, int &tm, int &tn, int &split, int &g) {
+    if constexpr (CL == 1) {
+        (void)rank;
+        pk_unit(a, u, tm, tn, split, g);
+    } else {
+        split = u % a.splits;
+        const int t = u / a.splits;
+        tn = t % a.tiles_n;
+        const int r = t / a.tiles_n;
+        tm = 2 * (r % a.tiles_pm) + rank;
+        g = r / a.tiles_pm;
+    }
+}
 
 // tile row -> output row m (or -1): pixel box rows (FPROP / DGRAD) or m0 + r.
 __device__ __forceinline__ int pk_row_m(const PkArgs &a, int tm, int r) {
@@ -105,10 +125,19 @@ __device__ __forceinline__ int pk_row_m(const PkArgs &a, int tm, int r) {
 constexpr int kPkThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kPkEpi = 256;
 
-template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE>
+// CL = 2: launched as clusters of two CTAs that process M-tile pairs sharing
+// (tile_n, split); each CTA loads its own A and half of the common B tile,
+// multicast into both CTAs' ring slot; a slot is free once BOTH CTAs' MMAs
+// have consumed it (empty barrier count 2, commits multicast to the pair).
+template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE, int CL = 1>
 __global__ void __launch_bounds__(kPkThreads, 1)
     gemm_pk_kernel(const __grid_constant__ GemmMaps maps, const PkArgs args, const typename Epi::Params ep) {
     using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages>;
+    static_assert(CL == 1 || (CL == 2 && MODE != GM_BATCH && MODE != GM_DGRAD && B_MN && BN / C::CH >= 2),
+                  "CTA pairs share an MN-major B tile of at least two chunks");
+    const int rank = CL == 1 ? 0 : int(ptx::cluster_ctarank());
+    const int first = CL == 1 ? int(blockIdx.x) : int(ptx::cluster_id_x());
+    const int stride = CL == 1 ? int(gridDim.x) : int(ptx::nclusters_x());
     extern __shared__ __align__(16) uint8_t smem_raw[];
     // 1024-byte alignment by pointer arithmetic on the shared array (keeps the
     // shared address space visible to the compiler: LDS/STS, not generic LD/ST)
@@ -134,7 +163,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     if (warp == 1 && ptx::lane_id() == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], 1);
+            ptx::mbar_init(&empty[s], CL);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
@@ -144,7 +173,10 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     }
     if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL == 1)
+        __syncthreads();
+    else
+        ptx::cluster_sync();  // the partner's barriers are initialised before any multicast
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     ptx::griddep_wait();
@@ -153,9 +185,9 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     if (warp == 0) {
         if (ptx::lane_id() == 0) {
             int it = 0;
-            for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
-                int tm, tn, sp;
-                pk_unit(args, u, tm, tn, sp);
+            for (int u = first; u < args.units; u += stride) {
+                int tm, tn, sp, g_;
+                pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g_);
                 const int lo = sp * args.iters_per_split, hi = min(args.total_iters, lo + args.iters_per_split);
                 const int m0 = tm * 128, n0 = tn * BN;
                 for (int g = lo; g < hi; ++g, ++it) {
@@ -165,7 +197,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
                     if constexpr (MODE == GM_PLAIN) {
                         load_operand<C, A_MN, 128>(sA + s * C::A_BYTES, &maps.a[seg], &full[s], m0, kb * C::BK);
-                        load_operand<C, B_MN, BN>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, kb * C::BK);
+                        load_b<C, B_MN, BN, CL>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, kb * C::BK, rank);
                     } else if constexpr (MODE == GM_BATCH) {
                         int tm2, tn2, sp2, g;
                         pk_unit(args, u, tm2, tn2, sp2, g);
@@ -187,8 +219,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                                                  n0 + c * C::CH, k0, hh, bb);
                         }
                     } else {
-                        conv_load<C, MODE, B_MN, BN>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args.cv, &full[s],
-                                                     seg, kb, tm, m0, n0);
+                        conv_load<C, MODE, B_MN, BN, CL>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args.cv,
+                                                         &full[s], seg, kb, tm, m0, n0, rank);
                     }
                 }
             }
@@ -196,9 +228,9 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     } else if (warp == 1) {
         if (ptx::lane_id() == 0) {
             int it = 0, j = 0;
-            for (int u = blockIdx.x; u < args.units; u += gridDim.x, ++j) {
-                int tm, tn, sp;
-                pk_unit(args, u, tm, tn, sp);
+            for (int u = first; u < args.units; u += stride, ++j) {
+                int tm, tn, sp, g_;
+                pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g_);
                 const int lo = sp * args.iters_per_split, hi = min(args.total_iters, lo + args.iters_per_split);
                 const int acc = j & 1;
                 if (j >= 2) ptx::mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
@@ -214,7 +246,10 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     for (int k = 0; k < C::BK / C::UMMA_K; ++k)
                         ptx::umma<KIND>(d, operand_desc<C, A_MN>(a_base, k), operand_desc<C, B_MN>(b_base, k), C::IDESC,
                                         (g > lo || k > 0) ? 1u : 0u);
-                    ptx::umma_commit(&empty[s]);
+                    if constexpr (CL == 1)
+                        ptx::umma_commit(&empty[s]);
+                    else
+                        ptx::umma_commit_mc(&empty[s], 3);
                 }
                 ptx::umma_commit(&tfull[acc]);
             }
@@ -230,12 +265,27 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             pk_bar(1, kPkEpi);
         }
         int j = 0;
-        for (int u = blockIdx.x; u < args.units; u += gridDim.x, ++j) {
+        for (int u = first; u < args.units; u += stride, ++j) {
             int tm, tn, sp, g;
-            pk_unit(args, u, tm, tn, sp, g);
+            pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g);
+            if (CL > 1 && tm >= args.tiles_m) {  // phantom tile: release the accumulator unread
+                if (tid == 0) {
+                    ptx::mbar_wait(&tfull[j & 1], (j >> 1) & 1);
+                    ptx::mbar_arrive(&tempty[j & 1]);
+                }
+                continue;
+            }
             const int64_t out_off = MODE == GM_BATCH ? (g / args.nh) * args.out_bs + (g % args.nh) * args.out_hs : 0;
             const int acc = j & 1;
             const bool split = args.splits > 1;
+            typename Epi::Pre pre[BN / C::EPI_COLS];
+            if (!split) {
+#pragma unroll
+                for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+                    const int c0 = tn * BN + h * C::EPI_COLS;
+                    pre[h] = Epi::col_stats_pre(ep, c0, min(C::EPI_COLS, args.N - c0), tid);
+                }
+            }
             if (tid < 128) rowm[tid] = pk_row_m(args, tm, tid);  // the previous unit's last barrier protects rowm / stile
             ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
             ptx::tc_fence_after();
@@ -266,10 +316,14 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                             *reinterpret_cast<const float4 *>(stile + r * C::LDS + cc);
                     }
                 } else {
-                    Epi::template run<kPkEpi>(ep, stile, C::LDS, rowm, 128, col0, min(C::EPI_COLS, args.N - col0), tm,
-                                              args.N, tid, out_off);
-                    Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), tm,
-                                                    tid);
+                    const int ncols = min(C::EPI_COLS, args.N - col0);
+                    if (ncols == C::EPI_COLS)
+                        Epi::template run<kPkEpi, C::EPI_COLS>(ep, stile, C::LDS, rowm, 128, col0, ncols, tm, args.N,
+                                                               tid, out_off);
+                    else
+                        Epi::template run<kPkEpi>(ep, stile, C::LDS, rowm, 128, col0, ncols, tm, args.N, tid, out_off);
+                    Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, ncols, tm, tid,
+                                                    h == 0 ? pre[0] : pre[BN / C::EPI_COLS - 1]);
                 }
                 pk_bar(1, kPkEpi);  // shared tile reused by the next pass / unit
             }
@@ -277,7 +331,10 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         }
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL == 1)
+        __syncthreads();
+    else
+        ptx::cluster_sync();  // the partner's last multicast commits have landed
     if (warp == 2) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
@@ -316,5 +373,66 @@ __global__ void __launch_bounds__(256) pk_reduce_kernel(const PkArgs args, const
                                       threadIdx.x, 0);
     Epi::template done<256>(ep, threadIdx.x, gridDim.x * gridDim.y * gridDim.z);
 }
+
+// ---------------------------------------------------------------- host side
+// CTA pairs are opt-in (CDP_PK_PAIRS=1): measured on B200 they are 1-4% slower than single
+// CTAs on ResNet-18/50 and ViT-B/16 (the operand fetch is not what bounds these GEMMs).
+inline bool pk_pairs_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("CDP_PK_PAIRS");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// Grid choice and launch of gemm_pk_kernel for prepared args (units = tiles x splits).
+template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE>
+struct PkLaunch {
+    using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages>;
+    static constexpr bool kPairable = MODE != GM_BATCH && MODE != GM_DGRAD && B_MN && BN / C::CH >= 2;
+
+    // Decide pairing (M tiles >= 2, pairable shape), fix up a.tiles_pm / a.units; returns the grid.
+    static int prepare(PkArgs &a, int sms, bool &paired) {
+        paired = false;
+        if constexpr (kPairable) {
+            if (pk_pairs_enabled() && a.tiles_m >= 2) {
+                paired = true;
+                a.tiles_pm = (a.tiles_m + 1) / 2;
+                a.units = a.tiles_pm * a.tiles_n * (a.nbatch > 0 ? a.nbatch : 1) * a.splits;
+                static int max_pairs = 0;
+                if (!max_pairs) {
+                    set_attr();
+                    max_pairs = std::max(1, max_active_clusters(gemm_pk_kernel<KIND, BN, A_MN, B_MN, Epi, MODE, 2>,
+                                                                kPkThreads, C::SMEM, 2));
+                }
+                return 2 * std::min(a.units, max_pairs);
+            }
+        }
+        return std::min(a.units, sms);
+    }
+    static void set_attr() {
+        static bool done = false;
+        if (done) return;
+        CDP_CUDA(cudaFuncSetAttribute(gemm_pk_kernel<KIND, BN, A_MN, B_MN, Epi, MODE, 1>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        if constexpr (kPairable)
+            CDP_CUDA(cudaFuncSetAttribute(gemm_pk_kernel<KIND, BN, A_MN, B_MN, Epi, MODE, 2>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        done = true;
+    }
+    static void launch(const GemmMaps &maps, const PkArgs &a, const typename Epi::Params &ep, cudaStream_t s, int grid,
+                       bool paired) {
+        set_attr();
+        if constexpr (kPairable) {
+            if (paired) {
+                launch_pdl_cluster(gemm_pk_kernel<KIND, BN, A_MN, B_MN, Epi, MODE, 2>, dim3(grid), dim3(kPkThreads),
+                                   C::SMEM, s, 2, maps, a, ep);
+                return;
+            }
+        }
+        launch_pdl(gemm_pk_kernel<KIND, BN, A_MN, B_MN, Epi, MODE, 1>, dim3(grid), dim3(kPkThreads), C::SMEM, s, maps,
+                   a, ep);
+    }
+};
 
 }  // namespace cdp

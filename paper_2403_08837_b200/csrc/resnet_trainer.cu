@@ -153,7 +153,7 @@ struct ResNetTrainer {
     std::vector<int64_t> act_P;
     DevBuf gbuf[4];            // fp32 gradients w.r.t. activations (block in / chain / chain / shortcut)
     CBuf cols, pooled, dz;     // stem im2col record, pooled features (+ ones column), dZ
-    DevBuf dpooled, z, loss_dev, loss_rows, stats_fwd, stats_bwd, bnpart[2], pool_arg;
+    DevBuf dpooled, z, loss_dev, loss_rows, stats_fwd, bnpart[2], pool_arg;
     int64_t max_act = 0;
     DevBuf ws_c, cnt_c, ws_h, cnt_h;
     size_t ws_c_floats = 0, ws_h_floats = 0;
@@ -344,7 +344,6 @@ struct ResNetTrainer {
         cols = make_cbuf(kind, int(c0.P), c0.K);
         for (auto &g : gbuf) g = DevBuf(size_t(max_act) * ysz());
         stats_fwd = DevBuf(size_t(max_stats) * 4);
-        stats_bwd = DevBuf(size_t(max_stats) * 2 * 4);  // [C][<=160 CTAs][3]
         bnpart[0] = DevBuf(size_t(max_part) * 8);
         bnpart[1] = DevBuf(size_t(max_part) * 8);
         if (pool_act >= 0) pool_arg = DevBuf(size_t(act_P[pool_act]) * act_C[pool_act]);
@@ -468,8 +467,6 @@ struct ResNetTrainer {
     int sms_ = 0;
     int last_stat_slots = 0, last_grid = 0;
     bool last_fused = false;
-    // BN whose backward statistics were fused into the data-gradient GEMM that produced its input
-    int fused_bn = -1, fused_slots = 0;
     int sms() {
         if (!sms_) sms_ = num_sms();
         return sms_;
@@ -478,7 +475,6 @@ struct ResNetTrainer {
     template <int K, int BNc, bool AMN, bool BMN, class Epi, int MODE>
     void run_pk(const char *name, double flops, const GemmPlan &gp, const typename Epi::Params &ep_in, cudaStream_t s,
                 bool hop) {
-        using Cfg = PkCfg<K, BNc, AMN, BMN, Epi::kStages>;
         PkArgs a{};
         a.M = gp.args.M;
         a.N = gp.args.N;
@@ -505,16 +501,12 @@ struct ResNetTrainer {
         }
         CDP_REQUIRE(need <= cap, "split-K workspace too small");
         a.ws = ws_for(hop);
-        auto kern = gemm_pk_kernel<K, BNc, AMN, BMN, Epi, MODE>;
-        static bool attr = false;
-        if (!attr) {
-            CDP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-            attr = true;
-        }
-        const int grid = std::min(a.units, sms());
+        using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;
+        bool paired = false;
+        const int grid = PL::prepare(a, sms(), paired);
         last_stat_slots = a.splits > 1 ? a.tiles_m : grid;  // EpiConvOut2 statistics rows
         last_grid = grid;
-        L(name, flops, 0.0, s, [&] { launch_pdl(kern, dim3(grid), dim3(kPkThreads), Cfg::SMEM, s, gp.maps, a, ep); });
+        L(name, flops, 0.0, s, [&] { PL::launch(gp.maps, a, ep, s, grid, paired); });
         if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
             constexpr int RC = kStats ? 128 : 16;  // 256 threads x one float4 (hop) / 8 float4 (stats)
@@ -705,20 +697,6 @@ struct ResNetTrainer {
         ConvL &c = convs[ci];
         zrecv<K>(c.tb, 1, s);
         if (ds >= 0) zrecv<K>(convs[ds].tb, 1, s);
-        if (fused_bn == ci) {  // statistics came out of the producing GEMM's epilogue
-            const int nct = sizing ? 148 : fused_slots;
-            ConvL *cd2 = ds >= 0 ? &convs[ds] : nullptr;
-            L("bn_finalize_bwd", 0, double(nct) * c.cout * 12, s, [&] {
-                launch_pdl(bn_finalize_bwd_cta_kernel, dim3((c.cout * 32 + 255) / 256), dim3(256), 0, s,
-                           (const float *)stats_bwd.as<float>(), nct, c.cout, c.dbeta.as<float>(),
-                           c.dgamma.as<float>(), cd2 ? cd2->dbeta.as<float>() : (float *)nullptr,
-                           cd2 ? cd2->dgamma.as<float>() : (float *)nullptr);
-            });
-            fused_bn = -1;
-            bn_bwd_apply<K>(ci, p, g, mask, s);
-            if (ds >= 0) bn_bwd_apply<K>(ds, p, g, mask, s);
-            return;
-        }
         const int nblk = int((c.P + kBnRows - 1) / kBnRows);
         const int C4 = c.cout / 4, TPR = C4 < 32 ? C4 : 32;
         const ConvL *cd = ds >= 0 ? &convs[ds] : nullptr;
@@ -757,11 +735,9 @@ struct ResNetTrainer {
 
     // conv data gradient into g_in (fp32 [Pin][cin]).
     // add != null: g_in = dgrad + (add masked by add_mask) (the block's residual branch).
-    // bn_ci >= 0: g_in feeds the backward of conv bn_ci's BN (+ projection bn_ds, same g'),
-    // masked by bn_mask: its statistics are fused into this GEMM's epilogue when it does not split.
     template <int K>
     void conv_dgrad(int ci, int vslot, void *g_in, cudaStream_t s, const void *add = nullptr,
-                    CTensor add_mask = CTensor{}, int bn_ci = -1, int bn_ds = -1, CTensor bn_mask = CTensor{}) {
+                    CTensor add_mask = CTensor{}) {
         ConvL &c = convs[ci];
         zrecv<K>(c.tw, 1, s);
         const CBuf &w = wc[vslot][c.tw];
@@ -769,49 +745,18 @@ struct ResNetTrainer {
         ep.stats = nullptr;
         ep.add = add;
         ep.add_mask = add_mask;
-        // Measured on B200: folding the statistics into the drain costs more (per-row operand loads
-        // while the accumulator is held) than the separate pass saves; opt-in via CDP_FUSE_BN_BWD=1.
-        static const bool fuse_env = [] {
-            const char *e = std::getenv("CDP_FUSE_BN_BWD");
-            return e && e[0] == '1';
-        }();
-        const bool want = fuse_env && bn_ci >= 0 && (c.impl == CI_PLAIN || c.stride == 1);  // not the phases
-        if (want) {
-            const ConvL &b1 = convs[bn_ci];
-            ep.bstats = stats_bwd.as<float>();
-            ep.bn_mask = bn_mask;
-            ep.bn_y = b1.y.p;
-            ep.bn_mean = b1.mean.as<float>();
-            ep.bn_rstd = b1.rstd.as<float>();
-            if (bn_ds >= 0) {
-                const ConvL &b2 = convs[bn_ds];
-                ep.bn_y2 = b2.y.p;
-                ep.bn_mean2 = b2.mean.as<float>();
-                ep.bn_rstd2 = b2.rstd.as<float>();
-            }
-        }
-        fused_bn = -1;
         if (c.impl == CI_PLAIN) {
             ep.out = g_in;
             ep.ld = c.cin;
             pk_plain<K, false, false, EpiConvOut2<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(), c.P,
                                                       c.cin, c.cout, ep, s, false);
-            if (want && (last_fused || sizing)) {
-                fused_bn = bn_ci;
-                fused_slots = last_grid;
-            }
         } else if (c.stride == 1) {
             ep.out = g_in;
             ep.ld = c.cin;
             pk_conv<K, GM_DGRAD, EpiConvOut2<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
-            if (want && (last_fused || sizing)) {
-                fused_bn = bn_ci;
-                fused_slots = last_grid;
-            }
         } else {
             // stride 2: four sub-pixel phases, each a stride-1 implicit GEMM over dy with its own taps
             // (pixels (2i + ph, 2j + pw)); phases without taps (1x1 convs) leave zeros
-            ep.bstats = nullptr;
             ep.out = g_in;
             ep.ld = c.cin;
             if (c.R == 1) {
@@ -1097,29 +1042,17 @@ struct ResNetTrainer {
                 const int ci = b.convs[i];
                 if (i > 0) {
                     void *out = chain[(n - 1 - i) & 1];
-                    conv_dgrad<K>(ci, vs(convs[ci].tw, p), out, cs, nullptr, CTensor{}, b.convs[i - 1], -1,
-                                  acts[b.mid[i - 1]].view());
+                    conv_dgrad<K>(ci, vs(convs[ci].tw, p), out, cs);
                     cudaEvent_t dg = ev(cs);
                     hop_conv<K>(ci, p, dy_next, dg);
                     bn_backward<K>(b.convs[i - 1], -1, p, out, acts[b.mid[i - 1]].view(), cs);
                     dy_next = ev(cs);
                 } else {
-                    // block input gradient = main branch + shortcut branch, written over G0; it feeds the
-                    // previous block's last BN (+ projection BN), or the stem BN (CIFAR stem)
-                    int nb = -1, nds = -1;
-                    CTensor nmask{};
-                    if (bi > 0) {
-                        nb = blocks[bi - 1].convs.back();
-                        nds = blocks[bi - 1].ds;
-                        nmask = acts[blocks[bi - 1].a_out].view();
-                    } else if (pool_act < 0) {
-                        nb = stem;
-                        nmask = acts[stem_act].view();
-                    }
+                    // block input gradient = main branch + shortcut branch, written over G0
                     if (b.ds >= 0)
-                        conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, G3, CTensor{}, nb, nds, nmask);
+                        conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, G3, CTensor{});
                     else
-                        conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, G0, m_out, nb, nds, nmask);
+                        conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, G0, m_out);
                     cudaEvent_t dg = ev(cs);
                     hop_conv<K>(ci, p, dy_next, dg);
                 }

@@ -280,7 +280,6 @@ struct VitTrainer {
     template <int BNc, bool AMN, bool BMN, class Epi, int MODE>
     void run_pk(const char *name, double flops, const GemmPlan &gp, const typename Epi::Params &ep_in, cudaStream_t s,
                 bool hop, int nh = 1, int nb = 1, int64_t out_bs = 0, int64_t out_hs = 0) {
-        using Cfg = PkCfg<0, BNc, AMN, BMN, Epi::kStages>;
         PkArgs a{};
         a.M = gp.args.M;
         a.N = gp.args.N;
@@ -308,14 +307,10 @@ struct VitTrainer {
         }
         CDP_REQUIRE(need <= cap, "split-K workspace too small");
         a.ws = ws_for(hop);
-        auto kern = gemm_pk_kernel<0, BNc, AMN, BMN, Epi, MODE>;
-        static bool attr = false;
-        if (!attr) {
-            CDP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-            attr = true;
-        }
-        const int grid = std::min(a.units, sms());
-        L_(name, flops, 0.0, s, [&] { launch_pdl(kern, dim3(grid), dim3(kPkThreads), Cfg::SMEM, s, gp.maps, a, ep); });
+        using PL = PkLaunch<0, BNc, AMN, BMN, Epi, MODE>;
+        bool paired = false;
+        const int grid = PL::prepare(a, sms(), paired);
+        L_(name, flops, 0.0, s, [&] { PL::launch(gp.maps, a, ep, s, grid, paired); });
         if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<0>>::value;
             constexpr int RC = kStats ? 128 : 16;  // 256 threads x one float4 (hop) / 8 float4 (stats)

@@ -226,13 +226,13 @@ def test_dp_allreduce_baseline_bit_identical_to_dp_ring(cuda):
     assert np.array_equal(out[True][1], out[False][1])
 
 
-def test_fused_bn_backward_statistics_option(cuda, monkeypatch):
-    """CDP_FUSE_BN_BWD=1 (BN-backward statistics reduced in the data-gradient GEMM's drain) matches the
-    float64 restatement like the default path (checked in a subprocess: the option is read once)."""
+def test_cta_pair_option(cuda):
+    """CDP_PK_PAIRS=1 (persistent GEMMs as 2-CTA clusters sharing the B tile through TMA multicast,
+    including a phantom tile for odd M-tile counts) matches the float64 restatement like the default
+    path (checked in a subprocess: the option is read once per process)."""
+    import os
     import subprocess
     import sys
-
-    import os
 
     here = os.path.abspath(__file__)
     code = ("import importlib.util as U, sys;"
@@ -241,8 +241,7 @@ def test_fused_bn_backward_statistics_option(cuda, monkeypatch):
             "init, x, y, perms, losses, final, stage = T._ranks(1, None, 'fp32', 3, arch='bottleneck');"
             "want, wl = T._oracle(init, x, y, perms, 1, None, stage, arch='bottleneck');"
             "assert T._rel(final, want) <= 2e-4, T._rel(final, want); print('ok')")
-
-    env = dict(os.environ, CDP_FUSE_BN_BWD="1")
+    env = dict(os.environ, CDP_PK_PAIRS="1")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+                       cwd=os.path.dirname(os.path.dirname(here)))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
