@@ -547,6 +547,35 @@ struct BnResidual {
     const float *mean, *rstd, *gamma, *beta;
 };
 
+// One thread keeps its 8 channels for the whole grid-stride loop when the stride is a
+// multiple of C/8 (always, for 256-thread blocks and C <= 2048): the per-channel
+// parameters are loaded once instead of per element.
+template <int KIND>
+__device__ __forceinline__ void bn_apply_elem(const void *__restrict__ y, size_t o, const F8 &mu, const F8 &rs,
+                                              const F8 &ga, const F8 &be, const BnResidual &res, const F8 &m2,
+                                              const F8 &r2, const F8 &g2, const F8 &b2, int relu, CTensor out) {
+    const F8 x = ld_y8<KIND>(y, o);
+    F8 ra, rx;
+    if (res.act.hi) ra = ld_c8<KIND>(res.act, o);
+    if (res.y) rx = ld_y8<KIND>(res.y, o);
+    F8 v;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v.v[k] = ga.v[k] * ((x.v[k] - mu.v[k]) * rs.v[k]) + be.v[k];
+    if (res.act.hi) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v.v[k] += ra.v[k];
+    }
+    if (res.y) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v.v[k] += g2.v[k] * ((rx.v[k] - m2.v[k]) * r2.v[k]) + b2.v[k];
+    }
+    if (relu) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v.v[k] = fmaxf(v.v[k], 0.f);
+    }
+    st_c8<KIND>(out, o, v);
+}
+
 template <int KIND>
 static __global__ void bn_apply_kernel(const void *__restrict__ y, int64_t P, int C, const float *mean, const float *rstd,
                                 const float *gamma, const float *beta, BnResidual res, int relu, CTensor out) {
@@ -554,31 +583,32 @@ static __global__ void bn_apply_kernel(const void *__restrict__ y, int64_t P, in
     ptx::griddep_launch();
     const int C8 = C / 8;
     const int64_t n = P * C8;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (stride % C8 == 0) {
         const int c = int(i % C8) * 8;
-        const size_t o = size_t(i) * 8;
-        const F8 x = ld_y8<KIND>(y, o);
-        F8 ra, rx;
-        if (res.act.hi) ra = ld_c8<KIND>(res.act, o);
-        if (res.y) rx = ld_y8<KIND>(res.y, o);
         const F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), be = ld_f8(beta, c);
-        F8 v;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v.v[k] = ga.v[k] * ((x.v[k] - mu.v[k]) * rs.v[k]) + be.v[k];
-        if (res.act.hi) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v.v[k] += ra.v[k];
-        }
+        F8 m2{}, r2{}, g2{}, b2{};
         if (res.y) {
-            const F8 m2 = ld_f8(res.mean, c), r2 = ld_f8(res.rstd, c), g2 = ld_f8(res.gamma, c), b2 = ld_f8(res.beta, c);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v.v[k] += g2.v[k] * ((rx.v[k] - m2.v[k]) * r2.v[k]) + b2.v[k];
+            m2 = ld_f8(res.mean, c);
+            r2 = ld_f8(res.rstd, c);
+            g2 = ld_f8(res.gamma, c);
+            b2 = ld_f8(res.beta, c);
         }
-        if (relu) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v.v[k] = fmaxf(v.v[k], 0.f);
+        for (; i < n; i += stride) bn_apply_elem<KIND>(y, size_t(i) * 8, mu, rs, ga, be, res, m2, r2, g2, b2, relu, out);
+        return;
+    }
+    for (; i < n; i += stride) {
+        const int c = int(i % C8) * 8;
+        F8 m2{}, r2{}, g2{}, b2{};
+        if (res.y) {
+            m2 = ld_f8(res.mean, c);
+            r2 = ld_f8(res.rstd, c);
+            g2 = ld_f8(res.gamma, c);
+            b2 = ld_f8(res.beta, c);
         }
-        st_c8<KIND>(out, o, v);
+        bn_apply_elem<KIND>(y, size_t(i) * 8, ld_f8(mean, c), ld_f8(rstd, c), ld_f8(gamma, c), ld_f8(beta, c), res, m2,
+                            r2, g2, b2, relu, out);
     }
 }
 
@@ -701,15 +731,25 @@ static __global__ void bn_bwd_apply_kernel(const void *__restrict__ g, CTensor m
     const int C8 = C / 8;
     const int64_t n = P * C8;
     const float inv = 1.f / float(P);
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % C8) * 8;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const bool fixed = stride % C8 == 0;  // the thread's channels never change (parameters loaded once)
+    int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    int c = int(i % C8) * 8;
+    F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), db = ld_f8(dbeta, c), dg = ld_f8(dgamma, c);
+    for (; i < n; i += stride) {
+        if (!fixed) {
+            c = int(i % C8) * 8;
+            mu = ld_f8(mean, c);
+            rs = ld_f8(rstd, c);
+            ga = ld_f8(gamma, c);
+            db = ld_f8(dbeta, c);
+            dg = ld_f8(dgamma, c);
+        }
         const size_t o = size_t(i) * 8;
         F8 gv = ld_y8<KIND>(g, o);
         const F8 x = ld_y8<KIND>(y, o);
         F8 mk;
         if (mask.hi) mk = ld_c8<KIND>(mask, o);
-        const F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), db = ld_f8(dbeta, c),
-                 dg = ld_f8(dgamma, c);
         F8 d;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {

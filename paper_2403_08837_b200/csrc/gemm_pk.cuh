@@ -369,8 +369,9 @@ __global__ void __launch_bounds__(256) pk_reduce_kernel(const PkArgs args, const
     }
     __syncthreads();
     const int col0 = tn * BN + c0;
-    Epi::template run_with_stats<256>(ep, st, CC + 4, rowm, RC, col0, min(CC, args.N - col0), tm, args.N,
-                                      threadIdx.x, 0);
+    // statistics slot of this row chunk: tm * (128 / RC) + chunk (the caller sizes ep.tiles accordingly)
+    Epi::template run_with_stats<256>(ep, st, CC + 4, rowm, RC, col0, min(CC, args.N - col0),
+                                      tm * (128 / RC) + int(blockIdx.y), args.N, threadIdx.x, 0);
     Epi::template done<256>(ep, threadIdx.x, gridDim.x * gridDim.y * gridDim.z);
 }
 

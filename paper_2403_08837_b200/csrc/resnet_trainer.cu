@@ -337,7 +337,7 @@ struct ResNetTrainer {
             c.dbeta = DevBuf(c.cout * 4);
             c.dgamma = DevBuf(c.cout * 4);
             c.dy = make_cbuf(kind, int(c.P), c.cout);
-            max_stats = std::max<int64_t>(max_stats, int64_t(std::max(c.tiles_fwd, 160)) * c.cout * 2);
+            max_stats = std::max<int64_t>(max_stats, int64_t(std::max(4 * c.tiles_fwd, 160)) * c.cout * 2);
             max_part = std::max<int64_t>(max_part, ((c.P + kBnRows - 1) / kBnRows) * c.cout * 2);
         }
         const ConvL &c0 = convs[stem];
@@ -490,7 +490,9 @@ struct ResNetTrainer {
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
         a.units = tiles * a.splits;
         last_fused = a.splits == 1;
-        const typename Epi::Params ep = a.splits > 1 ? Epi::for_split(ep_in) : ep_in;
+        typename Epi::Params ep = a.splits > 1 ? Epi::for_split(ep_in) : ep_in;
+        if constexpr (std::is_same<Epi, EpiConvOut2<K>>::value)
+            if (a.splits > 1) ep.tiles = a.tiles_m * 4;  // one statistics slot per 32-row chunk of a tile
         a.boxed = (MODE == GM_FPROP || MODE == GM_DGRAD) ? 1 : 0;
         a.cv = gp.args.cv;
         const size_t need = a.splits > 1 ? size_t(tiles) * a.splits * 128 * BNc : 0;
@@ -504,12 +506,12 @@ struct ResNetTrainer {
         using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;
         bool paired = false;
         const int grid = PL::prepare(a, sms(), paired);
-        last_stat_slots = a.splits > 1 ? a.tiles_m : grid;  // EpiConvOut2 statistics rows
+        last_stat_slots = a.splits > 1 ? a.tiles_m * 4 : grid;  // EpiConvOut2 statistics rows (RC = 32 below)
         last_grid = grid;
         L(name, flops, 0.0, s, [&] { PL::launch(gp.maps, a, ep, s, grid, paired); });
         if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
-            constexpr int RC = kStats ? 128 : 16;  // 256 threads x one float4 (hop) / 8 float4 (stats)
+            constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
             constexpr int CC = 64;
             L("splitk_reduce", 0, double(need) * 4, s, [&] {
                 launch_pdl(pk_reduce_kernel<BNc, Epi, RC, CC>, dim3(tiles, 128 / RC, BNc / CC), dim3(256), 0, s, a,

@@ -313,7 +313,7 @@ struct VitTrainer {
         L_(name, flops, 0.0, s, [&] { PL::launch(gp.maps, a, ep, s, grid, paired); });
         if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<0>>::value;
-            constexpr int RC = kStats ? 128 : 16;  // 256 threads x one float4 (hop) / 8 float4 (stats)
+            constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
             constexpr int CC = 64;
             L_("splitk_reduce", 0, double(need) * 4, s, [&] {
                 launch_pdl(pk_reduce_kernel<BNc, Epi, RC, CC>, dim3(tiles, 128 / RC, BNc / CC), dim3(256), 0, s, a,
