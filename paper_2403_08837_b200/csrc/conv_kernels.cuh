@@ -187,6 +187,14 @@ struct EpiConvOut2 {
     };
     static constexpr int kStages = 0;
     static Params for_split(const Params &p) { return p; }
+    // plain bf16 output rows (no residual / GELU / fp32 stream): the persistent kernel may store
+    // the tile with TMA (gemm_pk_kernel, PkArgs::tma_out)
+    static constexpr bool kTmaStore = KIND == 0;
+    static bool tma_eligible(const Params &p) {
+        return KIND == 0 && p.out && !p.add && !p.gelu_z && !p.gelu_out.hi && !p.out_f32 && (p.ld % 8) == 0 &&
+               (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
+    }
+    __device__ static bool has_stats(const Params &p) { return p.stats != nullptr; }
 
     // Drain hook (per warp, lane = tile row, v = 32 consecutive columns from TMEM).
     __device__ static void drain(const Params &p, bool split, int m, int col, float (&v)[32], float *srow,
@@ -398,6 +406,7 @@ struct EpiHop2 {
     using Params = HopParams;
     static constexpr int kStages = 0;
     static Params for_split(const Params &p) { return p; }
+    static constexpr bool kTmaStore = false;
     __device__ static void drain(const Params &, bool, int, int, float (&v)[32], float *srow, float *) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4)

@@ -23,6 +23,7 @@ namespace cdp {
 struct GemmMaps {
     CUtensorMap a[3];
     CUtensorMap b[3];
+    CUtensorMap o;  // output tile map of the TMA-store epilogue (gemm_pk_kernel, PkArgs::tma_out)
 };
 
 // Implicit-GEMM convolution geometry (MODE 1-3 of gemm_tc_kernel).  Pixels

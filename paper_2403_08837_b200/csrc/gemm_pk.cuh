@@ -19,6 +19,8 @@
 // (pk_reduce_kernel) sums the partials in split order - deterministic and
 // parallel over (tile, row chunk) - and runs the same epilogue.
 #pragma once
+#include <cuda_bf16.h>
+
 #include <cstdlib>
 
 #include "gemm.cuh"
@@ -41,6 +43,10 @@ struct PkArgs {
     // CTA pairs (CL = 2): units enumerate (tile-pair, tile_n, split); rank r of the
     // pair takes M tile 2 * pair + r (>= tiles_m: a phantom that only feeds its partner)
     int tiles_pm;
+    // TMA-store epilogue (Epi::kTmaStore, non-split units): the tile is converted to bf16 into a
+    // 128-byte-swizzled shared staging area in 64-column chunks and written by TMA through maps.o
+    // (2-D {N, M} for GM_PLAIN, 4-D {N, W, H, B} with the pixel box for FPROP / stride-1 DGRAD)
+    int tma_out;
 };
 
 template <int KIND, int BN, bool A_MN, bool B_MN, int ST>
@@ -120,6 +126,11 @@ __device__ __forceinline__ int pk_row_m(const PkArgs &a, int tm, int r) {
     if (a.boxed) return conv_box_row(a.cv, tm, r);
     const int m = tm * 128 + r;
     return m < a.M ? m : -1;
+}
+
+__device__ __forceinline__ uint32_t pk_bf16x2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
 }
 
 constexpr int kPkThreads = 384;  // 4 control warps + 8 epilogue warps
@@ -264,6 +275,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             Epi::template col_stats_init<kPkEpi>(ep, args.N, C::EPI_COLS, tid);
             pk_bar(1, kPkEpi);
         }
+        uint8_t *stage = smem + C::STAGES * C::STAGE_BYTES;  // bf16 staging of the TMA store (aliases stile)
+        static_assert(!Epi::kTmaStore || BN * 256 <= C::STILE_BYTES, "TMA staging exceeds the shared tile");
         int j = 0;
         for (int u = first; u < args.units; u += stride, ++j) {
             int tm, tn, sp, g;
@@ -278,6 +291,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             const int64_t out_off = MODE == GM_BATCH ? (g / args.nh) * args.out_bs + (g % args.nh) * args.out_hs : 0;
             const int acc = j & 1;
             const bool split = args.splits > 1;
+            const bool tma = Epi::kTmaStore && args.tma_out && !split;
             typename Epi::Pre pre[BN / C::EPI_COLS];
             if (!split) {
 #pragma unroll
@@ -287,9 +301,78 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 }
             }
             if (tid < 128) rowm[tid] = pk_row_m(args, tm, tid);  // the previous unit's last barrier protects rowm / stile
+            if constexpr (Epi::kTmaStore) {
+                if (tma) {  // the previous unit's TMA stores have read the staging area
+                    if (tid == 0) ptx::bulk_wait_read0();
+                    pk_bar(1, kPkEpi);
+                }
+            }
             ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
             ptx::tc_fence_after();
             const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+            if constexpr (Epi::kTmaStore) {
+                if (tma) {
+                    const int row_m = pk_row_m(args, tm, row);
+                    const bool stats = Epi::has_stats(ep);
+#pragma unroll 1
+                    for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+#pragma unroll 1
+                        for (int c = half * HC; c < (half + 1) * HC; c += 32) {
+                            const int uc = h * C::EPI_COLS + c;  // column within the unit
+                            float v[32];
+                            ptx::tmem_ld32(taddr + uc, v);
+                            uint8_t *rp = stage + (uc >> 6) * 16384 + row * 128;
+                            const int u0 = (uc & 63) >> 3;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                uint4 w;
+                                w.x = pk_bf16x2(v[8 * i], v[8 * i + 1]);
+                                w.y = pk_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+                                w.z = pk_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+                                w.w = pk_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+                                *reinterpret_cast<uint4 *>(rp + (((u0 + i) ^ (row & 7)) << 4)) = w;
+                            }
+                            if (stats) {  // squares in place, then the values again from TMEM (32 live)
+                                float *pp = spart + (q * C::EPI_COLS + c + ptx::lane_id()) * 3;
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) v[i] = row_m >= 0 ? v[i] * v[i] : 0.f;
+                                pp[1] = warp_colsum32(v);
+                                ptx::tmem_ld32(taddr + uc, v);
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) v[i] = row_m >= 0 ? v[i] : 0.f;
+                                pp[0] = warp_colsum32(v);
+                            }
+                        }
+                        ptx::fence_proxy_async_smem();  // staging writes -> async proxy (TMA store)
+                        if (h == BN / C::EPI_COLS - 1) ptx::tc_fence_before();
+                        pk_bar(1, kPkEpi);
+                        if (h == BN / C::EPI_COLS - 1 && tid == 0) ptx::mbar_arrive(&tempty[acc]);
+                        const int col0 = tn * BN + h * C::EPI_COLS;
+                        if (tid == 0) {
+#pragma unroll 1
+                            for (int k = 0; k < C::EPI_COLS / 64; ++k) {
+                                const int col = col0 + k * 64;
+                                if (col >= args.N) break;
+                                const uint8_t *src = stage + ((h * C::EPI_COLS) / 64 + k) * 16384;
+                                if (args.boxed) {
+                                    int w0, h0, b0;
+                                    conv_box_origin(args.cv, tm, w0, h0, b0);
+                                    ptx::tma_store_4d(&maps.o, src, col, w0, h0, b0);
+                                } else {
+                                    ptx::tma_store_2d(&maps.o, src, col, tm * 128);
+                                }
+                            }
+                            ptx::bulk_commit();
+                        }
+                        if (stats)
+                            Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0,
+                                                            min(C::EPI_COLS, args.N - col0), tm, tid,
+                                                            h == 0 ? pre[0] : pre[BN / C::EPI_COLS - 1]);
+                        pk_bar(1, kPkEpi);  // spart reused by the next pass
+                    }
+                    continue;
+                }
+            }
 #pragma unroll 1
             for (int h = 0; h < BN / C::EPI_COLS; ++h) {
                 const int row_m = pk_row_m(args, tm, row);  // own computation: rowm is not yet synced
@@ -329,6 +412,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             }
             if (!split) Epi::template done<kPkEpi>(ep, tid, unsigned(args.tiles_m * args.tiles_n));
         }
+        if constexpr (Epi::kTmaStore)
+            if (tid == 0) ptx::bulk_wait0();  // TMA stores complete before the CTA exits
     }
     ptx::tc_fence_before();
     if constexpr (CL == 1)
@@ -410,6 +495,31 @@ struct PkLaunch {
             }
         }
         return std::min(a.units, sms);
+    }
+    // TMA-store epilogue for plain bf16 outputs of non-split units (CDP_PK_TMA_STORE=0 disables).
+    static void setup_tma_out(GemmMaps &maps, PkArgs &a, const typename Epi::Params &ep) {
+        a.tma_out = 0;
+        if constexpr (Epi::kTmaStore) {
+            static const bool on = [] {
+                const char *e = std::getenv("CDP_PK_TMA_STORE");
+                return !(e && e[0] == '0');
+            }();
+            if (!on || a.splits > 1 || MODE == GM_BATCH || MODE == GM_WGRAD || a.N < 64 || !Epi::tma_eligible(ep))
+                return;
+            const uint64_t rs = uint64_t(ep.ld) * 2;
+            if (MODE == GM_PLAIN) {
+                maps.o = make_tmap_2d(ep.out, ElemType::BF16, uint64_t(a.N), uint64_t(a.M), rs, 64, 128);
+            } else {
+                const ConvGeom &g = a.cv;
+                if (g.omul != 1 || g.oH != g.Ho || g.oW != g.Wo) return;  // sub-pixel phase outputs
+                const uint64_t dims[4] = {uint64_t(a.N), uint64_t(g.Wo), uint64_t(g.Ho), uint64_t(g.Bn)};
+                const uint64_t str[3] = {rs, rs * g.Wo, rs * g.Wo * g.Ho};
+                const uint32_t box[4] = {64, uint32_t(g.bw), uint32_t(g.bh), uint32_t(g.bn)};
+                const uint32_t es[4] = {1, 1, 1, 1};
+                maps.o = make_tmap_4d(ep.out, ElemType::BF16, dims, str, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
+            }
+            a.tma_out = 1;
+        }
     }
     static void set_attr() {
         static bool done = false;

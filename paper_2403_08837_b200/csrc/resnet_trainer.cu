@@ -506,9 +506,11 @@ struct ResNetTrainer {
         using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;
         bool paired = false;
         const int grid = PL::prepare(a, sms(), paired);
+        GemmMaps maps = gp.maps;
+        PL::setup_tma_out(maps, a, ep);
         last_stat_slots = a.splits > 1 ? a.tiles_m * 4 : grid;  // EpiConvOut2 statistics rows (RC = 32 below)
         last_grid = grid;
-        L(name, flops, 0.0, s, [&] { PL::launch(gp.maps, a, ep, s, grid, paired); });
+        L(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
         if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
             constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)

@@ -310,7 +310,9 @@ struct VitTrainer {
         using PL = PkLaunch<0, BNc, AMN, BMN, Epi, MODE>;
         bool paired = false;
         const int grid = PL::prepare(a, sms(), paired);
-        L_(name, flops, 0.0, s, [&] { PL::launch(gp.maps, a, ep, s, grid, paired); });
+        GemmMaps maps = gp.maps;
+        PL::setup_tma_out(maps, a, ep);
+        L_(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
         if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<0>>::value;
             constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
