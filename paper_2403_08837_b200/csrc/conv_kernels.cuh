@@ -195,6 +195,16 @@ struct EpiConvOut2 {
                (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
     }
     __device__ static bool has_stats(const Params &p) { return p.stats != nullptr; }
+    // Unit start (persistent kernel, one thread per tile row): pull the row's extra operands
+    // (residual, mask, GELU input) into L2 while the mainloop runs.
+    __device__ static void prefetch_row(const Params &p, int m, int col0, int ncols, int64_t off) {
+        if (m < 0 || ((p.ld | col0 | ncols) & 7) || (off & 7)) return;
+        const size_t o = size_t(off) + size_t(m) * p.ld + col0;
+        const int ab = (p.out_f32 || KIND == 1) ? 4 : 2;
+        if (p.add) ptx::prefetch_l2(static_cast<const char *>(p.add) + o * ab, uint32_t(ncols * ab));
+        if (KIND == 0 && p.add_mask.hi) ptx::prefetch_l2(static_cast<const char *>(p.add_mask.hi) + o * 2, uint32_t(ncols * 2));
+        if (KIND == 0 && p.gelu_z) ptx::prefetch_l2(static_cast<const char *>(p.gelu_z) + o * 2, uint32_t(ncols * 2));
+    }
 
     // Drain hook (per warp, lane = tile row, v = 32 consecutive columns from TMEM).
     __device__ static void drain(const Params &p, bool split, int m, int col, float (&v)[32], float *srow,
@@ -407,6 +417,17 @@ struct EpiHop2 {
     static constexpr int kStages = 0;
     static Params for_split(const Params &p) { return p; }
     static constexpr bool kTmaStore = false;
+    // Unit start: pull the row's optimizer state (partial sum, theta, velocity) into L2.
+    __device__ static void prefetch_row(const Params &p, int m, int col0, int ncols, int64_t) {
+        if (m < 0 || (p.dout % 4) || (p.base % 4) || (col0 % 4) || (ncols % 4)) return;
+        const int64_t idx = p.base + int64_t(m) * p.dout + col0;
+        const uint32_t bytes = uint32_t(ncols) * 4;
+        if (p.mode == 1 || p.mode == 2) ptx::prefetch_l2(p.s_in + idx, bytes);
+        if (p.mode == 2 || p.mode == 3) {
+            ptx::prefetch_l2(p.theta_cur + idx, bytes);
+            if (p.momentum != 0.f) ptx::prefetch_l2(p.vel + idx, bytes);
+        }
+    }
     __device__ static void drain(const Params &, bool, int, int, float (&v)[32], float *srow, float *) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4)

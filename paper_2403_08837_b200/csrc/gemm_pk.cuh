@@ -275,8 +275,11 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             Epi::template col_stats_init<kPkEpi>(ep, args.N, C::EPI_COLS, tid);
             pk_bar(1, kPkEpi);
         }
-        uint8_t *stage = smem + C::STAGES * C::STAGE_BYTES;  // bf16 staging of the TMA store (aliases stile)
-        static_assert(!Epi::kTmaStore || BN * 256 <= C::STILE_BYTES, "TMA staging exceeds the shared tile");
+        // bf16 staging of the TMA store (aliases stile): two buffers of one pass (EPI_COLS columns) each,
+        // alternating per pass; a buffer is rewritten only after its previous store group was read
+        uint8_t *stage = smem + C::STAGES * C::STAGE_BYTES;
+        static_assert(!Epi::kTmaStore || 2 * C::EPI_COLS * 256 <= C::STILE_BYTES, "TMA staging exceeds the shared tile");
+        int pc = 0;  // TMA passes issued by this CTA
         int j = 0;
         for (int u = first; u < args.units; u += stride, ++j) {
             int tm, tn, sp, g;
@@ -300,12 +303,10 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     pre[h] = Epi::col_stats_pre(ep, c0, min(C::EPI_COLS, args.N - c0), tid);
                 }
             }
-            if (tid < 128) rowm[tid] = pk_row_m(args, tm, tid);  // the previous unit's last barrier protects rowm / stile
-            if constexpr (Epi::kTmaStore) {
-                if (tma) {  // the previous unit's TMA stores have read the staging area
-                    if (tid == 0) ptx::bulk_wait_read0();
-                    pk_bar(1, kPkEpi);
-                }
+            if (tid < 128) {  // the previous unit's last barrier protects rowm / stile
+                const int m = pk_row_m(args, tm, tid);
+                rowm[tid] = m;
+                if (!split) Epi::prefetch_row(ep, m, tn * BN, min(BN, args.N - tn * BN), out_off);
             }
             ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
             ptx::tc_fence_after();
@@ -315,14 +316,15 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     const int row_m = pk_row_m(args, tm, row);
                     const bool stats = Epi::has_stats(ep);
 #pragma unroll 1
-                    for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+                    for (int h = 0; h < BN / C::EPI_COLS; ++h, ++pc) {
+                        uint8_t *buf = stage + (pc & 1) * (C::EPI_COLS * 256);
 #pragma unroll 1
                         for (int c = half * HC; c < (half + 1) * HC; c += 32) {
                             const int uc = h * C::EPI_COLS + c;  // column within the unit
                             float v[32];
                             ptx::tmem_ld32(taddr + uc, v);
-                            uint8_t *rp = stage + (uc >> 6) * 16384 + row * 128;
-                            const int u0 = (uc & 63) >> 3;
+                            uint8_t *rp = buf + (c >> 6) * 16384 + row * 128;
+                            const int u0 = (c & 63) >> 3;
 #pragma unroll
                             for (int i = 0; i < 4; ++i) {
                                 uint4 w;
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                             for (int k = 0; k < C::EPI_COLS / 64; ++k) {
                                 const int col = col0 + k * 64;
                                 if (col >= args.N) break;
-                                const uint8_t *src = stage + ((h * C::EPI_COLS) / 64 + k) * 16384;
+                                const uint8_t *src = buf + k * 16384;
                                 if (args.boxed) {
                                     int w0, h0, b0;
                                     conv_box_origin(args.cv, tm, w0, h0, b0);
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                                 }
                             }
                             ptx::bulk_commit();
+                            ptx::bulk_wait_read1();  // the other buffer (previous pass) is free again
                         }
                         if (stats)
                             Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0,
