@@ -499,12 +499,14 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     d = gemm[dom]
     peak, src = peak_tensor()
     achieved = d[2] / (d[1] / 1e3) / 1e12
+    # DRAM bytes per launch of the same class from an ncu capture of one serialised step
+    # (tools/step_traffic.py; bf16 only)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r1_resnet_traffic.json")
-    if os.path.exists(tp):
+    tp = os.path.join(ROOT, "profiles", "r1_step_traffic.json")
+    if os.path.exists(tp) and args.dtype == "bf16":
         with open(tp) as fh:
-            traffic = (json.load(fh).get(f"{model}-{args.dtype}-{dom}") or {}).get("dram_bytes_per_launch")
-    out["roofline"] = {"bound": "tensor", "kernel": f"{dom} (gemm_tc_kernel, tcgen05 + TMA; {d[0]} launches)",
+            traffic = ((json.load(fh).get(model) or {}).get(dom) or {}).get("dram_bytes_per_launch")
+    out["roofline"] = {"bound": "tensor", "kernel": f"{dom} (gemm_pk_kernel, tcgen05 + TMA; {d[0]} launches)",
                        "achieved": round(achieved, 1), "peak": peak, "peak_source": src, "unit": "TFLOP/s",
                        "frac": round(achieved / peak, 4), "traffic": traffic,
                        "algorithmic_flops_per_launch": round(d[2] / d[0]), "launch_us": round(d[1] / d[0] * 1e3, 2),

@@ -175,7 +175,7 @@ class DeviceVit:
                                               fl.ctypes.data_as(N.c_double_p), by.ctypes.data_as(N.c_double_p),
                                               ms.ctypes.data_as(N.c_float_p), ctypes.byref(n)))
         raw = names.raw
-        return [(raw[i * NL:(i + 1) * NL].split(b"\\0", 1)[0].decode(), float(fl[i]), float(by[i]), float(ms[i]))
+        return [(raw[i * NL:(i + 1) * NL].split(b"\0", 1)[0].decode(), float(fl[i]), float(by[i]), float(ms[i]))
                 for i in range(min(n.value, max_ops))]
 
     def history(self, max_steps=1 << 14):

@@ -1,11 +1,11 @@
 """Quick timing probe of the ResNet CDP step on one GPU (development tool, not the bench).
-env: ARCH=resnet18|resnet50  MB  DT  STEPS  PROFILE=1 (per-kernel table from the instrumented step)"""
+env: CDP_ARCH=resnet18|resnet50 (not ARCH: the ncu launcher script overwrites it)  MB  DT  STEPS  PROFILE=1 (per-kernel table from the instrumented step)"""
 import collections, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2403_08837_b200.resnet import DeviceResNet, synthetic_cifar, RESNET18, RESNET50, layer_specs
 
-arch = os.environ.get("ARCH", "resnet18")
+arch = os.environ.get("CDP_ARCH", "resnet18")
 cfg = dict(RESNET18) if arch == "resnet18" else dict(RESNET50)
 hw, classes = (32, 10) if arch == "resnet18" else (224, 1000)
 B = int(os.environ.get("MB", "128"))
