@@ -1,4 +1,4 @@
-for M in resnet18 resnet50 vit_b16; do
-timeout 900 ncu --profile-from-start off --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file gpurun_out/${M}_traffic.csv python tools/step_traffic.py $M gpurun_out/${M}_ops.json > gpurun_out/${M}_traffic.log 2>&1
-echo "$M rc=$?"; tail -2 gpurun_out/${M}_traffic.log
-done
+timeout 900 python -m pytest tests/test_gpu_resnet.py tests/test_gpu_vit.py -m gpu -x -q 2>&1 | tail -2
+CDP_ARCH=resnet18 STEPS=20 PROFILE=1 timeout 300 python tools/resnet_probe.py 2>&1 | head -8
+CDP_ARCH=resnet50 STEPS=10 timeout 300 python tools/resnet_probe.py 2>&1 | head -1
+STEPS=10 PROFILE=1 timeout 300 python tools/vit_probe.py 2>&1 | head -14

@@ -178,6 +178,113 @@ __device__ __forceinline__ void conv_load(uint8_t *sa, uint8_t *sb, const GemmMa
     }
 }
 
+// Producer-side iterator over the k-blocks of one unit of the persistent kernel
+// (gemm_pk_kernel): the same loads as conv_load, with the per-unit geometry
+// hoisted and the per-k-block indices advanced by counters instead of integer
+// division (the single producer thread's address arithmetic was the mainloop's
+// critical path for the implicit-conv modes).
+template <class C, int MODE>
+struct ConvIter {
+    static constexpr int NQ = 128 / C::CH;  // 128-byte column chunks of the 128-row A tile (WGRAD)
+    int seg, kb, kb_per_seg;
+    int tap, cc, r, s;  // FPROP / DGRAD: k-block = (tap, channel chunk)
+    int w0, h0, b0;     // FPROP / DGRAD: the M tile's pixel box; WGRAD: the k-block's pixel box
+    int iw, ih;         // WGRAD: pixel box counters
+    int qc[NQ], qs[NQ], qr[NQ];  // WGRAD: channel / tap (s, r) of each A chunk
+
+    __device__ __forceinline__ void init(const ConvGeom &g, int kbps, int lo, int m_tile, int m0) {
+        kb_per_seg = kbps;
+        seg = lo / kbps;
+        kb = lo - seg * kbps;
+        if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD) {
+            tap = kb / g.cpt;
+            cc = kb - tap * g.cpt;
+            r = tap / g.S;
+            s = tap - r * g.S;
+            conv_box_origin(g, m_tile, w0, h0, b0);
+        } else if constexpr (MODE == GM_WGRAD) {
+            iw = kb % g.nbw;
+            const int t = kb / g.nbw;
+            ih = t % g.nbh;
+            b0 = (t / g.nbh) * g.bn;
+            w0 = iw * g.bw;
+            h0 = ih * g.bh;
+            const int taps = g.R * g.S;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int mrow = m0 + q * C::CH;
+                const int tq = min(mrow / g.C, taps - 1);
+                qc[q] = mrow - (mrow / g.C) * g.C;
+                qr[q] = tq / g.S;
+                qs[q] = tq - qr[q] * g.S;
+            }
+        }
+    }
+    __device__ __forceinline__ void next(const ConvGeom &g) {
+        if (++kb == kb_per_seg) {  // next 3xTF32 segment: restart the k sequence
+            kb = 0;
+            ++seg;
+            if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD) {
+                tap = cc = r = s = 0;
+            } else if constexpr (MODE == GM_WGRAD) {
+                iw = ih = 0;
+                w0 = h0 = b0 = 0;
+            }
+            return;
+        }
+        if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD) {
+            if (++cc == g.cpt) {
+                cc = 0;
+                ++tap;
+                if (++s == g.S) {
+                    s = 0;
+                    ++r;
+                }
+            }
+        } else if constexpr (MODE == GM_WGRAD) {
+            if (++iw == g.nbw) {
+                iw = 0;
+                w0 = 0;
+                if (++ih == g.nbh) {
+                    ih = 0;
+                    h0 = 0;
+                    b0 += g.bn;
+                } else {
+                    h0 += g.bh;
+                }
+            } else {
+                w0 += g.bw;
+            }
+        }
+    }
+    // Issue the k-block's loads (A, and the CL-shared B) onto `bar`.
+    template <bool B_MN, int BN, int CL>
+    __device__ __forceinline__ void load(uint8_t *sa, uint8_t *sb, const GemmMaps &maps, const ConvGeom &g,
+                                         uint64_t *bar, int n0, int rank) const {
+        if constexpr (MODE == GM_FPROP) {
+            ptx::tma_load_4d(sa, &maps.a[seg], bar, cc * C::CH, w0 * g.stride - g.pad + s, h0 * g.stride - g.pad + r,
+                             b0);
+            load_b<C, B_MN, BN, CL>(sb, &maps.b[seg], bar, n0, kb * C::BK, rank);
+        } else if constexpr (MODE == GM_DGRAD) {
+            static_assert(CL == 1, "paired B loads need an MN-major B");
+            ptx::tma_load_4d(sa, &maps.a[seg], bar, cc * C::CH, w0 + g.tow[tap], h0 + g.toh[tap], b0);
+            ptx::tma_load_2d(sb, &maps.b[seg], bar, cc * C::CH, g.twt[tap] * g.Cw + n0);
+        } else {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                ptx::tma_load_4d(sa + q * (C::BK * 128), &maps.a[seg], bar, qc[q], w0 * g.stride - g.pad + qs[q],
+                                 h0 * g.stride - g.pad + qr[q], b0);
+#pragma unroll
+            for (int q = 0; q < BN / C::CH; ++q) {
+                if constexpr (CL == 1)
+                    ptx::tma_load_4d(sb + q * (C::BK * 128), &maps.b[seg], bar, n0 + q * C::CH, w0, h0, b0);
+                else if ((q & 1) == rank)
+                    ptx::tma_load_4d_mc(sb + q * (C::BK * 128), &maps.b[seg], bar, n0 + q * C::CH, w0, h0, b0, 3);
+            }
+        }
+    }
+};
+
 template <class C, bool MN>
 __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
     if constexpr (!MN)

@@ -195,24 +195,24 @@ __global__ void __launch_bounds__(kPkThreads, 1)
 
     if (warp == 0) {
         if (ptx::lane_id() == 0) {
-            int it = 0;
+            int it = 0, s = 0, ph = 0;  // ring position: slot s of round ph (it = ph * STAGES + s)
             for (int u = first; u < args.units; u += stride) {
                 int tm, tn, sp, g_;
                 pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g_);
                 const int lo = sp * args.iters_per_split, hi = min(args.total_iters, lo + args.iters_per_split);
                 const int m0 = tm * 128, n0 = tn * BN;
+                ConvIter<C, MODE> ci;
+                if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD || MODE == GM_WGRAD)
+                    ci.init(args.cv, args.kb_per_seg, lo, tm, m0);
+                int seg = lo / args.kb_per_seg, kb = lo - seg * args.kb_per_seg;  // plain / batched modes
                 for (int g = lo; g < hi; ++g, ++it) {
-                    const int s = it % C::STAGES;
-                    if (it >= C::STAGES) ptx::mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
-                    const int seg = g / args.kb_per_seg, kb = g - seg * args.kb_per_seg;
+                    if (it >= C::STAGES) ptx::mbar_wait(&empty[s], (ph - 1) & 1);
                     ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
                     if constexpr (MODE == GM_PLAIN) {
                         load_operand<C, A_MN, 128>(sA + s * C::A_BYTES, &maps.a[seg], &full[s], m0, kb * C::BK);
                         load_b<C, B_MN, BN, CL>(sB + s * C::B_BYTES, &maps.b[seg], &full[s], n0, kb * C::BK, rank);
                     } else if constexpr (MODE == GM_BATCH) {
-                        int tm2, tn2, sp2, g;
-                        pk_unit(args, u, tm2, tn2, sp2, g);
-                        const int hh = g % args.nh, bb = g / args.nh, k0 = kb * C::BK;
+                        const int hh = g_ % args.nh, bb = g_ / args.nh, k0 = kb * C::BK;
                         if constexpr (!A_MN) {
                             ptx::tma_load_4d(sA + s * C::A_BYTES, &maps.a[seg], &full[s], k0, m0, hh, bb);
                         } else {
@@ -230,15 +230,24 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                                                  n0 + c * C::CH, k0, hh, bb);
                         }
                     } else {
-                        conv_load<C, MODE, B_MN, BN, CL>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args.cv,
-                                                         &full[s], seg, kb, tm, m0, n0, rank);
+                        ci.template load<B_MN, BN, CL>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args.cv,
+                                                       &full[s], n0, rank);
+                        ci.next(args.cv);
+                    }
+                    if (++kb == args.kb_per_seg) {
+                        kb = 0;
+                        ++seg;
+                    }
+                    if (++s == C::STAGES) {
+                        s = 0;
+                        ++ph;
                     }
                 }
             }
         }
     } else if (warp == 1) {
         if (ptx::lane_id() == 0) {
-            int it = 0, j = 0;
+            int s = 0, ph = 0, j = 0;
             for (int u = first; u < args.units; u += stride, ++j) {
                 int tm, tn, sp, g_;
                 pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g_);
@@ -247,9 +256,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 if (j >= 2) ptx::mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + uint32_t(acc * BN);
-                for (int g = lo; g < hi; ++g, ++it) {
-                    const int s = it % C::STAGES;
-                    ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+                for (int g = lo; g < hi; ++g) {
+                    ptx::mbar_wait(&full[s], ph & 1);
                     ptx::tc_fence_after();
                     const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
                     const uint32_t b_base = ptx::smem_u32(sB + s * C::B_BYTES);
@@ -261,6 +269,10 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                         ptx::umma_commit(&empty[s]);
                     else
                         ptx::umma_commit_mc(&empty[s], 3);
+                    if (++s == C::STAGES) {
+                        s = 0;
+                        ++ph;
+                    }
                 }
                 ptx::umma_commit(&tfull[acc]);
             }
