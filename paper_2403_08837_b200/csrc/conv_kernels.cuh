@@ -625,6 +625,7 @@ static __global__ void bn_apply_kernel(const void *__restrict__ y, int64_t P, in
             g2 = ld_f8(res.gamma, c);
             b2 = ld_f8(res.beta, c);
         }
+#pragma unroll 2
         for (; i < n; i += stride) bn_apply_elem<KIND>(y, size_t(i) * 8, mu, rs, ga, be, res, m2, r2, g2, b2, relu, out);
         return;
     }
@@ -672,6 +673,7 @@ static __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__
             mu2 = ld_f4(mean2, c);
             rs2 = ld_f4(rstd2, c);
         }
+#pragma unroll 4
         for (int64_t r = r0 + ty; r < r1; r += phases) {
             const size_t o = size_t(r) * C + c;
             float4 gv = ld_y4<KIND>(g, o);
