@@ -488,14 +488,18 @@ struct ResNetTrainer {
         if (tiles < sms()) splits = std::max(1, std::min(sms() / tiles, a.total_iters / 4));  // units <= one wave
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
+        using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;
+        PL::choose_sk(a);  // split-K reduced inside clusters over DSMEM when splits allow
         a.units = tiles * a.splits;
         last_fused = a.splits == 1;
+        // BN statistics slots per tile: one per 32-row reduce chunk, or one per cluster CTA slice
+        const int slots_per_tile = a.sk ? a.splits : 4;
         typename Epi::Params ep = a.splits > 1 ? Epi::for_split(ep_in) : ep_in;
         if constexpr (std::is_same<Epi, EpiConvOut2<K>>::value)
-            if (a.splits > 1) ep.tiles = a.tiles_m * 4;  // one statistics slot per 32-row chunk of a tile
+            if (a.splits > 1) ep.tiles = a.tiles_m * slots_per_tile;
         a.boxed = (MODE == GM_FPROP || MODE == GM_DGRAD) ? 1 : 0;
         a.cv = gp.args.cv;
-        const size_t need = a.splits > 1 ? size_t(tiles) * a.splits * 128 * BNc : 0;
+        const size_t need = (a.splits > 1 && !a.sk) ? size_t(tiles) * a.splits * 128 * BNc : 0;
         size_t &cap = hop ? ws_h_floats : ws_c_floats;
         if (sizing) {
             cap = std::max(cap, need);
@@ -503,15 +507,14 @@ struct ResNetTrainer {
         }
         CDP_REQUIRE(need <= cap, "split-K workspace too small");
         a.ws = ws_for(hop);
-        using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;
         bool paired = false;
         const int grid = PL::prepare(a, sms(), paired);
         GemmMaps maps = gp.maps;
         PL::setup_tma_out(maps, a, ep);
-        last_stat_slots = a.splits > 1 ? a.tiles_m * 4 : grid;  // EpiConvOut2 statistics rows (RC = 32 below)
+        last_stat_slots = a.splits > 1 ? a.tiles_m * slots_per_tile : grid;  // EpiConvOut2 statistics rows
         last_grid = grid;
         L(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
-        if (a.splits > 1) {
+        if (a.splits > 1 && !a.sk) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
             constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
             constexpr int CC = 64;
