@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcdp_b200.so")
+# CDP_LIB_PATH: an alternative build of the same library (A/B timing of two builds in one process pool)
+LIB_PATH = os.environ.get("CDP_LIB_PATH") or os.path.join(HERE, "libcdp_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "cdp_b200.h")
 
 c_int, c_float, c_double, c_void_p, c_size_t = ctypes.c_int, ctypes.c_float, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t

@@ -52,7 +52,13 @@ struct PkArgs {
     // of all the cluster's shared tiles over DSMEM in split order and runs the epilogue on them
     // (no workspace, no pk_reduce_kernel).  splits in {2, 4, 8}.
     int sk;
+    // Stride-2 data gradient with all sub-pixel phases in one launch (nph > 1): the batch index g of
+    // a unit is its phase, cvp[g] its geometry (tap table, output phase offsets); no split-K.
+    int nph;
+    ConvGeom cvp[4];
 };
+
+__device__ __forceinline__ const ConvGeom &pk_geom(const PkArgs &a, int g) { return a.nph > 1 ? a.cvp[g] : a.cv; }
 
 template <int KIND, int BN, bool A_MN, bool B_MN, int ST>
 struct PkCfg {
@@ -127,8 +133,8 @@ __device__ __forceinline__ void pk_unit_cl(const PkArgs &a, int u, int rank, int
 }
 
 // tile row -> output row m (or -1): pixel box rows (FPROP / DGRAD) or m0 + r.
-__device__ __forceinline__ int pk_row_m(const PkArgs &a, int tm, int r) {
-    if (a.boxed) return conv_box_row(a.cv, tm, r);
+__device__ __forceinline__ int pk_row_m(const PkArgs &a, int tm, int r, int g = 0) {
+    if (a.boxed) return conv_box_row(pk_geom(a, g), tm, r);
     const int m = tm * 128 + r;
     return m < a.M ? m : -1;
 }
@@ -147,7 +153,8 @@ constexpr int kPkEpi = 256;
 // have consumed it (empty barrier count 2, commits multicast to the pair).
 template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE, int CL = 1>
 __global__ void __launch_bounds__(kPkThreads, 1)
-    gemm_pk_kernel(const __grid_constant__ GemmMaps maps, const PkArgs args, const typename Epi::Params ep) {
+    gemm_pk_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ PkArgs args,
+                   const typename Epi::Params ep) {
     using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages>;
     static_assert(CL == 1 || (CL == 2 && MODE != GM_BATCH && MODE != GM_DGRAD && B_MN && BN / C::CH >= 2),
                   "CTA pairs share an MN-major B tile of at least two chunks");
@@ -211,11 +218,13 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             for (int u = first; u < args.units; u += stride) {
                 int tm, tn, sp, g_;
                 pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g_);
-                const int lo = sp * args.iters_per_split, hi = min(args.total_iters, lo + args.iters_per_split);
+                const ConvGeom &cg = pk_geom(args, g_);
+                const int kbps = args.nph > 1 ? cg.ntap * cg.cpt : args.kb_per_seg;
+                const int tot = args.nph > 1 ? kbps * args.n_seg : args.total_iters;
+                const int lo = sp * args.iters_per_split, hi = min(tot, lo + args.iters_per_split);
                 const int m0 = tm * 128, n0 = tn * BN;
                 ConvIter<C, MODE> ci;
-                if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD || MODE == GM_WGRAD)
-                    ci.init(args.cv, args.kb_per_seg, lo, tm, m0);
+                if constexpr (MODE == GM_FPROP || MODE == GM_DGRAD || MODE == GM_WGRAD) ci.init(cg, kbps, lo, tm, m0);
                 int seg = lo / args.kb_per_seg, kb = lo - seg * args.kb_per_seg;  // plain / batched modes
                 for (int g = lo; g < hi; ++g, ++it) {
                     if (it >= C::STAGES) ptx::mbar_wait(&empty[s], (ph - 1) & 1);
@@ -242,9 +251,9 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                                                  n0 + c * C::CH, k0, hh, bb);
                         }
                     } else {
-                        ci.template load<B_MN, BN, CL>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, args.cv,
-                                                       &full[s], n0, rank);
-                        ci.next(args.cv);
+                        ci.template load<B_MN, BN, CL>(sA + s * C::A_BYTES, sB + s * C::B_BYTES, maps, cg, &full[s],
+                                                       n0, rank);
+                        ci.next(cg);
                     }
                     if (++kb == args.kb_per_seg) {
                         kb = 0;
@@ -263,7 +272,9 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             for (int u = first; u < args.units; u += stride, ++j) {
                 int tm, tn, sp, g_;
                 pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g_);
-                const int lo = sp * args.iters_per_split, hi = min(args.total_iters, lo + args.iters_per_split);
+                const int tot = args.nph > 1 ? pk_geom(args, g_).ntap * pk_geom(args, g_).cpt * args.n_seg
+                                             : args.total_iters;
+                const int lo = sp * args.iters_per_split, hi = min(tot, lo + args.iters_per_split);
                 const int acc = j & 1;
                 if (j >= 2) ptx::mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
                 ptx::tc_fence_after();
@@ -329,7 +340,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 }
             }
             if (tid < 128) {  // the previous unit's last barrier protects rowm / stile
-                const int m = pk_row_m(args, tm, tid);
+                const int m = pk_row_m(args, tm, tid, g);
                 rowm[tid] = m;
                 if (!split) Epi::prefetch_row(ep, m, tn * BN, min(BN, args.N - tn * BN), out_off);
             }
@@ -338,7 +349,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
             if constexpr (Epi::kTmaStore) {
                 if (tma) {
-                    const int row_m = pk_row_m(args, tm, row);
+                    const int row_m = pk_row_m(args, tm, row, g);
                     const bool stats = Epi::has_stats(ep);
 #pragma unroll 1
                     for (int h = 0; h < BN / C::EPI_COLS; ++h, ++pc) {
@@ -403,7 +414,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             }
 #pragma unroll 1
             for (int h = 0; h < BN / C::EPI_COLS; ++h) {
-                const int row_m = pk_row_m(args, tm, row);  // own computation: rowm is not yet synced
+                const int row_m = pk_row_m(args, tm, row, g);  // own computation: rowm is not yet synced
 #pragma unroll 1
                 for (int c = half * HC; c < (half + 1) * HC; c += 32) {
                     float v[32];
@@ -491,7 +502,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
 // sum the split partials in split order into shared memory and run the
 // epilogue on that sub-tile.  256 threads.
 template <int BN, class Epi, int RC, int CC>
-__global__ void __launch_bounds__(256) pk_reduce_kernel(const PkArgs args, const typename Epi::Params ep) {
+__global__ void __launch_bounds__(256) pk_reduce_kernel(const __grid_constant__ PkArgs args,
+                                                        const typename Epi::Params ep) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     __shared__ __align__(16) float st[RC * (CC + 4)];

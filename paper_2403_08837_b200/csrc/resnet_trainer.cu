@@ -472,9 +472,11 @@ struct ResNetTrainer {
         return sms_;
     }
 
+    // phases / nph > 1: a stride-2 data gradient with its sub-pixel phases as one launch (the unit's
+    // batch index is its phase; no split-K)
     template <int K, int BNc, bool AMN, bool BMN, class Epi, int MODE>
     void run_pk(const char *name, double flops, const GemmPlan &gp, const typename Epi::Params &ep_in, cudaStream_t s,
-                bool hop) {
+                bool hop, const ConvGeom *phases = nullptr, int nph = 1) {
         PkArgs a{};
         a.M = gp.args.M;
         a.N = gp.args.N;
@@ -483,9 +485,18 @@ struct ResNetTrainer {
         a.kb_per_seg = gp.args.kb_per_seg;
         a.n_seg = gp.args.n_seg;
         a.total_iters = a.kb_per_seg * a.n_seg;
-        const int tiles = a.tiles_m * a.tiles_n;
+        a.nph = nph;
+        if (nph > 1) {
+            a.nbatch = nph;
+            for (int i = 0; i < nph; ++i) a.cvp[i] = phases[i];
+            int mx = 0;
+            for (int i = 0; i < nph; ++i) mx = std::max(mx, phases[i].ntap * phases[i].cpt * a.n_seg);
+            a.total_iters = mx;
+        }
+        const int tiles = a.tiles_m * a.tiles_n * nph;
         int splits = 1;
-        if (tiles < sms()) splits = std::max(1, std::min(sms() / tiles, a.total_iters / 4));  // units <= one wave
+        if (tiles < sms() && nph == 1)
+            splits = std::max(1, std::min(sms() / tiles, a.total_iters / 4));  // units <= one wave
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
         using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;
@@ -568,6 +579,38 @@ struct ResNetTrainer {
                 GemmPlan p = plan_conv<K, BNc, MODE>(a, w.hi.p, w.lo.p, w.ld, dy, c.R, c.S, c.stride, c.pad, c.cin,
                                                      c.cout, 1, nullptr, nullptr, phase);
                 run_pk<K, BNc, AMN, BMN, Epi, MODE>(name, flops, p, ep, s, hop);
+            } else {
+                throw CdpError("unsupported conv GEMM configuration");
+            }
+        });
+    }
+
+    // Stride-2 data gradient: the sub-pixel phases with taps as one launch (shared dy / W maps and
+    // pixel boxes; per-phase tap tables and output offsets).
+    template <int K, class Epi>
+    void pk_dgrad_phases(const char *name, int BN, const ConvL &c, const CBuf &w, const typename Epi::Params &ep,
+                         cudaStream_t s) {
+        CDP_REQUIRE(c.in_act >= 0, "stride-2 data gradient of the stem is never needed");
+        const Nhwc a = nhwc_act(c.in_act);
+        const Nhwc dy = nhwc_dy(c);
+        bn_switch(BN, [&](auto bnc) {
+            constexpr int BNc = decltype(bnc)::value;
+            if constexpr (BNc >= 64) {
+                ConvGeom ph[4];
+                GemmPlan first{};
+                int nph = 0;
+                double flops = 0.0;
+                for (int phase = 0; phase < 4; ++phase) {
+                    ConvGeom probe{};
+                    dgrad_taps(probe, c.R, c.S, c.pad, phase);
+                    if (probe.ntap == 0) continue;
+                    GemmPlan p = plan_conv<K, BNc, GM_DGRAD>(a, w.hi.p, w.lo.p, w.ld, dy, c.R, c.S, c.stride,
+                                                             c.pad, c.cin, c.cout, 1, nullptr, nullptr, phase);
+                    if (nph == 0) first = p;
+                    ph[nph++] = p.args.cv;
+                    flops += 2.0 * double(c.P) * probe.ntap * c.cin * c.cout;
+                }
+                run_pk<K, BNc, false, false, Epi, GM_DGRAD>(name, flops, first, ep, s, false, ph, nph);
             } else {
                 throw CdpError("unsupported conv GEMM configuration");
             }
@@ -770,12 +813,7 @@ struct ResNetTrainer {
                 CDP_REQUIRE(add == nullptr, "a 1x1 stride-2 data gradient cannot fold a residual branch");
                 if (!sizing) CDP_CUDA(cudaMemsetAsync(g_in, 0, size_t(c.Pin) * c.cin * ysz(), s));
             }
-            for (int ph = 0; ph < 4; ++ph) {
-                ConvGeom probe{};
-                dgrad_taps(probe, c.R, c.S, c.pad, ph);
-                if (probe.ntap == 0) continue;
-                pk_conv<K, GM_DGRAD, EpiConvOut2<K>>("conv_dgrad_s2", tile_n(c.cin), c, w, ep, s, false, ph);
-            }
+            pk_dgrad_phases<K, EpiConvOut2<K>>("conv_dgrad_s2", tile_n(c.cin), c, w, ep, s);
         }
     }
 
