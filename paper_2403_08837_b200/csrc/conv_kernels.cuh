@@ -374,21 +374,12 @@ struct EpiConvOut2 {
     }
     // Split-K reduce kernel: the whole 128-row tile is in `st` (rows in order).  Column
     // statistics: NTH/ncols row groups per column, combined in group order (fixed).
-    // PKB: inside the persistent kernel's epilogue (named barrier 3 over the NTH epilogue threads,
-    // `scratch` = 2 x NTH floats of its shared memory) instead of a standalone block.
-    template <int NTH, bool PKB = false>
+    template <int NTH>
     __device__ static void run_with_stats(const Params &p, const float *st, int lds, const int *rowm, int nrows,
-                                          int col0, int ncols, int tm, int N, int tid, int64_t off,
-                                          float *scratch = nullptr) {
+                                          int col0, int ncols, int tm, int N, int tid, int64_t off) {
         run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid, off);
         if (p.stats) {
-            float(*red)[NTH];
-            if constexpr (PKB) {
-                red = reinterpret_cast<float(*)[NTH]>(scratch);
-            } else {
-                __shared__ float red_s[2][NTH];
-                red = red_s;
-            }
+            __shared__ float red[2][NTH];
             const int groups = NTH / ncols;
             const int c = tid % ncols, grp = tid / ncols;
             float s = 0.f, q = 0.f;
@@ -401,10 +392,7 @@ struct EpiConvOut2 {
                 }
             red[0][tid] = s;
             red[1][tid] = q;
-            if constexpr (PKB)
-                pk_bar(3, NTH);
-            else
-                __syncthreads();
+            __syncthreads();
             if (tid < ncols) {
                 float a = 0.f, b = 0.f;
                 for (int g = 0; g < groups; ++g) {
@@ -451,10 +439,9 @@ struct EpiHop2 {
     __device__ static void col_stats(const Params &, const float *, int, int, int, int, int, Pre) {}
     template <int NTH>
     __device__ static void col_stats_init(const Params &, int, int, int) {}
-    template <int NTH, bool PKB = false>
+    template <int NTH>
     __device__ static void run_with_stats(const Params &p, const float *st, int lds, const int *rowm, int nrows,
-                                          int col0, int ncols, int tm, int N, int tid, int64_t off,
-                                          float * = nullptr) {
+                                          int col0, int ncols, int tm, int N, int tid, int64_t off) {
         run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid, off);
     }
     template <int NTH, int FIXC = 0>

@@ -47,11 +47,6 @@ struct PkArgs {
     // 128-byte-swizzled shared staging area in 64-column chunks and written by TMA through maps.o
     // (2-D {N, M} for GM_PLAIN, 4-D {N, W, H, B} with the pixel box for FPROP / stride-1 DGRAD)
     int tma_out;
-    // Split-K inside a cluster (sk = 1): the `splits` CTAs of a cluster compute the K ranges of one
-    // tile; each drains its partial into its shared tile, then CTA r sums rows [r*128/splits, ...)
-    // of all the cluster's shared tiles over DSMEM in split order and runs the epilogue on them
-    // (no workspace, no pk_reduce_kernel).  splits in {2, 4, 8}.
-    int sk;
     // Stride-2 data gradient with all sub-pixel phases in one launch (nph > 1): the batch index g of
     // a unit is its phase, cvp[g] its geometry (tap table, output phase offsets); no split-K.
     int nph;
@@ -158,12 +153,9 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages>;
     static_assert(CL == 1 || (CL == 2 && MODE != GM_BATCH && MODE != GM_DGRAD && B_MN && BN / C::CH >= 2),
                   "CTA pairs share an MN-major B tile of at least two chunks");
-    const bool sk = CL == 1 && args.sk;
-    const int rank = (CL == 1 && !sk) ? 0 : int(ptx::cluster_ctarank());
-    const int nct = sk ? args.splits : 1;
-    // split-cluster: cluster c takes units (tile t, split = rank) for t = c, c + nclusters, ...
-    const int first = sk ? int(ptx::cluster_id_x()) * nct + rank : CL == 1 ? int(blockIdx.x) : int(ptx::cluster_id_x());
-    const int stride = sk ? int(ptx::nclusters_x()) * nct : CL == 1 ? int(gridDim.x) : int(ptx::nclusters_x());
+    const int rank = CL == 1 ? 0 : int(ptx::cluster_ctarank());
+    const int first = CL == 1 ? int(blockIdx.x) : int(ptx::cluster_id_x());
+    const int stride = CL == 1 ? int(gridDim.x) : int(ptx::nclusters_x());
     extern __shared__ __align__(16) uint8_t smem_raw[];
     // 1024-byte alignment by pointer arithmetic on the shared array (keeps the
     // shared address space visible to the compiler: LDS/STS, not generic LD/ST)
@@ -177,9 +169,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     uint64_t *empty = full + C::STAGES;
     uint64_t *tfull = empty + C::STAGES;
     uint64_t *tempty = tfull + 2;
-    uint64_t *rdy = tempty + 2;  // split-cluster: all CTAs' partials of the pass are in shared memory
-    uint64_t *fre = rdy + 1;     // split-cluster: all CTAs finished reading this CTA's partial
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fre + 1);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const uint32_t warp = ptx::warp_id();
     if (warp == 0 && ptx::lane_id() == 0) {
@@ -197,16 +187,14 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             ptx::mbar_init(&tfull[a], 1);
             ptx::mbar_init(&tempty[a], 1);
         }
-        ptx::mbar_init(rdy, uint32_t(nct));
-        ptx::mbar_init(fre, uint32_t(nct));
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
     ptx::tc_fence_before();
-    if (CL == 1 && !sk)
+    if constexpr (CL == 1)
         __syncthreads();
     else
-        ptx::cluster_sync();  // the cluster's barriers are initialised before any remote access
+        ptx::cluster_sync();  // the partner's barriers are initialised before any multicast
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     ptx::griddep_wait();
@@ -314,8 +302,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         // alternating per pass; a buffer is rewritten only after its previous store group was read
         uint8_t *stage = smem + C::STAGES * C::STAGE_BYTES;
         static_assert(!Epi::kTmaStore || 2 * C::EPI_COLS * 256 <= C::STILE_BYTES, "TMA staging exceeds the shared tile");
-        int pc = 0;   // TMA passes issued by this CTA
-        int skp = 0;  // split-cluster passes (rdy / fre phase)
+        int pc = 0;  // TMA passes issued by this CTA
         int j = 0;
         for (int u = first; u < args.units; u += stride, ++j) {
             int tm, tn, sp, g;
@@ -428,38 +415,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 pk_bar(1, kPkEpi);
                 if (h == BN / C::EPI_COLS - 1 && tid == 0) ptx::mbar_arrive(&tempty[acc]);  // accumulator free
                 const int col0 = tn * BN + h * C::EPI_COLS;
-                if (split && sk) {
-                    // all partials of this pass are in the cluster's shared tiles
-                    if (tid == 0) {
-                        ptx::fence_acq_rel_cluster();
-                        for (int z = 0; z < nct; ++z) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(rdy), z));
-                    }
-                    ptx::mbar_wait_cluster(rdy, skp & 1);
-                    const int rs = 128 / nct, r0 = rank * rs;
-                    constexpr int C4 = C::EPI_COLS / 4;
-                    const uint32_t st0 = ptx::smem_u32(stile);
-                    for (int e = tid; e < rs * C4; e += kPkEpi) {
-                        const int r = r0 + e / C4, cc = (e % C4) * 4;
-                        const uint32_t off = st0 + uint32_t((r * C::LDS + cc) * 4);
-                        float4 acc = ptx::ld_dsmem_f4(ptx::mapa(off, 0));
-                        for (int z = 1; z < nct; ++z) {  // split order: deterministic
-                            const float4 t = ptx::ld_dsmem_f4(ptx::mapa(off, uint32_t(z)));
-                            acc.x += t.x;
-                            acc.y += t.y;
-                            acc.z += t.z;
-                            acc.w += t.w;
-                        }
-                        *reinterpret_cast<float4 *>(stile + r * C::LDS + cc) = acc;  // own slice rows only
-                    }
-                    pk_bar(1, kPkEpi);
-                    if (tid == 0) {  // done reading the other CTAs' tiles for this pass
-                        ptx::fence_acq_rel_cluster();
-                        for (int z = 0; z < nct; ++z) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(fre), z));
-                    }
-                    Epi::template run_with_stats<kPkEpi, true>(ep, stile + r0 * C::LDS, C::LDS, rowm + r0, rs, col0,
-                                                                min(C::EPI_COLS, args.N - col0), tm * nct + rank,
-                                                                args.N, tid, out_off, spart);
-                } else if (split) {
+                if (split) {
                     float *dst = args.ws + ((size_t(tm) * args.tiles_n + tn) * args.splits + sp) * 128 * BN +
                                  h * C::EPI_COLS;
                     constexpr int C4 = C::EPI_COLS / 4;
@@ -479,22 +435,17 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                                                     h == 0 ? pre[0] : pre[BN / C::EPI_COLS - 1]);
                 }
                 pk_bar(1, kPkEpi);  // shared tile reused by the next pass / unit
-                if (split && sk) {  // the other CTAs no longer read this CTA's tile
-                    ptx::mbar_wait_cluster(fre, skp & 1);
-                    ++skp;
-                }
             }
             if (!split) Epi::template done<kPkEpi>(ep, tid, unsigned(args.tiles_m * args.tiles_n));
-            else if (sk) Epi::template done<kPkEpi>(ep, tid, unsigned(args.tiles_m * args.tiles_n * nct));
         }
         if constexpr (Epi::kTmaStore)
             if (tid == 0) ptx::bulk_wait0();  // TMA stores complete before the CTA exits
     }
     ptx::tc_fence_before();
-    if (CL == 1 && !sk)
+    if constexpr (CL == 1)
         __syncthreads();
     else
-        ptx::cluster_sync();  // the cluster's last remote arrives / DSMEM reads are done
+        ptx::cluster_sync();  // the partner's last multicast commits have landed
     if (warp == 2) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
@@ -553,44 +504,9 @@ struct PkLaunch {
     using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages>;
     static constexpr bool kPairable = MODE != GM_BATCH && MODE != GM_DGRAD && B_MN && BN / C::CH >= 2;
 
-    // Split-K inside clusters, opt-in (CDP_PK_SK=1): a.splits rounded down to a power of two in
-    // [2, 8] that still partitions the k-blocks exactly; sets a.sk, a.splits, a.iters_per_split.
-    // Measured on B200 (ResNet-18 step 1.91 -> 2.25 ms): the cluster CTAs wait for each other every
-    // pass and fewer clusters are co-resident than single CTAs, which costs more than the separate
-    // reduce launches it removes.
-    static void choose_sk(PkArgs &a) {
-        a.sk = 0;
-        static const bool on = [] {
-            const char *e = std::getenv("CDP_PK_SK");
-            return e && e[0] == '1';
-        }();
-        if (!on || MODE == GM_BATCH || a.splits < 2 || a.splits > 8) return;
-        for (int p = 8; p >= 2; p >>= 1) {
-            if (p > a.splits) continue;
-            const int per = (a.total_iters + p - 1) / p;
-            if ((a.total_iters + per - 1) / per != p) continue;
-            a.splits = p;
-            a.iters_per_split = per;
-            a.sk = 1;
-            return;
-        }
-    }
-    static int max_clusters(int cx) {
-        static int cache[9] = {0};
-        if (!cache[cx]) {
-            set_attr();
-            cache[cx] = std::max(
-                1, max_active_clusters(gemm_pk_kernel<KIND, BN, A_MN, B_MN, Epi, MODE, 1>, kPkThreads, C::SMEM, cx));
-        }
-        return cache[cx];
-    }
     // Decide pairing (M tiles >= 2, pairable shape), fix up a.tiles_pm / a.units; returns the grid.
     static int prepare(PkArgs &a, int sms, bool &paired) {
         paired = false;
-        if (a.sk) {
-            const int tiles = a.units / a.splits;
-            return a.splits * std::min(tiles, max_clusters(a.splits));
-        }
         if constexpr (kPairable) {
             if (pk_pairs_enabled() && a.tiles_m >= 2) {
                 paired = true;
@@ -645,11 +561,6 @@ struct PkLaunch {
     static void launch(const GemmMaps &maps, const PkArgs &a, const typename Epi::Params &ep, cudaStream_t s, int grid,
                        bool paired) {
         set_attr();
-        if (a.sk) {
-            launch_pdl_cluster(gemm_pk_kernel<KIND, BN, A_MN, B_MN, Epi, MODE, 1>, dim3(grid), dim3(kPkThreads),
-                               C::SMEM, s, a.splits, maps, a, ep);
-            return;
-        }
         if constexpr (kPairable) {
             if (paired) {
                 launch_pdl_cluster(gemm_pk_kernel<KIND, BN, A_MN, B_MN, Epi, MODE, 2>, dim3(grid), dim3(kPkThreads),

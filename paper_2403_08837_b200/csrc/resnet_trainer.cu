@@ -500,17 +500,15 @@ struct ResNetTrainer {
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
         using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;
-        PL::choose_sk(a);  // split-K reduced inside clusters over DSMEM when splits allow
         a.units = tiles * a.splits;
         last_fused = a.splits == 1;
-        // BN statistics slots per tile: one per 32-row reduce chunk, or one per cluster CTA slice
-        const int slots_per_tile = a.sk ? a.splits : 4;
+        const int slots_per_tile = 4;  // BN statistics slots per split tile: one per 32-row reduce chunk
         typename Epi::Params ep = a.splits > 1 ? Epi::for_split(ep_in) : ep_in;
         if constexpr (std::is_same<Epi, EpiConvOut2<K>>::value)
             if (a.splits > 1) ep.tiles = a.tiles_m * slots_per_tile;
         a.boxed = (MODE == GM_FPROP || MODE == GM_DGRAD) ? 1 : 0;
         a.cv = gp.args.cv;
-        const size_t need = (a.splits > 1 && !a.sk) ? size_t(tiles) * a.splits * 128 * BNc : 0;
+        const size_t need = a.splits > 1 ? size_t(tiles) * a.splits * 128 * BNc : 0;
         size_t &cap = hop ? ws_h_floats : ws_c_floats;
         if (sizing) {
             cap = std::max(cap, need);
@@ -525,7 +523,7 @@ struct ResNetTrainer {
         last_stat_slots = a.splits > 1 ? a.tiles_m * slots_per_tile : grid;  // EpiConvOut2 statistics rows
         last_grid = grid;
         L(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
-        if (a.splits > 1 && !a.sk) {
+        if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
             constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
             constexpr int CC = 64;

@@ -298,12 +298,11 @@ struct VitTrainer {
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
         using PL = PkLaunch<0, BNc, AMN, BMN, Epi, MODE>;
-        PL::choose_sk(a);  // split-K reduced inside clusters over DSMEM when splits allow
         a.units = tiles * a.splits;
         typename Epi::Params ep = a.splits > 1 ? Epi::for_split(ep_in) : ep_in;
         if constexpr (std::is_same<Epi, EpiConvOut2<0>>::value)
-            if (a.splits > 1) ep.tiles = a.tiles_m * (a.sk ? a.splits : 4);
-        const size_t need = (a.splits > 1 && !a.sk) ? size_t(tiles) * a.splits * 128 * BNc : 0;
+            if (a.splits > 1) ep.tiles = a.tiles_m * 4;
+        const size_t need = a.splits > 1 ? size_t(tiles) * a.splits * 128 * BNc : 0;
         size_t &cap = hop ? ws_h_floats : ws_c_floats;
         if (sizing) {
             cap = std::max(cap, need);
@@ -316,7 +315,7 @@ struct VitTrainer {
         GemmMaps maps = gp.maps;
         PL::setup_tma_out(maps, a, ep);
         L_(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
-        if (a.splits > 1 && !a.sk) {
+        if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<0>>::value;
             constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
             constexpr int CC = 64;

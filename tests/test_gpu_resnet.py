@@ -245,23 +245,3 @@ def test_cta_pair_option(cuda):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=os.path.dirname(os.path.dirname(here)))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
-
-
-def test_split_cluster_option(cuda):
-    """CDP_PK_SK=1 (split-K reduced inside a cluster over DSMEM instead of pk_reduce_kernel, BN
-    statistics per cluster-CTA row slice) matches the float64 restatement like the default path."""
-    import os
-    import subprocess
-    import sys
-
-    here = os.path.abspath(__file__)
-    code = ("import importlib.util as U, sys;"
-            f"sys.path.insert(0, {os.path.dirname(os.path.dirname(here))!r});"
-            f"s = U.spec_from_file_location('tgr', {here!r}); T = U.module_from_spec(s); s.loader.exec_module(T);"
-            "init, x, y, perms, losses, final, stage = T._ranks(1, None, 'fp32', 3, arch='bottleneck');"
-            "want, wl = T._oracle(init, x, y, perms, 1, None, stage, arch='bottleneck');"
-            "assert T._rel(final, want) <= 2e-4, T._rel(final, want); print('ok')")
-    env = dict(os.environ, CDP_PK_SK="1")
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                       cwd=os.path.dirname(os.path.dirname(here)))
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
