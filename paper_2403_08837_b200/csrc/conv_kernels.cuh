@@ -229,13 +229,20 @@ struct EpiConvOut2 {
     }
     // Stores (8 columns per element: 16-byte bf16 / 2 x 16-byte fp32 stores).
     // FIXC: ncols known at compile time (the persistent kernel's full passes), 0 = runtime.
-    template <int NTH, int FIXC = 0>
+    // TAIL: aligned rows keep the 8-column vectors up to the last full vector and only the columns
+    // past it (a 197-token tile) take the scalar loop; otherwise a ragged ncols makes the whole tile
+    // scalar (fewer live registers: the split-K reduce kernel keeps its occupancy).
+    template <int NTH, int FIXC = 0, bool TAIL = false>
     __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
                                int ncols, int tm, int N, int tid, int64_t off) {
         if (FIXC) ncols = FIXC;
-        if (((p.ld | col0 | ncols) & 7) || (off & 7)) {  // unaligned rows (e.g. a 10-class head): scalar
-            for (int e = tid; e < nrows * ncols; e += NTH) {
-                const int r = e / ncols, c = e - r * ncols;
+        const bool rows_aligned = !(((p.ld | col0) & 7) || (off & 7));
+        int nv = ncols;  // columns of the 8-wide vector path
+        if (!rows_aligned || (ncols & 7)) {
+            nv = (TAIL && rows_aligned) ? (ncols & ~7) : 0;
+            const int nt = ncols - nv;
+            for (int e = tid; e < nrows * nt; e += NTH) {
+                const int r = e / nt, c = nv + (e - r * nt);
                 const int m = rowm[r];
                 if (m < 0) continue;
                 float x = st[r * lds + c];
@@ -255,9 +262,9 @@ struct EpiConvOut2 {
                 else
                     Fmt<0>::store(p.out, nullptr, o, x);
             }
-            return;
+            if (!TAIL || nv == 0) return;
         }
-        const int C8 = FIXC ? FIXC / 8 : ncols / 8;
+        const int C8 = FIXC ? FIXC / 8 : nv / 8;
         const int total = nrows * C8;
         constexpr int U = 2;
         for (int e0 = tid; e0 < total; e0 += NTH * U) {
@@ -444,9 +451,9 @@ struct EpiHop2 {
                                           int col0, int ncols, int tm, int N, int tid, int64_t off) {
         run<NTH>(p, st, lds, rowm, nrows, col0, ncols, tm, N, tid, off);
     }
-    template <int NTH, int FIXC = 0>
+    template <int NTH, int FIXC = 0, bool TAIL = false>
     __device__ static void run(const Params &p, const float *st, int lds, const int *rowm, int nrows, int col0,
-                               int ncols, int, int, int tid, int64_t) {  // FIXC unused (register pressure)
+                               int ncols, int, int, int tid, int64_t) {  // FIXC / TAIL unused (register pressure)
         bool bad_g = false, bad_u = false;
         const float lr = *p.lr;
         if ((p.dout % 4) == 0 && (p.base % 4) == 0 && (ncols % 4) == 0) {

@@ -430,7 +430,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                         Epi::template run<kPkEpi, C::EPI_COLS>(ep, stile, C::LDS, rowm, 128, col0, ncols, tm, args.N,
                                                                tid, out_off);
                     else
-                        Epi::template run<kPkEpi>(ep, stile, C::LDS, rowm, 128, col0, ncols, tm, args.N, tid, out_off);
+                        Epi::template run<kPkEpi, 0, true>(ep, stile, C::LDS, rowm, 128, col0, ncols, tm, args.N, tid,
+                                                           out_off);
                     Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, ncols, tm, tid,
                                                     h == 0 ? pre[0] : pre[BN / C::EPI_COLS - 1]);
                 }

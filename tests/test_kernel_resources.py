@@ -38,3 +38,12 @@ def test_gemm_pk_kernels_do_not_spill():
     bad = [(n, s) for n, _r, s in res if "gemm_pk_kernelILi0E" in n and s > 64]
     assert not bad, f"{len(bad)} bf16 gemm_pk_kernel instantiations use > 64 B of stack, e.g. {bad[:3]}"
     assert all(r <= 168 for _n, r, _s in res), "gemm_pk_kernel exceeds 168 registers (384-thread launch bound)"
+
+
+def test_split_k_reduce_keeps_occupancy():
+    """pk_reduce_kernel (256 threads) stays at <= 64 registers: the split-K tail is latency bound and
+    needs its resident blocks (an epilogue change once took it to 80-96 registers)."""
+    res = [r for r in _resources() if "pk_reduce_kernel" in r[0]]
+    assert res, "no pk_reduce_kernel in the library"
+    bad = [(n, r) for n, r, _s in res if r > 64]
+    assert not bad, f"pk_reduce_kernel over 64 registers: {bad[:3]}"
