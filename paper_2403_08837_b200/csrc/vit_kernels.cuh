@@ -142,7 +142,7 @@ static __global__ void ln_param_partial_kernel(const float *__restrict__ g, cons
 // columns lane + 32 k): dh_out = dh_in + dx (fp32) and, when copy.hi, the same row in compute
 // format (the next GEMM's operand); per-column (sum g, sum g xhat) of the block's rows combined
 // over the warps in fixed order -> partial[d][blk][2] (fp64), finalised by bn_finalize_bwd_kernel.
-constexpr int kLnBwdRows = 32;  // rows per CTA of the fused backward (4 per warp)
+constexpr int kLnBwdRows = 16;  // rows per CTA of the fused backward (2 per warp)
 template <int KIND, int CPL>
 static __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const float *__restrict__ g,
                                                                   const float *__restrict__ x, int rows,
@@ -189,6 +189,102 @@ static __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const float *_
         const int d = lane + 32 * k;
         red[(warp * D + d) * 2] = sg[k];
         red[(warp * D + d) * 2 + 1] = sx[k];
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int q = 0; q < 8; ++q) {
+            s0 += double(red[(q * D + d) * 2]);
+            s1 += double(red[(q * D + d) * 2 + 1]);
+        }
+        double *o = partial + (size_t(d) * gridDim.x + blockIdx.x) * 2;
+        o[0] = s0;  // -> dbeta
+        o[1] = s1;  // -> dgamma
+    }
+}
+
+// Same with 16-byte accesses: lane owns columns 4*lane + 128*k (k < C4 = D/128); both rows of a
+// warp are loaded before either is reduced (more loads in flight per thread).
+template <int KIND, int C4>
+static __global__ void __launch_bounds__(256) ln_bwd_fused4_kernel(const float *__restrict__ g,
+                                                                   const float *__restrict__ x, int rows,
+                                                                   int in_stride, int D, const float *gb,
+                                                                   const float *mean, const float *rstd,
+                                                                   const float *dh_in, float *dh_out, CTensor copy,
+                                                                   double *partial) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    extern __shared__ float red[];  // [8][D][2]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float4 sg[C4], sx[C4];
+#pragma unroll
+    for (int k = 0; k < C4; ++k) sg[k] = sx[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int r0 = blockIdx.x * kLnBwdRows, r1 = min(rows, r0 + kLnBwdRows);
+    const bool vcopy = copy.hi && (copy.ld % 4) == 0;
+    for (int w = r0 + warp; w < r1; w += 8) {
+        const size_t xo = size_t(w) * in_stride * D, go = size_t(w) * D;
+        const float mu = mean[w], rs = rstd[w];
+        float4 gv[C4], xh[C4];
+        float a = 0.f, b = 0.f;
+#pragma unroll
+        for (int k = 0; k < C4; ++k) {
+            const int d = 4 * lane + 128 * k;
+            gv[k] = *reinterpret_cast<const float4 *>(g + go + d);
+            const float4 xv = *reinterpret_cast<const float4 *>(x + xo + d);
+            xh[k] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        }
+#pragma unroll
+        for (int k = 0; k < C4; ++k) {
+            const int d = 4 * lane + 128 * k;
+            const float4 gm = *reinterpret_cast<const float4 *>(gb + d);
+            const float g0 = gv[k].x * gm.x, g1 = gv[k].y * gm.y, g2 = gv[k].z * gm.z, g3 = gv[k].w * gm.w;
+            a += g0 + g1 + g2 + g3;
+            b += g0 * xh[k].x + g1 * xh[k].y + g2 * xh[k].z + g3 * xh[k].w;
+            sg[k].x += gv[k].x;
+            sg[k].y += gv[k].y;
+            sg[k].z += gv[k].z;
+            sg[k].w += gv[k].w;
+            sx[k].x = fmaf(gv[k].x, xh[k].x, sx[k].x);
+            sx[k].y = fmaf(gv[k].y, xh[k].y, sx[k].y);
+            sx[k].z = fmaf(gv[k].z, xh[k].z, sx[k].z);
+            sx[k].w = fmaf(gv[k].w, xh[k].w, sx[k].w);
+        }
+        a = warp_sum(a) / float(D);
+        b = warp_sum(b) / float(D);
+#pragma unroll
+        for (int k = 0; k < C4; ++k) {
+            const int d = 4 * lane + 128 * k;
+            const float4 gm = *reinterpret_cast<const float4 *>(gb + d);
+            const float4 hi = dh_in ? *reinterpret_cast<const float4 *>(dh_in + xo + d) : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 v;
+            v.x = hi.x + rs * (gv[k].x * gm.x - a - xh[k].x * b);
+            v.y = hi.y + rs * (gv[k].y * gm.y - a - xh[k].y * b);
+            v.z = hi.z + rs * (gv[k].z * gm.z - a - xh[k].z * b);
+            v.w = hi.w + rs * (gv[k].w * gm.w - a - xh[k].w * b);
+            *reinterpret_cast<float4 *>(dh_out + xo + d) = v;
+            if (vcopy) {
+                store_wc4<KIND>(copy, size_t(w) * in_stride * copy.ld + d, v);
+            } else if (copy.hi) {
+                const size_t co = size_t(w) * in_stride * copy.ld + d;
+                Fmt<KIND>::store(copy.hi, copy.lo, co, v.x);
+                Fmt<KIND>::store(copy.hi, copy.lo, co + 1, v.y);
+                Fmt<KIND>::store(copy.hi, copy.lo, co + 2, v.z);
+                Fmt<KIND>::store(copy.hi, copy.lo, co + 3, v.w);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < C4; ++k) {
+        const int d = 4 * lane + 128 * k;
+        float *o = red + (warp * D + d) * 2;
+        o[0] = sg[k].x;
+        o[1] = sx[k].x;
+        o[2] = sg[k].y;
+        o[3] = sx[k].y;
+        o[4] = sg[k].z;
+        o[5] = sx[k].z;
+        o[6] = sg[k].w;
+        o[7] = sx[k].w;
     }
     __syncthreads();
     for (int d = threadIdx.x; d < D; d += blockDim.x) {

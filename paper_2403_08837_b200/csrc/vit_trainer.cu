@@ -495,14 +495,17 @@ struct VitTrainer {
                            dh_in, dh_out, copy, lnpart.as<double>());
             });
         };
-        switch (D / 32) {
-            case 2: go(ln_bwd_fused_kernel<0, 2>); break;
-            case 4: go(ln_bwd_fused_kernel<0, 4>); break;
-            case 8: go(ln_bwd_fused_kernel<0, 8>); break;
-            case 16: go(ln_bwd_fused_kernel<0, 16>); break;
-            case 24: go(ln_bwd_fused_kernel<0, 24>); break;
-            case 32: go(ln_bwd_fused_kernel<0, 32>); break;
-            default: throw CdpError("LayerNorm width must be 64, 128, 256, 512, 768 or 1024");
+        switch (D % 128 == 0 ? D / 128 : 0) {  // 16-byte columns
+            case 1: go(ln_bwd_fused4_kernel<0, 1>); break;
+            case 2: go(ln_bwd_fused4_kernel<0, 2>); break;
+            case 4: go(ln_bwd_fused4_kernel<0, 4>); break;
+            case 6: go(ln_bwd_fused4_kernel<0, 6>); break;
+            case 8: go(ln_bwd_fused4_kernel<0, 8>); break;
+            default:
+                switch (D / 32) {
+                    case 2: go(ln_bwd_fused_kernel<0, 2>); break;
+                    default: throw CdpError("LayerNorm width must be 64, 128, 256, 512, 768 or 1024");
+                }
         }
         ln_attr_ = !sizing;
         L_("ln_param_finalize", 0, double(nblk) * D * 16, s, [&] {
