@@ -88,53 +88,52 @@ static __global__ void ln_fwd_kernel(const float *__restrict__ x, int rows, int 
     }
 }
 
-// LayerNorm backward of the input, one warp per row:
-//   dx = rstd * (g*gamma - mean(g*gamma) - xhat * mean(g*gamma*xhat));  dh_out = dh_in + dx
-// (row r of g / dh_* is row r * in_stride of the residual stream; dh_in may be null).
-static __global__ void ln_bwd_kernel(const float *__restrict__ g, const float *__restrict__ x, int rows, int in_stride, int D,
-                              const float *gb, const float *mean, const float *rstd, const float *dh_in,
-                              float *dh_out) {
+// Same with the row held in registers as float4 columns (lane owns 4*lane + 128*k, k < C4 = D/128):
+// one read of x, 16-byte accesses.
+template <int KIND, int C4>
+static __global__ void ln_fwd4_kernel(const float *__restrict__ x, int rows, int in_stride, int D, const float *gb,
+                                      float eps, CTensor out, float *mean, float *rstd) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= rows) return;
-    const size_t xo = size_t(w) * in_stride * D, go = size_t(w) * D;
-    const float mu = mean[w], rs = rstd[w];
-    float a = 0.f, b = 0.f;
-    for (int d = lane; d < D; d += 32) {
-        const float gg = g[go + d] * gb[d];
-        a += gg;
-        b += gg * ((x[xo + d] - mu) * rs);
+    const float *xr = x + size_t(w) * in_stride * D;
+    float4 v[C4];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < C4; ++k) {
+        v[k] = *reinterpret_cast<const float4 *>(xr + 4 * lane + 128 * k);
+        s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
     }
-    a = warp_sum(a) / float(D);
-    b = warp_sum(b) / float(D);
-    for (int d = lane; d < D; d += 32) {
-        const float xh = (x[xo + d] - mu) * rs;
-        const float dx = rs * (g[go + d] * gb[d] - a - xh * b);
-        dh_out[xo + d] = (dh_in ? dh_in[xo + d] : 0.f) + dx;
+    const float mu = warp_sum(s) / float(D);
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < C4; ++k) {
+        const float a = v[k].x - mu, b = v[k].y - mu, c = v[k].z - mu, d = v[k].w - mu;
+        q += (a * a + b * b) + (c * c + d * d);
     }
-}
-
-// LayerNorm parameter gradients, row-block partials: partial[d][blk][2] = (sum g xhat, sum g)
-// over the block's rows in order (fp64) -> bn_finalize_bwd_kernel (dbeta = [1], dgamma = [0]).
-constexpr int kLnRows = 128;
-static __global__ void ln_param_partial_kernel(const float *__restrict__ g, const float *__restrict__ x, int rows,
-                                        int in_stride, int D, const float *mean, const float *rstd,
-                                        double *partial) {
-    ptx::griddep_wait();
-    ptx::griddep_launch();
-    const int r0 = blockIdx.x * kLnRows, r1 = min(rows, r0 + kLnRows);
-    for (int d = threadIdx.x; d < D; d += blockDim.x) {
-        double sx = 0.0, sg = 0.0;
-        for (int r = r0; r < r1; ++r) {
-            const float gv = g[size_t(r) * D + d];
-            const float xh = (x[size_t(r) * in_stride * D + d] - mean[r]) * rstd[r];
-            sg += double(gv);
-            sx += double(gv) * double(xh);
+    const float rs = rsqrtf(warp_sum(q) / float(D) + eps);
+    const bool vec = (out.ld % 4) == 0;
+#pragma unroll
+    for (int k = 0; k < C4; ++k) {
+        const int d = 4 * lane + 128 * k;
+        const float4 ga = *reinterpret_cast<const float4 *>(gb + d), be = *reinterpret_cast<const float4 *>(gb + D + d);
+        const float4 y = make_float4(ga.x * ((v[k].x - mu) * rs) + be.x, ga.y * ((v[k].y - mu) * rs) + be.y,
+                                     ga.z * ((v[k].z - mu) * rs) + be.z, ga.w * ((v[k].w - mu) * rs) + be.w);
+        const size_t o = size_t(w) * out.ld + d;
+        if (vec) {
+            store_wc4<KIND>(out, o, y);
+        } else {
+            Fmt<KIND>::store(out.hi, out.lo, o, y.x);
+            Fmt<KIND>::store(out.hi, out.lo, o + 1, y.y);
+            Fmt<KIND>::store(out.hi, out.lo, o + 2, y.z);
+            Fmt<KIND>::store(out.hi, out.lo, o + 3, y.w);
         }
-        double *o = partial + (size_t(d) * gridDim.x + blockIdx.x) * 2;
-        o[0] = sg;  // -> dbeta
-        o[1] = sx;  // -> dgamma
+    }
+    if (lane == 0) {
+        Fmt<KIND>::store(out.hi, out.lo, size_t(w) * out.ld + D, 1.f);
+        mean[w] = mu;
+        rstd[w] = rs;
     }
 }
 

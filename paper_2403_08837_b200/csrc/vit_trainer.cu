@@ -475,10 +475,20 @@ struct VitTrainer {
     // ---------------------------------------------------------------- layers
     void layernorm(const float *x, int rows, int stride, int unit, int p, const CTensor &out, float *mean,
                    float *rstd, cudaStream_t s) {
-        L_("ln_fwd", 0, double(rows) * D * 6, s, [&] {
-            launch_pdl(ln_fwd_kernel<0>, dim3((rows * 32 + 255) / 256), dim3(256), 0, s, x, rows, stride, D,
-                       th(unit, p), eps, out, mean, rstd);
-        });
+        auto go = [&](auto kern) {
+            L_("ln_fwd", 0, double(rows) * D * 6, s, [&] {
+                launch_pdl(kern, dim3((rows * 32 + 255) / 256), dim3(256), 0, s, x, rows, stride, D, th(unit, p), eps,
+                           out, mean, rstd);
+            });
+        };
+        switch (D % 128 == 0 ? D / 128 : 0) {  // row in registers as 16-byte columns
+            case 1: go(ln_fwd4_kernel<0, 1>); break;
+            case 2: go(ln_fwd4_kernel<0, 2>); break;
+            case 4: go(ln_fwd4_kernel<0, 4>); break;
+            case 6: go(ln_fwd4_kernel<0, 6>); break;
+            case 8: go(ln_fwd4_kernel<0, 8>); break;
+            default: go(ln_fwd_kernel<0>); break;
+        }
     }
     // LayerNorm backward of `unit`: dh_out = dh_in + LN'(g); parameter gradients -> dgam / dbet.
     void layernorm_bwd(const float *g, const float *x, int rows, int stride, int unit, int p, const float *mean,
