@@ -338,7 +338,7 @@ struct ResNetTrainer {
             c.dgamma = DevBuf(c.cout * 4);
             c.dy = make_cbuf(kind, int(c.P), c.cout);
             max_stats = std::max<int64_t>(max_stats, int64_t(std::max(4 * c.tiles_fwd, 160)) * c.cout * 2);
-            max_part = std::max<int64_t>(max_part, ((c.P + kBnRows - 1) / kBnRows) * c.cout * 2);
+            max_part = std::max<int64_t>(max_part, ((c.P + kBnRowsMin - 1) / kBnRowsMin) * c.cout * 2);
         }
         const ConvL &c0 = convs[stem];
         cols = make_cbuf(kind, int(c0.P), c0.K);
@@ -745,12 +745,14 @@ struct ResNetTrainer {
         ConvL &c = convs[ci];
         zrecv<K>(c.tb, 1, s);
         if (ds >= 0) zrecv<K>(convs[ds].tb, 1, s);
-        const int nblk = int((c.P + kBnRows - 1) / kBnRows);
+        const int rows_blk = bn_rows_per_block(c.P, c.cout);  // kBnRowsMin or kBnRows
+        const int nblk = int((c.P + rows_blk - 1) / rows_blk);
         const int C4 = c.cout / 4, TPR = C4 < 32 ? C4 : 32;
         const ConvL *cd = ds >= 0 ? &convs[ds] : nullptr;
         const double bytes = double(c.P) * c.cout * (ysz() + esz() + ysz() + (cd ? ysz() : 0));
         L("bn_bwd_stats", 0, bytes, s, [&] {
-            launch_pdl(bn_bwd_stats_kernel<K>, dim3(nblk, (C4 + TPR - 1) / TPR), dim3(256), 0, s, g, mask, c.P,
+            auto kern = rows_blk == kBnRowsMin ? bn_bwd_stats_kernel<K, kBnRowsMin> : bn_bwd_stats_kernel<K, kBnRows>;
+            launch_pdl(kern, dim3(nblk, (C4 + TPR - 1) / TPR), dim3(256), 0, s, g, mask, c.P,
                        c.cout, (const void *)c.y.p, (const float *)c.mean.as<float>(),
                        (const float *)c.rstd.as<float>(), bnpart[0].as<double>(),
                        cd ? (const void *)cd->y.p : (const void *)nullptr,
