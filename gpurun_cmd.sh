@@ -1,1 +1,8 @@
-timeout 900 python -m pytest tests/test_gpu_resnet.py -m gpu -x -q 2>&1 | tail -2
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/bench_r1_final.json 2> gpurun_out/bench_r1_final.err; echo "bench rc=$?"
+for M in resnet18 resnet50 vit_b16; do
+timeout 900 ncu --profile-from-start off --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file gpurun_out/${M}_traffic.csv python tools/step_traffic.py $M gpurun_out/${M}_ops.json > gpurun_out/${M}_traffic.log 2>&1
+echo "$M traffic rc=$?"
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r1_launches_resnet18_bench.csv python bench.py --steps 2 --warmup 1 --no-extras --no-cpu-baseline > /dev/null 2>&1; echo "launch list rc=$?"
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
