@@ -496,7 +496,7 @@ struct ResNetTrainer {
         const int tiles = a.tiles_m * a.tiles_n * nph;
         int splits = 1;
         if (tiles < sms() && nph == 1)
-            splits = std::max(1, std::min(sms() / tiles, a.total_iters / 4));  // units <= one wave
+            splits = std::max(1, std::min(sms() / tiles, a.total_iters / split_min_kb()));  // units <= one wave
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
         using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;

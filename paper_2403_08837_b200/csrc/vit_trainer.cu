@@ -294,7 +294,7 @@ struct VitTrainer {
         a.out_hs = out_hs;
         const int tiles = a.tiles_m * a.tiles_n * a.nbatch;
         int splits = 1;
-        if (MODE != GM_BATCH && tiles < sms()) splits = std::max(1, std::min(sms() / tiles, a.total_iters / 4));
+        if (MODE != GM_BATCH && tiles < sms()) splits = std::max(1, std::min(sms() / tiles, a.total_iters / split_min_kb()));
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
         using PL = PkLaunch<0, BNc, AMN, BMN, Epi, MODE>;
