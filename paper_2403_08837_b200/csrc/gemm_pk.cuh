@@ -499,13 +499,13 @@ inline bool pk_pairs_enabled() {
     return on;
 }
 
-// Split-K: at least this many k-blocks per split (CDP_SPLIT_MIN_KB, default 4; 16 is 0.6 % faster on
-// ResNet-18 but moves the fp32 (3xTF32) bottleneck parity case from 1e-4 to 5e-4 rel-L2).
+// Split-K: at least this many k-blocks per split (CDP_SPLIT_MIN_KB, default 16: 0.6 % faster on
+// ResNet-18 than 4; fp32 mode caps its units at one 3xTF32 segment regardless).
 inline int split_min_kb() {
     static const int v = [] {
         const char *e = std::getenv("CDP_SPLIT_MIN_KB");
         const int k = e ? std::atoi(e) : 0;
-        return k > 0 ? k : 4;
+        return k > 0 ? k : 16;
     }();
     return v;
 }

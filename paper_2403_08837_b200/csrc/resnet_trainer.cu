@@ -498,6 +498,17 @@ struct ResNetTrainer {
         if (tiles < sms() && nph == 1)
             splits = std::max(1, std::min(sms() / tiles, a.total_iters / split_min_kb()));  // units <= one wave
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
+        if (K == 1 && nph == 1) {
+            // fp32 mode: the TMEM accumulator is not exact fp32 over long K, and the small 3xTF32 cross
+            // terms must not be summed into the large hi.hi accumulation: every unit covers at most 256
+            // of K inside ONE segment (a divisor of the segment's k-blocks); pk_reduce_kernel then sums
+            // the partials in fp32 in split order (tests/test_gpu_gemm.py).  Plain GEMMs (1x1 convs, the
+            // stem) were the fp32 path's main error: update rel-L2 2.4e-3 -> 2.8e-6 on the bottleneck
+            // case.  (Merged stride-2 phases stay unsplit: their partials would share the workspace.)
+            int ips = std::min(a.iters_per_split, std::min(a.kb_per_seg, 8));
+            while (a.kb_per_seg % ips) --ips;
+            a.iters_per_split = ips;
+        }
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
         using PL = PkLaunch<K, BNc, AMN, BMN, Epi, MODE>;
         a.units = tiles * a.splits;
