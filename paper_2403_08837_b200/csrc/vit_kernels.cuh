@@ -331,6 +331,112 @@ static __global__ void softmax_bwd_kernel(const float *__restrict__ dP, const __
     }
 }
 
+// Vectorised row softmax / backward for rows of at most 128*NV columns: lane owns columns
+// 4*lane + 128*k (16-byte fp32 / 8-byte bf16 accesses, one read of each row); columns >= n
+// (the padded tail of a 197-token row) are masked.
+template <int NV>
+static __global__ void softmax_fwd4_kernel(const float *__restrict__ S, int rows, int n, int lds, float scale,
+                                           __nv_bfloat16 *P, int ldp) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float *sr = S + size_t(w) * lds;
+    float v[NV][4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int c = 4 * lane + 128 * k;
+        float4 t = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (c < n) t = *reinterpret_cast<const float4 *>(sr + c);
+        v[k][0] = t.x * scale;
+        v[k][1] = c + 1 < n ? t.y * scale : -INFINITY;
+        v[k][2] = c + 2 < n ? t.z * scale : -INFINITY;
+        v[k][3] = c + 3 < n ? t.w * scale : -INFINITY;
+        if (c >= n) v[k][0] = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mx = fmaxf(mx, v[k][j]);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v[k][j] = __expf(v[k][j] - mx);
+            sum += v[k][j];
+        }
+    const float inv = 1.f / warp_sum(sum);
+    __nv_bfloat16 *pr = P + size_t(w) * ldp;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int c = 4 * lane + 128 * k;
+        if (c + 3 < n) {
+            __nv_bfloat162 a = __floats2bfloat162_rn(v[k][0] * inv, v[k][1] * inv);
+            __nv_bfloat162 b = __floats2bfloat162_rn(v[k][2] * inv, v[k][3] * inv);
+            uint2 u;
+            u.x = *reinterpret_cast<uint32_t *>(&a);
+            u.y = *reinterpret_cast<uint32_t *>(&b);
+            *reinterpret_cast<uint2 *>(pr + c) = u;
+        } else {
+            for (int j = 0; j < 4 && c + j < n; ++j) pr[c + j] = __float2bfloat16_rn(v[k][j] * inv);
+        }
+    }
+}
+
+template <int NV>
+static __global__ void softmax_bwd4_kernel(const float *__restrict__ dP, const __nv_bfloat16 *__restrict__ P, int rows,
+                                           int n, int lds, int ldp, float scale, __nv_bfloat16 *dS) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float *dr = dP + size_t(w) * lds;
+    const __nv_bfloat16 *pr = P + size_t(w) * ldp;
+    float g[NV][4], p[NV][4];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int c = 4 * lane + 128 * k;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) g[k][j] = p[k][j] = 0.f;
+        if (c + 3 < n) {
+            const float4 t = *reinterpret_cast<const float4 *>(dr + c);
+            const uint2 u = *reinterpret_cast<const uint2 *>(pr + c);
+            const float2 p01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
+            const float2 p23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
+            g[k][0] = t.x, g[k][1] = t.y, g[k][2] = t.z, g[k][3] = t.w;
+            p[k][0] = p01.x, p[k][1] = p01.y, p[k][2] = p23.x, p[k][3] = p23.y;
+        } else {
+            for (int j = 0; j < 4 && c + j < n; ++j) {
+                g[k][j] = dr[c + j];
+                p[k][j] = __bfloat162float(pr[c + j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dot += g[k][j] * p[k][j];
+    }
+    dot = warp_sum(dot);
+    __nv_bfloat16 *sr = dS + size_t(w) * ldp;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int c = 4 * lane + 128 * k;
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = scale * p[k][j] * (g[k][j] - dot);
+        if (c + 3 < n) {
+            __nv_bfloat162 a = __floats2bfloat162_rn(o[0], o[1]);
+            __nv_bfloat162 b = __floats2bfloat162_rn(o[2], o[3]);
+            uint2 u;
+            u.x = *reinterpret_cast<uint32_t *>(&a);
+            u.y = *reinterpret_cast<uint32_t *>(&b);
+            *reinterpret_cast<uint2 *>(sr + c) = u;
+        } else {
+            for (int j = 0; j < 4 && c + j < n; ++j) sr[c + j] = __float2bfloat16_rn(o[j]);
+        }
+    }
+}
+
 // fp32 [rows][D] -> compute format [rows][ld] (GEMM operand), optional row gather
 // (out row r <- in row (r / per) * in_per + skip + r % per).
 template <int KIND>

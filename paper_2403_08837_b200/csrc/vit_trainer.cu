@@ -573,8 +573,15 @@ struct VitTrainer {
             bgemm<false, false>("attn_scores", Q, Kv, T, T, HD, S.p, lds, int64_t(H) * T * lds, int64_t(T) * lds, 1,
                                 s);
             L_("softmax", 0, double(B) * H * T * T * 6, s, [&] {
-                launch_pdl(softmax_fwd_kernel, dim3((B * H * T * 32 + 255) / 256), dim3(256), 0, s,
-                           (const float *)S.as<float>(), B * H * T, T, lds, scale, y.P.as<__nv_bfloat16>(), ldp);
+                const dim3 g((B * H * T * 32 + 255) / 256);
+                const float *Sp = S.as<float>();
+                __nv_bfloat16 *Pp = y.P.as<__nv_bfloat16>();
+                if (T <= 128)
+                    launch_pdl(softmax_fwd4_kernel<1>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
+                else if (T <= 256)
+                    launch_pdl(softmax_fwd4_kernel<2>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
+                else
+                    launch_pdl(softmax_fwd_kernel, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
             });
             bgemm<false, true>("attn_values", Pv, V, T, HD, T, y.attn.hi.p, y.attn.ld, int64_t(T) * y.attn.ld, HD, 0,
                                s);
@@ -730,9 +737,16 @@ struct VitTrainer {
             bgemm<false, false>("attn_dprobs", dO, qv(2 * D), T, T, HD, dP.p, lds, int64_t(H) * T * lds,
                                 int64_t(T) * lds, 1, cs);
             L_("softmax_bwd", 0, double(B) * H * T * T * 8, cs, [&] {
-                launch_pdl(softmax_bwd_kernel, dim3((B * H * T * 32 + 255) / 256), dim3(256), 0, cs,
-                           (const float *)dP.as<float>(), (const __nv_bfloat16 *)y.P.as<__nv_bfloat16>(), B * H * T,
-                           T, lds, ldp, scale, static_cast<__nv_bfloat16 *>(dS.hi.p));
+                const dim3 g((B * H * T * 32 + 255) / 256);
+                const float *dPp = dP.as<float>();
+                const __nv_bfloat16 *Pp = y.P.as<__nv_bfloat16>();
+                __nv_bfloat16 *dSp = static_cast<__nv_bfloat16 *>(dS.hi.p);
+                if (T <= 128)
+                    launch_pdl(softmax_bwd4_kernel<1>, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
+                else if (T <= 256)
+                    launch_pdl(softmax_bwd4_kernel<2>, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
+                else
+                    launch_pdl(softmax_bwd_kernel, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
             });
             __nv_bfloat16 *dq = static_cast<__nv_bfloat16 *>(y.dqkv.hi.p);
             const int64_t dld = y.dqkv.ld;
