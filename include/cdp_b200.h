@@ -37,6 +37,8 @@ const char *cdp_last_error(void);
 int cdp_version(void);
 /* Number of SMs of the current device (0 if no device). */
 int cdp_device_sm_count(void);
+/* Synchronous device -> host copy (tests / diagnostics read internal buffers with it). */
+int cdp_memcpy_d2h(void *dst, const void *src, size_t bytes);
 
 /* Compute precision of the layer kernels. */
 enum cdp_dtype {
@@ -202,6 +204,12 @@ int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out);
 int cdp_resnet_mark(cdp_resnet *tr, int k);
 int cdp_resnet_elapsed(cdp_resnet *tr, int a, int b, float *ms);
 int cdp_resnet_flush_l2(cdp_resnet *tr);
+/* Device address, size and row pitch (elements; 0 = flat) of one internal buffer, for tests and
+ * diagnostics after cdp_resnet_sync.  Names: "wc_hi"/"wc_lo" (index = slot * n_tensors + tensor),
+ * "act_hi"/"act_lo" (activation), "y", "dy_hi", "dy_lo", "mean", "rstd", "dgamma", "dbeta" (conv
+ * index), "gbuf" (0..3), "dpooled", "z", "pooled_hi", "pooled_lo", "dz_hi", "dz_lo", "region", "pool_arg" (max-pool window
+ * argmax, u8 r*3+s per output element). */
+int cdp_resnet_buffer(cdp_resnet *tr, const char *name, int index, void **ptr, size_t *bytes, int *ld);
 
 /* ---- Vision Transformers (BASELINE configs[3]: ViT-B/16, 224x224), bf16 operands ------------ */
 /* One worker per process, same ring / hop / pull protocol as the ResNet trainer.  Model:

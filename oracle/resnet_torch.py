@@ -7,6 +7,17 @@ gradients computed here with torch autograd in float64.
 
 Model conventions are those of paper_2403_08837_b200/resnet.py (CIFAR stem,
 training-mode batch norm with per-micro-batch statistics, eps 1e-5).
+
+Kinks.  ReLU and max pool are not differentiable at their switching points: a
+pre-activation within fp32 rounding of 0 (or two max-pool window entries within
+rounding of each other) can take a different branch in the fp32 device step and
+in this float64 step, and one such flip moves every upstream gradient by ~1e-3
+(found tracing the round-1 2-rank CDP-v2 "deviation": one activation of the last
+block at +1.07e-6 on the device and <= 0 here).  `Kinks` lets a caller supply the
+device's own branch decisions (ReLU masks, max-pool argmaxes, read back from the
+trainer after each step); they are used ONLY where this oracle's own value is
+within `delta` of the switching point, everywhere else the float64 decision
+stands.  `Kinks.used` counts the overridden elements.
 """
 
 from __future__ import annotations
@@ -15,6 +26,48 @@ import numpy as np
 import torch
 import torch.nn as nn
 import torch.nn.functional as F
+
+
+class Kinks:
+    """Device branch decisions for the ambiguous elements of one forward pass (see module doc).
+
+    relu: list of bool arrays NCHW (device activation > 0) in forward ReLU order (stem, then per block
+    the inner ReLUs and the output ReLU); pool: int array [B, C, Ho, Wo] of window indices r*3+s."""
+
+    def __init__(self, relu=None, pool=None, delta=1e-5):
+        self.relu, self.pool, self.delta = relu, pool, delta
+        self.k = 0
+        self.used = 0
+
+    def relu_fn(self, v):
+        if self.relu is None:
+            return F.relu(v)
+        dev = torch.from_numpy(np.asarray(self.relu[self.k]))
+        self.k += 1
+        m = v.detach() > 0
+        amb = v.detach().abs() < self.delta
+        self.used += int((amb & (m != dev)).sum())
+        m = torch.where(amb, dev, m)
+        return v * m.to(v.dtype)
+
+    def pool_fn(self, y):
+        if self.pool is None:
+            return F.max_pool2d(y, 3, 2, 1)
+        B, C, H, W = y.shape
+        Ho, Wo = (H + 2 - 3) // 2 + 1, (W + 2 - 3) // 2 + 1
+        yp = F.pad(y, (1, 1, 1, 1), value=float("-inf"))
+        win = torch.stack([yp[:, :, r:r + 2 * Ho:2, s:s + 2 * Wo:2] for r in range(3) for s in range(3)], dim=2)
+        best = win.detach().argmax(dim=2, keepdim=True)  # first maximum, as the device's strict '>' scan
+        top = win.detach().gather(2, best)
+        dev = torch.from_numpy(np.asarray(self.pool, dtype=np.int64)).unsqueeze(2)
+        near = (top - win.detach().gather(2, dev)).abs() < self.delta
+        self.used += int((near & (dev != best)).sum())
+        idx = torch.where(near, dev, best)
+        return win.gather(2, idx).squeeze(2)
+
+
+def _relu(kinks, v):
+    return F.relu(v) if kinks is None else kinks.relu_fn(v)
 
 
 class Block(nn.Module):
@@ -35,15 +88,15 @@ class Block(nn.Module):
             self.ds_conv = nn.Conv2d(cin, cout, 1, stride, 0, bias=False)
             self.ds_bn = nn.BatchNorm2d(cout, eps=1e-5, track_running_stats=False)
 
-    def forward(self, x):
+    def forward(self, x, kinks=None):
         y = x
         n = len(self.convs)
         for i, (cv, bn) in enumerate(zip(self.convs, self.bns)):
             y = bn(cv(y))
             if i < n - 1:
-                y = F.relu(y)
+                y = _relu(kinks, y)
         s = self.ds_bn(self.ds_conv(x)) if self.ds_conv is not None else x
-        return F.relu(y + s)
+        return _relu(kinks, y + s)
 
 
 class TorchResNet(nn.Module):
@@ -66,12 +119,12 @@ class TorchResNet(nn.Module):
         self.blocks = nn.ModuleList(blocks)
         self.fc = nn.Linear(cin, classes)
 
-    def forward(self, x):
-        y = F.relu(self.stem_bn(self.stem_conv(x)))
+    def forward(self, x, kinks=None):
+        y = _relu(kinks, self.stem_bn(self.stem_conv(x)))
         if self.imagenet:
-            y = F.max_pool2d(y, 3, 2, 1)
+            y = F.max_pool2d(y, 3, 2, 1) if kinks is None else kinks.pool_fn(y)
         for b in self.blocks:
-            y = b(y)
+            y = b(y, kinks)
         return self.fc(y.mean(dim=(2, 3)))
 
 
@@ -128,18 +181,21 @@ class ResNetOracle:
         self.model = TorchResNet(widths, depths, classes, block, stem).double()
         self.specs = specs
 
-    def loss_and_grads(self, params, x, y):
+    def loss_and_grads(self, params, x, y, kinks=None):
         load_flat(self.model, np.concatenate(params), self.specs)
         self.model.zero_grad(set_to_none=True)
         xt = torch.from_numpy(np.ascontiguousarray(np.asarray(x, np.float64).transpose(0, 3, 1, 2)))
-        loss = F.cross_entropy(self.model(xt), torch.from_numpy(np.asarray(y, np.int64)))
+        loss = F.cross_entropy(self.model(xt, kinks), torch.from_numpy(np.asarray(y, np.int64)))
         loss.backward()
         return float(loss.item()), grads_flat(self.model, self.specs)
 
 
 def run_cdp(widths, depths, init, inputs, labels, n_workers, micro_batch, perms, lr, momentum, fresh_tensor,
-            block="basic", stem="cifar", classes=10, weight_decay=0.0):
-    """`steps = len(perms)` CDP steps from `init` (flat); fresh_tensor = N x n_tensors table (None = DP)."""
+            block="basic", stem="cifar", classes=10, weight_decay=0.0, kinks=None, stats=None):
+    """`steps = len(perms)` CDP steps from `init` (flat); fresh_tensor = N x n_tensors table (None = DP).
+
+    kinks: optional kinks[t-1][i-1] -> Kinks (the device's branch decisions of worker i at step t);
+    stats: optional dict, receives "kink_overrides" (elements where they were used)."""
     from oracle import engine as OE
     from paper_2403_08837_b200.resnet import flat_to_tensors, layer_specs
 
@@ -150,11 +206,24 @@ def run_cdp(widths, depths, init, inputs, labels, n_workers, micro_batch, perms,
     prev = [a.copy() for a in cur]
     vel = [np.zeros_like(a) for a in cur] if momentum else None
     losses = []
+    used = 0
     for t, perm in enumerate(perms, start=1):
         batches = [(inputs[perm[i * micro_batch:(i + 1) * micro_batch]], labels[perm[i * micro_batch:(i + 1) * micro_batch]])
                    for i in range(n_workers)]
+        grads_fn = orc.loss_and_grads
+        if kinks is not None:
+            worker = iter(range(n_workers))
+
+            def grads_fn(params, x, y, _t=t, _w=worker):
+                k = kinks[_t - 1][next(_w)]
+                out = orc.loss_and_grads(params, x, y, k)
+                nonlocal used
+                used += k.used
+                return out
         new, loss = OE.advance(None, cur, prev, t, batches, lr, fresh_tensor, momentum, vel,
-                               weight_decay=weight_decay, grads_fn=orc.loss_and_grads)
+                               weight_decay=weight_decay, grads_fn=grads_fn)
         prev, cur = cur, new
         losses.append(loss)
+    if stats is not None:
+        stats["kink_overrides"] = used
     return np.concatenate(cur), losses

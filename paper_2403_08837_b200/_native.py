@@ -26,6 +26,7 @@ SIGNATURES = {
     "cdp_last_error": (ctypes.c_char_p, []),
     "cdp_version": (c_int, []),
     "cdp_device_sm_count": (c_int, []),
+    "cdp_memcpy_d2h": (c_int, [c_void_p, c_void_p, c_size_t]),
     "cdp_mlp_value_grad": (c_int, [c_int, c_int64_p, c_double_p, c_int, c_double_p, c_double_p, c_int64_p, c_int,
                                    c_int, c_double_p, c_double_p]),
     "cdp_quad_value_grad": (c_int, [c_int, c_int, c_double_p, c_double_p, c_int, c_double_p, c_double_p, c_double_p]),
@@ -89,6 +90,8 @@ SIGNATURES = {
     "cdp_resnet_mark": (c_int, [c_void_p, c_int]),
     "cdp_resnet_elapsed": (c_int, [c_void_p, c_int, c_int, c_float_p]),
     "cdp_resnet_flush_l2": (c_int, [c_void_p]),
+    "cdp_resnet_buffer": (c_int, [c_void_p, ctypes.c_char_p, c_int, ctypes.POINTER(c_void_p),
+                                  ctypes.POINTER(c_size_t), c_int_p]),
     "cdp_vit_create_rank": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int_p,
                                     c_u8_p, c_float, c_float, c_int, c_float_p, c_int_p, ctypes.POINTER(c_void_p)]),
     "cdp_vit_info": (c_int, [c_void_p, c_int64_p, c_int_p]),
@@ -151,3 +154,7 @@ def lib():
 def check(rc: int) -> None:
     if rc != 0:
         raise NativeError(lib().cdp_last_error().decode())
+
+
+def memcpy_d2h(dst: int, src: int, nbytes: int) -> None:
+    check(lib().cdp_memcpy_d2h(ctypes.c_void_p(dst), ctypes.c_void_p(src), nbytes))

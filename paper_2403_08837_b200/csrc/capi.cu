@@ -6,6 +6,10 @@ extern "C" const char *cdp_last_error(void) { return cdp::get_error(); }
 
 extern "C" int cdp_version(void) { return 1; }
 
+extern "C" int cdp_memcpy_d2h(void *dst, const void *src, size_t bytes) {
+    return cdp::guarded([&] { CDP_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
+}
+
 extern "C" int cdp_device_sm_count(void) {
     int n = 0;
     if (cdp::guarded([&] { n = cdp::num_sms(); }) != 0) return 0;

@@ -1525,6 +1525,64 @@ extern "C" int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out) {
     });
 }
 
+// Device address / size / row pitch of one internal buffer (tests and diagnostics read them
+// after cdp_resnet_sync; names in include/cdp_b200.h).
+extern "C" int cdp_resnet_buffer(cdp_resnet *tr, const char *name, int index, void **ptr, size_t *bytes, int *ld) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        const std::string n(name);
+        const DevBuf *d = nullptr;
+        int l = 0;
+        auto conv = [&]() -> ConvL & {
+            CDP_REQUIRE(index >= 0 && index < int(m.convs.size()), "conv index out of range");
+            return m.convs[index];
+        };
+        auto cb = [&](const CBuf &c, bool lo) {
+            d = lo ? &c.lo : &c.hi;
+            l = c.ld;
+        };
+        if (n == "wc_hi" || n == "wc_lo") {
+            CDP_REQUIRE(index >= 0 && index < 2 * int(m.tens.size()), "wc index: slot * n_tensors + tensor");
+            cb(m.wc[index / int(m.tens.size())][index % int(m.tens.size())], n == "wc_lo");
+        } else if (n == "act_hi" || n == "act_lo") {
+            CDP_REQUIRE(index >= 0 && index < int(m.acts.size()), "activation index out of range");
+            cb(m.acts[index], n == "act_lo");
+        } else if (n == "dy_hi" || n == "dy_lo") {
+            cb(conv().dy, n == "dy_lo");
+        } else if (n == "y") {
+            d = &conv().y;
+        } else if (n == "mean") {
+            d = &conv().mean;
+        } else if (n == "rstd") {
+            d = &conv().rstd;
+        } else if (n == "dgamma") {
+            d = &conv().dgamma;
+        } else if (n == "dbeta") {
+            d = &conv().dbeta;
+        } else if (n == "gbuf") {
+            CDP_REQUIRE(index >= 0 && index < 4, "gbuf index 0..3");
+            d = &m.gbuf[index];
+        } else if (n == "dpooled") {
+            d = &m.dpooled;
+        } else if (n == "z") {
+            d = &m.z;
+        } else if (n == "pooled_hi" || n == "pooled_lo") {
+            cb(m.pooled, n == "pooled_lo");
+        } else if (n == "dz_hi" || n == "dz_lo") {
+            cb(m.dz, n == "dz_lo");
+        } else if (n == "region") {
+            d = &m.region;
+        } else if (n == "pool_arg") {
+            d = &m.pool_arg;
+        } else {
+            throw CdpError("unknown buffer name " + n);
+        }
+        *ptr = d->p;
+        *bytes = d->bytes;
+        *ld = l;
+    });
+}
+
 extern "C" int cdp_resnet_mark(cdp_resnet *tr, int k) {
     return guarded([&] {
         auto &m = *tr->impl;

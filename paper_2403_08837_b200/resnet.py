@@ -167,6 +167,7 @@ class DeviceResNet:
         self.widths, self.depths = tuple(widths), tuple(depths)
         self.block, self.stem, self.classes, self.image_hw = block, stem, int(classes), int(image_hw)
         self.micro_batch, self.world, self.rank = int(micro_batch), int(world), int(rank)
+        self.dtype = dtype
         self.specs = layer_specs(self.widths, self.depths, 3, image_hw, block, stem, classes)
         n_t = len(self.specs)
         self.stage = np.ascontiguousarray(stage_of_tensor if stage_of_tensor is not None
@@ -346,6 +347,67 @@ class DeviceResNet:
         ms = ctypes.c_float()
         N.check(self.lib.cdp_resnet_elapsed(self.h, a, b, ctypes.byref(ms)))
         return ms.value
+
+    def buffer(self, name, index=0, dtype=np.float32, rows=None):
+        """Host copy of one internal device buffer (tests / diagnostics; include/cdp_b200.h
+        cdp_resnet_buffer).  With `rows`, a [rows][ld] view."""
+        ptr, nb, ld = ctypes.c_void_p(), ctypes.c_size_t(), ctypes.c_int()
+        N.check(self.lib.cdp_resnet_buffer(self.h, name.encode(), int(index), ctypes.byref(ptr), ctypes.byref(nb),
+                                           ctypes.byref(ld)))
+        self.sync()
+        out = np.empty(nb.value // np.dtype(dtype).itemsize, dtype=dtype)
+        N.memcpy_d2h(out.ctypes.data, ptr.value, out.nbytes)
+        if rows is not None:
+            out = out[: rows * ld.value].reshape(rows, ld.value)
+        return out
+
+    def activation_shapes(self):
+        """[(role, H, W, C)] of the trainer's activation buffers in creation order: "relu" (a ReLU output:
+        stem, block inner and block output activations) or "pool" (the ImageNet stem's max-pool output)."""
+        out = []
+        H = self.image_hw
+        w0 = self.widths[0]
+        if self.stem == "cifar":
+            out.append(("relu", H, H, w0))
+        else:
+            H = (H + 6 - 7) // 2 + 1
+            out.append(("relu", H, H, w0))
+            H = (H + 2 - 3) // 2 + 1
+            out.append(("pool", H, H, w0))
+        cin = w0
+        exp = 4 if self.block == "bottleneck" else 1
+        for l, (w, d) in enumerate(zip(self.widths, self.depths)):
+            for k in range(d):
+                stride = 2 if (l > 0 and k == 0) else 1
+                Ho = (H - 1) // stride + 1
+                if self.block == "basic":
+                    out += [("relu", Ho, Ho, w), ("relu", Ho, Ho, w)]
+                else:
+                    out += [("relu", H, H, w), ("relu", Ho, Ho, w), ("relu", Ho, Ho, w * exp)]
+                cin, H = w * exp, Ho
+        return out
+
+    def branch_decisions(self):
+        """The last step's ReLU masks (activation > 0, NCHW bool, forward order) and max-pool window argmaxes
+        ([B, C, Ho, Wo], or None), read from the device: the kink decisions a float64 restatement needs to
+        follow the same branch where its own value is within rounding of a switching point."""
+        B = self.micro_batch
+        relu, pool = [], None
+        fp32 = self.dtype == "fp32"
+        for a, (role, H, W, C) in enumerate(self.activation_shapes()):
+            rows = B * H * W
+            if fp32:
+                v = self.buffer("act_hi", a, np.float32, rows)[:, :C].astype(np.float64) + \
+                    self.buffer("act_lo", a, np.float32, rows)[:, :C]
+            else:
+                raw = self.buffer("act_hi", a, np.uint16, rows)[:, :C].astype(np.uint32) << 16
+                v = raw.view(np.float32)
+            if role == "relu":
+                relu.append(np.ascontiguousarray((v > 0).reshape(B, H, W, C).transpose(0, 3, 1, 2)))
+            else:
+                arg = self.buffer("pool_arg", 0, np.uint8)[: rows * C].reshape(B, H, W, C)
+                pool = np.ascontiguousarray(arg.transpose(0, 3, 1, 2).astype(np.int64))
+        return relu, pool
 
     def flush_l2(self):
         N.check(self.lib.cdp_resnet_flush_l2(self.h))

@@ -2,9 +2,13 @@
 
 Tolerances: fp32 mode (3xTF32 products, every TMEM accumulation at most 256 of K
 inside one 3xTF32 segment with the split partials summed in fp32, batch-norm
-reductions in fp64): parameters rel-L2 <= 1e-6 (measured 6e-8 / 8e-8) on the 16x16 /
-32x32 cases, 1e-4 (measured 1.7e-5) at 112x112, 3e-3 on the ill-conditioned four-stage
-case; losses rel <= 2e-4; bf16 mode: rel-L2 <= 3e-2.
+reductions in fp64): parameters rel-L2 <= 1e-6 on the 16x16 / 32x32 cases at 1-4
+ranks, 1e-4 at 112x112, 3e-3 on the ill-conditioned four-stage case; losses rel
+<= 1e-6; bf16 mode: rel-L2 <= 3e-2.  fp32 comparisons use the kink-aware
+restatement: at elements whose float64 value is within 1e-5 of a ReLU / max-pool
+switching point the restatement follows the device's branch (read back after every
+step), because a fp32-vs-fp64 flip there is a discrete ~1e-3 gradient change, not an
+arithmetic error (oracle/resnet_torch.py "Kinks").
 Parity is against the restatement only — the reference has no ResNet.
 """
 
@@ -32,7 +36,10 @@ def _data(n, seed=0, hw=HW, classes=10):
     return synthetic_cifar(n, seed, hw=hw, classes=classes)
 
 
-def _ranks(world, rule, dtype, steps, momentum=0.9, arch="basic"):
+def _ranks(world, rule, dtype, steps, momentum=0.9, arch="basic", capture=True, seed=5, weight_decay=0.0):
+    """Run `world` ranks (one process, one GPU: the N-rank emulation over peer pointers) for `steps` steps.
+    capture: step the ranks one step at a time (rank order, synchronised) and read each rank's branch
+    decisions (ReLU masks, max-pool argmaxes) after every step for the kink-aware restatement."""
     from oracle.resnet_torch import init_flat
     from paper_2403_08837_b200.resnet import DeviceResNet
 
@@ -40,17 +47,23 @@ def _ranks(world, rule, dtype, steps, momentum=0.9, arch="basic"):
     W, D = a.get("W", globals()["W"]), a.get("D", globals()["D"])
     x, y = _data(world * MB * 2, hw=a["hw"], classes=a["classes"])
     init = init_flat(W, D, seed=0, block=a["block"], stem=a["stem"], classes=a["classes"])
-    perms = [np.random.default_rng([5, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
-    tr = [DeviceResNet(W, D, MB, world, r, rule, dtype, momentum, inputs=x, labels=y, image_hw=a["hw"],
-                       block=a["block"], stem=a["stem"], classes=a["classes"])
+    perms = [np.random.default_rng([seed, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
+    tr = [DeviceResNet(W, D, MB, world, r, rule, dtype, momentum, weight_decay, inputs=x, labels=y,
+                       image_hw=a["hw"], block=a["block"], stem=a["stem"], classes=a["classes"])
           for r in range(world)]
     regions = [t.region() for t in tr]
     for t in tr:
         t.set_params(init, -1)
         t.connect(regions)
+    kinks = []
     for step in range(steps):
+        per_rank = []
         for r, t in enumerate(tr):
             t.step(perms[step][r * MB:(r + 1) * MB], 0.05)
+            if capture:
+                t.sync()
+                per_rank.append(t.branch_decisions())
+        kinks.append(per_rank)
     for t in tr:
         t.sync()
         assert t.ring_error() == 0
@@ -59,19 +72,26 @@ def _ranks(world, rule, dtype, steps, momentum=0.9, arch="basic"):
     stage = tr[0].stage
     for t in tr:
         t.close()
-    return init, x, y, perms, losses, final, stage
+    return init, x, y, perms, losses, final, stage, (kinks if capture else None)
 
 
-def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9, arch="basic"):
-    from oracle.resnet_torch import run_cdp
+def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9, arch="basic", kinks=None, weight_decay=0.0):
+    """The float64 restatement of the same run; with `kinks`, the device's branch decisions are followed at
+    elements within 1e-5 of a ReLU / max-pool switching point (oracle/resnet_torch.py, "Kinks")."""
+    from oracle.resnet_torch import Kinks, run_cdp
 
     W, D = ARCH[arch].get("W", globals()["W"]), ARCH[arch].get("D", globals()["D"])
     fresh = None
     if rule is not None:
         fresh = [[rule.reads_fresh(i, int(s)) for s in stage] for i in range(1, world + 1)]
     a = ARCH[arch]
-    return run_cdp(W, D, init, x.astype(np.float64), y, world, MB, perms, 0.05, momentum, fresh, block=a["block"],
-                   stem=a["stem"], classes=a["classes"])
+    k = None
+    if kinks is not None:
+        k = [[Kinks(relu, pool) for relu, pool in step] for step in kinks]
+    st = {}
+    out = run_cdp(W, D, init, x.astype(np.float64), y, world, MB, perms, 0.05, momentum, fresh, block=a["block"],
+                  stem=a["stem"], classes=a["classes"], kinks=k, stats=st, weight_decay=weight_decay)
+    return out[0], out[1], st.get("kink_overrides", 0)
 
 
 def _rel(a, b):
@@ -79,36 +99,69 @@ def _rel(a, b):
 
 
 @pytest.mark.parametrize("arch", ["basic", "bottleneck", "bottleneck112", "bottleneck112x4"])
-@pytest.mark.parametrize("dtype,tol", [("fp32", 2e-4), ("bf16", 3e-2)])
+@pytest.mark.parametrize("dtype,tol", [("fp32", 1e-6), ("bf16", 3e-2)])
 def test_single_gpu_steps_vs_torch_restatement(cuda, dtype, tol, arch):
     if dtype == "fp32":
         tol = ARCH[arch].get("fp32_tol", tol)
-    init, x, y, perms, losses, final, stage = _ranks(1, None, dtype, 3, arch=arch)
-    want, wl = _oracle(init, x, y, perms, 1, None, stage, arch=arch)
+    init, x, y, perms, losses, final, stage, kinks = _ranks(1, None, dtype, 3, arch=arch)
+    want, wl, _ = _oracle(init, x, y, perms, 1, None, stage, arch=arch, kinks=kinks if dtype == "fp32" else None)
     assert _rel(final, want) <= tol, _rel(final, want)
     assert np.all(np.abs(losses - np.array(wl)) <= tol * np.abs(np.array(wl)) + 1e-6), (losses, wl)
 
 
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("rule_name", ["cdp-v1", "cdp-v2"])
-def test_two_ranks_cdp_vs_torch_restatement(cuda, rule_name):
+def test_multi_rank_cdp_vs_torch_restatement(cuda, rule_name, world):
+    """N ranks, CDP-v1 / CDP-v2, fp32: the single-rank parity level (1e-6).  (Round 1's 1.3e-4 2-rank
+    CDP-v2 "deviation" was one ReLU pre-activation within fp32 rounding of 0 — the kink-aware
+    restatement follows the device's branch there, tests/test_gpu_resnet.py::test_kink_flip_explains.)"""
     from paper_2403_08837_b200.rules import rule_by_name
 
-    rule = rule_by_name(rule_name, 2)
-    init, x, y, perms, losses, final, stage = _ranks(2, rule, "fp32", 4)
-    want, wl = _oracle(init, x, y, perms, 2, rule, stage)
-    # measured: cdp-v1 < 1e-5, cdp-v2 1.3e-4 (single-rank fp32 steps are at 6e-8; round-2 item)
-    assert _rel(final, want) <= 2e-4, _rel(final, want)
-    assert np.all(np.abs(losses - np.array(wl)) <= 2e-4 * np.abs(np.array(wl))), (losses, wl)
+    rule = rule_by_name(rule_name, world)
+    init, x, y, perms, losses, final, stage, kinks = _ranks(world, rule, "fp32", 4)
+    want, wl, _ = _oracle(init, x, y, perms, world, rule, stage, kinks=kinks)
+    assert _rel(final, want) <= 1e-6, _rel(final, want)
+    assert np.all(np.abs(losses - np.array(wl)) <= 1e-6 * np.abs(np.array(wl))), (losses, wl)
 
 
-@pytest.mark.parametrize("arch", ["basic", "bottleneck"])
-def test_two_ranks_cdp_v2_bottleneck_vs_torch_restatement(cuda, arch):
+def test_kink_flip_explains_round1_deviation(cuda):
+    """The round-1 2-rank CDP-v2 case (seed 5, 4 steps): without the device's branch decisions the
+    restatement differs by ~1e-4 and at least one element sits within 1e-5 of a ReLU switching point;
+    with them it matches to 1e-6."""
     from paper_2403_08837_b200.rules import rule_by_name
 
     rule = rule_by_name("cdp-v2", 2)
-    init, x, y, perms, losses, final, stage = _ranks(2, rule, "fp32", 3, arch=arch)
-    want, wl = _oracle(init, x, y, perms, 2, rule, stage, arch=arch)
-    assert _rel(final, want) <= 2e-4, _rel(final, want)
+    init, x, y, perms, losses, final, stage, kinks = _ranks(2, rule, "fp32", 4)
+    plain, _, _ = _oracle(init, x, y, perms, 2, rule, stage)
+    follow, _, used = _oracle(init, x, y, perms, 2, rule, stage, kinks=kinks)
+    assert used >= 1
+    assert _rel(final, plain) > 1e-5
+    assert _rel(final, follow) <= 1e-6, _rel(final, follow)
+
+
+@pytest.mark.parametrize("arch", ["basic", "bottleneck"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_cdp_v2_archs_vs_torch_restatement(cuda, arch, world):
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = rule_by_name("cdp-v2", world)
+    init, x, y, perms, losses, final, stage, kinks = _ranks(world, rule, "fp32", 3, arch=arch)
+    want, wl, _ = _oracle(init, x, y, perms, world, rule, stage, arch=arch, kinks=kinks)
+    assert _rel(final, want) <= ARCH[arch]["fp32_tol"], _rel(final, want)
+
+
+@pytest.mark.parametrize("world,rule_name", [(1, None), (2, "cdp-v2")])
+def test_weight_decay_vs_torch_restatement(cuda, world, rule_name):
+    """SGD + momentum + weight decay fused into the last hop (north star (2)) vs the restatement's
+    `weight_decay` (g = acc/N + wd*theta_t; the reference engine has no wd, oracle/engine.py)."""
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = rule_by_name(rule_name, world) if rule_name else None
+    init, x, y, perms, losses, final, stage, kinks = _ranks(world, rule, "fp32", 3, weight_decay=5e-2)
+    want, wl, _ = _oracle(init, x, y, perms, world, rule, stage, kinks=kinks, weight_decay=5e-2)
+    nowd, _, _ = _oracle(init, x, y, perms, world, rule, stage, kinks=kinks)
+    assert _rel(final, want) <= 1e-6, _rel(final, want)
+    assert _rel(final, nowd) > 1e-4  # the decay term is really applied
 
 
 def test_profile_and_host_batch_steps(cuda):
@@ -143,10 +196,12 @@ def test_profile_and_host_batch_steps(cuda):
 
 
 @pytest.mark.parametrize("world,arch", [(2, "basic"), (4, "basic"), (3, "bottleneck")])
-def test_zero_cdp_state_passing_bit_identical_to_cdp_v2(cuda, world, arch):
-    """ZeRO-CDP (parameter state handed holder -> next user by P2P copy, ref comm.py:93-144) computes exactly
-    what CDP-v2 with a full replica per rank computes; a mid-run drain + sync (end of a run, then
-    continuing) does not change the result."""
+def test_zero_cdp_vs_torch_restatement(cuda, world, arch):
+    """ZeRO-CDP (parameter state handed holder -> next user by P2P copy, ref comm.py:93-144) matches the
+    float64 restatement of CDP-v2 at 1e-6 and is bit-identical to full-replica CDP-v2; a mid-run drain +
+    sync (end of a run, then continuing) does not change the result.  The ZeRO ranks cannot be stepped
+    one synchronised step at a time (a backward may wait for another rank's next-step forward), so the
+    restatement follows the branch decisions captured from the (bit-identical) full-replica run."""
     from oracle.resnet_torch import init_flat
     from paper_2403_08837_b200.resnet import DeviceResNet
     from paper_2403_08837_b200.rules import rule_by_name
@@ -158,6 +213,7 @@ def test_zero_cdp_state_passing_bit_identical_to_cdp_v2(cuda, world, arch):
     steps = 5
     perms = [np.random.default_rng([7, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
     out = {}
+    kinks = []
     for zero in (False, True):
         tr = [DeviceResNet(W, D, MB, world, r, rule, "fp32", 0.9, inputs=x, labels=y, image_hw=a["hw"],
                            block=a["block"], stem=a["stem"], classes=a["classes"], zero=zero) for r in range(world)]
@@ -166,8 +222,13 @@ def test_zero_cdp_state_passing_bit_identical_to_cdp_v2(cuda, world, arch):
             t.set_params(init, -1)
             t.connect(regions)
         for k in range(steps):
+            per_rank = []
             for r, t in enumerate(tr):
                 t.step(perms[k][r * MB:(r + 1) * MB], 0.05)
+                if not zero:
+                    t.sync()
+                    per_rank.append(t.branch_decisions())
+            kinks.append(per_rank)
             if zero and k == 2:  # end-of-run drain in the middle, then continue
                 for t in tr:
                     t.zero_drain()
@@ -179,12 +240,19 @@ def test_zero_cdp_state_passing_bit_identical_to_cdp_v2(cuda, world, arch):
             t.sync()
             assert t.ring_error() == 0
         out[zero] = (np.mean([t.history(steps)[0] for t in tr], axis=0), tr[-1].get_params(0),
-                     tr[0].stats()["zero_state_bytes_per_step"])
+                     tr[0].stats()["zero_state_bytes_per_step"], tr[0].stage)
         for t in tr:
             t.close()
     assert np.array_equal(out[True][0], out[False][0])
     assert np.array_equal(out[True][1], out[False][1])
     assert out[True][2] > 0 and out[False][2] == 0
+    from oracle.resnet_torch import Kinks, run_cdp
+
+    fresh = [[rule.reads_fresh(i, int(s)) for s in out[True][3]] for i in range(1, world + 1)]
+    k = [[Kinks(relu, pool) for relu, pool in st] for st in kinks[:steps]]
+    want, _ = run_cdp(W, D, init, x.astype(np.float64), y, world, MB, perms, 0.05, 0.9, fresh, block=a["block"],
+                      stem=a["stem"], classes=a["classes"], kinks=k)
+    assert _rel(out[True][1], want) <= ARCH[arch]["fp32_tol"], _rel(out[True][1], want)
 
 
 def test_dp_allreduce_baseline_bit_identical_to_dp_ring(cuda):
@@ -241,9 +309,9 @@ def test_cta_pair_option(cuda):
     code = ("import importlib.util as U, sys;"
             f"sys.path.insert(0, {os.path.dirname(os.path.dirname(here))!r});"
             f"s = U.spec_from_file_location('tgr', {here!r}); T = U.module_from_spec(s); s.loader.exec_module(T);"
-            "init, x, y, perms, losses, final, stage = T._ranks(1, None, 'fp32', 3, arch='bottleneck');"
-            "want, wl = T._oracle(init, x, y, perms, 1, None, stage, arch='bottleneck');"
-            "assert T._rel(final, want) <= 2e-4, T._rel(final, want); print('ok')")
+            "init, x, y, perms, losses, final, stage, kinks = T._ranks(1, None, 'fp32', 3, arch='bottleneck');"
+            "want, wl, _ = T._oracle(init, x, y, perms, 1, None, stage, arch='bottleneck', kinks=kinks);"
+            "assert T._rel(final, want) <= 1e-6, T._rel(final, want); print('ok')")
     env = dict(os.environ, CDP_PK_PAIRS="1")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=os.path.dirname(os.path.dirname(here)))
