@@ -210,6 +210,13 @@ int cdp_resnet_flush_l2(cdp_resnet *tr);
  * index), "gbuf" (0..3), "dpooled", "z", "pooled_hi", "pooled_lo", "dz_hi", "dz_lo", "region", "pool_arg" (max-pool window
  * argmax, u8 r*3+s per output element). */
 int cdp_resnet_buffer(cdp_resnet *tr, const char *name, int index, void **ptr, size_t *bytes, int *ld);
+/* Trace mode (create option bit 1, value 2): the executed-version record of every parameter access,
+ * 8 x uint32 per record: step t, rank, unit (1-based tensor), kind (0 forward read, 1 backward read,
+ * 2 update read of theta_t, 3 update's new slot), phase (0 before / 1 after the access), theta slot,
+ * version tag found in the slot, 0.  Copies up to max_records (count = all recorded since the last
+ * call) and clears the log.  Version tags travel with the data: set_params, updates, pulls and
+ * ZeRO-CDP state copies write them (ref engine.py:92-94 records (t, i, j, v) per read). */
+int cdp_resnet_trace(cdp_resnet *tr, uint32_t *records, int max_records, int *count);
 
 /* ---- Vision Transformers (BASELINE configs[3]: ViT-B/16, 224x224), bf16 operands ------------ */
 /* One worker per process, same ring / hop / pull protocol as the ResNet trainer.  Model:
@@ -224,6 +231,9 @@ int cdp_vit_create_rank(int image, int patch, int dim, int depth, int heads, int
                         int world, int rank, const int32_t *unit_stage, const uint8_t *stage_fresh, float momentum,
                         float weight_decay, int n_samples, const float *x, const int32_t *labels, cdp_vit **out);
 int cdp_vit_info(cdp_vit *tr, int64_t *n_params, int *n_units);
+/* Trace mode (set before cdp_vit_connect): records as cdp_resnet_trace, unit = 1-based hop unit. */
+int cdp_vit_set_trace(cdp_vit *tr, int on);
+int cdp_vit_trace(cdp_vit *tr, uint32_t *records, int max_records, int *count);
 int cdp_vit_region(cdp_vit *tr, void **base);
 int cdp_vit_ipc_handle(cdp_vit *tr, void *handle64);
 int cdp_vit_connect(cdp_vit *tr, void *const *regions);

@@ -90,11 +90,14 @@ SIGNATURES = {
     "cdp_resnet_mark": (c_int, [c_void_p, c_int]),
     "cdp_resnet_elapsed": (c_int, [c_void_p, c_int, c_int, c_float_p]),
     "cdp_resnet_flush_l2": (c_int, [c_void_p]),
+    "cdp_resnet_trace": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_uint32), c_int, c_int_p]),
     "cdp_resnet_buffer": (c_int, [c_void_p, ctypes.c_char_p, c_int, ctypes.POINTER(c_void_p),
                                   ctypes.POINTER(c_size_t), c_int_p]),
     "cdp_vit_create_rank": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int_p,
                                     c_u8_p, c_float, c_float, c_int, c_float_p, c_int_p, ctypes.POINTER(c_void_p)]),
     "cdp_vit_info": (c_int, [c_void_p, c_int64_p, c_int_p]),
+    "cdp_vit_set_trace": (c_int, [c_void_p, c_int]),
+    "cdp_vit_trace": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_uint32), c_int, c_int_p]),
     "cdp_vit_region": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_vit_ipc_handle": (c_int, [c_void_p, c_void_p]),
     "cdp_vit_connect": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
@@ -158,3 +161,24 @@ def check(rc: int) -> None:
 
 def memcpy_d2h(dst: int, src: int, nbytes: int) -> None:
     check(lib().cdp_memcpy_d2h(ctypes.c_void_p(dst), ctypes.c_void_p(src), nbytes))
+
+
+TRACE_FIELDS = ("t", "rank", "unit", "kind", "phase", "slot", "version")
+
+
+def read_access_trace(fn, handle, max_records=1 << 16):
+    """Executed-version records of a trace-mode trainer (cdp_resnet_trace / cdp_vit_trace): structured array
+    with fields t, rank, unit (1-based), kind (0 fwd / 1 bwd / 2 update read / 3 update's new slot),
+    phase (0 before / 1 after), slot, version (the tag of the data found in the slot)."""
+    import numpy as np
+
+    buf = np.zeros((max_records, 8), dtype=np.uint32)
+    n = ctypes.c_int()
+    check(fn(handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), max_records, ctypes.byref(n)))
+    if n.value > max_records:
+        raise RuntimeError(f"{n.value} trace records, read at most {max_records}")
+    r = buf[: n.value].astype(np.int64)
+    out = np.empty(n.value, dtype=np.dtype([(k, np.int64) for k in TRACE_FIELDS]))
+    for i, k in enumerate(TRACE_FIELDS):
+        out[k] = r[:, i]
+    return out

@@ -538,6 +538,7 @@ struct EpiHop2 {
                 if (p.mode == 0 || p.mode == 1) ptx::st_release_sys(&p.sync.own->ready[j], t);
                 if (p.mode == 2) {
                     p.sync.own->pulled[j][(t + 1) & 1] = 0;
+                    p.sync.own->vtag[(t + 1) & 1][j] = t + 1;  // version tag of the new slot (trace mode)
                     ptx::st_release_sys(&p.sync.own->updated[j], t + 1);
                 }
             }

@@ -154,6 +154,7 @@ struct RingFlags {
     uint32_t updated[kMaxStages];    // updater: stage j holds version `updated[j]`
     uint32_t pulled[kMaxStages][2];  // updater: readers that pulled version v (slot v % 2)
     uint32_t zdone[kMaxStages];      // ZeRO-CDP: global use index of this rank's last finished use of a unit
+    uint32_t vtag[2][kMaxStages];    // trace mode: version held by theta slot s of unit j (travels with the data)
     uint32_t err;                    // a spin-wait timed out (protocol failure)
     uint32_t pad[31];
 };
@@ -168,12 +169,16 @@ struct DistSync {
     int pre_external;         // the pre-hop waits ran in a preceding one-CTA kernel (hop_wait_kernel)
 };
 
+// A wait that is not satisfied within ~9 s (2^34 cycles) is a protocol failure (or a peer that
+// died): record it and trap, so the kernel never goes on to read partial sums / parameter slots
+// that are not ready (the launch fails loudly instead of silently corrupting training).
 __device__ __forceinline__ void spin_ge(const uint32_t *f, uint32_t v, uint32_t *err) {
     const long long t0 = clock64();
     while (ptx::ld_acquire_sys(f) < v) {
-        if (clock64() - t0 > (1ll << 32)) {  // ~2 s: report instead of hanging the GPU
+        if (clock64() - t0 > (1ll << 34)) {
             atomicExch(err, 1u);
-            return;
+            __threadfence_system();
+            __trap();
         }
         __nanosleep(64);
     }
@@ -447,6 +452,7 @@ struct EpiWgrad {
                 if (p.mode == 0 || p.mode == 1) ptx::st_release_sys(&p.sync.own->ready[j], t);
                 if (p.mode == 2) {
                     p.sync.own->pulled[j][(t + 1) & 1] = 0;
+                    p.sync.own->vtag[(t + 1) & 1][j] = t + 1;  // version tag of the new slot (trace mode)
                     ptx::st_release_sys(&p.sync.own->updated[j], t + 1);
                 }
             }

@@ -18,10 +18,48 @@ __global__ void pull_wait_kernel(RingFlags *updater, RingFlags *own, int unit, i
     if (v > 1 && threadIdx.x == 0) spin_ge(&updater->updated[unit - 1], v, &own->err);
 }
 
+// ---------------------------------------------------------------- trace mode (tests)
+// Every theta slot carries a version tag (RingFlags::vtag) written by whoever writes the slot's
+// data: set_params (host), the update (vtag_update_kernel after the update kernel on the same
+// stream), a pull (copies the updater's tag while the updater is still held off by `pulled`), a
+// ZeRO-CDP state copy (copies the predecessor's tags).  Around every read of a unit's parameters an
+// access record (step, rank, unit, kind, phase, slot, tag) is appended: the executed-version trace
+// of ref engine.py:92-94, made from the data actually present in the slot the kernel reads.
+enum AccessKind { A_FWD = 0, A_BWD = 1, A_UPD = 2, A_NEW = 3 };
+constexpr int kTraceWords = 8;
+
+struct TraceLog {
+    uint32_t *rec;
+    uint32_t *cursor;
+    uint32_t cap;
+};
+
+__global__ void access_record_kernel(TraceLog lg, const RingFlags *own, int rank, int unit, int kind, int phase,
+                                     int slot, const int *step) {
+    const uint32_t i = atomicAdd(lg.cursor, 1u);
+    if (i >= lg.cap) return;
+    uint32_t *r = lg.rec + size_t(i) * kTraceWords;
+    r[0] = uint32_t(*step);
+    r[1] = uint32_t(rank);
+    r[2] = uint32_t(unit);
+    r[3] = uint32_t(kind);
+    r[4] = uint32_t(phase);
+    r[5] = uint32_t(slot);
+    r[6] = ptx::ld_acquire_sys(&own->vtag[slot][unit - 1]);
+    r[7] = 0;
+}
+
+// After the update of `unit` at step t (same stream): its new slot holds version t + 1.
+__global__ void vtag_update_kernel(RingFlags *own, int unit, const int *step) {
+    const uint32_t t = uint32_t(*step);
+    __threadfence_system();
+    ptx::st_release_sys(&own->vtag[(t + 1) & 1][unit - 1], t + 1);
+}
+
 template <int KIND>
 __global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, int64_t n, int cols, CTensor wc,
                                    RingFlags *updater, RingFlags *own, int unit, int fresh, const int *step,
-                                   unsigned *cta_counter) {
+                                   unsigned *cta_counter, int trace) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int t = *step;
@@ -37,6 +75,8 @@ __global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, in
         __threadfence_system();
         if (atomicAdd(&cta_counter[unit - 1], 1u) == gridDim.x - 1) {
             cta_counter[unit - 1] = 0;
+            // the updater cannot overwrite slot v & 1 before this arrival: its tag is the copied version
+            if (trace) own->vtag[v & 1][unit - 1] = ptx::ld_acquire_sys(&updater->vtag[v & 1][unit - 1]);
             atomicAdd_system(&updater->pulled[unit - 1][v & 1], 1u);
         }
     }

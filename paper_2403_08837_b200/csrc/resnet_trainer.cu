@@ -86,11 +86,15 @@ __device__ __forceinline__ uint32_t zero_u(const ZeroUse &z, int t) {
 
 // Wait (one thread) until the predecessor's rank finished its use of `unit`.
 __global__ void zero_wait_kernel(ZeroUse z, int self, const RingFlags *src_flags, RingFlags *own, int unit,
-                                 const int *step, int step_delta) {
+                                 const int *step, int step_delta, int copy_tags) {
     const int t = *step + step_delta;
     if (threadIdx.x != 0 || z.src == self || t + z.dstep < 1) return;
     const uint32_t pu = zero_u(z, t) - 1;
     spin_ge(&src_flags->zdone[unit - 1], pu, &own->err);
+    if (copy_tags) {  // trace mode: the state copy that follows brings the predecessor's versions
+        own->vtag[0][unit - 1] = ptx::ld_acquire_sys(&src_flags->vtag[0][unit - 1]);
+        own->vtag[1][unit - 1] = ptx::ld_acquire_sys(&src_flags->vtag[1][unit - 1]);
+    }
 }
 
 // Copy the unit's state (both theta version slots, momentum) from the predecessor's HBM
@@ -181,6 +185,9 @@ struct ResNetTrainer {
     DevBuf flush_buf;
     bool sizing = false;       // dry run: size the split-K workspaces, launch nothing
     bool instr = false;        // eager instrumented step: events around every launch
+    bool trace = false;        // version tags + per-access records (tests; rank_common.cuh)
+    DevBuf tlog, tcur;
+    static constexpr uint32_t kTraceCap = 1u << 16;
     std::vector<OpRec> oprecs;
 
     ~ResNetTrainer() {
@@ -639,6 +646,7 @@ struct ResNetTrainer {
         ep.stats = stats_fwd.as<float>();
         ep.tiles = c.tiles_fwd;
         const CBuf &w = wc[vslot][c.tw];
+        rec(c.tw, A_FWD, 0, vslot, s);
         if (c.impl == CI_IMPLICIT) {
             pk_conv<K, GM_FPROP, EpiConvOut2<K>>("conv_fprop", tile_n(c.cout), c, w, ep, s, false);
         } else {
@@ -647,6 +655,7 @@ struct ResNetTrainer {
             pk_plain<K, false, true, EpiConvOut2<K>>(c.impl == CI_STEM ? "stem_fprop" : "conv_fprop_1x1",
                                                      tile_n(c.cout), in, w.view(), c.P, c.cout, Kd, ep, s, false);
         }
+        rec(c.tw, A_FWD, 1, vslot, s);
         const int slots = sizing ? c.tiles_fwd : last_stat_slots;
         L("bn_finalize_fwd", 0, double(slots) * c.cout * 8, s, [&] {
             launch_pdl(bn_finalize_fwd_kernel, dim3((c.cout * 32 + 255) / 256), dim3(256), 0, s,
@@ -658,18 +667,46 @@ struct ResNetTrainer {
     const float *gamma(int ci, int vslot) const { return theta[vslot] + tens[convs[ci].tb].base; }
     const float *beta(int ci, int vslot) const { return theta[vslot] + tens[convs[ci].tb].base + convs[ci].cout; }
     int vs(int tensor, int p) const { return tens[tensor].fresh ? p : (p ^ 1); }
+    // trace mode: one access record of `tensor`'s parameters in theta slot `slot` (stream order)
+    void rec(int tensor, int akind, int phase, int slot, cudaStream_t s) {
+        if (!trace) return;
+        L("trace_record", 0, 0, s, [&] {
+            access_record_kernel<<<1, 1, 0, s>>>(TraceLog{tlog.as<uint32_t>(), tcur.as<uint32_t>(), kTraceCap}, ring,
+                                                 rank, tensor + 1, akind, phase, slot,
+                                                 (const int *)&ctrl_dev.as<Control>()->step);
+            CDP_CUDA(cudaGetLastError());
+        });
+    }
+    // trace mode, around an update of `tensor` at step t (slot p): reads theta_t from p, writes t + 1 to p ^ 1
+    template <class F>
+    void traced_update(int tensor, int p, bool updates, cudaStream_t s, F &&launch) {
+        if (updates) rec(tensor, A_UPD, 0, p, s);
+        launch();
+        if (trace && updates) {
+            L("trace_vtag", 0, 0, s, [&] {
+                vtag_update_kernel<<<1, 1, 0, s>>>(ring, tensor + 1, (const int *)&ctrl_dev.as<Control>()->step);
+                CDP_CUDA(cudaGetLastError());
+            });
+            rec(tensor, A_NEW, 1, p ^ 1, s);
+        }
+    }
     int esz() const { return kind == 0 ? 2 : 8; }   // compute-format bytes per element
     int ysz() const { return kind == 0 ? 2 : 4; }   // Y-format (conv outputs, gradients) bytes per element
 
     template <int K>
-    void bn_apply(int ci, int vslot, const BnResidual &res, const CTensor &out, cudaStream_t s) {
+    void bn_apply(int ci, int vslot, const BnResidual &res, const CTensor &out, cudaStream_t s, int res_ci = -1,
+                  int res_slot = 0) {
         ConvL &c = convs[ci];
+        rec(c.tb, A_FWD, 0, vslot, s);
+        if (res_ci >= 0) rec(convs[res_ci].tb, A_FWD, 0, res_slot, s);
         const double bytes = double(c.P) * c.cout * (ysz() + esz() + (res.act.hi ? esz() : res.y ? ysz() : 0));
         L("bn_apply", 0, bytes, s, [&] {
             launch_pdl(bn_apply_kernel<K>, dim3(blocks_for(c.P * c.cout / 8)), dim3(256), 0, s, (const void *)c.y.p,
                        c.P, c.cout, (const float *)c.mean.as<float>(), (const float *)c.rstd.as<float>(),
                        gamma(ci, vslot), beta(ci, vslot), res, 1, out);
         });
+        rec(c.tb, A_FWD, 1, vslot, s);
+        if (res_ci >= 0) rec(convs[res_ci].tb, A_FWD, 1, res_slot, s);
     }
 
     template <int K>
@@ -729,7 +766,8 @@ struct ResNetTrainer {
                 res.act = acts[b.a_in].view();
             }
             const int last = b.convs.back();
-            bn_apply<K>(last, vs(convs[last].tb, p), res, acts[b.a_out].view(), s);
+            bn_apply<K>(last, vs(convs[last].tb, p), res, acts[b.a_out].view(), s, b.ds,
+                        b.ds >= 0 ? vs(convs[b.ds].tb, p) : 0);
             zdone(convs[last].tb, 0, s);
             if (b.ds >= 0) zdone(convs[b.ds].tb, 0, s);
         }
@@ -743,8 +781,10 @@ struct ResNetTrainer {
         typename EpiFwd<K>::Params ep{};
         ep.last = 1;
         ep.z = z.as<float>();
+        rec(fc_t, A_FWD, 0, vs(fc_t, p), s);
         gemm<K, true, false, EpiFwd<K>>("fc_fwd", 32, wc[vs(fc_t, p)][fc_t].view(), pooled.view(), classes, B,
                                         fc_in + 1, ep, s, false);
+        rec(fc_t, A_FWD, 1, vs(fc_t, p), s);
         zdone(fc_t, 0, s);
     }
 
@@ -786,12 +826,14 @@ struct ResNetTrainer {
     void bn_bwd_apply(int ci, int p, const void *g, const CTensor &mask, cudaStream_t s) {
         ConvL &cc = convs[ci];
         const int vslot = vs(cc.tb, p);
+        rec(cc.tb, A_BWD, 0, vslot, s);
         L("bn_bwd_apply", 0, double(cc.P) * cc.cout * (2 * ysz() + 2 * esz()), s, [&] {
             launch_pdl(bn_bwd_apply_kernel<K>, dim3(blocks_for(cc.P * cc.cout / 8)), dim3(256), 0, s, g, mask,
                        (const void *)cc.y.p, cc.P, cc.cout, (const float *)cc.mean.as<float>(),
                        (const float *)cc.rstd.as<float>(), gamma(ci, vslot), (const float *)cc.dbeta.as<float>(),
                        (const float *)cc.dgamma.as<float>(), cc.dy.view());
         });
+        rec(cc.tb, A_BWD, 1, vslot, s);
     }
 
     // conv data gradient into g_in (fp32 [Pin][cin]).
@@ -802,6 +844,7 @@ struct ResNetTrainer {
         ConvL &c = convs[ci];
         zrecv<K>(c.tw, 1, s);
         const CBuf &w = wc[vslot][c.tw];
+        rec(c.tw, A_BWD, 0, vslot, s);
         typename EpiConvOut2<K>::Params ep{};
         ep.stats = nullptr;
         ep.add = add;
@@ -826,6 +869,7 @@ struct ResNetTrainer {
             }
             pk_dgrad_phases<K, EpiConvOut2<K>>("conv_dgrad_s2", tile_n(c.cin), c, w, ep, s);
         }
+        rec(c.tw, A_BWD, 1, vslot, s);
     }
 
     HopParams hop_params(int tensor, int p) {
@@ -907,22 +951,26 @@ struct ResNetTrainer {
         ConvL &c = convs[ci];
         HopParams hp = hop_params(c.tw, p);
         hop_wait(hp, s);
-        if (c.impl == CI_IMPLICIT) {
-            pk_conv<K, GM_WGRAD, EpiHop2<K>>("conv_wgrad_hop", tile_n(c.cout), c, wc[0][c.tw], hp, s, true);
-        } else {
-            const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
-            pk_plain<K, true, true, EpiHop2<K>>(c.impl == CI_STEM ? "stem_wgrad_hop" : "conv_wgrad_hop_1x1",
-                                                tile_n(c.cout), in, c.dy.view(), c.K, c.cout, c.P, hp, s, true);
-        }
+        traced_update(c.tw, p, hp.mode == 2 || hp.mode == 3, s, [&] {
+            if (c.impl == CI_IMPLICIT) {
+                pk_conv<K, GM_WGRAD, EpiHop2<K>>("conv_wgrad_hop", tile_n(c.cout), c, wc[0][c.tw], hp, s, true);
+            } else {
+                const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
+                pk_plain<K, true, true, EpiHop2<K>>(c.impl == CI_STEM ? "stem_wgrad_hop" : "conv_wgrad_hop_1x1",
+                                                    tile_n(c.cout), in, c.dy.view(), c.K, c.cout, c.P, hp, s, true);
+            }
+        });
     }
 
     void bn_hop(int ci, int p, cudaStream_t s) {
         ConvL &c = convs[ci];
         HopParams hp = hop_params(c.tb, p);
         hop_wait(hp, s);
-        L("bn_hop", 0, double(c.cout) * 2 * 24, s, [&] {
-            launch_pdl(vector_hop_kernel, dim3(1), dim3(128), 0, s, hp, (const float *)c.dgamma.as<float>(),
-                       (const float *)c.dbeta.as<float>(), c.cout);
+        traced_update(c.tb, p, hp.mode == 2 || hp.mode == 3, s, [&] {
+            L("bn_hop", 0, double(c.cout) * 2 * 24, s, [&] {
+                launch_pdl(vector_hop_kernel, dim3(1), dim3(128), 0, s, hp, (const float *)c.dgamma.as<float>(),
+                           (const float *)c.dbeta.as<float>(), c.cout);
+            });
         });
     }
 
@@ -960,7 +1008,8 @@ struct ResNetTrainer {
         const RingFlags *src_flags = reinterpret_cast<const RingFlags *>(peers[z.src]);
         L("zero_wait", 0, 0, s, [&] {
             zero_wait_kernel<<<1, 32, 0, s>>>(z, rank, src_flags, ring, tensor + 1,
-                                              (const int *)&ctrl_dev.as<Control>()->step, step_delta);
+                                              (const int *)&ctrl_dev.as<Control>()->step, step_delta,
+                                              (trace && copy) ? 1 : 0);
             CDP_CUDA(cudaGetLastError());
         });
         if (!copy) return;
@@ -1007,7 +1056,8 @@ struct ResNetTrainer {
             launch_pdl(pull_tensor_kernel<K>, dim3(blocks_for(ts.n, 1024)), dim3(256), 0, s,
                        (const float *)(upd_theta[vslot] + ts.base), theta[vslot] + ts.base, ts.n,
                        std::max(ts.cols, 1), w, upd_ring, ring, tensor + 1, ts.fresh,
-                       (const int *)&ctrl_dev.as<Control>()->step, cta_counters.as<unsigned>() + kMaxStages);
+                       (const int *)&ctrl_dev.as<Control>()->step, cta_counters.as<unsigned>() + kMaxStages,
+                       trace ? 1 : 0);
         });
     }
 
@@ -1059,16 +1109,20 @@ struct ResNetTrainer {
         typename EpiDgradLinear::Params dep{dpooled.as<float>(), fc_in};
         const int vfc = vs(fc_t, p);
         zrecv<K>(fc_t, 1, cs);
+        rec(fc_t, A_BWD, 0, vfc, cs);
         gemm<K, false, false, EpiDgradLinear>("fc_dgrad", 32, wc[vfc][fc_t].view(), dz.view(), fc_in, B, classes, dep,
                                               cs, false);
+        rec(fc_t, A_BWD, 1, vfc, cs);
         cudaEvent_t fc_dgrad_done = ev(cs);
         wait(hs, dz_ready);
         if (zero || (!tens[fc_t].fresh && last_updater())) wait(hs, fc_dgrad_done);
         {
             HopParams hp = hop_params(fc_t, p);
             hop_wait(hp, hs);
-            gemm<K, true, true, EpiWgrad<K>>("fc_wgrad_hop", 64, pooled.view(), dz.view(), fc_in + 1, classes, B, hp,
-                                             hs, true);
+            traced_update(fc_t, p, hp.mode == 2 || hp.mode == 3, hs, [&] {
+                gemm<K, true, true, EpiWgrad<K>>("fc_wgrad_hop", 64, pooled.view(), dz.view(), fc_in + 1, classes, B,
+                                                 hp, hs, true);
+            });
             zdone(fc_t, 1, hs);
         }
         void *G0 = gbuf[0].p, *G1 = gbuf[1].p, *G2 = gbuf[2].p, *G3 = gbuf[3].p;
@@ -1226,6 +1280,9 @@ struct ResNetTrainer {
             const int slot = v == 0 ? (t & 1) : ((t & 1) ^ 1);
             CDP_CUDA(cudaMemcpyAsync(theta[slot], host, size_t(P) * 4, cudaMemcpyHostToDevice, main));
             pack_slot(slot);
+            // version tags: the current slot holds theta_t, the other theta_{t-1} (ref engine.py:8-10)
+            std::vector<uint32_t> tag(kMaxStages, uint32_t(v == 0 ? t : t - 1));
+            CDP_CUDA(cudaMemcpy(ring->vtag[slot], tag.data(), kMaxStages * 4, cudaMemcpyHostToDevice));
         }
         CDP_CUDA(cudaStreamSynchronize(main));
     }
@@ -1335,6 +1392,12 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
         tr->world = world;
         tr->n_samples = std::max(n_samples, micro_batch);
         tr->allreduce = (options & 1) != 0;
+        tr->trace = (options & 2) != 0;
+        CDP_REQUIRE(!(tr->allreduce && tr->trace), "trace mode covers the CDP / DP ring step, not the all-reduce baseline");
+        if (tr->trace) {
+            tr->tlog = DevBuf(size_t(ResNetTrainer::kTraceCap) * kTraceWords * 4);
+            tr->tcur = DevBuf(4);
+        }
         CDP_REQUIRE(!(tr->allreduce && zero_table), "the DP all-reduce baseline and ZeRO-CDP are exclusive");
         if (zero_table && world > 1) {
             tr->zero = true;
@@ -1580,6 +1643,21 @@ extern "C" int cdp_resnet_buffer(cdp_resnet *tr, const char *name, int index, vo
         *ptr = d->p;
         *bytes = d->bytes;
         *ld = l;
+    });
+}
+
+extern "C" int cdp_resnet_trace(cdp_resnet *tr, uint32_t *records, int max_records, int *count) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_REQUIRE(m.trace, "trainer created without the trace option");
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        uint32_t n = 0;
+        CDP_CUDA(cudaMemcpy(&n, m.tcur.p, 4, cudaMemcpyDeviceToHost));
+        CDP_REQUIRE(n <= ResNetTrainer::kTraceCap, "trace buffer overflow: read the records more often");
+        *count = int(n);
+        const int k = std::min<int>(int(n), max_records);
+        if (k > 0) CDP_CUDA(cudaMemcpy(records, m.tlog.p, size_t(k) * kTraceWords * 4, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemset(m.tcur.p, 0, 4));
     });
 }
 

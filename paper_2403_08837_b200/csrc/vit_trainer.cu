@@ -100,6 +100,9 @@ struct VitTrainer {
     std::vector<cudaEvent_t> marks;
     DevBuf flush_buf;
     bool sizing = false, instr = false;
+    bool trace = false;  // version tags + per-access records (tests; rank_common.cuh)
+    DevBuf tlog, tcur;
+    static constexpr uint32_t kTraceCap = 1u << 16;
     struct OpRec {
         std::string name;
         double flops, bytes;
@@ -396,6 +399,34 @@ struct VitTrainer {
     int vs(int unit, int p) const { return units[unit].fresh ? p : (p ^ 1); }
     const float *th(int unit, int p) const { return theta[vs(unit, p)] + units[unit].base; }
     const CBuf &W(int unit, int p) const { return wc[vs(unit, p)][unit]; }
+    void rec(int unit, int akind, int phase, int slot, cudaStream_t s) {
+        if (!trace) return;
+        L_("trace_record", 0, 0, s, [&] {
+            access_record_kernel<<<1, 1, 0, s>>>(TraceLog{tlog.as<uint32_t>(), tcur.as<uint32_t>(), kTraceCap}, ring,
+                                                 rank, unit + 1, akind, phase, slot,
+                                                 (const int *)&ctrl_dev.as<Control>()->step);
+            CDP_CUDA(cudaGetLastError());
+        });
+    }
+    // forward (A_FWD) / backward (A_BWD) read of `units` around `f` (trace mode)
+    template <class F>
+    void reading(std::initializer_list<int> us, int akind, int p, cudaStream_t s, F &&f) {
+        for (int u : us) rec(u, akind, 0, vs(u, p), s);
+        f();
+        for (int u : us) rec(u, akind, 1, vs(u, p), s);
+    }
+    template <class F>
+    void traced_update(int unit, int p, bool updates, cudaStream_t s, F &&launch) {
+        if (updates) rec(unit, A_UPD, 0, p, s);
+        launch();
+        if (trace && updates) {
+            L_("trace_vtag", 0, 0, s, [&] {
+                vtag_update_kernel<<<1, 1, 0, s>>>(ring, unit + 1, (const int *)&ctrl_dev.as<Control>()->step);
+                CDP_CUDA(cudaGetLastError());
+            });
+            rec(unit, A_NEW, 1, p ^ 1, s);
+        }
+    }
 
     HopParams hop_params(int unit, int p) {
         const VUnit &u = units[unit];
@@ -448,7 +479,7 @@ struct VitTrainer {
             launch_pdl(pull_tensor_kernel<0>, dim3(blocks_for(u.n, 1024)), dim3(256), 0, s,
                        (const float *)(upd_theta[vslot] + u.base), theta[vslot] + u.base, u.n, std::max(u.cols, 1),
                        w, upd_ring, ring, unit + 1, u.fresh, (const int *)&ctrl_dev.as<Control>()->step,
-                       cta_counters.as<unsigned>() + kMaxStages);
+                       cta_counters.as<unsigned>() + kMaxStages, trace ? 1 : 0);
         });
     }
 
@@ -460,21 +491,29 @@ struct VitTrainer {
         if (dgrad_done && !u.fresh && last_updater()) wait(hs, dgrad_done);
         HopParams hp = hop_params(unit, p);
         hop_wait(hp, hs);
-        gemm<true, true, EpiHop2<0>>("lin_wgrad_hop", opnd(a_in.hi, true, u.rows, krows, a_in.ld),
-                                     opnd(dy.hi, true, u.cols, krows, dy.ld), u.rows, u.cols, krows, hp, hs, true);
+        traced_update(unit, p, hp.mode >= 2, hs, [&] {
+            gemm<true, true, EpiHop2<0>>("lin_wgrad_hop", opnd(a_in.hi, true, u.rows, krows, a_in.ld),
+                                         opnd(dy.hi, true, u.cols, krows, dy.ld), u.rows, u.cols, krows, hp, hs, true);
+        });
     }
     void ln_hop(int unit, int p, const float *dg, const float *db, cudaEvent_t ready) {
         wait(hs, ready);
         HopParams hp = hop_params(unit, p);
         hop_wait(hp, hs);
-        L_("ln_hop", 0, double(D) * 2 * 24, hs, [&] {
-            launch_pdl(vector_hop_kernel, dim3(1), dim3(128), 0, hs, hp, dg, db, D);
+        traced_update(unit, p, hp.mode >= 2, hs, [&] {
+            L_("ln_hop", 0, double(D) * 2 * 24, hs, [&] {
+                launch_pdl(vector_hop_kernel, dim3(1), dim3(128), 0, hs, hp, dg, db, D);
+            });
         });
     }
 
     // ---------------------------------------------------------------- layers
     void layernorm(const float *x, int rows, int stride, int unit, int p, const CTensor &out, float *mean,
                    float *rstd, cudaStream_t s) {
+        reading({unit}, A_FWD, p, s, [&] { layernorm_(x, rows, stride, unit, p, out, mean, rstd, s); });
+    }
+    void layernorm_(const float *x, int rows, int stride, int unit, int p, const CTensor &out, float *mean,
+                    float *rstd, cudaStream_t s) {
         auto go = [&](auto kern) {
             L_("ln_fwd", 0, double(rows) * D * 6, s, [&] {
                 launch_pdl(kern, dim3((rows * 32 + 255) / 256), dim3(256), 0, s, x, rows, stride, D, th(unit, p), eps,
@@ -494,6 +533,13 @@ struct VitTrainer {
     void layernorm_bwd(const float *g, const float *x, int rows, int stride, int unit, int p, const float *mean,
                        const float *rstd, const float *dh_in, float *dh_out, float *dgam, float *dbet,
                        cudaStream_t s, CTensor copy = CTensor{}) {
+        reading({unit}, A_BWD, p, s, [&] {
+            layernorm_bwd_(g, x, rows, stride, unit, p, mean, rstd, dh_in, dh_out, dgam, dbet, s, copy);
+        });
+    }
+    void layernorm_bwd_(const float *g, const float *x, int rows, int stride, int unit, int p, const float *mean,
+                        const float *rstd, const float *dh_in, float *dh_out, float *dgam, float *dbet,
+                        cudaStream_t s, CTensor copy) {
         const int nblk = (rows + kLnBwdRows - 1) / kLnBwdRows;
         const size_t smem = size_t(8) * D * 2 * 4;
         auto go = [&](auto kern) {
@@ -542,12 +588,16 @@ struct VitTrainer {
             ep.ld = D;
             ep.out_f32 = 1;
             const CBuf &w = W(u_patch, p);
-            gemm<false, true, EpiConvOut2<0>>("patch_embed", opnd(patches.hi.p, false, B * NP, K0 + 1, patches.ld),
-                                              opnd(w.hi.p, true, D, K0 + 1, w.ld), B * NP, D, K0 + 1, ep, s, false);
+            reading({u_patch}, A_FWD, p, s, [&] {
+                gemm<false, true, EpiConvOut2<0>>("patch_embed", opnd(patches.hi.p, false, B * NP, K0 + 1, patches.ld),
+                                                  opnd(w.hi.p, true, D, K0 + 1, w.ld), B * NP, D, K0 + 1, ep, s, false);
+            });
         }
-        L_("embed_assemble", 0, double(R) * D * 12, s, [&] {
-            launch_pdl(embed_assemble_kernel, dim3(blocks_for(int64_t(R) * D)), dim3(256), 0, s,
-                       (const float *)E.as<float>(), th(u_cls, p), th(u_pos, p), B, T, D, layers[0].h.as<float>());
+        reading({u_cls, u_pos}, A_FWD, p, s, [&] {
+            L_("embed_assemble", 0, double(R) * D * 12, s, [&] {
+                launch_pdl(embed_assemble_kernel, dim3(blocks_for(int64_t(R) * D)), dim3(256), 0, s,
+                           (const float *)E.as<float>(), th(u_cls, p), th(u_pos, p), B, T, D, layers[0].h.as<float>());
+            });
         });
         const float scale = 1.f / std::sqrt(float(HD));
         for (int l = 0; l < L; ++l) {
@@ -560,9 +610,11 @@ struct VitTrainer {
                 ep.out = y.qkvb.hi.p;
                 ep.ld = y.qkvb.ld;
                 const CBuf &w = W(y.qkv, p);
-                gemm<false, true, EpiConvOut2<0>>("qkv", opnd(y.u1.hi.p, false, R, D + 1, y.u1.ld),
-                                                  opnd(w.hi.p, true, 3 * D, D + 1, w.ld), R, 3 * D, D + 1, ep, s,
-                                                  false);
+                reading({y.qkv}, A_FWD, p, s, [&] {
+                    gemm<false, true, EpiConvOut2<0>>("qkv", opnd(y.u1.hi.p, false, R, D + 1, y.u1.ld),
+                                                      opnd(w.hi.p, true, 3 * D, D + 1, w.ld), R, 3 * D, D + 1, ep, s,
+                                                      false);
+                });
             }
             // attention: S = Q K^T (fp32) -> P = softmax(scale S) (bf16) -> O = P V
             const int64_t qld = y.qkvb.ld;
@@ -592,8 +644,10 @@ struct VitTrainer {
                 ep.out_f32 = 1;
                 ep.add = y.h.p;
                 const CBuf &w = W(y.proj, p);
-                gemm<false, true, EpiConvOut2<0>>("proj", opnd(y.attn.hi.p, false, R, D + 1, y.attn.ld),
-                                                  opnd(w.hi.p, true, D, D + 1, w.ld), R, D, D + 1, ep, s, false);
+                reading({y.proj}, A_FWD, p, s, [&] {
+                    gemm<false, true, EpiConvOut2<0>>("proj", opnd(y.attn.hi.p, false, R, D + 1, y.attn.ld),
+                                                      opnd(w.hi.p, true, D, D + 1, w.ld), R, D, D + 1, ep, s, false);
+                });
             }
             layernorm(y.hmid.as<float>(), R, 1, y.ln2, p, y.u2.view(), y.m2.as<float>(), y.r2.as<float>(), s);
             {
@@ -602,8 +656,10 @@ struct VitTrainer {
                 ep.ld = y.z1.ld;
                 ep.gelu_out = y.g1.view();
                 const CBuf &w = W(y.fc1, p);
-                gemm<false, true, EpiConvOut2<0>>("fc1_gelu", opnd(y.u2.hi.p, false, R, D + 1, y.u2.ld),
-                                                  opnd(w.hi.p, true, F, D + 1, w.ld), R, F, D + 1, ep, s, false);
+                reading({y.fc1}, A_FWD, p, s, [&] {
+                    gemm<false, true, EpiConvOut2<0>>("fc1_gelu", opnd(y.u2.hi.p, false, R, D + 1, y.u2.ld),
+                                                      opnd(w.hi.p, true, F, D + 1, w.ld), R, F, D + 1, ep, s, false);
+                });
             }
             {
                 typename EpiConvOut2<0>::Params ep{};
@@ -612,8 +668,10 @@ struct VitTrainer {
                 ep.out_f32 = 1;
                 ep.add = y.hmid.p;
                 const CBuf &w = W(y.fc2, p);
-                gemm<false, true, EpiConvOut2<0>>("fc2", opnd(y.g1.hi.p, false, R, F + 1, y.g1.ld),
-                                                  opnd(w.hi.p, true, D, F + 1, w.ld), R, D, F + 1, ep, s, false);
+                reading({y.fc2}, A_FWD, p, s, [&] {
+                    gemm<false, true, EpiConvOut2<0>>("fc2", opnd(y.g1.hi.p, false, R, F + 1, y.g1.ld),
+                                                      opnd(w.hi.p, true, D, F + 1, w.ld), R, D, F + 1, ep, s, false);
+                });
             }
         }
         // head on the class token
@@ -625,8 +683,10 @@ struct VitTrainer {
         ep.ld = classes;
         ep.out_f32 = 1;
         const CBuf &w = W(u_head, p);
-        gemm<false, true, EpiConvOut2<0>>("head", opnd(uf.hi.p, false, B, D + 1, uf.ld),
-                                          opnd(w.hi.p, true, classes, D + 1, w.ld), B, classes, D + 1, ep, s, false);
+        reading({u_head}, A_FWD, p, s, [&] {
+            gemm<false, true, EpiConvOut2<0>>("head", opnd(uf.hi.p, false, B, D + 1, uf.ld),
+                                              opnd(w.hi.p, true, classes, D + 1, w.ld), B, classes, D + 1, ep, s, false);
+        });
     }
 
     void cast(const float *in, int rows, int per, int in_per, int skip, const CTensor &out, cudaStream_t s) {
@@ -672,8 +732,10 @@ struct VitTrainer {
             ep.ld = D;
             ep.out_f32 = 1;
             const CBuf &w = W(u_head, p);
-            gemm<false, false, EpiConvOut2<0>>("head_dgrad", opnd(dz.hi.p, false, B, classes, dz.ld),
-                                               opnd(w.hi.p, false, D, classes, w.ld), B, D, classes, ep, cs, false);
+            reading({u_head}, A_BWD, p, cs, [&] {
+                gemm<false, false, EpiConvOut2<0>>("head_dgrad", opnd(dz.hi.p, false, B, classes, dz.ld),
+                                                   opnd(w.hi.p, false, D, classes, w.ld), B, D, classes, ep, cs, false);
+            });
         }
         cudaEvent_t head_dg = ev(cs);
         lin_hop(u_head, p, uf.view(), B, dz.view(), dz_ready, head_dg);
@@ -696,8 +758,10 @@ struct VitTrainer {
                 ep.ld = y.dz1.ld;
                 ep.gelu_z = y.z1.hi.p;
                 const CBuf &w = W(y.fc2, p);
-                gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(y.dhc.hi.p, false, R, D, y.dhc.ld),
-                                                   opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
+                reading({y.fc2}, A_BWD, p, cs, [&] {
+                    gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(y.dhc.hi.p, false, R, D, y.dhc.ld),
+                                                       opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
+                });
             }
             cudaEvent_t dz1_ready = ev(cs);
             lin_hop(y.fc2, p, y.g1.view(), R, y.dhc.view(), dhc_ready, dz1_ready);
@@ -707,8 +771,10 @@ struct VitTrainer {
                 ep.ld = D;
                 ep.out_f32 = 1;
                 const CBuf &w = W(y.fc1, p);
-                gemm<false, false, EpiConvOut2<0>>("fc1_dgrad", opnd(y.dz1.hi.p, false, R, F, y.dz1.ld),
-                                                   opnd(w.hi.p, false, D, F, w.ld), R, D, F, ep, cs, false);
+                reading({y.fc1}, A_BWD, p, cs, [&] {
+                    gemm<false, false, EpiConvOut2<0>>("fc1_dgrad", opnd(y.dz1.hi.p, false, R, F, y.dz1.ld),
+                                                       opnd(w.hi.p, false, D, F, w.ld), R, D, F, ep, cs, false);
+                });
             }
             cudaEvent_t fc1_dg = ev(cs);
             lin_hop(y.fc1, p, y.u2.view(), R, y.dz1.view(), dz1_ready, fc1_dg);
@@ -722,8 +788,10 @@ struct VitTrainer {
                 ep.out = dattn.hi.p;
                 ep.ld = dattn.ld;
                 const CBuf &w = W(y.proj, p);
-                gemm<false, false, EpiConvOut2<0>>("proj_dgrad", opnd(y.dhmc.hi.p, false, R, D, y.dhmc.ld),
-                                                   opnd(w.hi.p, false, D, D, w.ld), R, D, D, ep, cs, false);
+                reading({y.proj}, A_BWD, p, cs, [&] {
+                    gemm<false, false, EpiConvOut2<0>>("proj_dgrad", opnd(y.dhmc.hi.p, false, R, D, y.dhmc.ld),
+                                                       opnd(w.hi.p, false, D, D, w.ld), R, D, D, ep, cs, false);
+                });
             }
             cudaEvent_t proj_dg = ev(cs);
             lin_hop(y.proj, p, y.attn.view(), R, y.dhmc.view(), dhmc_ready, proj_dg);
@@ -760,8 +828,10 @@ struct VitTrainer {
                 ep.ld = D;
                 ep.out_f32 = 1;
                 const CBuf &w = W(y.qkv, p);
-                gemm<false, false, EpiConvOut2<0>>("qkv_dgrad", opnd(y.dqkv.hi.p, false, R, 3 * D, dld),
-                                                   opnd(w.hi.p, false, D, 3 * D, w.ld), R, D, 3 * D, ep, cs, false);
+                reading({y.qkv}, A_BWD, p, cs, [&] {
+                    gemm<false, false, EpiConvOut2<0>>("qkv_dgrad", opnd(y.dqkv.hi.p, false, R, 3 * D, dld),
+                                                       opnd(w.hi.p, false, D, 3 * D, w.ld), R, D, 3 * D, ep, cs, false);
+                });
             }
             cudaEvent_t qkv_dg = ev(cs);
             lin_hop(y.qkv, p, y.u1.view(), R, y.dqkv.view(), dqkv_ready, qkv_dg);
@@ -782,9 +852,11 @@ struct VitTrainer {
             HopParams hp = hop_params(u, p);
             hop_wait(hp, hs);
             const float *g = u == u_pos ? gpos.as<float>() : gcls.as<float>();
-            L_("vec_hop", 0, double(units[u].n) * 24, hs, [&] {
-                launch_pdl(flat_hop_kernel, dim3(blocks_for(units[u].n, 1024)), dim3(256), 0, hs, hp, g,
-                           units[u].n);
+            traced_update(u, p, hp.mode >= 2, hs, [&] {
+                L_("vec_hop", 0, double(units[u].n) * 24, hs, [&] {
+                    launch_pdl(flat_hop_kernel, dim3(blocks_for(units[u].n, 1024)), dim3(256), 0, hs, hp, g,
+                               units[u].n);
+                });
             });
         }
         lin_hop(u_patch, p, patches.view(), B * NP, dE.view(), emb_ready, nullptr);
@@ -848,6 +920,8 @@ struct VitTrainer {
             const int slot = v == 0 ? (t & 1) : ((t & 1) ^ 1);
             CDP_CUDA(cudaMemcpyAsync(theta[slot], host, size_t(Pn) * 4, cudaMemcpyHostToDevice, main));
             pack_slot(slot);
+            std::vector<uint32_t> tag(kMaxStages, uint32_t(v == 0 ? t : t - 1));  // version tags (ref engine.py:8-10)
+            CDP_CUDA(cudaMemcpy(ring->vtag[slot], tag.data(), kMaxStages * 4, cudaMemcpyHostToDevice));
         }
         CDP_CUDA(cudaStreamSynchronize(main));
     }
@@ -947,6 +1021,33 @@ extern "C" int cdp_vit_create_rank(int image, int patch, int dim, int depth, int
             tr->units[i].fresh = stage_fresh[st - 1] != 0;
         }
         *out = new cdp_vit{std::move(tr)};
+    });
+}
+
+extern "C" int cdp_vit_set_trace(cdp_vit *tr, int on) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_REQUIRE(!m.exec[0], "set the trace option before cdp_vit_connect (it changes the captured step)");
+        m.trace = on != 0;
+        if (m.trace && !m.tlog.p) {
+            m.tlog = DevBuf(size_t(VitTrainer::kTraceCap) * kTraceWords * 4);
+            m.tcur = DevBuf(4);
+        }
+    });
+}
+
+extern "C" int cdp_vit_trace(cdp_vit *tr, uint32_t *records, int max_records, int *count) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_REQUIRE(m.trace, "trace option not set");
+        CDP_CUDA(cudaStreamSynchronize(m.main));
+        uint32_t n = 0;
+        CDP_CUDA(cudaMemcpy(&n, m.tcur.p, 4, cudaMemcpyDeviceToHost));
+        CDP_REQUIRE(n <= VitTrainer::kTraceCap, "trace buffer overflow: read the records more often");
+        *count = int(n);
+        const int k = std::min<int>(int(n), max_records);
+        if (k > 0) CDP_CUDA(cudaMemcpy(records, m.tlog.p, size_t(k) * kTraceWords * 4, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemset(m.tcur.p, 0, 4));
     });
 }
 

@@ -162,7 +162,8 @@ class DeviceResNet:
 
     def __init__(self, widths=RESNET18["widths"], depths=RESNET18["depths"], micro_batch=128, world=1, rank=0,
                  rule=None, dtype="bf16", momentum=0.0, weight_decay=0.0, inputs=None, labels=None, classes=10,
-                 image_hw=32, stage_of_tensor=None, block="basic", stem="cifar", zero=False, dp_allreduce=False):
+                 image_hw=32, stage_of_tensor=None, block="basic", stem="cifar", zero=False, dp_allreduce=False,
+                 trace=False):
         self.lib = N.lib()
         self.widths, self.depths = tuple(widths), tuple(depths)
         self.block, self.stem, self.classes, self.image_hw = block, stem, int(classes), int(image_hw)
@@ -202,7 +203,8 @@ class DeviceResNet:
             len(w), _i32p(w), _i32p(d), BLOCKS[block], STEMS[stem], 3, image_hw, image_hw, classes, self.micro_batch, world, rank,
             _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), DTYPES[dtype], float(momentum), float(weight_decay),
             n, x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
-            _i32p(ztab) if ztab is not None else None, 1 if dp_allreduce else 0, ctypes.byref(h)))
+            _i32p(ztab) if ztab is not None else None, (1 if dp_allreduce else 0) | (2 if trace else 0),
+            ctypes.byref(h)))
         self.dp_allreduce = bool(dp_allreduce)
         self.h = h
         self._keep = (x, lab)
@@ -360,6 +362,10 @@ class DeviceResNet:
         if rows is not None:
             out = out[: rows * ld.value].reshape(rows, ld.value)
         return out
+
+    def access_trace(self, max_records=1 << 16):
+        """Executed-version records since the last call (trace=True trainers; _native.read_access_trace)."""
+        return N.read_access_trace(self.lib.cdp_resnet_trace, self.h, max_records)
 
     def activation_shapes(self):
         """[(role, H, W, C)] of the trainer's activation buffers in creation order: "relu" (a ReLU output:

@@ -85,7 +85,7 @@ class DeviceVit:
     """One rank (worker) of CDP training of a ViT on this process's GPU (bf16)."""
 
     def __init__(self, cfg=None, micro_batch=32, world=1, rank=0, rule=None, momentum=0.0, weight_decay=0.0,
-                 inputs=None, labels=None, stage_of_unit=None):
+                 inputs=None, labels=None, stage_of_unit=None, trace=False):
         self.cfg = dict(VIT_B16 if cfg is None else cfg)
         self.lib = N.lib()
         self.micro_batch, self.world, self.rank = int(micro_batch), int(world), int(rank)
@@ -113,6 +113,8 @@ class DeviceVit:
             ctypes.byref(h)))
         self.h = h
         self._keep = (x, lab)
+        if trace:
+            N.check(self.lib.cdp_vit_set_trace(self.h, 1))
         np_, nu = ctypes.c_int64(), ctypes.c_int()
         N.check(self.lib.cdp_vit_info(self.h, ctypes.byref(np_), ctypes.byref(nu)))
         assert nu.value == len(self.units), (nu.value, len(self.units))
@@ -192,6 +194,10 @@ class DeviceVit:
 
     def zero_drain(self):
         pass
+
+    def access_trace(self, max_records=1 << 16):
+        """Executed-version records since the last call (trace=True trainers; _native.read_access_trace)."""
+        return N.read_access_trace(self.lib.cdp_vit_trace, self.h, max_records)
 
     def ring_error(self) -> int:
         e = ctypes.c_int()
