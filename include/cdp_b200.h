@@ -230,6 +230,23 @@ typedef struct cdp_vit cdp_vit;
 int cdp_vit_create_rank(int image, int patch, int dim, int depth, int heads, int mlp, int classes, int micro_batch,
                         int world, int rank, const int32_t *unit_stage, const uint8_t *stage_fresh, float momentum,
                         float weight_decay, int n_samples, const float *x, const int32_t *labels, cdp_vit **out);
+/* Single-GPU cyclic CDP (BASELINE configs[3]; ref schedule.py:236-257, all workers on gpu 0):
+ * n_workers micro-batches = stages on this GPU, stepped through the reference's SINGLE_GPU_CDP
+ * (or SINGLE_GPU_DP) timeline.  ops[n_ops][3] = (kind 0 F / 1 B, worker 1..n, stage 1..n) in
+ * timeline order (paper_2403_08837_b200/executor.compile_segment_plan); a stage task runs its
+ * segments (0 = embedding, 1..depth = blocks, depth+1 = final LN + head) forward ascending /
+ * backward descending.  fresh[n_workers][n_workers] is the rule table (1 = reads theta_t,
+ * ref rules.py:45-51; all ones for DP).  rec_slot[n_workers][depth + 2] = activation-record slot of
+ * (worker, segment) in its pool; pools[3] = embed / block / final slots (the plan's interval
+ * colouring: the peak-activation claim of ref costs.py:111-115 is the pool sizes).  Gradient chain
+ * S = g_1 + ... + g_n in worker order; worker n fuses the update.  probe != 0 adds a device
+ * counter of live record bytes (stats out[4] = its high-water mark).  Dataset as create_rank;
+ * step perms hold n_workers * micro_batch indices, worker-major. */
+int cdp_vit_create_cyclic(int image, int patch, int dim, int depth, int heads, int mlp, int classes, int micro_batch,
+                          int n_workers, const int32_t *unit_stage, const uint8_t *fresh, int n_ops,
+                          const int32_t *ops, const int32_t *rec_slot, const int32_t *pools, float momentum,
+                          float weight_decay, int probe, int n_samples, const float *x, const int32_t *labels,
+                          cdp_vit **out);
 int cdp_vit_info(cdp_vit *tr, int64_t *n_params, int *n_units);
 /* Trace mode (set before cdp_vit_connect): records as cdp_resnet_trace, unit = 1-based hop unit. */
 int cdp_vit_set_trace(cdp_vit *tr, int on);
@@ -247,7 +264,9 @@ int cdp_vit_profile_step(cdp_vit *tr, const int32_t *perm, float lr, int serial,
 int cdp_vit_history(cdp_vit *tr, int max, double *losses, uint32_t *flags, int *count);
 int cdp_vit_sync(cdp_vit *tr);
 int cdp_vit_ring_error(cdp_vit *tr, int *err);
-/* out[0..3] = activation bytes kept for the backward, parameter-state bytes, kernels per step, tensor flops. */
+/* out[0] activation-record bytes allocated (pool slots x record bytes), [1] parameter-state bytes,
+ * [2] kernels per step, [3] tensor flops per step, [4] executed high-water mark of live record bytes
+ * (probe), [5..7] bytes of one embed / block / final record, [8..10] slots per pool. */
 int cdp_vit_stats(cdp_vit *tr, int64_t *out, int n_out);
 int cdp_vit_mark(cdp_vit *tr, int k);
 int cdp_vit_elapsed(cdp_vit *tr, int a, int b, float *ms);

@@ -40,14 +40,43 @@ struct VUnit {
     int stage, fresh;
 };
 
-struct VLayer {
+// Forward record of one transformer block for one micro-batch: its input and everything its
+// backward reads.  Lives from the forward that writes its input to the block's backward; slots
+// come from the step plan's interval colouring (executor.compile_segment_plan).
+struct VRec {
+    DevBuf h, hmid;                   // fp32 residual stream: block input, after attention
+    DevBuf m1, r1, m2, r2;            // LayerNorm row statistics
+    CBuf u1, u2, attn, g1, qkvb, z1;  // LN outputs, attention output, GELU output, qkv, FC1 pre-activation
+    DevBuf P;                         // softmax probabilities bf16 [B*H][T][ldp]
+    size_t bytes() const {
+        return h.bytes + hmid.bytes + m1.bytes + r1.bytes + m2.bytes + r2.bytes + u1.hi.bytes + u2.hi.bytes +
+               attn.hi.bytes + g1.hi.bytes + qkvb.hi.bytes + z1.hi.bytes + P.bytes;
+    }
+};
+struct ERec {  // embedding record: the patch matrix [x, 1] (the patch weight gradient's operand)
+    CBuf patches;
+    size_t bytes() const { return patches.hi.bytes; }
+};
+struct FRec {  // final record: last block output, final LN statistics / output, logits, dlogits
+    DevBuf hL, mf, rf, z;
+    CBuf uf, dz;
+    size_t bytes() const { return hL.bytes + mf.bytes + rf.bytes + z.bytes + uf.hi.bytes + dz.hi.bytes; }
+};
+// Backward operands of one block read by the hop stream (weight gradients), plus its LN parameter gradients.
+struct VGrad {
+    CBuf dz1, dhmc, dqkv;
+    DevBuf dg1, db1, dg2, db2;
+};
+struct VBlock {
     int ln1, qkv, proj, ln2, fc1, fc2;  // unit indices
-    DevBuf h, hmid;                     // fp32 residual stream: block input, after attention
-    DevBuf m1, r1, m2, r2;              // LayerNorm row statistics
-    CBuf u1, u2, attn, g1, qkvb, z1;    // LN outputs, attention output, GELU output, qkv, FC1 pre-activation
-    DevBuf P;                           // softmax probabilities bf16 [B*H][T][ldp]
-    CBuf dhc, dz1, dhmc, dqkv;          // backward GEMM operands read by the hop stream (per layer)
-    DevBuf dg1, db1, dg2, db2;          // LayerNorm parameter gradients
+};
+// Gradient carried through one worker's backward: dL/dh (fp32) and its bf16 operand copy.
+struct VCarry {
+    DevBuf dh;
+    CBuf dhc[2];
+};
+struct VOp {
+    int kind, worker, stage;  // 0 = F, 1 = B; 1-based worker / stage
 };
 
 struct BView {  // a 4-D TMA view {inner, rows, heads, samples} of a token-major bf16 buffer
@@ -56,6 +85,17 @@ struct BView {  // a 4-D TMA view {inner, rows, heads, samples} of a token-major
     int64_t ld, hs, bs;  // elements
 };
 
+__global__ void live_probe_kernel(int64_t *ctr, int64_t delta) {  // [0] live record bytes, [1] high-water mark
+    ctr[0] += delta;
+    if (ctr[0] > ctr[1]) ctr[1] = ctr[0];
+}
+
+__global__ void loss_mean_kernel(const double *loss_w, int W, double *loss_out) {  // mean_i loss_i, ascending i
+    double a = 0.0;
+    for (int i = 0; i < W; ++i) a += loss_w[i];
+    *loss_out = a / W;
+}
+
 }  // namespace
 
 struct VitTrainer {
@@ -63,12 +103,20 @@ struct VitTrainer {
     int B = 0, img = 224, P = 16, G = 14, NP = 196, T = 197, D = 768, H = 12, HD = 64, F = 3072, L = 12;
     int classes = 1000, loss_kind = 1;
     float momentum = 0.f, wd = 0.f, eps = 1e-6f;
-    int rank = 0, world = 1;
+    int rank = 0, world = 1;  // multi-GPU ring: this process is worker rank + 1 of `world`
+    int W = 1;                // workers (micro-batches) run by this process: > 1 = single-GPU cyclic CDP
     std::vector<VUnit> units;
-    std::vector<VLayer> layers;
+    std::vector<VBlock> blocks;
     int u_patch = 0, u_cls = 0, u_pos = 0, u_ln = 0, u_head = 0;
     int64_t Pn = 0, Pp = 0;
     int R = 0, lds = 0, ldp = 0;
+    // step plan (W > 1): ops in timeline order, record slot of (worker, segment), pool sizes
+    std::vector<VOp> plan;
+    std::vector<std::vector<uint8_t>> freshw;  // [worker][unit]
+    std::vector<std::vector<int>> slot;        // [worker][segment 0..L+1]
+    int pool[3] = {1, 1, 1};                   // embed, block, final record slots
+    std::vector<int> seg_stage;                // [segment] (W > 1)
+    bool probe = false;
 
     // ---------------------------------------------------------------- state
     DevBuf region, cta_counters;
@@ -78,9 +126,13 @@ struct VitTrainer {
     RingFlags *prev_ring = nullptr, *upd_ring = nullptr;
     float *prev_partial = nullptr, *upd_theta[2] = {nullptr, nullptr};
     std::vector<CBuf> wc[2];
-    CBuf patches, uf, dz, dE;
-    DevBuf E, hL, mf, rf, z, loss_dev, loss_rows, S, dP, du, duf, dh, dhm, gpos, gcls, lnpart, dgf, dbf;
-    CBuf dattn, dS;
+    std::vector<VRec> brec;
+    std::vector<ERec> erec;
+    std::vector<FRec> frec;
+    std::vector<VGrad> grads;   // per block (W == 1: the hop stream lags the compute stream) or one (W > 1)
+    std::vector<VCarry> carry;  // per worker
+    DevBuf E, loss_w, loss_dev, loss_rows, S, dP, du, duf, dhm, gpos, gcls, lnpart, dgf, dbf, live;
+    CBuf dattn, dS, dE;
     DevBuf ws_c, ws_h, cnt_c, cnt_h;
     size_t ws_c_floats = 0, ws_h_floats = 0;
     DevBuf data_x, data_lab, ctrl_dev, perm_dev, flags_dev, hist_loss, hist_flags;
@@ -110,6 +162,7 @@ struct VitTrainer {
     };
     std::vector<OpRec> oprecs;
     int sms_ = 0;
+    int cw = 0;  // worker (0-based) whose segment is being recorded
 
     ~VitTrainer() {
         for (auto &e : exec)
@@ -160,8 +213,14 @@ struct VitTrainer {
         units.push_back(VUnit{kind, base, n, rows, cols, 1, 1});
         return int(units.size()) - 1;
     }
+    // segment of a unit: 0 = embedding (patch, cls, pos), 1..L = blocks, L + 1 = final LN + head
+    int seg_of_unit(int u) const {
+        if (u <= u_pos) return 0;
+        if (u >= u_ln) return L + 1;
+        return 1 + (u - u_pos - 1) / 6;
+    }
 
-    void build() {
+    void make_units() {
         G = img / P;
         NP = G * G;
         T = NP + 1;
@@ -175,55 +234,76 @@ struct VitTrainer {
         u_patch = add_unit(V_LIN, int64_t(K0 + 1) * D, K0 + 1, D);
         u_cls = add_unit(V_VEC, D, 0, 0);
         u_pos = add_unit(V_VEC, int64_t(T) * D, 0, 0);
-        layers.resize(L);
-        for (auto &ly : layers) {
-            ly.ln1 = add_unit(V_LN, 2 * D, 0, 0);
-            ly.qkv = add_unit(V_LIN, int64_t(D + 1) * 3 * D, D + 1, 3 * D);
-            ly.proj = add_unit(V_LIN, int64_t(D + 1) * D, D + 1, D);
-            ly.ln2 = add_unit(V_LN, 2 * D, 0, 0);
-            ly.fc1 = add_unit(V_LIN, int64_t(D + 1) * F, D + 1, F);
-            ly.fc2 = add_unit(V_LIN, int64_t(F + 1) * D, F + 1, D);
+        blocks.resize(L);
+        for (auto &bl : blocks) {
+            bl.ln1 = add_unit(V_LN, 2 * D, 0, 0);
+            bl.qkv = add_unit(V_LIN, int64_t(D + 1) * 3 * D, D + 1, 3 * D);
+            bl.proj = add_unit(V_LIN, int64_t(D + 1) * D, D + 1, D);
+            bl.ln2 = add_unit(V_LN, 2 * D, 0, 0);
+            bl.fc1 = add_unit(V_LIN, int64_t(D + 1) * F, D + 1, F);
+            bl.fc2 = add_unit(V_LIN, int64_t(F + 1) * D, F + 1, D);
         }
         u_ln = add_unit(V_LN, 2 * D, 0, 0);
         u_head = add_unit(V_LIN, int64_t(D + 1) * classes, D + 1, classes);
         Pn = units.back().base + units.back().n;
         CDP_REQUIRE(int(units.size()) <= kMaxStages, "too many parameter tensors for the ring flags");
-        // ---- activations / gradients
+    }
+
+    void build() {
+        // ---- records (pool sizes from the plan), per-block backward operands, per-worker carries
         auto ones = [&](CBuf &b, int rows, int col) {  // constant 1 in column `col` (bias folding)
             std::vector<__nv_bfloat16> one(size_t(rows), __float2bfloat16(1.f));
             CDP_CUDA(cudaMemcpy2D(static_cast<__nv_bfloat16 *>(b.hi.p) + col, size_t(b.ld) * 2, one.data(), 2, 2,
                                   size_t(rows), cudaMemcpyHostToDevice));
         };
-        patches = make_cbuf(0, B * NP, K0 + 1);
-        E = DevBuf(size_t(B) * NP * D * 4);
-        for (auto &ly : layers) {
-            ly.h = DevBuf(size_t(R) * D * 4);
-            ly.hmid = DevBuf(size_t(R) * D * 4);
-            ly.m1 = DevBuf(size_t(R) * 4);
-            ly.r1 = DevBuf(size_t(R) * 4);
-            ly.m2 = DevBuf(size_t(R) * 4);
-            ly.r2 = DevBuf(size_t(R) * 4);
-            ly.u1 = make_cbuf(0, R, D + 1);
-            ly.u2 = make_cbuf(0, R, D + 1);
-            ly.attn = make_cbuf(0, R, D + 1);
-            ones(ly.attn, R, D);
-            ly.g1 = make_cbuf(0, R, F + 1);
-            ones(ly.g1, R, F);
-            ly.qkvb = make_cbuf(0, R, 3 * D);
-            ly.z1 = make_cbuf(0, R, F);
-            ly.P = DevBuf(size_t(B) * H * T * ldp * 2);
-            ly.dhc = make_cbuf(0, R, D);
-            ly.dz1 = make_cbuf(0, R, F);
-            ly.dhmc = make_cbuf(0, R, D);
-            ly.dqkv = make_cbuf(0, R, 3 * D);
-            for (DevBuf *g : {&ly.dg1, &ly.db1, &ly.dg2, &ly.db2}) *g = DevBuf(size_t(D) * 4);
+        const int K0 = P * P * 3;
+        erec.resize(pool[0]);
+        for (auto &e : erec) e.patches = make_cbuf(0, B * NP, K0 + 1);
+        brec.resize(pool[1]);
+        for (auto &y : brec) {
+            y.h = DevBuf(size_t(R) * D * 4);
+            y.hmid = DevBuf(size_t(R) * D * 4);
+            y.m1 = DevBuf(size_t(R) * 4);
+            y.r1 = DevBuf(size_t(R) * 4);
+            y.m2 = DevBuf(size_t(R) * 4);
+            y.r2 = DevBuf(size_t(R) * 4);
+            y.u1 = make_cbuf(0, R, D + 1);
+            y.u2 = make_cbuf(0, R, D + 1);
+            y.attn = make_cbuf(0, R, D + 1);
+            ones(y.attn, R, D);
+            y.g1 = make_cbuf(0, R, F + 1);
+            ones(y.g1, R, F);
+            y.qkvb = make_cbuf(0, R, 3 * D);
+            y.z1 = make_cbuf(0, R, F);
+            y.P = DevBuf(size_t(B) * H * T * ldp * 2);
         }
-        hL = DevBuf(size_t(R) * D * 4);
-        mf = DevBuf(size_t(B) * 4);
-        rf = DevBuf(size_t(B) * 4);
-        uf = make_cbuf(0, B, D + 1);
-        z = DevBuf(size_t(B) * classes * 4);
-        dz = make_cbuf(0, B, classes);
+        frec.resize(pool[2]);
+        for (auto &f : frec) {
+            f.hL = DevBuf(size_t(R) * D * 4);
+            f.mf = DevBuf(size_t(B) * 4);
+            f.rf = DevBuf(size_t(B) * 4);
+            f.uf = make_cbuf(0, B, D + 1);
+            f.z = DevBuf(size_t(B) * classes * 4);
+            f.dz = make_cbuf(0, B, classes);
+        }
+        grads.resize(W > 1 ? 1 : L);
+        for (auto &g : grads) {
+            g.dz1 = make_cbuf(0, R, F);
+            g.dhmc = make_cbuf(0, R, D);
+            g.dqkv = make_cbuf(0, R, 3 * D);
+            for (DevBuf *v : {&g.dg1, &g.db1, &g.dg2, &g.db2}) *v = DevBuf(size_t(D) * 4);
+        }
+        // W == 1: one dhc per block output (the hop stream reads it after the compute stream moved on);
+        // W > 1: two per worker (block parity), the hop stream is joined at every segment
+        carry.resize(W);
+        for (auto &c : carry) c.dh = DevBuf(size_t(R) * D * 4);
+        dhc_layer.resize(W == 1 ? L : 0);
+        for (auto &d : dhc_layer) d = make_cbuf(0, R, D);
+        if (W > 1)
+            for (auto &c : carry)
+                for (auto &d : c.dhc) d = make_cbuf(0, R, D);
+        E = DevBuf(size_t(B) * NP * D * 4);
+        loss_w = DevBuf(size_t(W) * 8);
         loss_dev = DevBuf(8);
         loss_rows = DevBuf(size_t(B) * 8);
         S = DevBuf(size_t(B) * H * T * lds * 4);
@@ -231,7 +311,6 @@ struct VitTrainer {
         dS = make_cbuf(0, B * H * T, T);  // ld = ldp
         du = DevBuf(size_t(R) * D * 4);
         duf = DevBuf(size_t(B) * D * 4);
-        dh = DevBuf(size_t(R) * D * 4);
         dhm = DevBuf(size_t(R) * D * 4);
         dattn = make_cbuf(0, R, D);
         gpos = DevBuf(size_t(T) * D * 4);
@@ -240,6 +319,7 @@ struct VitTrainer {
         lnpart = DevBuf(size_t(D) * ((R + kLnBwdRows - 1) / kLnBwdRows) * 16);
         dgf = DevBuf(size_t(D) * 4);
         dbf = DevBuf(size_t(D) * 4);
+        live = DevBuf(16);
         // ---- shared region: RingFlags | theta0 | theta1 | partial | momentum
         region_off = (sizeof(RingFlags) + 255) / 256 * 256;
         Pp = (Pn + 63) / 64 * 64;
@@ -256,11 +336,11 @@ struct VitTrainer {
         CDP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         CDP_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
         ctrl_dev = DevBuf(sizeof(Control));
-        perm_dev = DevBuf(size_t(B) * 4);
+        perm_dev = DevBuf(size_t(W) * B * 4);
         flags_dev = DevBuf(sizeof(Flags));
         hist_loss = DevBuf(size_t(hist_cap) * 8);
         hist_flags = DevBuf(size_t(hist_cap) * sizeof(Flags));
-        stage_bytes = (sizeof(Control) + size_t(B) * 4 + 255) / 256 * 256;
+        stage_bytes = (sizeof(Control) + size_t(W) * B * 4 + 255) / 256 * 256;
         CDP_CUDA(cudaMallocHost(&stage_host, stage_bytes * RING_N));
         for (auto &e : stage_ev) CDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         cnt_c = DevBuf(1 << 18);
@@ -272,6 +352,13 @@ struct VitTrainer {
         events.clear();
         ws_c = DevBuf(std::max<size_t>(ws_c_floats, 1) * 4);
         ws_h = DevBuf(std::max<size_t>(ws_h_floats, 1) * 4);
+    }
+    std::vector<CBuf> dhc_layer;
+    // bf16 copy of dL/d(output of block l) for the current worker
+    const CBuf &dhc(int l) const { return W == 1 ? dhc_layer[l] : carry[cw].dhc[l & 1]; }
+    VGrad &grad_of(int l) { return grads[W > 1 ? 0 : l]; }
+    int64_t record_bytes(int pool_kind) const {
+        return int64_t(pool_kind == 0 ? erec[0].bytes() : pool_kind == 1 ? brec[0].bytes() : frec[0].bytes());
     }
 
     // ---------------------------------------------------------------- GEMMs
@@ -395,15 +482,19 @@ struct VitTrainer {
     void wait(cudaStream_t s, cudaEvent_t e) {
         if (!sizing) CDP_CUDA(cudaStreamWaitEvent(s, e, 0));
     }
-    bool last_updater() const { return rank == world - 1; }
-    int vs(int unit, int p) const { return units[unit].fresh ? p : (p ^ 1); }
+    // the worker that holds the complete gradient sum and runs the fused update
+    bool is_updater() const { return W > 1 ? cw == W - 1 : rank == world - 1; }
+    int wid() const { return W > 1 ? cw : rank; }  // worker index in trace records
+    bool fresh_of(int unit) const { return W > 1 ? freshw[cw][unit] != 0 : units[unit].fresh != 0; }
+    int vs(int unit, int p) const { return fresh_of(unit) ? p : (p ^ 1); }
     const float *th(int unit, int p) const { return theta[vs(unit, p)] + units[unit].base; }
-    const CBuf &W(int unit, int p) const { return wc[vs(unit, p)][unit]; }
-    void rec(int unit, int akind, int phase, int slot, cudaStream_t s) {
+    const CBuf &Wt(int unit, int p) const { return wc[vs(unit, p)][unit]; }
+    const int *perm_w() const { return perm_dev.as<int>() + size_t(cw) * B; }
+    void rec(int unit, int akind, int phase, int slot_, cudaStream_t s) {
         if (!trace) return;
         L_("trace_record", 0, 0, s, [&] {
             access_record_kernel<<<1, 1, 0, s>>>(TraceLog{tlog.as<uint32_t>(), tcur.as<uint32_t>(), kTraceCap}, ring,
-                                                 rank, unit + 1, akind, phase, slot,
+                                                 wid(), unit + 1, akind, phase, slot_,
                                                  (const int *)&ctrl_dev.as<Control>()->step);
             CDP_CUDA(cudaGetLastError());
         });
@@ -427,16 +518,28 @@ struct VitTrainer {
             rec(unit, A_NEW, 1, p ^ 1, s);
         }
     }
+    // live-record accounting (W > 1): the executed high-water mark of activation-record bytes
+    void live_delta(int pool_kind, int sign) {
+        if (!probe) return;
+        const int64_t d = sign * record_bytes(pool_kind);
+        L_("live_probe", 0, 0, cs, [&] {
+            live_probe_kernel<<<1, 1, 0, cs>>>(live.as<int64_t>(), d);
+            CDP_CUDA(cudaGetLastError());
+        });
+    }
 
     HopParams hop_params(int unit, int p) {
         const VUnit &u = units[unit];
         HopParams hp{};
-        hp.mode = world == 1 ? 3 : (rank == 0 ? 0 : rank == world - 1 ? 2 : 1);
+        if (W > 1)  // one GPU: the chain w1 -> ... -> wW runs in plan order on the hop stream
+            hp.mode = cw == 0 ? 0 : cw == W - 1 ? 2 : 1;
+        else
+            hp.mode = world == 1 ? 3 : (rank == 0 ? 0 : rank == world - 1 ? 2 : 1);
         hp.stage = unit + 1;
         hp.base = u.base;
         hp.din = u.rows;
         hp.dout = u.cols;
-        hp.s_in = rank > 0 ? prev_partial : partial;
+        hp.s_in = (W == 1 && rank > 0) ? prev_partial : partial;
         hp.s_out = partial;
         hp.theta_cur = theta[p];
         hp.theta_new = theta[p ^ 1];
@@ -444,12 +547,12 @@ struct VitTrainer {
         hp.lr = &ctrl_dev.as<Control>()->lr;
         hp.momentum = momentum;
         hp.wd = wd;
-        hp.n_mb = float(world);
+        hp.n_mb = float(W > 1 ? W : world);
         hp.wc_new = u.kind == V_LIN ? wc[p ^ 1][unit].view() : CTensor{};
         Flags *fl = flags_dev.as<Flags>();
         hp.grad_flags = &fl->grad;
         hp.upd_flags = &fl->upd;
-        hp.sync.enabled = 1;
+        hp.sync.enabled = W == 1 ? 1 : 0;
         hp.sync.n_readers = world - 1;
         hp.sync.step = &ctrl_dev.as<Control>()->step;
         hp.sync.own = ring;
@@ -459,14 +562,14 @@ struct VitTrainer {
         return hp;
     }
     void hop_wait(const HopParams &hp, cudaStream_t s) {
-        if (world == 1 || hp.mode >= 3) return;
+        if (world == 1 || W > 1 || hp.mode >= 3) return;
         L_("hop_wait", 0, 0, s, [&] {
             hop_wait_kernel<<<1, 128, 0, s>>>(hp);
             CDP_CUDA(cudaGetLastError());
         });
     }
     void pull(int unit, int p, cudaStream_t s) {
-        if (rank == world - 1 || world == 1 || sizing) return;
+        if (W > 1 || rank == world - 1 || world == 1 || sizing) return;
         const VUnit &u = units[unit];
         const int vslot = vs(unit, p);
         CTensor w = u.kind == V_LIN ? wc[vslot][unit].view() : CTensor{};
@@ -488,7 +591,7 @@ struct VitTrainer {
                  cudaEvent_t dgrad_done) {
         const VUnit &u = units[unit];
         wait(hs, dy_ready);
-        if (dgrad_done && !u.fresh && last_updater()) wait(hs, dgrad_done);
+        if (dgrad_done && !fresh_of(unit) && is_updater()) wait(hs, dgrad_done);
         HopParams hp = hop_params(unit, p);
         hop_wait(hp, hs);
         traced_update(unit, p, hp.mode >= 2, hs, [&] {
@@ -571,281 +674,297 @@ struct VitTrainer {
     }
     bool ln_attr_ = false;
 
-    void forward(int p, cudaStream_t s) {
-        // patch embedding + tokens
+    // ---------------------------------------------------------------- segments (forward)
+    ERec &erec_w() { return erec[slot[cw][0]]; }
+    VRec &brec_w(int l) { return brec[slot[cw][1 + l]]; }
+    FRec &frec_w() { return frec[slot[cw][L + 1]]; }
+
+    // embedding: patches -> tokens (+ class token, position embedding) into block 0's record
+    void fwd_embed(int p, cudaStream_t s) {
+        live_delta(0, +1);
+        live_delta(L > 0 ? 1 : 2, +1);
         pull(u_patch, p, s);
         pull(u_cls, p, s);
         pull(u_pos, p, s);
         const int K0 = P * P * 3;
+        CBuf &patches = erec_w().patches;
         L_("patch_im2col", 0, double(B) * NP * patches.ld * 2, s, [&] {
             launch_pdl(patch_im2col_kernel<0>, dim3(blocks_for(int64_t(B) * NP * patches.ld)), dim3(256), 0, s,
-                       (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), img, P, G, B * NP,
-                       patches.view());
+                       (const float *)data_x.as<float>(), perm_w(), img, P, G, B * NP, patches.view());
         });
         {
             typename EpiConvOut2<0>::Params ep{};
             ep.out = E.p;
             ep.ld = D;
             ep.out_f32 = 1;
-            const CBuf &w = W(u_patch, p);
+            const CBuf &w = Wt(u_patch, p);
             reading({u_patch}, A_FWD, p, s, [&] {
                 gemm<false, true, EpiConvOut2<0>>("patch_embed", opnd(patches.hi.p, false, B * NP, K0 + 1, patches.ld),
                                                   opnd(w.hi.p, true, D, K0 + 1, w.ld), B * NP, D, K0 + 1, ep, s, false);
             });
         }
+        float *h0 = L > 0 ? brec_w(0).h.as<float>() : frec_w().hL.as<float>();
         reading({u_cls, u_pos}, A_FWD, p, s, [&] {
             L_("embed_assemble", 0, double(R) * D * 12, s, [&] {
                 launch_pdl(embed_assemble_kernel, dim3(blocks_for(int64_t(R) * D)), dim3(256), 0, s,
-                           (const float *)E.as<float>(), th(u_cls, p), th(u_pos, p), B, T, D, layers[0].h.as<float>());
+                           (const float *)E.as<float>(), th(u_cls, p), th(u_pos, p), B, T, D, h0);
             });
         });
-        const float scale = 1.f / std::sqrt(float(HD));
-        for (int l = 0; l < L; ++l) {
-            VLayer &y = layers[l];
-            float *hout = l + 1 < L ? layers[l + 1].h.as<float>() : hL.as<float>();
-            for (int u : {y.ln1, y.qkv, y.proj, y.ln2, y.fc1, y.fc2}) pull(u, p, s);
-            layernorm(y.h.as<float>(), R, 1, y.ln1, p, y.u1.view(), y.m1.as<float>(), y.r1.as<float>(), s);
-            {
-                typename EpiConvOut2<0>::Params ep{};
-                ep.out = y.qkvb.hi.p;
-                ep.ld = y.qkvb.ld;
-                const CBuf &w = W(y.qkv, p);
-                reading({y.qkv}, A_FWD, p, s, [&] {
-                    gemm<false, true, EpiConvOut2<0>>("qkv", opnd(y.u1.hi.p, false, R, D + 1, y.u1.ld),
-                                                      opnd(w.hi.p, true, 3 * D, D + 1, w.ld), R, 3 * D, D + 1, ep, s,
-                                                      false);
-                });
-            }
-            // attention: S = Q K^T (fp32) -> P = softmax(scale S) (bf16) -> O = P V
-            const int64_t qld = y.qkvb.ld;
-            const BView Q{y.qkvb.hi.p, HD, T, qld, HD, int64_t(T) * qld};
-            const BView Kv{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + D, HD, T, qld, HD, int64_t(T) * qld};
-            const BView V{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + 2 * D, HD, T, qld, HD, int64_t(T) * qld};
-            const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
-            bgemm<false, false>("attn_scores", Q, Kv, T, T, HD, S.p, lds, int64_t(H) * T * lds, int64_t(T) * lds, 1,
-                                s);
-            L_("softmax", 0, double(B) * H * T * T * 6, s, [&] {
-                const dim3 g((B * H * T * 32 + 255) / 256);
-                const float *Sp = S.as<float>();
-                __nv_bfloat16 *Pp = y.P.as<__nv_bfloat16>();
-                if (T <= 128)
-                    launch_pdl(softmax_fwd4_kernel<1>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
-                else if (T <= 256)
-                    launch_pdl(softmax_fwd4_kernel<2>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
-                else
-                    launch_pdl(softmax_fwd_kernel, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
+    }
+
+    void fwd_block(int l, int p, cudaStream_t s) {
+        const VBlock &b = blocks[l];
+        VRec &y = brec_w(l);
+        live_delta(l + 1 < L ? 1 : 2, +1);
+        float *hout = l + 1 < L ? brec_w(l + 1).h.as<float>() : frec_w().hL.as<float>();
+        for (int u : {b.ln1, b.qkv, b.proj, b.ln2, b.fc1, b.fc2}) pull(u, p, s);
+        layernorm(y.h.as<float>(), R, 1, b.ln1, p, y.u1.view(), y.m1.as<float>(), y.r1.as<float>(), s);
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = y.qkvb.hi.p;
+            ep.ld = y.qkvb.ld;
+            const CBuf &w = Wt(b.qkv, p);
+            reading({b.qkv}, A_FWD, p, s, [&] {
+                gemm<false, true, EpiConvOut2<0>>("qkv", opnd(y.u1.hi.p, false, R, D + 1, y.u1.ld),
+                                                  opnd(w.hi.p, true, 3 * D, D + 1, w.ld), R, 3 * D, D + 1, ep, s,
+                                                  false);
             });
-            bgemm<false, true>("attn_values", Pv, V, T, HD, T, y.attn.hi.p, y.attn.ld, int64_t(T) * y.attn.ld, HD, 0,
-                               s);
-            {
-                typename EpiConvOut2<0>::Params ep{};
-                ep.out = y.hmid.p;
-                ep.ld = D;
-                ep.out_f32 = 1;
-                ep.add = y.h.p;
-                const CBuf &w = W(y.proj, p);
-                reading({y.proj}, A_FWD, p, s, [&] {
-                    gemm<false, true, EpiConvOut2<0>>("proj", opnd(y.attn.hi.p, false, R, D + 1, y.attn.ld),
-                                                      opnd(w.hi.p, true, D, D + 1, w.ld), R, D, D + 1, ep, s, false);
-                });
-            }
-            layernorm(y.hmid.as<float>(), R, 1, y.ln2, p, y.u2.view(), y.m2.as<float>(), y.r2.as<float>(), s);
-            {
-                typename EpiConvOut2<0>::Params ep{};
-                ep.out = y.z1.hi.p;
-                ep.ld = y.z1.ld;
-                ep.gelu_out = y.g1.view();
-                const CBuf &w = W(y.fc1, p);
-                reading({y.fc1}, A_FWD, p, s, [&] {
-                    gemm<false, true, EpiConvOut2<0>>("fc1_gelu", opnd(y.u2.hi.p, false, R, D + 1, y.u2.ld),
-                                                      opnd(w.hi.p, true, F, D + 1, w.ld), R, F, D + 1, ep, s, false);
-                });
-            }
-            {
-                typename EpiConvOut2<0>::Params ep{};
-                ep.out = hout;
-                ep.ld = D;
-                ep.out_f32 = 1;
-                ep.add = y.hmid.p;
-                const CBuf &w = W(y.fc2, p);
-                reading({y.fc2}, A_FWD, p, s, [&] {
-                    gemm<false, true, EpiConvOut2<0>>("fc2", opnd(y.g1.hi.p, false, R, F + 1, y.g1.ld),
-                                                      opnd(w.hi.p, true, D, F + 1, w.ld), R, D, F + 1, ep, s, false);
-                });
-            }
         }
-        // head on the class token
+        // attention: S = Q K^T (fp32) -> P = softmax(scale S) (bf16) -> O = P V
+        const float scale = 1.f / std::sqrt(float(HD));
+        const int64_t qld = y.qkvb.ld;
+        const BView Q{y.qkvb.hi.p, HD, T, qld, HD, int64_t(T) * qld};
+        const BView Kv{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + D, HD, T, qld, HD, int64_t(T) * qld};
+        const BView V{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + 2 * D, HD, T, qld, HD, int64_t(T) * qld};
+        const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+        bgemm<false, false>("attn_scores", Q, Kv, T, T, HD, S.p, lds, int64_t(H) * T * lds, int64_t(T) * lds, 1, s);
+        L_("softmax", 0, double(B) * H * T * T * 6, s, [&] {
+            const dim3 g((B * H * T * 32 + 255) / 256);
+            const float *Sp = S.as<float>();
+            __nv_bfloat16 *Pp = y.P.as<__nv_bfloat16>();
+            if (T <= 128)
+                launch_pdl(softmax_fwd4_kernel<1>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
+            else if (T <= 256)
+                launch_pdl(softmax_fwd4_kernel<2>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
+            else
+                launch_pdl(softmax_fwd_kernel, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
+        });
+        bgemm<false, true>("attn_values", Pv, V, T, HD, T, y.attn.hi.p, y.attn.ld, int64_t(T) * y.attn.ld, HD, 0, s);
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = y.hmid.p;
+            ep.ld = D;
+            ep.out_f32 = 1;
+            ep.add = y.h.p;
+            const CBuf &w = Wt(b.proj, p);
+            reading({b.proj}, A_FWD, p, s, [&] {
+                gemm<false, true, EpiConvOut2<0>>("proj", opnd(y.attn.hi.p, false, R, D + 1, y.attn.ld),
+                                                  opnd(w.hi.p, true, D, D + 1, w.ld), R, D, D + 1, ep, s, false);
+            });
+        }
+        layernorm(y.hmid.as<float>(), R, 1, b.ln2, p, y.u2.view(), y.m2.as<float>(), y.r2.as<float>(), s);
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = y.z1.hi.p;
+            ep.ld = y.z1.ld;
+            ep.gelu_out = y.g1.view();
+            const CBuf &w = Wt(b.fc1, p);
+            reading({b.fc1}, A_FWD, p, s, [&] {
+                gemm<false, true, EpiConvOut2<0>>("fc1_gelu", opnd(y.u2.hi.p, false, R, D + 1, y.u2.ld),
+                                                  opnd(w.hi.p, true, F, D + 1, w.ld), R, F, D + 1, ep, s, false);
+            });
+        }
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = hout;
+            ep.ld = D;
+            ep.out_f32 = 1;
+            ep.add = y.hmid.p;
+            const CBuf &w = Wt(b.fc2, p);
+            reading({b.fc2}, A_FWD, p, s, [&] {
+                gemm<false, true, EpiConvOut2<0>>("fc2", opnd(y.g1.hi.p, false, R, F + 1, y.g1.ld),
+                                                  opnd(w.hi.p, true, D, F + 1, w.ld), R, D, F + 1, ep, s, false);
+            });
+        }
+    }
+
+    // final LayerNorm + head on the class token, loss -> dz and this worker's loss slot
+    void fwd_final(int p, cudaStream_t s) {
+        FRec &f = frec_w();
         pull(u_ln, p, s);
         pull(u_head, p, s);
-        layernorm(hL.as<float>(), B, T, u_ln, p, uf.view(), mf.as<float>(), rf.as<float>(), s);
-        typename EpiConvOut2<0>::Params ep{};
-        ep.out = z.p;
-        ep.ld = classes;
-        ep.out_f32 = 1;
-        const CBuf &w = W(u_head, p);
-        reading({u_head}, A_FWD, p, s, [&] {
-            gemm<false, true, EpiConvOut2<0>>("head", opnd(uf.hi.p, false, B, D + 1, uf.ld),
-                                              opnd(w.hi.p, true, classes, D + 1, w.ld), B, classes, D + 1, ep, s, false);
-        });
-    }
-
-    void cast(const float *in, int rows, int per, int in_per, int skip, const CTensor &out, cudaStream_t s) {
-        L_("cast", 0, double(rows) * D * 6, s, [&] {
-            launch_pdl(cast_rows_kernel<0>, dim3(blocks_for(int64_t(rows) * D)), dim3(256), 0, s, in, rows, D, per,
-                       in_per, skip, out);
-        });
-    }
-
-    void record_step(int p) {
-        kernels_per_step = 0;
-        flops_per_step = 0.0;
-        cudaEvent_t fork = ev(main);
-        wait(cs, fork);
-        wait(hs, fork);
-        forward(p, cs);
-        // loss
+        layernorm(f.hL.as<float>(), B, T, u_ln, p, f.uf.view(), f.mf.as<float>(), f.rf.as<float>(), s);
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = f.z.p;
+            ep.ld = classes;
+            ep.out_f32 = 1;
+            const CBuf &w = Wt(u_head, p);
+            reading({u_head}, A_FWD, p, s, [&] {
+                gemm<false, true, EpiConvOut2<0>>("head", opnd(f.uf.hi.p, false, B, D + 1, f.uf.ld),
+                                                  opnd(w.hi.p, true, classes, D + 1, w.ld), B, classes, D + 1, ep, s,
+                                                  false);
+            });
+        }
         Flags *fl = flags_dev.as<Flags>();
+        double *lw = loss_w.as<double>() + cw;
         const int nt = std::max(32, round_up(B, 32));
         const size_t lsm = sizeof(double) * nt + sizeof(float) * B * classes;
         if (classes <= 64 && lsm <= 48 * 1024) {
-            L_("loss", 0, 0, cs, [&] {
-                launch_pdl(loss_kernel<0>, dim3(1), dim3(nt), lsm, cs, (const float *)z.as<float>(), B, classes,
-                           loss_kind, (const int *)perm_dev.as<int>(), (const int *)data_lab.as<int>(),
-                           (const float *)nullptr, dz.view(), loss_dev.as<double>(), &fl->loss);
+            L_("loss", 0, 0, s, [&] {
+                launch_pdl(loss_kernel<0>, dim3(1), dim3(nt), lsm, s, (const float *)f.z.as<float>(), B, classes,
+                           loss_kind, perm_w(), (const int *)data_lab.as<int>(), (const float *)nullptr, f.dz.view(),
+                           lw, &fl->loss);
             });
         } else {
-            L_("loss", 0, 0, cs, [&] {
-                launch_pdl(xent_rows_kernel<0>, dim3(B), dim3(256), 0, cs, (const float *)z.as<float>(), B, classes,
-                           (const int *)perm_dev.as<int>(), (const int *)data_lab.as<int>(), dz.view(),
-                           loss_rows.as<double>());
+            L_("loss", 0, 0, s, [&] {
+                launch_pdl(xent_rows_kernel<0>, dim3(B), dim3(256), 0, s, (const float *)f.z.as<float>(), B, classes,
+                           perm_w(), (const int *)data_lab.as<int>(), f.dz.view(), loss_rows.as<double>());
             });
-            L_("loss_sum", 0, 0, cs, [&] {
-                launch_pdl(loss_sum_kernel, dim3(1), dim3(1), 0, cs, (const double *)loss_rows.as<double>(), B,
-                           loss_dev.as<double>(), &fl->loss);
+            L_("loss_sum", 0, 0, s, [&] {
+                launch_pdl(loss_sum_kernel, dim3(1), dim3(1), 0, s, (const double *)loss_rows.as<double>(), B, lw,
+                           &fl->loss);
             });
         }
+    }
+
+    // ---------------------------------------------------------------- segments (backward)
+    void bwd_final(int p) {
+        FRec &f = frec_w();
+        VCarry &c = carry[cw];
         cudaEvent_t dz_ready = ev(cs);
-        // head: data gradient (fp32) and weight gradient + hop
         {
             typename EpiConvOut2<0>::Params ep{};
             ep.out = duf.p;
             ep.ld = D;
             ep.out_f32 = 1;
-            const CBuf &w = W(u_head, p);
+            const CBuf &w = Wt(u_head, p);
             reading({u_head}, A_BWD, p, cs, [&] {
-                gemm<false, false, EpiConvOut2<0>>("head_dgrad", opnd(dz.hi.p, false, B, classes, dz.ld),
+                gemm<false, false, EpiConvOut2<0>>("head_dgrad", opnd(f.dz.hi.p, false, B, classes, f.dz.ld),
                                                    opnd(w.hi.p, false, D, classes, w.ld), B, D, classes, ep, cs, false);
             });
         }
         cudaEvent_t head_dg = ev(cs);
-        lin_hop(u_head, p, uf.view(), B, dz.view(), dz_ready, head_dg);
+        lin_hop(u_head, p, f.uf.view(), B, f.dz.view(), dz_ready, head_dg);
         // final LayerNorm (class-token rows only): dh = 0 elsewhere (and its bf16 copy, the last block's operand)
+        const CBuf *out_c = L > 0 ? &dhc(L - 1) : nullptr;
         if (!sizing) {
-            CDP_CUDA(cudaMemsetAsync(dh.p, 0, dh.bytes, cs));
-            CDP_CUDA(cudaMemsetAsync(layers[L - 1].dhc.hi.p, 0, layers[L - 1].dhc.hi.bytes, cs));
+            CDP_CUDA(cudaMemsetAsync(c.dh.p, 0, c.dh.bytes, cs));
+            if (out_c) CDP_CUDA(cudaMemsetAsync(out_c->hi.p, 0, out_c->hi.bytes, cs));
         }
-        layernorm_bwd(duf.as<float>(), hL.as<float>(), B, T, u_ln, p, mf.as<float>(), rf.as<float>(), nullptr,
-                      dh.as<float>(), dgf.as<float>(), dbf.as<float>(), cs, layers[L - 1].dhc.view());
+        layernorm_bwd(duf.as<float>(), f.hL.as<float>(), B, T, u_ln, p, f.mf.as<float>(), f.rf.as<float>(), nullptr,
+                      c.dh.as<float>(), dgf.as<float>(), dbf.as<float>(), cs, out_c ? out_c->view() : CTensor{});
         ln_hop(u_ln, p, dgf.as<float>(), dbf.as<float>(), ev(cs));
+        live_delta(2, -1);
+    }
+
+    void bwd_block(int l, int p) {
+        const VBlock &b = blocks[l];
+        VRec &y = brec_w(l);
+        VGrad &gr = grad_of(l);
+        VCarry &c = carry[cw];
+        float *dh = c.dh.as<float>();
+        const CBuf &dhc_in = dhc(l);
         const float scale = 1.f / std::sqrt(float(HD));
-        for (int l = L - 1; l >= 0; --l) {
-            VLayer &y = layers[l];
-            // ---- MLP (y.dhc = bf16(dh), written by the LayerNorm backward that produced dh)
-            cudaEvent_t dhc_ready = ev(cs);
-            {
-                typename EpiConvOut2<0>::Params ep{};
-                ep.out = y.dz1.hi.p;
-                ep.ld = y.dz1.ld;
-                ep.gelu_z = y.z1.hi.p;
-                const CBuf &w = W(y.fc2, p);
-                reading({y.fc2}, A_BWD, p, cs, [&] {
-                    gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(y.dhc.hi.p, false, R, D, y.dhc.ld),
-                                                       opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
-                });
-            }
-            cudaEvent_t dz1_ready = ev(cs);
-            lin_hop(y.fc2, p, y.g1.view(), R, y.dhc.view(), dhc_ready, dz1_ready);
-            {
-                typename EpiConvOut2<0>::Params ep{};
-                ep.out = du.p;
-                ep.ld = D;
-                ep.out_f32 = 1;
-                const CBuf &w = W(y.fc1, p);
-                reading({y.fc1}, A_BWD, p, cs, [&] {
-                    gemm<false, false, EpiConvOut2<0>>("fc1_dgrad", opnd(y.dz1.hi.p, false, R, F, y.dz1.ld),
-                                                       opnd(w.hi.p, false, D, F, w.ld), R, D, F, ep, cs, false);
-                });
-            }
-            cudaEvent_t fc1_dg = ev(cs);
-            lin_hop(y.fc1, p, y.u2.view(), R, y.dz1.view(), dz1_ready, fc1_dg);
-            layernorm_bwd(du.as<float>(), y.hmid.as<float>(), R, 1, y.ln2, p, y.m2.as<float>(), y.r2.as<float>(),
-                          dh.as<float>(), dhm.as<float>(), y.dg2.as<float>(), y.db2.as<float>(), cs, y.dhmc.view());
-            ln_hop(y.ln2, p, y.dg2.as<float>(), y.db2.as<float>(), ev(cs));
-            // ---- attention
-            cudaEvent_t dhmc_ready = ev(cs);
-            {
-                typename EpiConvOut2<0>::Params ep{};
-                ep.out = dattn.hi.p;
-                ep.ld = dattn.ld;
-                const CBuf &w = W(y.proj, p);
-                reading({y.proj}, A_BWD, p, cs, [&] {
-                    gemm<false, false, EpiConvOut2<0>>("proj_dgrad", opnd(y.dhmc.hi.p, false, R, D, y.dhmc.ld),
-                                                       opnd(w.hi.p, false, D, D, w.ld), R, D, D, ep, cs, false);
-                });
-            }
-            cudaEvent_t proj_dg = ev(cs);
-            lin_hop(y.proj, p, y.attn.view(), R, y.dhmc.view(), dhmc_ready, proj_dg);
-            const int64_t qld = y.qkvb.ld;
-            auto qv = [&](int col) {
-                return BView{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + col, HD, T, qld, HD, int64_t(T) * qld};
-            };
-            const BView dO{dattn.hi.p, HD, T, dattn.ld, HD, int64_t(T) * dattn.ld};
-            const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
-            const BView dSv{dS.hi.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
-            bgemm<false, false>("attn_dprobs", dO, qv(2 * D), T, T, HD, dP.p, lds, int64_t(H) * T * lds,
-                                int64_t(T) * lds, 1, cs);
-            L_("softmax_bwd", 0, double(B) * H * T * T * 8, cs, [&] {
-                const dim3 g((B * H * T * 32 + 255) / 256);
-                const float *dPp = dP.as<float>();
-                const __nv_bfloat16 *Pp = y.P.as<__nv_bfloat16>();
-                __nv_bfloat16 *dSp = static_cast<__nv_bfloat16 *>(dS.hi.p);
-                if (T <= 128)
-                    launch_pdl(softmax_bwd4_kernel<1>, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
-                else if (T <= 256)
-                    launch_pdl(softmax_bwd4_kernel<2>, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
-                else
-                    launch_pdl(softmax_bwd_kernel, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
+        // ---- MLP (dhc_in = bf16(dh), written by the LayerNorm backward that produced dh)
+        cudaEvent_t dhc_ready = ev(cs);
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = gr.dz1.hi.p;
+            ep.ld = gr.dz1.ld;
+            ep.gelu_z = y.z1.hi.p;
+            const CBuf &w = Wt(b.fc2, p);
+            reading({b.fc2}, A_BWD, p, cs, [&] {
+                gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(dhc_in.hi.p, false, R, D, dhc_in.ld),
+                                                   opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
             });
-            __nv_bfloat16 *dq = static_cast<__nv_bfloat16 *>(y.dqkv.hi.p);
-            const int64_t dld = y.dqkv.ld;
-            bgemm<true, true>("attn_dvalues", Pv, dO, T, HD, T, dq + 2 * D, int(dld), int64_t(T) * dld, HD, 0, cs);
-            bgemm<false, true>("attn_dquery", dSv, qv(D), T, HD, T, dq, int(dld), int64_t(T) * dld, HD, 0, cs);
-            bgemm<true, true>("attn_dkey", dSv, qv(0), T, HD, T, dq + D, int(dld), int64_t(T) * dld, HD, 0, cs);
-            cudaEvent_t dqkv_ready = ev(cs);
-            {
-                typename EpiConvOut2<0>::Params ep{};
-                ep.out = du.p;
-                ep.ld = D;
-                ep.out_f32 = 1;
-                const CBuf &w = W(y.qkv, p);
-                reading({y.qkv}, A_BWD, p, cs, [&] {
-                    gemm<false, false, EpiConvOut2<0>>("qkv_dgrad", opnd(y.dqkv.hi.p, false, R, 3 * D, dld),
-                                                       opnd(w.hi.p, false, D, 3 * D, w.ld), R, D, 3 * D, ep, cs, false);
-                });
-            }
-            cudaEvent_t qkv_dg = ev(cs);
-            lin_hop(y.qkv, p, y.u1.view(), R, y.dqkv.view(), dqkv_ready, qkv_dg);
-            layernorm_bwd(du.as<float>(), y.h.as<float>(), R, 1, y.ln1, p, y.m1.as<float>(), y.r1.as<float>(),
-                          dhm.as<float>(), dh.as<float>(), y.dg1.as<float>(), y.db1.as<float>(), cs,
-                          l > 0 ? layers[l - 1].dhc.view() : CTensor{});
-            ln_hop(y.ln1, p, y.dg1.as<float>(), y.db1.as<float>(), ev(cs));
         }
-        // ---- embeddings
-        L_("token_grad", 0, double(R) * D * 4, cs, [&] {
-            launch_pdl(token_grad_kernel, dim3(blocks_for(int64_t(T) * D)), dim3(256), 0, cs,
-                       (const float *)dh.as<float>(), B, T, D, gpos.as<float>(), gcls.as<float>());
+        cudaEvent_t dz1_ready = ev(cs);
+        lin_hop(b.fc2, p, y.g1.view(), R, dhc_in.view(), dhc_ready, dz1_ready);
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = du.p;
+            ep.ld = D;
+            ep.out_f32 = 1;
+            const CBuf &w = Wt(b.fc1, p);
+            reading({b.fc1}, A_BWD, p, cs, [&] {
+                gemm<false, false, EpiConvOut2<0>>("fc1_dgrad", opnd(gr.dz1.hi.p, false, R, F, gr.dz1.ld),
+                                                   opnd(w.hi.p, false, D, F, w.ld), R, D, F, ep, cs, false);
+            });
+        }
+        cudaEvent_t fc1_dg = ev(cs);
+        lin_hop(b.fc1, p, y.u2.view(), R, gr.dz1.view(), dz1_ready, fc1_dg);
+        layernorm_bwd(du.as<float>(), y.hmid.as<float>(), R, 1, b.ln2, p, y.m2.as<float>(), y.r2.as<float>(), dh,
+                      dhm.as<float>(), gr.dg2.as<float>(), gr.db2.as<float>(), cs, gr.dhmc.view());
+        ln_hop(b.ln2, p, gr.dg2.as<float>(), gr.db2.as<float>(), ev(cs));
+        // ---- attention
+        cudaEvent_t dhmc_ready = ev(cs);
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = dattn.hi.p;
+            ep.ld = dattn.ld;
+            const CBuf &w = Wt(b.proj, p);
+            reading({b.proj}, A_BWD, p, cs, [&] {
+                gemm<false, false, EpiConvOut2<0>>("proj_dgrad", opnd(gr.dhmc.hi.p, false, R, D, gr.dhmc.ld),
+                                                   opnd(w.hi.p, false, D, D, w.ld), R, D, D, ep, cs, false);
+            });
+        }
+        cudaEvent_t proj_dg = ev(cs);
+        lin_hop(b.proj, p, y.attn.view(), R, gr.dhmc.view(), dhmc_ready, proj_dg);
+        const int64_t qld = y.qkvb.ld;
+        auto qv = [&](int col) {
+            return BView{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + col, HD, T, qld, HD, int64_t(T) * qld};
+        };
+        const BView dO{dattn.hi.p, HD, T, dattn.ld, HD, int64_t(T) * dattn.ld};
+        const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+        const BView dSv{dS.hi.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+        bgemm<false, false>("attn_dprobs", dO, qv(2 * D), T, T, HD, dP.p, lds, int64_t(H) * T * lds, int64_t(T) * lds,
+                            1, cs);
+        L_("softmax_bwd", 0, double(B) * H * T * T * 8, cs, [&] {
+            const dim3 g((B * H * T * 32 + 255) / 256);
+            const float *dPp = dP.as<float>();
+            const __nv_bfloat16 *Pp = y.P.as<__nv_bfloat16>();
+            __nv_bfloat16 *dSp = static_cast<__nv_bfloat16 *>(dS.hi.p);
+            if (T <= 128)
+                launch_pdl(softmax_bwd4_kernel<1>, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
+            else if (T <= 256)
+                launch_pdl(softmax_bwd4_kernel<2>, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
+            else
+                launch_pdl(softmax_bwd_kernel, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
         });
-        cast(dh.as<float>(), B * NP, NP, T, 1, dE.view(), cs);
+        __nv_bfloat16 *dq = static_cast<__nv_bfloat16 *>(gr.dqkv.hi.p);
+        const int64_t dld = gr.dqkv.ld;
+        bgemm<true, true>("attn_dvalues", Pv, dO, T, HD, T, dq + 2 * D, int(dld), int64_t(T) * dld, HD, 0, cs);
+        bgemm<false, true>("attn_dquery", dSv, qv(D), T, HD, T, dq, int(dld), int64_t(T) * dld, HD, 0, cs);
+        bgemm<true, true>("attn_dkey", dSv, qv(0), T, HD, T, dq + D, int(dld), int64_t(T) * dld, HD, 0, cs);
+        cudaEvent_t dqkv_ready = ev(cs);
+        {
+            typename EpiConvOut2<0>::Params ep{};
+            ep.out = du.p;
+            ep.ld = D;
+            ep.out_f32 = 1;
+            const CBuf &w = Wt(b.qkv, p);
+            reading({b.qkv}, A_BWD, p, cs, [&] {
+                gemm<false, false, EpiConvOut2<0>>("qkv_dgrad", opnd(gr.dqkv.hi.p, false, R, 3 * D, dld),
+                                                   opnd(w.hi.p, false, D, 3 * D, w.ld), R, D, 3 * D, ep, cs, false);
+            });
+        }
+        cudaEvent_t qkv_dg = ev(cs);
+        lin_hop(b.qkv, p, y.u1.view(), R, gr.dqkv.view(), dqkv_ready, qkv_dg);
+        layernorm_bwd(du.as<float>(), y.h.as<float>(), R, 1, b.ln1, p, y.m1.as<float>(), y.r1.as<float>(),
+                      dhm.as<float>(), dh, gr.dg1.as<float>(), gr.db1.as<float>(), cs,
+                      l > 0 ? dhc(l - 1).view() : CTensor{});
+        ln_hop(b.ln1, p, gr.dg1.as<float>(), gr.db1.as<float>(), ev(cs));
+        live_delta(1, -1);
+    }
+
+    void bwd_embed(int p) {
+        const float *dh = carry[cw].dh.as<float>();
+        L_("token_grad", 0, double(R) * D * 4, cs, [&] {
+            launch_pdl(token_grad_kernel, dim3(blocks_for(int64_t(T) * D)), dim3(256), 0, cs, dh, B, T, D,
+                       gpos.as<float>(), gcls.as<float>());
+        });
+        cast(dh, B * NP, NP, T, 1, dE.view(), cs);
         cudaEvent_t emb_ready = ev(cs);
         wait(hs, emb_ready);
         for (int u : {u_pos, u_cls}) {
@@ -859,10 +978,67 @@ struct VitTrainer {
                 });
             });
         }
-        lin_hop(u_patch, p, patches.view(), B * NP, dE.view(), emb_ready, nullptr);
+        lin_hop(u_patch, p, erec_w().patches.view(), B * NP, dE.view(), emb_ready, nullptr);
+        live_delta(0, -1);
+    }
+
+    void cast(const float *in, int rows, int per, int in_per, int skip, const CTensor &out, cudaStream_t s) {
+        L_("cast", 0, double(rows) * D * 6, s, [&] {
+            launch_pdl(cast_rows_kernel<0>, dim3(blocks_for(int64_t(rows) * D)), dim3(256), 0, s, in, rows, D, per,
+                       in_per, skip, out);
+        });
+    }
+
+    void fwd_seg(int s, int p) {
+        if (s == 0) fwd_embed(p, cs);
+        else if (s <= L) fwd_block(s - 1, p, cs);
+        else fwd_final(p, cs);
+    }
+    void bwd_seg(int s, int p) {
+        if (s == 0) bwd_embed(p);
+        else if (s <= L) bwd_block(s - 1, p);
+        else bwd_final(p);
+    }
+
+    // One training step of every worker this process runs.  W == 1 (one worker per GPU): forward over
+    // all segments, backward in reverse, weight gradients + hops on the hop stream lagging the compute
+    // stream.  W > 1 (single-GPU cyclic CDP): the plan's F / B tasks in timeline order (ref
+    // schedule.py:236-257), each expanded into its segments; the hop stream is joined before every
+    // segment, so per-block backward operands and released record slots are never overwritten while a
+    // weight gradient still reads them, and the gradient chain S = g_1 + ... + g_W runs in worker order.
+    void record_step(int p) {
+        kernels_per_step = 0;
+        flops_per_step = 0.0;
+        cudaEvent_t fork = ev(main);
+        wait(cs, fork);
+        wait(hs, fork);
+        if (W == 1) {
+            cw = 0;
+            for (int s = 0; s <= L + 1; ++s) fwd_seg(s, p);
+            for (int s = L + 1; s >= 0; --s) bwd_seg(s, p);
+        } else {
+            for (const VOp &op : plan) {
+                cw = op.worker - 1;
+                std::vector<int> segs;
+                for (int s = 0; s <= L + 1; ++s)
+                    if (seg_stage[s] == op.stage) segs.push_back(s);
+                if (op.kind == 1) std::reverse(segs.begin(), segs.end());
+                for (int s : segs) {
+                    wait(cs, ev(hs));
+                    if (op.kind == 0)
+                        fwd_seg(s, p);
+                    else
+                        bwd_seg(s, p);
+                }
+            }
+        }
         // join + bookkeeping
         wait(main, ev(cs));
         wait(main, ev(hs));
+        L_("loss_mean", 0, 0, main, [&] {
+            loss_mean_kernel<<<1, 1, 0, main>>>(loss_w.as<double>(), W, loss_dev.as<double>());
+            CDP_CUDA(cudaGetLastError());
+        });
         L_("finish_step", 0, 0, main, [&] {
             finish_step_kernel_rn<<<1, 1, 0, main>>>(loss_dev.as<double>(), flags_dev.as<Flags>(),
                                                      hist_loss.as<double>(), hist_flags.as<Flags>(), hist_cap,
@@ -905,23 +1081,23 @@ struct VitTrainer {
     }
 
     // ---------------------------------------------------------------- params / steps
-    void pack_slot(int slot) {
+    void pack_slot(int sl) {
         for (size_t i = 0; i < units.size(); ++i) {
             const VUnit &u = units[i];
             if (u.kind != V_LIN) continue;
-            pack_tensor_kernel<0><<<blocks_for(u.n), 256, 0, main>>>(theta[slot] + u.base, u.n, u.cols,
-                                                                     wc[slot][i].view());
+            pack_tensor_kernel<0><<<blocks_for(u.n), 256, 0, main>>>(theta[sl] + u.base, u.n, u.cols,
+                                                                     wc[sl][i].view());
             CDP_CUDA(cudaGetLastError());
         }
     }
     void set_params(int which, const float *host) {
         for (int v = 0; v < 2; ++v) {
             if (which >= 0 && v != which) continue;
-            const int slot = v == 0 ? (t & 1) : ((t & 1) ^ 1);
-            CDP_CUDA(cudaMemcpyAsync(theta[slot], host, size_t(Pn) * 4, cudaMemcpyHostToDevice, main));
-            pack_slot(slot);
+            const int sl = v == 0 ? (t & 1) : ((t & 1) ^ 1);
+            CDP_CUDA(cudaMemcpyAsync(theta[sl], host, size_t(Pn) * 4, cudaMemcpyHostToDevice, main));
+            pack_slot(sl);
             std::vector<uint32_t> tag(kMaxStages, uint32_t(v == 0 ? t : t - 1));  // version tags (ref engine.py:8-10)
-            CDP_CUDA(cudaMemcpy(ring->vtag[slot], tag.data(), kMaxStages * 4, cudaMemcpyHostToDevice));
+            CDP_CUDA(cudaMemcpy(ring->vtag[sl], tag.data(), kMaxStages * 4, cudaMemcpyHostToDevice));
         }
         CDP_CUDA(cudaStreamSynchronize(main));
     }
@@ -938,9 +1114,9 @@ struct VitTrainer {
         Control *c = reinterpret_cast<Control *>(blk);
         c->lr = lr;
         c->step = t;
-        std::memcpy(blk + sizeof(Control), perm, size_t(B) * 4);
+        std::memcpy(blk + sizeof(Control), perm, size_t(W) * B * 4);
         CDP_CUDA(cudaMemcpyAsync(ctrl_dev.p, blk, sizeof(Control), cudaMemcpyHostToDevice, main));
-        CDP_CUDA(cudaMemcpyAsync(perm_dev.p, blk + sizeof(Control), size_t(B) * 4, cudaMemcpyHostToDevice, main));
+        CDP_CUDA(cudaMemcpyAsync(perm_dev.p, blk + sizeof(Control), size_t(W) * B * 4, cudaMemcpyHostToDevice, main));
         CDP_CUDA(cudaEventRecord(stage_ev[k], main));
     }
     void step(const int *perm, float lr) {
@@ -950,10 +1126,11 @@ struct VitTrainer {
     }
     void step_host_batch(const float *x, const int32_t *labels, float lr) {
         const size_t im = size_t(img) * img * 3;
-        CDP_CUDA(cudaMemcpyAsync(data_x.p, x, size_t(B) * im * 4, cudaMemcpyHostToDevice, main));
-        CDP_CUDA(cudaMemcpyAsync(data_lab.p, labels, size_t(B) * 4, cudaMemcpyHostToDevice, main));
-        std::vector<int> ident(B);
-        for (int i = 0; i < B; ++i) ident[i] = i;
+        const int n = W * B;  // every worker's micro-batch, worker-major
+        CDP_CUDA(cudaMemcpyAsync(data_x.p, x, size_t(n) * im * 4, cudaMemcpyHostToDevice, main));
+        CDP_CUDA(cudaMemcpyAsync(data_lab.p, labels, size_t(n) * 4, cudaMemcpyHostToDevice, main));
+        std::vector<int> ident(n);
+        for (int i = 0; i < n; ++i) ident[i] = i;
         step(ident.data(), lr);
     }
     void profile_step(const int *perm, float lr, bool serial) {
@@ -986,40 +1163,106 @@ struct cdp_vit {
     std::unique_ptr<VitTrainer> impl;
 };
 
+static std::unique_ptr<VitTrainer> vit_new(int image, int patch, int dim, int depth, int heads, int mlp, int classes,
+                                           int micro_batch, int workers, float momentum, float weight_decay,
+                                           int n_samples, const float *x, const int32_t *labels) {
+    CDP_REQUIRE(micro_batch >= 1 && micro_batch <= 256, "micro-batch must be in [1, 256]");
+    CDP_REQUIRE(depth >= 1 && depth <= 40, "depth: 1..40");
+    auto tr = std::make_unique<VitTrainer>();
+    tr->B = micro_batch;
+    tr->img = image;
+    tr->P = patch;
+    tr->D = dim;
+    tr->L = depth;
+    tr->H = heads;
+    tr->F = mlp;
+    tr->classes = classes;
+    tr->momentum = momentum;
+    tr->wd = weight_decay;
+    tr->W = workers;
+    tr->n_samples = std::max(n_samples, micro_batch * workers);
+    const size_t im = size_t(image) * image * 3;
+    tr->data_x = DevBuf(size_t(tr->n_samples) * im * 4);
+    tr->data_lab = DevBuf(size_t(tr->n_samples) * 4);
+    if (x) CDP_CUDA(cudaMemcpy(tr->data_x.p, x, size_t(n_samples) * im * 4, cudaMemcpyHostToDevice));
+    if (labels) CDP_CUDA(cudaMemcpy(tr->data_lab.p, labels, size_t(n_samples) * 4, cudaMemcpyHostToDevice));
+    tr->make_units();
+    return tr;
+}
+
 extern "C" int cdp_vit_create_rank(int image, int patch, int dim, int depth, int heads, int mlp, int classes,
                                    int micro_batch, int world, int rank, const int32_t *unit_stage,
                                    const uint8_t *stage_fresh, float momentum, float weight_decay, int n_samples,
                                    const float *x, const int32_t *labels, cdp_vit **out) {
     return guarded([&] {
         CDP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
-        CDP_REQUIRE(micro_batch >= 1 && micro_batch <= 256, "micro-batch must be in [1, 256]");
-        CDP_REQUIRE(depth >= 1 && depth <= 40, "depth: 1..40");
-        auto tr = std::make_unique<VitTrainer>();
-        tr->B = micro_batch;
-        tr->img = image;
-        tr->P = patch;
-        tr->D = dim;
-        tr->L = depth;
-        tr->H = heads;
-        tr->F = mlp;
-        tr->classes = classes;
-        tr->momentum = momentum;
-        tr->wd = weight_decay;
+        auto tr = vit_new(image, patch, dim, depth, heads, mlp, classes, micro_batch, 1, momentum, weight_decay,
+                          n_samples, x, labels);
         tr->rank = rank;
         tr->world = world;
-        tr->n_samples = std::max(n_samples, micro_batch);
-        const size_t im = size_t(image) * image * 3;
-        tr->data_x = DevBuf(size_t(tr->n_samples) * im * 4);
-        tr->data_lab = DevBuf(size_t(tr->n_samples) * 4);
-        if (x) CDP_CUDA(cudaMemcpy(tr->data_x.p, x, size_t(n_samples) * im * 4, cudaMemcpyHostToDevice));
-        if (labels) CDP_CUDA(cudaMemcpy(tr->data_lab.p, labels, size_t(n_samples) * 4, cudaMemcpyHostToDevice));
-        tr->build();
         for (size_t i = 0; i < tr->units.size(); ++i) {
             const int st = unit_stage[i];
             CDP_REQUIRE(st >= 1 && st <= world, "unit stage out of range");
             tr->units[i].stage = st;
             tr->units[i].fresh = stage_fresh[st - 1] != 0;
         }
+        // one worker: every block keeps its own record (embed / final: one each)
+        tr->slot.assign(1, std::vector<int>(size_t(depth) + 2, 0));
+        for (int l = 0; l < depth; ++l) tr->slot[0][1 + l] = l;
+        tr->pool[1] = depth;
+        tr->build();
+        *out = new cdp_vit{std::move(tr)};
+    });
+}
+
+extern "C" int cdp_vit_create_cyclic(int image, int patch, int dim, int depth, int heads, int mlp, int classes,
+                                     int micro_batch, int n_workers, const int32_t *unit_stage, const uint8_t *fresh,
+                                     int n_ops, const int32_t *ops, const int32_t *rec_slot, const int32_t *pools,
+                                     float momentum, float weight_decay, int probe, int n_samples, const float *x,
+                                     const int32_t *labels, cdp_vit **out) {
+    return guarded([&] {
+        CDP_REQUIRE(n_workers >= 2, "single-GPU cyclic CDP needs at least two workers (micro-batches)");
+        auto tr = vit_new(image, patch, dim, depth, heads, mlp, classes, micro_batch, n_workers, momentum,
+                          weight_decay, n_samples, x, labels);
+        const int NS = depth + 2;
+        tr->seg_stage.assign(NS, 0);
+        for (size_t i = 0; i < tr->units.size(); ++i) {
+            const int st = unit_stage[i];
+            CDP_REQUIRE(st >= 1 && st <= n_workers, "unit stage out of range");
+            tr->units[i].stage = st;
+            int &ss = tr->seg_stage[tr->seg_of_unit(int(i))];
+            CDP_REQUIRE(ss == 0 || ss == st, "the units of an embedding / block / head segment must share a stage");
+            ss = st;
+        }
+        tr->freshw.assign(n_workers, std::vector<uint8_t>(tr->units.size(), 1));
+        for (int w = 0; w < n_workers; ++w)
+            for (size_t i = 0; i < tr->units.size(); ++i)
+                tr->freshw[w][i] = fresh[size_t(w) * n_workers + tr->units[i].stage - 1] != 0;
+        std::vector<int> f_seen(n_workers, 0), b_seen(n_workers, 0);
+        for (int k = 0; k < n_ops; ++k) {
+            const VOp op{ops[3 * k], ops[3 * k + 1], ops[3 * k + 2]};
+            CDP_REQUIRE((op.kind == 0 || op.kind == 1) && op.worker >= 1 && op.worker <= n_workers && op.stage >= 1 &&
+                            op.stage <= n_workers,
+                        "bad plan op");
+            ++(op.kind ? b_seen : f_seen)[op.worker - 1];
+            tr->plan.push_back(op);
+        }
+        for (int w = 0; w < n_workers; ++w)
+            CDP_REQUIRE(f_seen[w] == n_workers && b_seen[w] == n_workers, "the plan must hold every F / B task once");
+        for (int k = 0; k < 3; ++k) {
+            CDP_REQUIRE(pools[k] >= 1, "record pools need at least one slot");
+            tr->pool[k] = pools[k];
+        }
+        tr->slot.assign(n_workers, std::vector<int>(NS, 0));
+        for (int w = 0; w < n_workers; ++w)
+            for (int sg = 0; sg < NS; ++sg) {
+                const int v = rec_slot[size_t(w) * NS + sg];
+                const int k = sg == 0 ? 0 : sg <= depth ? 1 : 2;
+                CDP_REQUIRE(v >= 0 && v < pools[k], "record slot out of range");
+                tr->slot[w][sg] = v;
+            }
+        tr->probe = probe != 0;
+        tr->build();
         *out = new cdp_vit{std::move(tr)};
     });
 }
@@ -1162,19 +1405,25 @@ extern "C" int cdp_vit_ring_error(cdp_vit *tr, int *err) {
 }
 
 extern "C" int cdp_vit_stats(cdp_vit *tr, int64_t *out, int n_out) {
-    // [0] activation bytes kept for the backward, [1] parameter-state bytes, [2] kernels / step,
-    // [3] tensor-core flops / step
+    // [0] activation-record bytes allocated (record pools: embed / block / final slots x record bytes),
+    // [1] parameter-state bytes, [2] kernels / step, [3] tensor-core flops / step,
+    // [4] executed high-water mark of live record bytes (probe; 0 when off),
+    // [5..7] bytes of one embed / block / final record, [8..10] slots per pool
     return guarded([&] {
         auto &m = *tr->impl;
-        int64_t act = int64_t(m.patches.hi.bytes + m.E.bytes + m.hL.bytes + m.uf.hi.bytes);
-        for (auto &y : m.layers)
-            act += int64_t(y.h.bytes + y.hmid.bytes + y.u1.hi.bytes + y.u2.hi.bytes + y.attn.hi.bytes + y.g1.hi.bytes +
-                           y.qkvb.hi.bytes + y.z1.hi.bytes + y.P.bytes + 4 * y.m1.bytes);
+        int64_t act = 0;
+        for (int k = 0; k < 3; ++k) act += m.record_bytes(k) * m.pool[k];
         int64_t par = int64_t(m.Pp) * (m.vel ? 16 : 12);
         for (int v = 0; v < 2; ++v)
             for (auto &w : m.wc[v]) par += int64_t(w.hi.bytes);
-        int64_t vals[4] = {act, par, m.kernels_per_step, int64_t(m.flops_per_step)};
-        for (int i = 0; i < n_out && i < 4; ++i) out[i] = vals[i];
+        int64_t hw[2] = {0, 0};
+        if (m.probe) {
+            CDP_CUDA(cudaStreamSynchronize(m.main));
+            CDP_CUDA(cudaMemcpy(hw, m.live.p, 16, cudaMemcpyDeviceToHost));
+        }
+        int64_t vals[11] = {act, par, m.kernels_per_step, int64_t(m.flops_per_step), hw[1], m.record_bytes(0),
+                            m.record_bytes(1), m.record_bytes(2), m.pool[0], m.pool[1], m.pool[2]};
+        for (int i = 0; i < n_out && i < 11; ++i) out[i] = vals[i];
     });
 }
 

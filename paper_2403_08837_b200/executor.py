@@ -219,3 +219,125 @@ def compile_rank_plan(n_workers: int, rank: int, rule: UpdateRule | None = None,
     for l in range(n_layers, 0, -1):
         ops.append([OP_B, i, l, fresh(l), 0, 0, hop, 0])
     return np.asarray(ops, dtype=np.int32)
+
+
+@dataclass
+class SegmentPlan:
+    """Single-GPU plan over model segments (one worker = one micro-batch, all on one GPU).
+
+    ops     int32 [n_ops, 3]: (kind 0=F / 1=B, worker i, stage j) in timeline order;
+    slot    int32 [n_workers, n_segments]: activation-record slot of (i, segment) in its pool;
+    pools   int32 [n_pools]: slots per record pool (the interval colouring's width);
+    live    int32 [n_ops + 1, n_pools]: records live after each op (index 0 = before the step);
+    fresh   uint8 [n_workers, n_stages]: the rule table (all ones for DP)."""
+
+    ops: np.ndarray
+    slot: np.ndarray
+    pools: np.ndarray
+    live: np.ndarray
+    fresh: np.ndarray
+
+    def peak_bytes(self, record_bytes) -> int:
+        """High-water mark of live record bytes over the step (time-resolved, not pools x bytes)."""
+        return int((self.live.astype(np.int64) @ np.asarray(record_bytes, dtype=np.int64)).max())
+
+
+def segment_partition(seg_cost, n_stages: int) -> np.ndarray:
+    """Contiguous split of segments into `n_stages` non-empty stages minimising the largest stage
+    cost (exact DP; ties keep earlier boundaries).  Returns the 1-based stage of each segment."""
+    cost = np.asarray(seg_cost, dtype=np.float64)
+    S = len(cost)
+    if not 1 <= n_stages <= S:
+        raise ValueError("need 1 <= stages <= segments")
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    INF = float("inf")
+    best = np.full((n_stages + 1, S + 1), INF)
+    cut = np.zeros((n_stages + 1, S + 1), dtype=np.int64)
+    best[0, 0] = 0.0
+    for k in range(1, n_stages + 1):
+        for e in range(k, S + 1):
+            for b in range(k - 1, e):
+                v = max(best[k - 1, b], cum[e] - cum[b])
+                if v < best[k, e]:
+                    best[k, e], cut[k, e] = v, b
+    stage = np.zeros(S, dtype=np.int32)
+    e = S
+    for k in range(n_stages, 0, -1):
+        b = int(cut[k, e])
+        stage[b:e] = k
+        e = b
+    return stage
+
+
+def compile_segment_plan(n_workers: int, seg_stage, seg_pool, rule: UpdateRule | None = None,
+                         weights: CostWeights = CostWeights()) -> SegmentPlan:
+    """Cyclic (rule) or lockstep DP (rule None) single-GPU plan from the reference Timeline
+    (SINGLE_GPU_CDP / SINGLE_GPU_DP, ref schedule.py:178-257) expanded onto segments.
+
+    The record of (worker i, segment s) holds s's input and what B(i, s) reads: it is acquired by
+    the forward that writes that input (F of segment s-1; segment 0 by its own forward) and
+    released after B(i, s).  Slots are coloured greedily in timeline order (lowest free slot), which
+    for these interval graphs uses exactly the maximum number of simultaneously live records — the
+    (N+1)/2 vs N micro-batches of ref costs.py:111-115 when the segments are homogeneous."""
+    n = n_workers
+    seg_stage = [int(s) for s in seg_stage]
+    seg_pool = [int(p) for p in seg_pool]
+    S = len(seg_stage)
+    if len(seg_pool) != S:
+        raise ValueError("seg_pool must name a pool per segment")
+    _check_stage_map(seg_stage, n)
+    if rule is not None:
+        if rule.n != n:
+            raise ValueError("rule size does not match the number of workers")
+        rule.check_feasible()
+    tasks = sorted(_template_tasks(n, n, rule, weights), key=lambda x: (x[0], x[1], x[2]))
+    fresh = np.ones((n, n), dtype=np.uint8)
+    if rule is not None:
+        fresh[:] = np.array(rule.fresh, dtype=np.uint8)
+    n_pools = max(seg_pool) + 1
+    free = [[] for _ in range(n_pools)]
+    count = [0] * n_pools
+    live = [0] * n_pools
+    slot = -np.ones((n, S), dtype=np.int32)
+    held = set()
+    curve = [list(live)]
+    ops = []
+
+    def acquire(i, s):
+        k = seg_pool[s]
+        if free[k]:
+            free[k].sort()
+            v = free[k].pop(0)
+        else:
+            v = count[k]
+            count[k] += 1
+        if slot[i - 1, s] not in (-1, v):
+            raise AssertionError("a record must keep its slot from step to step (periodic plan)")
+        slot[i - 1, s] = v
+        held.add((i, s))
+        live[k] += 1
+
+    def release(i, s):
+        k = seg_pool[s]
+        held.remove((i, s))
+        free[k].append(int(slot[i - 1, s]))
+        live[k] -= 1
+
+    segs_of = {j: [s for s in range(S) if seg_stage[s] == j] for j in range(1, n + 1)}
+    for _start, i, kind, j in tasks:
+        ops.append((kind, i, j))
+        if kind == 0:
+            for s in segs_of[j]:
+                if s == 0:
+                    acquire(i, 0)
+                if s + 1 < S:
+                    acquire(i, s + 1)
+        else:
+            for s in segs_of[j][::-1]:
+                release(i, s)
+        curve.append(list(live))
+    if held:
+        raise AssertionError("every record must be released by the end of the step")
+    return SegmentPlan(np.asarray(ops, dtype=np.int32).reshape(-1, 3), slot,
+                       np.asarray([max(c, 1) for c in count], dtype=np.int32),
+                       np.asarray(curve, dtype=np.int32), fresh)

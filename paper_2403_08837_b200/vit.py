@@ -59,6 +59,32 @@ def stage_partition(units, n_stages):
     return stage.astype(np.int32)
 
 
+def vit_segments(units, depth):
+    """Segment of every unit: 0 = embedding (patch, cls, pos), 1..depth = blocks, depth + 1 = final
+    LN + head; and the per-segment tensor-core flops (the single-GPU executor's stage tasks run whole
+    segments, so stage boundaries fall between segments)."""
+    seg = np.array([0, 0, 0] + [1 + k // 6 for k in range(6 * depth)] + [depth + 1, depth + 1], dtype=np.int32)
+    assert len(seg) == len(units)
+    cost = np.zeros(depth + 2)
+    for s, (_n, _shape, f) in zip(seg, units):
+        cost[s] += f
+    return seg, cost
+
+
+def cyclic_plan(cfg, n_workers, rule=None):
+    """Single-GPU CDP (rule) or DP (None) plan for `n_workers` micro-batches of this ViT on one GPU:
+    (unit stage, SegmentPlan).  Segments are split into N FLOP-balanced contiguous stages; record
+    pools: 0 = embedding records, 1 = block records (shared by all blocks), 2 = final records."""
+    from .executor import compile_segment_plan, segment_partition
+
+    units = vit_units(**cfg)
+    depth = cfg["depth"]
+    seg, cost = vit_segments(units, depth)
+    seg_stage = segment_partition(np.maximum(cost, 1.0), n_workers)
+    pool = [0] + [1] * depth + [2]
+    return seg_stage[seg].astype(np.int32), compile_segment_plan(n_workers, seg_stage, pool, rule)
+
+
 def vit_init(cfg, seed=0) -> np.ndarray:
     """Deterministic initialisation in the trainer layout (numpy PCG64): linear weights N(0, 0.02),
     biases 0, LayerNorm (1, 0), class token / position embedding N(0, 0.02)."""
@@ -122,6 +148,50 @@ class DeviceVit:
         assert self.P == sum(int(np.prod(s)) for _, s, _ in self.units)
         self._opened = []
 
+    @classmethod
+    def single_gpu(cls, cfg=None, micro_batch=32, n_workers=4, rule=None, momentum=0.0, weight_decay=0.0,
+                   inputs=None, labels=None, probe=True, trace=False):
+        """Single-GPU cyclic CDP (rule) or DP (rule None): `n_workers` micro-batches = stages on this
+        GPU, stepped through the reference SINGLE_GPU_CDP / SINGLE_GPU_DP timeline with activation
+        records from the plan's interval colouring (cdp_vit_create_cyclic).  step() takes
+        n_workers * micro_batch indices, worker-major (ref models.py:173-185)."""
+        self = cls.__new__(cls)
+        self.cfg = dict(VIT_B16 if cfg is None else cfg)
+        self.lib = N.lib()
+        self.micro_batch, self.world, self.rank = int(micro_batch), 1, 0
+        self.n_workers = int(n_workers)
+        self.units = vit_units(**self.cfg)
+        stage, plan = cyclic_plan(self.cfg, self.n_workers, rule)
+        self.stage, self.plan = np.ascontiguousarray(stage, dtype=np.int32), plan
+        x = lab = None
+        n = 0
+        if inputs is not None:
+            x = np.ascontiguousarray(inputs, dtype=np.float32)
+            lab = np.ascontiguousarray(labels, dtype=np.int32)
+            n = x.shape[0]
+        c = self.cfg
+        ops = np.ascontiguousarray(plan.ops, dtype=np.int32)
+        slot = np.ascontiguousarray(plan.slot, dtype=np.int32)
+        pools = np.ascontiguousarray(plan.pools, dtype=np.int32)
+        fresh = np.ascontiguousarray(plan.fresh, dtype=np.uint8)
+        h = ctypes.c_void_p()
+        N.check(self.lib.cdp_vit_create_cyclic(
+            c["image"], c["patch"], c["dim"], c["depth"], c["heads"], c["mlp"], c["classes"], self.micro_batch,
+            self.n_workers, _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), len(ops), _i32p(ops), _i32p(slot),
+            _i32p(pools), float(momentum), float(weight_decay), int(bool(probe)), n,
+            x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
+            ctypes.byref(h)))
+        self.h = h
+        self._keep = (x, lab)
+        if trace:
+            N.check(self.lib.cdp_vit_set_trace(self.h, 1))
+        np_, nu = ctypes.c_int64(), ctypes.c_int()
+        N.check(self.lib.cdp_vit_info(self.h, ctypes.byref(np_), ctypes.byref(nu)))
+        self.P = np_.value
+        self._opened = []
+        self.connect([self.region()])
+        return self
+
     def region(self) -> int:
         b = ctypes.c_void_p()
         N.check(self.lib.cdp_vit_region(self.h, ctypes.byref(b)))
@@ -159,7 +229,7 @@ class DeviceVit:
 
     def step(self, perm, lr):
         p = np.ascontiguousarray(perm, dtype=np.int32)
-        assert p.size == self.micro_batch
+        assert p.size == self.micro_batch * getattr(self, "n_workers", 1)
         N.check(self.lib.cdp_vit_step(self.h, _i32p(p), float(lr)))
 
     def step_host_batch_ptr(self, x_ptr: int, y_ptr: int, lr: float):
@@ -205,10 +275,11 @@ class DeviceVit:
         return e.value
 
     def stats(self) -> dict:
-        out = np.zeros(4, dtype=np.int64)
-        N.check(self.lib.cdp_vit_stats(self.h, out.ctypes.data_as(N.c_int64_p), 4))
+        out = np.zeros(11, dtype=np.int64)
+        N.check(self.lib.cdp_vit_stats(self.h, out.ctypes.data_as(N.c_int64_p), 11))
         return {"activation_bytes": int(out[0]), "param_state_bytes": int(out[1]), "kernels_per_step": int(out[2]),
-                "tensor_flops_per_step": int(out[3])}
+                "tensor_flops_per_step": int(out[3]), "live_record_high_water_bytes": int(out[4]),
+                "record_bytes": [int(v) for v in out[5:8]], "record_slots": [int(v) for v in out[8:11]]}
 
     def mark(self, k):
         N.check(self.lib.cdp_vit_mark(self.h, k))
