@@ -5,30 +5,28 @@
                     [--model resnet18|resnet50|mlp] [--dtype bf16|fp32] [--rule cdp-v2|cdp-v1|dp]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Headline workload (default, --model resnet18) = BASELINE configs[1]:
-ResNet-18 (CIFAR variant: 3x3 stem, no max pool) on CIFAR-10-shaped synthetic
-data (32x32x3, 10 classes), CDP-v2, ONE micro-batch of B = 128 per GPU,
-N = micro-batches = stages = GPUs (FLOP-balanced contiguous tensor groups),
-SGD lr 0.05 momentum 0.9, bf16 operands / fp32 master state.  One step = the
-whole job's training step: every rank's forward + backward, the per-tensor
-gradient hops rank -> rank+1 over peer memory fused into the weight-gradient
-GEMM epilogues, the fused update on the last rank, the parameter pulls; one
-CUDA graph per rank, no collective.  Per-GPU work is fixed as N grows (weak
-scaling).
+Headline workload (default, --model resnet50) = BASELINE configs[2], the north-star target:
+ResNet-50 (torchvision v1.5 layout) on ImageNet-shaped synthetic data (224x224x3, 1000 classes),
+CDP-v2, ONE micro-batch of B = 128 per GPU, N = micro-batches = stages = GPUs (FLOP-balanced
+contiguous tensor groups), SGD lr 0.05 momentum 0.9, bf16 operands / fp32 master state.  One step =
+the whole job's training step: every rank's forward + backward, the per-tensor gradient hops
+rank -> rank+1 over peer memory fused into the weight-gradient GEMM epilogues, the fused update on
+the last rank, the parameter pulls; one CUDA graph per rank, no collective.  Per-GPU work is fixed
+as N grows (weak scaling).
 
-`value` = samples/s of the device-timed step (CUDA events on each rank's
-launch stream around each graph launch, inputs resident in HBM, L2 flushed by
-a 256 MiB memset before every timed step, max over ranks); `e2e` = the same
-through the public API with the step's images / labels copied H2D from pinned
-host memory inside every step and the loss read back every step.  `roofline`
-= the dominant tensor-core kernel class of a serialised instrumented step
-(algorithmic conv flops / event-timed duration) against MEASURED_PEAKS.json.
-At N = 1 the line also carries `resnet50` (BASELINE configs[2] shape on one
-GPU: ResNet-50 224x224, B = 128, bf16, CDP-v2) and `single_gpu_cdp`
-(configs[0]: the reference's own CPU-runnable MLP case with its CPU time).
-`cpu_baseline` / `--impl reference`: the reference has no ResNet,
-so the CPU arm is the oracle port (oracle/resnet_torch.py: the reference's
-`_advance` semantics over torch-CPU float64 autograd) on all host cores, on a
+`value` = samples/s of the device-timed step (CUDA events on each rank's launch stream around each
+graph launch, inputs resident in HBM, L2 flushed by a 256 MiB memset before every timed step, max
+over ranks); `e2e` = the same through the public API with the step's images / labels copied H2D
+from pinned host memory inside every step and the loss read back every step.  `roofline` = the
+dominant tensor-core kernel class of a serialised instrumented step (algorithmic conv flops /
+event-timed duration) against MEASURED_PEAKS.json.  N > 1 adds `exposed_comm` (ring step minus the
+compute-only step of the same per-rank work) and `p2p` (hop / pull bytes per rank, GB/s in the
+kernels that move them).  At N = 1 the line also carries `resnet18` (configs[1] shape),
+`vit_b16_single_gpu_cdp` (configs[3]: ViT-B/16, 4 and 12 sequential micro-batches on one GPU,
+CDP-v2 vs DP with the device-measured activation high-water marks) and `single_gpu_cdp` (configs[0]:
+the reference's own CPU-runnable MLP case with its CPU time).  `cpu_baseline` / `--impl reference`:
+the reference has no ResNet, so the CPU arm is the oracle port (oracle/resnet_torch.py:
+the reference's `_advance` semantics over torch-CPU float64 autograd) on all host cores, on a
 bounded sample of the same workload.
 """
 
@@ -344,7 +342,9 @@ VIT_MB = 32  # BASELINE configs[3] / SURVEY §8d: ViT-B/16, B = 32
 
 
 def make_trainer(args, model, ws, rank, rule, allreduce, zero):
-    """(trainer, micro-batch, image side, classes, dataset x, labels) for a bench model."""
+    """(trainer, micro-batch, image side, classes, dataset x, labels) for a bench model.  With ws = 1 and
+    rule = None the trainer is the compute-only twin of a ring rank (same per-GPU work, fused update,
+    no peer reads / waits / pulls): the baseline of `exposed_comm_ms`."""
     from paper_2403_08837_b200.resnet import DeviceResNet, init_params, layer_specs, synthetic_images
 
     if model == "vit_b16":
@@ -450,6 +450,7 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     losses, flags = tr.history(steps + warmup)
     assert np.all(np.isfinite(losses)) and not flags.any(), "non-finite step in the timed region"
     st = tr.stats()
+    P = tr.P
     out = {"value": round(ws * B / (ms / 1e3), 1), "ms_per_step": round(ms, 4), "clocks": clk.summary(),
            "losses_first_last": [round(float(losses[0]), 5), round(float(losses[-1]), 5)],
            "activation_bytes": {"per_gpu": st["activation_bytes"], "sum_over_gpus": st["activation_bytes"] * ws},
@@ -511,6 +512,31 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
                        "frac": round(achieved / peak, 4), "traffic": traffic,
                        "algorithmic_flops_per_launch": round(d[2] / d[0]), "launch_us": round(d[1] / d[0] * 1e3, 2),
                        "share_of_serial_step": round(d[1] / tot, 3)}
+    # ---- P2P traffic of this step (bytes per rank, one micro-batch per GPU): the gradient hop reads the
+    # previous rank's partial sum S (4 B / param, ranks 2..N, fused into the weight-gradient epilogues);
+    # every reader pulls the versions it reads from the updater (4 B / param, ranks 1..N-1); ZeRO-CDP
+    # copies states instead of pulling.  GB/s = those bytes / the event-timed durations of the kernels
+    # that move them on this rank (the hop-fused GEMMs also compute, so theirs is a lower bound).
+    if ws > 1:
+        hop_b = 4 * P if rank > 0 else 0
+        pull_b = 0 if (rank == ws - 1 or zero or allreduce) else 4 * P
+        zero_b = int(st.get("zero_state_bytes_per_step", 0))
+        hop_ms = sum(a[1] for k, a in agg.items() if "hop" in k and "wait" not in k)
+        pull_ms = sum(a[1] for k, a in agg.items() if k in ("pull", "zero_copy"))
+        vals = torch.tensor([hop_b, pull_b, zero_b, hop_ms, pull_ms], dtype=torch.float64, device="cuda")
+        allv = [torch.zeros_like(vals) for _ in range(ws)]
+        torch.distributed.all_gather(allv, vals)
+        allv = [v.cpu().numpy() for v in allv]
+        out["p2p"] = {
+            "grad_hop_read_bytes_per_rank": [int(v[0]) for v in allv],
+            "param_pull_read_bytes_per_rank": [int(v[1]) for v in allv],
+            "zero_state_bytes_per_rank": [int(v[2]) for v in allv],
+            "bytes_per_step_all_ranks": int(sum(v[0] + v[1] + v[2] for v in allv)),
+            "grad_gbs_in_hop_kernels_rank1": round(allv[1][0] / (allv[1][3] / 1e3) / 1e9, 1) if allv[1][3] else None,
+            "pull_gbs_rank0": round((allv[0][1] + allv[0][2]) / (allv[0][4] / 1e3) / 1e9, 1) if allv[0][4] else None,
+            "note": "peer HBM over NVLink when ranks sit on different GPUs; same-GPU ranks (tests) read local HBM"}
+    else:
+        out["p2p"] = {"bytes_per_step_all_ranks": 0, "note": "one GPU: no peer traffic (the hop is local)"}
     out["kernel_breakdown"] = {
         k: {"launches": a[0], "ms": round(a[1], 4), "share": round(a[1] / tot, 3),
             **({"tflops": round(a[2] / (a[1] / 1e3) / 1e12, 1)} if a[2] else
@@ -518,17 +544,111 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
         for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])}
     out["serial_step_ms"] = round(tot, 4)
     tr.close()
+    # ---- exposed gradient communication (N > 1): full ring step - compute-only step of the same rank work
+    if ws > 1 and not allreduce:
+        from paper_2403_08837_b200.dist import resolve as _resolve
+
+        co, *_ = make_trainer(args, model, 1, 0, _resolve(args.rule, 1), False, False)
+        co.connect([co.region()])
+        cperms = [np.random.default_rng([0, t]).permutation(2 * B)[:B] for t in range(warmup + steps)]
+        for t in range(warmup):
+            co.step(cperms[t], RN_LR)
+        co.sync()
+        torch.distributed.barrier()
+        for k in range(steps):
+            co.flush_l2()
+            co.mark(2 * k)
+            co.step(cperms[warmup + k], RN_LR)
+            co.mark(2 * k + 1)
+        co.sync()
+        cms = float(np.mean([co.elapsed(2 * k, 2 * k + 1) for k in range(steps)]))
+        co.close()
+        t = torch.tensor([cms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        cms = float(t.item())
+        out["exposed_comm"] = {"compute_only_ms_per_step": round(cms, 4),
+                               "exposed_comm_ms": round(ms - cms, 4), "exposed_frac": round((ms - cms) / ms, 4),
+                               "how": "max-over-ranks step of the ring minus max-over-ranks step of the same "
+                                      "per-rank work as a one-GPU trainer (fused update, no peer reads / waits / "
+                                      "pulls), both device-timed with L2 flushed"}
+    elif ws == 1:
+        out["exposed_comm"] = {"exposed_comm_ms": 0.0, "note": "one GPU: no gradient communication"}
     return out
 
 
-def vit_activation_model(res, n=4):
-    """configs[3] reading: single-GPU CDP over N sequential micro-batches keeps (N+1)/2 micro-batches of
-    activations alive vs N for DP (ref costs.py:111-115, cross-checked by tests/test_plan_parity.py); the
-    per-micro-batch bytes are the trainer's measured activation records."""
-    per = res["activation_bytes"]["per_gpu"]
-    return {"micro_batches": n, "activation_bytes_per_micro_batch": per,
-            "cdp_peak_bytes": per * (n + 1) // 2, "dp_peak_bytes": per * n, "cdp_over_dp": (n + 1) / (2 * n),
-            "source": "measured per-micro-batch records x the reference plan's live-activation count"}
+def vit_single_gpu(n, steps, warmup, profile=False):
+    """BASELINE configs[3]: ViT-B/16 224x224, n sequential micro-batches of VIT_MB on ONE GPU, stepped
+    through the reference's SINGLE_GPU_CDP (cdp-v2) and SINGLE_GPU_DP timelines by the cyclic executor
+    (DeviceVit.single_gpu).  Peak activation = the device's live-record high-water mark (a counter
+    updated around every record acquire / release in the captured step), cross-checked against the
+    allocator (cudaMemGetInfo delta of creating the trainer) and the plan's time-resolved peak."""
+    import torch
+
+    from paper_2403_08837_b200.resnet import synthetic_images
+    from paper_2403_08837_b200.rules import rule_by_name
+    from paper_2403_08837_b200.vit import VIT_B16, DeviceVit, vit_init
+
+    B = VIT_MB
+    x, y = synthetic_images(2 * B * n, seed=0, hw=224, classes=1000)
+    init = vit_init(VIT_B16, seed=0)
+    perms = [np.random.default_rng([0, t]).permutation(len(x))[:n * B] for t in range(1, warmup + steps + 2)]
+    res = {}
+    for name in ("cdp-v2", "dp"):
+        rule = None if name == "dp" else rule_by_name(name, n)
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        tr = DeviceVit.single_gpu(VIT_B16, B, n, rule, RN_MOMENTUM, inputs=x, labels=y, probe=True)
+        torch.cuda.synchronize()
+        alloc = free0 - torch.cuda.mem_get_info()[0]
+        tr.set_params(init, -1)
+        for t in range(warmup):
+            tr.step(perms[t], RN_LR)
+        tr.sync()
+        with ClockSampler(0) as clk:
+            for k in range(steps):
+                tr.flush_l2()
+                tr.mark(2 * k)
+                tr.step(perms[warmup + k], RN_LR)
+                tr.mark(2 * k + 1)
+            tr.sync()
+        ms = float(np.mean([tr.elapsed(2 * k, 2 * k + 1) for k in range(steps)]))
+        losses, flags = tr.history(warmup + steps)
+        assert np.all(np.isfinite(losses)) and not flags.any(), "non-finite ViT step"
+        st = tr.stats()
+        plan_peak = tr.plan.peak_bytes(st["record_bytes"])
+        assert st["live_record_high_water_bytes"] == plan_peak, (st, plan_peak)
+        r = {"value": round(n * B / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3),
+             "peak_activation_bytes": st["live_record_high_water_bytes"],
+             "activation_record_pool_bytes": st["activation_bytes"], "record_slots": st["record_slots"],
+             "record_bytes": st["record_bytes"], "trainer_device_bytes_allocated": int(alloc),
+             "gpu_launches": st["kernels_per_step"] * steps, "clocks": clk.summary(),
+             "tensor_tflops_per_s": round(st["tensor_flops_per_step"] / (ms / 1e3) / 1e12, 1)}
+        if profile and name == "cdp-v2":
+            ops = tr.profile_step(perms[warmup + steps], RN_LR, serial=True)
+            agg = kernel_table(ops)
+            tot = sum(a[1] for a in agg.values())
+            gemm = {k: a for k, a in agg.items() if a[2] > 0}
+            dom = max(gemm, key=lambda k: gemm[k][1])
+            d = gemm[dom]
+            peak, src = peak_tensor()
+            achieved = d[2] / (d[1] / 1e3) / 1e12
+            r["roofline"] = {"bound": "tensor", "kernel": f"{dom} ({d[0]} launches)", "achieved": round(achieved, 1),
+                             "peak": peak, "peak_source": src, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                             "share_of_serial_step": round(d[1] / tot, 3)}
+            r["kernel_breakdown"] = {
+                k: {"launches": a[0], "ms": round(a[1], 3), "share": round(a[1] / tot, 3),
+                    **({"tflops": round(a[2] / (a[1] / 1e3) / 1e12, 1)} if a[2] else
+                       {"gbs": round(a[3] / (a[1] / 1e3) / 1e9, 1)})}
+                for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])[:16]}
+        tr.close()
+        res[name] = r
+    c, d = res["cdp-v2"], res["dp"]
+    return {"workload": f"configs[3]: ViT-B/16 224x224, {n} sequential micro-batches of {B} on one GPU "
+                        f"({n} stages, block-aligned), cdp-v2 vs dp, bf16 operands, fp32 master / momentum",
+            "value": c["value"], "unit": UNIT, "ms_per_step": c["ms_per_step"], "cdp_v2": c, "dp": d,
+            "peak_activation_cdp_over_dp": round(c["peak_activation_bytes"] / d["peak_activation_bytes"], 4),
+            "expected_ratio_ref_costs_py": round((n + 1) / (2 * n), 4),
+            "allocated_cdp_over_dp": round(c["trainer_device_bytes_allocated"] / d["trainer_device_bytes_allocated"], 4)}
 
 
 def cpu_resnet_reference(model, ws, rule, sample_images, steps, threads):
@@ -596,7 +716,7 @@ def main_resnet(args, ws, rank, local):
     res = run_resnet(args, ws, rank, local, model, args.steps, args.warmup)
     if rank != 0:
         return None
-    peak_note = "configs[1]" if model == "resnet18" else "configs[2] shape"
+    peak_note = "configs[1]" if model == "resnet18" else "configs[2] (north-star target; N GPUs = N stages)"
     out = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
@@ -614,6 +734,7 @@ def main_resnet(args, ws, rank, local):
         "activation_bytes": res["activation_bytes"], "tensor_tflops_per_s": res["tensor_tflops_per_s"],
         "clocks": res["clocks"], "kernel_breakdown": res["kernel_breakdown"],
         "serial_step_ms": res["serial_step_ms"], "losses_first_last": res["losses_first_last"],
+        "exposed_comm": res.get("exposed_comm"), "p2p": res.get("p2p"),
     }
     if args.zero and ws > 1:
         out["zero_cdp"] = {"state_bytes_received_per_step_rank0": res["zero_state_bytes_per_step"],
@@ -664,7 +785,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--rule", default="cdp-v2", choices=["cdp-v2", "cdp-v1", "dp", "dp-allreduce"])
-    ap.add_argument("--model", default="resnet18", choices=["resnet18", "resnet50", "vit_b16", "mlp"])
+    ap.add_argument("--model", default="resnet50", choices=["resnet18", "resnet50", "vit_b16", "mlp"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the resnet50 / config-1 sub-lines at N=1")
     ap.add_argument("--zero", action="store_true", help="ZeRO-CDP state passing (ResNets, N > 1)")
@@ -705,20 +826,22 @@ def main():
         out = main_resnet(args, ws, rank, local)
         if rank == 0:
             if ws == 1 and not args.no_extras:
-                if args.model == "resnet18":
-                    r50 = run_resnet(args, 1, 0, local, "resnet50", 10, 3, e2e=False)
-                    out["resnet50"] = {"workload": resnet_workload("resnet50", 1, args.rule, args.dtype),
-                                       "value": r50["value"], "unit": UNIT, "ms_per_step": r50["ms_per_step"],
-                                       "tensor_tflops_per_s": r50["tensor_tflops_per_s"],
-                                       "roofline": r50["roofline"], "activation_bytes": r50["activation_bytes"],
-                                       "clocks": r50["clocks"], "kernel_breakdown": r50["kernel_breakdown"]}
-                    vit = run_resnet(args, 1, 0, local, "vit_b16", 10, 3, e2e=False)
-                    out["vit_b16"] = {"workload": resnet_workload("vit_b16", 1, args.rule, "bf16"),
-                                      "value": vit["value"], "unit": UNIT, "ms_per_step": vit["ms_per_step"],
-                                      "tensor_tflops_per_s": vit["tensor_tflops_per_s"], "roofline": vit["roofline"],
-                                      "activation_bytes": vit["activation_bytes"],
-                                      "single_gpu_cdp_activation_model": vit_activation_model(vit),
-                                      "clocks": vit["clocks"], "kernel_breakdown": vit["kernel_breakdown"]}
+                if args.model in ("resnet18", "resnet50"):
+                    other = "resnet18" if args.model == "resnet50" else "resnet50"
+                    r = run_resnet(args, 1, 0, local, other, 20, 5, e2e=True)
+                    out[other] = {"workload": resnet_workload(other, 1, args.rule, args.dtype),
+                                  "baseline_config": "configs[1]" if other == "resnet18" else "configs[2]",
+                                  "value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
+                                  "e2e": r["e2e"], "tensor_tflops_per_s": r["tensor_tflops_per_s"],
+                                  "roofline": r["roofline"], "activation_bytes": r["activation_bytes"],
+                                  "clocks": r["clocks"], "kernel_breakdown": r["kernel_breakdown"]}
+                out["vit_b16_single_gpu_cdp"] = vit_single_gpu(4, 5, 3, profile=True)
+                v12 = vit_single_gpu(12, 3, 2)
+                out["vit_b16_single_gpu_cdp_n12"] = {k: v12[k] for k in (
+                    "workload", "value", "unit", "ms_per_step", "peak_activation_cdp_over_dp",
+                    "expected_ratio_ref_costs_py", "allocated_cdp_over_dp")}
+                out["vit_b16_single_gpu_cdp_n12"]["peak_activation_bytes"] = {
+                    "cdp_v2": v12["cdp_v2"]["peak_activation_bytes"], "dp": v12["dp"]["peak_activation_bytes"]}
                 out["single_gpu_cdp"] = single_gpu_config1(args.dtype)
             if ws == 1 and not args.no_cpu_baseline:
                 threads = os.cpu_count() or 1
