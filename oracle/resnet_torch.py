@@ -177,22 +177,34 @@ def grads_flat(model: TorchResNet, specs) -> list:
 class ResNetOracle:
     """value + per-tensor gradients of one micro-batch, float64 on the CPU."""
 
-    def __init__(self, widths, depths, specs, block="basic", stem="cifar", classes=10):
-        self.model = TorchResNet(widths, depths, classes, block, stem).double()
+    def __init__(self, widths, depths, specs, block="basic", stem="cifar", classes=10, dtype=torch.float64):
+        # dtype "bf16-autocast": float32 model under torch.autocast(bfloat16) (bf16 conv / linear
+        # operands and outputs, float32 batch norm) — torch's own bf16 training step
+        self.autocast = dtype == "bf16-autocast"
+        if self.autocast:
+            dtype = torch.float32
+        self.model = TorchResNet(widths, depths, classes, block, stem).to(dtype)
+        self.dtype = dtype
         self.specs = specs
 
     def loss_and_grads(self, params, x, y, kinks=None):
         load_flat(self.model, np.concatenate(params), self.specs)
         self.model.zero_grad(set_to_none=True)
-        xt = torch.from_numpy(np.ascontiguousarray(np.asarray(x, np.float64).transpose(0, 3, 1, 2)))
-        loss = F.cross_entropy(self.model(xt, kinks), torch.from_numpy(np.asarray(y, np.int64)))
+        xt = torch.from_numpy(np.ascontiguousarray(np.asarray(x, np.float64).transpose(0, 3, 1, 2))).to(self.dtype)
+        with torch.autocast("cpu", dtype=torch.bfloat16, enabled=self.autocast):
+            z = self.model(xt, kinks)
+        loss = F.cross_entropy(z.to(self.dtype), torch.from_numpy(np.asarray(y, np.int64)))
         loss.backward()
         return float(loss.item()), grads_flat(self.model, self.specs)
 
 
 def run_cdp(widths, depths, init, inputs, labels, n_workers, micro_batch, perms, lr, momentum, fresh_tensor,
-            block="basic", stem="cifar", classes=10, weight_decay=0.0, kinks=None, stats=None):
+            block="basic", stem="cifar", classes=10, weight_decay=0.0, kinks=None, stats=None, dtype=None):
     """`steps = len(perms)` CDP steps from `init` (flat); fresh_tensor = N x n_tensors table (None = DP).
+
+    dtype: the per-micro-batch forward / backward arithmetic (default float64; torch.float32 gives torch's
+    own fp32 step, "bf16-autocast" its bf16 autocast step — the yardsticks for the device's fp32 / bf16
+    tolerances at deep configurations); the accumulation and update stay float64 (oracle/engine.advance).
 
     kinks: optional kinks[t-1][i-1] -> Kinks (the device's branch decisions of worker i at step t);
     stats: optional dict, receives "kink_overrides" (elements where they were used)."""
@@ -201,7 +213,7 @@ def run_cdp(widths, depths, init, inputs, labels, n_workers, micro_batch, perms,
 
     hw = int(np.asarray(inputs).shape[1])
     specs = layer_specs(widths, depths, 3, hw, block, stem, classes)
-    orc = ResNetOracle(widths, depths, specs, block, stem, classes)
+    orc = ResNetOracle(widths, depths, specs, block, stem, classes, dtype or torch.float64)
     cur = [a.copy() for a in flat_to_tensors(np.asarray(init, np.float64), specs)]
     prev = [a.copy() for a in cur]
     vel = [np.zeros_like(a) for a in cur] if momentum else None

@@ -83,3 +83,18 @@ def test_vit_197_tokens_vs_restatement(cuda):
     init, x, y, perms, losses, final, stage = _run(1, None, 2, cfg=CFG197, mb=2)
     want, wl = _oracle(init, x, y, perms, 1, None, stage, cfg=CFG197, mb=2)
     _check(init, losses, final, want, wl)
+
+
+VITB16 = dict(image=224, patch=16, dim=768, depth=12, heads=12, mlp=3072, classes=1000)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_vit_b16_bench_shape_vs_restatement(cuda, world):
+    """Full ViT-B/16 (224x224, 197 tokens, 12 x 768 / 12 heads / 3072, 1000 classes; BASELINE configs[3]'s
+    shape at B = 2) against the float64 restatement: one rank, and two CDP-v2 ranks."""
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = rule_by_name("cdp-v2", world) if world > 1 else None
+    init, x, y, perms, losses, final, stage = _run(world, rule, 2, cfg=VITB16, mb=2)
+    want, wl = _oracle(init, x, y, perms, world, rule, stage, cfg=VITB16, mb=2)
+    _check(init, losses, final, want, wl)
