@@ -121,8 +121,12 @@ __device__ __forceinline__ F8 ld_c8(const CTensor &t, size_t i) {
 }
 template <int KIND>
 __device__ __forceinline__ void st_c8(const CTensor &t, size_t i, const F8 &a) {
-    store_wc4<KIND>(t, i, make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
-    store_wc4<KIND>(t, i + 4, make_float4(a.v[4], a.v[5], a.v[6], a.v[7]));
+    if constexpr (KIND == 0) {  // one 16-byte store (i is a multiple of 8 at every call site)
+        *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(t.hi) + i) = f8_to_bf16x8(a);
+    } else {
+        store_wc4<KIND>(t, i, make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
+        store_wc4<KIND>(t, i + 4, make_float4(a.v[4], a.v[5], a.v[6], a.v[7]));
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -157,6 +161,57 @@ static __global__ void stem_im2col_kernel(const float *__restrict__ data, const 
         const size_t o = size_t(p) * cols.ld + k0;
         store_wc4<KIND>(cols, o, make_float4(v[0], v[1], v[2], v[3]));
         store_wc4<KIND>(cols, o + 4, make_float4(v[4], v[5], v[6], v[7]));
+    }
+}
+
+// Row-staged stem im2col: one CTA per (image, output row).  The R input rows the
+// output row reads (zero-padded left / right / outside the image) are staged in
+// shared memory with coalesced loads; a per-column offset table (k -> (r, s*C + c))
+// turns the gather into one shared-memory read per element; the CTA's output rows
+// form one contiguous [Wo][ld] block written with coalesced 16-byte stores.  (The
+// per-element version: 0.57 ms, 0.9 TB/s, for the 514 MB ImageNet-stem record.)
+// Requires (W + 2 pad) * C * R floats + ld ints of shared memory (dynamic).
+template <int KIND, int R, int C>
+static __global__ void __launch_bounds__(256) stem_im2col_rows_kernel(const float *__restrict__ data, const int *perm,
+                                                                       int H, int W, int stride, int pad, int Ho,
+                                                                       int Wo, CTensor cols) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    extern __shared__ float sm_rows[];
+    constexpr int S = R, K = R * S * C;
+    const int Wp = W + 2 * pad;
+    const int rowlen = Wp * C;
+    int *koff = reinterpret_cast<int *>(sm_rows + R * rowlen);
+    const int ho = blockIdx.x % Ho, b = blockIdx.x / Ho;
+    const float *img = data + size_t(__ldg(perm + b)) * H * W * C;
+    for (int k = threadIdx.x; k < cols.ld; k += blockDim.x) {
+        if (k < K) {
+            const int r = k / (S * C), rem = k - r * (S * C);
+            koff[k] = r * rowlen + rem;
+        } else {
+            koff[k] = -1;
+        }
+    }
+    for (int i = threadIdx.x; i < R * rowlen; i += blockDim.x) {
+        const int r = i / rowlen, q = i - r * rowlen;
+        const int h = ho * stride - pad + r, w = q / C - pad;
+        float x = 0.f;
+        if (h >= 0 && h < H && w >= 0 && w < W) x = __ldg(img + (size_t(h) * W + w) * C + (q - (q / C) * C));
+        sm_rows[i] = x;
+    }
+    __syncthreads();
+    const int G = cols.ld / 8;
+    const size_t row0 = (size_t(b) * Ho + ho) * Wo;
+    for (int e = threadIdx.x; e < Wo * G; e += blockDim.x) {
+        const int wo = e / G, k0 = (e - wo * G) * 8;
+        const int base = wo * stride * C;
+        F8 v;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int o = koff[k0 + j];
+            v.v[j] = o >= 0 ? sm_rows[o + base] : 0.f;
+        }
+        st_c8<KIND>(cols, (row0 + wo) * cols.ld + k0, v);
     }
 }
 
@@ -418,6 +473,69 @@ struct EpiConvOut2 {
     __device__ static void done(const Params &, int, unsigned) {}
 };
 
+// Direct epilogue of the bf16 residual-gradient add (the ResNet block-input data gradient,
+// out may alias add): EpiConvOut2's output rows with `add` (and `add_mask`), no statistics,
+// no split-K.  gemm_pk_kernel instantiates ONLY the direct path for it (kDirect): each drained
+// accumulator row (lane = row, 16 columns per step) is combined with its own row's residual /
+// mask and stored from registers — no shared tile, no second pass over the tile.  (In the
+// general epilogue the shared-tile round trip plus the dependent residual loads made the 1x1
+// data gradients of ResNet-50 run at 1.9 TB/s; a direct branch inside the general kernel
+// spills: its own instantiation keeps the register budget.)
+template <int KIND>
+struct EpiConvAdd : EpiConvOut2<KIND> {
+    using Params = typename EpiConvOut2<KIND>::Params;
+    static constexpr bool kDirect = true;
+    static constexpr bool kTmaStore = false;
+    static constexpr bool kNoSplit = true;
+    static bool eligible(const Params &p, int N, int BN) {
+        return KIND == 0 && p.add && !p.stats && !p.out_f32 && !p.gelu_z && !p.gelu_out.hi && (p.ld % 8) == 0 &&
+               N % BN == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
+    }
+    // Direct epilogue (bf16 residual-gradient add: the ResNet block-input data gradient, out may
+    // alias add): the drained accumulator row (lane = row, 32 columns) is combined with its own
+    // row's residual (and mask) and stored from registers — no shared tile, no second pass.  The
+    // row's 64-byte residual / mask segments are loaded before the TMEM read (eight 16-byte loads
+    // in flight per thread): with K = 64..512 this epilogue has almost no MMA work to hide behind,
+    // and its L2 round trips were the kernel (1.9 TB/s in the shared-tile path).
+    // 16 columns per call (two 16-byte vectors of residual and mask per thread in flight)
+    struct DirectPre {
+        uint4 a[2], m[2];
+    };
+    __device__ static void direct_load(const Params &p, int m, int col, int64_t off, DirectPre &d) {
+        if (m < 0) return;
+        const size_t o = size_t(off) + size_t(m) * p.ld + col;
+        const uint4 *pa = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.add) + o);
+        d.a[0] = pa[0];
+        d.a[1] = pa[1];
+        if (p.add_mask.hi) {
+            const uint4 *pm = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.add_mask.hi) + o);
+            d.m[0] = pm[0];
+            d.m[1] = pm[1];
+        }
+    }
+    __device__ static void direct_store(const Params &p, int m, int col, int64_t off, const DirectPre &d,
+                                        const float (&v)[16]) {
+        if (m < 0) return;
+        const size_t o = size_t(off) + size_t(m) * p.ld + col;
+        uint4 *po = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + o);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            F8 a, x;
+            bf16x8_to_f8(d.a[i], a);
+            if (p.add_mask.hi) {
+                F8 mk;
+                bf16x8_to_f8(d.m[i], mk);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x.v[k] = v[8 * i + k] + (mk.v[k] > 0.f ? a.v[k] : 0.f);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x.v[k] = v[8 * i + k] + a.v[k];
+            }
+            po[i] = f8_to_bf16x8(x);
+        }
+    }
+};
+
 // Weight gradient fused with the CDP hop / SGD update (same modes, arithmetic
 // and ring protocol as EpiWgrad; the pre-hop waits run in hop_wait_kernel).
 template <int KIND>
@@ -587,27 +705,57 @@ struct BnResidual {
     const float *mean, *rstd, *gamma, *beta;
 };
 
-// One thread keeps its 8 channels for the whole grid-stride loop when the stride is a
-// multiple of C/8 (always, for 256-thread blocks and C <= 2048): the per-channel
-// parameters are loaded once instead of per element.
+// Per-channel affine of the normalisation for 8 channels.  bf16 mode: y_hat * gamma + beta
+// = x * a + b with a = gamma * rstd, b = beta - mean * a (one FMA per element, 16 registers;
+// the bf16 input has far less precision than the fp32 rounding of b).  fp32 (3xTF32 parity)
+// mode keeps gamma * ((x - mean) * rstd) + beta exactly as the restatement computes it.
 template <int KIND>
-__device__ __forceinline__ void bn_apply_elem(const void *__restrict__ y, size_t o, const F8 &mu, const F8 &rs,
-                                              const F8 &ga, const F8 &be, const BnResidual &res, const F8 &m2,
-                                              const F8 &r2, const F8 &g2, const F8 &b2, int relu, CTensor out) {
-    const F8 x = ld_y8<KIND>(y, o);
-    F8 ra, rx;
-    if (res.act.hi) ra = ld_c8<KIND>(res.act, o);
-    if (res.y) rx = ld_y8<KIND>(res.y, o);
-    F8 v;
+struct BnAff {
+    F8 a, b, g, e;  // KIND 0: a, b; KIND 1: a = mean, b = rstd, g = gamma, e = beta
+    __device__ __forceinline__ void load(const float *mean, const float *rstd, const float *gamma, const float *beta,
+                                         int c) {
+        if constexpr (KIND == 0) {
+            const F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), be = ld_f8(beta, c);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v.v[k] = ga.v[k] * ((x.v[k] - mu.v[k]) * rs.v[k]) + be.v[k];
-    if (res.act.hi) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v.v[k] += ra.v[k];
+            for (int k = 0; k < 8; ++k) {
+                a.v[k] = ga.v[k] * rs.v[k];
+                b.v[k] = fmaf(-mu.v[k], a.v[k], be.v[k]);
+            }
+        } else {
+            a = ld_f8(mean, c);
+            b = ld_f8(rstd, c);
+            g = ld_f8(gamma, c);
+            e = ld_f8(beta, c);
+        }
     }
-    if (res.y) {
+    __device__ __forceinline__ float operator()(float x, int k) const {
+        if constexpr (KIND == 0)
+            return fmaf(x, a.v[k], b.v[k]);
+        else
+            return g.v[k] * ((x - a.v[k]) * b.v[k]) + e.v[k];
+    }
+};
+
+// RES: 0 none, 1 identity shortcut (compute-format act), 2 projection shortcut (a second
+// BN-normalised conv output).  One thread keeps its 8 channels (their coefficients in
+// registers) for the whole grid-stride loop when the stride is a multiple of C/8 (always,
+// for 256-thread blocks and C <= 2048); two vectors per iteration in flight.  The
+// residual kinds are separate instantiations so the plain one keeps its registers low
+// (occupancy: the generic version held 96 registers, 2 blocks / SM, 3 TB/s).
+template <int KIND, int RES>
+__device__ __forceinline__ void bn_apply_vec(const void *__restrict__ y, size_t o, const BnAff<KIND> &f,
+                                             const BnResidual &res, const BnAff<KIND> &f2, int relu, CTensor out) {
+    F8 v = ld_y8<KIND>(y, o);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v.v[k] += g2.v[k] * ((rx.v[k] - m2.v[k]) * r2.v[k]) + b2.v[k];
+    for (int k = 0; k < 8; ++k) v.v[k] = f(v.v[k], k);
+    if constexpr (RES == 1) {
+        const F8 r = ld_c8<KIND>(res.act, o);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v.v[k] += r.v[k];
+    } else if constexpr (RES == 2) {
+        const F8 r = ld_y8<KIND>(res.y, o);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v.v[k] += f2(r.v[k], k);
     }
     if (relu) {
 #pragma unroll
@@ -616,40 +764,31 @@ __device__ __forceinline__ void bn_apply_elem(const void *__restrict__ y, size_t
     st_c8<KIND>(out, o, v);
 }
 
-template <int KIND>
-static __global__ void bn_apply_kernel(const void *__restrict__ y, int64_t P, int C, const float *mean, const float *rstd,
-                                const float *gamma, const float *beta, BnResidual res, int relu, CTensor out) {
+template <int KIND, int RES>
+static __global__ void __launch_bounds__(256) bn_apply_kernel(const void *__restrict__ y, int64_t P, int C,
+                                                              const float *mean, const float *rstd,
+                                                              const float *gamma, const float *beta, BnResidual res,
+                                                              int relu, CTensor out) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int C8 = C / 8;
     const int64_t n = P * C8;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (stride % C8 == 0) {
-        const int c = int(i % C8) * 8;
-        const F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), be = ld_f8(beta, c);
-        F8 m2{}, r2{}, g2{}, b2{};
-        if (res.y) {
-            m2 = ld_f8(res.mean, c);
-            r2 = ld_f8(res.rstd, c);
-            g2 = ld_f8(res.gamma, c);
-            b2 = ld_f8(res.beta, c);
-        }
+    const bool fixed = stride % C8 == 0;
+    BnAff<KIND> f, f2;
+    f.load(mean, rstd, gamma, beta, int(i % C8) * 8);
+    if constexpr (RES == 2) f2.load(res.mean, res.rstd, res.gamma, res.beta, int(i % C8) * 8);
+    if (fixed) {
 #pragma unroll 2
-        for (; i < n; i += stride) bn_apply_elem<KIND>(y, size_t(i) * 8, mu, rs, ga, be, res, m2, r2, g2, b2, relu, out);
+        for (; i < n; i += stride) bn_apply_vec<KIND, RES>(y, size_t(i) * 8, f, res, f2, relu, out);
         return;
     }
     for (; i < n; i += stride) {
         const int c = int(i % C8) * 8;
-        F8 m2{}, r2{}, g2{}, b2{};
-        if (res.y) {
-            m2 = ld_f8(res.mean, c);
-            r2 = ld_f8(res.rstd, c);
-            g2 = ld_f8(res.gamma, c);
-            b2 = ld_f8(res.beta, c);
-        }
-        bn_apply_elem<KIND>(y, size_t(i) * 8, ld_f8(mean, c), ld_f8(rstd, c), ld_f8(gamma, c), ld_f8(beta, c), res, m2,
-                            r2, g2, b2, relu, out);
+        f.load(mean, rstd, gamma, beta, c);
+        if constexpr (RES == 2) f2.load(res.mean, res.rstd, res.gamma, res.beta, c);
+        bn_apply_vec<KIND, RES>(y, size_t(i) * 8, f, res, f2, relu, out);
     }
 }
 
@@ -767,40 +906,69 @@ static __global__ void bn_finalize_bwd_kernel(const double *__restrict__ partial
 }
 
 // Backward through BN (+ReLU mask): dx = gamma * rstd * (g' - dbeta/P - xhat * dgamma/P)
-// in compute format (the conv's output gradient, a GEMM operand).
+// in compute format (the conv's output gradient, a GEMM operand).  bf16 mode: per channel
+// the thread keeps mean, k1 = gamma * rstd, k2 = dbeta / P, k3 = rstd * dgamma / P and
+// computes dx = k1 * (g' - k2 - (x - mean) * k3) (32 coefficient registers instead of 40);
+// fp32 (parity) mode keeps the restatement's evaluation order.
 template <int KIND>
-static __global__ void bn_bwd_apply_kernel(const void *__restrict__ g, CTensor mask, const void *__restrict__ y, int64_t P,
-                                    int C, const float *mean, const float *rstd, const float *gamma,
-                                    const float *dbeta, const float *dgamma, CTensor dx) {
+struct BnBwd {
+    F8 mu, k1, k2, k3, k4;  // KIND 1: k1 = rstd, k2 = gamma, k3 = dbeta, k4 = dgamma
+    float inv;
+    __device__ __forceinline__ void load(const float *mean, const float *rstd, const float *gamma,
+                                         const float *dbeta, const float *dgamma, int c) {
+        mu = ld_f8(mean, c);
+        if constexpr (KIND == 0) {
+            const F8 rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), db = ld_f8(dbeta, c), dg = ld_f8(dgamma, c);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                k1.v[k] = ga.v[k] * rs.v[k];
+                k2.v[k] = db.v[k] * inv;
+                k3.v[k] = rs.v[k] * (dg.v[k] * inv);
+            }
+        } else {
+            k1 = ld_f8(rstd, c);
+            k2 = ld_f8(gamma, c);
+            k3 = ld_f8(dbeta, c);
+            k4 = ld_f8(dgamma, c);
+        }
+    }
+    __device__ __forceinline__ float operator()(float g, float x, int k) const {
+        if constexpr (KIND == 0)
+            return k1.v[k] * (g - k2.v[k] - (x - mu.v[k]) * k3.v[k]);
+        else
+            return k2.v[k] * k1.v[k] * (g - k3.v[k] * inv - ((x - mu.v[k]) * k1.v[k]) * k4.v[k] * inv);
+    }
+};
+
+template <int KIND, bool MASK>
+static __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const void *__restrict__ g, CTensor mask,
+                                                                  const void *__restrict__ y, int64_t P, int C,
+                                                                  const float *mean, const float *rstd,
+                                                                  const float *gamma, const float *dbeta,
+                                                                  const float *dgamma, CTensor dx) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int C8 = C / 8;
     const int64_t n = P * C8;
-    const float inv = 1.f / float(P);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     const bool fixed = stride % C8 == 0;  // the thread's channels never change (parameters loaded once)
     int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    int c = int(i % C8) * 8;
-    F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c), ga = ld_f8(gamma, c), db = ld_f8(dbeta, c), dg = ld_f8(dgamma, c);
+    BnBwd<KIND> f;
+    f.inv = 1.f / float(P);
+    f.load(mean, rstd, gamma, dbeta, dgamma, int(i % C8) * 8);
+#pragma unroll 2
     for (; i < n; i += stride) {
-        if (!fixed) {
-            c = int(i % C8) * 8;
-            mu = ld_f8(mean, c);
-            rs = ld_f8(rstd, c);
-            ga = ld_f8(gamma, c);
-            db = ld_f8(dbeta, c);
-            dg = ld_f8(dgamma, c);
-        }
+        if (!fixed) f.load(mean, rstd, gamma, dbeta, dgamma, int(i % C8) * 8);
         const size_t o = size_t(i) * 8;
-        F8 gv = ld_y8<KIND>(g, o);
+        const F8 gv = ld_y8<KIND>(g, o);
         const F8 x = ld_y8<KIND>(y, o);
         F8 mk;
-        if (mask.hi) mk = ld_c8<KIND>(mask, o);
+        if constexpr (MASK) mk = ld_c8<KIND>(mask, o);
         F8 d;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const float gk = (mask.hi && !(mk.v[k] > 0.f)) ? 0.f : gv.v[k];
-            d.v[k] = ga.v[k] * rs.v[k] * (gk - db.v[k] * inv - ((x.v[k] - mu.v[k]) * rs.v[k]) * dg.v[k] * inv);
+            const float gk = (MASK && !(mk.v[k] > 0.f)) ? 0.f : gv.v[k];
+            d.v[k] = f(gk, x.v[k], k);
         }
         st_c8<KIND>(dx, o, d);
     }
@@ -810,37 +978,45 @@ static __global__ void bn_bwd_apply_kernel(const void *__restrict__ g, CTensor m
 // Max pool 3x3 / stride 2 / pad 1 (ImageNet stem).  Forward keeps the winning
 // tap (first maximum in (r, s) order) per output element; backward is a
 // deterministic gather over the (at most 4) windows containing an input pixel.
+// 8 channels per thread: 16-byte activation / gradient accesses, 8-byte tap records.
 template <int KIND>
 static __global__ void maxpool_fwd_kernel(CTensor in, int B, int H, int W, int C, int Ho, int Wo, CTensor out,
                                    uint8_t *arg) {
     ptx::griddep_wait();
     ptx::griddep_launch();
-    const int C4 = C / 4;
-    const int64_t n = int64_t(B) * Ho * Wo * C4;
+    const int C8 = C / 8;
+    const int64_t n = int64_t(B) * Ho * Wo * C8;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % C4) * 4;
-        const int p = int(i / C4);
+        const int c = int(i % C8) * 8;
+        const int p = int(i / C8);
         const int wo = p % Wo, t = p / Wo, ho = t % Ho, b = t / Ho;
-        float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        int bt[4] = {0, 0, 0, 0};
+        F8 best;
+        uint8_t bt[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            best.v[j] = -INFINITY;
+            bt[j] = 0;
+        }
         for (int r = 0; r < 3; ++r) {
             const int h = ho * 2 - 1 + r;
             if (h < 0 || h >= H) continue;
             for (int s = 0; s < 3; ++s) {
                 const int w = wo * 2 - 1 + s;
                 if (w < 0 || w >= W) continue;
-                const float4 v = ld_c4<KIND>(in, ((size_t(b) * H + h) * W + w) * in.ld + c);
-                const float vv[4] = {v.x, v.y, v.z, v.w};
+                const F8 v = ld_c8<KIND>(in, ((size_t(b) * H + h) * W + w) * in.ld + c);
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (vv[j] > best[j]) {
-                        best[j] = vv[j];
-                        bt[j] = r * 3 + s;
+                for (int j = 0; j < 8; ++j)
+                    if (v.v[j] > best.v[j]) {
+                        best.v[j] = v.v[j];
+                        bt[j] = uint8_t(r * 3 + s);
                     }
             }
         }
-        store_wc4<KIND>(out, size_t(p) * out.ld + c, make_float4(best[0], best[1], best[2], best[3]));
-        *reinterpret_cast<uchar4 *>(arg + size_t(p) * C + c) = make_uchar4(bt[0], bt[1], bt[2], bt[3]);
+        st_c8<KIND>(out, size_t(p) * out.ld + c, best);
+        uint2 packed;
+        packed.x = uint32_t(bt[0]) | uint32_t(bt[1]) << 8 | uint32_t(bt[2]) << 16 | uint32_t(bt[3]) << 24;
+        packed.y = uint32_t(bt[4]) | uint32_t(bt[5]) << 8 | uint32_t(bt[6]) << 16 | uint32_t(bt[7]) << 24;
+        *reinterpret_cast<uint2 *>(arg + size_t(p) * C + c) = packed;
     }
 }
 
@@ -849,13 +1025,15 @@ static __global__ void maxpool_bwd_kernel(const void *__restrict__ gout, const u
                                    int C, int Ho, int Wo, void *gin) {
     ptx::griddep_wait();
     ptx::griddep_launch();
-    const int C4 = C / 4;
-    const int64_t n = int64_t(B) * H * W * C4;
+    const int C8 = C / 8;
+    const int64_t n = int64_t(B) * H * W * C8;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int c = int(i % C4) * 4;
-        const int p = int(i / C4);
+        const int c = int(i % C8) * 8;
+        const int p = int(i / C8);
         const int w = p % W, t = p / W, h = t % H, b = t / H;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        F8 acc;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc.v[j] = 0.f;
         for (int r = 0; r < 3; ++r) {
             const int hh = h + 1 - r;
             if (hh < 0 || (hh & 1)) continue;
@@ -867,16 +1045,17 @@ static __global__ void maxpool_bwd_kernel(const void *__restrict__ gout, const u
                 const int wo = ww >> 1;
                 if (wo >= Wo) continue;
                 const size_t o = ((size_t(b) * Ho + ho) * Wo + wo) * C + c;
-                const uchar4 a = *reinterpret_cast<const uchar4 *>(arg + o);
-                const float4 g = ld_y4<KIND>(gout, o);
-                const int tap = r * 3 + s;
-                if (a.x == tap) acc.x += g.x;
-                if (a.y == tap) acc.y += g.y;
-                if (a.z == tap) acc.z += g.z;
-                if (a.w == tap) acc.w += g.w;
+                const uint2 a = __ldg(reinterpret_cast<const uint2 *>(arg + o));
+                const F8 g = ld_y8<KIND>(gout, o);
+                const uint32_t tap = uint32_t(r * 3 + s);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t aj = ((j < 4 ? a.x : a.y) >> (8 * (j & 3))) & 0xffu;
+                    if (aj == tap) acc.v[j] += g.v[j];
+                }
             }
         }
-        st_y4<KIND>(gin, size_t(p) * C + c, acc);
+        st_y8<KIND>(gin, size_t(p) * C + c, acc);
     }
 }
 

@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "gemm.cuh"
 #include "host.h"
@@ -52,6 +53,12 @@ struct PkArgs {
     int nph;
     ConvGeom cvp[4];
 };
+
+// Epilogues with a direct (register-only) path declare kDirect (EpiConvOut2 bf16).
+template <class E, class = void>
+struct pk_direct : std::false_type {};
+template <class E>
+struct pk_direct<E, std::void_t<decltype(E::kDirect)>> : std::bool_constant<E::kDirect> {};
 
 __device__ __forceinline__ const ConvGeom &pk_geom(const PkArgs &a, int g) { return a.nph > 1 ? a.cvp[g] : a.cv; }
 
@@ -399,6 +406,25 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     continue;
                 }
             }
+            if constexpr (pk_direct<Epi>::value) {  // the only epilogue of this instantiation (no split)
+                const int row_m = pk_row_m(args, tm, row, g);
+#pragma unroll 1
+                for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+#pragma unroll 1
+                    for (int c = half * HC; c < (half + 1) * HC; c += 16) {
+                        const int col = tn * BN + h * C::EPI_COLS + c;
+                        typename Epi::DirectPre dp;
+                        Epi::direct_load(ep, row_m, col, out_off, dp);
+                        float v[16];
+                        ptx::tmem_ld16(taddr + h * C::EPI_COLS + c, v);
+                        Epi::direct_store(ep, row_m, col, out_off, dp, v);
+                    }
+                }
+                ptx::tc_fence_before();
+                pk_bar(1, kPkEpi);
+                if (tid == 0) ptx::mbar_arrive(&tempty[acc]);  // accumulator free
+                continue;
+            } else {
 #pragma unroll 1
             for (int h = 0; h < BN / C::EPI_COLS; ++h) {
                 const int row_m = pk_row_m(args, tm, row, g);  // own computation: rowm is not yet synced
@@ -438,6 +464,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 pk_bar(1, kPkEpi);  // shared tile reused by the next pass / unit
             }
             if (!split) Epi::template done<kPkEpi>(ep, tid, unsigned(args.tiles_m * args.tiles_n));
+            }
         }
         if constexpr (Epi::kTmaStore)
             if (tid == 0) ptx::bulk_wait0();  // TMA stores complete before the CTA exits

@@ -502,7 +502,7 @@ struct ResNetTrainer {
         }
         const int tiles = a.tiles_m * a.tiles_n * nph;
         int splits = 1;
-        if (tiles < sms() && nph == 1)
+        if (tiles < sms() && nph == 1 && !pk_direct<Epi>::value)
             splits = std::max(1, std::min(sms() / tiles, a.total_iters / split_min_kb()));  // units <= one wave
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
         if (K == 1 && nph == 1) {
@@ -541,7 +541,7 @@ struct ResNetTrainer {
         last_stat_slots = a.splits > 1 ? a.tiles_m * slots_per_tile : grid;  // EpiConvOut2 statistics rows
         last_grid = grid;
         L(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
-        if (a.splits > 1) {
+        if constexpr (!pk_direct<Epi>::value) if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
             constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
             constexpr int CC = 64;
@@ -701,9 +701,10 @@ struct ResNetTrainer {
         if (res_ci >= 0) rec(convs[res_ci].tb, A_FWD, 0, res_slot, s);
         const double bytes = double(c.P) * c.cout * (ysz() + esz() + (res.act.hi ? esz() : res.y ? ysz() : 0));
         L("bn_apply", 0, bytes, s, [&] {
-            launch_pdl(bn_apply_kernel<K>, dim3(blocks_for(c.P * c.cout / 8)), dim3(256), 0, s, (const void *)c.y.p,
-                       c.P, c.cout, (const float *)c.mean.as<float>(), (const float *)c.rstd.as<float>(),
-                       gamma(ci, vslot), beta(ci, vslot), res, 1, out);
+            auto kern = res.act.hi ? bn_apply_kernel<K, 1> : res.y ? bn_apply_kernel<K, 2> : bn_apply_kernel<K, 0>;
+            launch_pdl(kern, dim3(blocks_for(c.P * c.cout / 8)), dim3(256), 0, s, (const void *)c.y.p, c.P, c.cout,
+                       (const float *)c.mean.as<float>(), (const float *)c.rstd.as<float>(), gamma(ci, vslot),
+                       beta(ci, vslot), res, 1, out);
         });
         rec(c.tb, A_FWD, 1, vslot, s);
         if (res_ci >= 0) rec(convs[res_ci].tb, A_FWD, 1, res_slot, s);
@@ -713,15 +714,16 @@ struct ResNetTrainer {
     void forward(int p, cudaStream_t s, const std::function<void(int)> &pull) {
         ConvL &c0 = convs[stem];
         L("stem_im2col", 0, double(c0.P) * cols.ld * esz(), s, [&] {
-            const int64_t n = c0.P * (cols.ld / 8);
+            const size_t smem = size_t(c0.R) * (Win + 2 * c0.pad) * Cin0 * 4 + size_t(cols.ld) * 4;
+            CDP_REQUIRE(smem <= 48 * 1024, "stem input rows exceed the shared-memory stage");
             if (c0.R == 3)
-                launch_pdl(stem_im2col_kernel<K, 3, 3>, dim3(blocks_for(n)), dim3(256), 0, s,
+                launch_pdl(stem_im2col_rows_kernel<K, 3, 3>, dim3(B * c0.Ho), dim3(256), smem, s,
                            (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), Hin, Win, c0.stride,
-                           c0.pad, c0.Ho, c0.Wo, int(c0.P), cols.view());
+                           c0.pad, c0.Ho, c0.Wo, cols.view());
             else
-                launch_pdl(stem_im2col_kernel<K, 7, 3>, dim3(blocks_for(n)), dim3(256), 0, s,
+                launch_pdl(stem_im2col_rows_kernel<K, 7, 3>, dim3(B * c0.Ho), dim3(256), smem, s,
                            (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), Hin, Win, c0.stride,
-                           c0.pad, c0.Ho, c0.Wo, int(c0.P), cols.view());
+                           c0.pad, c0.Ho, c0.Wo, cols.view());
         });
         pull(c0.tw);
         pull(c0.tb);
@@ -732,7 +734,7 @@ struct ResNetTrainer {
         if (pool_act >= 0) {
             const int a = stem_act, o = pool_act;
             L("maxpool_fwd", 0, double(act_P[a] + act_P[o]) * act_C[a] * esz(), s, [&] {
-                launch_pdl(maxpool_fwd_kernel<K>, dim3(blocks_for(act_P[o] * act_C[o] / 4)), dim3(256), 0, s,
+                launch_pdl(maxpool_fwd_kernel<K>, dim3(blocks_for(act_P[o] * act_C[o] / 8)), dim3(256), 0, s,
                            acts[a].view(), B, act_H[a], act_W[a], act_C[a], act_H[o], act_W[o], acts[o].view(),
                            pool_arg.as<uint8_t>());
             });
@@ -828,7 +830,8 @@ struct ResNetTrainer {
         const int vslot = vs(cc.tb, p);
         rec(cc.tb, A_BWD, 0, vslot, s);
         L("bn_bwd_apply", 0, double(cc.P) * cc.cout * (2 * ysz() + 2 * esz()), s, [&] {
-            launch_pdl(bn_bwd_apply_kernel<K>, dim3(blocks_for(cc.P * cc.cout / 8)), dim3(256), 0, s, g, mask,
+            launch_pdl(mask.hi ? bn_bwd_apply_kernel<K, true> : bn_bwd_apply_kernel<K, false>,
+                       dim3(blocks_for(cc.P * cc.cout / 8)), dim3(256), 0, s, g, mask,
                        (const void *)cc.y.p, cc.P, cc.cout, (const float *)cc.mean.as<float>(),
                        (const float *)cc.rstd.as<float>(), gamma(ci, vslot), (const float *)cc.dbeta.as<float>(),
                        (const float *)cc.dgamma.as<float>(), cc.dy.view());
@@ -836,6 +839,12 @@ struct ResNetTrainer {
         rec(cc.tb, A_BWD, 1, vslot, s);
     }
 
+    template <class P>
+    static P ep_with(P ep, void *out, int ld) {
+        ep.out = out;
+        ep.ld = ld;
+        return ep;
+    }
     // conv data gradient into g_in (fp32 [Pin][cin]).
     // add != null: g_in = dgrad + (add masked by add_mask) (the block's residual branch).
     template <int K>
@@ -849,15 +858,25 @@ struct ResNetTrainer {
         ep.stats = nullptr;
         ep.add = add;
         ep.add_mask = add_mask;
+        // residual-gradient add: the direct (register) epilogue, its own GEMM instantiation
+        const bool direct = EpiConvAdd<K>::eligible(ep_with(ep, g_in, c.cin), c.cin, tile_n(c.cin)) &&
+                            std::getenv("CDP_NO_DIRECT_ADD") == nullptr;
         if (c.impl == CI_PLAIN) {
             ep.out = g_in;
             ep.ld = c.cin;
-            pk_plain<K, false, false, EpiConvOut2<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(), c.P,
-                                                      c.cin, c.cout, ep, s, false);
+            if (direct)
+                pk_plain<K, false, false, EpiConvAdd<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(), c.P,
+                                                         c.cin, c.cout, ep, s, false);
+            else
+                pk_plain<K, false, false, EpiConvOut2<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(),
+                                                          c.P, c.cin, c.cout, ep, s, false);
         } else if (c.stride == 1) {
             ep.out = g_in;
             ep.ld = c.cin;
-            pk_conv<K, GM_DGRAD, EpiConvOut2<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
+            if (direct)
+                pk_conv<K, GM_DGRAD, EpiConvAdd<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
+            else
+                pk_conv<K, GM_DGRAD, EpiConvOut2<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
         } else {
             // stride 2: four sub-pixel phases, each a stride-1 implicit GEMM over dy with its own taps
             // (pixels (2i + ph, 2j + pw)); phases without taps (1x1 convs) leave zeros
@@ -1175,7 +1194,7 @@ struct ResNetTrainer {
             const int a = stem_act, o = pool_act;
             L("maxpool_bwd", 0, double(act_P[o]) * act_C[o] * (1 + ysz()) + double(act_P[a]) * act_C[a] * ysz(), cs,
               [&] {
-                launch_pdl(maxpool_bwd_kernel<K>, dim3(blocks_for(act_P[a] * act_C[a] / 4)), dim3(256), 0, cs,
+                launch_pdl(maxpool_bwd_kernel<K>, dim3(blocks_for(act_P[a] * act_C[a] / 8)), dim3(256), 0, cs,
                            (const void *)G0, (const uint8_t *)pool_arg.as<uint8_t>(), B, act_H[a], act_W[a],
                            act_C[a], act_H[o], act_W[o], G1);
             });
