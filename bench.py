@@ -500,6 +500,12 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     d = gemm[dom]
     peak, src = peak_tensor()
     achieved = d[2] / (d[1] / 1e3) / 1e12
+    # the class's bound from its arithmetic intensity (algorithmic flops / algorithmic HBM bytes, both
+    # recorded per launch by the trainer) against the ridge point of the measured peaks: the 1x1 convs
+    # of ResNet-50 (K = 64..512) sit far below it and are judged against HBM bandwidth
+    hbm, hsrc = peak_hbm()
+    ridge = peak * 1e12 / (hbm * 1e9)
+    ai = d[2] / d[3] if d[3] > 0 else float("inf")
     # DRAM bytes per launch of the same class from an ncu capture of one serialised step
     # (tools/step_traffic.py; bf16 only)
     traffic = None
@@ -510,8 +516,15 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     out["roofline"] = {"bound": "tensor", "kernel": f"{dom} (gemm_pk_kernel, tcgen05 + TMA; {d[0]} launches)",
                        "achieved": round(achieved, 1), "peak": peak, "peak_source": src, "unit": "TFLOP/s",
                        "frac": round(achieved / peak, 4), "traffic": traffic,
-                       "algorithmic_flops_per_launch": round(d[2] / d[0]), "launch_us": round(d[1] / d[0] * 1e3, 2),
-                       "share_of_serial_step": round(d[1] / tot, 3)}
+                       "algorithmic_flops_per_launch": round(d[2] / d[0]),
+                       "algorithmic_bytes_per_launch": round(d[3] / d[0]),
+                       "arithmetic_intensity_flop_per_byte": round(ai, 1), "ridge_flop_per_byte": round(ridge, 1),
+                       "launch_us": round(d[1] / d[0] * 1e3, 2), "share_of_serial_step": round(d[1] / tot, 3)}
+    if ai < ridge:
+        gbs = d[3] / (d[1] / 1e3) / 1e9
+        out["roofline"].update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "peak_source": hsrc,
+                                "unit": "GB/s", "frac": round(gbs / hbm, 4),
+                                "tensor_tflops": round(achieved, 1), "tensor_frac": round(achieved / peak, 4)})
     # ---- P2P traffic of this step (bytes per rank, one micro-batch per GPU): the gradient hop reads the
     # previous rank's partial sum S (4 B / param, ranks 2..N, fused into the weight-gradient epilogues);
     # every reader pulls the versions it reads from the updater (4 B / param, ranks 1..N-1); ZeRO-CDP
@@ -539,8 +552,8 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
         out["p2p"] = {"bytes_per_step_all_ranks": 0, "note": "one GPU: no peer traffic (the hop is local)"}
     out["kernel_breakdown"] = {
         k: {"launches": a[0], "ms": round(a[1], 4), "share": round(a[1] / tot, 3),
-            **({"tflops": round(a[2] / (a[1] / 1e3) / 1e12, 1)} if a[2] else
-               {"gbs": round(a[3] / (a[1] / 1e3) / 1e9, 1)})}
+            **({"tflops": round(a[2] / (a[1] / 1e3) / 1e12, 1)} if a[2] else {}),
+            **({"gbs": round(a[3] / (a[1] / 1e3) / 1e9, 1)} if a[3] or not a[2] else {})}
         for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])}
     out["serial_step_ms"] = round(tot, 4)
     tr.close()

@@ -18,9 +18,14 @@
  *                           drivers step_dp / step_cdp / run_experiment
  *                           (engine.py:119-215): the whole training step,
  *                           device resident, one CUDA graph per step.
- *   cdp_hop_*            <- comm.py:37-67 `schedule_cdp_ring_reduce` hop
- *                           (+ engine.py:96-109 accumulate/update) as kernels
- *   cdp_shard_copy       <- comm.py:126-143 ZeRO-CDP STATE_TRANSFER
+ *   cdp_resnet_* / cdp_vit_*  <- the same step for the named models, one worker per
+ *                           process (rank): the comm.py:37-67 `schedule_cdp_ring_reduce`
+ *                           hop and the engine.py:96-109 accumulate / update run inside
+ *                           the weight-gradient GEMM epilogues over peer memory; the
+ *                           comm.py:126-143 ZeRO-CDP STATE_TRANSFER runs as peer state
+ *                           copies inside the step (cdp_resnet_create_rank zero_table).
+ *                           There is no separate hop or shard-copy entry point: both are
+ *                           fused into the step graph.
  */
 #ifndef CDP_B200_H
 #define CDP_B200_H
@@ -169,6 +174,12 @@ int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const int32_t *d
  * rank's gradient into the flat buffer (cdp_resnet_partial); the caller sums it across ranks on the
  * trainer stream (cdp_resnet_stream, e.g. ncclAllReduce) and calls cdp_resnet_apply_update. */
 int cdp_resnet_apply_update(cdp_resnet *tr);
+/* ZeRO-DP baseline (ref comm.py:108-124: the owner of each stage broadcasts its states, the
+ * gradients are reduced to the owner): the owner updates only its tensors [first, end), the
+ * non-owners repack the compute copies of the tensors written into theta slot `which` (0 current,
+ * 1 previous; cdp_resnet_buffer "theta") by the caller's broadcast. */
+int cdp_resnet_apply_update_range(cdp_resnet *tr, int first_tensor, int end_tensor);
+int cdp_resnet_pack_range(cdp_resnet *tr, int which, int first_tensor, int end_tensor);
 int cdp_resnet_partial(cdp_resnet *tr, void **ptr, size_t *n);
 int cdp_resnet_stream(cdp_resnet *tr, void **stream);
 /* zero_table != NULL (world > 1): ZeRO-CDP state passing (ref comm.py:93-144), [world stages][2 (F, B)]
@@ -207,7 +218,8 @@ int cdp_resnet_flush_l2(cdp_resnet *tr);
 /* Device address, size and row pitch (elements; 0 = flat) of one internal buffer, for tests and
  * diagnostics after cdp_resnet_sync.  Names: "wc_hi"/"wc_lo" (index = slot * n_tensors + tensor),
  * "act_hi"/"act_lo" (activation), "y", "dy_hi", "dy_lo", "mean", "rstd", "dgamma", "dbeta" (conv
- * index), "gbuf" (0..3), "dpooled", "z", "pooled_hi", "pooled_lo", "dz_hi", "dz_lo", "region", "pool_arg" (max-pool window
+ * index), "gbuf" (0..3), "dpooled", "z", "pooled_hi", "pooled_lo", "dz_hi", "dz_lo", "theta" (0 current, 1 previous
+ * slot), "region", "pool_arg" (max-pool window
  * argmax, u8 r*3+s per output element). */
 int cdp_resnet_buffer(cdp_resnet *tr, const char *name, int index, void **ptr, size_t *bytes, int *ld);
 /* Trace mode (create option bit 1, value 2): the executed-version record of every parameter access,

@@ -12,8 +12,10 @@ rests on (ref `pkg/src/cyclicdp/costs.py:111-119`, `:140-153`):
 `activation_series` measures the same quantity from a plan (records live
 from F.start through B.end, ref `costs.py:157-170`); the executor allocates
 activation slots from exactly these intervals, so the planned peak is the
-peak the device holds (checked against `torch.cuda.max_memory_allocated`
-in the GPU tests).  The analytic Table-1 reproduction and extrapolation
+peak the device holds (checked against the device's own live-record
+high-water counter in tests/test_gpu_vit_cyclic.py; the trainers allocate
+with cudaMalloc, outside torch's caching allocator, so the bench reports the
+trainer's allocated bytes beside it).  The analytic Table-1 reproduction and extrapolation
 tooling (`costs.py:155-527`) are out of scope.
 """
 

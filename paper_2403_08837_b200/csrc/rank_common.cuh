@@ -56,6 +56,81 @@ __global__ void vtag_update_kernel(RingFlags *own, int unit, const int *step) {
     ptx::st_release_sys(&own->vtag[(t + 1) & 1][unit - 1], t + 1);
 }
 
+// ---------------------------------------------------------------- peer state copies
+// Copy of one parameter tensor's state from peer HBM (NVLink when the ranks are GPUs): up to
+// three fp32 arrays (theta slots, momentum) of the tensor's [rows][cols] flat layout, and the
+// compute-format packing of the first two into their GEMM copies (bf16 / fp32 hi+lo rows of
+// pitch wc.ld).  16-byte volatile loads (the peer rewrites the slot between steps), every load
+// of an element group issued before its stores, and no per-element index arithmetic beyond an
+// add: a thread's (row offset, column quad) is fixed for the whole loop (one division per thread
+// at entry).  Rows of <= 4 * blockDim columns are packed several per block pass; wider rows loop
+// over their columns; tensors whose rows are not float4-aligned (the 10-class classifier) or
+// flat vectors without a packed copy fall back to the scalar / flat paths.
+struct StateCopy {
+    const float *src[3];
+    float *dst[3];
+    int narr;
+    CTensor wc[2];  // wc[k].hi: pack array k into it
+    int64_t n;
+    int cols;
+};
+
+template <int KIND>
+__device__ __forceinline__ void state_copy_quad(const StateCopy &c, size_t o, size_t ow) {
+    float4 x[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (k < c.narr) x[k] = __ldcv(reinterpret_cast<const float4 *>(c.src[k] + o));
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (k < c.narr) {
+            *reinterpret_cast<float4 *>(c.dst[k] + o) = x[k];
+            if (k < 2 && c.wc[k].hi) store_wc4<KIND>(c.wc[k], ow, x[k]);
+        }
+}
+
+template <int KIND>
+__device__ void state_copy(const StateCopy &c) {
+    bool aligned = (c.n & 3) == 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (k < c.narr)
+            aligned = aligned && ((reinterpret_cast<uintptr_t>(c.src[k]) | reinterpret_cast<uintptr_t>(c.dst[k])) & 15) == 0;
+    const bool packed = c.wc[0].hi || c.wc[1].hi;
+    if (aligned && !packed) {  // flat vector (batch-norm gamma | beta): float4 over the flat range
+        const int64_t n4 = c.n / 4;
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x)
+            state_copy_quad<KIND>(c, size_t(i) * 4, 0);
+        return;
+    }
+    if (aligned && (c.cols & 3) == 0 && (c.wc[0].ld & 3) == 0 && (c.wc[1].ld & 3) == 0) {
+        const int q = c.cols / 4;
+        const int64_t rows = c.n / c.cols;
+        if (q <= int(blockDim.x)) {
+            const int rpb = blockDim.x / q;
+            const int r0 = threadIdx.x / q, c4 = (threadIdx.x - r0 * q) * 4;
+            if (r0 >= rpb) return;
+            for (int64_t r = blockIdx.x * int64_t(rpb) + r0; r < rows; r += int64_t(gridDim.x) * rpb)
+                state_copy_quad<KIND>(c, size_t(r) * c.cols + c4, size_t(r) * c.wc[0].ld + c4);
+        } else {
+            for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
+                for (int c4 = threadIdx.x * 4; c4 < c.cols; c4 += blockDim.x * 4)
+                    state_copy_quad<KIND>(c, size_t(r) * c.cols + c4, size_t(r) * c.wc[0].ld + c4);
+        }
+        return;
+    }
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < c.n; i += int64_t(gridDim.x) * blockDim.x) {
+        const size_t w = size_t(i / c.cols) * c.wc[0].ld + i % c.cols;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (k < c.narr) {
+                const float x = __ldcv(c.src[k] + i);
+                c.dst[k][i] = x;
+                if (k < 2 && c.wc[k].hi) Fmt<KIND>::store(c.wc[k].hi, c.wc[k].lo, w, x);
+            }
+    }
+}
+
 template <int KIND>
 __global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, int64_t n, int cols, CTensor wc,
                                    RingFlags *updater, RingFlags *own, int unit, int fresh, const int *step,
@@ -65,11 +140,14 @@ __global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, in
     const int t = *step;
     const uint32_t v = uint32_t(fresh ? t : t - 1);
     if (v <= 1) return;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const float x = __ldcv(src + i);
-        dst[i] = x;
-        if (wc.hi) Fmt<KIND>::store(wc.hi, wc.lo, size_t(i / cols) * wc.ld + i % cols, x);
-    }
+    StateCopy c{};
+    c.src[0] = src;
+    c.dst[0] = dst;
+    c.narr = 1;
+    c.wc[0] = wc;
+    c.n = n;
+    c.cols = cols;
+    state_copy<KIND>(c);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
