@@ -107,17 +107,19 @@ __global__ void zero_copy_kernel(ZeroUse z, int self, const float *src_t0, const
     ptx::griddep_launch();
     const int t = *step;
     if (z.src == self || t + z.dstep < 1) return;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const float a = __ldcv(src_t0 + i), b = __ldcv(src_t1 + i);
-        t0[i] = a;
-        t1[i] = b;
-        if (v) v[i] = __ldcv(src_v + i);
-        if (wc0.hi) {
-            const size_t w = size_t(i / cols) * wc0.ld + i % cols;
-            Fmt<KIND>::store(wc0.hi, wc0.lo, w, a);
-            Fmt<KIND>::store(wc1.hi, wc1.lo, w, b);
-        }
-    }
+    StateCopy c{};
+    c.src[0] = src_t0;
+    c.src[1] = src_t1;
+    c.src[2] = src_v;
+    c.dst[0] = t0;
+    c.dst[1] = t1;
+    c.dst[2] = v;
+    c.narr = v ? 3 : 2;
+    c.wc[0] = wc0;
+    c.wc[1] = wc1;
+    c.n = n;
+    c.cols = cols;
+    state_copy<KIND>(c);  // rank_common.cuh: 16-byte peer loads, no per-element division
 }
 
 // Publish the end of this rank's use of `unit` (after all its kernels on the stream).
@@ -175,7 +177,7 @@ struct ResNetTrainer {
     cudaEvent_t stage_ev[RING_N] = {};
     int stage_next = 0;
     int hist_cap = 1 << 14;
-    cudaStream_t main = nullptr, cs = nullptr, hs = nullptr;
+    cudaStream_t main = nullptr, cs = nullptr, hs = nullptr, ps = nullptr;  // ps: parameter pulls (run ahead)
     std::vector<cudaEvent_t> events;
     cudaGraphExec_t exec[2] = {nullptr, nullptr};
     int t = 1;
@@ -199,7 +201,7 @@ struct ResNetTrainer {
         for (auto e : stage_ev)
             if (e) cudaEventDestroy(e);
         if (stage_host) cudaFreeHost(stage_host);
-        for (auto s : {main, cs, hs})
+        for (auto s : {main, cs, hs, ps})
             if (s) cudaStreamDestroy(s);
     }
 
@@ -377,6 +379,7 @@ struct ResNetTrainer {
         CDP_CUDA(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
         CDP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         CDP_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+        CDP_CUDA(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
         ctrl_dev = DevBuf(sizeof(Control));
         perm_dev = DevBuf(size_t(B) * 4);
         flags_dev = DevBuf(sizeof(Flags));
@@ -398,6 +401,24 @@ struct ResNetTrainer {
         events.clear();
         ws_c = DevBuf(std::max<size_t>(ws_c_floats, 1) * 4);
         ws_h = DevBuf(std::max<size_t>(ws_h_floats, 1) * 4);
+    }
+
+    // Algorithmic HBM bytes of the next GEMM launch (operands once, outputs, fused epilogue
+    // operands / optimizer state): set by the caller, consumed by run_plan / run_pk (the bench's
+    // roofline picks HBM or tensor per class from flops / bytes).
+    double gemm_bytes = 0.0;
+    double take_bytes() {
+        const double b = gemm_bytes;
+        gemm_bytes = 0.0;
+        return b;
+    }
+    // per-parameter optimizer-state bytes of a hop / update epilogue
+    double hop_bytes_per_param() const {
+        const double wc_b = kind == 0 ? 2.0 : 8.0;
+        if (world == 1) return 16.0 + wc_b + (vel ? 0.0 : -8.0);  // G = g: theta, v read + written, compute copy
+        if (rank == 0) return 4.0;                                  // S = g
+        if (rank < world - 1) return 8.0;                           // S = S_in + g
+        return 20.0 + wc_b + (vel ? 0.0 : -8.0);                    // S_in + update
     }
 
     // ---------------------------------------------------------------- GEMM plumbing
@@ -427,7 +448,7 @@ struct ResNetTrainer {
         }
         CDP_REQUIRE(need <= cap, "split-K workspace too small");
         CDP_REQUIRE(size_t(p.grid.x) * p.grid.y * 4 <= (1u << 18), "split-K counters too small");
-        L(name, flops, 0.0, s, [&] { launch_gemm<K, BN, AMN, BMN, Epi, MODE>(p, ep, s); });
+        L(name, flops, take_bytes(), s, [&] { launch_gemm<K, BN, AMN, BMN, Epi, MODE>(p, ep, s); });
     }
 
     static Operand opnd(const CTensor &t, bool lo, bool mn, int64_t mn_ext, int64_t k_ext) {
@@ -540,7 +561,7 @@ struct ResNetTrainer {
         PL::setup_tma_out(maps, a, ep);
         last_stat_slots = a.splits > 1 ? a.tiles_m * slots_per_tile : grid;  // EpiConvOut2 statistics rows
         last_grid = grid;
-        L(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
+        L(name, flops, take_bytes(), s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
         if constexpr (!pk_direct<Epi>::value) if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<K>>::value;
             constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
@@ -647,6 +668,8 @@ struct ResNetTrainer {
         ep.tiles = c.tiles_fwd;
         const CBuf &w = wc[vslot][c.tw];
         rec(c.tw, A_FWD, 0, vslot, s);
+        gemm_bytes = double(c.impl == CI_STEM ? c.P * cols.ld : c.Pin * c.cin) * esz() +
+                     double(c.K) * c.cout * esz() + double(c.P) * c.cout * ysz();
         if (c.impl == CI_IMPLICIT) {
             pk_conv<K, GM_FPROP, EpiConvOut2<K>>("conv_fprop", tile_n(c.cout), c, w, ep, s, false);
         } else {
@@ -858,6 +881,8 @@ struct ResNetTrainer {
         ep.stats = nullptr;
         ep.add = add;
         ep.add_mask = add_mask;
+        gemm_bytes = double(c.P) * c.cout * esz() + double(c.K) * c.cout * esz() + double(c.Pin) * c.cin * ysz() +
+                     (add ? double(c.Pin) * c.cin * (ysz() + (add_mask.hi ? esz() : 0)) : 0.0);
         // residual-gradient add: the direct (register) epilogue, its own GEMM instantiation
         const bool direct = EpiConvAdd<K>::eligible(ep_with(ep, g_in, c.cin), c.cin, tile_n(c.cin)) &&
                             std::getenv("CDP_NO_DIRECT_ADD") == nullptr;
@@ -927,13 +952,16 @@ struct ResNetTrainer {
         return hp;
     }
 
-    // DP all-reduce baseline: the update of the step just run from the summed flat gradient.
-    void apply_update() {
+    // DP all-reduce baseline: the update of the step just run from the summed flat gradient
+    // (tensors [t0, t1): the ZeRO-DP baseline updates only the stage this rank owns).
+    void apply_update(int t0 = 0, int t1 = -1) {
         CDP_REQUIRE(allreduce, "apply_update is the DP all-reduce baseline's update");
         CDP_REQUIRE(t >= 2, "no step has run");
+        if (t1 < 0) t1 = int(tens.size());
+        CDP_REQUIRE(t0 >= 0 && t0 <= t1 && t1 <= int(tens.size()), "tensor range out of bounds");
         const int p = (t - 1) & 1;
         Flags *fl = flags_dev.as<Flags>();
-        for (size_t k = 0; k < tens.size(); ++k) {
+        for (size_t k = size_t(t0); k < size_t(t1); ++k) {
             const TensorSpec &ts = tens[k];
             HopParams hp{};
             hp.mode = 3;
@@ -971,6 +999,8 @@ struct ResNetTrainer {
         HopParams hp = hop_params(c.tw, p);
         hop_wait(hp, s);
         traced_update(c.tw, p, hp.mode == 2 || hp.mode == 3, s, [&] {
+            gemm_bytes = double(c.impl == CI_STEM ? c.P * cols.ld : c.Pin * c.cin) * esz() +
+                         double(c.P) * c.cout * esz() + double(c.K) * c.cout * hop_bytes_per_param();
             if (c.impl == CI_IMPLICIT) {
                 pk_conv<K, GM_WGRAD, EpiHop2<K>>("conv_wgrad_hop", tile_n(c.cout), c, wc[0][c.tw], hp, s, true);
             } else {
@@ -1102,7 +1132,18 @@ struct ResNetTrainer {
         cudaEvent_t fork = ev(main);
         wait(cs, fork);
         wait(hs, fork);
-        forward<K>(p, cs, [&](int tensor) { pull_tensor<K>(tensor, p, cs); });
+        wait(ps, fork);
+        // parameter pulls run ahead on their own stream (their waits for the updater block only that
+        // stream); each forward waits for its own tensor's pull only.  ZeRO-CDP state copies stay on
+        // the compute stream (their use-window order is the protocol).
+        forward<K>(p, cs, [&](int tensor) {
+            if (zero || rank == world - 1 || world == 1 || allreduce) {
+                pull_tensor<K>(tensor, p, cs);
+                return;
+            }
+            pull_tensor<K>(tensor, p, ps);
+            wait(cs, ev(ps));
+        });
         // loss + classifier backward
         Flags *fl = flags_dev.as<Flags>();
         const int nt = std::max(32, round_up(B, 32));
@@ -1206,6 +1247,7 @@ struct ResNetTrainer {
         // join + bookkeeping
         wait(main, ev(cs));
         wait(main, ev(hs));
+        wait(main, ev(ps));
         L("finish_step", 0, 0, main, [&] {
             finish_step_kernel_rn<<<1, 1, 0, main>>>(loss_dev.as<double>(), flags_dev.as<Flags>(),
                                                      hist_loss.as<double>(), hist_flags.as<Flags>(), hist_cap,
@@ -1259,16 +1301,20 @@ struct ResNetTrainer {
                 else
                     record_step<1>(p);
             } catch (...) {
-                cudaEvent_t a, b;
+                cudaEvent_t a, b, c;
                 cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
                 cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&c, cudaEventDisableTiming);
                 cudaEventRecord(a, cs);
                 cudaEventRecord(b, hs);
+                cudaEventRecord(c, ps);
                 cudaStreamWaitEvent(main, a, 0);
                 cudaStreamWaitEvent(main, b, 0);
+                cudaStreamWaitEvent(main, c, 0);
                 if (cudaStreamEndCapture(main, &g) == cudaSuccess && g) cudaGraphDestroy(g);
                 cudaEventDestroy(a);
                 cudaEventDestroy(b);
+                cudaEventDestroy(c);
                 cudaGetLastError();
                 throw;
             }
@@ -1281,6 +1327,24 @@ struct ResNetTrainer {
     // ---------------------------------------------------------------- params / steps
     void pack_slot(int slot) {
         for (size_t i = 0; i < tens.size(); ++i) {
+            const TensorSpec &ts = tens[i];
+            if (ts.kind == T_BN) continue;
+            if (kind == 0)
+                pack_tensor_kernel<0><<<blocks_for(ts.n), 256, 0, main>>>(theta[slot] + ts.base, ts.n, ts.cols,
+                                                                          wc[slot][i].view());
+            else
+                pack_tensor_kernel<1><<<blocks_for(ts.n), 256, 0, main>>>(theta[slot] + ts.base, ts.n, ts.cols,
+                                                                          wc[slot][i].view());
+            CDP_CUDA(cudaGetLastError());
+        }
+    }
+
+    // Repack the compute copies of tensors [t0, t1) of theta slot `which` (0 current, 1 previous)
+    // after its fp32 values were written from outside (the ZeRO-DP baseline's NCCL broadcast).
+    void pack_range(int which, int t0, int t1) {
+        CDP_REQUIRE(t0 >= 0 && t0 <= t1 && t1 <= int(tens.size()), "tensor range out of bounds");
+        const int slot = which == 0 ? (t & 1) : ((t & 1) ^ 1);
+        for (int i = t0; i < t1; ++i) {
             const TensorSpec &ts = tens[i];
             if (ts.kind == T_BN) continue;
             if (kind == 0)
@@ -1350,8 +1414,8 @@ struct ResNetTrainer {
         stage_control(perm, lr);
         clear_oprecs();
         instr = true;
-        cudaStream_t saved_cs = cs, saved_hs = hs;
-        if (serial) cs = hs = main;
+        cudaStream_t saved_cs = cs, saved_hs = hs, saved_ps = ps;
+        if (serial) cs = hs = ps = main;
         try {
             if (kind == 0)
                 record_step<0>(t & 1);
@@ -1361,10 +1425,12 @@ struct ResNetTrainer {
             instr = false;
             cs = saved_cs;
             hs = saved_hs;
+            ps = saved_ps;
             throw;
         }
         cs = saved_cs;
         hs = saved_hs;
+        ps = saved_ps;
         instr = false;
         ++t;
         CDP_CUDA(cudaStreamSynchronize(main));
@@ -1512,6 +1578,14 @@ extern "C" int cdp_resnet_apply_update(cdp_resnet *tr) {
     return guarded([&] { tr->impl->apply_update(); });
 }
 
+extern "C" int cdp_resnet_apply_update_range(cdp_resnet *tr, int first_tensor, int end_tensor) {
+    return guarded([&] { tr->impl->apply_update(first_tensor, end_tensor); });
+}
+
+extern "C" int cdp_resnet_pack_range(cdp_resnet *tr, int which, int first_tensor, int end_tensor) {
+    return guarded([&] { tr->impl->pack_range(which, first_tensor, end_tensor); });
+}
+
 extern "C" int cdp_resnet_partial(cdp_resnet *tr, void **ptr, size_t *n) {
     return guarded([&] {
         *ptr = tr->impl->partial;
@@ -1652,6 +1726,13 @@ extern "C" int cdp_resnet_buffer(cdp_resnet *tr, const char *name, int index, vo
             cb(m.pooled, n == "pooled_lo");
         } else if (n == "dz_hi" || n == "dz_lo") {
             cb(m.dz, n == "dz_lo");
+        } else if (n == "theta") {  // index 0: current slot, 1: previous (fp32, P values)
+            CDP_REQUIRE(index == 0 || index == 1, "theta index: 0 current, 1 previous");
+            const int slot = index == 0 ? (m.t & 1) : ((m.t & 1) ^ 1);
+            *ptr = m.theta[slot];
+            *bytes = size_t(m.P) * 4;
+            *ld = 0;
+            return;
         } else if (n == "region") {
             d = &m.region;
         } else if (n == "pool_arg") {
