@@ -589,6 +589,81 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     return out
 
 
+def run_resnet_variant(args, ws, rank, local, model, steps, warmup, mode):
+    """Timed steps of one comparison variant at the same N, shape and per-GPU micro-batch (all ranks):
+    "dp-allreduce" (DP: NCCL all-reduce of the flat gradient + update), "zero-cdp" (ZeRO-CDP: P2P state
+    passing along the reference holder chain) or "zero-dp" (ZeRO-DP: per-stage owner broadcast +
+    gradient reduce to the owner, resnet.ZeroDpRank).  Device-timed (trainer stream events), L2 flushed,
+    max over ranks."""
+    import argparse as _ap
+
+    import torch
+
+    from paper_2403_08837_b200.dist import exchange_handles, resolve
+
+    allreduce = mode in ("dp-allreduce", "zero-dp")
+    zero = mode == "zero-cdp"
+    a2 = _ap.Namespace(**vars(args))
+    a2.rule = "dp-allreduce" if allreduce else "cdp-v2"
+    rule = None if allreduce else resolve("cdp-v2", ws)
+    tr, B, hw, classes, x, y = make_trainer(a2, model, ws, rank, rule, allreduce, zero)
+    if ws > 1:
+        tr.connect_ipc(exchange_handles(tr.ipc_handle()))
+    else:
+        tr.connect([tr.region()])
+    perms = [np.random.default_rng([0, t]).permutation(x.shape[0])[rank * B:(rank + 1) * B]
+             for t in range(1, warmup + steps + 2)]
+    zd = None
+    if mode == "zero-dp":
+        from paper_2403_08837_b200.resnet import ZeroDpRank
+
+        zd = ZeroDpRank(tr)
+    elif mode == "dp-allreduce":
+        ext = torch.cuda.ExternalStream(tr.stream_handle())
+        grad = tr.partial_tensor()
+
+    def do_step(perm):
+        if zd is not None:
+            zd.step(perm, RN_LR)
+            return
+        tr.step(perm, RN_LR)
+        if mode == "dp-allreduce":
+            if ws > 1:
+                with torch.cuda.stream(ext):
+                    torch.distributed.all_reduce(grad)
+            tr.apply_update()
+
+    for t in range(warmup):
+        do_step(perms[t])
+    tr.zero_drain()
+    tr.sync()
+    if ws > 1:
+        torch.distributed.barrier()
+    for k in range(steps):
+        tr.flush_l2()
+        tr.mark(2 * k)
+        do_step(perms[warmup + k])
+        tr.mark(2 * k + 1)
+    tr.zero_drain()
+    tr.sync()
+    if tr.ring_error():
+        raise RuntimeError(f"rank {rank}: ring protocol timed out ({mode})")
+    ms = float(np.mean([tr.elapsed(2 * k, 2 * k + 1) for k in range(steps)]))
+    st = tr.stats()
+    state_b = zd.bytes_per_step if zd is not None else int(st.get("zero_state_bytes_per_step", 0))
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        v = torch.tensor([float(state_b)], device="cuda")
+        allv = [torch.zeros_like(v) for _ in range(ws)]
+        torch.distributed.all_gather(allv, v)
+        state_b = [int(a.item()) for a in allv]
+    tr.close()
+    return {"value": round(ws * B / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 4),
+            "state_bytes_per_step_per_rank": state_b, "param_state_bytes_per_rank": st["param_state_bytes"]}
+
+
 def vit_single_gpu(n, steps, warmup, profile=False):
     """BASELINE configs[3]: ViT-B/16 224x224, n sequential micro-batches of VIT_MB on ONE GPU, stepped
     through the reference's SINGLE_GPU_CDP (cdp-v2) and SINGLE_GPU_DP timelines by the cyclic executor
@@ -727,6 +802,18 @@ def main_resnet(args, ws, rank, local):
 
     model = args.model
     res = run_resnet(args, ws, rank, local, model, args.steps, args.warmup)
+    # ---- comparison points at the same N (configs[2]: CDP-v2 vs the DP all-reduce baseline; configs[4]:
+    # ZeRO-CDP P2P state passing vs the ZeRO-DP broadcast baseline).  Run on every rank; a failure of a
+    # baseline is reported, not fatal to the headline.
+    baselines = None
+    if ws > 1 and not args.no_extras and args.rule == "cdp-v2" and not args.zero and model != "vit_b16":
+        baselines = {}
+        steps_v = max(3, min(args.steps, 20))
+        for mode in ("dp-allreduce", "zero-cdp", "zero-dp"):
+            try:
+                baselines[mode] = run_resnet_variant(args, ws, rank, local, model, steps_v, 3, mode)
+            except Exception as e:  # noqa: BLE001 - reported in the JSON line
+                baselines[mode] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank != 0:
         return None
     peak_note = "configs[1]" if model == "resnet18" else "configs[2] (north-star target; N GPUs = N stages)"
@@ -753,6 +840,14 @@ def main_resnet(args, ws, rank, local):
         out["zero_cdp"] = {"state_bytes_received_per_step_rank0": res["zero_state_bytes_per_step"],
                            "what": "both theta version slots + momentum of every received tensor use (P2P copy "
                                    "kernels, ref comm.py:93-144 holder chain)"}
+    if baselines is not None:
+        b = out["baselines"] = baselines
+        if "value" in b.get("dp-allreduce", {}):
+            b["cdp_over_dp_allreduce"] = round(out["value"] / b["dp-allreduce"]["value"], 4)
+        if "value" in b.get("zero-cdp", {}) and "value" in b.get("zero-dp", {}):
+            b["zero_cdp_over_zero_dp"] = round(b["zero-cdp"]["value"] / b["zero-dp"]["value"], 4)
+        b["model_state_volume_per_device_ref_costs_py"] = {
+            "zero_cdp": f"2(N-1)/N Psi_P = {2 * (ws - 1) / ws:.3f} Psi_P", "zero_dp": "2 Psi_P (ref costs.py:140-153)"}
     return out
 
 

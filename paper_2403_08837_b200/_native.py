@@ -69,6 +69,8 @@ SIGNATURES = {
                                        c_int_p, c_int_p, c_int, ctypes.POINTER(c_void_p)]),
     "cdp_resnet_zero_drain": (c_int, [c_void_p]),
     "cdp_resnet_apply_update": (c_int, [c_void_p]),
+    "cdp_resnet_apply_update_range": (c_int, [c_void_p, c_int, c_int]),
+    "cdp_resnet_pack_range": (c_int, [c_void_p, c_int, c_int, c_int]),
     "cdp_resnet_partial": (c_int, [c_void_p, ctypes.POINTER(c_void_p), ctypes.POINTER(ctypes.c_size_t)]),
     "cdp_resnet_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_resnet_step_host_batch": (c_int, [c_void_p, c_float_p, c_int_p, c_float]),

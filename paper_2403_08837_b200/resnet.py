@@ -318,8 +318,39 @@ class DeviceResNet:
         N.check(self.lib.cdp_resnet_stream(self.h, ctypes.byref(s)))
         return s.value or 0
 
-    def apply_update(self):
-        N.check(self.lib.cdp_resnet_apply_update(self.h))
+    def apply_update(self, first_tensor=0, end_tensor=None):
+        """Update from the summed flat gradient; a tensor range updates only those tensors (ZeRO-DP)."""
+        if first_tensor == 0 and end_tensor is None:
+            N.check(self.lib.cdp_resnet_apply_update(self.h))
+        else:
+            end = len(self.specs) if end_tensor is None else int(end_tensor)
+            N.check(self.lib.cdp_resnet_apply_update_range(self.h, int(first_tensor), end))
+
+    def theta_tensor(self, which=0):
+        """torch view (no copy) of theta slot `which` (0: the version the next step reads fresh)."""
+        import torch
+
+        ptr, nb, ld = ctypes.c_void_p(), ctypes.c_size_t(), ctypes.c_int()
+        N.check(self.lib.cdp_resnet_buffer(self.h, b"theta", int(which), ctypes.byref(ptr), ctypes.byref(nb),
+                                           ctypes.byref(ld)))
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (nb.value // 4,), "typestr": "<f4", "data": (ptr.value, False),
+                                        "version": 3}
+
+        return torch.as_tensor(_View(), device="cuda")
+
+    def pack_range(self, which, first_tensor, end_tensor):
+        """Repack the GEMM copies of tensors [first, end) after theta slot `which` was written externally."""
+        N.check(self.lib.cdp_resnet_pack_range(self.h, int(which), int(first_tensor), int(end_tensor)))
+
+    def tensor_bases(self) -> np.ndarray:
+        np_, nt = ctypes.c_int64(), ctypes.c_int()
+        N.check(self.lib.cdp_resnet_info(self.h, ctypes.byref(np_), ctypes.byref(nt), None, None))
+        base = np.zeros(nt.value, dtype=np.int64)
+        N.check(self.lib.cdp_resnet_info(self.h, ctypes.byref(np_), ctypes.byref(nt),
+                                         base.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), None))
+        return base
 
     def zero_drain(self):
         """ZeRO-CDP: publish the next step's forward uses (call on every rank before synchronising at the
@@ -461,3 +492,76 @@ def synthetic_cifar(n, seed=0, hw=32, classes=10):
     """x ~ N(0,1) NHWC [n][hw][hw][3], labels uniform in [0, classes) from default_rng([seed, 0xD0])."""
     rng = np.random.default_rng([seed, 0xD0])
     return rng.normal(0.0, 1.0, size=(n, hw, hw, 3)).astype(np.float32), rng.integers(0, classes, size=n).astype(np.int32)
+
+
+class ZeroDpRank:
+    """ZeRO-DP baseline rank (ref comm.py:108-124, costs.py:140-153): stage s is owned by rank s - 1;
+    before the step every owner broadcasts its stage's current parameters (NCCL / gloo broadcast on
+    the trainer stream, the non-owners repack their GEMM copies), the step computes this rank's
+    gradient (the DP all-reduce trainer's gradient-only epilogues), the gradient of every stage is
+    reduced to its owner and only the owner updates that stage.  The reference moves 2 Psi_P per
+    device per step (a broadcast for the forward and one for the backward of each stage, its states
+    freed in between); this realisation keeps the broadcast parameters resident across the step, so
+    it moves Psi_P of parameters (broadcast) + Psi_P of gradients (reduce) — `bytes_per_step` reports
+    what it moves.  Not the hot path: the comparison point for ZeRO-CDP's P2P state passing."""
+
+    def __init__(self, trainer: "DeviceResNet", group=None):
+        import torch
+        import torch.distributed as dist
+
+        if not trainer.dp_allreduce:
+            raise ValueError("ZeRO-DP runs on a DP all-reduce (gradient-only) trainer")
+        self.tr, self.group = trainer, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        base = trainer.tensor_bases()
+        n_t = len(trainer.specs)
+        ends = list(base[1:]) + [trainer.P]
+        self.ranges = []  # per stage: (first tensor, end tensor, first param, end param)
+        for s in range(1, self.world + 1):
+            idx = [k for k in range(n_t) if int(trainer.stage[k]) == s]
+            if not idx or idx != list(range(idx[0], idx[-1] + 1)):
+                raise ValueError("stages must be contiguous tensor ranges")
+            self.ranges.append((idx[0], idx[-1] + 1, int(base[idx[0]]), int(ends[idx[-1]])))
+        h = trainer.stream_handle()
+        self.ext = torch.cuda.ExternalStream(h) if h else None  # None: host tensors (CPU tests)
+        self.gloo = dist.get_backend(group) == "gloo"
+        self.grad = trainer.partial_tensor()
+        other = sum(r[3] - r[2] for i, r in enumerate(self.ranges) if i != self.rank)
+        # this rank's traffic per step: the parameters of the stages it does not own (received by
+        # broadcast) and its gradient of those stages (sent to their owners by the reduce)
+        self.bytes_per_step = 8 * other
+
+    def broadcast(self):
+        import torch.distributed as dist
+
+        theta = self.tr.theta_tensor(0)
+        with self._on_stream():
+            for s, (t0, t1, p0, p1) in enumerate(self.ranges):
+                dist.broadcast(theta[p0:p1], src=s, group=self.group)
+        for s, (t0, t1, p0, p1) in enumerate(self.ranges):
+            if s != self.rank:
+                self.tr.pack_range(0, t0, t1)
+
+    def reduce_update(self):
+        import torch.distributed as dist
+
+        with self._on_stream():
+            for s, (t0, t1, p0, p1) in enumerate(self.ranges):
+                if self.gloo:  # gloo has no CUDA reduce: the all-reduce gives the owner the same sum
+                    dist.all_reduce(self.grad[p0:p1], group=self.group)
+                else:
+                    dist.reduce(self.grad[p0:p1], dst=s, group=self.group)
+        t0, t1, _, _ = self.ranges[self.rank]
+        self.tr.apply_update(t0, t1)
+
+    def _on_stream(self):
+        import contextlib
+
+        import torch
+
+        return torch.cuda.stream(self.ext) if self.ext is not None else contextlib.nullcontext()
+
+    def step(self, perm, lr):
+        self.broadcast()
+        self.tr.step(perm, lr)
+        self.reduce_update()
