@@ -166,6 +166,21 @@ def executed_order_violations(tl, executed: dict) -> list:
     return bad
 
 
+def _planned_peak(tl, record_bytes) -> int:
+    """The plan's peak live record bytes (records live from F.start through B.end, ref costs.py:157-170)."""
+    from .costs import activation_records
+
+    delta = [0] * (tl.horizon + 2)
+    for _dev, lo, hi, stage, _i, _t in activation_records(tl):
+        delta[max(1, lo)] += int(record_bytes[stage - 1])
+        delta[min(tl.horizon, hi) + 1] -= int(record_bytes[stage - 1])
+    acc, peak = 0, 0
+    for g in range(1, tl.horizon + 1):
+        acc += delta[g]
+        peak = max(peak, acc)
+    return peak
+
+
 def cmd_trace(args) -> int:
     import numpy as np
 
@@ -191,6 +206,23 @@ def cmd_trace(args) -> int:
                             args.training_steps)
     tl = build_dp_timeline(cfg) if rule is None else build_cdp_timeline(cfg, rule)
     _write(Path(args.out), "executed.txt", executed_to_text(tl, executed))
+    if args.training_steps >= 3:
+        import json
+
+        from .accounting import executed_activation, executed_balance
+        from .costs import activation_records
+
+        esz = 2 if args.dtype == "bf16" else 8
+        rb = [args.batch * ((d + 15) // 16 * 16) * esz for d in task.model.dims[:-1]]  # executor.record_bytes
+        act = executed_activation(executed, rb, args.training_steps)
+        planned = _planned_peak(tl, rb)
+        bal = executed_balance(tl, executed)
+        rep = {"executed": {"peak_activation_bytes": act.peak_bytes, "steady_max_bytes": act.steady_max_bytes,
+                            "steady_min_bytes": act.steady_min_bytes, "steady_mean_bytes": round(act.mean_bytes, 1)},
+               "planned_peak_activation_bytes": planned, "balance": bal}
+        _write(Path(args.out), "accounting.json", json.dumps(rep, indent=1))
+        print(f"executed peak activation {act.peak_bytes} B (planned {planned} B); "
+              f"max hops per worker per boundary {bal['max_sends_or_receives_per_worker']}")
     bad = executed_order_violations(tl, executed)
     for b in bad:
         print(f"violation[executed-order]: {b}", file=sys.stderr)

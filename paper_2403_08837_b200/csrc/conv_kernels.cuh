@@ -497,34 +497,39 @@ struct EpiConvAdd : EpiConvOut2<KIND> {
     // row's 64-byte residual / mask segments are loaded before the TMEM read (eight 16-byte loads
     // in flight per thread): with K = 64..512 this epilogue has almost no MMA work to hide behind,
     // and its L2 round trips were the kernel (1.9 TB/s in the shared-tile path).
-    // 16 columns per call (two 16-byte vectors of residual and mask per thread in flight)
+    // 64 columns (one thread's half of an epilogue pass) per load: eight 16-byte vectors of residual
+    // and eight of mask in flight per thread, issued BEFORE the accumulator is ready (they depend on
+    // the row only) — the stall profile of the 16-column version was the first use of these loads
     struct DirectPre {
-        uint4 a[2], m[2];
+        uint4 a[8], m[8];
     };
+    template <int NC>  // NC = 32 or 64 columns
     __device__ static void direct_load(const Params &p, int m, int col, int64_t off, DirectPre &d) {
+        static_assert(NC == 32 || NC == 64, "direct epilogue loads 32 or 64 columns");
         if (m < 0) return;
         const size_t o = size_t(off) + size_t(m) * p.ld + col;
         const uint4 *pa = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.add) + o);
-        d.a[0] = pa[0];
-        d.a[1] = pa[1];
+#pragma unroll
+        for (int i = 0; i < NC / 8; ++i) d.a[i] = pa[i];
         if (p.add_mask.hi) {
             const uint4 *pm = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.add_mask.hi) + o);
-            d.m[0] = pm[0];
-            d.m[1] = pm[1];
+#pragma unroll
+            for (int i = 0; i < NC / 8; ++i) d.m[i] = pm[i];
         }
     }
-    __device__ static void direct_store(const Params &p, int m, int col, int64_t off, const DirectPre &d,
+    // columns [col + 16 q, col + 16 q + 16) of the 64 loaded ones, from v[16] (TMEM)
+    __device__ static void direct_store(const Params &p, int m, int col, int q, int64_t off, const DirectPre &d,
                                         const float (&v)[16]) {
         if (m < 0) return;
-        const size_t o = size_t(off) + size_t(m) * p.ld + col;
+        const size_t o = size_t(off) + size_t(m) * p.ld + col + 16 * q;
         uint4 *po = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + o);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             F8 a, x;
-            bf16x8_to_f8(d.a[i], a);
+            bf16x8_to_f8(d.a[2 * q + i], a);
             if (p.add_mask.hi) {
                 F8 mk;
-                bf16x8_to_f8(d.m[i], mk);
+                bf16x8_to_f8(d.m[2 * q + i], mk);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) x.v[k] = v[8 * i + k] + (mk.v[k] > 0.f ? a.v[k] : 0.f);
             } else {

@@ -338,6 +338,29 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 rowm[tid] = m;
                 if (!split) Epi::prefetch_row(ep, m, tn * BN, min(BN, args.N - tn * BN), out_off);
             }
+            if constexpr (pk_direct<Epi>::value) {  // the only epilogue of this instantiation (no split)
+                const int row_m = pk_row_m(args, tm, row, g);
+                typename Epi::DirectPre dp;
+                Epi::template direct_load<HC>(ep, row_m, tn * BN + half * HC, out_off, dp);  // before the accumulator
+                ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
+                ptx::tc_fence_after();
+                const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+#pragma unroll 1
+                for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+                    const int col = tn * BN + h * C::EPI_COLS + half * HC;
+                    if (h > 0) Epi::template direct_load<HC>(ep, row_m, col, out_off, dp);
+#pragma unroll
+                    for (int qq = 0; qq < HC / 16; ++qq) {
+                        float v[16];
+                        ptx::tmem_ld16(taddr + h * C::EPI_COLS + half * HC + 16 * qq, v);
+                        Epi::direct_store(ep, row_m, col, qq, out_off, dp, v);
+                    }
+                }
+                ptx::tc_fence_before();
+                pk_bar(1, kPkEpi);
+                if (tid == 0) ptx::mbar_arrive(&tempty[acc]);  // accumulator free
+                continue;
+            } else {
             ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
             ptx::tc_fence_after();
             const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
@@ -406,25 +429,6 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     continue;
                 }
             }
-            if constexpr (pk_direct<Epi>::value) {  // the only epilogue of this instantiation (no split)
-                const int row_m = pk_row_m(args, tm, row, g);
-#pragma unroll 1
-                for (int h = 0; h < BN / C::EPI_COLS; ++h) {
-#pragma unroll 1
-                    for (int c = half * HC; c < (half + 1) * HC; c += 16) {
-                        const int col = tn * BN + h * C::EPI_COLS + c;
-                        typename Epi::DirectPre dp;
-                        Epi::direct_load(ep, row_m, col, out_off, dp);
-                        float v[16];
-                        ptx::tmem_ld16(taddr + h * C::EPI_COLS + c, v);
-                        Epi::direct_store(ep, row_m, col, out_off, dp, v);
-                    }
-                }
-                ptx::tc_fence_before();
-                pk_bar(1, kPkEpi);
-                if (tid == 0) ptx::mbar_arrive(&tempty[acc]);  // accumulator free
-                continue;
-            } else {
 #pragma unroll 1
             for (int h = 0; h < BN / C::EPI_COLS; ++h) {
                 const int row_m = pk_row_m(args, tm, row, g);  // own computation: rowm is not yet synced
