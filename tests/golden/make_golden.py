@@ -14,6 +14,8 @@ the copy with the reference's own setup.py) and records:
 * kernels.npz     mlp_value_grad / quad_value_grad outputs on seeded inputs;
 * toy_runs.npz    run_experiment losses, final params and version traces on
                   small MLP (mse, xent) and quadratic tasks, momentum 0 / 0.9;
+* closed_form.json  closed_form_costs (ref costs.py:64-153) activation per device and state
+                  volume per step for the hot-path schemes over n, micro-batch and profiles;
 * config1.npz     config-1 shape (3072-256-256-256-10, N=4, B=32, xent):
                   data checksums, 20-step losses and a fixed sample of the
                   final parameters for dp / cdp-v1 / cdp-v2, momentum 0.9.
@@ -218,10 +220,30 @@ def config1(steps=20):
     np.savez_compressed(os.path.join(OUT, "config1.npz"), **out)
 
 
+def closed_forms():
+    from cyclicdp import ParallelismConfig, Scheme, make_homogeneous_profile
+    from cyclicdp.costs import closed_form_costs
+
+    out = []
+    for sch in (Scheme.SINGLE_GPU_DP, Scheme.SINGLE_GPU_CDP, Scheme.MULTI_GPU_DP, Scheme.MULTI_GPU_CDP,
+                Scheme.ZERO_DP, Scheme.ZERO_CDP):
+        for n in (1, 2, 3, 4, 8):
+            for b in (1, 2, 5):
+                for pp, pa in ((12, 60), (7, 3), (480, 4800)):
+                    prof = make_homogeneous_profile(n, pp * n, pa * n, 1)
+                    r = closed_form_costs(ParallelismConfig(sch, n, b, 3), prof)
+                    out.append([sch.value, n, b, pp * n, pa * n, str(r.peak_activation_memory_per_device),
+                                str(r.state_comm_volume_per_training_step)])
+    with open(os.path.join(OUT, "closed_form.json"), "w") as fh:
+        json.dump(out, fh)
+    return len(out)
+
+
 if __name__ == "__main__":
     tmp = load_reference()
     try:
         print("plans:", plans())
+        print("closed forms:", closed_forms())
         kernels()
         toy_runs()
         if "--skip-config1" not in sys.argv:
