@@ -238,6 +238,8 @@ struct EpiConvOut2 {
         int tiles;
         const void *add;     // Y-format [rows][ld] added to the output (residual gradient), or null
         CTensor add_mask;    // add masked by (add_mask > 0) when add_mask.hi
+        CTensor out_mask;    // the final value masked by (out_mask > 0) when out_mask.hi (a ReLU's gradient
+                             // mask applied by the producer: its consumers then read no mask)
         int out_f32;         // 1: fp32 output rows (and `add` is fp32): the ViT residual stream
         CTensor gelu_out;    // also write gelu(out) here (compute format, own ld), or null
         const void *gelu_z;  // out *= gelu'(z), z Y-format with the output's layout, or null
@@ -248,7 +250,8 @@ struct EpiConvOut2 {
     // the tile with TMA (gemm_pk_kernel, PkArgs::tma_out)
     static constexpr bool kTmaStore = KIND == 0;
     static bool tma_eligible(const Params &p) {
-        return KIND == 0 && p.out && !p.add && !p.gelu_z && !p.gelu_out.hi && !p.out_f32 && (p.ld % 8) == 0 &&
+        return KIND == 0 && p.out && !p.add && !p.out_mask.hi && !p.gelu_z && !p.gelu_out.hi && !p.out_f32 &&
+               (p.ld % 8) == 0 &&
                (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
     }
     __device__ static bool has_stats(const Params &p) { return p.stats != nullptr; }
@@ -310,6 +313,7 @@ struct EpiConvOut2 {
                     if (p.add_mask.hi && !(Fmt<KIND>::load(p.add_mask.hi, p.add_mask.lo, o) > 0.f)) a = 0.f;
                     x += a;
                 }
+                if (p.out_mask.hi && !(Fmt<KIND>::load(p.out_mask.hi, p.out_mask.lo, o) > 0.f)) x = 0.f;
                 if (p.gelu_z) x *= gelu_grad(KIND == 0 ? Fmt<0>::load(p.gelu_z, nullptr, o)
                                                        : static_cast<const float *>(p.gelu_z)[o]);
                 if (p.gelu_out.hi)
@@ -348,10 +352,11 @@ struct EpiConvOut2 {
                         a[u][0] = ld_y4<KIND>(p.add, o[u]);
                         a[u][1] = ld_y4<KIND>(p.add, o[u] + 4);
                     }
-                    if (p.add_mask.hi) {
-                        mk[u][0] = ld_c4<KIND>(p.add_mask, o[u]);
-                        mk[u][1] = ld_c4<KIND>(p.add_mask, o[u] + 4);
-                    }
+                }
+                if (p.add_mask.hi || p.out_mask.hi) {  // exclusive: one mask register set
+                    const CTensor &mt = p.add_mask.hi ? p.add_mask : p.out_mask;
+                    mk[u][0] = ld_c4<KIND>(mt, o[u]);
+                    mk[u][1] = ld_c4<KIND>(mt, o[u] + 4);
                 }
             }
 #pragma unroll
@@ -366,6 +371,7 @@ struct EpiConvOut2 {
                         v[u][k].z += b.z;
                         v[u][k].w += b.w;
                     }
+                    if (p.out_mask.hi) v[u][k] = relu_mask4(v[u][k], mk[u][k]);
                 }
                 if (p.gelu_z) {
                     const F8 zz = ld_y8<KIND>(p.gelu_z, o[u]);
@@ -417,15 +423,19 @@ struct EpiConvOut2 {
     }
     // The running value of the thread's column, loaded before the unit's accumulator is
     // ready (hides the load latency; the same thread stored it at its previous unit).
-    using Pre = float2;
-    __device__ static Pre col_stats_pre(const Params &p, int col0, int ncols, int tid) {
-        if (!p.stats || tid >= ncols) return make_float2(0.f, 0.f);
-        return *reinterpret_cast<const float2 *>(p.stats + (size_t(col0 + tid) * gridDim.x + blockIdx.x) * 2);
+    // (an 8-byte cp.async into the thread's own shared slot: a register load here was spilled and its
+    // wait stalled the epilogue at every unit start)
+    __device__ static void col_stats_pre(const Params &p, int col0, int ncols, int tid, float *slot) {
+        if (!p.stats || tid >= ncols) return;
+        ptx::cp_async8(slot + 2 * tid, p.stats + (size_t(col0 + tid) * gridDim.x + blockIdx.x) * 2);
+        ptx::cp_async_commit();
     }
     template <int NTH>  // one column per thread (ncols <= NTH)
     __device__ static void col_stats(const Params &p, const float *part, int pcols, int col0, int ncols, int tm,
-                                     int tid, Pre cur) {
+                                     int tid, const float *slot) {
         if (p.stats && tid < ncols) {
+            ptx::cp_async_wait_all();
+            const float2 cur = *reinterpret_cast<const float2 *>(slot + 2 * tid);
             float s = 0.f, q = 0.f;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -511,11 +521,33 @@ struct EpiConvAdd : EpiConvOut2<KIND> {
         const uint4 *pa = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.add) + o);
 #pragma unroll
         for (int i = 0; i < NC / 8; ++i) d.a[i] = pa[i];
-        if (p.add_mask.hi) {
-            const uint4 *pm = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.add_mask.hi) + o);
+        if (p.add_mask.hi || p.out_mask.hi) {
+            const void *mp = p.add_mask.hi ? p.add_mask.hi : p.out_mask.hi;
+            const uint4 *pm = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(mp) + o);
 #pragma unroll
             for (int i = 0; i < NC / 8; ++i) d.m[i] = pm[i];
         }
+    }
+    // accumulator + residual for vector u of the loaded row; mask 0: none, 1: masks the residual,
+    // 2: masks the sum (the ReLU gradient mask of the output)
+    __device__ static F8 combine(const DirectPre &d, int u, int mask, const float *v) {
+        F8 a, x;
+        bf16x8_to_f8(d.a[u], a);
+        if (mask) {
+            F8 mk;
+            bf16x8_to_f8(d.m[u], mk);
+            if (mask == 1) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x.v[k] = v[k] + (mk.v[k] > 0.f ? a.v[k] : 0.f);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x.v[k] = mk.v[k] > 0.f ? v[k] + a.v[k] : 0.f;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x.v[k] = v[k] + a.v[k];
+        }
+        return x;
     }
     // columns [col + 16 q, col + 16 q + 16) of the 64 loaded ones, from v[16] (TMEM)
     __device__ static void direct_store(const Params &p, int m, int col, int q, int64_t off, const DirectPre &d,
@@ -525,19 +557,42 @@ struct EpiConvAdd : EpiConvOut2<KIND> {
         uint4 *po = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + o);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            F8 a, x;
-            bf16x8_to_f8(d.a[2 * q + i], a);
-            if (p.add_mask.hi) {
-                F8 mk;
-                bf16x8_to_f8(d.m[2 * q + i], mk);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) x.v[k] = v[8 * i + k] + (mk.v[k] > 0.f ? a.v[k] : 0.f);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) x.v[k] = v[8 * i + k] + a.v[k];
-            }
-            po[i] = f8_to_bf16x8(x);
+            po[i] = f8_to_bf16x8(combine(d, 2 * q + i, p.add_mask.hi ? 1 : p.out_mask.hi ? 2 : 0, v + 8 * i));
         }
+    }
+};
+
+// EpiConvAdd with the residual gradient / mask rows staged into shared memory by TMA (warp 3 of
+// gemm_pk_kernel issues one 64-column x 128-row box of each per chunk, kEbufSlots chunks ahead):
+// the epilogue threads no longer wait on their own global loads (the ncu profile of the register
+// version: 40 % of warp samples in long-scoreboard stalls on those loads, 3.0 TB/s).  BN >= 128.
+template <int KIND>
+struct EpiConvAddT : EpiConvAdd<KIND> {
+    using Params = typename EpiConvOut2<KIND>::Params;
+    using DirectPre = typename EpiConvAdd<KIND>::DirectPre;
+    static constexpr bool kTmaAdd = true;
+    static constexpr int kEbufSlots = 3;
+    static constexpr int kStages = 2;  // mainloop ring depth (the operand ring takes the rest)
+    // the thread's row (64 columns) of a 128-byte-swizzled slot: residual at +0, mask at +16 KB
+    __device__ static void smem_load(const uint8_t *slot, int row, bool mask, DirectPre &d) {
+        const uint8_t *ra = slot + row * 128;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d.a[i] = *reinterpret_cast<const uint4 *>(ra + ((i ^ (row & 7)) << 4));
+        if (mask) {
+            const uint8_t *rm = ra + 16384;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d.m[i] = *reinterpret_cast<const uint4 *>(rm + ((i ^ (row & 7)) << 4));
+        }
+    }
+    // columns [16 q, 16 q + 16) of the chunk: accumulator + (masked) residual, written as bf16 over the
+    // residual in the slot (same swizzle: the slot's first 16 KB is then the output box of a TMA store)
+    __device__ static void smem_store(uint8_t *slot, int row, int q, int mask, const DirectPre &d,
+                                      const float (&v)[16]) {
+        uint8_t *ra = slot + row * 128;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            *reinterpret_cast<uint4 *>(ra + (((2 * q + i) ^ (row & 7)) << 4)) =
+                f8_to_bf16x8(EpiConvAdd<KIND>::combine(d, 2 * q + i, mask, v + 8 * i));
     }
 };
 
@@ -565,10 +620,9 @@ struct EpiHop2 {
         for (int i = 0; i < 32; i += 4)
             *reinterpret_cast<float4 *>(srow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     }
-    struct Pre {};
-    __device__ static Pre col_stats_pre(const Params &, int, int, int) { return Pre{}; }
+    __device__ static void col_stats_pre(const Params &, int, int, int, float *) {}
     template <int NTH>
-    __device__ static void col_stats(const Params &, const float *, int, int, int, int, int, Pre) {}
+    __device__ static void col_stats(const Params &, const float *, int, int, int, int, int, const float *) {}
     template <int NTH>
     __device__ static void col_stats_init(const Params &, int, int, int) {}
     template <int NTH>
@@ -1084,7 +1138,8 @@ static __global__ void avgpool_kernel(CTensor act, int B, int HW, int C, CTensor
 
 // d act[b, k, c] = dpooled[b][c] / HW (Y format), 4 channels per thread.
 template <int KIND>
-static __global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, int HW, int C, void *g) {
+static __global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, int HW, int C, void *g,
+                                               CTensor mask) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int C4 = C / 4;
@@ -1094,7 +1149,9 @@ static __global__ void avgpool_backward_kernel(const float *dp, int ldp, int B, 
         const int c = int(i % C4) * 4;
         const int64_t r = i / C4;
         const float *s = dp + (r / HW) * ldp + c;
-        st_y4<KIND>(g, size_t(r) * C + c, make_float4(s[0] * inv, s[1] * inv, s[2] * inv, s[3] * inv));
+        float4 v = make_float4(s[0] * inv, s[1] * inv, s[2] * inv, s[3] * inv);
+        if (mask.hi) v = relu_mask4(v, ld_c4<KIND>(mask, size_t(r) * C + c));  // the last block's ReLU
+        st_y4<KIND>(g, size_t(r) * C + c, v);
     }
 }
 

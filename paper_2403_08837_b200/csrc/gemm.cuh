@@ -24,6 +24,7 @@ struct GemmMaps {
     CUtensorMap a[3];
     CUtensorMap b[3];
     CUtensorMap o;  // output tile map of the TMA-store epilogue (gemm_pk_kernel, PkArgs::tma_out)
+    CUtensorMap e[2];  // epilogue operand maps (residual gradient, mask) of a kTmaAdd epilogue
 };
 
 // Implicit-GEMM convolution geometry (MODE 1-3 of gemm_tc_kernel).  Pixels

@@ -48,6 +48,9 @@ struct PkArgs {
     // 128-byte-swizzled shared staging area in 64-column chunks and written by TMA through maps.o
     // (2-D {N, M} for GM_PLAIN, 4-D {N, W, H, B} with the pixel box for FPROP / stride-1 DGRAD)
     int tma_out;
+    // TMA-staged epilogue operands (Epi::kTmaAdd): number of operand maps in GemmMaps::e (1: residual,
+    // 2: residual + mask); 2-D {N, M} maps for GM_PLAIN, 4-D {N, W, H, B} pixel-box maps otherwise
+    int tma_add;
     // Stride-2 data gradient with all sub-pixel phases in one launch (nph > 1): the batch index g of
     // a unit is its phase, cvp[g] its geometry (tap table, output phase offsets); no split-K.
     int nph;
@@ -60,9 +63,28 @@ struct pk_direct : std::false_type {};
 template <class E>
 struct pk_direct<E, std::void_t<decltype(E::kDirect)>> : std::bool_constant<E::kDirect> {};
 
+// Epilogues whose extra row operands (residual gradient, mask) are staged into shared memory by TMA
+// (warp 3 as their producer) declare kTmaAdd and kEbufSlots (ring slots of 64 columns x 128 rows of
+// both operands, 128-byte swizzled: 32 KB each).
+template <class E, class = void>
+struct pk_tma_add : std::false_type {};
+template <class E>
+struct pk_tma_add<E, std::void_t<decltype(E::kTmaAdd)>> : std::bool_constant<E::kTmaAdd> {};
+template <class E>
+constexpr int pk_ebuf_slots() {
+    if constexpr (pk_tma_add<E>::value)
+        return E::kEbufSlots;
+    else
+        return 0;
+}
+template <class E>
+constexpr int pk_ebuf_bytes() {
+    return pk_ebuf_slots<E>() * 32768;
+}
+
 __device__ __forceinline__ const ConvGeom &pk_geom(const PkArgs &a, int g) { return a.nph > 1 ? a.cvp[g] : a.cv; }
 
-template <int KIND, int BN, bool A_MN, bool B_MN, int ST>
+template <int KIND, int BN, bool A_MN, bool B_MN, int ST, int EB = 0>
 struct PkCfg {
     static constexpr int BM = 128;
     static constexpr int ELEM = KIND == 0 ? 2 : 4;
@@ -75,11 +97,14 @@ struct PkCfg {
     static constexpr int EPI_COLS = BN < 128 ? BN : 128;  // columns staged per epilogue pass
     static constexpr int LDS = EPI_COLS + 4;
     static constexpr int STILE_BYTES = 128 * LDS * 4;
+    // epilogue region: the fp32 shared tile, or (EB > 0) the TMA-staged epilogue operand ring
+    static constexpr int EPI_BYTES = EB > STILE_BYTES ? EB : STILE_BYTES;
     static constexpr int PART_BYTES = 4 * EPI_COLS * 3 * 4;  // per TMEM quarter column: up to 3 statistics
-    static constexpr int BUDGET = 220 * 1024 - STILE_BYTES - PART_BYTES - 2048;
+    static constexpr int BUDGET = 220 * 1024 - EPI_BYTES - PART_BYTES - 2048;
     static constexpr int STAGES = ST ? ST : (BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES);
     static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + STILE_BYTES + PART_BYTES + 512 + 256;
+    static constexpr int PRE_BYTES = 2 * 128 * 8;  // running column statistics of the unit (cp.async)
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + PART_BYTES + 512 + 256 + PRE_BYTES;
     static constexpr uint32_t IDESC = ptx::instr_desc(KIND == 0 ? 1u : 2u, A_MN, B_MN, 128, BN);
     static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN must be 64, 128 or 256");
     static_assert(!B_MN || BN % CH == 0, "MN-major B needs BN multiple of the 128-byte row");
@@ -157,7 +182,7 @@ template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE, int CL = 
 __global__ void __launch_bounds__(kPkThreads, 1)
     gemm_pk_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ PkArgs args,
                    const typename Epi::Params ep) {
-    using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages>;
+    using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages, pk_ebuf_bytes<Epi>()>;
     static_assert(CL == 1 || (CL == 2 && MODE != GM_BATCH && MODE != GM_DGRAD && B_MN && BN / C::CH >= 2),
                   "CTA pairs share an MN-major B tile of at least two chunks");
     const int rank = CL == 1 ? 0 : int(ptx::cluster_ctarank());
@@ -170,13 +195,20 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     uint8_t *sA = smem;
     uint8_t *sB = smem + C::STAGES * C::A_BYTES;
     float *stile = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
-    float *spart = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + C::STILE_BYTES);
-    int *rowm = reinterpret_cast<int *>(smem + C::STAGES * C::STAGE_BYTES + C::STILE_BYTES + C::PART_BYTES);
+    float *spart = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
+    int *rowm = reinterpret_cast<int *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + C::PART_BYTES);
     uint64_t *full = reinterpret_cast<uint64_t *>(rowm + 128);
     uint64_t *empty = full + C::STAGES;
     uint64_t *tfull = empty + C::STAGES;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    // TMA-staged epilogue operand ring (64-column halves of 128-column passes: BN >= 128)
+    constexpr int NES = C::EPI_COLS == 128 ? pk_ebuf_slots<Epi>() : 0;
+    uint64_t *efull = tempty + 2;
+    uint64_t *eempty = efull + NES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(eempty + NES);
+    float *spre = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(rowm) + 512 + 256);  // [2][128][2]
+    uint8_t *ebuf = smem + C::STAGES * C::STAGE_BYTES;
+    static_assert(C::STAGES * 2 + 4 + 2 * NES <= 30, "barrier area");
 
     const uint32_t warp = ptx::warp_id();
     if (warp == 0 && ptx::lane_id() == 0) {
@@ -193,6 +225,10 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
             ptx::mbar_init(&tempty[a], 1);
+        }
+        for (int a = 0; a < NES; ++a) {
+            ptx::mbar_init(&efull[a], 1);
+            ptx::mbar_init(&eempty[a], 4);  // the four TMEM-quarter warps of one column half
         }
         ptx::fence_barrier_init();
     }
@@ -295,6 +331,37 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 ptx::umma_commit(&tfull[acc]);
             }
         }
+    } else if (warp == 3) {
+        // epilogue operand producer (kTmaAdd): per unit, per 64-column chunk, one TMA box of the
+        // residual gradient (and one of its mask) into the next ring slot, as early as the ring allows
+        if constexpr (NES > 0) {
+            if (ptx::lane_id() == 0) {
+                constexpr int NCH = BN / 64;
+                const uint32_t bytes = args.tma_add == 2 ? 32768u : 16384u;
+                int seq = 0;
+                for (int u = first; u < args.units; u += stride) {
+                    int tm, tn, sp, g_;
+                    pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g_);
+                    int w0 = 0, h0 = 0, b0 = 0;
+                    if (args.boxed) conv_box_origin(args.cv, tm, w0, h0, b0);
+#pragma unroll 1
+                    for (int k = 0; k < NCH; ++k, ++seq) {
+                        const int slot = seq % NES;
+                        if (seq >= NES) ptx::mbar_wait(&eempty[slot], ((seq / NES) - 1) & 1);
+                        ptx::mbar_arrive_expect_tx(&efull[slot], bytes);
+                        uint8_t *dst = ebuf + slot * 32768;
+                        const int col = tn * BN + k * 64;
+#pragma unroll 1
+                        for (int o = 0; o < args.tma_add; ++o) {
+                            if (args.boxed)
+                                ptx::tma_load_4d(dst + o * 16384, &maps.e[o], &efull[slot], col, w0, h0, b0);
+                            else
+                                ptx::tma_load_2d(dst + o * 16384, &maps.e[o], &efull[slot], col, tm * 128);
+                        }
+                    }
+                }
+            }
+        }
     } else if (warp >= 4) {
         const int tid = threadIdx.x - 128;  // 0..255
         const int q = warp & 3;             // TMEM lane quarter this warp may access
@@ -325,12 +392,13 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             const int acc = j & 1;
             const bool split = args.splits > 1;
             const bool tma = Epi::kTmaStore && args.tma_out && !split;
-            typename Epi::Pre pre[BN / C::EPI_COLS];
-            if (!split) {
+            static_assert(BN / C::EPI_COLS <= 2 && C::EPI_COLS <= 128, "statistics prefetch slots");
+            if (!split) {  // the running statistics of the unit's columns, copied asynchronously (no register
+                           // waits on them; col_stats waits for the thread's own copies)
 #pragma unroll
                 for (int h = 0; h < BN / C::EPI_COLS; ++h) {
                     const int c0 = tn * BN + h * C::EPI_COLS;
-                    pre[h] = Epi::col_stats_pre(ep, c0, min(C::EPI_COLS, args.N - c0), tid);
+                    Epi::col_stats_pre(ep, c0, min(C::EPI_COLS, args.N - c0), tid, spre + h * 256);
                 }
             }
             if (tid < 128) {  // the previous unit's last barrier protects rowm / stile
@@ -338,7 +406,58 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 rowm[tid] = m;
                 if (!split) Epi::prefetch_row(ep, m, tn * BN, min(BN, args.N - tn * BN), out_off);
             }
-            if constexpr (pk_direct<Epi>::value) {  // the only epilogue of this instantiation (no split)
+            if constexpr (NES > 0) {  // direct epilogue on TMA-staged residual / mask rows (no split)
+                const int row_m = pk_row_m(args, tm, row, g);
+                typename Epi::DirectPre dp;
+                ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
+                ptx::tc_fence_after();
+                const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+#pragma unroll 1
+                for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+                    const int seq = j * (BN / 64) + 2 * h + half, slot = seq % NES;
+                    uint8_t *sl = ebuf + slot * 32768;
+                    const int mask = args.tma_add == 2 ? (ep.add_mask.hi ? 1 : 2) : 0;
+                    ptx::mbar_wait(&efull[slot], (seq / NES) & 1);
+                    Epi::smem_load(sl, row, mask != 0, dp);
+                    const int col = tn * BN + h * C::EPI_COLS + half * HC;
+                    if (args.tma_out) {  // output through the slot: bf16 over the residual, one TMA store
+#pragma unroll
+                        for (int qq = 0; qq < HC / 16; ++qq) {
+                            float v[16];
+                            ptx::tmem_ld16(taddr + h * C::EPI_COLS + half * HC + 16 * qq, v);
+                            Epi::smem_store(sl, row, qq, mask, dp, v);  // (mask: 0 none, 1 residual, 2 sum)
+                        }
+                        ptx::fence_proxy_async_smem();
+                        pk_bar(3 + half, 128);  // the half's four warps wrote their rows
+                        if (q == 0 && ptx::lane_id() == 0) {
+                            if (args.boxed) {
+                                int w0, h0, b0;
+                                conv_box_origin(args.cv, tm, w0, h0, b0);
+                                ptx::tma_store_4d(&maps.o, sl, col, w0, h0, b0);
+                            } else {
+                                ptx::tma_store_2d(&maps.o, sl, col, tm * 128);
+                            }
+                            ptx::bulk_commit();
+                            ptx::bulk_wait_read0();  // the slot is reusable once the store has read it
+                        }
+                        __syncwarp();
+                        if (ptx::lane_id() == 0) ptx::mbar_arrive(&eempty[slot]);
+                    } else {
+                        __syncwarp();
+                        if (ptx::lane_id() == 0) ptx::mbar_arrive(&eempty[slot]);
+#pragma unroll
+                        for (int qq = 0; qq < HC / 16; ++qq) {
+                            float v[16];
+                            ptx::tmem_ld16(taddr + h * C::EPI_COLS + half * HC + 16 * qq, v);
+                            Epi::direct_store(ep, row_m, col, qq, out_off, dp, v);
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                pk_bar(1, kPkEpi);
+                if (tid == 0) ptx::mbar_arrive(&tempty[acc]);  // accumulator free
+                continue;
+            } else if constexpr (pk_direct<Epi>::value) {  // the only epilogue of this instantiation (no split)
                 const int row_m = pk_row_m(args, tm, row, g);
                 typename Epi::DirectPre dp;
                 Epi::template direct_load<HC>(ep, row_m, tn * BN + half * HC, out_off, dp);  // before the accumulator
@@ -423,7 +542,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                         if (stats)
                             Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0,
                                                             min(C::EPI_COLS, args.N - col0), tm, tid,
-                                                            h == 0 ? pre[0] : pre[BN / C::EPI_COLS - 1]);
+                                                            spre + h * 256);
                         pk_bar(1, kPkEpi);  // spart reused by the next pass
                     }
                     continue;
@@ -462,8 +581,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     else
                         Epi::template run<kPkEpi, 0, true>(ep, stile, C::LDS, rowm, 128, col0, ncols, tm, args.N, tid,
                                                            out_off);
-                    Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, ncols, tm, tid,
-                                                    h == 0 ? pre[0] : pre[BN / C::EPI_COLS - 1]);
+                    Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0, ncols, tm, tid, spre + h * 256);
                 }
                 pk_bar(1, kPkEpi);  // shared tile reused by the next pass / unit
             }
@@ -472,6 +590,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         }
         if constexpr (Epi::kTmaStore)
             if (tid == 0) ptx::bulk_wait0();  // TMA stores complete before the CTA exits
+        if constexpr (NES > 0)
+            if (q == 0 && ptx::lane_id() == 0) ptx::bulk_wait0();  // the slot stores of both halves
     }
     ptx::tc_fence_before();
     if constexpr (CL == 1)
@@ -544,7 +664,7 @@ inline int split_min_kb() {
 // Grid choice and launch of gemm_pk_kernel for prepared args (units = tiles x splits).
 template <int KIND, int BN, bool A_MN, bool B_MN, class Epi, int MODE>
 struct PkLaunch {
-    using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages>;
+    using C = PkCfg<KIND, BN, A_MN, B_MN, Epi::kStages, pk_ebuf_bytes<Epi>()>;
     static constexpr bool kPairable = MODE != GM_BATCH && MODE != GM_DGRAD && B_MN && BN / C::CH >= 2;
 
     // Decide pairing (M tiles >= 2, pairable shape), fix up a.tiles_pm / a.units; returns the grid.
@@ -589,6 +709,52 @@ struct PkLaunch {
                 maps.o = make_tmap_4d(ep.out, ElemType::BF16, dims, str, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
             }
             a.tma_out = 1;
+        }
+    }
+    // TMA-staged epilogue operands (Epi::kTmaAdd): maps of the residual gradient and its mask with the
+    // output's tile geometry (boxes of 64 columns x the 128 tile rows).
+    static void setup_tma_add(GemmMaps &maps, PkArgs &a, const typename Epi::Params &ep) {
+        a.tma_add = 0;
+        if constexpr (pk_tma_add<Epi>::value) {
+            CDP_REQUIRE(a.splits == 1 && MODE != GM_BATCH && MODE != GM_WGRAD && BN >= 128 && a.N % BN == 0,
+                        "TMA-staged epilogue operands: unsplit plain / stride-1 conv tiles of 128 or 256 columns");
+            const uint64_t rs = uint64_t(ep.ld) * 2;
+            CDP_REQUIRE(!(ep.add_mask.hi && ep.out_mask.hi), "one mask per residual-add epilogue");
+            const void *src[2] = {ep.add, ep.add_mask.hi ? ep.add_mask.hi : ep.out_mask.hi};
+            const int n = src[1] ? 2 : 1;
+            for (int o = 0; o < n; ++o) {
+                if (MODE == GM_PLAIN) {
+                    maps.e[o] = make_tmap_2d(src[o], ElemType::BF16, uint64_t(a.N), uint64_t(a.M), rs, 64, 128);
+                } else {
+                    const ConvGeom &g = a.cv;
+                    CDP_REQUIRE(g.omul == 1 && g.oH == g.Ho && g.oW == g.Wo, "TMA-staged operands: stride-1 tiles");
+                    const uint64_t dims[4] = {uint64_t(a.N), uint64_t(g.Wo), uint64_t(g.Ho), uint64_t(g.Bn)};
+                    const uint64_t str[3] = {rs, rs * g.Wo, rs * g.Wo * g.Ho};
+                    const uint32_t box[4] = {64, uint32_t(g.bw), uint32_t(g.bh), uint32_t(g.bn)};
+                    const uint32_t es[4] = {1, 1, 1, 1};
+                    maps.e[o] = make_tmap_4d(src[o], ElemType::BF16, dims, str, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
+                }
+            }
+            a.tma_add = n;
+            // output boxes stored from the slots (CDP_TMA_ADD_STORE=0: direct 16-byte stores)
+            static const bool st_on = [] {
+                const char *e = std::getenv("CDP_TMA_ADD_STORE");
+                return !(e && e[0] == '0');
+            }();
+            a.tma_out = 0;
+            if (st_on && (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0) {
+                if (MODE == GM_PLAIN) {
+                    maps.o = make_tmap_2d(ep.out, ElemType::BF16, uint64_t(a.N), uint64_t(a.M), rs, 64, 128);
+                } else {
+                    const ConvGeom &g = a.cv;
+                    const uint64_t dims[4] = {uint64_t(a.N), uint64_t(g.Wo), uint64_t(g.Ho), uint64_t(g.Bn)};
+                    const uint64_t str[3] = {rs, rs * g.Wo, rs * g.Wo * g.Ho};
+                    const uint32_t box[4] = {64, uint32_t(g.bw), uint32_t(g.bh), uint32_t(g.bn)};
+                    const uint32_t es[4] = {1, 1, 1, 1};
+                    maps.o = make_tmap_4d(ep.out, ElemType::BF16, dims, str, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
+                }
+                a.tma_out = 1;
+            }
         }
     }
     static void set_attr() {

@@ -559,6 +559,7 @@ struct ResNetTrainer {
         const int grid = PL::prepare(a, sms(), paired);
         GemmMaps maps = gp.maps;
         PL::setup_tma_out(maps, a, ep);
+        PL::setup_tma_add(maps, a, ep);
         last_stat_slots = a.splits > 1 ? a.tiles_m * slots_per_tile : grid;  // EpiConvOut2 statistics rows
         last_grid = grid;
         L(name, flops, take_bytes(), s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
@@ -825,7 +826,7 @@ struct ResNetTrainer {
         const int nblk = int((c.P + rows_blk - 1) / rows_blk);
         const int C4 = c.cout / 4, TPR = C4 < 32 ? C4 : 32;
         const ConvL *cd = ds >= 0 ? &convs[ds] : nullptr;
-        const double bytes = double(c.P) * c.cout * (ysz() + esz() + ysz() + (cd ? ysz() : 0));
+        const double bytes = double(c.P) * c.cout * (ysz() + (mask.hi ? esz() : 0) + ysz() + (cd ? ysz() : 0));
         L("bn_bwd_stats", 0, bytes, s, [&] {
             auto kern = rows_blk == kBnRowsMin ? bn_bwd_stats_kernel<K, kBnRowsMin> : bn_bwd_stats_kernel<K, kBnRows>;
             launch_pdl(kern, dim3(nblk, (C4 + TPR - 1) / TPR), dim3(256), 0, s, g, mask, c.P,
@@ -852,7 +853,7 @@ struct ResNetTrainer {
         ConvL &cc = convs[ci];
         const int vslot = vs(cc.tb, p);
         rec(cc.tb, A_BWD, 0, vslot, s);
-        L("bn_bwd_apply", 0, double(cc.P) * cc.cout * (2 * ysz() + 2 * esz()), s, [&] {
+        L("bn_bwd_apply", 0, double(cc.P) * cc.cout * (2 * ysz() + (mask.hi ? 2 : 1) * esz()), s, [&] {
             launch_pdl(mask.hi ? bn_bwd_apply_kernel<K, true> : bn_bwd_apply_kernel<K, false>,
                        dim3(blocks_for(cc.P * cc.cout / 8)), dim3(256), 0, s, g, mask,
                        (const void *)cc.y.p, cc.P, cc.cout, (const float *)cc.mean.as<float>(),
@@ -868,11 +869,16 @@ struct ResNetTrainer {
         ep.ld = ld;
         return ep;
     }
+    // the TMA-staged residual-add epilogue exists for bf16 (KIND 0) only
+    template <int K, class F>
+    static void pk_tadd(F &&f) {
+        if constexpr (K == 0) f(EpiConvAddT<0>{});
+    }
     // conv data gradient into g_in (fp32 [Pin][cin]).
     // add != null: g_in = dgrad + (add masked by add_mask) (the block's residual branch).
     template <int K>
     void conv_dgrad(int ci, int vslot, void *g_in, cudaStream_t s, const void *add = nullptr,
-                    CTensor add_mask = CTensor{}) {
+                    CTensor add_mask = CTensor{}, CTensor out_mask = CTensor{}) {
         ConvL &c = convs[ci];
         zrecv<K>(c.tw, 1, s);
         const CBuf &w = wc[vslot][c.tw];
@@ -881,15 +887,25 @@ struct ResNetTrainer {
         ep.stats = nullptr;
         ep.add = add;
         ep.add_mask = add_mask;
+        ep.out_mask = out_mask;
         gemm_bytes = double(c.P) * c.cout * esz() + double(c.K) * c.cout * esz() + double(c.Pin) * c.cin * ysz() +
-                     (add ? double(c.Pin) * c.cin * (ysz() + (add_mask.hi ? esz() : 0)) : 0.0);
+                     (add ? double(c.Pin) * c.cin * ysz() : 0.0) +
+                     double(c.Pin) * c.cin * esz() * ((add_mask.hi ? 1 : 0) + (out_mask.hi ? 1 : 0));
         // residual-gradient add: the direct (register) epilogue, its own GEMM instantiation
         const bool direct = EpiConvAdd<K>::eligible(ep_with(ep, g_in, c.cin), c.cin, tile_n(c.cin)) &&
                             std::getenv("CDP_NO_DIRECT_ADD") == nullptr;
+        // residual / mask rows staged by TMA (tiles of 128 / 256 columns; CDP_NO_TMA_ADD=1 disables)
+        static const bool tma_add_on = std::getenv("CDP_NO_TMA_ADD") == nullptr;
+        const bool tadd = K == 0 && direct && tma_add_on && tile_n(c.cin) >= 128 && c.impl == CI_PLAIN;
         if (c.impl == CI_PLAIN) {
             ep.out = g_in;
             ep.ld = c.cin;
-            if (direct)
+            if (tadd)
+                pk_tadd<K>([&](auto e) {
+                    pk_plain<K, false, false, decltype(e)>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(),
+                                                           c.P, c.cin, c.cout, ep, s, false);
+                });
+            else if (direct)
                 pk_plain<K, false, false, EpiConvAdd<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(), c.P,
                                                          c.cin, c.cout, ep, s, false);
             else
@@ -898,7 +914,9 @@ struct ResNetTrainer {
         } else if (c.stride == 1) {
             ep.out = g_in;
             ep.ld = c.cin;
-            if (direct)
+            if (tadd)
+                pk_tadd<K>([&](auto e) { pk_conv<K, GM_DGRAD, decltype(e)>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false); });
+            else if (direct)
                 pk_conv<K, GM_DGRAD, EpiConvAdd<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
             else
                 pk_conv<K, GM_DGRAD, EpiConvOut2<K>>("conv_dgrad", tile_n(c.cin), c, w, ep, s, false);
@@ -1191,14 +1209,14 @@ struct ResNetTrainer {
         const int HW = int(act_P[la] / B);
         L("avgpool_bwd", 0, double(act_P[la]) * fc_in * ysz(), cs, [&] {
             launch_pdl(avgpool_backward_kernel<K>, dim3(blocks_for(act_P[la] * fc_in / 4)), dim3(256), 0, cs,
-                       (const float *)dpooled.as<float>(), fc_in, B, HW, fc_in, G0);
+                       (const float *)dpooled.as<float>(), fc_in, B, HW, fc_in, G0, acts[la].view());
         });
         for (int bi = int(blocks.size()) - 1; bi >= 0; --bi) {
             BlockL &b = blocks[bi];
             const int n = int(b.convs.size());
-            const CTensor m_out = acts[b.a_out].view();
-            // last BN (+ projection BN): g' = G0 masked by the block output
-            bn_backward<K>(b.convs[n - 1], b.ds, p, G0, m_out, cs);
+            // last BN (+ projection BN): g' = G0, already masked by the block output's ReLU by its producer
+            // (the average-pool backward, or the next block's input data gradient)
+            bn_backward<K>(b.convs[n - 1], b.ds, p, G0, CTensor{}, cs);
             cudaEvent_t dy_last = ev(cs);
             // projection shortcut first: its data gradient is folded into the first conv's
             if (b.ds >= 0) {
@@ -1218,11 +1236,10 @@ struct ResNetTrainer {
                     bn_backward<K>(b.convs[i - 1], -1, p, out, acts[b.mid[i - 1]].view(), cs);
                     dy_next = ev(cs);
                 } else {
-                    // block input gradient = main branch + shortcut branch, written over G0
-                    if (b.ds >= 0)
-                        conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, G3, CTensor{});
-                    else
-                        conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, G0, m_out);
+                    // block input gradient = main branch + shortcut branch, written over G0 and masked by
+                    // the previous block's output ReLU (its BN backward and residual then read no mask)
+                    conv_dgrad<K>(ci, vs(convs[ci].tw, p), G0, cs, b.ds >= 0 ? G3 : G0, CTensor{},
+                                  acts[b.a_in].view());
                     cudaEvent_t dg = ev(cs);
                     hop_conv<K>(ci, p, dy_next, dg);
                 }
