@@ -430,6 +430,25 @@ struct EpiConvOut2 {
         ptx::cp_async8(slot + 2 * tid, p.stats + (size_t(col0 + tid) * gridDim.x + blockIdx.x) * 2);
         ptx::cp_async_commit();
     }
+    // TMA-store epilogue: the unit's column sums were reduced from the bf16 staging tile into
+    // part[8 warps][pcols][2] (gemm_pk_kernel, pk_tile_stats); thread `tid` adds its column's eight
+    // warp partials in warp order to the running value.
+    __device__ static void col_stats8(const Params &p, const float *part, int pcols, int col0, int ncols, int tid,
+                                      const float *slot) {
+        if (p.stats && tid < ncols) {
+            ptx::cp_async_wait_all();
+            const float2 cur = *reinterpret_cast<const float2 *>(slot + 2 * tid);
+            float s = 0.f, q = 0.f;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const float2 t = *reinterpret_cast<const float2 *>(part + (w * pcols + tid) * 2);
+                s += t.x;
+                q += t.y;
+            }
+            *reinterpret_cast<float2 *>(p.stats + (size_t(col0 + tid) * gridDim.x + blockIdx.x) * 2) =
+                make_float2(cur.x + s, cur.y + q);
+        }
+    }
     template <int NTH>  // one column per thread (ncols <= NTH)
     __device__ static void col_stats(const Params &p, const float *part, int pcols, int col0, int ncols, int tm,
                                      int tid, const float *slot) {

@@ -99,8 +99,9 @@ struct PkCfg {
     static constexpr int STILE_BYTES = 128 * LDS * 4;
     // epilogue region: the fp32 shared tile, or (EB > 0) the TMA-staged epilogue operand ring
     static constexpr int EPI_BYTES = EB > STILE_BYTES ? EB : STILE_BYTES;
-    static constexpr int PART_BYTES = 4 * EPI_COLS * 3 * 4;  // per TMEM quarter column: up to 3 statistics
-    static constexpr int BUDGET = 220 * 1024 - EPI_BYTES - PART_BYTES - 2048;
+    // per TMEM quarter column up to 3 statistics (drain path), or [8 warps][EPI_COLS][2] (TMA-store path)
+    static constexpr int PART_BYTES = (4 * EPI_COLS * 3 * 4 > 8 * EPI_COLS * 8) ? 4 * EPI_COLS * 3 * 4 : 8 * EPI_COLS * 8;
+    static constexpr int BUDGET = 224 * 1024 - EPI_BYTES - PART_BYTES - 2048;
     static constexpr int STAGES = ST ? ST : (BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES);
     static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
     static constexpr int PRE_BYTES = 2 * 128 * 8;  // running column statistics of the unit (cp.async)
@@ -130,6 +131,47 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
         }
     }
     return v[0];
+}
+
+// Per-column (sum, sum of squares) of the valid rows of one 128-row x 128-column bf16 staging pass
+// (two 128-byte-swizzled boxes of 64 columns), read back from shared memory: thread tid takes the
+// 8-column chunk tid % 16 of rows 8 (tid / 16) .. + 7 (one conflict-free 16-byte read per row), the two
+// row groups of a warp are combined by one shuffle level, and part[w][col][2] gets warp w's partial.
+// The statistics are those of the stored bf16 outputs; about 4 instructions per element against ~11
+// for the TMEM-register butterfly (FSEL / SHFL: 55 % of the 1x1 forward epilogue's instructions).
+__device__ __forceinline__ void pk_tile_stats(const uint8_t *buf, const int *rowm, float *part, int tid) {
+    const int cg = tid & 15, rg = tid >> 4, k = cg >> 3, j = cg & 7;
+    const int4 rm0 = *reinterpret_cast<const int4 *>(rowm + 8 * rg);
+    const int4 rm1 = *reinterpret_cast<const int4 *>(rowm + 8 * rg + 4);
+    const int rv[8] = {rm0.x, rm0.y, rm0.z, rm0.w, rm1.x, rm1.y, rm1.z, rm1.w};
+    float sm[8], sq[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sm[c] = sq[c] = 0.f;
+    const uint8_t *base = buf + k * 16384 + (8 * rg) * 128;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(base + i * 128 + ((j ^ i) << 4));
+        if (rv[i] < 0) continue;
+        const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float lo = __uint_as_float(u[e] << 16), hi = __uint_as_float(u[e] & 0xffff0000u);
+            sm[2 * e] += lo;
+            sq[2 * e] = fmaf(lo, lo, sq[2 * e]);
+            sm[2 * e + 1] += hi;
+            sq[2 * e + 1] = fmaf(hi, hi, sq[2 * e + 1]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], 16);
+        sq[c] += __shfl_xor_sync(0xffffffffu, sq[c], 16);
+    }
+    if ((tid & 16) == 0) {
+        float4 *o = reinterpret_cast<float4 *>(part + ((tid >> 5) * 128 + cg * 8) * 2);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = make_float4(sm[2 * c], sq[2 * c], sm[2 * c + 1], sq[2 * c + 1]);
+    }
 }
 
 __device__ __forceinline__ void pk_unit(const PkArgs &a, int u, int &tm, int &tn, int &split, int &g) {
@@ -506,15 +548,17 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                                 w.w = pk_bf16x2(v[8 * i + 6], v[8 * i + 7]);
                                 *reinterpret_cast<uint4 *>(rp + (((u0 + i) ^ (row & 7)) << 4)) = w;
                             }
-                            if (stats) {  // squares in place, then the values again from TMEM (32 live)
-                                float *pp = spart + (q * C::EPI_COLS + c + ptx::lane_id()) * 3;
+                            if constexpr (C::EPI_COLS != 128) {
+                                if (stats) {  // squares in place, then the values again from TMEM (32 live)
+                                    float *pp = spart + (q * C::EPI_COLS + c + ptx::lane_id()) * 3;
 #pragma unroll
-                                for (int i = 0; i < 32; ++i) v[i] = row_m >= 0 ? v[i] * v[i] : 0.f;
-                                pp[1] = warp_colsum32(v);
-                                ptx::tmem_ld32(taddr + uc, v);
+                                    for (int i = 0; i < 32; ++i) v[i] = row_m >= 0 ? v[i] * v[i] : 0.f;
+                                    pp[1] = warp_colsum32(v);
+                                    ptx::tmem_ld32(taddr + uc, v);
 #pragma unroll
-                                for (int i = 0; i < 32; ++i) v[i] = row_m >= 0 ? v[i] : 0.f;
-                                pp[0] = warp_colsum32(v);
+                                    for (int i = 0; i < 32; ++i) v[i] = row_m >= 0 ? v[i] : 0.f;
+                                    pp[0] = warp_colsum32(v);
+                                }
                             }
                         }
                         ptx::fence_proxy_async_smem();  // staging writes -> async proxy (TMA store)
@@ -539,11 +583,19 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                             ptx::bulk_commit();
                             ptx::bulk_wait_read1();  // the other buffer (previous pass) is free again
                         }
-                        if (stats)
-                            Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0,
-                                                            min(C::EPI_COLS, args.N - col0), tm, tid,
-                                                            spre + h * 256);
-                        pk_bar(1, kPkEpi);  // spart reused by the next pass
+                        if (stats) {
+                            if constexpr (C::EPI_COLS == 128) {  // from the stored bf16 tile (staging read-back)
+                                pk_tile_stats(buf, rowm, spart, tid);
+                                pk_bar(1, kPkEpi);
+                                Epi::col_stats8(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), tid,
+                                                spre + h * 256);
+                            } else {
+                                Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0,
+                                                                min(C::EPI_COLS, args.N - col0), tm, tid,
+                                                                spre + h * 256);
+                            }
+                        }
+                        pk_bar(1, kPkEpi);  // spart / staging reused by the next pass
                     }
                     continue;
                 }
