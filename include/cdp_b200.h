@@ -283,6 +283,14 @@ int cdp_vit_stats(cdp_vit *tr, int64_t *out, int n_out);
 int cdp_vit_mark(cdp_vit *tr, int k);
 int cdp_vit_elapsed(cdp_vit *tr, int a, int b, float *ms);
 int cdp_vit_flush_l2(cdp_vit *tr);
+/* Fused multi-head attention (csrc/attn_kernels.cuh) on caller-owned device buffers: bf16 token-major
+ * qkv [B*T][qkv_ld] (Q | K | V blocks of H*64 columns, head h at +h*64), O [B*T][o_ld], lse fp32
+ * [B*H*T]; backward != 0 also writes dQ | dK | dV into dqkv from dO.  T <= 256, head dim 64, scale 1/8.
+ * No reference counterpart (the reference trains no attention model): the ViT trainer's layer compute
+ * (north_star (4)), exported for its parity tests. */
+int cdp_attention(const void *qkv, int64_t qkv_ld, const void *dout, int64_t dout_ld, int T, int H, int B, void *o,
+                  int64_t o_ld, float *lse, void *dqkv, int64_t dqkv_ld, int backward);
+
 
 /* ---- tensor-core GEMM self-test (parity tests of the tcgen05 kernel) --- */
 /* D[m][n] = sum_s A_s . B_s.  kind 0 = bf16, 1 = fp32/tf32.  A K-major:

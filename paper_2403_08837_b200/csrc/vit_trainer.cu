@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/cdp_b200.h"
+#include "attn_kernels.cuh"
 #include "gemm_launch.cuh"
 #include "rank_common.cuh"
 #include "trainer_common.cuh"
@@ -47,10 +48,11 @@ struct VRec {
     DevBuf h, hmid;                   // fp32 residual stream: block input, after attention
     DevBuf m1, r1, m2, r2;            // LayerNorm row statistics
     CBuf u1, u2, attn, g1, qkvb, z1;  // LN outputs, attention output, GELU output, qkv, FC1 pre-activation
-    DevBuf P;                         // softmax probabilities bf16 [B*H][T][ldp]
+    DevBuf P;                         // unfused attention: softmax probabilities bf16 [B*H][T][ldp]
+    DevBuf lse;                       // fused attention: row log-sum-exp fp32 [B*H][T]
     size_t bytes() const {
         return h.bytes + hmid.bytes + m1.bytes + r1.bytes + m2.bytes + r2.bytes + u1.hi.bytes + u2.hi.bytes +
-               attn.hi.bytes + g1.hi.bytes + qkvb.hi.bytes + z1.hi.bytes + P.bytes;
+               attn.hi.bytes + g1.hi.bytes + qkvb.hi.bytes + z1.hi.bytes + P.bytes + lse.bytes;
     }
 };
 struct ERec {  // embedding record: the patch matrix [x, 1] (the patch weight gradient's operand)
@@ -110,6 +112,7 @@ struct VitTrainer {
     int u_patch = 0, u_cls = 0, u_pos = 0, u_ln = 0, u_head = 0;
     int64_t Pn = 0, Pp = 0;
     int R = 0, lds = 0, ldp = 0;
+    bool fused_attn = true;
     // step plan (W > 1): ops in timeline order, record slot of (worker, segment), pool sizes
     std::vector<VOp> plan;
     std::vector<std::vector<uint8_t>> freshw;  // [worker][unit]
@@ -230,6 +233,9 @@ struct VitTrainer {
         R = B * T;
         lds = round_up(T, 4);
         ldp = round_up(T, 16);
+        // fused attention (attn_kernels.cuh): one key tile, T <= 256 (CDP_VIT_UNFUSED=1: batched GEMMs +
+        // row-softmax kernels)
+        fused_attn = T <= 256 && std::getenv("CDP_VIT_UNFUSED") == nullptr;
         const int K0 = P * P * 3;
         u_patch = add_unit(V_LIN, int64_t(K0 + 1) * D, K0 + 1, D);
         u_cls = add_unit(V_VEC, D, 0, 0);
@@ -275,7 +281,10 @@ struct VitTrainer {
             ones(y.g1, R, F);
             y.qkvb = make_cbuf(0, R, 3 * D);
             y.z1 = make_cbuf(0, R, F);
-            y.P = DevBuf(size_t(B) * H * T * ldp * 2);
+            if (fused_attn)
+                y.lse = DevBuf(size_t(B) * H * T * 4);
+            else
+                y.P = DevBuf(size_t(B) * H * T * ldp * 2);
         }
         frec.resize(pool[2]);
         for (auto &f : frec) {
@@ -306,9 +315,11 @@ struct VitTrainer {
         loss_w = DevBuf(size_t(W) * 8);
         loss_dev = DevBuf(8);
         loss_rows = DevBuf(size_t(B) * 8);
-        S = DevBuf(size_t(B) * H * T * lds * 4);
-        dP = DevBuf(size_t(B) * H * T * lds * 4);
-        dS = make_cbuf(0, B * H * T, T);  // ld = ldp
+        if (!fused_attn) {
+            S = DevBuf(size_t(B) * H * T * lds * 4);
+            dP = DevBuf(size_t(B) * H * T * lds * 4);
+            dS = make_cbuf(0, B * H * T, T);  // ld = ldp
+        }
         du = DevBuf(size_t(R) * D * 4);
         duf = DevBuf(size_t(B) * D * 4);
         dhm = DevBuf(size_t(R) * D * 4);
@@ -432,6 +443,69 @@ struct VitTrainer {
             } else {
                 throw CdpError("unsupported GEMM tile width");
             }
+        });
+    }
+
+    // ---------------------------------------------------------------- fused attention
+    // 4-D TMA view {64 dims, T tokens, H heads, B samples} of a token-major bf16 buffer (row stride ld)
+    CUtensorMap attn_map(const void *ptr, int64_t ld, int box_rows) const {
+        const uint64_t dims[4] = {uint64_t(HD), uint64_t(T), uint64_t(H), uint64_t(B)};
+        const uint64_t st[3] = {uint64_t(ld) * 2, uint64_t(HD) * 2, uint64_t(T) * ld * 2};
+        const uint32_t box[4] = {64u, uint32_t(box_rows), 1u, 1u};
+        const uint32_t es[4] = {1u, 1u, 1u, 1u};
+        return make_tmap_4d(ptr, ElemType::BF16, dims, st, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    AttnMaps attn_maps(const VRec &y) const {
+        AttnMaps m;
+        std::memset(&m, 0, sizeof(m));
+        const int64_t qld = y.qkvb.ld;
+        const __nv_bfloat16 *qkv = static_cast<const __nv_bfloat16 *>(y.qkvb.hi.p);
+        m.q = attn_map(qkv, qld, 128);
+        m.k = attn_map(qkv + D, qld, 256);
+        m.v = attn_map(qkv + 2 * D, qld, 256);
+        m.dout = attn_map(dattn.hi.p, dattn.ld, 128);
+        return m;
+    }
+    AttnArgs attn_args(const VRec &y) const {
+        AttnArgs a{};
+        a.T = T;
+        a.H = H;
+        a.B = B;
+        a.scale = 1.f / std::sqrt(float(HD));
+        a.o = static_cast<__nv_bfloat16 *>(y.attn.hi.p);
+        a.o_ld = y.attn.ld;
+        a.lse = y.lse.as<float>();
+        return a;
+    }
+    void attention_fwd(const VRec &y, cudaStream_t s) {
+        const double tt = double(T) * T * HD * B * H;
+        L_("attention", 4.0 * tt, double(R) * D * 2 * 4 + double(B) * H * T * 4, s, [&] {
+            static bool attr = false;
+            if (!attr) {
+                CDP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              kAttnFwdSmem));
+                attr = true;
+            }
+            launch_pdl(attn_fwd_kernel, dim3(B * H), dim3(kAttnThreads), kAttnFwdSmem, s, attn_maps(y), attn_args(y));
+        });
+    }
+    void attention_bwd(const VRec &y, const CBuf &dqkv, cudaStream_t s) {
+        const double tt = double(T) * T * HD * B * H;
+        AttnArgs a = attn_args(y);
+        a.dout = static_cast<const __nv_bfloat16 *>(dattn.hi.p);
+        a.dout_ld = dattn.ld;
+        a.dqkv = static_cast<__nv_bfloat16 *>(dqkv.hi.p);
+        a.dqkv_ld = dqkv.ld;
+        a.dk_off = D;
+        a.dv_off = 2 * D;
+        L_("attention_bwd", 10.0 * tt, double(R) * D * 2 * 8 + double(B) * H * T * 4, s, [&] {
+            static bool attr = false;
+            if (!attr) {
+                CDP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              kAttnBwdSmem));
+                attr = true;
+            }
+            launch_pdl(attn_bwd_kernel, dim3(B * H), dim3(kAttnThreads), kAttnBwdSmem, s, attn_maps(y), a);
         });
     }
 
@@ -737,6 +811,9 @@ struct VitTrainer {
         const BView Kv{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + D, HD, T, qld, HD, int64_t(T) * qld};
         const BView V{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + 2 * D, HD, T, qld, HD, int64_t(T) * qld};
         const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+        if (fused_attn) {
+            attention_fwd(y, s);
+        } else {
         bgemm<false, false>("attn_scores", Q, Kv, T, T, HD, S.p, lds, int64_t(H) * T * lds, int64_t(T) * lds, 1, s);
         L_("softmax", 0, double(B) * H * T * T * 6, s, [&] {
             const dim3 g((B * H * T * 32 + 255) / 256);
@@ -750,6 +827,7 @@ struct VitTrainer {
                 launch_pdl(softmax_fwd_kernel, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
         });
         bgemm<false, true>("attn_values", Pv, V, T, HD, T, y.attn.hi.p, y.attn.ld, int64_t(T) * y.attn.ld, HD, 0, s);
+        }
         {
             typename EpiConvOut2<0>::Params ep{};
             ep.out = y.hmid.p;
@@ -915,6 +993,10 @@ struct VitTrainer {
         auto qv = [&](int col) {
             return BView{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + col, HD, T, qld, HD, int64_t(T) * qld};
         };
+        const int64_t dld = gr.dqkv.ld;
+        if (fused_attn) {
+            attention_bwd(y, gr.dqkv, cs);
+        } else {
         const BView dO{dattn.hi.p, HD, T, dattn.ld, HD, int64_t(T) * dattn.ld};
         const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
         const BView dSv{dS.hi.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
@@ -933,10 +1015,10 @@ struct VitTrainer {
                 launch_pdl(softmax_bwd_kernel, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
         });
         __nv_bfloat16 *dq = static_cast<__nv_bfloat16 *>(gr.dqkv.hi.p);
-        const int64_t dld = gr.dqkv.ld;
         bgemm<true, true>("attn_dvalues", Pv, dO, T, HD, T, dq + 2 * D, int(dld), int64_t(T) * dld, HD, 0, cs);
         bgemm<false, true>("attn_dquery", dSv, qv(D), T, HD, T, dq, int(dld), int64_t(T) * dld, HD, 0, cs);
         bgemm<true, true>("attn_dkey", dSv, qv(0), T, HD, T, dq + D, int(dld), int64_t(T) * dld, HD, 0, cs);
+        }
         cudaEvent_t dqkv_ready = ev(cs);
         {
             typename EpiConvOut2<0>::Params ep{};
@@ -1452,5 +1534,56 @@ extern "C" int cdp_vit_flush_l2(cdp_vit *tr) {
         auto &m = *tr->impl;
         if (!m.flush_buf.p) m.flush_buf = DevBuf(size_t(256) << 20);
         CDP_CUDA(cudaMemsetAsync(m.flush_buf.p, m.t & 0xff, m.flush_buf.bytes, m.main));
+    });
+}
+
+// Fused attention on caller-owned device buffers (tests / tools): forward O = softmax(Q K^T / 8) V and
+// the row log-sum-exp; with backward != 0 also dQ, dK, dV from dO into dqkv (Q | K | V column blocks
+// of width H * 64, like qkv).  Synchronous.
+extern "C" int cdp_attention(const void *qkv, int64_t qkv_ld, const void *dout, int64_t dout_ld, int T, int H, int B,
+                             void *o, int64_t o_ld, float *lse, void *dqkv, int64_t dqkv_ld, int backward) {
+    using namespace cdp;
+    return guarded([&] {
+        CDP_REQUIRE(T >= 1 && T <= 256 && H >= 1 && B >= 1, "fused attention: 1 <= T <= 256");
+        CDP_REQUIRE(qkv_ld % 8 == 0 && o_ld % 8 == 0 && (!backward || (dout_ld % 8 == 0 && dqkv_ld % 8 == 0)),
+                    "row strides must be multiples of 8 elements");
+        const int64_t D = int64_t(H) * 64;
+        auto map = [&](const void *ptr, int64_t ld, int rows) {
+            const uint64_t dims[4] = {64u, uint64_t(T), uint64_t(H), uint64_t(B)};
+            const uint64_t st[3] = {uint64_t(ld) * 2, 128u, uint64_t(T) * ld * 2};
+            const uint32_t box[4] = {64u, uint32_t(rows), 1u, 1u};
+            const uint32_t es[4] = {1u, 1u, 1u, 1u};
+            return make_tmap_4d(ptr, ElemType::BF16, dims, st, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
+        };
+        AttnMaps m;
+        std::memset(&m, 0, sizeof(m));
+        const __nv_bfloat16 *q = static_cast<const __nv_bfloat16 *>(qkv);
+        m.q = map(q, qkv_ld, 128);
+        m.k = map(q + D, qkv_ld, 256);
+        m.v = map(q + 2 * D, qkv_ld, 256);
+        if (backward) m.dout = map(dout, dout_ld, 128);
+        AttnArgs a{};
+        a.T = T;
+        a.H = H;
+        a.B = B;
+        a.scale = 0.125f;
+        a.o = static_cast<__nv_bfloat16 *>(o);
+        a.o_ld = o_ld;
+        a.lse = lse;
+        CDP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnFwdSmem));
+        attn_fwd_kernel<<<B * H, kAttnThreads, kAttnFwdSmem>>>(m, a);
+        CDP_CUDA(cudaGetLastError());
+        if (backward) {
+            a.dout = static_cast<const __nv_bfloat16 *>(dout);
+            a.dout_ld = dout_ld;
+            a.dqkv = static_cast<__nv_bfloat16 *>(dqkv);
+            a.dqkv_ld = dqkv_ld;
+            a.dk_off = D;
+            a.dv_off = 2 * D;
+            CDP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnBwdSmem));
+            attn_bwd_kernel<<<B * H, kAttnThreads, kAttnBwdSmem>>>(m, a);
+            CDP_CUDA(cudaGetLastError());
+        }
+        CDP_CUDA(cudaDeviceSynchronize());
     });
 }

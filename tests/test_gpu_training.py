@@ -181,3 +181,27 @@ def test_cdp_activation_memory_below_dp(cuda):
     cdp = DeviceMlpTrainer(dims, 32, 4, 1, min_delay_rule(4), dtype="bf16")
     a_dp, a_cdp = dp.stats()["activation_bytes"], cdp.stats()["activation_bytes"]
     assert a_cdp * 16 == a_dp * 10  # N(N+1)/2 vs N^2 records at N = 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("mom", [0.0, 0.9])
+def test_weight_decay_vs_oracle(cuda, mom, dtype):
+    """SGD(+momentum) with weight decay fused into the last hop (g = acc / N + wd * theta_t) against the
+    oracle's `weight_decay` extension of the reference step (oracle/engine.py; the reference engine has none)."""
+    from oracle import engine as OE
+    from paper_2403_08837_b200.training import make_mlp_task, run_experiment
+
+    kw = dict(n=4, micro_batch_size=8, seed=9, width=32, in_dim=24, out_dim=5, loss_kind="xent")
+    res = run_experiment(make_mlp_task(**kw), steps=15, lr=0.05, momentum=mom, dtype=dtype, weight_decay=0.02)
+    ref = OE.run_experiment(OE.make_mlp_task(**kw), steps=15, lr=0.05, momentum=mom, weight_decay=0.02)
+    base = run_experiment(make_mlp_task(**kw), steps=15, lr=0.05, momentum=mom, dtype=dtype)
+    t = TOL[dtype]
+    for rule in ("dp", "cdp-v1", "cdp-v2"):
+        got = np.concatenate(res.runs[rule].final_params)
+        assert rel_l2(got, np.concatenate(ref[rule].final_params)) <= t["theta"], rule
+        ref_l = np.array(ref[rule].losses)
+        assert np.all(np.abs(np.array(res.runs[rule].losses) - ref_l) <= t["theta"] * np.abs(ref_l) + 1e-7), rule
+        # the decay is not a no-op at the fp32 tolerance (the bf16 one is of the size of the decay's effect)
+        if dtype == "fp32":
+            assert rel_l2(got, np.concatenate(base.runs[rule].final_params)) > 100 * t["theta"], rule
