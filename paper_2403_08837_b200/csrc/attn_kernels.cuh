@@ -1,6 +1,6 @@
 // Fused multi-head attention for the ViT trainer (sm_100a, bf16 operands, fp32 TMEM accumulators).
 //
-// One CTA per (head, sample).  The whole key range of a ViT-B/16 sequence (T = 197 <= 256) is one
+// Forward: one CTA per (query tile, head, sample); backward: one per (head, sample).  The whole key range of a ViT-B/16 sequence (T = 197 <= 256) is one
 // tile, so the softmax is exact in one pass over a 128 x 256 score tile held in TMEM — no online
 // rescaling — and only the per-row log-sum-exp leaves the forward (the backward recomputes the
 // probabilities from it, flash-attention style).  Replaces the batched score / value GEMMs, the
@@ -38,7 +38,7 @@ struct AttnArgs {
 };
 
 constexpr int kAttnThreads = 256;
-constexpr int kAttnFwdSmem = 147456 + 256 + 1024;
+constexpr int kAttnFwdSmem = 98304 + 256 + 1024;
 constexpr int kAttnBwdSmem = 163840 + 256 + 1024;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -65,30 +65,31 @@ __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
 }  // namespace attn
 
 // ---------------------------------------------------------------- forward
-__global__ void __launch_bounds__(kAttnThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnMaps maps, const AttnArgs a) {
+// One CTA per (query tile, head, sample).  Shared memory: [0, 64 KB) holds Q (16 KB) and K (32 KB) for
+// the score MMA and then the probability tile (64 KB) over them; V at 64 KB: 96 KB and 256 TMEM
+// columns, so two CTAs share an SM (one's softmax overlaps the other's loads and MMAs).
+__global__ void __launch_bounds__(kAttnThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnMaps maps, const AttnArgs a) {
     using namespace attn;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint8_t *sQ = smem, *sK = smem + 16384, *sV = smem + 49152, *sP = smem + 81920;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 147456);
-    uint64_t *bar_kv = bars, *bar_q = bars + 1, *bar_s = bars + 2, *bar_p = bars + 3, *bar_o = bars + 4,
-             *bar_free = bars + 5;
+    uint8_t *sQ = smem, *sK = smem + 16384, *sP = smem, *sV = smem + 65536;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 98304);
+    uint64_t *bar_in = bars, *bar_s = bars + 1, *bar_p = bars + 2, *bar_o = bars + 3;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 8);
     const int warp = int(ptx::warp_id()), lane = int(ptx::lane_id());
-    const int h = int(blockIdx.x) % a.H, b = int(blockIdx.x) / a.H;
     const int T = a.T, ntile = (T + 127) / 128;
+    const int i = int(blockIdx.x) % ntile, g = int(blockIdx.x) / ntile;
+    const int h = g % a.H, b = g / a.H;
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&maps.q);
         ptx::tma_prefetch_desc(&maps.k);
         ptx::tma_prefetch_desc(&maps.v);
     }
     if (warp == 1 && lane == 0) {
-        ptx::mbar_init(bar_kv, 1);
-        ptx::mbar_init(bar_q, 1);
+        ptx::mbar_init(bar_in, 1);
         ptx::mbar_init(bar_s, 1);
         ptx::mbar_init(bar_p, 4);
         ptx::mbar_init(bar_o, 1);
-        ptx::mbar_init(bar_free, 4);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<256>(tmem_slot);
@@ -100,102 +101,89 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_fwd_kernel(const __grid_
     ptx::griddep_launch();
     if (warp == 0) {
         if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(bar_kv, 65536);
-            ptx::tma_load_4d(sK, &maps.k, bar_kv, 0, 0, h, b);
-            ptx::tma_load_4d(sV, &maps.v, bar_kv, 0, 0, h, b);
-            for (int i = 0; i < ntile; ++i) {
-                if (i > 0) ptx::mbar_wait(bar_s, (i - 1) & 1);  // the previous tile's S read Q
-                ptx::mbar_arrive_expect_tx(bar_q, 16384);
-                ptx::tma_load_4d(sQ, &maps.q, bar_q, 0, i * 128, h, b);
-            }
+            ptx::mbar_arrive_expect_tx(bar_in, 16384 + 65536);
+            ptx::tma_load_4d(sQ, &maps.q, bar_in, 0, i * 128, h, b);
+            ptx::tma_load_4d(sK, &maps.k, bar_in, 0, 0, h, b);
+            ptx::tma_load_4d(sV, &maps.v, bar_in, 0, 0, h, b);
         }
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t qa = ptx::smem_u32(sQ), ka = ptx::smem_u32(sK), va = ptx::smem_u32(sV),
                            pa = ptx::smem_u32(sP);
             const int ksteps = (T + 15) / 16;  // 16-key MMA steps of P V (the rest of P is zero)
-            ptx::mbar_wait(bar_kv, 0);
-            for (int i = 0; i < ntile; ++i) {
-                ptx::mbar_wait(bar_q, i & 1);
-                if (i > 0) ptx::mbar_wait(bar_free, (i - 1) & 1);  // the epilogue drained O of the previous tile
-                ptx::tc_fence_after();
+            ptx::mbar_wait(bar_in, 0);
+            ptx::tc_fence_after();
 #pragma unroll
-                for (int k = 0; k < 4; ++k) ptx::umma<0>(tmem, desc_k(qa + k * 32), desc_k(ka + k * 32), kIdS, k > 0);
-                ptx::umma_commit(bar_s);
-                ptx::mbar_wait(bar_p, i & 1);
-                ptx::tc_fence_after();
-                for (int k = 0; k < ksteps; ++k)
-                    ptx::umma<0>(tmem, desc_k(pa + (k >> 2) * 16384 + (k & 3) * 32), desc_mn(va + k * 2048, 8192),
-                                 kIdO, k > 0);
-                ptx::umma_commit(bar_o);
-            }
+            for (int k = 0; k < 4; ++k) ptx::umma<0>(tmem, desc_k(qa + k * 32), desc_k(ka + k * 32), kIdS, k > 0);
+            ptx::umma_commit(bar_s);  // (Q and K are free once it arrives: P is written over them)
+            ptx::mbar_wait(bar_p, 0);
+            ptx::tc_fence_after();
+            for (int k = 0; k < ksteps; ++k)
+                ptx::umma<0>(tmem, desc_k(pa + (k >> 2) * 16384 + (k & 3) * 32), desc_mn(va + k * 2048, 8192), kIdO,
+                             k > 0);
+            ptx::umma_commit(bar_o);
         }
     } else if (warp >= 4) {
         const int q = warp & 3, r = q * 32 + lane;
         const uint32_t trow = tmem + (uint32_t(q * 32) << 16);
         const float sl2 = a.scale * kLog2e;
-        for (int i = 0; i < ntile; ++i) {
-            const int t = i * 128 + r;
-            ptx::mbar_wait(bar_s, i & 1);
-            ptx::tc_fence_after();
-            float mx = -INFINITY;
+        const int t = i * 128 + r;
+        ptx::mbar_wait(bar_s, 0);
+        ptx::tc_fence_after();
+        float mx = -INFINITY;
 #pragma unroll 1
-            for (int c = 0; c * 32 < T; ++c) {
-                float v[32];
-                ptx::tmem_ld32(trow + c * 32, v);
+        for (int c = 0; c * 32 < T; ++c) {
+            float v[32];
+            ptx::tmem_ld32(trow + c * 32, v);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (c * 32 + j < T) mx = fmaxf(mx, v[j]);
-            }
-            const float off = mx * sl2;
-            float sum = 0.f;
+            for (int j = 0; j < 32; ++j)
+                if (c * 32 + j < T) mx = fmaxf(mx, v[j]);
+        }
+        const float off = mx * sl2;
+        float sum = 0.f;
 #pragma unroll 1
-            for (int c = 0; c < 8; ++c) {  // every 32-key group of the tile (zeros past T)
-                float v[32];
-                if (c * 32 < T) ptx::tmem_ld32(trow + c * 32, v);
+        for (int c = 0; c < 8; ++c) {  // every 32-key group of the tile (zeros past T)
+            float v[32];
+            if (c * 32 < T) ptx::tmem_ld32(trow + c * 32, v);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float e = (c * 32 + j < T) ? exp2f(fmaf(v[j], sl2, -off)) : 0.f;
-                    v[j] = e;
-                    sum += e;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint4 w;
-                    w.x = pack2(v[8 * u], v[8 * u + 1]);
-                    w.y = pack2(v[8 * u + 2], v[8 * u + 3]);
-                    w.z = pack2(v[8 * u + 4], v[8 * u + 5]);
-                    w.w = pack2(v[8 * u + 6], v[8 * u + 7]);
-                    *reinterpret_cast<uint4 *>(sP + p_off(r, c * 32 + 8 * u)) = w;
-                }
+            for (int j = 0; j < 32; ++j) {
+                const float e = (c * 32 + j < T) ? exp2f(fmaf(v[j], sl2, -off)) : 0.f;
+                v[j] = e;
+                sum += e;
             }
-            ptx::fence_proxy_async_smem();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(bar_p);
-            const float inv = 1.f / sum;
-            ptx::mbar_wait(bar_o, i & 1);
-            ptx::tc_fence_after();
-            float o0[32], o1[32];
-            ptx::tmem_ld32(trow, o0);
-            ptx::tmem_ld32(trow + 32, o1);
-            if (t < T) {
-                uint4 *dst = reinterpret_cast<uint4 *>(a.o + (int64_t(b) * T + t) * a.o_ld + h * 64);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const float *s = u < 4 ? o0 + 8 * u : o1 + 8 * (u - 4);
-                    uint4 w;
-                    w.x = pack2(s[0] * inv, s[1] * inv);
-                    w.y = pack2(s[2] * inv, s[3] * inv);
-                    w.z = pack2(s[4] * inv, s[5] * inv);
-                    w.w = pack2(s[6] * inv, s[7] * inv);
-                    dst[u] = w;
-                }
-                a.lse[(int64_t(b) * a.H + h) * T + t] = mx * a.scale + logf(sum);
+            for (int u = 0; u < 4; ++u) {
+                uint4 w;
+                w.x = pack2(v[8 * u], v[8 * u + 1]);
+                w.y = pack2(v[8 * u + 2], v[8 * u + 3]);
+                w.z = pack2(v[8 * u + 4], v[8 * u + 5]);
+                w.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+                *reinterpret_cast<uint4 *>(sP + p_off(r, c * 32 + 8 * u)) = w;
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(bar_free);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar_p);
+        const float inv = 1.f / sum;
+        ptx::mbar_wait(bar_o, 0);
+        ptx::tc_fence_after();
+        float o0[32], o1[32];
+        ptx::tmem_ld32(trow, o0);
+        ptx::tmem_ld32(trow + 32, o1);
+        if (t < T) {
+            uint4 *dst = reinterpret_cast<uint4 *>(a.o + (int64_t(b) * T + t) * a.o_ld + h * 64);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float *sv = u < 4 ? o0 + 8 * u : o1 + 8 * (u - 4);
+                uint4 w;
+                w.x = pack2(sv[0] * inv, sv[1] * inv);
+                w.y = pack2(sv[2] * inv, sv[3] * inv);
+                w.z = pack2(sv[4] * inv, sv[5] * inv);
+                w.w = pack2(sv[6] * inv, sv[7] * inv);
+                dst[u] = w;
+            }
+            a.lse[(int64_t(b) * a.H + h) * T + t] = mx * a.scale + logf(sum);
         }
     }
     ptx::tc_fence_before();

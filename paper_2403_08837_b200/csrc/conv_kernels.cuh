@@ -879,7 +879,17 @@ constexpr int kBnRows = 256;     // largest row block
 constexpr int kBnRowsMin = 64;   // smallest row block (the partial buffers are sized for it)
 // Row block: 64 rows for small tensors (<= 4M elements: more blocks in flight), else 256 (fewer
 // partials for the finalise).  Measured per rule on B200 (ResNet-18 / ResNet-50 step).
-inline int bn_rows_per_block(int64_t P, int C) { return P * C <= (int64_t(4) << 20) ? kBnRowsMin : kBnRows; }
+constexpr int kBnRowsBig = 1024;  // large tensors: longer per-thread row loops, 4x fewer partials
+inline int64_t bn_big_threshold() {
+    static const int64_t v = [] {
+        const char *e = std::getenv("CDP_BN_BIG_ELEMS");
+        return e ? std::atoll(e) : (int64_t(24) << 20);
+    }();
+    return v;
+}
+inline int bn_rows_per_block(int64_t P, int C) {
+    return P * C <= (int64_t(4) << 20) ? kBnRowsMin : P * C >= bn_big_threshold() ? kBnRowsBig : kBnRows;
+}
 
 template <int KIND, int ROWS>
 static __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__restrict__ g, CTensor mask, int64_t P, int C,

@@ -828,7 +828,9 @@ struct ResNetTrainer {
         const ConvL *cd = ds >= 0 ? &convs[ds] : nullptr;
         const double bytes = double(c.P) * c.cout * (ysz() + (mask.hi ? esz() : 0) + ysz() + (cd ? ysz() : 0));
         L("bn_bwd_stats", 0, bytes, s, [&] {
-            auto kern = rows_blk == kBnRowsMin ? bn_bwd_stats_kernel<K, kBnRowsMin> : bn_bwd_stats_kernel<K, kBnRows>;
+            auto kern = rows_blk == kBnRowsMin ? bn_bwd_stats_kernel<K, kBnRowsMin>
+                        : rows_blk == kBnRows  ? bn_bwd_stats_kernel<K, kBnRows>
+                                               : bn_bwd_stats_kernel<K, kBnRowsBig>;
             launch_pdl(kern, dim3(nblk, (C4 + TPR - 1) / TPR), dim3(256), 0, s, g, mask, c.P,
                        c.cout, (const void *)c.y.p, (const float *)c.mean.as<float>(),
                        (const float *)c.rstd.as<float>(), bnpart[0].as<double>(),

@@ -486,7 +486,8 @@ struct VitTrainer {
                                               kAttnFwdSmem));
                 attr = true;
             }
-            launch_pdl(attn_fwd_kernel, dim3(B * H), dim3(kAttnThreads), kAttnFwdSmem, s, attn_maps(y), attn_args(y));
+            launch_pdl(attn_fwd_kernel, dim3(B * H * ((T + 127) / 128)), dim3(kAttnThreads), kAttnFwdSmem, s,
+                       attn_maps(y), attn_args(y));
         });
     }
     void attention_bwd(const VRec &y, const CBuf &dqkv, cudaStream_t s) {
@@ -1571,7 +1572,7 @@ extern "C" int cdp_attention(const void *qkv, int64_t qkv_ld, const void *dout, 
         a.o_ld = o_ld;
         a.lse = lse;
         CDP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnFwdSmem));
-        attn_fwd_kernel<<<B * H, kAttnThreads, kAttnFwdSmem>>>(m, a);
+        attn_fwd_kernel<<<B * H * ((T + 127) / 128), kAttnThreads, kAttnFwdSmem>>>(m, a);
         CDP_CUDA(cudaGetLastError());
         if (backward) {
             a.dout = static_cast<const __nv_bfloat16 *>(dout);
