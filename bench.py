@@ -509,7 +509,9 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     # DRAM bytes per launch of the same class from an ncu capture of one serialised step
     # (tools/step_traffic.py; bf16 only)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r1_step_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r2_step_traffic.json")
+    if not os.path.exists(tp):
+        tp = os.path.join(ROOT, "profiles", "r1_step_traffic.json")
     if os.path.exists(tp) and args.dtype == "bf16":
         with open(tp) as fh:
             traffic = ((json.load(fh).get(model) or {}).get(dom) or {}).get("dram_bytes_per_launch")
