@@ -428,9 +428,14 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
         tr.zero_drain()
         tr.sync()
 
+    frames = bool(getattr(tr, "zero_frames", False))
     for t in range(warmup):
         do_step(perms[t])
-    settle()
+    # ZeRO-CDP state frames: a drain ends the run (the last states move into next-step forward frames) and a
+    # rank cannot synchronise mid-run, so warm-up and timed steps run back to back (the per-step device
+    # events time each step) and the e2e loop / instrumented step (both synchronise per step) are skipped
+    if not frames:
+        settle()
     if ws > 1:
         torch.distributed.barrier()
     with ClockSampler(local) as clk:
@@ -459,7 +464,10 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
            "zero_state_bytes_per_step": st.get("zero_state_bytes_per_step", 0),
            "tensor_tflops_per_s": round(st["tensor_flops_per_step"] / (ms / 1e3) / 1e12, 1)}
     # ---- e2e: public API, pinned host images copied H2D every step, loss read back every step
-    if e2e:
+    if e2e and frames:
+        out["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                      "note": "ZeRO-CDP state frames: a run cannot be synchronised mid-way (see run_resnet)"}
+    elif e2e:
         x_pin = torch.empty((B, hw, hw, 3), dtype=torch.float32, pin_memory=True)
         y_pin = torch.empty((B,), dtype=torch.int32, pin_memory=True)
         host = [(x[p], y[p]) for p in perms[:steps + 2]]
@@ -488,76 +496,83 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
                       "h2d_bytes_per_step": B * hw * hw * 3 * 4 + B * 4 + 16 + B * 4, "d2h_bytes_per_step": 8,
                       "ms_per_step": round(e, 4)}
     # ---- per-kernel breakdown: one serialised instrumented (real) step
-    if ws > 1:
-        torch.distributed.barrier()
-    ops = tr.profile_step(perms[warmup + steps], RN_LR, serial=ws == 1)
-    reduce_update()
-    settle()
-    agg = kernel_table(ops)
-    tot = sum(a[1] for a in agg.values())
-    gemm = {k: a for k, a in agg.items() if a[2] > 0}
-    dom = max(gemm, key=lambda k: gemm[k][1])
-    d = gemm[dom]
-    peak, src = peak_tensor()
-    achieved = d[2] / (d[1] / 1e3) / 1e12
-    # the class's bound from its arithmetic intensity (algorithmic flops / algorithmic HBM bytes, both
-    # recorded per launch by the trainer) against the ridge point of the measured peaks: the 1x1 convs
-    # of ResNet-50 (K = 64..512) sit far below it and are judged against HBM bandwidth
-    hbm, hsrc = peak_hbm()
-    ridge = peak * 1e12 / (hbm * 1e9)
-    ai = d[2] / d[3] if d[3] > 0 else float("inf")
-    # DRAM bytes per launch of the same class from an ncu capture of one serialised step
-    # (tools/step_traffic.py; bf16 only)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "r2_step_traffic.json")
-    if not os.path.exists(tp):
-        tp = os.path.join(ROOT, "profiles", "r1_step_traffic.json")
-    if os.path.exists(tp) and args.dtype == "bf16":
-        with open(tp) as fh:
-            traffic = ((json.load(fh).get(model) or {}).get(dom) or {}).get("dram_bytes_per_launch")
-    out["roofline"] = {"bound": "tensor", "kernel": f"{dom} (gemm_pk_kernel, tcgen05 + TMA; {d[0]} launches)",
-                       "achieved": round(achieved, 1), "peak": peak, "peak_source": src, "unit": "TFLOP/s",
-                       "frac": round(achieved / peak, 4), "traffic": traffic,
-                       "algorithmic_flops_per_launch": round(d[2] / d[0]),
-                       "algorithmic_bytes_per_launch": round(d[3] / d[0]),
-                       "arithmetic_intensity_flop_per_byte": round(ai, 1), "ridge_flop_per_byte": round(ridge, 1),
-                       "launch_us": round(d[1] / d[0] * 1e3, 2), "share_of_serial_step": round(d[1] / tot, 3)}
-    if ai < ridge:
-        gbs = d[3] / (d[1] / 1e3) / 1e9
-        out["roofline"].update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "peak_source": hsrc,
-                                "unit": "GB/s", "frac": round(gbs / hbm, 4),
-                                "tensor_tflops": round(achieved, 1), "tensor_frac": round(achieved / peak, 4)})
-    # ---- P2P traffic of this step (bytes per rank, one micro-batch per GPU): the gradient hop reads the
-    # previous rank's partial sum S (4 B / param, ranks 2..N, fused into the weight-gradient epilogues);
-    # every reader pulls the versions it reads from the updater (4 B / param, ranks 1..N-1); ZeRO-CDP
-    # copies states instead of pulling.  GB/s = those bytes / the event-timed durations of the kernels
-    # that move them on this rank (the hop-fused GEMMs also compute, so theirs is a lower bound).
-    if ws > 1:
-        hop_b = 4 * P if rank > 0 else 0
-        pull_b = 0 if (rank == ws - 1 or zero or allreduce) else 4 * P
-        zero_b = int(st.get("zero_state_bytes_per_step", 0))
-        hop_ms = sum(a[1] for k, a in agg.items() if "hop" in k and "wait" not in k)
-        pull_ms = sum(a[1] for k, a in agg.items() if k in ("pull", "zero_copy"))
-        vals = torch.tensor([hop_b, pull_b, zero_b, hop_ms, pull_ms], dtype=torch.float64, device="cuda")
-        allv = [torch.zeros_like(vals) for _ in range(ws)]
-        torch.distributed.all_gather(allv, vals)
-        allv = [v.cpu().numpy() for v in allv]
-        out["p2p"] = {
-            "grad_hop_read_bytes_per_rank": [int(v[0]) for v in allv],
-            "param_pull_read_bytes_per_rank": [int(v[1]) for v in allv],
-            "zero_state_bytes_per_rank": [int(v[2]) for v in allv],
-            "bytes_per_step_all_ranks": int(sum(v[0] + v[1] + v[2] for v in allv)),
-            "grad_gbs_in_hop_kernels_rank1": round(allv[1][0] / (allv[1][3] / 1e3) / 1e9, 1) if allv[1][3] else None,
-            "pull_gbs_rank0": round((allv[0][1] + allv[0][2]) / (allv[0][4] / 1e3) / 1e9, 1) if allv[0][4] else None,
-            "note": "peer HBM over NVLink when ranks sit on different GPUs; same-GPU ranks (tests) read local HBM"}
+    if frames:
+        out["kernel_breakdown"] = None
+        out["roofline"] = None
+        out["serial_step_ms"] = None
+        out["p2p"] = {"zero_state_bytes_per_rank0": int(st.get("zero_state_bytes_per_step", 0)),
+                      "note": "ZeRO-CDP state frames: no instrumented step (see above)"}
     else:
-        out["p2p"] = {"bytes_per_step_all_ranks": 0, "note": "one GPU: no peer traffic (the hop is local)"}
-    out["kernel_breakdown"] = {
-        k: {"launches": a[0], "ms": round(a[1], 4), "share": round(a[1] / tot, 3),
-            **({"tflops": round(a[2] / (a[1] / 1e3) / 1e12, 1)} if a[2] else {}),
-            **({"gbs": round(a[3] / (a[1] / 1e3) / 1e9, 1)} if a[3] or not a[2] else {})}
-        for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])}
-    out["serial_step_ms"] = round(tot, 4)
+        if ws > 1:
+            torch.distributed.barrier()
+        ops = tr.profile_step(perms[warmup + steps], RN_LR, serial=ws == 1)
+        reduce_update()
+        settle()
+        agg = kernel_table(ops)
+        tot = sum(a[1] for a in agg.values())
+        gemm = {k: a for k, a in agg.items() if a[2] > 0}
+        dom = max(gemm, key=lambda k: gemm[k][1])
+        d = gemm[dom]
+        peak, src = peak_tensor()
+        achieved = d[2] / (d[1] / 1e3) / 1e12
+        # the class's bound from its arithmetic intensity (algorithmic flops / algorithmic HBM bytes, both
+        # recorded per launch by the trainer) against the ridge point of the measured peaks: the 1x1 convs
+        # of ResNet-50 (K = 64..512) sit far below it and are judged against HBM bandwidth
+        hbm, hsrc = peak_hbm()
+        ridge = peak * 1e12 / (hbm * 1e9)
+        ai = d[2] / d[3] if d[3] > 0 else float("inf")
+        # DRAM bytes per launch of the same class from an ncu capture of one serialised step
+        # (tools/step_traffic.py; bf16 only)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "r2_step_traffic.json")
+        if not os.path.exists(tp):
+            tp = os.path.join(ROOT, "profiles", "r1_step_traffic.json")
+        if os.path.exists(tp) and args.dtype == "bf16":
+            with open(tp) as fh:
+                traffic = ((json.load(fh).get(model) or {}).get(dom) or {}).get("dram_bytes_per_launch")
+        out["roofline"] = {"bound": "tensor", "kernel": f"{dom} (gemm_pk_kernel, tcgen05 + TMA; {d[0]} launches)",
+                           "achieved": round(achieved, 1), "peak": peak, "peak_source": src, "unit": "TFLOP/s",
+                           "frac": round(achieved / peak, 4), "traffic": traffic,
+                           "algorithmic_flops_per_launch": round(d[2] / d[0]),
+                           "algorithmic_bytes_per_launch": round(d[3] / d[0]),
+                           "arithmetic_intensity_flop_per_byte": round(ai, 1), "ridge_flop_per_byte": round(ridge, 1),
+                           "launch_us": round(d[1] / d[0] * 1e3, 2), "share_of_serial_step": round(d[1] / tot, 3)}
+        if ai < ridge:
+            gbs = d[3] / (d[1] / 1e3) / 1e9
+            out["roofline"].update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "peak_source": hsrc,
+                                    "unit": "GB/s", "frac": round(gbs / hbm, 4),
+                                    "tensor_tflops": round(achieved, 1), "tensor_frac": round(achieved / peak, 4)})
+        # ---- P2P traffic of this step (bytes per rank, one micro-batch per GPU): the gradient hop reads the
+        # previous rank's partial sum S (4 B / param, ranks 2..N, fused into the weight-gradient epilogues);
+        # every reader pulls the versions it reads from the updater (4 B / param, ranks 1..N-1); ZeRO-CDP
+        # copies states instead of pulling.  GB/s = those bytes / the event-timed durations of the kernels
+        # that move them on this rank (the hop-fused GEMMs also compute, so theirs is a lower bound).
+        if ws > 1:
+            hop_b = 4 * P if rank > 0 else 0
+            pull_b = 0 if (rank == ws - 1 or zero or allreduce) else 4 * P
+            zero_b = int(st.get("zero_state_bytes_per_step", 0))
+            hop_ms = sum(a[1] for k, a in agg.items() if "hop" in k and "wait" not in k)
+            pull_ms = sum(a[1] for k, a in agg.items() if k in ("pull", "zero_copy"))
+            vals = torch.tensor([hop_b, pull_b, zero_b, hop_ms, pull_ms], dtype=torch.float64, device="cuda")
+            allv = [torch.zeros_like(vals) for _ in range(ws)]
+            torch.distributed.all_gather(allv, vals)
+            allv = [v.cpu().numpy() for v in allv]
+            out["p2p"] = {
+                "grad_hop_read_bytes_per_rank": [int(v[0]) for v in allv],
+                "param_pull_read_bytes_per_rank": [int(v[1]) for v in allv],
+                "zero_state_bytes_per_rank": [int(v[2]) for v in allv],
+                "bytes_per_step_all_ranks": int(sum(v[0] + v[1] + v[2] for v in allv)),
+                "grad_gbs_in_hop_kernels_rank1": round(allv[1][0] / (allv[1][3] / 1e3) / 1e9, 1) if allv[1][3] else None,
+                "pull_gbs_rank0": round((allv[0][1] + allv[0][2]) / (allv[0][4] / 1e3) / 1e9, 1) if allv[0][4] else None,
+                "note": "peer HBM over NVLink when ranks sit on different GPUs; same-GPU ranks (tests) read local HBM"}
+        else:
+            out["p2p"] = {"bytes_per_step_all_ranks": 0, "note": "one GPU: no peer traffic (the hop is local)"}
+        out["kernel_breakdown"] = {
+            k: {"launches": a[0], "ms": round(a[1], 4), "share": round(a[1] / tot, 3),
+                **({"tflops": round(a[2] / (a[1] / 1e3) / 1e12, 1)} if a[2] else {}),
+                **({"gbs": round(a[3] / (a[1] / 1e3) / 1e9, 1)} if a[3] or not a[2] else {})}
+            for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])}
+        out["serial_step_ms"] = round(tot, 4)
     tr.close()
     # ---- exposed gradient communication (N > 1): full ring step - compute-only step of the same rank work
     if ws > 1 and not allreduce:
@@ -637,8 +652,9 @@ def run_resnet_variant(args, ws, rank, local, model, steps, warmup, mode):
 
     for t in range(warmup):
         do_step(perms[t])
-    tr.zero_drain()
-    tr.sync()
+    if not getattr(tr, "zero_frames", False):  # (state frames: a drain ends the run, see run_resnet)
+        tr.zero_drain()
+        tr.sync()
     if ws > 1:
         torch.distributed.barrier()
     for k in range(steps):
@@ -841,7 +857,10 @@ def main_resnet(args, ws, rank, local):
     if args.zero and ws > 1:
         out["zero_cdp"] = {"state_bytes_received_per_step_rank0": res["zero_state_bytes_per_step"],
                            "what": "both theta version slots + momentum of every received tensor use (P2P copy "
-                                   "kernels, ref comm.py:93-144 holder chain)"}
+                                   "kernels, ref comm.py:93-144 holder chain)",
+                           "param_state_bytes_rank0": res["param_state_bytes"],
+                           "layout": "two stage frames per rank (parameter-balanced, block-aligned stages); "
+                                     "theta slots + momentum + compute copies + the gradient partial sum"}
     if baselines is not None:
         b = out["baselines"] = baselines
         if "value" in b.get("dp-allreduce", {}):

@@ -185,9 +185,19 @@ int cdp_resnet_stream(cdp_resnet *tr, void **stream);
 /* zero_table != NULL (world > 1): ZeRO-CDP state passing (ref comm.py:93-144), [world stages][2 (F, B)]
  * [world ranks][3] = (use-index base, predecessor rank, predecessor step offset) from zero.py; every
  * use of a parameter tensor copies the tensor's state (both theta slots + momentum) from its
- * predecessor's HBM.  cdp_resnet_zero_drain publishes the forward uses of the next (unlaunched) step
- * at the end of a run (call on every rank before synchronising). */
+ * predecessor's HBM.  The state lives in two stage frames per rank (ref schedule.py:449-458: a worker
+ * holds only the stage it uses; stage s in frame (s - 1) & 1, frames reused once the successor copied
+ * them); options bit 2 keeps full replicas instead.  cdp_resnet_zero_drain publishes the forward uses
+ * of the next (unlaunched) step at the end of a run (call on every rank before synchronising). */
 int cdp_resnet_zero_drain(cdp_resnet *tr);
+/* ZeRO-CDP frames: this rank's frame contents in the full parameter layout (which 0: current version,
+ * 1: previous) and its last finished use index per tensor (last_use[n_tensors]); the newest state of a
+ * tensor is on the rank with the largest last_use (paper_2403_08837_b200.resnet.gather_zero_params). */
+int cdp_resnet_zero_state(cdp_resnet *tr, int which, float *theta, uint32_t *last_use);
+/* ZeRO-CDP frames: the end-of-run drain plan of this rank, n_rows x (stage, previous-occupant stage,
+ * its last use kind, step offset, successor step offset) from zero.py frame_drain_plan; a drained run
+ * cannot take further steps. */
+int cdp_resnet_zero_drain_plan(cdp_resnet *tr, const int32_t *rows, int n_rows);
 /* Parameter count, tensor count and (optional) per-tensor base offsets / kinds (0 conv, 1 bn, 2 fc). */
 int cdp_resnet_info(cdp_resnet *tr, int64_t *n_params, int *n_tensors, int64_t *tensor_base, int32_t *tensor_kind);
 int cdp_resnet_region(cdp_resnet *tr, void **base);

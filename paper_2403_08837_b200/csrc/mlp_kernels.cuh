@@ -154,6 +154,7 @@ struct RingFlags {
     uint32_t updated[kMaxStages];    // updater: stage j holds version `updated[j]`
     uint32_t pulled[kMaxStages][2];  // updater: readers that pulled version v (slot v % 2)
     uint32_t zdone[kMaxStages];      // ZeRO-CDP: global use index of this rank's last finished use of a unit
+    uint32_t zcopied[kMaxStages];    // ZeRO-CDP frames: use index of the successor that copied this rank's unit
     uint32_t vtag[2][kMaxStages];    // trace mode: version held by theta slot s of unit j (travels with the data)
     uint32_t err;                    // a spin-wait timed out (protocol failure)
     uint32_t pad[31];

@@ -99,18 +99,22 @@ __global__ void zero_wait_kernel(ZeroUse z, int self, const RingFlags *src_flags
 
 // Copy the unit's state (both theta version slots, momentum) from the predecessor's HBM
 // (peer memory) and repack the compute copies of both slots.
+// ZeRO-CDP frames: a use without predecessor (step 1) loads the initial state from mapped host
+// memory (init_t: theta, init_v: zeros) into the frame; with full replicas (init_t null) every rank
+// already holds it.
 template <int KIND>
 __global__ void zero_copy_kernel(ZeroUse z, int self, const float *src_t0, const float *src_t1, const float *src_v,
                                  float *t0, float *t1, float *v, int64_t n, int cols, CTensor wc0, CTensor wc1,
-                                 const int *step) {
+                                 const int *step, const float *init_t, const float *init_v) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     const int t = *step;
-    if (z.src == self || t + z.dstep < 1) return;
+    const bool initial = t + z.dstep < 1;
+    if (initial ? init_t == nullptr : z.src == self) return;
     StateCopy c{};
-    c.src[0] = src_t0;
-    c.src[1] = src_t1;
-    c.src[2] = src_v;
+    c.src[0] = initial ? init_t : src_t0;
+    c.src[1] = initial ? init_t : src_t1;
+    c.src[2] = initial ? init_v : src_v;
     c.dst[0] = t0;
     c.dst[1] = t1;
     c.dst[2] = v;
@@ -120,6 +124,28 @@ __global__ void zero_copy_kernel(ZeroUse z, int self, const float *src_t0, const
     c.n = n;
     c.cols = cols;
     state_copy<KIND>(c);  // rank_common.cuh: 16-byte peer loads, no per-element division
+}
+
+// ZeRO-CDP frames: tell the predecessor its copy of `unit` has been taken (its frame may be reused).
+__global__ void zero_copied_kernel(ZeroUse z, int self, RingFlags *src_flags, int unit, const int *step) {
+    const int t = *step;
+    if (z.src == self || t + z.dstep < 1) return;
+    __threadfence_system();
+    ptx::st_release_sys(&src_flags->zcopied[unit - 1], zero_u(z, t));
+}
+
+// ZeRO-CDP frames: before a window copies a stage into a frame, the stage that used the frame two
+// windows earlier (use index base_last of step t + dl) must have been copied out by its successor
+// (use index + 1, in step t + dl + delta) — when both uses exist.
+struct FrameWait {
+    int unit0, unit1;  // units (tensor + 1) of the previous occupant
+    int base_last, dl, delta, uses_per_step;
+};
+__global__ void zero_frame_wait_kernel(FrameWait f, RingFlags *own, const int *step) {
+    const int t = *step;
+    if (threadIdx.x != 0 || t + f.dl < 1 || t + f.dl + f.delta < 1) return;
+    const uint32_t want = uint32_t(f.base_last + (t + f.dl - 1) * f.uses_per_step) + kZeroOff + 1;
+    for (int u = f.unit0; u < f.unit1; ++u) spin_ge(&own->zcopied[u - 1], want, &own->err);
 }
 
 // Publish the end of this rank's use of `unit` (after all its kernels on the stream).
@@ -153,7 +179,23 @@ struct ResNetTrainer {
     size_t region_off = 0;
     RingFlags *prev_ring = nullptr, *upd_ring = nullptr;
     float *prev_partial = nullptr, *upd_theta[2] = {nullptr, nullptr};
-    std::vector<CBuf> wc[2];   // per tensor (empty CBuf for BN)
+    std::vector<CBuf> wc[2];   // per tensor (empty CBuf for BN); full-replica mode
+    std::vector<CTensor> wcv[2];  // per tensor: the GEMM compute copy of theta slot v (a frame view in ZeRO mode)
+    // ZeRO-CDP frames: a rank keeps the state (theta slots, momentum, compute copies) of only the stages it
+    // is using.  Stage s lives in frame (s - 1) & 1 at stage-relative offsets; a rank's consecutive
+    // use windows alternate frames (zero.py), so two frames of the largest stage replace the full replica.
+    bool frames = false;
+    int64_t framePp[2] = {0, 0}, th_stride = 0;  // floats per frame (largest stage of its parity); per slot
+    std::vector<int64_t> foff;                   // per tensor: float offset inside a theta slot
+    std::vector<int64_t> stage_lo, stage_hi;     // per stage: parameter range [lo, hi)
+    std::vector<int> stage_t0, stage_t1;         // per stage: tensor range
+    DevBuf wcpool[2][2];                         // [slot][hi / lo] compute-copy frames
+    float *init_host = nullptr;                  // mapped pinned: initial theta | zeros (step-1 state source)
+    const float *init_dev = nullptr;             // its device alias
+    const int32_t *stage_in = nullptr;           // tensor -> stage, set before build()
+    std::vector<int> zwin_done;                  // per (stage, kind): frame wait recorded in this step
+    std::vector<int> zdrain;                     // end-of-run drain plan rows (zero.py frame_drain_plan)
+    bool drained = false;                        // frames: a drained run cannot continue
     std::vector<CBuf> acts;    // activations (compute format)
     std::vector<int> act_C, act_H, act_W;
     std::vector<int64_t> act_P;
@@ -201,6 +243,7 @@ struct ResNetTrainer {
         for (auto e : stage_ev)
             if (e) cudaEventDestroy(e);
         if (stage_host) cudaFreeHost(stage_host);
+        if (init_host) cudaFreeHost(init_host);
         for (auto s : {main, cs, hs, ps})
             if (s) cudaStreamDestroy(s);
     }
@@ -282,6 +325,82 @@ struct ResNetTrainer {
         return int(convs.size()) - 1;
     }
 
+    // Parameter-state layout: full replica (foff = base) or ZeRO-CDP frames (stage-relative offsets).
+    void layout_state() {
+        foff.resize(tens.size());
+        th_stride = Pp;
+        for (size_t i = 0; i < tens.size(); ++i) foff[i] = tens[i].base;
+        if (!frames) return;
+        const int ns = world;
+        stage_lo.assign(ns, INT64_MAX);
+        stage_hi.assign(ns, 0);
+        stage_t0.assign(ns, INT32_MAX);
+        stage_t1.assign(ns, 0);
+        for (size_t i = 0; i < tens.size(); ++i) {
+            const int s = tens[i].stage - 1;
+            CDP_REQUIRE(s >= 0 && s < ns, "ZeRO-CDP frames: tensor stage out of range");
+            stage_lo[s] = std::min(stage_lo[s], tens[i].base);
+            stage_hi[s] = std::max(stage_hi[s], tens[i].base + tens[i].n);
+            stage_t0[s] = std::min(stage_t0[s], int(i));
+            stage_t1[s] = std::max(stage_t1[s], int(i) + 1);
+        }
+        framePp[0] = framePp[1] = 0;
+        for (int s = 0; s < ns; ++s) {
+            CDP_REQUIRE(stage_t1[s] > stage_t0[s], "ZeRO-CDP frames: a stage without tensors");
+            for (int i = stage_t0[s]; i < stage_t1[s]; ++i)
+                CDP_REQUIRE(tens[i].stage == s + 1, "ZeRO-CDP frames: stages must be contiguous tensor ranges");
+            framePp[s & 1] = std::max<int64_t>(framePp[s & 1], stage_hi[s] - stage_lo[s]);
+        }
+        for (auto &f : framePp) f = (f + 63) / 64 * 64;
+        th_stride = framePp[0] + framePp[1];
+        // the initial state (theta | zeros) in mapped pinned host memory: read by the step-1 state loads only
+        CDP_CUDA(cudaHostAlloc(&init_host, size_t(P) * 8, cudaHostAllocMapped));
+        std::memset(init_host, 0, size_t(P) * 8);
+        void *d = nullptr;
+        CDP_CUDA(cudaHostGetDevicePointer(&d, init_host, 0));
+        init_dev = static_cast<const float *>(d);
+        for (size_t i = 0; i < tens.size(); ++i) {
+            const int s = tens[i].stage - 1;
+            foff[i] = (s & 1 ? framePp[0] : 0) + (tens[i].base - stage_lo[s]);
+        }
+    }
+    // GEMM compute copies: per tensor (full replica) or per frame with stage-relative sub-buffers.
+    void alloc_compute_copies() {
+        for (int v = 0; v < 2; ++v) {
+            wcv[v].assign(tens.size(), CTensor{});
+            if (!frames) {
+                for (auto &ts : tens) wc[v].push_back(ts.kind == T_BN ? CBuf{} : make_cbuf(kind, ts.rows, ts.cols));
+                for (size_t i = 0; i < tens.size(); ++i) wcv[v][i] = wc[v][i].view();
+                continue;
+            }
+            const size_t esz = kind == 0 ? 2 : 4;
+            std::vector<size_t> off(tens.size(), 0);
+            size_t frame_bytes[2] = {0, 0};  // per frame parity: the largest stage's compute copies
+            for (size_t s = 0; s < stage_t0.size(); ++s) {
+                size_t o = 0;
+                for (int i = stage_t0[s]; i < stage_t1[s]; ++i) {
+                    if (tens[i].kind == T_BN) continue;
+                    off[i] = o;
+                    o += (size_t(tens[i].rows) * round_up(std::max(tens[i].cols, 1), 16) * esz + 255) / 256 * 256;
+                }
+                frame_bytes[s & 1] = std::max(frame_bytes[s & 1], o);
+            }
+            wcpool[v][0] = DevBuf(frame_bytes[0] + frame_bytes[1]);
+            if (kind == 1) wcpool[v][1] = DevBuf(frame_bytes[0] + frame_bytes[1]);
+            for (size_t i = 0; i < tens.size(); ++i) {
+                if (tens[i].kind == T_BN) continue;
+                const size_t o = ((tens[i].stage - 1) & 1 ? frame_bytes[0] : 0) + off[i];
+                wcv[v][i] = CTensor{wcpool[v][0].as<uint8_t>() + o,
+                                    kind == 1 ? static_cast<void *>(wcpool[v][1].as<uint8_t>() + o) : nullptr,
+                                    round_up(std::max(tens[i].cols, 1), 16)};
+            }
+        }
+    }
+    float *thp(int slot, int tensor) const { return theta[slot] + foff[tensor]; }
+    // a "virtual base" whose element tens[tensor].base lands on the tensor's first value (kernels index by base)
+    float *thv(int slot, int tensor) const { return theta[slot] + foff[tensor] - tens[tensor].base; }
+    float *velv(int tensor) const { return vel ? vel + foff[tensor] - tens[tensor].base : nullptr; }
+
     void build(const int *widths, const int *depths, int n_layers) {
         int H = Hin, W = Win;
         // stem
@@ -337,6 +456,8 @@ struct ResNetTrainer {
         fc_in = cin;
         fc_t = add_tensor(T_FC, int64_t(cin + 1) * classes, cin + 1, classes);
         P = tens.back().base + tens.back().n;
+        if (stage_in)
+            for (size_t i = 0; i < tens.size(); ++i) tens[i].stage = stage_in[i];
         // ---- buffers
         int64_t max_stats = 1, max_part = 1;
         for (auto &c : convs) {
@@ -362,19 +483,19 @@ struct ResNetTrainer {
         z = DevBuf(size_t(B) * classes * 4);
         loss_dev = DevBuf(8);
         loss_rows = DevBuf(size_t(B) * 8);
-        // shared region: RingFlags | theta0 | theta1 | partial
         region_off = (sizeof(RingFlags) + 255) / 256 * 256;
         Pp = (P + 63) / 64 * 64;
-        // shared region: RingFlags | theta0 | theta1 | partial | momentum
-        region = DevBuf(region_off + size_t(Pp) * 4 * (momentum != 0.f ? 4 : 3));
+        layout_state();
+        // shared region: RingFlags | theta slot 0 | theta slot 1 | partial | momentum (a slot is the full
+        // parameter vector, or two stage frames in ZeRO-CDP mode)
+        region = DevBuf(region_off + size_t(2 * th_stride + Pp + (momentum != 0.f ? th_stride : 0)) * 4);
         ring = region.as<RingFlags>();
         theta[0] = reinterpret_cast<float *>(region.as<uint8_t>() + region_off);
-        theta[1] = theta[0] + Pp;
-        partial = theta[1] + Pp;
+        theta[1] = theta[0] + th_stride;
+        partial = theta[1] + th_stride;
         if (momentum != 0.f) vel = partial + Pp;
         cta_counters = DevBuf(2 * kMaxStages * 4);
-        for (int v = 0; v < 2; ++v)
-            for (auto &ts : tens) wc[v].push_back(ts.kind == T_BN ? CBuf{} : make_cbuf(kind, ts.rows, ts.cols));
+        alloc_compute_copies();
         CDP_REQUIRE(int(tens.size()) <= kMaxStages, "too many parameter tensors for the ring flags");
         CDP_CUDA(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
         CDP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -600,7 +721,7 @@ struct ResNetTrainer {
     }
 
     template <int K, int MODE, class Epi>
-    void pk_conv(const char *name, int BN, const ConvL &c, const CBuf &w, const typename Epi::Params &ep,
+    void pk_conv(const char *name, int BN, const ConvL &c, const CTensor &w, const typename Epi::Params &ep,
                  cudaStream_t s, bool hop, int phase = -1) {
         const Nhwc a = c.in_act >= 0 ? nhwc_act(c.in_act) : Nhwc{};
         const Nhwc dy = nhwc_dy(c);
@@ -614,7 +735,7 @@ struct ResNetTrainer {
             constexpr int BNc = decltype(bnc)::value;
             constexpr bool AMN = MODE == GM_WGRAD, BMN = MODE != GM_DGRAD;
             if constexpr (BNc >= 64 && (!BMN || BNc % (K == 0 ? 64 : 32) == 0)) {
-                GemmPlan p = plan_conv<K, BNc, MODE>(a, w.hi.p, w.lo.p, w.ld, dy, c.R, c.S, c.stride, c.pad, c.cin,
+                GemmPlan p = plan_conv<K, BNc, MODE>(a, w.hi, w.lo, w.ld, dy, c.R, c.S, c.stride, c.pad, c.cin,
                                                      c.cout, 1, nullptr, nullptr, phase);
                 run_pk<K, BNc, AMN, BMN, Epi, MODE>(name, flops, p, ep, s, hop);
             } else {
@@ -626,7 +747,7 @@ struct ResNetTrainer {
     // Stride-2 data gradient: the sub-pixel phases with taps as one launch (shared dy / W maps and
     // pixel boxes; per-phase tap tables and output offsets).
     template <int K, class Epi>
-    void pk_dgrad_phases(const char *name, int BN, const ConvL &c, const CBuf &w, const typename Epi::Params &ep,
+    void pk_dgrad_phases(const char *name, int BN, const ConvL &c, const CTensor &w, const typename Epi::Params &ep,
                          cudaStream_t s) {
         CDP_REQUIRE(c.in_act >= 0, "stride-2 data gradient of the stem is never needed");
         const Nhwc a = nhwc_act(c.in_act);
@@ -642,7 +763,7 @@ struct ResNetTrainer {
                     ConvGeom probe{};
                     dgrad_taps(probe, c.R, c.S, c.pad, phase);
                     if (probe.ntap == 0) continue;
-                    GemmPlan p = plan_conv<K, BNc, GM_DGRAD>(a, w.hi.p, w.lo.p, w.ld, dy, c.R, c.S, c.stride,
+                    GemmPlan p = plan_conv<K, BNc, GM_DGRAD>(a, w.hi, w.lo, w.ld, dy, c.R, c.S, c.stride,
                                                              c.pad, c.cin, c.cout, 1, nullptr, nullptr, phase);
                     if (nph == 0) first = p;
                     ph[nph++] = p.args.cv;
@@ -667,7 +788,7 @@ struct ResNetTrainer {
         ep.ld = c.cout;
         ep.stats = stats_fwd.as<float>();
         ep.tiles = c.tiles_fwd;
-        const CBuf &w = wc[vslot][c.tw];
+        const CTensor w = wcv[vslot][c.tw];
         rec(c.tw, A_FWD, 0, vslot, s);
         gemm_bytes = double(c.impl == CI_STEM ? c.P * cols.ld : c.Pin * c.cin) * esz() +
                      double(c.K) * c.cout * esz() + double(c.P) * c.cout * ysz();
@@ -677,7 +798,7 @@ struct ResNetTrainer {
             const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
             const int64_t Kd = c.impl == CI_STEM ? c.K : c.cin;
             pk_plain<K, false, true, EpiConvOut2<K>>(c.impl == CI_STEM ? "stem_fprop" : "conv_fprop_1x1",
-                                                     tile_n(c.cout), in, w.view(), c.P, c.cout, Kd, ep, s, false);
+                                                     tile_n(c.cout), in, w, c.P, c.cout, Kd, ep, s, false);
         }
         rec(c.tw, A_FWD, 1, vslot, s);
         const int slots = sizing ? c.tiles_fwd : last_stat_slots;
@@ -688,8 +809,8 @@ struct ResNetTrainer {
         });
     }
 
-    const float *gamma(int ci, int vslot) const { return theta[vslot] + tens[convs[ci].tb].base; }
-    const float *beta(int ci, int vslot) const { return theta[vslot] + tens[convs[ci].tb].base + convs[ci].cout; }
+    const float *gamma(int ci, int vslot) const { return thp(vslot, convs[ci].tb); }
+    const float *beta(int ci, int vslot) const { return thp(vslot, convs[ci].tb) + convs[ci].cout; }
     int vs(int tensor, int p) const { return tens[tensor].fresh ? p : (p ^ 1); }
     // trace mode: one access record of `tensor`'s parameters in theta slot `slot` (stream order)
     void rec(int tensor, int akind, int phase, int slot, cudaStream_t s) {
@@ -808,7 +929,7 @@ struct ResNetTrainer {
         ep.last = 1;
         ep.z = z.as<float>();
         rec(fc_t, A_FWD, 0, vs(fc_t, p), s);
-        gemm<K, true, false, EpiFwd<K>>("fc_fwd", 32, wc[vs(fc_t, p)][fc_t].view(), pooled.view(), classes, B,
+        gemm<K, true, false, EpiFwd<K>>("fc_fwd", 32, wcv[vs(fc_t, p)][fc_t], pooled.view(), classes, B,
                                         fc_in + 1, ep, s, false);
         rec(fc_t, A_FWD, 1, vs(fc_t, p), s);
         zdone(fc_t, 0, s);
@@ -883,7 +1004,7 @@ struct ResNetTrainer {
                     CTensor add_mask = CTensor{}, CTensor out_mask = CTensor{}) {
         ConvL &c = convs[ci];
         zrecv<K>(c.tw, 1, s);
-        const CBuf &w = wc[vslot][c.tw];
+        const CTensor w = wcv[vslot][c.tw];
         rec(c.tw, A_BWD, 0, vslot, s);
         typename EpiConvOut2<K>::Params ep{};
         ep.stats = nullptr;
@@ -904,14 +1025,14 @@ struct ResNetTrainer {
             ep.ld = c.cin;
             if (tadd)
                 pk_tadd<K>([&](auto e) {
-                    pk_plain<K, false, false, decltype(e)>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(),
+                    pk_plain<K, false, false, decltype(e)>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w,
                                                            c.P, c.cin, c.cout, ep, s, false);
                 });
             else if (direct)
-                pk_plain<K, false, false, EpiConvAdd<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(), c.P,
+                pk_plain<K, false, false, EpiConvAdd<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w, c.P,
                                                          c.cin, c.cout, ep, s, false);
             else
-                pk_plain<K, false, false, EpiConvOut2<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w.view(),
+                pk_plain<K, false, false, EpiConvOut2<K>>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w,
                                                           c.P, c.cin, c.cout, ep, s, false);
         } else if (c.stride == 1) {
             ep.out = g_in;
@@ -946,14 +1067,14 @@ struct ResNetTrainer {
         hp.dout = ts.cols;
         hp.s_in = rank > 0 ? prev_partial : partial;
         hp.s_out = partial;
-        hp.theta_cur = theta[p];
-        hp.theta_new = theta[p ^ 1];
-        hp.vel = vel;
+        hp.theta_cur = thv(p, tensor);
+        hp.theta_new = thv(p ^ 1, tensor);
+        hp.vel = velv(tensor);
         hp.lr = &ctrl_dev.as<Control>()->lr;
         hp.momentum = momentum;
         hp.wd = wd;
         hp.n_mb = float(world);
-        hp.wc_new = ts.kind == T_BN ? CTensor{} : wc[p ^ 1][tensor].view();
+        hp.wc_new = ts.kind == T_BN ? CTensor{} : wcv[p ^ 1][tensor];
         Flags *fl = flags_dev.as<Flags>();
         hp.grad_flags = &fl->grad;
         hp.upd_flags = &fl->upd;
@@ -988,14 +1109,14 @@ struct ResNetTrainer {
             hp.stage = int(k) + 1;
             hp.base = ts.base;
             hp.s_in = partial;
-            hp.theta_cur = theta[p];
-            hp.theta_new = theta[p ^ 1];
-            hp.vel = vel;
+            hp.theta_cur = thv(p, int(k));
+            hp.theta_new = thv(p ^ 1, int(k));
+            hp.vel = velv(int(k));
             hp.lr = &ctrl_dev.as<Control>()->lr;
             hp.momentum = momentum;
             hp.wd = wd;
             hp.n_mb = float(world);
-            hp.wc_new = ts.kind == T_BN ? CTensor{} : wc[p ^ 1][k].view();
+            hp.wc_new = ts.kind == T_BN ? CTensor{} : wcv[p ^ 1][k];
             hp.upd_flags = &fl->upd;
             if (kind == 0)
                 launch_pdl(update_flat_kernel<0>, dim3(blocks_for(ts.n)), dim3(256), 0, main, hp, ts.n,
@@ -1022,7 +1143,7 @@ struct ResNetTrainer {
             gemm_bytes = double(c.impl == CI_STEM ? c.P * cols.ld : c.Pin * c.cin) * esz() +
                          double(c.P) * c.cout * esz() + double(c.K) * c.cout * hop_bytes_per_param();
             if (c.impl == CI_IMPLICIT) {
-                pk_conv<K, GM_WGRAD, EpiHop2<K>>("conv_wgrad_hop", tile_n(c.cout), c, wc[0][c.tw], hp, s, true);
+                pk_conv<K, GM_WGRAD, EpiHop2<K>>("conv_wgrad_hop", tile_n(c.cout), c, wcv[0][c.tw], hp, s, true);
             } else {
                 const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
                 pk_plain<K, true, true, EpiHop2<K>>(c.impl == CI_STEM ? "stem_wgrad_hop" : "conv_wgrad_hop_1x1",
@@ -1063,35 +1184,92 @@ struct ResNetTrainer {
         return ZeroUse{e[0], e[1], e[2], 2 * world};
     }
     const float *peer_theta(int r, int slot) const {
-        return reinterpret_cast<const float *>(peers[r] + region_off) + size_t(slot) * Pp;
+        return reinterpret_cast<const float *>(peers[r] + region_off) + size_t(slot) * th_stride;
     }
     // Before this rank's first access to `tensor` in its F (0) / B (1) use: wait for the
     // predecessor, copy the state from its HBM.
     template <int K>
-    void zrecv(int tensor, int kindFB, cudaStream_t s, int step_delta = 0, bool copy = true) {
+    void zrecv(int tensor, int kindFB, cudaStream_t s, int step_delta = 0, bool copy = true, bool auto_wait = true) {
         if (!zero || sizing) return;
         CDP_REQUIRE(int(peers.size()) == world, "ZeRO-CDP needs connected peers");
         const ZeroUse z = zuse(tensor, kindFB);
-        if (z.src == rank) return;
+        // self-succession (the same rank's previous use of the stage): nothing to copy — except, with
+        // frames, the step-1 load of the initial state (dstep -1: no predecessor in step 1)
+        if (z.src == rank && !(frames && copy && z.dstep < 0)) return;
         const TensorSpec &ts = tens[tensor];
         const RingFlags *src_flags = reinterpret_cast<const RingFlags *>(peers[z.src]);
-        L("zero_wait", 0, 0, s, [&] {
+        if (frames && copy && z.src != rank && auto_wait) frame_wait(tens[tensor].stage, kindFB, s);
+        if (z.src != rank) L("zero_wait", 0, 0, s, [&] {
             zero_wait_kernel<<<1, 32, 0, s>>>(z, rank, src_flags, ring, tensor + 1,
                                               (const int *)&ctrl_dev.as<Control>()->step, step_delta,
                                               (trace && copy) ? 1 : 0);
             CDP_CUDA(cudaGetLastError());
         });
         if (!copy) return;
-        const float *sv = vel ? reinterpret_cast<const float *>(peers[z.src] + region_off) + 3 * size_t(Pp) : nullptr;
-        CTensor w0 = ts.kind == T_BN ? CTensor{} : wc[0][tensor].view();
-        CTensor w1 = ts.kind == T_BN ? CTensor{} : wc[1][tensor].view();
-        zero_bytes_per_step += ts.n * 4 * (vel ? 3 : 2);
+        const float *sv =
+            vel ? reinterpret_cast<const float *>(peers[z.src] + region_off) + 2 * th_stride + Pp + foff[tensor] : nullptr;
+        CTensor w0 = ts.kind == T_BN ? CTensor{} : wcv[0][tensor];
+        CTensor w1 = ts.kind == T_BN ? CTensor{} : wcv[1][tensor];
+        if (z.src != rank) zero_bytes_per_step += ts.n * 4 * (vel ? 3 : 2);
+        const float *it = frames ? init_dev + ts.base : nullptr;
+        const float *iv = frames ? init_dev + P + ts.base : nullptr;
         L("zero_copy", 0, double(ts.n) * (vel ? 3 : 2) * 8, s, [&] {
             launch_pdl(zero_copy_kernel<K>, dim3(blocks_for(ts.n, 1024)), dim3(256), 0, s, z, rank,
-                       peer_theta(z.src, 0) + ts.base, peer_theta(z.src, 1) + ts.base,
-                       sv ? sv + ts.base : (const float *)nullptr, theta[0] + ts.base, theta[1] + ts.base,
-                       vel ? vel + ts.base : (float *)nullptr, ts.n, std::max(ts.cols, 1), w0, w1,
-                       (const int *)&ctrl_dev.as<Control>()->step);
+                       peer_theta(z.src, 0) + foff[tensor], peer_theta(z.src, 1) + foff[tensor], sv, thp(0, tensor),
+                       thp(1, tensor), vel ? vel + foff[tensor] : (float *)nullptr, ts.n, std::max(ts.cols, 1), w0,
+                       w1, (const int *)&ctrl_dev.as<Control>()->step, it, iv);
+        });
+        if (frames && z.src != rank)
+            L("zero_copied", 0, 0, s, [&] {
+                zero_copied_kernel<<<1, 1, 0, s>>>(z, rank, reinterpret_cast<RingFlags *>(peers[z.src]), tensor + 1,
+                                                   (const int *)&ctrl_dev.as<Control>()->step);
+                CDP_CUDA(cudaGetLastError());
+            });
+    }
+    // The frame-reuse wait of a window that starts with stage `stage`'s `kindFB` use on this rank (once
+    // per window and recorded step: before its first state copy).
+    void frame_wait(int stage, int kindFB, cudaStream_t s) {
+        int &done = zwin_done[size_t(stage - 1) * 2 + kindFB];
+        if (done) return;
+        done = 1;
+        const int N = world, per = 2 * N;
+        // this rank's uses, three steps: (kind, stage, step offset) in order F1..FN, BN..B1
+        struct Op {
+            int k, st, dt;
+        };
+        std::vector<Op> ops;
+        for (int dt = -3; dt <= 1; ++dt) {
+            for (int j = 1; j <= N; ++j) ops.push_back({0, j, dt});
+            for (int j = N; j >= 1; --j) ops.push_back({1, j, dt});
+        }
+        std::vector<std::pair<int, int>> win;  // [first op, last op]
+        for (int i = 0; i < int(ops.size()); ++i) {
+            if (!win.empty() && ops[win.back().second].st == ops[i].st)
+                win.back().second = i;
+            else
+                win.push_back({i, i});
+        }
+        int w = -1;
+        for (int i = 2; i < int(win.size()); ++i) {
+            const Op &f = ops[win[i].first];
+            if (f.k == kindFB && f.st == stage && f.dt == 0) w = i;
+        }
+        CDP_REQUIRE(w >= 2, "ZeRO-CDP frames: window not found");
+        const Op &last = ops[win[w - 2].second];
+        const int sp = last.st - 1;
+        auto base_of = [&](int st0, int k, int r) { return ztab[((size_t(st0) * 2 + k) * world + r) * 3]; };
+        const int bl = base_of(sp, last.k, rank);
+        int delta = INT32_MIN;
+        for (int k = 0; k < 2; ++k)
+            for (int r = 0; r < world; ++r) {
+                const int b2 = base_of(sp, k, r);
+                if ((((bl + 1 - b2) % per) + per) % per == 0) delta = (bl + 1 - b2) / per;
+            }
+        CDP_REQUIRE(delta != INT32_MIN, "ZeRO-CDP frames: successor use not found");
+        const FrameWait f{stage_t0[sp] + 1, stage_t1[sp] + 1, bl, last.dt, delta, per};
+        L("zero_frame_wait", 0, 0, s, [&] {
+            zero_frame_wait_kernel<<<1, 32, 0, s>>>(f, ring, (const int *)&ctrl_dev.as<Control>()->step);
+            CDP_CUDA(cudaGetLastError());
         });
     }
     void zdone(int tensor, int kindFB, cudaStream_t s, int step_delta = 0) {
@@ -1115,7 +1293,7 @@ struct ResNetTrainer {
         const int vslot = vs(tensor, p);
         if (sizing) return;
         CDP_REQUIRE(upd_ring && upd_theta[vslot], "pull outside a connected multi-GPU trainer");
-        CTensor w = ts.kind == T_BN ? CTensor{} : wc[vslot][tensor].view();
+        CTensor w = ts.kind == T_BN ? CTensor{} : wcv[vslot][tensor];
         L("pull_wait", 0, 0, s, [&] {
             pull_wait_kernel<<<1, 32, 0, s>>>(upd_ring, ring, tensor + 1, ts.fresh,
                                               (const int *)&ctrl_dev.as<Control>()->step);
@@ -1123,7 +1301,7 @@ struct ResNetTrainer {
         });
         L("pull", 0, double(ts.n) * (4 + 4 + esz()), s, [&] {
             launch_pdl(pull_tensor_kernel<K>, dim3(blocks_for(ts.n, 1024)), dim3(256), 0, s,
-                       (const float *)(upd_theta[vslot] + ts.base), theta[vslot] + ts.base, ts.n,
+                       (const float *)(upd_theta[vslot] + ts.base), thp(vslot, tensor), ts.n,
                        std::max(ts.cols, 1), w, upd_ring, ring, tensor + 1, ts.fresh,
                        (const int *)&ctrl_dev.as<Control>()->step, cta_counters.as<unsigned>() + kMaxStages,
                        trace ? 1 : 0);
@@ -1149,6 +1327,7 @@ struct ResNetTrainer {
         kernels_per_step = 0;
         flops_per_step = 0.0;
         zero_bytes_per_step = 0;
+        zwin_done.assign(size_t(world) * 2, 0);
         cudaEvent_t fork = ev(main);
         wait(cs, fork);
         wait(hs, fork);
@@ -1190,7 +1369,7 @@ struct ResNetTrainer {
         const int vfc = vs(fc_t, p);
         zrecv<K>(fc_t, 1, cs);
         rec(fc_t, A_BWD, 0, vfc, cs);
-        gemm<K, false, false, EpiDgradLinear>("fc_dgrad", 32, wc[vfc][fc_t].view(), dz.view(), fc_in, B, classes, dep,
+        gemm<K, false, false, EpiDgradLinear>("fc_dgrad", 32, wcv[vfc][fc_t], dz.view(), fc_in, B, classes, dep,
                                               cs, false);
         rec(fc_t, A_BWD, 1, vfc, cs);
         cudaEvent_t fc_dgrad_done = ev(cs);
@@ -1285,6 +1464,53 @@ struct ResNetTrainer {
         // synchronisation here (other ranks' drains may be what this rank's last step waits for)
         std::vector<int> ident(B, 0);
         stage_control(ident.data(), 0.f);
+        if (frames) {
+            // the next step's forward state copies a frame reuse of this step waits for (zero.py
+            // frame_drain_plan: w4's B2 hands its state to w1's F4 of step t + 1 at N = 4), in use order,
+            // with their explicit frame waits; the other forwards only publish as with full replicas
+            CDP_REQUIRE(!drained, "ZeRO-CDP frames: the run was already drained");
+            const int per = 2 * world;
+            auto base_of = [&](int st0, int k) { return ztab[((size_t(st0) * 2 + k) * world + rank) * 3]; };
+            for (int st = 1; st <= world; ++st) {
+                const int *row = nullptr;
+                for (size_t k = 0; k + 5 <= zdrain.size(); k += 5)
+                    if (zdrain[k] == st) row = &zdrain[k];
+                if (row) {
+                    if (row[1] >= 0) {
+                        const FrameWait f{stage_t0[row[1]] + 1, stage_t1[row[1]] + 1, base_of(row[1], row[2]), row[3],
+                                          row[4], per};
+                        L("zero_frame_wait", 0, 0, main, [&] {
+                            zero_frame_wait_kernel<<<1, 32, 0, main>>>(f, ring,
+                                                                       (const int *)&ctrl_dev.as<Control>()->step);
+                            CDP_CUDA(cudaGetLastError());
+                        });
+                    }
+                    for (int k = stage_t0[st - 1]; k < stage_t1[st - 1]; ++k) {
+                        if (kind == 0)
+                            zrecv<0>(k, 0, main, 0, true, false);
+                        else
+                            zrecv<1>(k, 0, main, 0, true, false);
+                        zdone(k, 0, main);
+                    }
+                    continue;
+                }
+                for (int k = stage_t0[st - 1]; k < stage_t1[st - 1]; ++k) {
+                    bool needed = false;
+                    for (int j = 0; j < world; ++j) {
+                        const int *e = &ztab[((size_t(st - 1) * 2 + 1) * world + j) * 3];
+                        needed |= (e[1] == rank && e[2] == 1);
+                    }
+                    if (!needed) continue;
+                    if (kind == 0)
+                        zrecv<0>(k, 0, main, 0, false);
+                    else
+                        zrecv<1>(k, 0, main, 0, false);
+                    zdone(k, 0, main);
+                }
+            }
+            drained = true;
+            return;
+        }
         for (size_t k = 0; k < tens.size(); ++k) {
             const int tensor = int(k);
             // only forwards some other rank's backward of the last step waits for (zero.py drain_units)
@@ -1349,11 +1575,11 @@ struct ResNetTrainer {
             const TensorSpec &ts = tens[i];
             if (ts.kind == T_BN) continue;
             if (kind == 0)
-                pack_tensor_kernel<0><<<blocks_for(ts.n), 256, 0, main>>>(theta[slot] + ts.base, ts.n, ts.cols,
-                                                                          wc[slot][i].view());
+                pack_tensor_kernel<0><<<blocks_for(ts.n), 256, 0, main>>>(thp(slot, int(i)), ts.n, ts.cols,
+                                                                          wcv[slot][i]);
             else
-                pack_tensor_kernel<1><<<blocks_for(ts.n), 256, 0, main>>>(theta[slot] + ts.base, ts.n, ts.cols,
-                                                                          wc[slot][i].view());
+                pack_tensor_kernel<1><<<blocks_for(ts.n), 256, 0, main>>>(thp(slot, int(i)), ts.n, ts.cols,
+                                                                          wcv[slot][i]);
             CDP_CUDA(cudaGetLastError());
         }
     }
@@ -1367,16 +1593,27 @@ struct ResNetTrainer {
             const TensorSpec &ts = tens[i];
             if (ts.kind == T_BN) continue;
             if (kind == 0)
-                pack_tensor_kernel<0><<<blocks_for(ts.n), 256, 0, main>>>(theta[slot] + ts.base, ts.n, ts.cols,
-                                                                          wc[slot][i].view());
+                pack_tensor_kernel<0><<<blocks_for(ts.n), 256, 0, main>>>(thp(slot, int(i)), ts.n, ts.cols,
+                                                                          wcv[slot][i]);
             else
-                pack_tensor_kernel<1><<<blocks_for(ts.n), 256, 0, main>>>(theta[slot] + ts.base, ts.n, ts.cols,
-                                                                          wc[slot][i].view());
+                pack_tensor_kernel<1><<<blocks_for(ts.n), 256, 0, main>>>(thp(slot, int(i)), ts.n, ts.cols,
+                                                                          wcv[slot][i]);
             CDP_CUDA(cudaGetLastError());
         }
     }
 
     void set_params(int which, const float *host) {
+        if (frames) {  // the initial state every step-1 use without predecessor loads (both version slots)
+            CDP_REQUIRE(which < 0 && t == 1, "ZeRO-CDP frames: set_params(-1) before the first step only");
+            std::memcpy(init_host, host, size_t(P) * 4);
+            std::memset(init_host + P, 0, size_t(P) * 4);
+            for (int v = 0; v < 2; ++v) {
+                std::vector<uint32_t> tag(kMaxStages, uint32_t(v == 0 ? t : t - 1));
+                CDP_CUDA(cudaMemcpy(ring->vtag[v == 0 ? (t & 1) : ((t & 1) ^ 1)], tag.data(), kMaxStages * 4,
+                                    cudaMemcpyHostToDevice));
+            }
+            return;
+        }
         for (int v = 0; v < 2; ++v) {
             if (which >= 0 && v != which) continue;
             const int slot = v == 0 ? (t & 1) : ((t & 1) ^ 1);
@@ -1390,9 +1627,22 @@ struct ResNetTrainer {
     }
 
     void get_params(int which, float *host) {
+        CDP_REQUIRE(!frames, "ZeRO-CDP frames hold single stages: gather with cdp_resnet_zero_state");
         CDP_CUDA(cudaStreamSynchronize(main));
         const int slot = which == 0 ? (t & 1) : ((t & 1) ^ 1);
         CDP_CUDA(cudaMemcpy(host, theta[slot], size_t(P) * 4, cudaMemcpyDeviceToHost));
+    }
+
+    // ZeRO-CDP frames: this rank's frame contents in the full parameter layout (every tensor, valid or
+    // not) and its last finished use index per tensor (the holder of a stage's newest state is the rank
+    // with the largest one).
+    void zero_state(int which, float *host, uint32_t *last_use) {
+        CDP_REQUIRE(frames, "zero_state: ZeRO-CDP frames only");
+        CDP_CUDA(cudaDeviceSynchronize());
+        const int slot = which == 0 ? (t & 1) : ((t & 1) ^ 1);
+        for (size_t i = 0; i < tens.size(); ++i)
+            CDP_CUDA(cudaMemcpy(host + tens[i].base, thp(slot, int(i)), size_t(tens[i].n) * 4, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemcpy(last_use, ring->zdone, tens.size() * 4, cudaMemcpyDeviceToHost));
     }
 
     void stage_control(const int *perm, float lr) {
@@ -1410,6 +1660,8 @@ struct ResNetTrainer {
     }
 
     void step(const int *perm, float lr) {
+        CDP_REQUIRE(!drained, "ZeRO-CDP frames: a drained run cannot continue (its last states sit in next-step "
+                              "forward frames); gather the parameters and start a new run");
         stage_control(perm, lr);
         CDP_CUDA(cudaGraphLaunch(exec[t & 1], main));
         ++t;
@@ -1505,6 +1757,7 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
         CDP_REQUIRE(!(tr->allreduce && zero_table), "the DP all-reduce baseline and ZeRO-CDP are exclusive");
         if (zero_table && world > 1) {
             tr->zero = true;
+            tr->frames = (options & 4) == 0;  // options bit 2: full replicas (state copied, nothing freed)
             tr->ztab.assign(zero_table, zero_table + size_t(world) * 2 * world * 3);
             for (int k = 0; k < world * 2 * world; ++k) {
                 CDP_REQUIRE(tr->ztab[k * 3 + 1] >= 0 && tr->ztab[k * 3 + 1] < world, "ZeRO table: bad source rank");
@@ -1516,7 +1769,9 @@ extern "C" int cdp_resnet_create_rank(int n_layers, const int32_t *widths, const
         tr->data_lab = DevBuf(size_t(tr->n_samples) * 4);
         if (x) CDP_CUDA(cudaMemcpy(tr->data_x.p, x, size_t(n_samples) * HWC * 4, cudaMemcpyHostToDevice));
         if (labels) CDP_CUDA(cudaMemcpy(tr->data_lab.p, labels, size_t(n_samples) * 4, cudaMemcpyHostToDevice));
+        tr->stage_in = tensor_stage;
         tr->build(widths, depths, n_layers);
+        tr->stage_in = nullptr;
         for (size_t i = 0; i < tr->tens.size(); ++i) {
             const int st = tensor_stage[i];
             CDP_REQUIRE(st >= 1 && st <= world, "tensor stage out of range");
@@ -1558,7 +1813,7 @@ extern "C" int cdp_resnet_connect(cdp_resnet *tr, void *const *regions) {
         auto at = [&](int r) { return static_cast<uint8_t *>(regions[r]); };
         if (m.rank > 0) {
             m.prev_ring = reinterpret_cast<RingFlags *>(at(m.rank - 1));
-            m.prev_partial = reinterpret_cast<float *>(at(m.rank - 1) + m.region_off) + 2 * m.Pp;
+            m.prev_partial = reinterpret_cast<float *>(at(m.rank - 1) + m.region_off) + 2 * m.th_stride;
         }
         m.peers.assign(size_t(m.world), nullptr);
         for (int r = 0; r < m.world; ++r) m.peers[r] = at(r);
@@ -1614,6 +1869,17 @@ extern "C" int cdp_resnet_partial(cdp_resnet *tr, void **ptr, size_t *n) {
 
 extern "C" int cdp_resnet_stream(cdp_resnet *tr, void **stream) {
     return guarded([&] { *stream = tr->impl->main; });
+}
+
+extern "C" int cdp_resnet_zero_drain_plan(cdp_resnet *tr, const int32_t *rows, int n_rows) {
+    return guarded([&] {
+        CDP_REQUIRE(n_rows >= 0 && (n_rows == 0 || rows), "drain plan rows");
+        tr->impl->zdrain.assign(rows, rows + size_t(n_rows) * 5);
+    });
+}
+
+extern "C" int cdp_resnet_zero_state(cdp_resnet *tr, int which, float *theta, uint32_t *last_use) {
+    return guarded([&] { tr->impl->zero_state(which, theta, last_use); });
 }
 
 extern "C" int cdp_resnet_zero_drain(cdp_resnet *tr) {
@@ -1690,9 +1956,13 @@ extern "C" int cdp_resnet_stats(cdp_resnet *tr, int64_t *out, int n_out) {
         int64_t act = int64_t(m.cols.hi.bytes + m.cols.lo.bytes);
         for (auto &a : m.acts) act += int64_t(a.hi.bytes + a.lo.bytes);
         for (auto &c : m.convs) act += int64_t(c.y.bytes + c.dy.hi.bytes + c.dy.lo.bytes);
-        int64_t par = int64_t(m.Pp) * (m.vel ? 16 : 12);
-        for (int v = 0; v < 2; ++v)
+        // persistent parameter state: theta slots, momentum, compute copies (frames in ZeRO-CDP mode) and
+        // the gradient partial sum
+        int64_t par = int64_t(m.th_stride) * (m.vel ? 12 : 8) + int64_t(m.Pp) * 4;
+        for (int v = 0; v < 2; ++v) {
             for (auto &w : m.wc[v]) par += int64_t(w.hi.bytes + w.lo.bytes);
+            par += int64_t(m.wcpool[v][0].bytes + m.wcpool[v][1].bytes);
+        }
         int64_t scratch = 0;
         for (auto &g : m.gbuf) scratch += int64_t(g.bytes);
         int64_t vals[6] = {act, par, m.kernels_per_step, int64_t(m.flops_per_step), scratch, m.zero_bytes_per_step};

@@ -71,9 +71,53 @@ def layer_specs(widths, depths, in_ch=3, hw=32, block="basic", stem="cifar", cla
     return out
 
 
-def stage_partition(specs, n_stages):
-    """Contiguous groups of tensors with balanced FLOPs (BN/fc ride with their neighbour)."""
-    flops = np.array([max(f, 1) for _, _, f in specs], dtype=np.float64)
+def block_starts(widths, depths, block="basic", stem="cifar"):
+    """Tensor indices (layer_specs order) where a residual block, or the classifier, starts."""
+    starts, i, cin = [], 2, widths[0]
+    exp = 4 if block == "bottleneck" else 1
+    for l, (w, d) in enumerate(zip(widths, depths)):
+        for k in range(d):
+            stride = 2 if (l > 0 and k == 0) else 1
+            starts.append(i)
+            i += 2 * (2 if block == "basic" else 3) + (2 if (stride != 1 or cin != w * exp) else 0)
+            cin = w * exp
+    starts.append(i)  # the classifier
+    return starts
+
+
+def zero_partition(widths, depths, hw, block, stem, classes, n_stages):
+    """ZeRO-CDP stages: balanced parameter counts with boundaries only at residual-block (or classifier)
+    starts.  A block's last BN and its projection shortcut are one BN-backward kernel and its output's
+    BN apply reads both, so a boundary inside a block would interleave two stages' use windows on a rank,
+    against the reference order the state-frame reuse waits rely on (csrc/resnet_trainer.cu)."""
+    specs = layer_specs(widths, depths, 3, hw, block, stem, classes)
+    return stage_partition(specs, n_stages, "params", starts=block_starts(widths, depths, block, stem))
+
+
+def stage_partition(specs, n_stages, by="flops", starts=None):
+    """Contiguous groups of tensors with balanced FLOPs (BN/fc ride with their neighbour), or balanced
+    parameter counts (by="params"); `starts`: the only tensor indices a stage may begin at (besides 0)."""
+    if starts is not None:
+        w = np.array([max(float(np.prod(s)), 1.0) if by == "params" else max(f, 1) for _, s, f in specs])
+        cum = np.concatenate([[0.0], np.cumsum(w)])
+        cand = sorted(set(int(c) for c in starts if 0 < c < len(specs)))
+        if len(cand) < n_stages - 1:
+            raise ValueError(f"{n_stages} stages need {n_stages - 1} block boundaries, the model has {len(cand)}")
+        bounds, lo = [], 0
+        for k in range(1, n_stages):
+            # the remaining boundaries must still fit after this one
+            options = [c for c in cand if c > lo and len([x for x in cand if x > c]) >= n_stages - 1 - k]
+            c = min(options, key=lambda c: abs(cum[c] - cum[-1] * k / n_stages))
+            bounds.append(c)
+            lo = c
+        stage = np.ones(len(specs), dtype=np.int32)
+        for b in bounds:
+            stage[b:] += 1
+        return stage
+    if by == "params":
+        flops = np.array([max(float(np.prod(s)), 1.0) for _, s, _ in specs], dtype=np.float64)
+    else:
+        flops = np.array([max(f, 1) for _, _, f in specs], dtype=np.float64)
     cum = np.cumsum(flops)
     total = cum[-1]
     stage = np.empty(len(specs), dtype=np.int32)
@@ -163,7 +207,7 @@ class DeviceResNet:
     def __init__(self, widths=RESNET18["widths"], depths=RESNET18["depths"], micro_batch=128, world=1, rank=0,
                  rule=None, dtype="bf16", momentum=0.0, weight_decay=0.0, inputs=None, labels=None, classes=10,
                  image_hw=32, stage_of_tensor=None, block="basic", stem="cifar", zero=False, dp_allreduce=False,
-                 trace=False):
+                 trace=False, zero_frames=True):
         self.lib = N.lib()
         self.widths, self.depths = tuple(widths), tuple(depths)
         self.block, self.stem, self.classes, self.image_hw = block, stem, int(classes), int(image_hw)
@@ -172,7 +216,10 @@ class DeviceResNet:
         self.specs = layer_specs(self.widths, self.depths, 3, image_hw, block, stem, classes)
         n_t = len(self.specs)
         self.stage = np.ascontiguousarray(stage_of_tensor if stage_of_tensor is not None
-                                          else stage_partition(self.specs, world), dtype=np.int32)
+                                          else zero_partition(self.widths, self.depths, image_hw, block, stem,
+                                                              classes, world) if (zero and zero_frames and world > 1)
+                                          else stage_partition(self.specs, world),
+                                          dtype=np.int32)
         fresh = np.ones(world, dtype=np.uint8)
         if rule is not None:
             if rule.n != world:
@@ -203,9 +250,18 @@ class DeviceResNet:
             len(w), _i32p(w), _i32p(d), BLOCKS[block], STEMS[stem], 3, image_hw, image_hw, classes, self.micro_batch, world, rank,
             _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), DTYPES[dtype], float(momentum), float(weight_decay),
             n, x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
-            _i32p(ztab) if ztab is not None else None, (1 if dp_allreduce else 0) | (2 if trace else 0),
+            _i32p(ztab) if ztab is not None else None,
+            (1 if dp_allreduce else 0) | (2 if trace else 0) | (0 if zero_frames else 4),
             ctypes.byref(h)))
         self.dp_allreduce = bool(dp_allreduce)
+        # ZeRO-CDP keeps two stage frames of parameter state per rank (include/cdp_b200.h); full replicas
+        # with zero_frames=False
+        self.zero_frames = self.zero and bool(zero_frames)
+        if self.zero_frames:
+            from .zero import frame_drain_plan
+
+            rows = np.ascontiguousarray(np.array(frame_drain_plan(world)[rank], dtype=np.int32).reshape(-1, 5))
+            N.check(self.lib.cdp_resnet_zero_drain_plan(h, _i32p(rows) if len(rows) else None, len(rows)))
         self.h = h
         self._keep = (x, lab)
         np_, nt = ctypes.c_int64(), ctypes.c_int()
@@ -351,6 +407,15 @@ class DeviceResNet:
         N.check(self.lib.cdp_resnet_info(self.h, ctypes.byref(np_), ctypes.byref(nt),
                                          base.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), None))
         return base
+
+    def zero_state(self, which=0):
+        """ZeRO-CDP frames: (this rank's frame contents in the full layout, last finished use per tensor)."""
+        n_t = len(self.specs)
+        theta = np.zeros(self.P, dtype=np.float32)
+        last = np.zeros(n_t, dtype=np.uint32)
+        N.check(self.lib.cdp_resnet_zero_state(self.h, int(which), theta.ctypes.data_as(N.c_float_p),
+                                               last.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))))
+        return theta, last
 
     def zero_drain(self):
         """ZeRO-CDP: publish the next step's forward uses (call on every rank before synchronising at the
@@ -565,3 +630,18 @@ class ZeroDpRank:
         self.broadcast()
         self.tr.step(perm, lr)
         self.reduce_update()
+
+
+def gather_zero_params(ranks, which=0) -> np.ndarray:
+    """The newest parameter state of a ZeRO-CDP (frames) job: every tensor from the rank whose last finished
+    use of it is the latest (call after zero_drain + sync on every rank).  Full-replica ranks: the last
+    rank's copy (the updater holds every stage's newest version)."""
+    if not ranks[0].zero_frames:
+        return ranks[-1].get_params(which)
+    states = [r.zero_state(which) for r in ranks]
+    base = [int(b) for b in ranks[0].tensor_bases()] + [ranks[0].P]
+    out = np.zeros(ranks[0].P, dtype=np.float32)
+    for i in range(len(base) - 1):
+        holder = max(range(len(ranks)), key=lambda r: int(states[r][1][i]))
+        out[base[i]:base[i + 1]] = states[holder][0][base[i]:base[i + 1]]
+    return out

@@ -144,3 +144,89 @@ def state_bytes_per_step(plan: ZeroPlan, stage_params, rank: int, momentum: bool
             if int(plan.prev[s, ki, rank]) != rank:
                 total += per_param * int(stage_params[s])
     return total
+
+
+
+def frame_drain_plan(n: int) -> list:
+    """End-of-run drain of ZeRO-CDP state frames (csrc/resnet_trainer.cu), per rank.
+
+    A rank keeps the state of stage s in frame (s - 1) & 1 and reuses a frame once the previous
+    occupant's successor has copied it out.  In the CDP-v2 ZeRO placement the last ranks' late backward
+    windows hand their state to NEXT-step forwards of earlier ranks (N = 4: w4's B2 -> w1's F4 of step
+    t + 1), so at the end of a run those forwards' state copies must still happen: the drain of rank r
+    copies stage s's state for its next-step forward, for every s in the returned list, in order (the
+    closure: forwards whose copy a frame reuse waits for, their own frame reuses, their predecessors).
+    Each entry is (stage s (1-based), previous occupant stage (0-based, -1: none), kind of its last
+    use, that use's step offset and its successor's step offset from it): the frame wait before the
+    copy, relative to the drain's step (the next, unlaunched one).  A drained run cannot continue."""
+    cfg = ParallelismConfig(scheme=Scheme.ZERO_CDP, n=n, training_steps=8)
+    tl = build_zero_timeline(cfg, make_homogeneous_profile(n, n, n, 1), cyclic=True)
+    tasks = [t for t in tl.tasks if t.kind in KINDS]
+    T = 4  # a steady last step; offsets are relative to T + 1
+    succ, pred = {}, {}
+    for s in range(1, n + 1):
+        uses = sorted((t for t in tasks if t.stage == s), key=lambda t: t.start)
+        for a, b in zip(uses, uses[1:]):
+            succ[id(a)], pred[id(b)] = b, a
+    devs = [f"w{r + 1}" for r in range(n)]
+    seqs = {d: sorted((t for t in tasks if t.device == d), key=lambda t: t.start) for d in devs}
+
+    def windows(d):
+        wins = []
+        for t in seqs[d]:
+            if wins and wins[-1][-1].stage == t.stage:
+                wins[-1].append(t)
+            else:
+                wins.append([t])
+        return wins
+
+    drained = set()
+
+    def executed(t):  # ran in steps <= T, or in the drain (F1 of T + 1 is a no-copy publish)
+        return t.training_step <= T or id(t) in drained or (
+            t.training_step == T + 1 and t.kind is TaskKind.FORWARD and t.stage == 1)
+
+    waits = {}
+    changed = True
+    while changed:
+        changed = False
+        waits = {}
+        for d in devs:
+            last_in_frame = {}
+            for w in windows(d):
+                if not executed(w[0]):
+                    continue
+                f = (w[0].stage - 1) & 1
+                occ = last_in_frame.get(f)
+                p = pred.get(id(w[0]))
+                copies = p is not None and p.device != d
+                if copies and id(w[0]) in drained:
+                    if occ is None:
+                        waits[id(w[0])] = (-1, 0, 0, 0)
+                    else:
+                        lu = [t for t in occ if executed(t)][-1]
+                        sc = succ[id(lu)]
+                        waits[id(w[0])] = (lu.stage - 1, KINDS.index(lu.kind), lu.training_step - (T + 1),
+                                           sc.training_step - lu.training_step)
+                if occ is not None and copies:
+                    lu = [t for t in occ if executed(t)][-1]
+                    sc = succ.get(id(lu))
+                    if sc is not None and not executed(sc):
+                        if sc.kind is not TaskKind.FORWARD or sc.training_step != T + 1:
+                            raise AssertionError("ZeRO-CDP frames: a frame reuse waits on an undrainable use")
+                        drained.add(id(sc))
+                        changed = True
+                last_in_frame[f] = w
+        for i in list(drained):
+            t = next(x for x in tasks if id(x) == i)
+            p = pred[i]
+            if not executed(p):
+                if p.kind is not TaskKind.FORWARD or p.training_step != T + 1:
+                    raise AssertionError("ZeRO-CDP frames: a drained forward has an undrainable predecessor")
+                drained.add(id(p))
+                changed = True
+    out = []
+    for r, d in enumerate(devs):
+        rows = sorted(((t.stage,) + waits[id(t)] for t in tasks if id(t) in drained and t.device == d))
+        out.append(rows)
+    return out

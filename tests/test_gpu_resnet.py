@@ -203,28 +203,36 @@ def test_profile_and_host_batch_steps(cuda):
         assert np.array_equal(params, res[0][1])
 
 
-@pytest.mark.parametrize("world,arch", [(2, "basic"), (4, "basic"), (3, "bottleneck")])
+@pytest.mark.parametrize("world,arch", [(2, "basic"), (4, "basic"), (3, "bottleneck"), (3, "basic")])
 def test_zero_cdp_vs_torch_restatement(cuda, world, arch):
-    """ZeRO-CDP (parameter state handed holder -> next user by P2P copy, ref comm.py:93-144) matches the
-    float64 restatement of CDP-v2 at 1e-6 and is bit-identical to full-replica CDP-v2; a mid-run drain +
-    sync (end of a run, then continuing) does not change the result.  The ZeRO ranks cannot be stepped
-    one synchronised step at a time (a backward may wait for another rank's next-step forward), so the
-    restatement follows the branch decisions captured from the (bit-identical) full-replica run."""
+    """ZeRO-CDP (parameter state handed holder -> next user by P2P copy, ref comm.py:93-144) matches the float64
+    restatement of CDP-v2 at 1e-6 and is bit-identical to CDP-v2 without ZeRO, in both layouts:
+    * state frames (the default): each rank holds two stage frames (ref schedule.py:449-458: a worker holds
+      the stage it uses), the end-of-run drain makes the next-step forward copies the last frame reuses wait
+      for (zero.py frame_drain_plan), the newest state is gathered from the last holders;
+    * full replicas: a mid-run drain + sync (end of a run, then continuing) does not change the result.
+    The ZeRO ranks cannot be stepped one synchronised step at a time (a backward may wait for another rank's
+    next-step forward), so the restatement follows the branch decisions captured from the full-replica run
+    without ZeRO."""
     from oracle.resnet_torch import init_flat
-    from paper_2403_08837_b200.resnet import DeviceResNet
+    from paper_2403_08837_b200.resnet import DeviceResNet, gather_zero_params, zero_partition
     from paper_2403_08837_b200.rules import rule_by_name
 
     a = ARCH[arch]
     rule = rule_by_name("cdp-v2", world)
+    # parameter-balanced, block-aligned stages (the ZeRO-CDP default), the same for every mode
+    stage = zero_partition(W, D, a["hw"], a["block"], a["stem"], a["classes"], world)
     x, y = _data(world * MB * 2, hw=a["hw"], classes=a["classes"])
     init = init_flat(W, D, seed=0, block=a["block"], stem=a["stem"], classes=a["classes"])
     steps = 5
     perms = [np.random.default_rng([7, t]).permutation(len(x))[: world * MB] for t in range(1, steps + 1)]
     out = {}
     kinks = []
-    for zero in (False, True):
+    for mode in ("none", "frames", "replicas"):
+        zero = mode != "none"
         tr = [DeviceResNet(W, D, MB, world, r, rule, "fp32", 0.9, inputs=x, labels=y, image_hw=a["hw"],
-                           block=a["block"], stem=a["stem"], classes=a["classes"], zero=zero) for r in range(world)]
+                           block=a["block"], stem=a["stem"], classes=a["classes"], zero=zero,
+                           zero_frames=mode == "frames", stage_of_tensor=stage) for r in range(world)]
         regions = [t.region() for t in tr]
         for t in tr:
             t.set_params(init, -1)
@@ -236,8 +244,9 @@ def test_zero_cdp_vs_torch_restatement(cuda, world, arch):
                 if not zero:
                     t.sync()
                     per_rank.append(t.branch_decisions())
-            kinks.append(per_rank)
-            if zero and k == 2:  # end-of-run drain in the middle, then continue
+            if not zero:
+                kinks.append(per_rank)
+            if mode == "replicas" and k == 2:  # end-of-run drain in the middle, then continue
                 for t in tr:
                     t.zero_drain()
                 for t in tr:
@@ -247,20 +256,29 @@ def test_zero_cdp_vs_torch_restatement(cuda, world, arch):
         for t in tr:
             t.sync()
             assert t.ring_error() == 0
-        out[zero] = (np.mean([t.history(steps)[0] for t in tr], axis=0), tr[-1].get_params(0),
-                     tr[0].stats()["zero_state_bytes_per_step"], tr[0].stage)
+        out[mode] = (np.mean([t.history(steps)[0] for t in tr], axis=0), gather_zero_params(tr, 0),
+                     tr[0].stats()["zero_state_bytes_per_step"], tr[0].stage,
+                     max(t.stats()["param_state_bytes"] for t in tr))
+        if mode == "frames":
+            with pytest.raises(Exception):  # a drained frame run cannot continue
+                tr[0].step(perms[0][:MB], 0.05)
         for t in tr:
             t.close()
-    assert np.array_equal(out[True][0], out[False][0])
-    assert np.array_equal(out[True][1], out[False][1])
-    assert out[True][2] > 0 and out[False][2] == 0
+    for mode in ("frames", "replicas"):
+        assert np.array_equal(out[mode][0], out["none"][0]), mode
+        assert np.array_equal(out[mode][1], out["none"][1]), mode
+        assert out[mode][2] > 0, mode
+    assert out["none"][2] == 0
+    # two stage frames per rank instead of the whole model: below the full replica from 3 stages on
+    if world >= 3:
+        assert out["frames"][4] < out["replicas"][4], (out["frames"][4], out["replicas"][4])
     from oracle.resnet_torch import Kinks, run_cdp
 
-    fresh = [[rule.reads_fresh(i, int(s)) for s in out[True][3]] for i in range(1, world + 1)]
+    fresh = [[rule.reads_fresh(i, int(s)) for s in out["none"][3]] for i in range(1, world + 1)]
     k = [[Kinks(relu, pool) for relu, pool in st] for st in kinks[:steps]]
     want, _ = run_cdp(W, D, init, x.astype(np.float64), y, world, MB, perms, 0.05, 0.9, fresh, block=a["block"],
                       stem=a["stem"], classes=a["classes"], kinks=k)
-    assert _rel(out[True][1], want) <= ARCH[arch]["fp32_tol"], _rel(out[True][1], want)
+    assert _rel(out["frames"][1], want) <= ARCH[arch]["fp32_tol"], _rel(out["frames"][1], want)
 
 
 def test_dp_allreduce_baseline_bit_identical_to_dp_ring(cuda):

@@ -76,3 +76,32 @@ def test_drain_units_are_next_step_forward_predecessors(n):
     got = {(s, r) for r in range(n) for s in drain_units(plan, r)}
     want = {(s + 1, int(plan.prev[s, 1, j])) for s in range(n) for j in range(n) if int(plan.dstep[s, 1, j]) == 1}
     assert got == want
+
+
+def test_frame_drain_plan():
+    """End-of-run drain of the ZeRO-CDP state frames: the next-step forward copies the last frame reuses wait
+    for (N = 4: w1's F3 / F4, w2's F3), derivable for N = 2..8 (every needed copy's predecessors are
+    earlier steps or drained forwards — the planner raises otherwise)."""
+    from paper_2403_08837_b200.zero import frame_drain_plan
+
+    assert frame_drain_plan(2) == [[], []]
+    assert frame_drain_plan(3) == [[(3, 0, 0, 0, -1)], [], []]
+    assert frame_drain_plan(4) == [[(3, 0, 0, 0, -1), (4, 1, 1, -1, 0)], [(3, 0, 0, 0, -1)], [], []]
+    for n in (5, 6, 8):
+        plan = frame_drain_plan(n)
+        assert len(plan) == n and not plan[-1] and not plan[-2]  # the last ranks drain nothing
+        for rows in plan:
+            assert [r[0] for r in rows] == sorted(r[0] for r in rows)  # use order
+
+
+def test_zero_partition_is_block_aligned():
+    from paper_2403_08837_b200.resnet import RESNET50, block_starts, layer_specs, zero_partition
+
+    W, D = RESNET50["widths"], RESNET50["depths"]
+    starts = set(block_starts(W, D, "bottleneck", "imagenet"))
+    specs = layer_specs(W, D, 3, 224, "bottleneck", "imagenet", 1000)
+    for n in (2, 4, 8):
+        st = zero_partition(W, D, 224, "bottleneck", "imagenet", 1000, n)
+        assert len(st) == len(specs) and st[0] == 1 and st[-1] == n
+        cuts = [i for i in range(1, len(st)) if st[i] != st[i - 1]]
+        assert len(cuts) == n - 1 and set(cuts) <= starts
