@@ -139,18 +139,32 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
 // row groups of a warp are combined by one shuffle level, and part[w][col][2] gets warp w's partial.
 // The statistics are those of the stored bf16 outputs; about 4 instructions per element against ~11
 // for the TMEM-register butterfly (FSEL / SHFL: 55 % of the 1x1 forward epilogue's instructions).
+template <int COLS>  // 128: two 64-column boxes, 8 rows per thread; 64: one box, 4 rows per thread
 __device__ __forceinline__ void pk_tile_stats(const uint8_t *buf, const int *rowm, float *part, int tid) {
-    const int cg = tid & 15, rg = tid >> 4, k = cg >> 3, j = cg & 7;
-    const int4 rm0 = *reinterpret_cast<const int4 *>(rowm + 8 * rg);
-    const int4 rm1 = *reinterpret_cast<const int4 *>(rowm + 8 * rg + 4);
-    const int rv[8] = {rm0.x, rm0.y, rm0.z, rm0.w, rm1.x, rm1.y, rm1.z, rm1.w};
+    static_assert(COLS == 128 || COLS == 64, "staging pass width");
+    constexpr int CG = COLS / 8, RPT = 128 * CG / 256;  // column groups; rows per thread
+    const int cg = tid % CG, rg = tid / CG, k = cg >> 3, j = cg & 7;
+    int rv[8];
+    {
+        const int4 m0 = *reinterpret_cast<const int4 *>(rowm + RPT * rg);
+        const int4 m1 = RPT == 8 ? *reinterpret_cast<const int4 *>(rowm + RPT * rg + 4) : m0;
+        rv[0] = m0.x;
+        rv[1] = m0.y;
+        rv[2] = m0.z;
+        rv[3] = m0.w;
+        rv[4] = m1.x;
+        rv[5] = m1.y;
+        rv[6] = m1.z;
+        rv[7] = m1.w;
+    }
     float sm[8], sq[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) sm[c] = sq[c] = 0.f;
-    const uint8_t *base = buf + k * 16384 + (8 * rg) * 128;
+    const uint8_t *base = buf + k * 16384 + (RPT * rg) * 128;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(base + i * 128 + ((j ^ i) << 4));
+    for (int i = 0; i < RPT; ++i) {
+        const int r = RPT * rg + i;
+        const uint4 w = *reinterpret_cast<const uint4 *>(base + i * 128 + ((j ^ (r & 7)) << 4));
         if (rv[i] < 0) continue;
         const uint32_t u[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -163,12 +177,14 @@ __device__ __forceinline__ void pk_tile_stats(const uint8_t *buf, const int *row
         }
     }
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], 16);
-        sq[c] += __shfl_xor_sync(0xffffffffu, sq[c], 16);
-    }
-    if ((tid & 16) == 0) {
-        float4 *o = reinterpret_cast<float4 *>(part + ((tid >> 5) * 128 + cg * 8) * 2);
+    for (int off = CG; off < 32; off <<= 1)  // the warp's row groups of this column group
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], off);
+            sq[c] += __shfl_xor_sync(0xffffffffu, sq[c], off);
+        }
+    if ((tid & 31) < CG) {
+        float4 *o = reinterpret_cast<float4 *>(part + ((tid >> 5) * COLS + cg * 8) * 2);
 #pragma unroll
         for (int c = 0; c < 4; ++c) o[c] = make_float4(sm[2 * c], sq[2 * c], sm[2 * c + 1], sq[2 * c + 1]);
     }
@@ -548,18 +564,6 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                                 w.w = pk_bf16x2(v[8 * i + 6], v[8 * i + 7]);
                                 *reinterpret_cast<uint4 *>(rp + (((u0 + i) ^ (row & 7)) << 4)) = w;
                             }
-                            if constexpr (C::EPI_COLS != 128) {
-                                if (stats) {  // squares in place, then the values again from TMEM (32 live)
-                                    float *pp = spart + (q * C::EPI_COLS + c + ptx::lane_id()) * 3;
-#pragma unroll
-                                    for (int i = 0; i < 32; ++i) v[i] = row_m >= 0 ? v[i] * v[i] : 0.f;
-                                    pp[1] = warp_colsum32(v);
-                                    ptx::tmem_ld32(taddr + uc, v);
-#pragma unroll
-                                    for (int i = 0; i < 32; ++i) v[i] = row_m >= 0 ? v[i] : 0.f;
-                                    pp[0] = warp_colsum32(v);
-                                }
-                            }
                         }
                         ptx::fence_proxy_async_smem();  // staging writes -> async proxy (TMA store)
                         if (h == BN / C::EPI_COLS - 1) ptx::tc_fence_before();
@@ -583,17 +587,11 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                             ptx::bulk_commit();
                             ptx::bulk_wait_read1();  // the other buffer (previous pass) is free again
                         }
-                        if (stats) {
-                            if constexpr (C::EPI_COLS == 128) {  // from the stored bf16 tile (staging read-back)
-                                pk_tile_stats(buf, rowm, spart, tid);
-                                pk_bar(1, kPkEpi);
-                                Epi::col_stats8(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), tid,
-                                                spre + h * 256);
-                            } else {
-                                Epi::template col_stats<kPkEpi>(ep, spart, C::EPI_COLS, col0,
-                                                                min(C::EPI_COLS, args.N - col0), tm, tid,
-                                                                spre + h * 256);
-                            }
+                        if (stats) {  // from the stored bf16 tile (staging read-back)
+                            pk_tile_stats<C::EPI_COLS>(buf, rowm, spart, tid);
+                            pk_bar(1, kPkEpi);
+                            Epi::col_stats8(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), tid,
+                                            spre + h * 256);
                         }
                         pk_bar(1, kPkEpi);  // spart / staging reused by the next pass
                     }
