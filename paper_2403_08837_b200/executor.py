@@ -341,3 +341,29 @@ def compile_segment_plan(n_workers: int, seg_stage, seg_pool, rule: UpdateRule |
     return SegmentPlan(np.asarray(ops, dtype=np.int32).reshape(-1, 3), slot,
                        np.asarray([max(c, 1) for c in count], dtype=np.int32),
                        np.asarray(curve, dtype=np.int32), fresh)
+
+
+def plan_live_peak(plan: StepPlan, dims, micro_batch: int, elem_bytes: int) -> dict:
+    """Peak of the LIVE activation records over the plan's op order (the order the executor issues them):
+    record (i, l) - the input of layer l for micro-batch i - is live from the forward that produces it to
+    the backward of layer l.  The time-resolved quantity the reference's (N+1)/2-vs-N record count is
+    about (ref costs.py:111-115); the allocation (`record_bytes`) keeps per-layer slots for the whole step,
+    so with unequal layer widths its ratio is larger."""
+    pad = lambda c: (c + 15) // 16 * 16
+    size = {l: micro_batch * pad(dims[l - 1]) * elem_bytes for l in range(1, len(dims))}
+    live, peak_b, peak_n, cur_b, cur_n = set(), 0, 0, 0, 0
+    n_layers = len(dims) - 1
+    for row in plan.ops:
+        kind, i, l = int(row[0]), int(row[1]), int(row[2])
+        if kind == OP_F:
+            for rec in ([(i, 1)] if l == 1 else []) + ([(i, l + 1)] if l < n_layers else []):
+                if rec not in live:
+                    live.add(rec)
+                    cur_b += size[rec[1]]
+                    cur_n += 1
+        elif kind == OP_B and (i, l) in live:
+            live.discard((i, l))
+            cur_b -= size[l]
+            cur_n -= 1
+        peak_b, peak_n = max(peak_b, cur_b), max(peak_n, cur_n)
+    return {"peak_live_bytes": peak_b, "peak_live_records": peak_n}

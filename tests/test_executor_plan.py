@@ -106,3 +106,22 @@ def _simulate_slots_layers(plan, n_layers):
                 owner[(l + 1, rout)] = i
         else:
             assert owner[(l, rin)] == i
+
+
+def test_plan_live_record_peak_matches_reference_count():
+    """Single-GPU CDP holds N(N+1)/2 live records at its peak against DP's N^2 (ref costs.py:111-115), over the
+    op order the executor issues; with layer 1 much wider than the rest the byte ratio stays larger."""
+    from paper_2403_08837_b200.executor import compile_step_plan, plan_live_peak
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    for n in (2, 3, 4, 6):
+        dims = [64] * (n + 1)
+        dp = plan_live_peak(compile_step_plan(n, n, None), dims, 8, 2)
+        assert dp["peak_live_records"] == n * n
+        for r in ("cdp-v1", "cdp-v2"):
+            cdp = plan_live_peak(compile_step_plan(n, n, rule_by_name(r, n)), dims, 8, 2)
+            assert cdp["peak_live_records"] == n * (n + 1) // 2, (n, r)
+    wide = [3072, 256, 256, 256, 10]
+    cdp = plan_live_peak(compile_step_plan(4, 4, rule_by_name("cdp-v1", 4)), wide, 32, 2)
+    dp = plan_live_peak(compile_step_plan(4, 4, None), wide, 32, 2)
+    assert 0.8 < cdp["peak_live_bytes"] / dp["peak_live_bytes"] < 0.95
