@@ -198,6 +198,10 @@ int cdp_resnet_zero_state(cdp_resnet *tr, int which, float *theta, uint32_t *las
  * its last use kind, step offset, successor step offset) from zero.py frame_drain_plan; a drained run
  * cannot take further steps. */
 int cdp_resnet_zero_drain_plan(cdp_resnet *tr, const int32_t *rows, int n_rows);
+/* Theta delivery along the readers (before connect; CDP ring runs): [n_stages = world][2] = (rank this
+ * rank pulls each new version of the stage from, -1 = the updater; rank that pulls it from this one, -1 =
+ * none) in the rule's reader order (resnet.pull_chain).  Without it every reader pulls from the updater. */
+int cdp_resnet_pull_chain(cdp_resnet *tr, const int32_t *pred_succ, int n_stages);
 /* Parameter count, tensor count and (optional) per-tensor base offsets / kinds (0 conv, 1 bn, 2 fc). */
 int cdp_resnet_info(cdp_resnet *tr, int64_t *n_params, int *n_tensors, int64_t *tensor_base, int32_t *tensor_kind);
 int cdp_resnet_region(cdp_resnet *tr, void **base);

@@ -70,6 +70,7 @@ SIGNATURES = {
     "cdp_resnet_zero_drain": (c_int, [c_void_p]),
     "cdp_resnet_zero_state": (c_int, [c_void_p, c_int, c_float_p, ctypes.POINTER(ctypes.c_uint32)]),
     "cdp_resnet_zero_drain_plan": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_int32), c_int]),
+    "cdp_resnet_pull_chain": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_int32), c_int]),
     "cdp_resnet_apply_update": (c_int, [c_void_p]),
     "cdp_resnet_apply_update_range": (c_int, [c_void_p, c_int, c_int]),
     "cdp_resnet_pack_range": (c_int, [c_void_p, c_int, c_int, c_int]),

@@ -156,6 +156,8 @@ struct RingFlags {
     uint32_t zdone[kMaxStages];      // ZeRO-CDP: global use index of this rank's last finished use of a unit
     uint32_t zcopied[kMaxStages];    // ZeRO-CDP frames: use index of the successor that copied this rank's unit
     uint32_t vtag[2][kMaxStages];    // trace mode: version held by theta slot s of unit j (travels with the data)
+    uint32_t fwd_have[kMaxStages];   // pull chain: newest version of unit j this reader holds (pulled)
+    uint32_t fwd_pulled[kMaxStages][2];  // pull chain: version the next reader took from this reader's slot
     uint32_t err;                    // a spin-wait timed out (protocol failure)
     uint32_t pad[31];
 };

@@ -160,6 +160,58 @@ __global__ void pull_tensor_kernel(const float *__restrict__ src, float *dst, in
     }
 }
 
+// ---------------------------------------------------------------- theta forwarding along the readers
+// The readers of version v of a unit pull it in the order they read it (the reader order of the rule:
+// fresh readers in worker order at step v, then stale readers at step v + 1); the first takes it from
+// the updater, each later one from the reader before it, so every rank serves one copy per version
+// instead of the updater serving all N - 1 (the egress hot spot of the N - 1 pulls from rank N - 1).
+// A reader overwrites its slot v & 1 with v + 2 only after its successor took v from it.
+__global__ void chain_wait_kernel(const RingFlags *pred, int pred_is_updater, RingFlags *own, int unit, int fresh,
+                                  int has_succ, const int *step) {
+    const int t = *step;
+    const uint32_t v = uint32_t(fresh ? t : t - 1);
+    if (v <= 1 || threadIdx.x != 0) return;
+    if (pred_is_updater)
+        spin_ge(&pred->updated[unit - 1], v, &own->err);
+    else
+        spin_ge(&pred->fwd_have[unit - 1], v, &own->err);
+    if (has_succ && v > 3) spin_ge(&own->fwd_pulled[unit - 1][v & 1], v - 2, &own->err);
+}
+
+template <int KIND>
+__global__ void chain_pull_kernel(const float *__restrict__ src, float *dst, int64_t n, int cols, CTensor wc,
+                                  RingFlags *pred, int pred_is_updater, RingFlags *own, int unit, int fresh,
+                                  const int *step, unsigned *cta_counter, int trace) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int t = *step;
+    const uint32_t v = uint32_t(fresh ? t : t - 1);
+    if (v <= 1) return;
+    StateCopy c{};
+    c.src[0] = src;
+    c.dst[0] = dst;
+    c.narr = 1;
+    c.wc[0] = wc;
+    c.n = n;
+    c.cols = cols;
+    state_copy<KIND>(c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(&cta_counter[unit - 1], 1u) == gridDim.x - 1) {
+            cta_counter[unit - 1] = 0;
+            // the source cannot overwrite slot v & 1 before this arrival: its tag is the copied version
+            if (trace) own->vtag[v & 1][unit - 1] = ptx::ld_acquire_sys(&pred->vtag[v & 1][unit - 1]);
+            __threadfence_system();
+            ptx::st_release_sys(&own->fwd_have[unit - 1], v);
+            if (pred_is_updater)
+                atomicAdd_system(&pred->pulled[unit - 1][v & 1], 1u);
+            else
+                ptx::st_release_sys(&pred->fwd_pulled[unit - 1][v & 1], v);
+        }
+    }
+}
+
 __global__ void finish_step_kernel_rn(const double *loss, Flags *flags, double *hist_loss, Flags *hist_flags, int cap,
                                       const int *step) {
     const int c = *step - 1;

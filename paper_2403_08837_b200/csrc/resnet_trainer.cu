@@ -195,6 +195,8 @@ struct ResNetTrainer {
     const int32_t *stage_in = nullptr;           // tensor -> stage, set before build()
     std::vector<int> zwin_done;                  // per (stage, kind): frame wait recorded in this step
     std::vector<int> zdrain;                     // end-of-run drain plan rows (zero.py frame_drain_plan)
+    std::vector<int> chain;                      // pull chain per stage: (predecessor rank or -1 = updater,
+                                                 // successor rank or -1); empty: every reader pulls from the updater
     bool drained = false;                        // frames: a drained run cannot continue
     std::vector<CBuf> acts;    // activations (compute format)
     std::vector<int> act_C, act_H, act_W;
@@ -1079,7 +1081,8 @@ struct ResNetTrainer {
         hp.grad_flags = &fl->grad;
         hp.upd_flags = &fl->upd;
         hp.sync.enabled = 1;
-        hp.sync.n_readers = zero ? 0 : world - 1;  // ZeRO-CDP: no parameter pulls from the updater
+        // ZeRO-CDP: no parameter pulls; pull chain: only the first reader takes from the updater
+        hp.sync.n_readers = zero ? 0 : !chain.empty() ? 1 : world - 1;
         hp.sync.step = &ctrl_dev.as<Control>()->step;
         hp.sync.own = ring;
         hp.sync.prev = prev_ring;
@@ -1294,6 +1297,23 @@ struct ResNetTrainer {
         if (sizing) return;
         CDP_REQUIRE(upd_ring && upd_theta[vslot], "pull outside a connected multi-GPU trainer");
         CTensor w = ts.kind == T_BN ? CTensor{} : wcv[vslot][tensor];
+        if (!chain.empty()) {  // forwarding along the reader order (pull chain)
+            const int st = ts.stage - 1, pr = chain[size_t(st) * 2], sc = chain[size_t(st) * 2 + 1];
+            RingFlags *pf = pr < 0 ? upd_ring : reinterpret_cast<RingFlags *>(peers[pr]);
+            const float *src = pr < 0 ? upd_theta[vslot] + ts.base : peer_theta(pr, vslot) + foff[tensor];
+            L("pull_wait", 0, 0, s, [&] {
+                chain_wait_kernel<<<1, 32, 0, s>>>(pf, pr < 0 ? 1 : 0, ring, tensor + 1, ts.fresh, sc >= 0 ? 1 : 0,
+                                                   (const int *)&ctrl_dev.as<Control>()->step);
+                CDP_CUDA(cudaGetLastError());
+            });
+            L("pull", 0, double(ts.n) * (4 + 4 + esz()), s, [&] {
+                launch_pdl(chain_pull_kernel<K>, dim3(blocks_for(ts.n, 1024)), dim3(256), 0, s, src,
+                           thp(vslot, tensor), ts.n, std::max(ts.cols, 1), w, pf, pr < 0 ? 1 : 0, ring, tensor + 1,
+                           ts.fresh, (const int *)&ctrl_dev.as<Control>()->step,
+                           cta_counters.as<unsigned>() + kMaxStages, trace ? 1 : 0);
+            });
+            return;
+        }
         L("pull_wait", 0, 0, s, [&] {
             pull_wait_kernel<<<1, 32, 0, s>>>(upd_ring, ring, tensor + 1, ts.fresh,
                                               (const int *)&ctrl_dev.as<Control>()->step);
@@ -1869,6 +1889,19 @@ extern "C" int cdp_resnet_partial(cdp_resnet *tr, void **ptr, size_t *n) {
 
 extern "C" int cdp_resnet_stream(cdp_resnet *tr, void **stream) {
     return guarded([&] { *stream = tr->impl->main; });
+}
+
+extern "C" int cdp_resnet_pull_chain(cdp_resnet *tr, const int32_t *pred_succ, int n_stages) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_REQUIRE(!m.exec[0], "the pull chain is set before connect (graph capture)");
+        CDP_REQUIRE(n_stages == 0 || (n_stages == m.world && pred_succ), "pull chain: one row per stage");
+        CDP_REQUIRE(!m.zero && !m.allreduce, "pull chain: CDP ring runs only");
+        for (int k = 0; k < 2 * n_stages; ++k)
+            CDP_REQUIRE(pred_succ[k] >= -1 && pred_succ[k] < m.world - 1 && pred_succ[k] != m.rank,
+                        "pull chain: ranks of other readers");
+        m.chain.assign(pred_succ, pred_succ + size_t(n_stages) * 2);
+    });
 }
 
 extern "C" int cdp_resnet_zero_drain_plan(cdp_resnet *tr, const int32_t *rows, int n_rows) {

@@ -21,6 +21,7 @@ unpinned" by the reference).  Conventions:
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -257,6 +258,12 @@ class DeviceResNet:
         # ZeRO-CDP keeps two stage frames of parameter state per rank (include/cdp_b200.h); full replicas
         # with zero_frames=False
         self.zero_frames = self.zero and bool(zero_frames)
+        # theta delivery along the reader order (csrc/rank_common.cuh chain kernels); CDP_PULL_CHAIN=0: every
+        # reader pulls from the updater
+        self.pull_chain = None
+        if world > 1 and not self.zero and not dp_allreduce and os.environ.get("CDP_PULL_CHAIN", "1") != "0":
+            self.pull_chain = pull_chain(rule, world, rank)
+            N.check(self.lib.cdp_resnet_pull_chain(h, _i32p(self.pull_chain), world))
         if self.zero_frames:
             from .zero import frame_drain_plan
 
@@ -630,6 +637,22 @@ class ZeroDpRank:
         self.broadcast()
         self.tr.step(perm, lr)
         self.reduce_update()
+
+
+def pull_chain(rule, world: int, rank: int) -> np.ndarray:
+    """[world stages][2] (predecessor, successor) of `rank` in the order the readers (ranks 0 .. world-2; the
+    last rank updates) read each new version of a stage: fresh readers at step v in worker order, then stale
+    readers at step v + 1 (ref rules.py:45-51); -1: the updater / none."""
+    out = np.full((world, 2), -1, dtype=np.int32)
+    readers = range(world - 1)
+    for j in range(1, world + 1):
+        fresh = [rule is None or rule.reads_fresh(r + 1, j) for r in readers]
+        order = [r for r in readers if fresh[r]] + [r for r in readers if not fresh[r]]
+        if rank in order:
+            k = order.index(rank)
+            out[j - 1, 0] = order[k - 1] if k > 0 else -1
+            out[j - 1, 1] = order[k + 1] if k + 1 < len(order) else -1
+    return out
 
 
 def gather_zero_params(ranks, which=0) -> np.ndarray:

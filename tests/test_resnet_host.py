@@ -94,3 +94,27 @@ def test_bottleneck_imagenet_layout_roundtrip():
     m = TorchResNet(w, d, 10, "bottleneck", "imagenet").double()
     load_flat(m, flat, specs)
     assert np.array_equal(torch_to_flat(m), flat)
+
+
+def test_pull_chain_follows_the_reader_order():
+    """Theta forwarding: per stage, the readers (ranks 0..N-2) form one chain - fresh readers in worker order,
+    then stale ones - whose head pulls from the updater; each reader serves exactly its successor."""
+    from paper_2403_08837_b200.resnet import pull_chain
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    for n in (2, 3, 4, 8):
+        for rule in (None, rule_by_name("cdp-v1", n), rule_by_name("cdp-v2", n)):
+            ch = [pull_chain(rule, n, r) for r in range(n - 1)]
+            for j in range(n):
+                heads = [r for r in range(n - 1) if ch[r][j, 0] == -1]
+                assert len(heads) == 1
+                order, r = [], heads[0]
+                while r != -1:
+                    order.append(r)
+                    nxt = int(ch[r][j, 1])
+                    if nxt != -1:
+                        assert ch[nxt][j, 0] == r
+                    r = nxt
+                assert sorted(order) == list(range(n - 1))
+                fresh = [rule is None or rule.reads_fresh(r + 1, j + 1) for r in order]
+                assert fresh == sorted(fresh, reverse=True)  # fresh readers first
