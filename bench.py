@@ -562,6 +562,10 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
                 "param_pull_read_bytes_per_rank": [int(v[1]) for v in allv],
                 "zero_state_bytes_per_rank": [int(v[2]) for v in allv],
                 "bytes_per_step_all_ranks": int(sum(v[0] + v[1] + v[2] for v in allv)),
+            "pull_sources": ("reader chain (csrc/rank_common.cuh): the updater and every reader serve at most one "
+                             "copy of each version, 4 B / param per step"
+                             if getattr(tr, "pull_chain", None) is not None else
+                             "every reader pulls from the updater: (N-1) x 4 B / param of updater egress"),
                 "grad_gbs_in_hop_kernels_rank1": round(allv[1][0] / (allv[1][3] / 1e3) / 1e9, 1) if allv[1][3] else None,
                 "pull_gbs_rank0": round((allv[0][1] + allv[0][2]) / (allv[0][4] / 1e3) / 1e9, 1) if allv[0][4] else None,
                 "note": "peer HBM over NVLink when ranks sit on different GPUs; same-GPU ranks (tests) read local HBM"}
