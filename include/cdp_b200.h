@@ -297,6 +297,8 @@ int cdp_vit_stats(cdp_vit *tr, int64_t *out, int n_out);
 int cdp_vit_mark(cdp_vit *tr, int k);
 int cdp_vit_elapsed(cdp_vit *tr, int a, int b, float *ms);
 int cdp_vit_flush_l2(cdp_vit *tr);
+/* Theta delivery along the readers, as cdp_resnet_pull_chain (before connect). */
+int cdp_vit_pull_chain(cdp_vit *tr, const int32_t *pred_succ, int n_stages);
 /* Fused multi-head attention (csrc/attn_kernels.cuh) on caller-owned device buffers: bf16 token-major
  * qkv [B*T][qkv_ld] (Q | K | V blocks of H*64 columns, head h at +h*64), O [B*T][o_ld], lse fp32
  * [B*H*T]; backward != 0 also writes dQ | dK | dV into dqkv from dO.  T <= 256, head dim 64, scale 1/8.

@@ -123,6 +123,7 @@ SIGNATURES = {
     "cdp_vit_mark": (c_int, [c_void_p, c_int]),
     "cdp_vit_elapsed": (c_int, [c_void_p, c_int, c_int, c_float_p]),
     "cdp_vit_flush_l2": (c_int, [c_void_p]),
+    "cdp_vit_pull_chain": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_int32), c_int]),
     "cdp_attention": (c_int, [c_void_p, ctypes.c_int64, c_void_p, ctypes.c_int64, c_int, c_int, c_int, c_void_p,
                               ctypes.c_int64, c_void_p, c_void_p, ctypes.c_int64, c_int]),
     "cdp_test_gemm": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p), c_int,

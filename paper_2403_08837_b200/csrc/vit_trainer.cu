@@ -127,6 +127,8 @@ struct VitTrainer {
     RingFlags *ring = nullptr;
     size_t region_off = 0;
     RingFlags *prev_ring = nullptr, *upd_ring = nullptr;
+    std::vector<uint8_t *> peer_regions;  // every rank's shared region (the pull chain's sources)
+    std::vector<int> chain;               // pull chain per stage (predecessor or -1 = updater, successor or -1)
     float *prev_partial = nullptr, *upd_theta[2] = {nullptr, nullptr};
     std::vector<CBuf> wc[2];
     std::vector<VRec> brec;
@@ -628,7 +630,7 @@ struct VitTrainer {
         hp.grad_flags = &fl->grad;
         hp.upd_flags = &fl->upd;
         hp.sync.enabled = W == 1 ? 1 : 0;
-        hp.sync.n_readers = world - 1;
+        hp.sync.n_readers = chain.empty() ? world - 1 : 1;  // pull chain: only its head takes from the updater
         hp.sync.step = &ctrl_dev.as<Control>()->step;
         hp.sync.own = ring;
         hp.sync.prev = prev_ring;
@@ -648,6 +650,25 @@ struct VitTrainer {
         const VUnit &u = units[unit];
         const int vslot = vs(unit, p);
         CTensor w = u.kind == V_LIN ? wc[vslot][unit].view() : CTensor{};
+        if (!chain.empty()) {  // forwarding along the reader order (rank_common.cuh chain kernels)
+            const int st = u.stage - 1, pr = chain[size_t(st) * 2], sc = chain[size_t(st) * 2 + 1];
+            RingFlags *pf = pr < 0 ? upd_ring : reinterpret_cast<RingFlags *>(peer_regions[pr]);
+            const float *src = (pr < 0 ? upd_theta[vslot]
+                                       : reinterpret_cast<const float *>(peer_regions[pr] + region_off) + vslot * Pp) +
+                               u.base;
+            L_("pull_wait", 0, 0, s, [&] {
+                chain_wait_kernel<<<1, 32, 0, s>>>(pf, pr < 0 ? 1 : 0, ring, unit + 1, u.fresh, sc >= 0 ? 1 : 0,
+                                                   (const int *)&ctrl_dev.as<Control>()->step);
+                CDP_CUDA(cudaGetLastError());
+            });
+            L_("pull", 0, double(u.n) * 10, s, [&] {
+                launch_pdl(chain_pull_kernel<0>, dim3(blocks_for(u.n, 1024)), dim3(256), 0, s, src,
+                           theta[vslot] + u.base, u.n, std::max(u.cols, 1), w, pf, pr < 0 ? 1 : 0, ring, unit + 1,
+                           u.fresh, (const int *)&ctrl_dev.as<Control>()->step,
+                           cta_counters.as<unsigned>() + kMaxStages, trace ? 1 : 0);
+            });
+            return;
+        }
         L_("pull_wait", 0, 0, s, [&] {
             pull_wait_kernel<<<1, 32, 0, s>>>(upd_ring, ring, unit + 1, u.fresh,
                                               (const int *)&ctrl_dev.as<Control>()->step);
@@ -1396,6 +1417,18 @@ extern "C" int cdp_vit_ipc_handle(cdp_vit *tr, void *handle64) {
     });
 }
 
+extern "C" int cdp_vit_pull_chain(cdp_vit *tr, const int32_t *pred_succ, int n_stages) {
+    return guarded([&] {
+        auto &m = *tr->impl;
+        CDP_REQUIRE(!m.exec[0], "the pull chain is set before connect (graph capture)");
+        CDP_REQUIRE(n_stages == 0 || (n_stages == m.world && pred_succ), "pull chain: one row per stage");
+        for (int k = 0; k < 2 * n_stages; ++k)
+            CDP_REQUIRE(pred_succ[k] >= -1 && pred_succ[k] < m.world - 1 && pred_succ[k] != m.rank,
+                        "pull chain: ranks of other readers");
+        m.chain.assign(pred_succ, pred_succ + size_t(n_stages) * 2);
+    });
+}
+
 extern "C" int cdp_vit_connect(cdp_vit *tr, void *const *regions) {
     return guarded([&] {
         auto &m = *tr->impl;
@@ -1408,6 +1441,8 @@ extern "C" int cdp_vit_connect(cdp_vit *tr, void *const *regions) {
         m.upd_ring = reinterpret_cast<RingFlags *>(at(u));
         m.upd_theta[0] = reinterpret_cast<float *>(at(u) + m.region_off);
         m.upd_theta[1] = m.upd_theta[0] + m.Pp;
+        m.peer_regions.assign(size_t(m.world), nullptr);
+        for (int r = 0; r < m.world; ++r) m.peer_regions[r] = at(r);
         m.capture();
     });
 }

@@ -15,6 +15,7 @@ for the CDP step (ViT GEMMs on tcgen05), parity-checked against a torch-CPU floa
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -142,6 +143,13 @@ class DeviceVit:
         if trace:
             N.check(self.lib.cdp_vit_set_trace(self.h, 1))
         np_, nu = ctypes.c_int64(), ctypes.c_int()
+        # theta delivery along the reader order (see resnet.pull_chain); CDP_PULL_CHAIN=0: from the updater
+        self.pull_chain = None
+        if world > 1 and os.environ.get("CDP_PULL_CHAIN", "1") != "0":
+            from .resnet import pull_chain
+
+            self.pull_chain = pull_chain(rule, world, rank)
+            N.check(self.lib.cdp_vit_pull_chain(self.h, _i32p(self.pull_chain), world))
         N.check(self.lib.cdp_vit_info(self.h, ctypes.byref(np_), ctypes.byref(nu)))
         assert nu.value == len(self.units), (nu.value, len(self.units))
         self.P = np_.value
