@@ -1453,7 +1453,7 @@ struct ResNetTrainer {
             const int a = stem_act, o = pool_act;
             L("maxpool_bwd", 0, double(act_P[o]) * act_C[o] * (1 + ysz()) + double(act_P[a]) * act_C[a] * ysz(), cs,
               [&] {
-                launch_pdl(maxpool_bwd_kernel<K>, dim3(blocks_for(act_P[a] * act_C[a] / 8)), dim3(256), 0, cs,
+                launch_pdl(maxpool_bwd_owner_kernel<K>, dim3(blocks_for(act_P[o] * act_C[o] / 8)), dim3(256), 0, cs,
                            (const void *)G0, (const uint8_t *)pool_arg.as<uint8_t>(), B, act_H[a], act_W[a],
                            act_C[a], act_H[o], act_W[o], G1);
             });
