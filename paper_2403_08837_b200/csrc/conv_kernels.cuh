@@ -166,10 +166,9 @@ static __global__ void stem_im2col_kernel(const float *__restrict__ data, const 
 
 // Row-staged stem im2col: one CTA per (image, output row).  The R input rows the
 // output row reads (zero-padded left / right / outside the image) are staged in
-// shared memory with coalesced loads; a per-column offset table (k -> (r, s*C + c))
-// turns the gather into one shared-memory read per element; the CTA's output rows
-// form one contiguous [Wo][ld] block written with coalesced 16-byte stores.  (The
-// per-element version: 0.57 ms, 0.9 TB/s, for the 514 MB ImageNet-stem record.)
+// shared memory with 16-byte loads; each thread then writes one output pixel's
+// record row from them (the CTA's output rows form one contiguous [Wo][ld] block).
+// (The per-element version: 0.57 ms, 0.9 TB/s, for the 514 MB ImageNet-stem record.)
 // Requires (W + 2 pad) * C * R floats + ld ints of shared memory (dynamic).
 template <int KIND, int R, int C>
 static __global__ void __launch_bounds__(256) stem_im2col_rows_kernel(const float *__restrict__ data, const int *perm,
@@ -181,37 +180,45 @@ static __global__ void __launch_bounds__(256) stem_im2col_rows_kernel(const floa
     constexpr int S = R, K = R * S * C;
     const int Wp = W + 2 * pad;
     const int rowlen = Wp * C;
-    int *koff = reinterpret_cast<int *>(sm_rows + R * rowlen);
     const int ho = blockIdx.x % Ho, b = blockIdx.x / Ho;
     const float *img = data + size_t(__ldg(perm + b)) * H * W * C;
-    for (int k = threadIdx.x; k < cols.ld; k += blockDim.x) {
-        if (k < K) {
-            const int r = k / (S * C), rem = k - r * (S * C);
-            koff[k] = r * rowlen + rem;
-        } else {
-            koff[k] = -1;
-        }
+    // stage the R input rows: 16-byte loads of each row's W * C contiguous floats (one division per
+    // vector, none per element: the per-element version was instruction-bound at 1.8 TB/s), zero pads
+    const int WC4 = W * C / 4, padc = pad * C;
+    for (int i = threadIdx.x; i < R * WC4; i += blockDim.x) {
+        const int r = i / WC4, q4 = i - r * WC4;
+        const int h = ho * stride - pad + r;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (h >= 0 && h < H) x = __ldg(reinterpret_cast<const float4 *>(img + size_t(h) * W * C) + q4);
+        float *d = sm_rows + r * rowlen + padc + 4 * q4;
+        d[0] = x.x;
+        d[1] = x.y;
+        d[2] = x.z;
+        d[3] = x.w;
     }
-    for (int i = threadIdx.x; i < R * rowlen; i += blockDim.x) {
-        const int r = i / rowlen, q = i - r * rowlen;
-        const int h = ho * stride - pad + r, w = q / C - pad;
-        float x = 0.f;
-        if (h >= 0 && h < H && w >= 0 && w < W) x = __ldg(img + (size_t(h) * W + w) * C + (q - (q / C) * C));
-        sm_rows[i] = x;
+    for (int i = threadIdx.x; i < R * 2 * padc; i += blockDim.x) {
+        const int r = i / (2 * padc), q = i - r * 2 * padc;
+        sm_rows[r * rowlen + (q < padc ? q : padc + W * C + (q - padc))] = 0.f;
     }
     __syncthreads();
-    const int G = cols.ld / 8;
+    // gather: one thread per output pixel, its K = R * S * C values in k order (per tap row r a contiguous
+    // S * C run of the staged row), packed 8 at a time into 16-byte stores (no offset table: the table
+    // version was shared-memory bound, 92 % MIO)
+    constexpr int KP = (K + 7) / 8 * 8;
     const size_t row0 = (size_t(b) * Ho + ho) * Wo;
-    for (int e = threadIdx.x; e < Wo * G; e += blockDim.x) {
-        const int wo = e / G, k0 = (e - wo * G) * 8;
-        const int base = wo * stride * C;
+    for (int wo = threadIdx.x; wo < Wo; wo += blockDim.x) {
+        const float *src = sm_rows + wo * stride * C;
+        const size_t o = (row0 + wo) * cols.ld;
         F8 v;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int o = koff[k0 + j];
-            v.v[j] = o >= 0 ? sm_rows[o + base] : 0.f;
+        for (int k = 0; k < KP; ++k) {
+            const int r = k / (S * C), rem = k - r * (S * C);
+            v.v[k & 7] = k < K ? src[r * rowlen + rem] : 0.f;
+            if ((k & 7) == 7) st_c8<KIND>(cols, o + k - 7, v);
         }
-        st_c8<KIND>(cols, (row0 + wo) * cols.ld + k0, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v.v[j] = 0.f;
+        for (int k = KP; k < cols.ld; k += 8) st_c8<KIND>(cols, o + k, v);
     }
 }
 
@@ -1085,19 +1092,44 @@ static __global__ void maxpool_fwd_kernel(CTensor in, int B, int H, int W, int C
             best.v[j] = -INFINITY;
             bt[j] = 0;
         }
-        for (int r = 0; r < 3; ++r) {
-            const int h = ho * 2 - 1 + r;
-            if (h < 0 || h >= H) continue;
-            for (int s = 0; s < 3; ++s) {
-                const int w = wo * 2 - 1 + s;
-                if (w < 0 || w >= W) continue;
-                const F8 v = ld_c8<KIND>(in, ((size_t(b) * H + h) * W + w) * in.ld + c);
+        if constexpr (KIND == 0) {  // the nine window loads issued before any compare (latency-bound otherwise)
+            uint4 raw[9];
+            bool ok[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const int h = ho * 2 - 1 + k / 3, w = wo * 2 - 1 + k % 3;
+                ok[k] = h >= 0 && h < H && w >= 0 && w < W;
+                raw[k] = ok[k] ? *reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(in.hi) +
+                                                                  ((size_t(b) * H + h) * W + w) * in.ld + c)
+                               : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                if (!ok[k]) continue;
+                F8 v;
+                bf16x8_to_f8(raw[k], v);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     if (v.v[j] > best.v[j]) {
                         best.v[j] = v.v[j];
-                        bt[j] = uint8_t(r * 3 + s);
+                        bt[j] = uint8_t(k);
                     }
+            }
+        } else {
+            for (int r = 0; r < 3; ++r) {
+                const int h = ho * 2 - 1 + r;
+                if (h < 0 || h >= H) continue;
+                for (int s = 0; s < 3; ++s) {
+                    const int w = wo * 2 - 1 + s;
+                    if (w < 0 || w >= W) continue;
+                    const F8 v = ld_c8<KIND>(in, ((size_t(b) * H + h) * W + w) * in.ld + c);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (v.v[j] > best.v[j]) {
+                            best.v[j] = v.v[j];
+                            bt[j] = uint8_t(r * 3 + s);
+                        }
+                }
             }
         }
         st_c8<KIND>(out, size_t(p) * out.ld + c, best);

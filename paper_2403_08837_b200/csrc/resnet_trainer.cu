@@ -863,6 +863,7 @@ struct ResNetTrainer {
         L("stem_im2col", 0, double(c0.P) * cols.ld * esz(), s, [&] {
             const size_t smem = size_t(c0.R) * (Win + 2 * c0.pad) * Cin0 * 4 + size_t(cols.ld) * 4;
             CDP_REQUIRE(smem <= 48 * 1024, "stem input rows exceed the shared-memory stage");
+            CDP_REQUIRE((Win * Cin0) % 4 == 0, "stem rows are staged as 16-byte vectors (W * C % 4 == 0)");
             if (c0.R == 3)
                 launch_pdl(stem_im2col_rows_kernel<K, 3, 3>, dim3(B * c0.Ho), dim3(256), smem, s,
                            (const float *)data_x.as<float>(), (const int *)perm_dev.as<int>(), Hin, Win, c0.stride,
