@@ -213,6 +213,7 @@ def run_ours(args, ws, rank, local):
     tr.set_params(np.concatenate(task.init_params()), which=-1)
     if ws > 1:
         tr.connect_ipc(exchange_handles(tr.ipc_handle()))
+        torch.distributed.barrier()  # every rank captured its graphs before any step spins on a peer
     else:
         tr.connect([tr.region()])
     perms = [task.permutation(t)[rank * MB:(rank + 1) * MB] for t in range(1, args.warmup + args.steps + 2)]
@@ -403,6 +404,7 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
     n_data = x.shape[0]
     if ws > 1:
         tr.connect_ipc(exchange_handles(tr.ipc_handle()))
+        torch.distributed.barrier()  # every rank captured its graphs before any step spins on a peer
     else:
         tr.connect([tr.region()])
     perms = [np.random.default_rng([0, t]).permutation(n_data)[rank * B:(rank + 1) * B]
@@ -630,6 +632,7 @@ def run_resnet_variant(args, ws, rank, local, model, steps, warmup, mode):
     tr, B, hw, classes, x, y = make_trainer(a2, model, ws, rank, rule, allreduce, zero)
     if ws > 1:
         tr.connect_ipc(exchange_handles(tr.ipc_handle()))
+        torch.distributed.barrier()  # every rank captured its graphs before any step spins on a peer
     else:
         tr.connect([tr.region()])
     perms = [np.random.default_rng([0, t]).permutation(x.shape[0])[rank * B:(rank + 1) * B]
