@@ -470,33 +470,40 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
         out["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                       "note": "ZeRO-CDP state frames: a run cannot be synchronised mid-way (see run_resnet)"}
     elif e2e:
-        x_pin = torch.empty((B, hw, hw, 3), dtype=torch.float32, pin_memory=True)
-        y_pin = torch.empty((B,), dtype=torch.int32, pin_memory=True)
-        host = [(x[p], y[p]) for p in perms[:steps + 2]]
-        e_ms = []
+        # pinned host batches (a ring of 4 distinct batches, filled before the timed region); every step
+        # copies its batch H2D on the copy stream while the previous step computes (two input slots) and
+        # copies its loss back D2H; device time from the first copy to the last loss / steps
+        ring = 4
+        x_pins = [torch.empty((B, hw, hw, 3), dtype=torch.float32, pin_memory=True) for _ in range(ring)]
+        y_pins = [torch.empty((B,), dtype=torch.int32, pin_memory=True) for _ in range(ring)]
+        for k in range(ring):
+            x_pins[k].numpy()[:] = x[perms[k]]
+            y_pins[k].numpy()[:] = y[perms[k]]
+        ke = min(steps, 20) + 2
+        tr.step_host_batch_async(x_pins[0].data_ptr(), y_pins[0].data_ptr(), RN_LR, 0)  # warm the copy path
+        tr.sync()
         if ws > 1:
             torch.distributed.barrier()
-        for k in range(min(steps, 20) + 2):
-            x_pin.numpy()[:] = host[k][0]
-            y_pin.numpy()[:] = host[k][1]
+        tr.mark(0)
+        for k in range(ke):
             tr.flush_l2()
-            tr.mark(0)
-            tr.step_host_batch_ptr(x_pin.data_ptr(), y_pin.data_ptr(), RN_LR)
+            tr.step_host_batch_async(x_pins[k % ring].data_ptr(), y_pins[k % ring].data_ptr(), RN_LR, k % 2)
             reduce_update()
-            tr.zero_drain()
-            loss = tr.last_loss()
-            tr.mark(1)
-            assert np.isfinite(loss)
-            if k >= 2:
-                e_ms.append(tr.elapsed(0, 1))
-        e = float(np.mean(e_ms))
+        tr.mark(1)
+        tr.sync()
+        losses_e, flags_e = tr.history(ke)
+        assert np.all(np.isfinite(losses_e)) and not flags_e.any()
+        e = tr.elapsed(0, 1) / ke
         if ws > 1:
             t = torch.tensor([e], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e = float(t.item())
         out["e2e"] = {"value": round(ws * B / (e / 1e3), 1), "unit": UNIT,
                       "h2d_bytes_per_step": B * hw * hw * 3 * 4 + B * 4 + 16 + B * 4, "d2h_bytes_per_step": 8,
-                      "ms_per_step": round(e, 4)}
+                      "ms_per_step": round(e, 4),
+                      "how": "public API step_host_batch_async: every step copies its pinned host batch H2D (copy "
+                             "stream, two input slots: overlaps the previous step) and its loss D2H; device time "
+                             "from before the first copy to after the last step / steps, L2 flushed every step"}
     # ---- per-kernel breakdown: one serialised instrumented (real) step
     if frames:
         out["kernel_breakdown"] = None

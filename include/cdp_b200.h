@@ -213,6 +213,11 @@ int cdp_resnet_get_params(cdp_resnet *tr, int which, float *theta);
 int cdp_resnet_step(cdp_resnet *tr, const int32_t *perm, float lr);
 /* End-to-end step: micro_batch images x (host, fp32 NHWC) and labels copied H2D inside the step. */
 int cdp_resnet_step_host_batch(cdp_resnet *tr, const float *x, const int32_t *labels, float lr);
+/* Pipelined end-to-end step (needs >= 2 micro-batches of dataset rows): the pinned host batch is copied
+ * H2D on a copy stream into input slot `slot` (0 / 1) while the previous step computes; the step waits for
+ * its copy, reads its rows, and its loss is copied back to pinned host memory.  Asynchronous: the caller
+ * must not rewrite the host batch until the step has synchronised (cdp_resnet_sync). */
+int cdp_resnet_step_host_batch_async(cdp_resnet *tr, const float *x, const int32_t *labels, float lr, int slot);
 /* Loss of the most recent step (synchronises). */
 int cdp_resnet_last_loss(cdp_resnet *tr, double *loss);
 /* One real training step launched eagerly with timing events around every kernel:

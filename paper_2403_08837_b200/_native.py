@@ -77,6 +77,7 @@ SIGNATURES = {
     "cdp_resnet_partial": (c_int, [c_void_p, ctypes.POINTER(c_void_p), ctypes.POINTER(ctypes.c_size_t)]),
     "cdp_resnet_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "cdp_resnet_step_host_batch": (c_int, [c_void_p, c_float_p, c_int_p, c_float]),
+    "cdp_resnet_step_host_batch_async": (c_int, [c_void_p, c_float_p, c_int_p, c_float, c_int]),
     "cdp_resnet_last_loss": (c_int, [c_void_p, c_double_p]),
     "cdp_resnet_profile_step": (c_int, [c_void_p, c_int_p, c_float, c_int, c_int, ctypes.c_char_p, c_int, c_double_p,
                                         c_double_p, c_float_p, c_int_p]),

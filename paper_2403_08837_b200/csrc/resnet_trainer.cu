@@ -222,6 +222,9 @@ struct ResNetTrainer {
     int stage_next = 0;
     int hist_cap = 1 << 14;
     cudaStream_t main = nullptr, cs = nullptr, hs = nullptr, ps = nullptr;  // ps: parameter pulls (run ahead)
+    cudaStream_t cps = nullptr;           // pipelined input copies (step_host_batch_async)
+    cudaEvent_t in_ev[2] = {}, done_ev[2] = {};
+    double *loss_host = nullptr;          // pinned: the losses the pipelined steps read back
     std::vector<cudaEvent_t> events;
     cudaGraphExec_t exec[2] = {nullptr, nullptr};
     int t = 1;
@@ -246,7 +249,10 @@ struct ResNetTrainer {
             if (e) cudaEventDestroy(e);
         if (stage_host) cudaFreeHost(stage_host);
         if (init_host) cudaFreeHost(init_host);
-        for (auto s : {main, cs, hs, ps})
+        for (auto e : {in_ev[0], in_ev[1], done_ev[0], done_ev[1]})
+            if (e) cudaEventDestroy(e);
+        if (loss_host) cudaFreeHost(loss_host);
+        for (auto s : {main, cs, hs, ps, cps})
             if (s) cudaStreamDestroy(s);
     }
 
@@ -1699,6 +1705,34 @@ struct ResNetTrainer {
         step(ident.data(), lr);
     }
 
+    // Pipelined end-to-end step: the H2D copy of this step's batch runs on a copy stream into dataset
+    // rows [slot * B, slot * B + B) (two slots), so it overlaps the previous step's compute; the step
+    // waits for its copy, the copy into a slot waits for the step that last read it, and the loss is
+    // read back (D2H, into pinned memory) after every step.
+    void step_host_batch_async(const float *x, const int32_t *labels, float lr, int slot) {
+        CDP_REQUIRE(slot == 0 || slot == 1, "input slot 0 or 1");
+        CDP_REQUIRE(n_samples >= 2 * B, "the pipelined input needs 2 micro-batches of dataset rows");
+        if (!cps) {
+            CDP_CUDA(cudaStreamCreateWithFlags(&cps, cudaStreamNonBlocking));
+            for (auto *e : {&in_ev[0], &in_ev[1], &done_ev[0], &done_ev[1]})
+                CDP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            CDP_CUDA(cudaMallocHost(&loss_host, 2 * sizeof(double)));
+        }
+        const size_t img = size_t(Hin) * Win * Cin0;
+        CDP_CUDA(cudaStreamWaitEvent(cps, done_ev[slot], 0));
+        CDP_CUDA(cudaMemcpyAsync(data_x.as<float>() + size_t(slot) * B * img, x, size_t(B) * img * 4,
+                                 cudaMemcpyHostToDevice, cps));
+        CDP_CUDA(cudaMemcpyAsync(data_lab.as<int32_t>() + size_t(slot) * B, labels, size_t(B) * 4,
+                                 cudaMemcpyHostToDevice, cps));
+        CDP_CUDA(cudaEventRecord(in_ev[slot], cps));
+        CDP_CUDA(cudaStreamWaitEvent(main, in_ev[slot], 0));
+        std::vector<int> rows(B);
+        for (int i = 0; i < B; ++i) rows[i] = slot * B + i;
+        step(rows.data(), lr);
+        CDP_CUDA(cudaEventRecord(done_ev[slot], main));
+        CDP_CUDA(cudaMemcpyAsync(loss_host + slot, loss_dev.p, 8, cudaMemcpyDeviceToHost, main));
+    }
+
     // One real training step run eagerly (not from the graph) with timing events
     // around every launch; returns the per-launch records.
     // serial: every launch on one stream (clean per-kernel durations, no overlap).
@@ -1867,6 +1901,11 @@ extern "C" int cdp_resnet_step(cdp_resnet *tr, const int32_t *perm, float lr) {
 
 extern "C" int cdp_resnet_step_host_batch(cdp_resnet *tr, const float *x, const int32_t *labels, float lr) {
     return guarded([&] { tr->impl->step_host_batch(x, labels, lr); });
+}
+
+extern "C" int cdp_resnet_step_host_batch_async(cdp_resnet *tr, const float *x, const int32_t *labels, float lr,
+                                                int slot) {
+    return guarded([&] { tr->impl->step_host_batch_async(x, labels, lr, slot); });
 }
 
 extern "C" int cdp_resnet_apply_update(cdp_resnet *tr) {

@@ -322,6 +322,12 @@ class DeviceResNet:
         N.check(self.lib.cdp_resnet_step_host_batch(self.h, ctypes.cast(x_ptr, N.c_float_p),
                                                     ctypes.cast(y_ptr, ctypes.POINTER(ctypes.c_int)), float(lr)))
 
+    def step_host_batch_async(self, x_ptr: int, y_ptr: int, lr: float, slot: int):
+        """Pipelined step on a pinned host batch (include/cdp_b200.h): its H2D copy overlaps the previous
+        step; do not rewrite the host buffers before a sync."""
+        N.check(self.lib.cdp_resnet_step_host_batch_async(self.h, ctypes.cast(x_ptr, N.c_float_p),
+                                                          ctypes.cast(y_ptr, N.c_int_p), float(lr), int(slot)))
+
     def step_host_batch(self, x, y, lr):
         xa = np.ascontiguousarray(x, dtype=np.float32)
         ya = np.ascontiguousarray(y, dtype=np.int32)

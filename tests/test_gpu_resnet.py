@@ -384,3 +384,35 @@ def test_bench_shapes_vs_torch_restatement(cuda, arch, world, steps, dtype):
     else:
         assert rel <= max(3e-2, 1.25 * t_rel), (rel, t_rel)
         assert lrel <= max(1e-2, 2 * t_lrel), (losses, wl, tl)
+
+
+def test_pipelined_host_batch_steps_match_graph_steps(cuda):
+    """step_host_batch_async (H2D copy of step k+1 on a copy stream while step k computes, two input slots,
+    loss read back every step) runs the same math as graph steps on the same batches."""
+    import torch
+
+    from oracle.resnet_torch import init_flat
+    from paper_2403_08837_b200.resnet import DeviceResNet
+
+    x, y = _data(MB * 4)
+    init = init_flat(W, D, seed=0)
+    batches = [np.random.default_rng([5, k]).permutation(len(x))[:MB] for k in range(5)]
+    out = []
+    for how in ("graph", "async"):
+        tr = DeviceResNet(W, D, MB, 1, 0, None, "fp32", 0.9, inputs=x, labels=y, image_hw=HW)
+        tr.set_params(init, -1)
+        tr.connect([tr.region()])
+        pins = []
+        for k, b in enumerate(batches):
+            if how == "graph":
+                tr.step(b, 0.05)
+            else:
+                xp = torch.from_numpy(np.ascontiguousarray(x[b])).pin_memory()
+                yp = torch.from_numpy(np.ascontiguousarray(y[b].astype(np.int32))).pin_memory()
+                pins.append((xp, yp))
+                tr.step_host_batch_async(xp.data_ptr(), yp.data_ptr(), 0.05, k % 2)
+        tr.sync()
+        out.append((tr.history(len(batches))[0], tr.get_params(0)))
+        tr.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
