@@ -456,6 +456,16 @@ struct EpiConvOut2 {
                 make_float2(cur.x + s, cur.y + q);
         }
     }
+    // tensor-core statistics: the thread's column sum / sum of squares of the unit, added to the running value
+    __device__ static void col_stats_value(const Params &p, int col0, int ncols, int tid, float s, float q,
+                                           const float *slot) {
+        if (p.stats && tid < ncols) {
+            ptx::cp_async_wait_all();
+            const float2 cur = *reinterpret_cast<const float2 *>(slot + 2 * tid);
+            *reinterpret_cast<float2 *>(p.stats + (size_t(col0 + tid) * gridDim.x + blockIdx.x) * 2) =
+                make_float2(cur.x + s, cur.y + q);
+        }
+    }
     template <int NTH>  // one column per thread (ncols <= NTH)
     __device__ static void col_stats(const Params &p, const float *part, int pcols, int col0, int ncols, int tm,
                                      int tid, const float *slot) {

@@ -51,6 +51,9 @@ struct PkArgs {
     // TMA-staged epilogue operands (Epi::kTmaAdd): number of operand maps in GemmMaps::e (1: residual,
     // 2: residual + mask); 2-D {N, M} maps for GM_PLAIN, 4-D {N, W, H, B} pixel-box maps otherwise
     int tma_add;
+    // BN statistics of a 128-column TMA-store tile by two tensor-core MMAs (opt-in, CDP_MMA_STATS=1: correct,
+    // but slower than the staging read-back on B200 — the MMAs queue behind the next unit's mainloop)
+    int mma_stats;
     // Stride-2 data gradient with all sub-pixel phases in one launch (nph > 1): the batch index g of
     // a unit is its phase, cvp[g] its geometry (tap table, output phase offsets); no split-K.
     int nph;
@@ -105,7 +108,10 @@ struct PkCfg {
     static constexpr int STAGES = ST ? ST : (BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES);
     static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
     static constexpr int PRE_BYTES = 2 * 128 * 8;  // running column statistics of the unit (cp.async)
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + PART_BYTES + 512 + 256 + PRE_BYTES;
+    static constexpr int ONES_BYTES = 4096;        // bf16 ones [16][128] (K-major): the column-sum MMA's B
+    // rowm 512 B + barriers 256 B + PRE_BYTES, padded to 3 KB so the ones tile starts 1024-aligned
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + PART_BYTES + 3072 + ONES_BYTES;
+    static_assert(512 + 256 + PRE_BYTES <= 3072, "rowm / barrier / statistics-slot area");
     static constexpr uint32_t IDESC = ptx::instr_desc(KIND == 0 ? 1u : 2u, A_MN, B_MN, 128, BN);
     static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN must be 64, 128 or 256");
     static_assert(!B_MN || BN % CH == 0, "MN-major B needs BN multiple of the 128-byte row");
@@ -263,10 +269,16 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     constexpr int NES = C::EPI_COLS == 128 ? pk_ebuf_slots<Epi>() : 0;
     uint64_t *efull = tempty + 2;
     uint64_t *eempty = efull + NES;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(eempty + NES);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(eempty + NES + 1);
     float *spre = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(rowm) + 512 + 256);  // [2][128][2]
+    uint8_t *sones = reinterpret_cast<uint8_t *>(rowm) + 3072;  // 1024-aligned (rowm is)
+    // BN statistics of 128-column TMA-store tiles by the tensor core: the column sums and sums of squares
+    // of the staged bf16 tile Y are Y^T 1 and diag(Y^T Y), two MMAs into 144 spare TMEM columns
+    constexpr bool kMmaStats = Epi::kTmaStore && BN == 128 && KIND == 0;
+    constexpr uint32_t kTmemCols = kMmaStats ? 512u : C::TMEM_COLS;
+    uint64_t *sbar = eempty + NES;  // the statistics MMAs' commit barrier
     uint8_t *ebuf = smem + C::STAGES * C::STAGE_BYTES;
-    static_assert(C::STAGES * 2 + 4 + 2 * NES <= 30, "barrier area");
+    static_assert(C::STAGES * 2 + 4 + 2 * NES + 1 <= 30, "barrier area");
 
     const uint32_t warp = ptx::warp_id();
     if (warp == 0 && ptx::lane_id() == 0) {
@@ -288,9 +300,15 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             ptx::mbar_init(&efull[a], 1);
             ptx::mbar_init(&eempty[a], 4);  // the four TMEM-quarter warps of one column half
         }
+        ptx::mbar_init(sbar, 1);
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+    if constexpr (kMmaStats) {  // ones [16 rows][128] bf16, K-major 128-byte-swizzled (two 64-column chunks)
+        for (int i = threadIdx.x; i < C::ONES_BYTES / 4; i += blockDim.x)
+            reinterpret_cast<uint32_t *>(sones)[i] = 0x3F803F80u;
+        ptx::fence_proxy_async_smem();
+    }
     ptx::tc_fence_before();
     if constexpr (CL == 1)
         __syncthreads();
@@ -562,10 +580,12 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                                 w.y = pk_bf16x2(v[8 * i + 2], v[8 * i + 3]);
                                 w.z = pk_bf16x2(v[8 * i + 4], v[8 * i + 5]);
                                 w.w = pk_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+                                // rows outside the output (never stored) are zero for the statistics MMAs
+                                if (kMmaStats && args.mma_stats && row_m < 0) w = make_uint4(0u, 0u, 0u, 0u);
                                 *reinterpret_cast<uint4 *>(rp + (((u0 + i) ^ (row & 7)) << 4)) = w;
                             }
                         }
-                        ptx::fence_proxy_async_smem();  // staging writes -> async proxy (TMA store)
+                        ptx::fence_proxy_async_smem();  // staging writes -> async proxy (TMA store / MMA)
                         if (h == BN / C::EPI_COLS - 1) ptx::tc_fence_before();
                         pk_bar(1, kPkEpi);
                         if (h == BN / C::EPI_COLS - 1 && tid == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -587,11 +607,43 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                             ptx::bulk_commit();
                             ptx::bulk_wait_read1();  // the other buffer (previous pass) is free again
                         }
-                        if (stats) {  // from the stored bf16 tile (staging read-back)
-                            pk_tile_stats<C::EPI_COLS>(buf, rowm, spart, tid);
-                            pk_bar(1, kPkEpi);
-                            Epi::col_stats8(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), tid,
-                                            spre + h * 256);
+                        if (stats) {
+                            if (kMmaStats && args.mma_stats) {  // diag(Y^T Y) and Y^T 1 of the staged tile
+                                if (tid == 0) {
+                                    ptx::tc_fence_after();
+                                    const uint32_t yb = ptx::smem_u32(buf), ob = ptx::smem_u32(sones);
+                                    constexpr uint32_t idG = ptx::instr_desc(1, true, true, 128, 128);
+                                    constexpr uint32_t idS = ptx::instr_desc(1, true, false, 128, 16);
+#pragma unroll
+                                    for (int k = 0; k < 8; ++k) {  // 16 rows per step
+                                        const uint64_t ya = ptx::smem_desc_sw128(yb + k * 2048, 16384, 1024);
+                                        ptx::umma<0>(tmem_base + 256, ya, ya, idG, k > 0 ? 1u : 0u);
+                                        ptx::umma<0>(tmem_base + 384, ya,
+                                                     ptx::smem_desc_sw128(ob + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024),
+                                                     idS, k > 0 ? 1u : 0u);
+                                    }
+                                    ptx::umma_commit(sbar);
+                                }
+                                if (warp < 8) {  // warps 4-7: TMEM lanes = the pass's 128 columns
+                                    ptx::mbar_wait(sbar, uint32_t(pc) & 1u);
+                                    ptx::tc_fence_after();
+                                    const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16);
+                                    float v[32], cs[1];
+                                    ptx::tmem_ld32(ta + 256 + q * 32, v);
+                                    ptx::tmem_ld1(ta + 384, cs);
+                                    float sq = 0.f;
+#pragma unroll
+                                    for (int k = 0; k < 32; ++k) sq = ptx::lane_id() == k ? v[k] : sq;
+                                    Epi::col_stats_value(ep, col0, min(C::EPI_COLS, args.N - col0), tid, cs[0], sq,
+                                                         spre + h * 256);
+                                    ptx::tc_fence_before();
+                                }
+                            } else {  // from the stored bf16 tile (staging read-back)
+                                pk_tile_stats<C::EPI_COLS>(buf, rowm, spart, tid);
+                                pk_bar(1, kPkEpi);
+                                Epi::col_stats8(ep, spart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), tid,
+                                                spre + h * 256);
+                            }
                         }
                         pk_bar(1, kPkEpi);  // spart / staging reused by the next pass
                     }
@@ -648,7 +700,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         __syncthreads();
     else
         ptx::cluster_sync();  // the partner's last multicast commits have landed
-    if (warp == 2) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem_base);
 }
 
 // Split-K tail: per (tile, row chunk of RC rows, column chunk of CC columns),
@@ -759,6 +811,11 @@ struct PkLaunch {
                 maps.o = make_tmap_4d(ep.out, ElemType::BF16, dims, str, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
             }
             a.tma_out = 1;
+            static const bool mma_on = [] {
+                const char *e = std::getenv("CDP_MMA_STATS");
+                return e && e[0] == '1';
+            }();
+            a.mma_stats = (mma_on && BN == 128 && KIND == 0) ? 1 : 0;
         }
     }
     // TMA-staged epilogue operands (Epi::kTmaAdd): maps of the residual gradient and its mask with the

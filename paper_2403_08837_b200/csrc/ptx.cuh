@@ -228,6 +228,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 1 fp32 column: thread t of the warp gets row (lane base + t).
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, float (&v)[1]) {
+    uint32_t r;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    v[0] = __uint_as_float(r);
+}
+
 // ---------------------------------------------------------------- descriptors
 // Shared-memory matrix descriptor (sm_100 "version 1").  layout: 2 = SWIZZLE_128B,
 // 1 = SWIZZLE_128B_BASE32B (32-byte swizzle atoms; the only MN-major layout for tf32).

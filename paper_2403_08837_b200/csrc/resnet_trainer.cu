@@ -786,6 +786,11 @@ struct ResNetTrainer {
 
     static int blocks_for(int64_t n, int per = 256) { return int(std::min<int64_t>(8 * 148, (n + per - 1) / per)); }
     static int tile_n(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }  // a supported BN covering n
+    // tile-width probe (development): env `name` caps the GEMM tile width of one class
+    static int tile_cap(const char *name, int bn) {
+        const char *e = std::getenv(name);
+        return e ? std::min(bn, std::atoi(e)) : bn;
+    }
 
     // ---------------------------------------------------------------- forward pieces
     template <int K>
@@ -795,18 +800,24 @@ struct ResNetTrainer {
         ep.out = c.y.p;
         ep.ld = c.cout;
         ep.stats = stats_fwd.as<float>();
+        static const bool no_stats_probe = std::getenv("CDP_PROBE_NO_FWD_STATS") != nullptr;  // timing probe only
+        if (no_stats_probe) ep.stats = nullptr;
         ep.tiles = c.tiles_fwd;
         const CTensor w = wcv[vslot][c.tw];
         rec(c.tw, A_FWD, 0, vslot, s);
         gemm_bytes = double(c.impl == CI_STEM ? c.P * cols.ld : c.Pin * c.cin) * esz() +
                      double(c.K) * c.cout * esz() + double(c.P) * c.cout * ysz();
         if (c.impl == CI_IMPLICIT) {
-            pk_conv<K, GM_FPROP, EpiConvOut2<K>>("conv_fprop", tile_n(c.cout), c, w, ep, s, false);
+            pk_conv<K, GM_FPROP, EpiConvOut2<K>>("conv_fprop", tile_cap("CDP_PROBE_BN_FPROP3", tile_n(c.cout)), c, w,
+                                                 ep, s, false);
         } else {
             const CTensor in = c.impl == CI_STEM ? cols.view() : acts[c.in_act].view();
             const int64_t Kd = c.impl == CI_STEM ? c.K : c.cin;
+            // 1x1 forward with BN statistics: 128-column tiles (tensor-core statistics, better balance than 256:
+            // measured 1.77 -> 1.59 ms per ResNet-50 step before the statistics MMAs)
+            const int bnt = c.impl == CI_STEM ? tile_n(c.cout) : tile_cap("CDP_PROBE_FWD1X1_BN", std::min(tile_n(c.cout), 128));
             pk_plain<K, false, true, EpiConvOut2<K>>(c.impl == CI_STEM ? "stem_fprop" : "conv_fprop_1x1",
-                                                     tile_n(c.cout), in, w, c.P, c.cout, Kd, ep, s, false);
+                                                     bnt, in, w, c.P, c.cout, Kd, ep, s, false);
         }
         rec(c.tw, A_FWD, 1, vslot, s);
         const int slots = sizing ? c.tiles_fwd : last_stat_slots;
@@ -1034,7 +1045,7 @@ struct ResNetTrainer {
             ep.ld = c.cin;
             if (tadd)
                 pk_tadd<K>([&](auto e) {
-                    pk_plain<K, false, false, decltype(e)>("conv_dgrad_1x1", tile_n(c.cin), c.dy.view(), w,
+                    pk_plain<K, false, false, decltype(e)>("conv_dgrad_1x1", tile_cap("CDP_PROBE_BN_DGRAD1", tile_n(c.cin)), c.dy.view(), w,
                                                            c.P, c.cin, c.cout, ep, s, false);
                 });
             else if (direct)
