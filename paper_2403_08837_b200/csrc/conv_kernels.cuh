@@ -227,6 +227,12 @@ __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.f + erff(x
 __device__ __forceinline__ float gelu_grad(float x) {
     return 0.5f * (1.f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * __expf(-0.5f * x * x);
 }
+// gelu(x) and gelu'(x) from one erf (the forward stores gelu'(z) for the backward instead of z)
+__device__ __forceinline__ void gelu_both(float x, float &g, float &d) {
+    const float e = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+    g = x * e;
+    d = e + x * 0.39894228040143268f * __expf(-0.5f * x * x);
+}
 
 // ---------------------------------------------------------------------------
 // Epilogues of the persistent GEMM (gemm_pk_kernel / pk_reduce_kernel): run()
@@ -250,6 +256,8 @@ struct EpiConvOut2 {
         int out_f32;         // 1: fp32 output rows (and `add` is fp32): the ViT residual stream
         CTensor gelu_out;    // also write gelu(out) here (compute format, own ld), or null
         const void *gelu_z;  // out *= gelu'(z), z Y-format with the output's layout, or null
+        const void *mul;     // out *= mul (Y format, the output's layout): a stored gelu'(z), or null
+        int out_gelu_grad;   // with gelu_out: the stored output is gelu'(x) instead of x (the backward's factor)
     };
     static constexpr int kStages = 0;
     static Params for_split(const Params &p) { return p; }
@@ -257,7 +265,7 @@ struct EpiConvOut2 {
     // the tile with TMA (gemm_pk_kernel, PkArgs::tma_out)
     static constexpr bool kTmaStore = KIND == 0;
     static bool tma_eligible(const Params &p) {
-        return KIND == 0 && p.out && !p.add && !p.out_mask.hi && !p.gelu_z && !p.gelu_out.hi && !p.out_f32 &&
+        return KIND == 0 && p.out && !p.add && !p.out_mask.hi && !p.gelu_z && !p.mul && !p.gelu_out.hi && !p.out_f32 &&
                (p.ld % 8) == 0 &&
                (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
     }
@@ -271,6 +279,7 @@ struct EpiConvOut2 {
         if (p.add) ptx::prefetch_l2(static_cast<const char *>(p.add) + o * ab, uint32_t(ncols * ab));
         if (KIND == 0 && p.add_mask.hi) ptx::prefetch_l2(static_cast<const char *>(p.add_mask.hi) + o * 2, uint32_t(ncols * 2));
         if (KIND == 0 && p.gelu_z) ptx::prefetch_l2(static_cast<const char *>(p.gelu_z) + o * 2, uint32_t(ncols * 2));
+        if (KIND == 0 && p.mul) ptx::prefetch_l2(static_cast<const char *>(p.mul) + o * 2, uint32_t(ncols * 2));
     }
 
     // Drain hook (per warp, lane = tile row, v = 32 consecutive columns from TMEM).
@@ -323,8 +332,13 @@ struct EpiConvOut2 {
                 if (p.out_mask.hi && !(Fmt<KIND>::load(p.out_mask.hi, p.out_mask.lo, o) > 0.f)) x = 0.f;
                 if (p.gelu_z) x *= gelu_grad(KIND == 0 ? Fmt<0>::load(p.gelu_z, nullptr, o)
                                                        : static_cast<const float *>(p.gelu_z)[o]);
-                if (p.gelu_out.hi)
-                    Fmt<KIND>::store(p.gelu_out.hi, p.gelu_out.lo, size_t(m) * p.gelu_out.ld + col0 + c, gelu(x));
+                if (p.mul) x *= KIND == 0 ? Fmt<0>::load(p.mul, nullptr, o) : static_cast<const float *>(p.mul)[o];
+                if (p.gelu_out.hi) {
+                    float gl, gd;
+                    gelu_both(x, gl, gd);
+                    Fmt<KIND>::store(p.gelu_out.hi, p.gelu_out.lo, size_t(m) * p.gelu_out.ld + col0 + c, gl);
+                    if (p.out_gelu_grad) x = gd;
+                }
                 if (p.out_f32 || KIND == 1)
                     static_cast<float *>(p.out)[o] = x;
                 else
@@ -380,21 +394,28 @@ struct EpiConvOut2 {
                     }
                     if (p.out_mask.hi) v[u][k] = relu_mask4(v[u][k], mk[u][k]);
                 }
-                if (p.gelu_z) {
-                    const F8 zz = ld_y8<KIND>(p.gelu_z, o[u]);
+                if (p.gelu_z || p.mul) {  // (exclusive) gelu'(z) from z, or a stored factor
+                    const F8 zz = ld_y8<KIND>(p.gelu_z ? p.gelu_z : p.mul, o[u]);
                     float w8[8] = {v[u][0].x, v[u][0].y, v[u][0].z, v[u][0].w,
                                    v[u][1].x, v[u][1].y, v[u][1].z, v[u][1].w};
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) w8[i] *= gelu_grad(zz.v[i]);
+                    for (int i = 0; i < 8; ++i) w8[i] *= p.gelu_z ? gelu_grad(zz.v[i]) : zz.v[i];
                     v[u][0] = make_float4(w8[0], w8[1], w8[2], w8[3]);
                     v[u][1] = make_float4(w8[4], w8[5], w8[6], w8[7]);
                 }
                 if (p.gelu_out.hi) {
                     const size_t og = size_t(gm[u]) * p.gelu_out.ld + gc[u];
-                    store_wc4<KIND>(p.gelu_out, og, make_float4(gelu(v[u][0].x), gelu(v[u][0].y), gelu(v[u][0].z),
-                                                                gelu(v[u][0].w)));
-                    store_wc4<KIND>(p.gelu_out, og + 4, make_float4(gelu(v[u][1].x), gelu(v[u][1].y),
-                                                                    gelu(v[u][1].z), gelu(v[u][1].w)));
+                    float w8[8] = {v[u][0].x, v[u][0].y, v[u][0].z, v[u][0].w,
+                                   v[u][1].x, v[u][1].y, v[u][1].z, v[u][1].w};
+                    float g8[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) gelu_both(w8[i], g8[i], w8[i]);  // w8: gelu'(x) from here on
+                    store_wc4<KIND>(p.gelu_out, og, make_float4(g8[0], g8[1], g8[2], g8[3]));
+                    store_wc4<KIND>(p.gelu_out, og + 4, make_float4(g8[4], g8[5], g8[6], g8[7]));
+                    if (p.out_gelu_grad) {
+                        v[u][0] = make_float4(w8[0], w8[1], w8[2], w8[3]);
+                        v[u][1] = make_float4(w8[4], w8[5], w8[6], w8[7]);
+                    }
                 }
                 if (p.out_f32) {
                     st_f4(static_cast<float *>(p.out), o[u], v[u][0]);

@@ -47,7 +47,7 @@ struct VUnit {
 struct VRec {
     DevBuf h, hmid;                   // fp32 residual stream: block input, after attention
     DevBuf m1, r1, m2, r2;            // LayerNorm row statistics
-    CBuf u1, u2, attn, g1, qkvb, z1;  // LN outputs, attention output, GELU output, qkv, FC1 pre-activation
+    CBuf u1, u2, attn, g1, qkvb, z1;  // LN outputs, attention output, GELU output, qkv, gelu'(FC1 pre-activation)
     DevBuf P;                         // unfused attention: softmax probabilities bf16 [B*H][T][ldp]
     DevBuf lse;                       // fused attention: row log-sum-exp fp32 [B*H][T]
     size_t bytes() const {
@@ -865,9 +865,10 @@ struct VitTrainer {
         layernorm(y.hmid.as<float>(), R, 1, b.ln2, p, y.u2.view(), y.m2.as<float>(), y.r2.as<float>(), s);
         {
             typename EpiConvOut2<0>::Params ep{};
-            ep.out = y.z1.hi.p;
+            ep.out = y.z1.hi.p;  // gelu'(z) (the backward's factor), not z
             ep.ld = y.z1.ld;
             ep.gelu_out = y.g1.view();
+            ep.out_gelu_grad = 1;
             const CBuf &w = Wt(b.fc1, p);
             reading({b.fc1}, A_FWD, p, s, [&] {
                 gemm<false, true, EpiConvOut2<0>>("fc1_gelu", opnd(y.u2.hi.p, false, R, D + 1, y.u2.ld),
@@ -972,7 +973,7 @@ struct VitTrainer {
             typename EpiConvOut2<0>::Params ep{};
             ep.out = gr.dz1.hi.p;
             ep.ld = gr.dz1.ld;
-            ep.gelu_z = y.z1.hi.p;
+            ep.mul = y.z1.hi.p;  // stored gelu'(z)
             const CBuf &w = Wt(b.fc2, p);
             reading({b.fc2}, A_BWD, p, cs, [&] {
                 gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(dhc_in.hi.p, false, R, D, dhc_in.ld),
