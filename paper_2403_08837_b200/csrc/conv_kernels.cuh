@@ -555,8 +555,13 @@ struct EpiConvAdd : EpiConvOut2<KIND> {
     static constexpr bool kTmaStore = false;
     static constexpr bool kNoSplit = true;
     static bool eligible(const Params &p, int N, int BN) {
-        return KIND == 0 && p.add && !p.stats && !p.out_f32 && !p.gelu_z && !p.gelu_out.hi && (p.ld % 8) == 0 &&
-               N % BN == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
+        return KIND == 0 && (p.add != nullptr) != (p.mul != nullptr) && !p.stats && !p.out_f32 && !p.gelu_z &&
+               !p.gelu_out.hi && !(p.mul && (p.add_mask.hi || p.out_mask.hi)) && (p.ld % 8) == 0 && N % BN == 0 &&
+               (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
+    }
+    // combine mode of the row operands: 0 add, 1 add masked residual, 2 add then mask, 3 multiply (p.mul)
+    __host__ __device__ static int mode(const Params &p) {
+        return p.mul ? 3 : p.add_mask.hi ? 1 : p.out_mask.hi ? 2 : 0;
     }
     // Direct epilogue (bf16 residual-gradient add: the ResNet block-input data gradient, out may
     // alias add): the drained accumulator row (lane = row, 32 columns) is combined with its own
@@ -575,7 +580,7 @@ struct EpiConvAdd : EpiConvOut2<KIND> {
         static_assert(NC == 32 || NC == 64, "direct epilogue loads 32 or 64 columns");
         if (m < 0) return;
         const size_t o = size_t(off) + size_t(m) * p.ld + col;
-        const uint4 *pa = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.add) + o);
+        const uint4 *pa = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.add ? p.add : p.mul) + o);
 #pragma unroll
         for (int i = 0; i < NC / 8; ++i) d.a[i] = pa[i];
         if (p.add_mask.hi || p.out_mask.hi) {
@@ -590,6 +595,11 @@ struct EpiConvAdd : EpiConvOut2<KIND> {
     __device__ static F8 combine(const DirectPre &d, int u, int mask, const float *v) {
         F8 a, x;
         bf16x8_to_f8(d.a[u], a);
+        if (mask == 3) {  // the row operand is a factor (a stored gelu'(z))
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x.v[k] = v[k] * a.v[k];
+            return x;
+        }
         if (mask) {
             F8 mk;
             bf16x8_to_f8(d.m[u], mk);
@@ -614,7 +624,7 @@ struct EpiConvAdd : EpiConvOut2<KIND> {
         uint4 *po = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + o);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            po[i] = f8_to_bf16x8(combine(d, 2 * q + i, p.add_mask.hi ? 1 : p.out_mask.hi ? 2 : 0, v + 8 * i));
+            po[i] = f8_to_bf16x8(combine(d, 2 * q + i, mode(p), v + 8 * i));
         }
     }
 };

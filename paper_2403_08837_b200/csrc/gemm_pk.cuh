@@ -492,9 +492,9 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 for (int h = 0; h < BN / C::EPI_COLS; ++h) {
                     const int seq = j * (BN / 64) + 2 * h + half, slot = seq % NES;
                     uint8_t *sl = ebuf + slot * 32768;
-                    const int mask = args.tma_add == 2 ? (ep.add_mask.hi ? 1 : 2) : 0;
+                    const int mask = ep.mul ? 3 : args.tma_add == 2 ? (ep.add_mask.hi ? 1 : 2) : 0;
                     ptx::mbar_wait(&efull[slot], (seq / NES) & 1);
-                    Epi::smem_load(sl, row, mask != 0, dp);
+                    Epi::smem_load(sl, row, mask == 1 || mask == 2, dp);
                     const int col = tn * BN + h * C::EPI_COLS + half * HC;
                     if (args.tma_out) {  // output through the slot: bf16 over the residual, one TMA store
 #pragma unroll
@@ -827,7 +827,7 @@ struct PkLaunch {
                         "TMA-staged epilogue operands: unsplit plain / stride-1 conv tiles of 128 or 256 columns");
             const uint64_t rs = uint64_t(ep.ld) * 2;
             CDP_REQUIRE(!(ep.add_mask.hi && ep.out_mask.hi), "one mask per residual-add epilogue");
-            const void *src[2] = {ep.add, ep.add_mask.hi ? ep.add_mask.hi : ep.out_mask.hi};
+            const void *src[2] = {ep.add ? ep.add : ep.mul, ep.add_mask.hi ? ep.add_mask.hi : ep.out_mask.hi};
             const int n = src[1] ? 2 : 1;
             for (int o = 0; o < n; ++o) {
                 if (MODE == GM_PLAIN) {

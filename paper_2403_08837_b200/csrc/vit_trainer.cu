@@ -417,6 +417,7 @@ struct VitTrainer {
         const int grid = PL::prepare(a, sms(), paired);
         GemmMaps maps = gp.maps;
         PL::setup_tma_out(maps, a, ep);
+        PL::setup_tma_add(maps, a, ep);
         L_(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
         if (a.splits > 1) {
             constexpr bool kStats = std::is_same<Epi, EpiConvOut2<0>>::value;
@@ -975,9 +976,15 @@ struct VitTrainer {
             ep.ld = gr.dz1.ld;
             ep.mul = y.z1.hi.p;  // stored gelu'(z)
             const CBuf &w = Wt(b.fc2, p);
+            // the factor rows TMA-staged into shared memory by warp 3, the product stored by TMA (EpiConvAddT)
+            static const bool staged = std::getenv("CDP_NO_TMA_ADD") == nullptr;
             reading({b.fc2}, A_BWD, p, cs, [&] {
-                gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(dhc_in.hi.p, false, R, D, dhc_in.ld),
-                                                   opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
+                if (staged && EpiConvAddT<0>::eligible(ep, F, tile_n(F)) && tile_n(F) >= 128)
+                    gemm<false, false, EpiConvAddT<0>>("fc2_dgrad_gelu", opnd(dhc_in.hi.p, false, R, D, dhc_in.ld),
+                                                       opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
+                else
+                    gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(dhc_in.hi.p, false, R, D, dhc_in.ld),
+                                                       opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
             });
         }
         cudaEvent_t dz1_ready = ev(cs);
