@@ -800,8 +800,6 @@ struct ResNetTrainer {
         ep.out = c.y.p;
         ep.ld = c.cout;
         ep.stats = stats_fwd.as<float>();
-        static const bool no_stats_probe = std::getenv("CDP_PROBE_NO_FWD_STATS") != nullptr;  // timing probe only
-        if (no_stats_probe) ep.stats = nullptr;
         ep.tiles = c.tiles_fwd;
         const CTensor w = wcv[vslot][c.tw];
         rec(c.tw, A_FWD, 0, vslot, s);
