@@ -355,7 +355,7 @@ def make_trainer(args, model, ws, rank, rule, allreduce, zero):
             raise SystemExit("vit_b16: --rule dp-allreduce / --zero are built for the ResNets")
         B = VIT_MB
         x, y = synthetic_images(2 * B * ws, seed=0, hw=224, classes=1000)
-        tr = DeviceVit(VIT_B16, B, ws, rank, rule, RN_MOMENTUM, inputs=x, labels=y)
+        tr = DeviceVit(VIT_B16, B, ws, rank, rule, RN_MOMENTUM, inputs=x, labels=y, dtype=args.dtype)
         tr.set_params(vit_init(VIT_B16, seed=0), -1)
         return tr, B, 224, 1000, x, y
     cfg, hw, classes = resnet_cfg(model)
@@ -480,14 +480,22 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
             x_pins[k].numpy()[:] = x[perms[k]]
             y_pins[k].numpy()[:] = y[perms[k]]
         ke = min(steps, 20) + 2
-        tr.step_host_batch_async(x_pins[0].data_ptr(), y_pins[0].data_ptr(), RN_LR, 0)  # warm the copy path
+        pipelined = hasattr(tr, "step_host_batch_async")  # ResNets; the ViT copies on its step stream
+
+        def host_step(k):
+            if pipelined:
+                tr.step_host_batch_async(x_pins[k % ring].data_ptr(), y_pins[k % ring].data_ptr(), RN_LR, k % 2)
+            else:
+                tr.step_host_batch_ptr(x_pins[k % ring].data_ptr(), y_pins[k % ring].data_ptr(), RN_LR)
+
+        host_step(0)  # warm the copy path
         tr.sync()
         if ws > 1:
             torch.distributed.barrier()
         tr.mark(0)
         for k in range(ke):
             tr.flush_l2()
-            tr.step_host_batch_async(x_pins[k % ring].data_ptr(), y_pins[k % ring].data_ptr(), RN_LR, k % 2)
+            host_step(k)
             reduce_update()
         tr.mark(1)
         tr.sync()
@@ -499,11 +507,16 @@ def run_resnet(args, ws, rank, local, model, steps, warmup, e2e=True):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e = float(t.item())
         out["e2e"] = {"value": round(ws * B / (e / 1e3), 1), "unit": UNIT,
-                      "h2d_bytes_per_step": B * hw * hw * 3 * 4 + B * 4 + 16 + B * 4, "d2h_bytes_per_step": 8,
+                      "h2d_bytes_per_step": B * hw * hw * 3 * 4 + B * 4 + 16 + B * 4,
+                      "d2h_bytes_per_step": 8 if pipelined else 0,
                       "ms_per_step": round(e, 4),
-                      "how": "public API step_host_batch_async: every step copies its pinned host batch H2D (copy "
-                             "stream, two input slots: overlaps the previous step) and its loss D2H; device time "
-                             "from before the first copy to after the last step / steps, L2 flushed every step"}
+                      "how": ("public API step_host_batch_async: every step copies its pinned host batch H2D (copy "
+                              "stream, two input slots: overlaps the previous step) and its loss D2H; device time "
+                              "from before the first copy to after the last step / steps, L2 flushed every step"
+                              if pipelined else
+                              "public API step_host_batch: every step copies its pinned host batch H2D on the step "
+                              "stream before the step (no overlap; losses stay in the device history); device time "
+                              "from before the first copy to after the last step / steps, L2 flushed every step")}
     # ---- per-kernel breakdown: one serialised instrumented (real) step
     if frames:
         out["kernel_breakdown"] = None
@@ -822,7 +835,8 @@ def resnet_workload(model, ws, rule_name, dtype):
     elif model == "vit_b16":
         what = "ViT-B/16 (torchvision layout), 224x224x3, 1000 classes, fp32 residual stream"
         mb = VIT_MB
-        dtype = "bf16"
+        if dtype == "fp32":
+            dtype = "fp32 (3xTF32, unfused attention: the parity mode)"
     else:
         what = "ResNet-50 (torchvision v1.5 layout), 224x224x3, 1000 classes"
     return (f"{what}; {rule_name}; one micro-batch of {mb} per GPU; {ws} stage(s) = {ws} GPU(s); {dtype} "
@@ -848,7 +862,9 @@ def main_resnet(args, ws, rank, local):
                 baselines[mode] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank != 0:
         return None
-    peak_note = "configs[1]" if model == "resnet18" else "configs[2] (north-star target; N GPUs = N stages)"
+    peak_note = ("configs[1]" if model == "resnet18" else
+                 "configs[3]'s model, one micro-batch per GPU (N GPUs = N stages)" if model == "vit_b16" else
+                 "configs[2] (north-star target; N GPUs = N stages)")
     out = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",

@@ -256,11 +256,14 @@ int cdp_resnet_trace(cdp_resnet *tr, uint32_t *records, int max_records, int *co
  * on the class token.  Hop units in order: patch [[W^T]; b] ([patch*patch*3 + 1][dim]), cls [dim],
  * pos [tokens][dim], per block ln1 [g | b], qkv [[W^T]; b] ([dim+1][3 dim]), proj, ln2, fc1
  * ([dim+1][mlp]), fc2 ([mlp+1][dim]), final ln, head ([dim+1][classes]); unit_stage[i] groups them
- * into world stages.  Dataset: x fp32 NHWC [n][image][image][3], labels int32. */
+ * into world stages.  Dataset: x fp32 NHWC [n][image][image][3], labels int32.  dtype
+ * CDP_DTYPE_BF16: bf16 operands, fused attention (the bench path); CDP_DTYPE_FP32: operands as
+ * tf32 hi + lo pairs (3xTF32 tcgen05 products), attention as batched GEMMs with an fp32 softmax. */
 typedef struct cdp_vit cdp_vit;
 int cdp_vit_create_rank(int image, int patch, int dim, int depth, int heads, int mlp, int classes, int micro_batch,
                         int world, int rank, const int32_t *unit_stage, const uint8_t *stage_fresh, float momentum,
-                        float weight_decay, int n_samples, const float *x, const int32_t *labels, cdp_vit **out);
+                        float weight_decay, int n_samples, const float *x, const int32_t *labels, int dtype,
+                        cdp_vit **out);
 /* Single-GPU cyclic CDP (BASELINE configs[3]; ref schedule.py:236-257, all workers on gpu 0):
  * n_workers micro-batches = stages on this GPU, stepped through the reference's SINGLE_GPU_CDP
  * (or SINGLE_GPU_DP) timeline.  ops[n_ops][3] = (kind 0 F / 1 B, worker 1..n, stage 1..n) in
@@ -277,7 +280,7 @@ int cdp_vit_create_cyclic(int image, int patch, int dim, int depth, int heads, i
                           int n_workers, const int32_t *unit_stage, const uint8_t *fresh, int n_ops,
                           const int32_t *ops, const int32_t *rec_slot, const int32_t *pools, float momentum,
                           float weight_decay, int probe, int n_samples, const float *x, const int32_t *labels,
-                          cdp_vit **out);
+                          int dtype, cdp_vit **out);
 int cdp_vit_info(cdp_vit *tr, int64_t *n_params, int *n_units);
 /* Trace mode (set before cdp_vit_connect): records as cdp_resnet_trace, unit = 1-based hop unit. */
 int cdp_vit_set_trace(cdp_vit *tr, int on);

@@ -100,10 +100,11 @@ SIGNATURES = {
     "cdp_resnet_buffer": (c_int, [c_void_p, ctypes.c_char_p, c_int, ctypes.POINTER(c_void_p),
                                   ctypes.POINTER(c_size_t), c_int_p]),
     "cdp_vit_create_rank": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int_p,
-                                    c_u8_p, c_float, c_float, c_int, c_float_p, c_int_p, ctypes.POINTER(c_void_p)]),
+                                    c_u8_p, c_float, c_float, c_int, c_float_p, c_int_p, c_int,
+                                    ctypes.POINTER(c_void_p)]),
     "cdp_vit_create_cyclic": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int_p, c_u8_p,
                                       c_int, c_int_p, c_int_p, c_int_p, c_float, c_float, c_int, c_int, c_float_p,
-                                      c_int_p, ctypes.POINTER(c_void_p)]),
+                                      c_int_p, c_int, ctypes.POINTER(c_void_p)]),
     "cdp_vit_info": (c_int, [c_void_p, c_int64_p, c_int_p]),
     "cdp_vit_set_trace": (c_int, [c_void_p, c_int]),
     "cdp_vit_trace": (c_int, [c_void_p, ctypes.POINTER(ctypes.c_uint32), c_int, c_int_p]),

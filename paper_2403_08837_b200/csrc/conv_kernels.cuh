@@ -258,6 +258,7 @@ struct EpiConvOut2 {
         const void *gelu_z;  // out *= gelu'(z), z Y-format with the output's layout, or null
         const void *mul;     // out *= mul (Y format, the output's layout): a stored gelu'(z), or null
         int out_gelu_grad;   // with gelu_out: the stored output is gelu'(x) instead of x (the backward's factor)
+        void *out_lo;        // KIND 1: store `out` in compute format (hi = out, lo = out_lo; a GEMM operand), or null
     };
     static constexpr int kStages = 0;
     static Params for_split(const Params &p) { return p; }
@@ -339,7 +340,9 @@ struct EpiConvOut2 {
                     Fmt<KIND>::store(p.gelu_out.hi, p.gelu_out.lo, size_t(m) * p.gelu_out.ld + col0 + c, gl);
                     if (p.out_gelu_grad) x = gd;
                 }
-                if (p.out_f32 || KIND == 1)
+                if (KIND == 1 && p.out_lo && !p.out_f32)
+                    Fmt<1>::store(p.out, p.out_lo, o, x);
+                else if (p.out_f32 || KIND == 1)
                     static_cast<float *>(p.out)[o] = x;
                 else
                     Fmt<0>::store(p.out, nullptr, o, x);
@@ -431,6 +434,9 @@ struct EpiConvOut2 {
                     w.z = *reinterpret_cast<uint32_t *>(&b2);
                     w.w = *reinterpret_cast<uint32_t *>(&b3);
                     *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out) + o[u]) = w;
+                } else if (p.out_lo) {  // KIND 1 compute format
+                    store_wc4<KIND>(CTensor{p.out, p.out_lo, 0}, o[u], v[u][0]);
+                    store_wc4<KIND>(CTensor{p.out, p.out_lo, 0}, o[u] + 4, v[u][1]);
                 } else {
                     st_y4<KIND>(p.out, o[u], v[u][0]);
                     st_y4<KIND>(p.out, o[u] + 4, v[u][1]);

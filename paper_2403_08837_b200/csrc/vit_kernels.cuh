@@ -331,6 +331,42 @@ static __global__ void softmax_bwd_kernel(const float *__restrict__ dP, const __
     }
 }
 
+// Compute-format row softmax / backward (the fp32 mode: P and dS as hi + lo operands of the 3xTF32
+// attention GEMMs); one warp per row, accurate expf.
+template <int KIND>
+static __global__ void softmax_fwd_c_kernel(const float *__restrict__ S, int rows, int n, int lds, float scale,
+                                            CTensor P) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float *sr = S + size_t(w) * lds;
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, sr[j] * scale);
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int j = lane; j < n; j += 32) sum += expf(sr[j] * scale - mx);
+    const float inv = 1.f / warp_sum(sum);
+    for (int j = lane; j < n; j += 32)
+        Fmt<KIND>::store(P.hi, P.lo, size_t(w) * P.ld + j, expf(sr[j] * scale - mx) * inv);
+}
+
+template <int KIND>
+static __global__ void softmax_bwd_c_kernel(const float *__restrict__ dP, CTensor P, int rows, int n, int lds,
+                                            float scale, CTensor dS) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    float dot = 0.f;
+    for (int j = lane; j < n; j += 32) dot += dP[size_t(w) * lds + j] * Fmt<KIND>::load(P.hi, P.lo, size_t(w) * P.ld + j);
+    dot = warp_sum(dot);
+    for (int j = lane; j < n; j += 32) {
+        const float p = Fmt<KIND>::load(P.hi, P.lo, size_t(w) * P.ld + j);
+        Fmt<KIND>::store(dS.hi, dS.lo, size_t(w) * dS.ld + j, scale * p * (dP[size_t(w) * lds + j] - dot));
+    }
+}
+
 // Vectorised row softmax / backward for rows of at most 128*NV columns: lane owns columns
 // 4*lane + 128*k (16-byte fp32 / 8-byte bf16 accesses, one read of each row); columns >= n
 // (the padded tail of a 197-token row) are masked.

@@ -34,6 +34,8 @@ namespace {
 
 enum VitUnitKind { V_LIN = 0, V_LN = 1, V_VEC = 2 };
 
+inline size_t cbytes(const CBuf &b) { return b.hi.bytes + b.lo.bytes; }  // compute format: hi (+ lo, fp32 mode)
+
 struct VUnit {
     int kind;
     int64_t base, n;
@@ -48,21 +50,21 @@ struct VRec {
     DevBuf h, hmid;                   // fp32 residual stream: block input, after attention
     DevBuf m1, r1, m2, r2;            // LayerNorm row statistics
     CBuf u1, u2, attn, g1, qkvb, z1;  // LN outputs, attention output, GELU output, qkv, gelu'(FC1 pre-activation)
-    DevBuf P;                         // unfused attention: softmax probabilities bf16 [B*H][T][ldp]
+    CBuf P;                           // unfused attention: softmax probabilities [B*H][T][ldp] (compute format)
     DevBuf lse;                       // fused attention: row log-sum-exp fp32 [B*H][T]
     size_t bytes() const {
-        return h.bytes + hmid.bytes + m1.bytes + r1.bytes + m2.bytes + r2.bytes + u1.hi.bytes + u2.hi.bytes +
-               attn.hi.bytes + g1.hi.bytes + qkvb.hi.bytes + z1.hi.bytes + P.bytes + lse.bytes;
+        return h.bytes + hmid.bytes + m1.bytes + r1.bytes + m2.bytes + r2.bytes + cbytes(u1) + cbytes(u2) +
+               cbytes(attn) + cbytes(g1) + cbytes(qkvb) + z1.hi.bytes + cbytes(P) + lse.bytes;
     }
 };
 struct ERec {  // embedding record: the patch matrix [x, 1] (the patch weight gradient's operand)
     CBuf patches;
-    size_t bytes() const { return patches.hi.bytes; }
+    size_t bytes() const { return cbytes(patches); }
 };
 struct FRec {  // final record: last block output, final LN statistics / output, logits, dlogits
     DevBuf hL, mf, rf, z;
     CBuf uf, dz;
-    size_t bytes() const { return hL.bytes + mf.bytes + rf.bytes + z.bytes + uf.hi.bytes + dz.hi.bytes; }
+    size_t bytes() const { return hL.bytes + mf.bytes + rf.bytes + z.bytes + cbytes(uf) + cbytes(dz); }
 };
 // Backward operands of one block read by the hop stream (weight gradients), plus its LN parameter gradients.
 struct VGrad {
@@ -81,10 +83,15 @@ struct VOp {
     int kind, worker, stage;  // 0 = F, 1 = B; 1-based worker / stage
 };
 
-struct BView {  // a 4-D TMA view {inner, rows, heads, samples} of a token-major bf16 buffer
+struct BView {  // a 4-D TMA view {inner, rows, heads, samples} of a token-major compute-format buffer
     const void *ptr;
     int inner, rows;
     int64_t ld, hs, bs;  // elements
+    const void *lo;      // fp32 mode: the lo half (same layout), else null
+};
+struct COpnd {  // a GEMM operand in compute format: hi (bf16, or tf32-exact fp32) and the fp32 mode's lo half
+    Operand hi;
+    const void *lo;
 };
 
 __global__ void live_probe_kernel(int64_t *ctr, int64_t delta) {  // [0] live record bytes, [1] high-water mark
@@ -100,7 +107,11 @@ __global__ void loss_mean_kernel(const double *loss_w, int W, double *loss_out) 
 
 }  // namespace
 
+// KIND 0: bf16 operands (the bench path); KIND 1: fp32 mode (operands as hi + lo tf32 pairs, 3xTF32 tcgen05
+// products, unfused attention with fp32 softmax) for fp32-tolerance parity with the restatement.
+template <int KIND>
 struct VitTrainer {
+    static constexpr int ES = KIND == 0 ? 2 : 4;  // compute-format bytes per element
     // ---------------------------------------------------------------- config
     int B = 0, img = 224, P = 16, G = 14, NP = 196, T = 197, D = 768, H = 12, HD = 64, F = 3072, L = 12;
     int classes = 1000, loss_kind = 1;
@@ -210,7 +221,8 @@ struct VitTrainer {
         return sms_;
     }
     static int blocks_for(int64_t n, int per = 256) { return int(std::min<int64_t>(8 * 148, (n + per - 1) / per)); }
-    static int tile_n(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }  // a supported BN covering n
+    // a supported BN covering n (fp32 mode: at most 128, the fp32 operand stages are twice as large)
+    static int tile_n(int n) { return n <= 64 ? 64 : (n <= 128 || KIND == 1) ? 128 : 256; }
 
     // ---------------------------------------------------------------- model
     int add_unit(int kind, int64_t n, int rows, int cols) {
@@ -237,7 +249,7 @@ struct VitTrainer {
         ldp = round_up(T, 16);
         // fused attention (attn_kernels.cuh): one key tile, T <= 256 (CDP_VIT_UNFUSED=1: batched GEMMs +
         // row-softmax kernels)
-        fused_attn = T <= 256 && std::getenv("CDP_VIT_UNFUSED") == nullptr;
+        fused_attn = KIND == 0 && T <= 256 && std::getenv("CDP_VIT_UNFUSED") == nullptr;  // bf16 kernels
         const int K0 = P * P * 3;
         u_patch = add_unit(V_LIN, int64_t(K0 + 1) * D, K0 + 1, D);
         u_cls = add_unit(V_VEC, D, 0, 0);
@@ -259,14 +271,20 @@ struct VitTrainer {
 
     void build() {
         // ---- records (pool sizes from the plan), per-block backward operands, per-worker carries
-        auto ones = [&](CBuf &b, int rows, int col) {  // constant 1 in column `col` (bias folding)
-            std::vector<__nv_bfloat16> one(size_t(rows), __float2bfloat16(1.f));
-            CDP_CUDA(cudaMemcpy2D(static_cast<__nv_bfloat16 *>(b.hi.p) + col, size_t(b.ld) * 2, one.data(), 2, 2,
-                                  size_t(rows), cudaMemcpyHostToDevice));
+        auto ones = [&](CBuf &b, int rows, int col) {  // constant 1 in column `col` (bias folding; lo stays 0)
+            if (KIND == 0) {
+                std::vector<__nv_bfloat16> one(size_t(rows), __float2bfloat16(1.f));
+                CDP_CUDA(cudaMemcpy2D(static_cast<__nv_bfloat16 *>(b.hi.p) + col, size_t(b.ld) * 2, one.data(), 2, 2,
+                                      size_t(rows), cudaMemcpyHostToDevice));
+            } else {
+                std::vector<float> one(size_t(rows), 1.f);
+                CDP_CUDA(cudaMemcpy2D(static_cast<float *>(b.hi.p) + col, size_t(b.ld) * 4, one.data(), 4, 4,
+                                      size_t(rows), cudaMemcpyHostToDevice));
+            }
         };
         const int K0 = P * P * 3;
         erec.resize(pool[0]);
-        for (auto &e : erec) e.patches = make_cbuf(0, B * NP, K0 + 1);
+        for (auto &e : erec) e.patches = make_cbuf(KIND, B * NP, K0 + 1);
         brec.resize(pool[1]);
         for (auto &y : brec) {
             y.h = DevBuf(size_t(R) * D * 4);
@@ -275,33 +293,33 @@ struct VitTrainer {
             y.r1 = DevBuf(size_t(R) * 4);
             y.m2 = DevBuf(size_t(R) * 4);
             y.r2 = DevBuf(size_t(R) * 4);
-            y.u1 = make_cbuf(0, R, D + 1);
-            y.u2 = make_cbuf(0, R, D + 1);
-            y.attn = make_cbuf(0, R, D + 1);
+            y.u1 = make_cbuf(KIND, R, D + 1);
+            y.u2 = make_cbuf(KIND, R, D + 1);
+            y.attn = make_cbuf(KIND, R, D + 1);
             ones(y.attn, R, D);
-            y.g1 = make_cbuf(0, R, F + 1);
+            y.g1 = make_cbuf(KIND, R, F + 1);
             ones(y.g1, R, F);
-            y.qkvb = make_cbuf(0, R, 3 * D);
-            y.z1 = make_cbuf(0, R, F);
+            y.qkvb = make_cbuf(KIND, R, 3 * D);
+            y.z1 = make_cbuf(KIND, R, F);
             if (fused_attn)
                 y.lse = DevBuf(size_t(B) * H * T * 4);
             else
-                y.P = DevBuf(size_t(B) * H * T * ldp * 2);
+                y.P = make_cbuf(KIND, B * H * T, T);  // ld = ldp
         }
         frec.resize(pool[2]);
         for (auto &f : frec) {
             f.hL = DevBuf(size_t(R) * D * 4);
             f.mf = DevBuf(size_t(B) * 4);
             f.rf = DevBuf(size_t(B) * 4);
-            f.uf = make_cbuf(0, B, D + 1);
+            f.uf = make_cbuf(KIND, B, D + 1);
             f.z = DevBuf(size_t(B) * classes * 4);
-            f.dz = make_cbuf(0, B, classes);
+            f.dz = make_cbuf(KIND, B, classes);
         }
         grads.resize(W > 1 ? 1 : L);
         for (auto &g : grads) {
-            g.dz1 = make_cbuf(0, R, F);
-            g.dhmc = make_cbuf(0, R, D);
-            g.dqkv = make_cbuf(0, R, 3 * D);
+            g.dz1 = make_cbuf(KIND, R, F);
+            g.dhmc = make_cbuf(KIND, R, D);
+            g.dqkv = make_cbuf(KIND, R, 3 * D);
             for (DevBuf *v : {&g.dg1, &g.db1, &g.dg2, &g.db2}) *v = DevBuf(size_t(D) * 4);
         }
         // W == 1: one dhc per block output (the hop stream reads it after the compute stream moved on);
@@ -309,10 +327,10 @@ struct VitTrainer {
         carry.resize(W);
         for (auto &c : carry) c.dh = DevBuf(size_t(R) * D * 4);
         dhc_layer.resize(W == 1 ? L : 0);
-        for (auto &d : dhc_layer) d = make_cbuf(0, R, D);
+        for (auto &d : dhc_layer) d = make_cbuf(KIND, R, D);
         if (W > 1)
             for (auto &c : carry)
-                for (auto &d : c.dhc) d = make_cbuf(0, R, D);
+                for (auto &d : c.dhc) d = make_cbuf(KIND, R, D);
         E = DevBuf(size_t(B) * NP * D * 4);
         loss_w = DevBuf(size_t(W) * 8);
         loss_dev = DevBuf(8);
@@ -320,15 +338,15 @@ struct VitTrainer {
         if (!fused_attn) {
             S = DevBuf(size_t(B) * H * T * lds * 4);
             dP = DevBuf(size_t(B) * H * T * lds * 4);
-            dS = make_cbuf(0, B * H * T, T);  // ld = ldp
+            dS = make_cbuf(KIND, B * H * T, T);  // ld = ldp
         }
         du = DevBuf(size_t(R) * D * 4);
         duf = DevBuf(size_t(B) * D * 4);
         dhm = DevBuf(size_t(R) * D * 4);
-        dattn = make_cbuf(0, R, D);
+        dattn = make_cbuf(KIND, R, D);
         gpos = DevBuf(size_t(T) * D * 4);
         gcls = DevBuf(size_t(D) * 4);
-        dE = make_cbuf(0, B * NP, D);
+        dE = make_cbuf(KIND, B * NP, D);
         lnpart = DevBuf(size_t(D) * ((R + kLnBwdRows - 1) / kLnBwdRows) * 16);
         dgf = DevBuf(size_t(D) * 4);
         dbf = DevBuf(size_t(D) * 4);
@@ -344,7 +362,7 @@ struct VitTrainer {
         if (momentum != 0.f) vel = partial + Pp;
         cta_counters = DevBuf(2 * kMaxStages * 4);
         for (int v = 0; v < 2; ++v)
-            for (auto &u : units) wc[v].push_back(u.kind == V_LIN ? make_cbuf(0, u.rows, u.cols) : CBuf{});
+            for (auto &u : units) wc[v].push_back(u.kind == V_LIN ? make_cbuf(KIND, u.rows, u.cols) : CBuf{});
         CDP_CUDA(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
         CDP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         CDP_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
@@ -399,11 +417,18 @@ struct VitTrainer {
         int splits = 1;
         if (MODE != GM_BATCH && tiles < sms()) splits = std::max(1, std::min(sms() / tiles, a.total_iters / split_min_kb()));
         a.iters_per_split = (a.total_iters + splits - 1) / splits;
+        if (KIND == 1 && MODE != GM_BATCH) {
+            // fp32 mode (as resnet_trainer.cu run_pk): every unit covers at most 256 of K inside one 3xTF32
+            // segment, the partials summed in fp32 by pk_reduce_kernel in split order
+            int ips = std::min(a.iters_per_split, std::min(a.kb_per_seg, 8));
+            while (a.kb_per_seg % ips) --ips;
+            a.iters_per_split = ips;
+        }
         a.splits = (a.total_iters + a.iters_per_split - 1) / a.iters_per_split;
-        using PL = PkLaunch<0, BNc, AMN, BMN, Epi, MODE>;
+        using PL = PkLaunch<KIND, BNc, AMN, BMN, Epi, MODE>;
         a.units = tiles * a.splits;
         typename Epi::Params ep = a.splits > 1 ? Epi::for_split(ep_in) : ep_in;
-        if constexpr (std::is_same<Epi, EpiConvOut2<0>>::value)
+        if constexpr (std::is_same<Epi, EpiConvOut2<KIND>>::value)
             if (a.splits > 1) ep.tiles = a.tiles_m * 4;
         const size_t need = a.splits > 1 ? size_t(tiles) * a.splits * 128 * BNc : 0;
         size_t &cap = hop ? ws_h_floats : ws_c_floats;
@@ -420,7 +445,7 @@ struct VitTrainer {
         PL::setup_tma_add(maps, a, ep);
         L_(name, flops, 0.0, s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
         if (a.splits > 1) {
-            constexpr bool kStats = std::is_same<Epi, EpiConvOut2<0>>::value;
+            constexpr bool kStats = std::is_same<Epi, EpiConvOut2<KIND>>::value;
             constexpr int RC = kStats ? 32 : 16;  // rows per block: 256 threads x 2 float4 (stats) / 1 float4 (hop)
             constexpr int CC = 64;
             L_("splitk_reduce", 0, double(need) * 4, s, [&] {
@@ -433,15 +458,25 @@ struct VitTrainer {
     static Operand opnd(const void *ptr, bool mn, int64_t mn_ext, int64_t k_ext, int64_t ld) {
         return Operand{ptr, mn, uint64_t(mn_ext), uint64_t(k_ext), uint64_t(ld)};
     }
+    static COpnd copnd(const CBuf &b, bool mn, int64_t mn_ext, int64_t k_ext) {
+        return COpnd{opnd(b.hi.p, mn, mn_ext, k_ext, b.ld), b.lo.p};
+    }
+    static COpnd copnd(const CTensor &t, bool mn, int64_t mn_ext, int64_t k_ext) {
+        return COpnd{opnd(t.hi, mn, mn_ext, k_ext, t.ld), t.lo};
+    }
 
-    // D[M,N] = A . B with plain 2-D operands (bf16).
+    // D[M,N] = A . B with plain 2-D operands (bf16; fp32 mode: A.hi B.hi + A.hi B.lo + A.lo B.hi, 3xTF32).
     template <bool AMN, bool BMN, class Epi>
-    void gemm(const char *name, const Operand &A, const Operand &Bo, int64_t M, int64_t N, int64_t Kd,
+    void gemm(const char *name, const COpnd &A, const COpnd &Bo, int64_t M, int64_t N, int64_t Kd,
               const typename Epi::Params &ep, cudaStream_t s, bool hop) {
+        Operand a[3] = {A.hi, A.hi, A.hi}, b[3] = {Bo.hi, Bo.hi, Bo.hi};
+        const int nseg = KIND == 0 ? 1 : 3;
+        b[1].ptr = Bo.lo;
+        a[2].ptr = A.lo;
         bn_switch(tile_n(int(N)), [&](auto bnc) {
             constexpr int BNc = decltype(bnc)::value;
-            if constexpr (BNc >= 64) {
-                GemmPlan p = plan_gemm<0, BNc, AMN, BMN>(&A, &Bo, 1, int(M), int(N), int(Kd), 1, nullptr, nullptr);
+            if constexpr (BNc >= 64 && (KIND == 0 || BNc <= 128)) {
+                GemmPlan p = plan_gemm<KIND, BNc, AMN, BMN>(a, b, nseg, int(M), int(N), int(Kd), 1, nullptr, nullptr);
                 run_pk<BNc, AMN, BMN, Epi, GM_PLAIN>(name, 2.0 * M * N * Kd, p, ep, s, hop);
             } else {
                 throw CdpError("unsupported GEMM tile width");
@@ -513,35 +548,56 @@ struct VitTrainer {
         });
     }
 
+    // 4-D views of the token-major buffers: 64 columns from `col` of a [R][ld] buffer (per head: +64), and
+    // the [B*H*T][ldp] probability-shaped buffers
+    BView qview(const CBuf &b, int col) const {
+        auto at = [&](const DevBuf &h) -> const void * {
+            return h.p ? static_cast<const uint8_t *>(h.p) + size_t(col) * ES : nullptr;
+        };
+        return BView{at(b.hi), HD, T, b.ld, HD, int64_t(T) * b.ld, at(b.lo)};
+    }
+    BView pview(const CBuf &b) const {
+        return BView{b.hi.p, T, T, b.ld, int64_t(T) * b.ld, int64_t(H) * T * b.ld, b.lo.p};
+    }
+
     // Batched GEMM over (head, sample): operands are 4-D views {inner, rows, heads, samples}.
     template <bool AMN, bool BMN>
     void bgemm(const char *name, const BView &A, const BView &Bv, int M, int N, int K, void *out, int ld_out,
-               int64_t out_bs, int64_t out_hs, int out_f32, cudaStream_t s) {
+               int64_t out_bs, int64_t out_hs, int out_f32, cudaStream_t s, void *out_lo = nullptr) {
         bn_switch(tile_n(N), [&](auto bnc) {
             constexpr int BNc = decltype(bnc)::value;
-            if constexpr (BNc >= 64) {
-                using Cfg = PkCfg<0, BNc, AMN, BMN, 0>;
+            if constexpr (BNc >= 64 && (KIND == 0 || BNc <= 128)) {
+                using Cfg = PkCfg<KIND, BNc, AMN, BMN, 0>;
                 GemmPlan p{};
                 std::memset(&p.maps, 0, sizeof(p.maps));
-                auto mk = [&](const BView &v, bool mn, int box_rows) {
+                auto mk = [&](const BView &v, const void *ptr, bool mn, int box_rows) {
                     const uint64_t dims[4] = {uint64_t(v.inner), uint64_t(v.rows), uint64_t(H), uint64_t(B)};
-                    const uint64_t st[3] = {uint64_t(v.ld) * 2, uint64_t(v.hs) * 2, uint64_t(v.bs) * 2};
-                    const uint32_t box[4] = {64u, uint32_t(mn ? Cfg::BK : box_rows), 1u, 1u};
+                    const uint64_t st[3] = {uint64_t(v.ld) * ES, uint64_t(v.hs) * ES, uint64_t(v.bs) * ES};
+                    const uint32_t box[4] = {uint32_t(128 / ES), uint32_t(mn ? Cfg::BK : box_rows), 1u, 1u};
                     const uint32_t es[4] = {1u, 1u, 1u, 1u};
-                    return make_tmap_4d(v.ptr, ElemType::BF16, dims, st, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
+                    return make_tmap_4d(ptr, KIND == 0 ? ElemType::BF16 : ElemType::F32, dims, st, box, es,
+                                        (KIND == 1 && mn) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                                          : CU_TENSOR_MAP_SWIZZLE_128B);
                 };
-                p.maps.a[0] = mk(A, AMN, 128);
-                p.maps.b[0] = mk(Bv, BMN, BNc);
+                p.maps.a[0] = mk(A, A.ptr, AMN, 128);
+                p.maps.b[0] = mk(Bv, Bv.ptr, BMN, BNc);
+                if (KIND == 1) {  // 3xTF32: A.hi B.hi + A.hi B.lo + A.lo B.hi
+                    p.maps.a[1] = p.maps.a[0];
+                    p.maps.b[1] = mk(Bv, Bv.lo, BMN, BNc);
+                    p.maps.a[2] = mk(A, A.lo, AMN, 128);
+                    p.maps.b[2] = p.maps.b[0];
+                }
                 p.args.M = M;
                 p.args.N = N;
                 p.args.kb_per_seg = (K + Cfg::BK - 1) / Cfg::BK;
-                p.args.n_seg = 1;
+                p.args.n_seg = KIND == 0 ? 1 : 3;
                 p.grid = dim3((M + 127) / 128, (N + BNc - 1) / BNc, 1);
-                typename EpiConvOut2<0>::Params ep{};
+                typename EpiConvOut2<KIND>::Params ep{};
                 ep.out = out;
+                ep.out_lo = out_lo;
                 ep.ld = ld_out;
                 ep.out_f32 = out_f32;
-                run_pk<BNc, AMN, BMN, EpiConvOut2<0>, GM_BATCH>(name, 2.0 * M * N * K * H * B, p, ep, s, false, H, B,
+                run_pk<BNc, AMN, BMN, EpiConvOut2<KIND>, GM_BATCH>(name, 2.0 * M * N * K * H * B, p, ep, s, false, H, B,
                                                                  out_bs, out_hs);
             } else {
                 throw CdpError("unsupported batched GEMM tile width");
@@ -663,7 +719,7 @@ struct VitTrainer {
                 CDP_CUDA(cudaGetLastError());
             });
             L_("pull", 0, double(u.n) * 10, s, [&] {
-                launch_pdl(chain_pull_kernel<0>, dim3(blocks_for(u.n, 1024)), dim3(256), 0, s, src,
+                launch_pdl(chain_pull_kernel<KIND>, dim3(blocks_for(u.n, 1024)), dim3(256), 0, s, src,
                            theta[vslot] + u.base, u.n, std::max(u.cols, 1), w, pf, pr < 0 ? 1 : 0, ring, unit + 1,
                            u.fresh, (const int *)&ctrl_dev.as<Control>()->step,
                            cta_counters.as<unsigned>() + kMaxStages, trace ? 1 : 0);
@@ -676,7 +732,7 @@ struct VitTrainer {
             CDP_CUDA(cudaGetLastError());
         });
         L_("pull", 0, double(u.n) * 10, s, [&] {
-            launch_pdl(pull_tensor_kernel<0>, dim3(blocks_for(u.n, 1024)), dim3(256), 0, s,
+            launch_pdl(pull_tensor_kernel<KIND>, dim3(blocks_for(u.n, 1024)), dim3(256), 0, s,
                        (const float *)(upd_theta[vslot] + u.base), theta[vslot] + u.base, u.n, std::max(u.cols, 1),
                        w, upd_ring, ring, unit + 1, u.fresh, (const int *)&ctrl_dev.as<Control>()->step,
                        cta_counters.as<unsigned>() + kMaxStages, trace ? 1 : 0);
@@ -692,8 +748,8 @@ struct VitTrainer {
         HopParams hp = hop_params(unit, p);
         hop_wait(hp, hs);
         traced_update(unit, p, hp.mode >= 2, hs, [&] {
-            gemm<true, true, EpiHop2<0>>("lin_wgrad_hop", opnd(a_in.hi, true, u.rows, krows, a_in.ld),
-                                         opnd(dy.hi, true, u.cols, krows, dy.ld), u.rows, u.cols, krows, hp, hs, true);
+            gemm<true, true, EpiHop2<KIND>>("lin_wgrad_hop", copnd(a_in, true, u.rows, krows),
+                                         copnd(dy, true, u.cols, krows), u.rows, u.cols, krows, hp, hs, true);
         });
     }
     void ln_hop(int unit, int p, const float *dg, const float *db, cudaEvent_t ready) {
@@ -721,12 +777,12 @@ struct VitTrainer {
             });
         };
         switch (D % 128 == 0 ? D / 128 : 0) {  // row in registers as 16-byte columns
-            case 1: go(ln_fwd4_kernel<0, 1>); break;
-            case 2: go(ln_fwd4_kernel<0, 2>); break;
-            case 4: go(ln_fwd4_kernel<0, 4>); break;
-            case 6: go(ln_fwd4_kernel<0, 6>); break;
-            case 8: go(ln_fwd4_kernel<0, 8>); break;
-            default: go(ln_fwd_kernel<0>); break;
+            case 1: go(ln_fwd4_kernel<KIND, 1>); break;
+            case 2: go(ln_fwd4_kernel<KIND, 2>); break;
+            case 4: go(ln_fwd4_kernel<KIND, 4>); break;
+            case 6: go(ln_fwd4_kernel<KIND, 6>); break;
+            case 8: go(ln_fwd4_kernel<KIND, 8>); break;
+            default: go(ln_fwd_kernel<KIND>); break;
         }
     }
     // LayerNorm backward of `unit`: dh_out = dh_in + LN'(g); parameter gradients -> dgam / dbet.
@@ -752,14 +808,14 @@ struct VitTrainer {
             });
         };
         switch (D % 128 == 0 ? D / 128 : 0) {  // 16-byte columns
-            case 1: go(ln_bwd_fused4_kernel<0, 1>); break;
-            case 2: go(ln_bwd_fused4_kernel<0, 2>); break;
-            case 4: go(ln_bwd_fused4_kernel<0, 4>); break;
-            case 6: go(ln_bwd_fused4_kernel<0, 6>); break;
-            case 8: go(ln_bwd_fused4_kernel<0, 8>); break;
+            case 1: go(ln_bwd_fused4_kernel<KIND, 1>); break;
+            case 2: go(ln_bwd_fused4_kernel<KIND, 2>); break;
+            case 4: go(ln_bwd_fused4_kernel<KIND, 4>); break;
+            case 6: go(ln_bwd_fused4_kernel<KIND, 6>); break;
+            case 8: go(ln_bwd_fused4_kernel<KIND, 8>); break;
             default:
                 switch (D / 32) {
-                    case 2: go(ln_bwd_fused_kernel<0, 2>); break;
+                    case 2: go(ln_bwd_fused_kernel<KIND, 2>); break;
                     default: throw CdpError("LayerNorm width must be 64, 128, 256, 512, 768 or 1024");
                 }
         }
@@ -786,21 +842,21 @@ struct VitTrainer {
         const int K0 = P * P * 3;
         CBuf &patches = erec_w().patches;
         L_("patch_im2col", 0, double(B) * NP * patches.ld * 2, s, [&] {
-            launch_pdl(patch_im2col_kernel<0>, dim3(blocks_for(int64_t(B) * NP * patches.ld)), dim3(256), 0, s,
+            launch_pdl(patch_im2col_kernel<KIND>, dim3(blocks_for(int64_t(B) * NP * patches.ld)), dim3(256), 0, s,
                        (const float *)data_x.as<float>(), perm_w(), img, P, G, B * NP, patches.view());
         });
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = E.p;
             ep.ld = D;
             ep.out_f32 = 1;
             const CBuf &w = Wt(u_patch, p);
             reading({u_patch}, A_FWD, p, s, [&] {
-                gemm<false, true, EpiConvOut2<0>>("patch_embed", opnd(patches.hi.p, false, B * NP, K0 + 1, patches.ld),
-                                                  opnd(w.hi.p, true, D, K0 + 1, w.ld), B * NP, D, K0 + 1, ep, s, false);
+                gemm<false, true, EpiConvOut2<KIND>>("patch_embed", copnd(patches, false, B * NP, K0 + 1),
+                                                  copnd(w, true, D, K0 + 1), B * NP, D, K0 + 1, ep, s, false);
             });
         }
-        float *h0 = L > 0 ? brec_w(0).h.as<float>() : frec_w().hL.as<float>();
+        float *h0 = L > 0 ? brec_w(0).h.template as<float>() : frec_w().hL.template as<float>();
         reading({u_cls, u_pos}, A_FWD, p, s, [&] {
             L_("embed_assemble", 0, double(R) * D * 12, s, [&] {
                 launch_pdl(embed_assemble_kernel, dim3(blocks_for(int64_t(R) * D)), dim3(256), 0, s,
@@ -813,27 +869,26 @@ struct VitTrainer {
         const VBlock &b = blocks[l];
         VRec &y = brec_w(l);
         live_delta(l + 1 < L ? 1 : 2, +1);
-        float *hout = l + 1 < L ? brec_w(l + 1).h.as<float>() : frec_w().hL.as<float>();
+        float *hout = l + 1 < L ? brec_w(l + 1).h.template as<float>() : frec_w().hL.template as<float>();
         for (int u : {b.ln1, b.qkv, b.proj, b.ln2, b.fc1, b.fc2}) pull(u, p, s);
         layernorm(y.h.as<float>(), R, 1, b.ln1, p, y.u1.view(), y.m1.as<float>(), y.r1.as<float>(), s);
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = y.qkvb.hi.p;
+            ep.out_lo = y.qkvb.lo.p;
             ep.ld = y.qkvb.ld;
             const CBuf &w = Wt(b.qkv, p);
             reading({b.qkv}, A_FWD, p, s, [&] {
-                gemm<false, true, EpiConvOut2<0>>("qkv", opnd(y.u1.hi.p, false, R, D + 1, y.u1.ld),
-                                                  opnd(w.hi.p, true, 3 * D, D + 1, w.ld), R, 3 * D, D + 1, ep, s,
+                gemm<false, true, EpiConvOut2<KIND>>("qkv", copnd(y.u1, false, R, D + 1),
+                                                  copnd(w, true, 3 * D, D + 1), R, 3 * D, D + 1, ep, s,
                                                   false);
             });
         }
         // attention: S = Q K^T (fp32) -> P = softmax(scale S) (bf16) -> O = P V
         const float scale = 1.f / std::sqrt(float(HD));
         const int64_t qld = y.qkvb.ld;
-        const BView Q{y.qkvb.hi.p, HD, T, qld, HD, int64_t(T) * qld};
-        const BView Kv{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + D, HD, T, qld, HD, int64_t(T) * qld};
-        const BView V{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + 2 * D, HD, T, qld, HD, int64_t(T) * qld};
-        const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+        const BView Q = qview(y.qkvb, 0), Kv = qview(y.qkvb, D), V = qview(y.qkvb, 2 * D);
+        const BView Pv = pview(y.P);
         if (fused_attn) {
             attention_fwd(y, s);
         } else {
@@ -841,51 +896,54 @@ struct VitTrainer {
         L_("softmax", 0, double(B) * H * T * T * 6, s, [&] {
             const dim3 g((B * H * T * 32 + 255) / 256);
             const float *Sp = S.as<float>();
-            __nv_bfloat16 *Pp = y.P.as<__nv_bfloat16>();
-            if (T <= 128)
+            __nv_bfloat16 *Pp = y.P.hi.as<__nv_bfloat16>();
+            if (KIND == 1)
+                launch_pdl(softmax_fwd_c_kernel<KIND>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, y.P.view());
+            else if (T <= 128)
                 launch_pdl(softmax_fwd4_kernel<1>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
             else if (T <= 256)
                 launch_pdl(softmax_fwd4_kernel<2>, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
             else
                 launch_pdl(softmax_fwd_kernel, g, dim3(256), 0, s, Sp, B * H * T, T, lds, scale, Pp, ldp);
         });
-        bgemm<false, true>("attn_values", Pv, V, T, HD, T, y.attn.hi.p, y.attn.ld, int64_t(T) * y.attn.ld, HD, 0, s);
+        bgemm<false, true>("attn_values", Pv, V, T, HD, T, y.attn.hi.p, y.attn.ld, int64_t(T) * y.attn.ld, HD, 0, s,
+                           y.attn.lo.p);
         }
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = y.hmid.p;
             ep.ld = D;
             ep.out_f32 = 1;
             ep.add = y.h.p;
             const CBuf &w = Wt(b.proj, p);
             reading({b.proj}, A_FWD, p, s, [&] {
-                gemm<false, true, EpiConvOut2<0>>("proj", opnd(y.attn.hi.p, false, R, D + 1, y.attn.ld),
-                                                  opnd(w.hi.p, true, D, D + 1, w.ld), R, D, D + 1, ep, s, false);
+                gemm<false, true, EpiConvOut2<KIND>>("proj", copnd(y.attn, false, R, D + 1),
+                                                  copnd(w, true, D, D + 1), R, D, D + 1, ep, s, false);
             });
         }
         layernorm(y.hmid.as<float>(), R, 1, b.ln2, p, y.u2.view(), y.m2.as<float>(), y.r2.as<float>(), s);
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = y.z1.hi.p;  // gelu'(z) (the backward's factor), not z
             ep.ld = y.z1.ld;
             ep.gelu_out = y.g1.view();
             ep.out_gelu_grad = 1;
             const CBuf &w = Wt(b.fc1, p);
             reading({b.fc1}, A_FWD, p, s, [&] {
-                gemm<false, true, EpiConvOut2<0>>("fc1_gelu", opnd(y.u2.hi.p, false, R, D + 1, y.u2.ld),
-                                                  opnd(w.hi.p, true, F, D + 1, w.ld), R, F, D + 1, ep, s, false);
+                gemm<false, true, EpiConvOut2<KIND>>("fc1_gelu", copnd(y.u2, false, R, D + 1),
+                                                  copnd(w, true, F, D + 1), R, F, D + 1, ep, s, false);
             });
         }
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = hout;
             ep.ld = D;
             ep.out_f32 = 1;
             ep.add = y.hmid.p;
             const CBuf &w = Wt(b.fc2, p);
             reading({b.fc2}, A_FWD, p, s, [&] {
-                gemm<false, true, EpiConvOut2<0>>("fc2", opnd(y.g1.hi.p, false, R, F + 1, y.g1.ld),
-                                                  opnd(w.hi.p, true, D, F + 1, w.ld), R, D, F + 1, ep, s, false);
+                gemm<false, true, EpiConvOut2<KIND>>("fc2", copnd(y.g1, false, R, F + 1),
+                                                  copnd(w, true, D, F + 1), R, D, F + 1, ep, s, false);
             });
         }
     }
@@ -897,14 +955,14 @@ struct VitTrainer {
         pull(u_head, p, s);
         layernorm(f.hL.as<float>(), B, T, u_ln, p, f.uf.view(), f.mf.as<float>(), f.rf.as<float>(), s);
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = f.z.p;
             ep.ld = classes;
             ep.out_f32 = 1;
             const CBuf &w = Wt(u_head, p);
             reading({u_head}, A_FWD, p, s, [&] {
-                gemm<false, true, EpiConvOut2<0>>("head", opnd(f.uf.hi.p, false, B, D + 1, f.uf.ld),
-                                                  opnd(w.hi.p, true, classes, D + 1, w.ld), B, classes, D + 1, ep, s,
+                gemm<false, true, EpiConvOut2<KIND>>("head", copnd(f.uf, false, B, D + 1),
+                                                  copnd(w, true, classes, D + 1), B, classes, D + 1, ep, s,
                                                   false);
             });
         }
@@ -914,13 +972,13 @@ struct VitTrainer {
         const size_t lsm = sizeof(double) * nt + sizeof(float) * B * classes;
         if (classes <= 64 && lsm <= 48 * 1024) {
             L_("loss", 0, 0, s, [&] {
-                launch_pdl(loss_kernel<0>, dim3(1), dim3(nt), lsm, s, (const float *)f.z.as<float>(), B, classes,
+                launch_pdl(loss_kernel<KIND>, dim3(1), dim3(nt), lsm, s, (const float *)f.z.as<float>(), B, classes,
                            loss_kind, perm_w(), (const int *)data_lab.as<int>(), (const float *)nullptr, f.dz.view(),
                            lw, &fl->loss);
             });
         } else {
             L_("loss", 0, 0, s, [&] {
-                launch_pdl(xent_rows_kernel<0>, dim3(B), dim3(256), 0, s, (const float *)f.z.as<float>(), B, classes,
+                launch_pdl(xent_rows_kernel<KIND>, dim3(B), dim3(256), 0, s, (const float *)f.z.as<float>(), B, classes,
                            perm_w(), (const int *)data_lab.as<int>(), f.dz.view(), loss_rows.as<double>());
             });
             L_("loss_sum", 0, 0, s, [&] {
@@ -936,14 +994,14 @@ struct VitTrainer {
         VCarry &c = carry[cw];
         cudaEvent_t dz_ready = ev(cs);
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = duf.p;
             ep.ld = D;
             ep.out_f32 = 1;
             const CBuf &w = Wt(u_head, p);
             reading({u_head}, A_BWD, p, cs, [&] {
-                gemm<false, false, EpiConvOut2<0>>("head_dgrad", opnd(f.dz.hi.p, false, B, classes, f.dz.ld),
-                                                   opnd(w.hi.p, false, D, classes, w.ld), B, D, classes, ep, cs, false);
+                gemm<false, false, EpiConvOut2<KIND>>("head_dgrad", copnd(f.dz, false, B, classes),
+                                                   copnd(w, false, D, classes), B, D, classes, ep, cs, false);
             });
         }
         cudaEvent_t head_dg = ev(cs);
@@ -953,6 +1011,7 @@ struct VitTrainer {
         if (!sizing) {
             CDP_CUDA(cudaMemsetAsync(c.dh.p, 0, c.dh.bytes, cs));
             if (out_c) CDP_CUDA(cudaMemsetAsync(out_c->hi.p, 0, out_c->hi.bytes, cs));
+            if (out_c && out_c->lo.p) CDP_CUDA(cudaMemsetAsync(out_c->lo.p, 0, out_c->lo.bytes, cs));
         }
         layernorm_bwd(duf.as<float>(), f.hL.as<float>(), B, T, u_ln, p, f.mf.as<float>(), f.rf.as<float>(), nullptr,
                       c.dh.as<float>(), dgf.as<float>(), dbf.as<float>(), cs, out_c ? out_c->view() : CTensor{});
@@ -971,33 +1030,37 @@ struct VitTrainer {
         // ---- MLP (dhc_in = bf16(dh), written by the LayerNorm backward that produced dh)
         cudaEvent_t dhc_ready = ev(cs);
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = gr.dz1.hi.p;
+            ep.out_lo = gr.dz1.lo.p;
             ep.ld = gr.dz1.ld;
             ep.mul = y.z1.hi.p;  // stored gelu'(z)
             const CBuf &w = Wt(b.fc2, p);
             // the factor rows TMA-staged into shared memory by warp 3, the product stored by TMA (EpiConvAddT)
             static const bool staged = std::getenv("CDP_NO_TMA_ADD") == nullptr;
             reading({b.fc2}, A_BWD, p, cs, [&] {
-                if (staged && EpiConvAddT<0>::eligible(ep, F, tile_n(F)) && tile_n(F) >= 128)
-                    gemm<false, false, EpiConvAddT<0>>("fc2_dgrad_gelu", opnd(dhc_in.hi.p, false, R, D, dhc_in.ld),
-                                                       opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
-                else
-                    gemm<false, false, EpiConvOut2<0>>("fc2_dgrad_gelu", opnd(dhc_in.hi.p, false, R, D, dhc_in.ld),
-                                                       opnd(w.hi.p, false, F, D, w.ld), R, F, D, ep, cs, false);
+                if constexpr (KIND == 0) {
+                    if (staged && EpiConvAddT<KIND>::eligible(ep, F, tile_n(F)) && tile_n(F) >= 128) {
+                        gemm<false, false, EpiConvAddT<KIND>>("fc2_dgrad_gelu", copnd(dhc_in, false, R, D),
+                                                              copnd(w, false, F, D), R, F, D, ep, cs, false);
+                        return;
+                    }
+                }
+                gemm<false, false, EpiConvOut2<KIND>>("fc2_dgrad_gelu", copnd(dhc_in, false, R, D),
+                                                      copnd(w, false, F, D), R, F, D, ep, cs, false);
             });
         }
         cudaEvent_t dz1_ready = ev(cs);
         lin_hop(b.fc2, p, y.g1.view(), R, dhc_in.view(), dhc_ready, dz1_ready);
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = du.p;
             ep.ld = D;
             ep.out_f32 = 1;
             const CBuf &w = Wt(b.fc1, p);
             reading({b.fc1}, A_BWD, p, cs, [&] {
-                gemm<false, false, EpiConvOut2<0>>("fc1_dgrad", opnd(gr.dz1.hi.p, false, R, F, gr.dz1.ld),
-                                                   opnd(w.hi.p, false, D, F, w.ld), R, D, F, ep, cs, false);
+                gemm<false, false, EpiConvOut2<KIND>>("fc1_dgrad", copnd(gr.dz1, false, R, F),
+                                                   copnd(w, false, D, F), R, D, F, ep, cs, false);
             });
         }
         cudaEvent_t fc1_dg = ev(cs);
@@ -1008,57 +1071,64 @@ struct VitTrainer {
         // ---- attention
         cudaEvent_t dhmc_ready = ev(cs);
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = dattn.hi.p;
+            ep.out_lo = dattn.lo.p;
             ep.ld = dattn.ld;
             const CBuf &w = Wt(b.proj, p);
             reading({b.proj}, A_BWD, p, cs, [&] {
-                gemm<false, false, EpiConvOut2<0>>("proj_dgrad", opnd(gr.dhmc.hi.p, false, R, D, gr.dhmc.ld),
-                                                   opnd(w.hi.p, false, D, D, w.ld), R, D, D, ep, cs, false);
+                gemm<false, false, EpiConvOut2<KIND>>("proj_dgrad", copnd(gr.dhmc, false, R, D),
+                                                   copnd(w, false, D, D), R, D, D, ep, cs, false);
             });
         }
         cudaEvent_t proj_dg = ev(cs);
         lin_hop(b.proj, p, y.attn.view(), R, gr.dhmc.view(), dhmc_ready, proj_dg);
         const int64_t qld = y.qkvb.ld;
-        auto qv = [&](int col) {
-            return BView{static_cast<__nv_bfloat16 *>(y.qkvb.hi.p) + col, HD, T, qld, HD, int64_t(T) * qld};
-        };
+        auto qv = [&](int col) { return qview(y.qkvb, col); };
         const int64_t dld = gr.dqkv.ld;
         if (fused_attn) {
             attention_bwd(y, gr.dqkv, cs);
         } else {
-        const BView dO{dattn.hi.p, HD, T, dattn.ld, HD, int64_t(T) * dattn.ld};
-        const BView Pv{y.P.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
-        const BView dSv{dS.hi.p, T, T, ldp, int64_t(T) * ldp, int64_t(H) * T * ldp};
+        const BView dO = qview(dattn, 0);
+        const BView Pv = pview(y.P);
+        const BView dSv = pview(dS);
         bgemm<false, false>("attn_dprobs", dO, qv(2 * D), T, T, HD, dP.p, lds, int64_t(H) * T * lds, int64_t(T) * lds,
                             1, cs);
         L_("softmax_bwd", 0, double(B) * H * T * T * 8, cs, [&] {
             const dim3 g((B * H * T * 32 + 255) / 256);
             const float *dPp = dP.as<float>();
-            const __nv_bfloat16 *Pp = y.P.as<__nv_bfloat16>();
+            const __nv_bfloat16 *Pp = y.P.hi.as<__nv_bfloat16>();
             __nv_bfloat16 *dSp = static_cast<__nv_bfloat16 *>(dS.hi.p);
-            if (T <= 128)
+            if (KIND == 1)
+                launch_pdl(softmax_bwd_c_kernel<KIND>, g, dim3(256), 0, cs, dPp, y.P.view(), B * H * T, T, lds, scale,
+                           dS.view());
+            else if (T <= 128)
                 launch_pdl(softmax_bwd4_kernel<1>, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
             else if (T <= 256)
                 launch_pdl(softmax_bwd4_kernel<2>, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
             else
                 launch_pdl(softmax_bwd_kernel, g, dim3(256), 0, cs, dPp, Pp, B * H * T, T, lds, ldp, scale, dSp);
         });
-        __nv_bfloat16 *dq = static_cast<__nv_bfloat16 *>(gr.dqkv.hi.p);
-        bgemm<true, true>("attn_dvalues", Pv, dO, T, HD, T, dq + 2 * D, int(dld), int64_t(T) * dld, HD, 0, cs);
-        bgemm<false, true>("attn_dquery", dSv, qv(D), T, HD, T, dq, int(dld), int64_t(T) * dld, HD, 0, cs);
-        bgemm<true, true>("attn_dkey", dSv, qv(0), T, HD, T, dq + D, int(dld), int64_t(T) * dld, HD, 0, cs);
+        auto dq = [&](const DevBuf &half, int col) -> void * {
+            return half.p ? static_cast<uint8_t *>(half.p) + size_t(col) * ES : nullptr;
+        };
+        bgemm<true, true>("attn_dvalues", Pv, dO, T, HD, T, dq(gr.dqkv.hi, 2 * D), int(dld), int64_t(T) * dld, HD, 0,
+                          cs, dq(gr.dqkv.lo, 2 * D));
+        bgemm<false, true>("attn_dquery", dSv, qv(D), T, HD, T, dq(gr.dqkv.hi, 0), int(dld), int64_t(T) * dld, HD, 0,
+                           cs, dq(gr.dqkv.lo, 0));
+        bgemm<true, true>("attn_dkey", dSv, qv(0), T, HD, T, dq(gr.dqkv.hi, D), int(dld), int64_t(T) * dld, HD, 0, cs,
+                          dq(gr.dqkv.lo, D));
         }
         cudaEvent_t dqkv_ready = ev(cs);
         {
-            typename EpiConvOut2<0>::Params ep{};
+            typename EpiConvOut2<KIND>::Params ep{};
             ep.out = du.p;
             ep.ld = D;
             ep.out_f32 = 1;
             const CBuf &w = Wt(b.qkv, p);
             reading({b.qkv}, A_BWD, p, cs, [&] {
-                gemm<false, false, EpiConvOut2<0>>("qkv_dgrad", opnd(gr.dqkv.hi.p, false, R, 3 * D, dld),
-                                                   opnd(w.hi.p, false, D, 3 * D, w.ld), R, D, 3 * D, ep, cs, false);
+                gemm<false, false, EpiConvOut2<KIND>>("qkv_dgrad", copnd(gr.dqkv, false, R, 3 * D),
+                                                   copnd(w, false, D, 3 * D), R, D, 3 * D, ep, cs, false);
             });
         }
         cudaEvent_t qkv_dg = ev(cs);
@@ -1096,7 +1166,7 @@ struct VitTrainer {
 
     void cast(const float *in, int rows, int per, int in_per, int skip, const CTensor &out, cudaStream_t s) {
         L_("cast", 0, double(rows) * D * 6, s, [&] {
-            launch_pdl(cast_rows_kernel<0>, dim3(blocks_for(int64_t(rows) * D)), dim3(256), 0, s, in, rows, D, per,
+            launch_pdl(cast_rows_kernel<KIND>, dim3(blocks_for(int64_t(rows) * D)), dim3(256), 0, s, in, rows, D, per,
                        in_per, skip, out);
         });
     }
@@ -1197,7 +1267,7 @@ struct VitTrainer {
         for (size_t i = 0; i < units.size(); ++i) {
             const VUnit &u = units[i];
             if (u.kind != V_LIN) continue;
-            pack_tensor_kernel<0><<<blocks_for(u.n), 256, 0, main>>>(theta[sl] + u.base, u.n, u.cols,
+            pack_tensor_kernel<KIND><<<blocks_for(u.n), 256, 0, main>>>(theta[sl] + u.base, u.n, u.cols,
                                                                      wc[sl][i].view());
             CDP_CUDA(cudaGetLastError());
         }
@@ -1272,15 +1342,29 @@ struct VitTrainer {
 using namespace cdp;
 
 struct cdp_vit {
-    std::unique_ptr<VitTrainer> impl;
+    std::unique_ptr<VitTrainer<0>> b16;  // bf16 operands
+    std::unique_ptr<VitTrainer<1>> f32;  // fp32 mode
 };
 
-static std::unique_ptr<VitTrainer> vit_new(int image, int patch, int dim, int depth, int heads, int mlp, int classes,
+// run fn on the trainer of either mode (C-ABI entry points), errors as cdp status codes
+template <class Fn>
+static int with_vit(cdp_vit *tr, Fn &&fn) {
+    return guarded([&] {
+        CDP_REQUIRE(tr && (tr->b16 || tr->f32), "null ViT trainer");
+        if (tr->b16)
+            fn(*tr->b16);
+        else
+            fn(*tr->f32);
+    });
+}
+
+template <int KIND>
+static std::unique_ptr<VitTrainer<KIND>> vit_new(int image, int patch, int dim, int depth, int heads, int mlp, int classes,
                                            int micro_batch, int workers, float momentum, float weight_decay,
                                            int n_samples, const float *x, const int32_t *labels) {
     CDP_REQUIRE(micro_batch >= 1 && micro_batch <= 256, "micro-batch must be in [1, 256]");
     CDP_REQUIRE(depth >= 1 && depth <= 40, "depth: 1..40");
-    auto tr = std::make_unique<VitTrainer>();
+    auto tr = std::make_unique<VitTrainer<KIND>>();
     tr->B = micro_batch;
     tr->img = image;
     tr->P = patch;
@@ -1305,11 +1389,13 @@ static std::unique_ptr<VitTrainer> vit_new(int image, int patch, int dim, int de
 extern "C" int cdp_vit_create_rank(int image, int patch, int dim, int depth, int heads, int mlp, int classes,
                                    int micro_batch, int world, int rank, const int32_t *unit_stage,
                                    const uint8_t *stage_fresh, float momentum, float weight_decay, int n_samples,
-                                   const float *x, const int32_t *labels, cdp_vit **out) {
+                                   const float *x, const int32_t *labels, int dtype, cdp_vit **out) {
     return guarded([&] {
         CDP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
-        auto tr = vit_new(image, patch, dim, depth, heads, mlp, classes, micro_batch, 1, momentum, weight_decay,
-                          n_samples, x, labels);
+        CDP_REQUIRE(dtype == CDP_DTYPE_BF16 || dtype == CDP_DTYPE_FP32, "dtype: CDP_DTYPE_BF16 or CDP_DTYPE_FP32");
+        auto make = [&](auto kind) {
+        auto tr = vit_new<decltype(kind)::value>(image, patch, dim, depth, heads, mlp, classes, micro_batch, 1,
+                                                 momentum, weight_decay, n_samples, x, labels);
         tr->rank = rank;
         tr->world = world;
         for (size_t i = 0; i < tr->units.size(); ++i) {
@@ -1323,7 +1409,14 @@ extern "C" int cdp_vit_create_rank(int image, int patch, int dim, int depth, int
         for (int l = 0; l < depth; ++l) tr->slot[0][1 + l] = l;
         tr->pool[1] = depth;
         tr->build();
-        *out = new cdp_vit{std::move(tr)};
+        return tr;
+        };
+        std::unique_ptr<cdp_vit> h(new cdp_vit{});
+        if (dtype == CDP_DTYPE_BF16)
+            h->b16 = make(std::integral_constant<int, 0>{});
+        else
+            h->f32 = make(std::integral_constant<int, 1>{});
+        *out = h.release();
     });
 }
 
@@ -1331,11 +1424,13 @@ extern "C" int cdp_vit_create_cyclic(int image, int patch, int dim, int depth, i
                                      int micro_batch, int n_workers, const int32_t *unit_stage, const uint8_t *fresh,
                                      int n_ops, const int32_t *ops, const int32_t *rec_slot, const int32_t *pools,
                                      float momentum, float weight_decay, int probe, int n_samples, const float *x,
-                                     const int32_t *labels, cdp_vit **out) {
+                                     const int32_t *labels, int dtype, cdp_vit **out) {
     return guarded([&] {
         CDP_REQUIRE(n_workers >= 2, "single-GPU cyclic CDP needs at least two workers (micro-batches)");
-        auto tr = vit_new(image, patch, dim, depth, heads, mlp, classes, micro_batch, n_workers, momentum,
-                          weight_decay, n_samples, x, labels);
+        CDP_REQUIRE(dtype == CDP_DTYPE_BF16 || dtype == CDP_DTYPE_FP32, "dtype: CDP_DTYPE_BF16 or CDP_DTYPE_FP32");
+        auto make = [&](auto kind) {
+        auto tr = vit_new<decltype(kind)::value>(image, patch, dim, depth, heads, mlp, classes, micro_batch,
+                                                 n_workers, momentum, weight_decay, n_samples, x, labels);
         const int NS = depth + 2;
         tr->seg_stage.assign(NS, 0);
         for (size_t i = 0; i < tr->units.size(); ++i) {
@@ -1375,30 +1470,35 @@ extern "C" int cdp_vit_create_cyclic(int image, int patch, int dim, int depth, i
             }
         tr->probe = probe != 0;
         tr->build();
-        *out = new cdp_vit{std::move(tr)};
+        return tr;
+        };
+        std::unique_ptr<cdp_vit> h(new cdp_vit{});
+        if (dtype == CDP_DTYPE_BF16)
+            h->b16 = make(std::integral_constant<int, 0>{});
+        else
+            h->f32 = make(std::integral_constant<int, 1>{});
+        *out = h.release();
     });
 }
 
 extern "C" int cdp_vit_set_trace(cdp_vit *tr, int on) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         CDP_REQUIRE(!m.exec[0], "set the trace option before cdp_vit_connect (it changes the captured step)");
         m.trace = on != 0;
         if (m.trace && !m.tlog.p) {
-            m.tlog = DevBuf(size_t(VitTrainer::kTraceCap) * kTraceWords * 4);
+            m.tlog = DevBuf(size_t(std::decay_t<decltype(m)>::kTraceCap) * kTraceWords * 4);
             m.tcur = DevBuf(4);
         }
     });
 }
 
 extern "C" int cdp_vit_trace(cdp_vit *tr, uint32_t *records, int max_records, int *count) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         CDP_REQUIRE(m.trace, "trace option not set");
         CDP_CUDA(cudaStreamSynchronize(m.main));
         uint32_t n = 0;
         CDP_CUDA(cudaMemcpy(&n, m.tcur.p, 4, cudaMemcpyDeviceToHost));
-        CDP_REQUIRE(n <= VitTrainer::kTraceCap, "trace buffer overflow: read the records more often");
+        CDP_REQUIRE(n <= std::decay_t<decltype(m)>::kTraceCap, "trace buffer overflow: read the records more often");
         *count = int(n);
         const int k = std::min<int>(int(n), max_records);
         if (k > 0) CDP_CUDA(cudaMemcpy(records, m.tlog.p, size_t(k) * kTraceWords * 4, cudaMemcpyDeviceToHost));
@@ -1407,27 +1507,26 @@ extern "C" int cdp_vit_trace(cdp_vit *tr, uint32_t *records, int max_records, in
 }
 
 extern "C" int cdp_vit_info(cdp_vit *tr, int64_t *n_params, int *n_units) {
-    return guarded([&] {
-        *n_params = tr->impl->Pn;
-        *n_units = int(tr->impl->units.size());
+    return with_vit(tr, [&](auto &m) {
+        *n_params = m.Pn;
+        *n_units = int(m.units.size());
     });
 }
 
 extern "C" int cdp_vit_region(cdp_vit *tr, void **base) {
-    return guarded([&] { *base = tr->impl->region.p; });
+    return with_vit(tr, [&](auto &m) { *base = m.region.p; });
 }
 
 extern "C" int cdp_vit_ipc_handle(cdp_vit *tr, void *handle64) {
-    return guarded([&] {
+    return with_vit(tr, [&](auto &m) {
         cudaIpcMemHandle_t h;
-        CDP_CUDA(cudaIpcGetMemHandle(&h, tr->impl->region.p));
+        CDP_CUDA(cudaIpcGetMemHandle(&h, m.region.p));
         std::memcpy(handle64, &h, sizeof(h));
     });
 }
 
 extern "C" int cdp_vit_pull_chain(cdp_vit *tr, const int32_t *pred_succ, int n_stages) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         CDP_REQUIRE(!m.exec[0], "the pull chain is set before connect (graph capture)");
         CDP_REQUIRE(n_stages == 0 || (n_stages == m.world && pred_succ), "pull chain: one row per stage");
         for (int k = 0; k < 2 * n_stages; ++k)
@@ -1438,8 +1537,7 @@ extern "C" int cdp_vit_pull_chain(cdp_vit *tr, const int32_t *pred_succ, int n_s
 }
 
 extern "C" int cdp_vit_connect(cdp_vit *tr, void *const *regions) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         auto at = [&](int r) { return static_cast<uint8_t *>(regions[r]); };
         if (m.rank > 0) {
             m.prev_ring = reinterpret_cast<RingFlags *>(at(m.rank - 1));
@@ -1463,25 +1561,24 @@ extern "C" void cdp_vit_destroy(cdp_vit *tr) {
 }
 
 extern "C" int cdp_vit_set_params(cdp_vit *tr, int which, const float *theta) {
-    return guarded([&] { tr->impl->set_params(which, theta); });
+    return with_vit(tr, [&](auto &m) { m.set_params(which, theta); });
 }
 
 extern "C" int cdp_vit_get_params(cdp_vit *tr, int which, float *theta) {
-    return guarded([&] { tr->impl->get_params(which, theta); });
+    return with_vit(tr, [&](auto &m) { m.get_params(which, theta); });
 }
 
 extern "C" int cdp_vit_step(cdp_vit *tr, const int32_t *perm, float lr) {
-    return guarded([&] { tr->impl->step(perm, lr); });
+    return with_vit(tr, [&](auto &m) { m.step(perm, lr); });
 }
 
 extern "C" int cdp_vit_step_host_batch(cdp_vit *tr, const float *x, const int32_t *labels, float lr) {
-    return guarded([&] { tr->impl->step_host_batch(x, labels, lr); });
+    return with_vit(tr, [&](auto &m) { m.step_host_batch(x, labels, lr); });
 }
 
 extern "C" int cdp_vit_profile_step(cdp_vit *tr, const int32_t *perm, float lr, int serial, int max_ops, char *names,
                                     int name_len, double *flops, double *bytes, float *ms, int *n_ops) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         m.profile_step(perm, lr, serial != 0);
         const int n = std::min<int>(max_ops, int(m.oprecs.size()));
         *n_ops = int(m.oprecs.size());
@@ -1497,8 +1594,7 @@ extern "C" int cdp_vit_profile_step(cdp_vit *tr, const int32_t *perm, float lr, 
 }
 
 extern "C" int cdp_vit_history(cdp_vit *tr, int max, double *losses, uint32_t *flags, int *count) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         CDP_CUDA(cudaStreamSynchronize(m.main));
         const int c = m.t - 1;
         *count = c;
@@ -1518,14 +1614,14 @@ extern "C" int cdp_vit_history(cdp_vit *tr, int max, double *losses, uint32_t *f
 }
 
 extern "C" int cdp_vit_sync(cdp_vit *tr) {
-    return guarded([&] { CDP_CUDA(cudaStreamSynchronize(tr->impl->main)); });
+    return with_vit(tr, [&](auto &m) { CDP_CUDA(cudaStreamSynchronize(m.main)); });
 }
 
 extern "C" int cdp_vit_ring_error(cdp_vit *tr, int *err) {
-    return guarded([&] {
-        CDP_CUDA(cudaStreamSynchronize(tr->impl->main));
+    return with_vit(tr, [&](auto &m) {
+        CDP_CUDA(cudaStreamSynchronize(m.main));
         uint32_t e = 0;
-        CDP_CUDA(cudaMemcpy(&e, &tr->impl->ring->err, 4, cudaMemcpyDeviceToHost));
+        CDP_CUDA(cudaMemcpy(&e, &m.ring->err, 4, cudaMemcpyDeviceToHost));
         *err = int(e);
     });
 }
@@ -1535,13 +1631,12 @@ extern "C" int cdp_vit_stats(cdp_vit *tr, int64_t *out, int n_out) {
     // [1] parameter-state bytes, [2] kernels / step, [3] tensor-core flops / step,
     // [4] executed high-water mark of live record bytes (probe; 0 when off),
     // [5..7] bytes of one embed / block / final record, [8..10] slots per pool
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         int64_t act = 0;
         for (int k = 0; k < 3; ++k) act += m.record_bytes(k) * m.pool[k];
         int64_t par = int64_t(m.Pp) * (m.vel ? 16 : 12);
         for (int v = 0; v < 2; ++v)
-            for (auto &w : m.wc[v]) par += int64_t(w.hi.bytes);
+            for (auto &w : m.wc[v]) par += int64_t(cbytes(w));
         int64_t hw[2] = {0, 0};
         if (m.probe) {
             CDP_CUDA(cudaStreamSynchronize(m.main));
@@ -1554,8 +1649,7 @@ extern "C" int cdp_vit_stats(cdp_vit *tr, int64_t *out, int n_out) {
 }
 
 extern "C" int cdp_vit_mark(cdp_vit *tr, int k) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         while (int(m.marks.size()) <= k) {
             cudaEvent_t e;
             CDP_CUDA(cudaEventCreate(&e));
@@ -1566,16 +1660,14 @@ extern "C" int cdp_vit_mark(cdp_vit *tr, int k) {
 }
 
 extern "C" int cdp_vit_elapsed(cdp_vit *tr, int a, int b, float *ms) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         CDP_CUDA(cudaEventSynchronize(m.marks[b]));
         CDP_CUDA(cudaEventElapsedTime(ms, m.marks[a], m.marks[b]));
     });
 }
 
 extern "C" int cdp_vit_flush_l2(cdp_vit *tr) {
-    return guarded([&] {
-        auto &m = *tr->impl;
+    return with_vit(tr, [&](auto &m) {
         if (!m.flush_buf.p) m.flush_buf = DevBuf(size_t(256) << 20);
         CDP_CUDA(cudaMemsetAsync(m.flush_buf.p, m.t & 0xff, m.flush_buf.bytes, m.main));
     });

@@ -20,6 +20,7 @@ import os
 import numpy as np
 
 from . import _native as N
+from .device import DTYPES
 
 VIT_B16 = dict(image=224, patch=16, dim=768, depth=12, heads=12, mlp=3072, classes=1000)
 
@@ -109,10 +110,14 @@ def _i32p(a):
 
 
 class DeviceVit:
-    """One rank (worker) of CDP training of a ViT on this process's GPU (bf16)."""
+    """One rank (worker) of CDP training of a ViT on this process's GPU.  dtype "bf16" (bf16 operands,
+    fused attention) or "fp32" (3xTF32 operands, fp32 softmax: parity at fp32 tolerance)."""
 
     def __init__(self, cfg=None, micro_batch=32, world=1, rank=0, rule=None, momentum=0.0, weight_decay=0.0,
-                 inputs=None, labels=None, stage_of_unit=None, trace=False):
+                 inputs=None, labels=None, stage_of_unit=None, trace=False, dtype="bf16"):
+        if dtype not in DTYPES:
+            raise ValueError(f"dtype must be one of {sorted(DTYPES)}")
+        self.dtype = dtype
         self.cfg = dict(VIT_B16 if cfg is None else cfg)
         self.lib = N.lib()
         self.micro_batch, self.world, self.rank = int(micro_batch), int(world), int(rank)
@@ -137,7 +142,7 @@ class DeviceVit:
             c["image"], c["patch"], c["dim"], c["depth"], c["heads"], c["mlp"], c["classes"], self.micro_batch,
             world, rank, _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), float(momentum), float(weight_decay), n,
             x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
-            ctypes.byref(h)))
+            DTYPES[dtype], ctypes.byref(h)))
         self.h = h
         self._keep = (x, lab)
         if trace:
@@ -158,12 +163,15 @@ class DeviceVit:
 
     @classmethod
     def single_gpu(cls, cfg=None, micro_batch=32, n_workers=4, rule=None, momentum=0.0, weight_decay=0.0,
-                   inputs=None, labels=None, probe=True, trace=False):
+                   inputs=None, labels=None, probe=True, trace=False, dtype="bf16"):
         """Single-GPU cyclic CDP (rule) or DP (rule None): `n_workers` micro-batches = stages on this
         GPU, stepped through the reference SINGLE_GPU_CDP / SINGLE_GPU_DP timeline with activation
         records from the plan's interval colouring (cdp_vit_create_cyclic).  step() takes
         n_workers * micro_batch indices, worker-major (ref models.py:173-185)."""
         self = cls.__new__(cls)
+        if dtype not in DTYPES:
+            raise ValueError(f"dtype must be one of {sorted(DTYPES)}")
+        self.dtype = dtype
         self.cfg = dict(VIT_B16 if cfg is None else cfg)
         self.lib = N.lib()
         self.micro_batch, self.world, self.rank = int(micro_batch), 1, 0
@@ -188,7 +196,7 @@ class DeviceVit:
             self.n_workers, _i32p(self.stage), fresh.ctypes.data_as(N.c_u8_p), len(ops), _i32p(ops), _i32p(slot),
             _i32p(pools), float(momentum), float(weight_decay), int(bool(probe)), n,
             x.ctypes.data_as(N.c_float_p) if x is not None else None, _i32p(lab) if lab is not None else None,
-            ctypes.byref(h)))
+            DTYPES[dtype], ctypes.byref(h)))
         self.h = h
         self._keep = (x, lab)
         if trace:

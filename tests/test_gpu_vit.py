@@ -4,7 +4,11 @@ restatement (oracle/vit_torch.py, pinned to torchvision's VisionTransformer in t
 bf16 tolerances (BASELINE north star: a separately stated bf16 tolerance): per-step losses within 5e-3
 relative, and the parameter UPDATE (theta_K - theta_0) within 2.5e-2 relative L2 of the oracle's update
 (measured on B200: 5e-3 and 6e-4)
-(the parameters themselves would hide gradient errors behind the unchanged initialisation)."""
+(the parameters themselves would hide gradient errors behind the unchanged initialisation).
+
+fp32 mode (dtype "fp32": operands as tf32 hi + lo pairs, 3xTF32 tcgen05 products, fp32 softmax): the
+fp32 tolerances of the north star, update rel-L2 <= 1e-5 and per-step losses within 5e-6 relative
+(measured on B200: 1.2e-6 - 1.8e-6 at 1-4 ranks, 5.6e-6 on full ViT-B/16; losses <= 9.2e-7)."""
 
 import numpy as np
 import pytest
@@ -18,7 +22,7 @@ CFG197 = dict(image=56, patch=4, dim=128, depth=1, heads=2, mlp=256, classes=10)
 MB = 4
 
 
-def _run(world, rule, steps, momentum=0.9, lr=0.1, cfg=CFG, mb=MB):
+def _run(world, rule, steps, momentum=0.9, lr=0.1, cfg=CFG, mb=MB, dtype="bf16"):
     from oracle.vit_torch import init_flat
     from paper_2403_08837_b200.resnet import synthetic_cifar
     from paper_2403_08837_b200.vit import DeviceVit
@@ -26,7 +30,7 @@ def _run(world, rule, steps, momentum=0.9, lr=0.1, cfg=CFG, mb=MB):
     x, y = synthetic_cifar(world * mb * 2, seed=4, hw=cfg["image"], classes=cfg["classes"])
     init = init_flat(**cfg, seed=0)
     perms = [np.random.default_rng([6, t]).permutation(len(x))[: world * mb] for t in range(1, steps + 1)]
-    tr = [DeviceVit(cfg, mb, world, r, rule, momentum, inputs=x, labels=y) for r in range(world)]
+    tr = [DeviceVit(cfg, mb, world, r, rule, momentum, inputs=x, labels=y, dtype=dtype) for r in range(world)]
     regions = [t.region() for t in tr]
     for t in tr:
         t.set_params(init, -1)
@@ -56,11 +60,17 @@ def _oracle(init, x, y, perms, world, rule, stage, momentum=0.9, lr=0.1, cfg=CFG
     return run_cdp(cfg, init, x.astype(np.float64), y, world, mb, perms, lr, momentum, fresh)
 
 
-def _check(init, losses, final, want, wl):
+def _check(init, losses, final, want, wl, tol_upd=2.5e-2, tol_loss=5e-3):
     d_ours, d_want = final - init, want - init
     rel = float(np.linalg.norm(d_ours - d_want) / np.linalg.norm(d_want))
-    assert rel <= 2.5e-2, rel
-    assert np.all(np.abs(losses - np.array(wl)) <= 5e-3 * np.abs(np.array(wl))), (losses, wl)
+    dl = float(np.max(np.abs(losses - np.array(wl)) / np.abs(np.array(wl))))
+    print(f"update rel-L2 {rel:.2e}, max loss rel {dl:.2e}")
+    assert rel <= tol_upd, rel
+    assert dl <= tol_loss, (losses, wl)
+    return rel
+
+
+FP32_TOL = dict(tol_upd=1e-5, tol_loss=5e-6)
 
 
 def test_single_gpu_vit_steps_vs_restatement(cuda):
@@ -98,3 +108,35 @@ def test_vit_b16_bench_shape_vs_restatement(cuda, world):
     init, x, y, perms, losses, final, stage = _run(world, rule, 2, cfg=VITB16, mb=2)
     want, wl = _oracle(init, x, y, perms, world, rule, stage, cfg=VITB16, mb=2)
     _check(init, losses, final, want, wl)
+
+
+@pytest.mark.parametrize("world,rule_name", [(1, None), (2, "cdp-v1"), (2, "cdp-v2"), (3, "cdp-v2"), (4, "cdp-v1")])
+def test_vit_fp32_vs_restatement(cuda, world, rule_name):
+    """fp32 mode: single rank and 2-4 CDP ranks against the float64 restatement at fp32 tolerance (the
+    CDP-v1 / v2 version semantics of every forward / backward read show up at this level)."""
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = rule_by_name(rule_name, world) if rule_name else None
+    init, x, y, perms, losses, final, stage = _run(world, rule, 3, dtype="fp32")
+    want, wl = _oracle(init, x, y, perms, world, rule, stage)
+    _check(init, losses, final, want, wl, **FP32_TOL)
+
+
+def test_vit_fp32_197_tokens_vs_restatement(cuda):
+    """fp32 mode, 197 tokens (two query tiles, ragged key tiles in the batched attention GEMMs)."""
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = rule_by_name("cdp-v2", 2)
+    init, x, y, perms, losses, final, stage = _run(2, rule, 2, cfg=CFG197, mb=2, dtype="fp32")
+    want, wl = _oracle(init, x, y, perms, 2, rule, stage, cfg=CFG197, mb=2)
+    _check(init, losses, final, want, wl, **FP32_TOL)
+
+
+def test_vit_b16_fp32_bench_shape_vs_restatement(cuda):
+    """Full ViT-B/16 in fp32 mode, two CDP-v2 ranks, B = 2, two steps, against the float64 restatement."""
+    from paper_2403_08837_b200.rules import rule_by_name
+
+    rule = rule_by_name("cdp-v2", 2)
+    init, x, y, perms, losses, final, stage = _run(2, rule, 2, cfg=VITB16, mb=2, dtype="fp32")
+    want, wl = _oracle(init, x, y, perms, 2, rule, stage, cfg=VITB16, mb=2)
+    _check(init, losses, final, want, wl, **FP32_TOL)
