@@ -1,14 +1,17 @@
 // Device-resident CDP training step for Vision Transformers (BASELINE configs[3]:
-// ViT-B/16, 224x224), bf16 operands, fp32 residual stream / master state.
+// ViT-B/16, 224x224), bf16 operands (fp32 mode: tf32 hi + lo pairs, 3xTF32), fp32
+// residual stream / master state.
 //
 // Same step semantics as the other trainers (ref training/engine.py:66-116: the
 // per-stage version rule, gradient hops w_i -> w_{i+1} fused into the weight-gradient
 // GEMM epilogues, the SGD-momentum update on the last worker, parameter pulls), one
-// worker (micro-batch) per process.  Layer compute:
+// worker (micro-batch) per process, or N workers on one GPU (cyclic executor).  Layer compute:
 //   linear layers  = persistent tcgen05 GEMMs (gemm_pk_kernel, GM_PLAIN) with the bias
 //                    folded in by a ones column ([x, 1] . [W; b] = the reference's
 //                    flat [W][b] layout); GELU and the residual add fused in epilogues;
-//   attention      = batched tcgen05 GEMMs (GM_BATCH) over 4-D TMA views of the fused
+//   attention      = fused kernels (attn_kernels.cuh: scores / probabilities in TMEM and
+//                    shared memory, bf16), or (fp32 mode, T > 256, CDP_VIT_UNFUSED=1)
+//                    batched tcgen05 GEMMs (GM_BATCH) over 4-D TMA views of the fused
 //                    qkv buffer {64 dims, tokens, heads, samples} + row softmax kernels;
 //   LayerNorm      = warp-per-row kernels, parameter gradients by fixed-order row blocks.
 // Hop units (parameter tensors, torchvision order): patch [[W^T]; b], cls, pos, per
