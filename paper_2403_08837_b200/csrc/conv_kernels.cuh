@@ -912,6 +912,46 @@ static __global__ void __launch_bounds__(256) bn_apply_kernel(const void *__rest
     f.load(mean, rstd, gamma, beta, int(i % C8) * 8);
     if constexpr (RES == 2) f2.load(res.mean, res.rstd, res.gamma, res.beta, int(i % C8) * 8);
     if (fixed) {
+        if constexpr (KIND == 0) {
+            // U vectors' loads issued before any store (the compiler cannot move a load above a store to
+            // `out`, which it must assume may alias: one vector in flight per thread otherwise)
+            constexpr int U = RES == 0 ? 4 : 2;
+            const uint4 *yv = static_cast<const uint4 *>(y);
+            const uint4 *rv = RES == 1 ? static_cast<const uint4 *>(res.act.hi)
+                                       : RES == 2 ? static_cast<const uint4 *>(res.y) : nullptr;
+            for (; i < n; i += stride * U) {
+                uint4 a[U], r[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t j = i + u * stride;
+                    if (j < n) {
+                        a[u] = yv[j];
+                        if constexpr (RES != 0) r[u] = rv[j];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t j = i + u * stride;
+                    if (j >= n) break;
+                    F8 v;
+                    bf16x8_to_f8(a[u], v);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) v.v[k] = f(v.v[k], k);
+                    if constexpr (RES != 0) {
+                        F8 q;
+                        bf16x8_to_f8(r[u], q);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) v.v[k] += RES == 1 ? q.v[k] : f2(q.v[k], k);
+                    }
+                    if (relu) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) v.v[k] = fmaxf(v.v[k], 0.f);
+                    }
+                    static_cast<uint4 *>(out.hi)[j] = f8_to_bf16x8(v);
+                }
+            }
+            return;
+        }
 #pragma unroll 2
         for (; i < n; i += stride) bn_apply_vec<KIND, RES>(y, size_t(i) * 8, f, res, f2, relu, out);
         return;
@@ -1021,6 +1061,111 @@ static __global__ void __launch_bounds__(256) bn_bwd_stats_kernel(const void *__
     }
 }
 
+// bf16 backward statistics, 8 channels (16 bytes) per thread: TPR = min(C/8, 32) threads per row,
+// 256/TPR row phases, U rows' loads issued before their arithmetic.  The grid is sized to the GPU
+// (two CTAs per SM) and every CTA strides over row chunks of phases * U rows in a fixed order (the
+// 4-channel kernel above ran fixed 1024-row blocks: 392 CTAs on the 64-channel ResNet-50 tensors =
+// 1.3 waves, 3.4 TB/s).  Same partial layout [C][CTAs][2] (bn_finalize_bwd_kernel over gridDim.x
+// partials); phases combined in fixed order in fp64.
+template <bool MASK, bool Y2>
+static __global__ void __launch_bounds__(256, 2)
+    bn_bwd_stats8_kernel(const __nv_bfloat16 *__restrict__ g, const __nv_bfloat16 *__restrict__ mask, int64_t P,
+                         int C, const __nv_bfloat16 *__restrict__ y, const float *mean, const float *rstd,
+                         double *partial, const __nv_bfloat16 *__restrict__ y2, const float *mean2,
+                         const float *rstd2, double *partial2) {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    constexpr int NA = Y2 ? 3 : 2;
+    constexpr int U = Y2 ? 2 : 4;
+    __shared__ __align__(16) float red[NA][256 * 8];
+    const int C8 = C / 8;
+    const int TPR = C8 < 32 ? C8 : 32;
+    const int phases = 256 / TPR;
+    const int tx = threadIdx.x % TPR, ty = threadIdx.x / TPR;
+    const int c = (blockIdx.y * TPR + tx) * 8;
+    const int64_t chunk = int64_t(phases) * U;
+    float a0[8], a1[8], b1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a0[k] = a1[k] = b1[k] = 0.f;
+    if (ty < phases && c < C) {
+        const F8 mu = ld_f8(mean, c), rs = ld_f8(rstd, c);
+        F8 mu2 = mu, rs2 = rs;
+        if constexpr (Y2) {
+            mu2 = ld_f8(mean2, c);
+            rs2 = ld_f8(rstd2, c);
+        }
+        const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+        for (int64_t rb = int64_t(blockIdx.x) * chunk + ty; rb < P; rb += int64_t(gridDim.x) * chunk) {
+            uint4 gr[U], yr[U], mr[U], y2r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {  // rows past the end contribute g = 0
+                const int64_t r = rb + int64_t(u) * phases;
+                const bool in = r < P;
+                const size_t o = size_t(in ? r : rb) * C + c;
+                gr[u] = in ? *reinterpret_cast<const uint4 *>(g + o) : z4;
+                yr[u] = *reinterpret_cast<const uint4 *>(y + o);
+                if constexpr (MASK) mr[u] = *reinterpret_cast<const uint4 *>(mask + o);
+                if constexpr (Y2) y2r[u] = *reinterpret_cast<const uint4 *>(y2 + o);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                F8 gv, x;
+                bf16x8_to_f8(gr[u], gv);
+                bf16x8_to_f8(yr[u], x);
+                if constexpr (MASK) {
+                    F8 mk;
+                    bf16x8_to_f8(mr[u], mk);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) gv.v[k] = mk.v[k] > 0.f ? gv.v[k] : 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    a0[k] += gv.v[k];
+                    a1[k] = fmaf(gv.v[k], (x.v[k] - mu.v[k]) * rs.v[k], a1[k]);
+                }
+                if constexpr (Y2) {
+                    F8 x2;
+                    bf16x8_to_f8(y2r[u], x2);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) b1[k] = fmaf(gv.v[k], (x2.v[k] - mu2.v[k]) * rs2.v[k], b1[k]);
+                }
+            }
+        }
+    }
+    const int slot = threadIdx.x * 8;
+    *reinterpret_cast<float4 *>(&red[0][slot]) = make_float4(a0[0], a0[1], a0[2], a0[3]);
+    *reinterpret_cast<float4 *>(&red[0][slot + 4]) = make_float4(a0[4], a0[5], a0[6], a0[7]);
+    *reinterpret_cast<float4 *>(&red[1][slot]) = make_float4(a1[0], a1[1], a1[2], a1[3]);
+    *reinterpret_cast<float4 *>(&red[1][slot + 4]) = make_float4(a1[4], a1[5], a1[6], a1[7]);
+    if constexpr (Y2) {
+        *reinterpret_cast<float4 *>(&red[NA - 1][slot]) = make_float4(b1[0], b1[1], b1[2], b1[3]);
+        *reinterpret_cast<float4 *>(&red[NA - 1][slot + 4]) = make_float4(b1[4], b1[5], b1[6], b1[7]);
+    }
+    __syncthreads();
+    // thread k < TPR*8 combines channel (blockIdx.y*TPR*8 + k) over the phases in order
+    const int k = threadIdx.x;
+    if (k < TPR * 8) {
+        const int cc = blockIdx.y * TPR * 8 + k;
+        if (cc < C) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+            for (int ph = 0; ph < phases; ++ph) {
+                const int idx = ph * TPR * 8 + k;
+                s0 += double(red[0][idx]);
+                s1 += double(red[1][idx]);
+                if constexpr (Y2) s2 += double(red[NA - 1][idx]);
+            }
+            double *o = partial + (size_t(cc) * gridDim.x + blockIdx.x) * 2;  // [C][blocks][2]
+            o[0] = s0;
+            o[1] = s1;
+            if constexpr (Y2) {
+                double *o2 = partial2 + (size_t(cc) * gridDim.x + blockIdx.x) * 2;
+                o2[0] = s0;
+                o2[1] = s2;
+            }
+        }
+    }
+}
+
 // Backward finalise: dbeta = sum g', dgamma = sum g' xhat over the row blocks in order.
 static __global__ void bn_finalize_bwd_kernel(const double *__restrict__ partial, int nblk, int C, float *dbeta,
                                        float *dgamma) {
@@ -1098,6 +1243,39 @@ static __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const void *__
     BnBwd<KIND> f;
     f.inv = 1.f / float(P);
     f.load(mean, rstd, gamma, dbeta, dgamma, int(i % C8) * 8);
+    if constexpr (KIND == 0) if (fixed) {  // U vectors' loads before any store (see bn_apply_kernel)
+        constexpr int U = MASK ? 2 : 4;
+        const uint4 *gp = static_cast<const uint4 *>(g), *yp = static_cast<const uint4 *>(y);
+        const uint4 *mp = static_cast<const uint4 *>(mask.hi);
+        for (; i < n; i += stride * U) {
+            uint4 a[U], b[U], m[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t j = i + u * stride;
+                if (j < n) {
+                    a[u] = gp[j];
+                    b[u] = yp[j];
+                    if constexpr (MASK) m[u] = mp[j];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t j = i + u * stride;
+                if (j >= n) break;
+                F8 gv, x, mk, d;
+                bf16x8_to_f8(a[u], gv);
+                bf16x8_to_f8(b[u], x);
+                if constexpr (MASK) bf16x8_to_f8(m[u], mk);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float gk = (MASK && !(mk.v[k] > 0.f)) ? 0.f : gv.v[k];
+                    d.v[k] = f(gk, x.v[k], k);
+                }
+                static_cast<uint4 *>(dx.hi)[j] = f8_to_bf16x8(d);
+            }
+        }
+        return;
+    }
 #pragma unroll 2
     for (; i < n; i += stride) {
         if (!fixed) f.load(mean, rstd, gamma, dbeta, dgamma, int(i % C8) * 8);

@@ -961,11 +961,32 @@ struct ResNetTrainer {
         ConvL &c = convs[ci];
         zrecv<K>(c.tb, 1, s);
         if (ds >= 0) zrecv<K>(convs[ds].tb, 1, s);
+        static const bool stats4 = std::getenv("CDP_BN_STATS4") != nullptr;  // A/B: the 4-channel kernel
+        const bool s8 = K == 0 && c.cout % 8 == 0 && !stats4;
         const int rows_blk = bn_rows_per_block(c.P, c.cout);  // kBnRowsMin or kBnRows
-        const int nblk = int((c.P + rows_blk - 1) / rows_blk);
+        int nblk = int((c.P + rows_blk - 1) / rows_blk);
         const int C4 = c.cout / 4, TPR = C4 < 32 ? C4 : 32;
         const ConvL *cd = ds >= 0 ? &convs[ds] : nullptr;
         const double bytes = double(c.P) * c.cout * (ysz() + (mask.hi ? esz() : 0) + ysz() + (cd ? ysz() : 0));
+        if (s8) {
+            const int C8 = c.cout / 8, T8 = C8 < 32 ? C8 : 32, gy = (C8 + T8 - 1) / T8;
+            const int64_t chunk = int64_t(256 / T8) * (cd ? 2 : 4);
+            const int64_t nchunks = (c.P + chunk - 1) / chunk;
+            // two CTAs per SM over the channel groups, at most one chunk per CTA, within the partial buffer
+            nblk = int(std::min<int64_t>({nchunks, std::max(1, 2 * sms() / gy), (c.P + kBnRowsMin - 1) / kBnRowsMin}));
+            L("bn_bwd_stats", 0, bytes, s, [&] {
+                auto kern = mask.hi ? (cd ? bn_bwd_stats8_kernel<true, true> : bn_bwd_stats8_kernel<true, false>)
+                                    : (cd ? bn_bwd_stats8_kernel<false, true> : bn_bwd_stats8_kernel<false, false>);
+                launch_pdl(kern, dim3(nblk, gy), dim3(256), 0, s,
+                           (const __nv_bfloat16 *)g, (const __nv_bfloat16 *)mask.hi, c.P, c.cout,
+                           (const __nv_bfloat16 *)c.y.p, (const float *)c.mean.as<float>(),
+                           (const float *)c.rstd.as<float>(), bnpart[0].as<double>(),
+                           cd ? (const __nv_bfloat16 *)cd->y.p : (const __nv_bfloat16 *)nullptr,
+                           cd ? (const float *)cd->mean.as<float>() : (const float *)nullptr,
+                           cd ? (const float *)cd->rstd.as<float>() : (const float *)nullptr,
+                           cd ? bnpart[1].as<double>() : (double *)nullptr);
+            });
+        } else
         L("bn_bwd_stats", 0, bytes, s, [&] {
             auto kern = rows_blk == kBnRowsMin ? bn_bwd_stats_kernel<K, kBnRowsMin>
                         : rows_blk == kBnRows  ? bn_bwd_stats_kernel<K, kBnRows>

@@ -58,3 +58,8 @@ if os.environ.get("PROFILE"):
         for i, (name, fl, by, t) in sorted(enumerate(ops), key=lambda kv: -kv[1][3])[:int(os.environ["TOP"])]:
             rate = f"{fl / t / 1e9:8.1f} TFLOP/s" if fl else f"{by / t / 1e6:8.1f} GB/s"
             print(f"  #{i:4d} {name:24s} {t * 1e3:8.1f} us  {rate}  flops {fl:.3g} bytes {by:.3g}")
+    if os.environ.get("OPS"):  # every launch of the named classes (comma-separated), in step order
+        want = set(os.environ["OPS"].split(","))
+        for i, (name, fl, by, t) in enumerate(ops):
+            if name in want:
+                print(f"  #{i:4d} {name:24s} {t * 1e3:8.1f} us  {by / 1e6:8.2f} MB  {by / t / 1e6:8.1f} GB/s")
