@@ -110,8 +110,9 @@ def test_resnet_executed_versions(cuda, world, rule_name, zero):
     _consistency(world, rule_name, steps, _stage_trace(recs, stage))
 
 
-@pytest.mark.parametrize("world,rule_name", [(1, None), (2, "cdp-v2"), (3, "cdp-v1"), (3, "cdp-v2")])
-def test_vit_executed_versions(cuda, world, rule_name):
+@pytest.mark.parametrize("world,rule_name,dtype", [(1, None, "bf16"), (2, "cdp-v2", "bf16"), (3, "cdp-v1", "bf16"),
+                                                   (3, "cdp-v2", "bf16"), (2, "cdp-v2", "fp32"), (3, "cdp-v1", "fp32")])
+def test_vit_executed_versions(cuda, world, rule_name, dtype):
     from paper_2403_08837_b200.rules import rule_by_name
     from paper_2403_08837_b200.vit import DeviceVit, vit_init
 
@@ -121,7 +122,7 @@ def test_vit_executed_versions(cuda, world, rule_name):
     x = rng.normal(size=(world * MB * 2, 32, 32, 3)).astype(np.float32)
     y = rng.integers(0, 10, size=len(x)).astype(np.int32)
     steps = 4
-    tr = [DeviceVit(cfg, MB, world, r, rule, 0.9, inputs=x, labels=y, trace=True) for r in range(world)]
+    tr = [DeviceVit(cfg, MB, world, r, rule, 0.9, inputs=x, labels=y, trace=True, dtype=dtype) for r in range(world)]
     regions = [t.region() for t in tr]
     init = vit_init(cfg, 0)
     for t in tr:
