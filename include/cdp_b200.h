@@ -42,6 +42,9 @@ const char *cdp_last_error(void);
 int cdp_version(void);
 /* Number of SMs of the current device (0 if no device). */
 int cdp_device_sm_count(void);
+/* Select the device of the calling thread for this library's CUDA runtime (the library links its own
+ * runtime; the Python layer binds it to torch's current device, one process per GPU). */
+int cdp_set_device(int device);
 /* Synchronous device -> host copy (tests / diagnostics read internal buffers with it). */
 int cdp_memcpy_d2h(void *dst, const void *src, size_t bytes);
 

@@ -7,6 +7,7 @@ is missing or no CUDA device is visible, and every caller propagates it.
 from __future__ import annotations
 
 import ctypes
+import sys
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -26,6 +27,7 @@ SIGNATURES = {
     "cdp_last_error": (ctypes.c_char_p, []),
     "cdp_version": (c_int, []),
     "cdp_device_sm_count": (c_int, []),
+    "cdp_set_device": (c_int, [c_int]),
     "cdp_memcpy_d2h": (c_int, [c_void_p, c_void_p, c_size_t]),
     "cdp_mlp_value_grad": (c_int, [c_int, c_int64_p, c_double_p, c_int, c_double_p, c_double_p, c_int64_p, c_int,
                                    c_int, c_double_p, c_double_p]),
@@ -161,10 +163,22 @@ def lib():
     global _lib
     if _lib is None:
         L = load_library()
+        _bind_device(L)
         if L.cdp_device_sm_count() <= 0:
             raise NativeUnavailable("no CUDA device visible to libcdp_b200 (the sm_100a path has no CPU fallback)")
         _lib = L
+    else:
+        _bind_device(_lib)
     return _lib
+
+
+def _bind_device(L):
+    """The library links its own CUDA runtime: select torch's current device for this thread (one process
+    per GPU: the rank's torch.cuda.set_device(LOCAL_RANK) then also places the trainers)."""
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_initialized():
+        if L.cdp_set_device(int(torch.cuda.current_device())) != 0:
+            raise NativeError(L.cdp_last_error().decode())
 
 
 def check(rc: int) -> None:

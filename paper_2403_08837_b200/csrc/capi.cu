@@ -10,6 +10,10 @@ extern "C" int cdp_memcpy_d2h(void *dst, const void *src, size_t bytes) {
     return cdp::guarded([&] { CDP_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
 }
 
+extern "C" int cdp_set_device(int device) {
+    return cdp::guarded([&] { CDP_CUDA(cudaSetDevice(device)); });
+}
+
 extern "C" int cdp_device_sm_count(void) {
     int n = 0;
     if (cdp::guarded([&] { n = cdp::num_sms(); }) != 0) return 0;
