@@ -483,6 +483,34 @@ struct EpiConvOut2 {
                 make_float2(cur.x + s, cur.y + q);
         }
     }
+    // Grouped TMA-store epilogue (PkArgs::grouped): each 128-thread group of epilogue warps keeps its own
+    // running statistics in slot sl of nsl = 2 * gridDim.x per column; thread gt owns columns gt + 128 k.
+    __device__ static void gstats_init(const Params &p, int N, int gt, int nsl, int sl) {
+        if (p.stats)
+            for (int a = gt; a < N; a += 128)
+                *reinterpret_cast<float2 *>(p.stats + (size_t(a) * nsl + sl) * 2) = make_float2(0.f, 0.f);
+    }
+    __device__ static void gstats_pre(const Params &p, int col0, int ncols, int gt, float *slot, int nsl, int sl) {
+        if (!p.stats || gt >= ncols) return;
+        ptx::cp_async8(slot + 2 * gt, p.stats + (size_t(col0 + gt) * nsl + sl) * 2);
+        ptx::cp_async_commit();
+    }
+    // the group's four warp partials part[4][pcols][2] in warp order, added to the running value
+    __device__ static void gstats_add(const Params &p, const float *part, int pcols, int col0, int ncols, int gt,
+                                      const float *slot, int nsl, int sl) {
+        if (p.stats && gt < ncols) {
+            ptx::cp_async_wait_all();
+            const float2 cur = *reinterpret_cast<const float2 *>(slot + 2 * gt);
+            float s = 0.f, q = 0.f;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const float2 t = *reinterpret_cast<const float2 *>(part + (w * pcols + gt) * 2);
+                s += t.x;
+                q += t.y;
+            }
+            *reinterpret_cast<float2 *>(p.stats + (size_t(col0 + gt) * nsl + sl) * 2) = make_float2(cur.x + s, cur.y + q);
+        }
+    }
     // tensor-core statistics: the thread's column sum / sum of squares of the unit, added to the running value
     __device__ static void col_stats_value(const Params &p, int col0, int ncols, int tid, float s, float q,
                                            const float *slot) {

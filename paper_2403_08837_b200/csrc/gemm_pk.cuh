@@ -54,6 +54,11 @@ struct PkArgs {
     // BN statistics of a 128-column TMA-store tile by two tensor-core MMAs (opt-in, CDP_MMA_STATS=1: correct,
     // but slower than the staging read-back on B200 — the MMAs queue behind the next unit's mainloop)
     int mma_stats;
+    // Grouped TMA-store epilogue (plain bf16 outputs of unsplit units, CDP_PK_GROUPED=0 disables): epilogue
+    // warps 4-7 take the units of accumulator 0, warps 8-11 those of accumulator 1, each group a whole
+    // tile with its own staging buffer, barrier and statistics slot (two tiles' epilogues in flight:
+    // the one-group-per-tile epilogue left 62 % of issue cycles without an eligible warp)
+    int grouped;
     // Stride-2 data gradient with all sub-pixel phases in one launch (nph > 1): the batch index g of
     // a unit is its phase, cvp[g] its geometry (tap table, output phase offsets); no split-K.
     int nph;
@@ -163,9 +168,9 @@ __device__ __forceinline__ void pk_tile_stats(const uint8_t *buf, const int *row
         rv[6] = m1.z;
         rv[7] = m1.w;
     }
-    float sm[8], sq[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) sm[c] = sq[c] = 0.f;
+    // column pairs (2e, 2e + 1) accumulated as packed f32x2 (FADD2 / FFMA2: the same IEEE per-lane
+    // rounding as scalar FADD / FFMA, half the instructions of the epilogue's busiest loop)
+    uint64_t s2[4] = {0, 0, 0, 0}, q2[4] = {0, 0, 0, 0};
     const uint8_t *base = buf + k * 16384 + (RPT * rg) * 128;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -175,12 +180,17 @@ __device__ __forceinline__ void pk_tile_stats(const uint8_t *buf, const int *row
         const uint32_t u[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const float lo = __uint_as_float(u[e] << 16), hi = __uint_as_float(u[e] & 0xffff0000u);
-            sm[2 * e] += lo;
-            sq[2 * e] = fmaf(lo, lo, sq[2 * e]);
-            sm[2 * e + 1] += hi;
-            sq[2 * e + 1] = fmaf(hi, hi, sq[2 * e + 1]);
+            uint64_t x;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(u[e] << 16), "r"(u[e] & 0xffff0000u));
+            asm("add.rn.f32x2 %0, %1, %0;" : "+l"(s2[e]) : "l"(x));
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(q2[e]) : "l"(x));
         }
+    }
+    float sm[8], sq[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(sm[2 * e]), "=f"(sm[2 * e + 1]) : "l"(s2[e]));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(sq[2 * e]), "=f"(sq[2 * e + 1]) : "l"(q2[e]));
     }
 #pragma unroll
     for (int off = CG; off < 32; off <<= 1)  // the warp's row groups of this column group
@@ -191,6 +201,48 @@ __device__ __forceinline__ void pk_tile_stats(const uint8_t *buf, const int *row
         }
     if ((tid & 31) < CG) {
         float4 *o = reinterpret_cast<float4 *>(part + ((tid >> 5) * COLS + cg * 8) * 2);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = make_float4(sm[2 * c], sq[2 * c], sm[2 * c + 1], sq[2 * c + 1]);
+    }
+}
+
+// Column (sum, sum of squares) of a staged bf16 pass by one 128-thread group (grouped epilogue): rows
+// outside the output were staged as zeros, so no row mask; partials part[4 warps][COLS][2].
+template <int COLS>
+__device__ __forceinline__ void pk_tile_stats_g(const uint8_t *buf, float *part, int gt) {
+    static_assert(COLS == 128 || COLS == 64, "staging pass width");
+    constexpr int CG = COLS / 8, RPT = 128 * CG / 128;  // column groups; rows per thread
+    const int cg = gt % CG, rg = gt / CG, k = cg >> 3, j = cg & 7;
+    uint64_t s2[4] = {0, 0, 0, 0}, q2[4] = {0, 0, 0, 0};
+    const uint8_t *base = buf + k * 16384 + (RPT * rg) * 128;
+#pragma unroll 4
+    for (int i = 0; i < RPT; ++i) {
+        const int r = RPT * rg + i;
+        const uint4 w = *reinterpret_cast<const uint4 *>(base + i * 128 + ((j ^ (r & 7)) << 4));
+        const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            uint64_t x;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(u[e] << 16), "r"(u[e] & 0xffff0000u));
+            asm("add.rn.f32x2 %0, %1, %0;" : "+l"(s2[e]) : "l"(x));
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(q2[e]) : "l"(x));
+        }
+    }
+    float sm[8], sq[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(sm[2 * e]), "=f"(sm[2 * e + 1]) : "l"(s2[e]));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(sq[2 * e]), "=f"(sq[2 * e + 1]) : "l"(q2[e]));
+    }
+#pragma unroll
+    for (int off = CG; off < 32; off <<= 1)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], off);
+            sq[c] += __shfl_xor_sync(0xffffffffu, sq[c], off);
+        }
+    if ((gt & 31) < CG) {
+        float4 *o = reinterpret_cast<float4 *>(part + ((gt >> 5) * COLS + cg * 8) * 2);
 #pragma unroll
         for (int c = 0; c < 4; ++c) o[c] = make_float4(sm[2 * c], sq[2 * c], sm[2 * c + 1], sq[2 * c + 1]);
     }
@@ -444,6 +496,92 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         const int half = (warp - 4) >> 2;   // column half of each staging pass
         const int row = q * 32 + ptx::lane_id();
         constexpr int HC = C::EPI_COLS / 2;
+        bool grouped_run = false;
+        if constexpr (Epi::kTmaStore && NES == 0) {
+            if (args.grouped) {  // PkArgs::grouped: group `half` takes the units of accumulator `half`
+                const int gt = row, grp = half, gbar = 3 + grp;
+                uint8_t *buf = smem + C::STAGES * C::STAGE_BYTES + grp * (C::EPI_COLS * 256);
+                float *gpart = spart + grp * (4 * C::EPI_COLS * 2);
+                float *gpre = grp == 0 ? spre : reinterpret_cast<float *>(sones);  // [2 passes][128][2]
+                const int nsl = 2 * int(gridDim.x), sl = 2 * int(blockIdx.x) + grp;
+                const bool stats = Epi::has_stats(ep);
+                Epi::gstats_init(ep, args.N, gt, nsl, sl);
+                int j = 0;
+                for (int u = first; u < args.units; u += stride, ++j) {
+                    if ((j & 1) != grp) continue;
+                    int tm, tn, sp, g;
+                    pk_unit_cl<CL>(args, u, rank, tm, tn, sp, g);
+                    if (CL > 1 && tm >= args.tiles_m) {  // phantom tile: release the accumulator unread
+                        if (gt == 0) {
+                            ptx::mbar_wait(&tfull[grp], (j >> 1) & 1);
+                            ptx::mbar_arrive(&tempty[grp]);
+                        }
+                        continue;
+                    }
+#pragma unroll
+                    for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+                        const int c0 = tn * BN + h * C::EPI_COLS;
+                        Epi::gstats_pre(ep, c0, min(C::EPI_COLS, args.N - c0), gt, gpre + h * 256, nsl, sl);
+                    }
+                    const bool live = pk_row_m(args, tm, row, g) >= 0;
+                    ptx::mbar_wait(&tfull[grp], (j >> 1) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(grp * BN);
+#pragma unroll 1
+                    for (int h = 0; h < BN / C::EPI_COLS; ++h) {
+#pragma unroll 1
+                        for (int c = 0; c < C::EPI_COLS; c += 32) {
+                            float v[32];
+                            ptx::tmem_ld32(taddr + h * C::EPI_COLS + c, v);
+                            uint8_t *rp = buf + (c >> 6) * 16384 + row * 128;
+                            const int u0 = (c & 63) >> 3;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                uint4 w;
+                                w.x = pk_bf16x2(v[8 * i], v[8 * i + 1]);
+                                w.y = pk_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+                                w.z = pk_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+                                w.w = pk_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+                                if (!live) w = make_uint4(0u, 0u, 0u, 0u);  // never stored; zero for the statistics
+                                *reinterpret_cast<uint4 *>(rp + (((u0 + i) ^ (row & 7)) << 4)) = w;
+                            }
+                        }
+                        ptx::fence_proxy_async_smem();
+                        if (h == BN / C::EPI_COLS - 1) ptx::tc_fence_before();
+                        pk_bar(gbar, 128);
+                        if (h == BN / C::EPI_COLS - 1 && gt == 0) ptx::mbar_arrive(&tempty[grp]);
+                        const int col0 = tn * BN + h * C::EPI_COLS;
+                        if (gt == 0) {
+#pragma unroll 1
+                            for (int k = 0; k < C::EPI_COLS / 64; ++k) {
+                                const int col = col0 + k * 64;
+                                if (col >= args.N) break;
+                                const uint8_t *src = buf + k * 16384;
+                                if (args.boxed) {
+                                    int w0, h0, b0;
+                                    conv_box_origin(args.cv, tm, w0, h0, b0);
+                                    ptx::tma_store_4d(&maps.o, src, col, w0, h0, b0);
+                                } else {
+                                    ptx::tma_store_2d(&maps.o, src, col, tm * 128);
+                                }
+                            }
+                            ptx::bulk_commit();
+                        }
+                        if (stats) {
+                            pk_tile_stats_g<C::EPI_COLS>(buf, gpart, gt);
+                            pk_bar(gbar, 128);
+                            Epi::gstats_add(ep, gpart, C::EPI_COLS, col0, min(C::EPI_COLS, args.N - col0), gt,
+                                            gpre + h * 256, nsl, sl);
+                        }
+                        if (gt == 0) ptx::bulk_wait_read0();  // the buffer is rewritten by the next pass
+                        pk_bar(gbar, 128);                    // (and gpart by the next statistics)
+                    }
+                }
+                if (gt == 0) ptx::bulk_wait0();  // TMA stores complete before the CTA exits
+                grouped_run = true;
+            }
+        }
+        if (!grouped_run) {
         if (args.splits == 1) {
             Epi::template col_stats_init<kPkEpi>(ep, args.N, C::EPI_COLS, tid);
             pk_bar(1, kPkEpi);
@@ -694,6 +832,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             if (tid == 0) ptx::bulk_wait0();  // TMA stores complete before the CTA exits
         if constexpr (NES > 0)
             if (q == 0 && ptx::lane_id() == 0) ptx::bulk_wait0();  // the slot stores of both halves
+        }
     }
     ptx::tc_fence_before();
     if constexpr (CL == 1)
@@ -816,6 +955,11 @@ struct PkLaunch {
                 return e && e[0] == '1';
             }();
             a.mma_stats = (mma_on && BN == 128 && KIND == 0) ? 1 : 0;
+            static const bool grouped_on = [] {
+                const char *e = std::getenv("CDP_PK_GROUPED");
+                return !(e && e[0] == '0');
+            }();
+            a.grouped = (grouped_on && !a.mma_stats) ? 1 : 0;
         }
     }
     // TMA-staged epilogue operands (Epi::kTmaAdd): maps of the residual gradient and its mask with the

@@ -475,7 +475,7 @@ struct ResNetTrainer {
             c.dbeta = DevBuf(c.cout * 4);
             c.dgamma = DevBuf(c.cout * 4);
             c.dy = make_cbuf(kind, int(c.P), c.cout);
-            max_stats = std::max<int64_t>(max_stats, int64_t(std::max(4 * c.tiles_fwd, 160)) * c.cout * 2);
+            max_stats = std::max<int64_t>(max_stats, int64_t(std::max(4 * c.tiles_fwd, 320)) * c.cout * 2);
             max_part = std::max<int64_t>(max_part, ((c.P + kBnRowsMin - 1) / kBnRowsMin) * c.cout * 2);
         }
         const ConvL &c0 = convs[stem];
@@ -689,7 +689,8 @@ struct ResNetTrainer {
         GemmMaps maps = gp.maps;
         PL::setup_tma_out(maps, a, ep);
         PL::setup_tma_add(maps, a, ep);
-        last_stat_slots = a.splits > 1 ? a.tiles_m * slots_per_tile : grid;  // EpiConvOut2 statistics rows
+        // EpiConvOut2 statistics rows (grouped TMA-store epilogue: one slot per CTA and epilogue group)
+        last_stat_slots = a.splits > 1 ? a.tiles_m * slots_per_tile : grid * (a.grouped ? 2 : 1);
         last_grid = grid;
         L(name, flops, take_bytes(), s, [&] { PL::launch(maps, a, ep, s, grid, paired); });
         if constexpr (!pk_direct<Epi>::value) if (a.splits > 1) {
