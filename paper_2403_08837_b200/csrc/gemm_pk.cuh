@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 1);
+            ptx::mbar_init(&tempty[a], NES > 0 ? 2 : 1);  // staged-operand epilogue: one arrival per column half
         }
         for (int a = 0; a < NES; ++a) {
             ptx::mbar_init(&efull[a], 1);
@@ -599,6 +599,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 if (tid == 0) {
                     ptx::mbar_wait(&tfull[j & 1], (j >> 1) & 1);
                     ptx::mbar_arrive(&tempty[j & 1]);
+                    if (NES > 0) ptx::mbar_arrive(&tempty[j & 1]);
                 }
                 continue;
             }
@@ -667,9 +668,11 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                         }
                     }
                 }
+                // each column half frees the accumulator for itself (no CTA-wide barrier per unit: the halves
+                // only meet in the operand ring's order)
                 ptx::tc_fence_before();
-                pk_bar(1, kPkEpi);
-                if (tid == 0) ptx::mbar_arrive(&tempty[acc]);  // accumulator free
+                pk_bar(3 + half, 128);
+                if (q == 0 && ptx::lane_id() == 0) ptx::mbar_arrive(&tempty[acc]);
                 continue;
             } else if constexpr (pk_direct<Epi>::value) {  // the only epilogue of this instantiation (no split)
                 const int row_m = pk_row_m(args, tm, row, g);
