@@ -32,3 +32,28 @@ def test_no_cpu_fallback():
 
     with pytest.raises(_native.NativeUnavailable):
         load_backend("python")
+
+
+def test_library_follows_torch_current_device(monkeypatch):
+    """The library links its own CUDA runtime; lib() binds it to torch's current device (one process per
+    GPU: the rank's torch.cuda.set_device(LOCAL_RANK) places the trainers) and leaves it alone when torch
+    has not initialised CUDA."""
+    import torch
+
+    calls = []
+
+    class FakeLib:
+        def cdp_set_device(self, d):
+            calls.append(d)
+            return 0
+
+        def cdp_last_error(self):
+            return b""
+
+    monkeypatch.setattr(torch.cuda, "is_initialized", lambda: False)
+    _native._bind_device(FakeLib())
+    assert calls == []
+    monkeypatch.setattr(torch.cuda, "is_initialized", lambda: True)
+    monkeypatch.setattr(torch.cuda, "current_device", lambda: 3)
+    _native._bind_device(FakeLib())
+    assert calls == [3]
