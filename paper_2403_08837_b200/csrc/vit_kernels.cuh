@@ -141,14 +141,26 @@ static __global__ void ln_fwd4_kernel(const float *__restrict__ x, int rows, int
 // columns lane + 32 k): dh_out = dh_in + dx (fp32) and, when copy.hi, the same row in compute
 // format (the next GEMM's operand); per-column (sum g, sum g xhat) of the block's rows combined
 // over the warps in fixed order -> partial[d][blk][2] (fp64), finalised by bn_finalize_bwd_kernel.
-constexpr int kLnBwdRows = 16;  // rows per CTA of the fused backward (2 per warp)
+#ifndef LN_BWD_MINB
+#define LN_BWD_MINB 2  // two CTAs per SM (<= 128 registers): at 136 registers one CTA per SM ran 2.7 waves
+#endif
+constexpr int kLnBwdRows = 16;  // smallest rows per CTA of the fused backward (2 per warp; sizes the partials)
+// rows per CTA at run time (CDP_LN_BWD_ROWS, a multiple of 16): 16 by default
+inline int ln_bwd_rows() {
+    static const int v = [] {
+        const char *e = std::getenv("CDP_LN_BWD_ROWS");
+        const int r = e ? std::atoi(e) : 16;
+        return r >= 16 && r % 16 == 0 ? r : 16;
+    }();
+    return v;
+}
 template <int KIND, int CPL>
 static __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const float *__restrict__ g,
                                                                   const float *__restrict__ x, int rows,
                                                                   int in_stride, int D, const float *gb,
                                                                   const float *mean, const float *rstd,
                                                                   const float *dh_in, float *dh_out, CTensor copy,
-                                                                  double *partial) {
+                                                                  double *partial, int rpc) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     extern __shared__ float red[];  // [8][D][2]
@@ -156,7 +168,7 @@ static __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const float *_
     float sg[CPL], sx[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) sg[k] = sx[k] = 0.f;
-    const int r0 = blockIdx.x * kLnBwdRows, r1 = min(rows, r0 + kLnBwdRows);
+    const int r0 = blockIdx.x * rpc, r1 = min(rows, r0 + rpc);
     for (int w = r0 + warp; w < r1; w += 8) {
         const size_t xo = size_t(w) * in_stride * D, go = size_t(w) * D;
         const float mu = mean[w], rs = rstd[w];
@@ -205,12 +217,12 @@ static __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const float *_
 // Same with 16-byte accesses: lane owns columns 4*lane + 128*k (k < C4 = D/128); both rows of a
 // warp are loaded before either is reduced (more loads in flight per thread).
 template <int KIND, int C4>
-static __global__ void __launch_bounds__(256) ln_bwd_fused4_kernel(const float *__restrict__ g,
+static __global__ void __launch_bounds__(256, LN_BWD_MINB) ln_bwd_fused4_kernel(const float *__restrict__ g,
                                                                    const float *__restrict__ x, int rows,
                                                                    int in_stride, int D, const float *gb,
                                                                    const float *mean, const float *rstd,
                                                                    const float *dh_in, float *dh_out, CTensor copy,
-                                                                   double *partial) {
+                                                                   double *partial, int rpc) {
     ptx::griddep_wait();
     ptx::griddep_launch();
     extern __shared__ float red[];  // [8][D][2]
@@ -218,7 +230,7 @@ static __global__ void __launch_bounds__(256) ln_bwd_fused4_kernel(const float *
     float4 sg[C4], sx[C4];
 #pragma unroll
     for (int k = 0; k < C4; ++k) sg[k] = sx[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int r0 = blockIdx.x * kLnBwdRows, r1 = min(rows, r0 + kLnBwdRows);
+    const int r0 = blockIdx.x * rpc, r1 = min(rows, r0 + rpc);
     const bool vcopy = copy.hi && (copy.ld % 4) == 0;
     for (int w = r0 + warp; w < r1; w += 8) {
         const size_t xo = size_t(w) * in_stride * D, go = size_t(w) * D;

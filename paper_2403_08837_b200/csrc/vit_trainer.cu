@@ -799,7 +799,8 @@ struct VitTrainer {
     void layernorm_bwd_(const float *g, const float *x, int rows, int stride, int unit, int p, const float *mean,
                         const float *rstd, const float *dh_in, float *dh_out, float *dgam, float *dbet,
                         cudaStream_t s, CTensor copy) {
-        const int nblk = (rows + kLnBwdRows - 1) / kLnBwdRows;
+        const int rpc = ln_bwd_rows();
+        const int nblk = (rows + rpc - 1) / rpc;
         const size_t smem = size_t(8) * D * 2 * 4;
         auto go = [&](auto kern) {
             if (!ln_attr_) {
@@ -807,7 +808,7 @@ struct VitTrainer {
             }
             L_("ln_bwd", 0, double(rows) * D * (16 + (copy.hi ? 2 : 0)), s, [&] {
                 launch_pdl(kern, dim3(nblk), dim3(256), smem, s, g, x, rows, stride, D, th(unit, p), mean, rstd,
-                           dh_in, dh_out, copy, lnpart.as<double>());
+                           dh_in, dh_out, copy, lnpart.as<double>(), rpc);
             });
         };
         switch (D % 128 == 0 ? D / 128 : 0) {  // 16-byte columns
