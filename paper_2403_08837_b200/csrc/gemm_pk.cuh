@@ -319,6 +319,9 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     uint64_t *tempty = tfull + 2;
     // TMA-staged epilogue operand ring (64-column halves of 128-column passes: BN >= 128)
     constexpr int NES = C::EPI_COLS == 128 ? pk_ebuf_slots<Epi>() : 0;
+    // arrivals that free an accumulator: the staged-operand epilogue's two column halves, the direct
+    // (register-only) epilogue's eight warps, else one (after a CTA-wide epilogue barrier)
+    constexpr int kTemptyArrivals = NES > 0 ? 2 : pk_direct<Epi>::value ? 8 : 1;
     uint64_t *efull = tempty + 2;
     uint64_t *eempty = efull + NES;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(eempty + NES + 1);
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], NES > 0 ? 2 : 1);  // staged-operand epilogue: one arrival per column half
+            ptx::mbar_init(&tempty[a], kTemptyArrivals);
         }
         for (int a = 0; a < NES; ++a) {
             ptx::mbar_init(&efull[a], 1);
@@ -598,8 +601,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             if (CL > 1 && tm >= args.tiles_m) {  // phantom tile: release the accumulator unread
                 if (tid == 0) {
                     ptx::mbar_wait(&tfull[j & 1], (j >> 1) & 1);
-                    ptx::mbar_arrive(&tempty[j & 1]);
-                    if (NES > 0) ptx::mbar_arrive(&tempty[j & 1]);
+                    for (int k = 0; k < kTemptyArrivals; ++k) ptx::mbar_arrive(&tempty[j & 1]);
                 }
                 continue;
             }
@@ -692,9 +694,10 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                         Epi::direct_store(ep, row_m, col, qq, out_off, dp, v);
                     }
                 }
+                // every warp frees the accumulator for itself: no CTA-wide barrier per unit (nothing shared)
                 ptx::tc_fence_before();
-                pk_bar(1, kPkEpi);
-                if (tid == 0) ptx::mbar_arrive(&tempty[acc]);  // accumulator free
+                __syncwarp();
+                if (ptx::lane_id() == 0) ptx::mbar_arrive(&tempty[acc]);
                 continue;
             } else {
             ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
