@@ -786,6 +786,19 @@ struct ResNetTrainer {
     }
 
     static int blocks_for(int64_t n, int per = 256) { return int(std::min<int64_t>(8 * 148, (n + per - 1) / per)); }
+    // grid-stride elementwise kernels: at most one wave of resident 256-thread CTAs (blocks_for's 8 per SM is
+    // two waves for a kernel that holds 4; CDP_BN_GRID_OCC=0 keeps blocks_for)
+    template <class Kern>
+    int resident_blocks(Kern kern, int64_t n) {
+        static const int64_t max_vec = [] {  // vectors (8 elements) up to which the one-wave grid is used
+            const char *e = std::getenv("CDP_BN_GRID_OCC");
+            return e ? std::atoll(e) : (int64_t(1) << 20);
+        }();
+        if (n > max_vec) return blocks_for(n);
+        int occ = 0;
+        CDP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
+        return int(std::min<int64_t>(int64_t(std::max(occ, 1)) * sms(), (n + 255) / 256));
+    }
     static int tile_n(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }  // a supported BN covering n
     // tile-width probe (development): env `name` caps the GEMM tile width of one class
     static int tile_cap(const char *name, int bn) {
@@ -865,7 +878,7 @@ struct ResNetTrainer {
         const double bytes = double(c.P) * c.cout * (ysz() + esz() + (res.act.hi ? esz() : res.y ? ysz() : 0));
         L("bn_apply", 0, bytes, s, [&] {
             auto kern = res.act.hi ? bn_apply_kernel<K, 1> : res.y ? bn_apply_kernel<K, 2> : bn_apply_kernel<K, 0>;
-            launch_pdl(kern, dim3(blocks_for(c.P * c.cout / 8)), dim3(256), 0, s, (const void *)c.y.p, c.P, c.cout,
+            launch_pdl(kern, dim3(resident_blocks(kern, c.P * c.cout / 8)), dim3(256), 0, s, (const void *)c.y.p, c.P, c.cout,
                        (const float *)c.mean.as<float>(), (const float *)c.rstd.as<float>(), gamma(ci, vslot),
                        beta(ci, vslot), res, 1, out);
         });
@@ -1017,8 +1030,8 @@ struct ResNetTrainer {
         const int vslot = vs(cc.tb, p);
         rec(cc.tb, A_BWD, 0, vslot, s);
         L("bn_bwd_apply", 0, double(cc.P) * cc.cout * (2 * ysz() + (mask.hi ? 2 : 1) * esz()), s, [&] {
-            launch_pdl(mask.hi ? bn_bwd_apply_kernel<K, true> : bn_bwd_apply_kernel<K, false>,
-                       dim3(blocks_for(cc.P * cc.cout / 8)), dim3(256), 0, s, g, mask,
+            auto kern = mask.hi ? bn_bwd_apply_kernel<K, true> : bn_bwd_apply_kernel<K, false>;
+            launch_pdl(kern, dim3(resident_blocks(kern, cc.P * cc.cout / 8)), dim3(256), 0, s, g, mask,
                        (const void *)cc.y.p, cc.P, cc.cout, (const float *)cc.mean.as<float>(),
                        (const float *)cc.rstd.as<float>(), gamma(ci, vslot), (const float *)cc.dbeta.as<float>(),
                        (const float *)cc.dgamma.as<float>(), cc.dy.view());
