@@ -98,13 +98,16 @@ static __global__ void ln_fwd4_kernel(const float *__restrict__ x, int rows, int
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= rows) return;
     const float *xr = x + size_t(w) * in_stride * D;
-    float4 v[C4];
+    float4 v[C4], ga[C4], be[C4];
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < C4; ++k) {
+    for (int k = 0; k < C4; ++k) {  // gamma / beta with the row: their loads overlap the reductions
         v[k] = *reinterpret_cast<const float4 *>(xr + 4 * lane + 128 * k);
-        s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        ga[k] = *reinterpret_cast<const float4 *>(gb + 4 * lane + 128 * k);
+        be[k] = *reinterpret_cast<const float4 *>(gb + D + 4 * lane + 128 * k);
     }
+#pragma unroll
+    for (int k = 0; k < C4; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
     const float mu = warp_sum(s) / float(D);
     float q = 0.f;
 #pragma unroll
@@ -117,9 +120,8 @@ static __global__ void ln_fwd4_kernel(const float *__restrict__ x, int rows, int
 #pragma unroll
     for (int k = 0; k < C4; ++k) {
         const int d = 4 * lane + 128 * k;
-        const float4 ga = *reinterpret_cast<const float4 *>(gb + d), be = *reinterpret_cast<const float4 *>(gb + D + d);
-        const float4 y = make_float4(ga.x * ((v[k].x - mu) * rs) + be.x, ga.y * ((v[k].y - mu) * rs) + be.y,
-                                     ga.z * ((v[k].z - mu) * rs) + be.z, ga.w * ((v[k].w - mu) * rs) + be.w);
+        const float4 y = make_float4(ga[k].x * ((v[k].x - mu) * rs) + be[k].x, ga[k].y * ((v[k].y - mu) * rs) + be[k].y,
+                                     ga[k].z * ((v[k].z - mu) * rs) + be[k].z, ga[k].w * ((v[k].w - mu) * rs) + be[k].w);
         const size_t o = size_t(w) * out.ld + d;
         if (vec) {
             store_wc4<KIND>(out, o, y);
